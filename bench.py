@@ -1,0 +1,378 @@
+#!/usr/bin/env python
+"""Benchmark of the CRK-HACC short-range substep on B200 (BASELINE.json metric:
+pair interactions/s and short-range substep time; % of FP32 peak).
+
+A step = one whole short-range substep: build lists (sort,
+leaves, lists), gravity + kick, geometry, corrections, extras, accel/du-dt, over the
+device-resident 2x256^3 perturbed-lattice workload (config 4 at 1 GPU = config 5's
+per-GPU size).  Prints ONE JSON line (rank 0).
+
+  python bench.py [--gpus N] [--steps K] [--warmup W] [--config c4] [--impl reference]
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import subprocess
+import sys
+import threading
+import time
+
+import numpy as np
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+# canonical flop per ordered pair (FMA = 2, MUFU = 1, compare/select = 0)
+FLOP_PER_PAIR = {"gravity": 30, "geometry": 22, "corrections": 114, "extras": 103, "accel_dudt": 256}
+PASSES = ["build_lists", "gravity", "geometry", "corrections", "extras", "accel_dudt"]
+METRIC = "pair interactions/s & short-range substep time at 1/2/4/8 B200; % FP32 peak"
+
+
+def _peaks():
+    try:
+        with open(os.path.join(ROOT, "MEASURED_PEAKS.json")) as f:
+            return json.load(f)
+    except Exception:
+        return {}
+
+
+class ClockSampler:
+    """nvidia-smi clocks / throttle reasons sampled during the timed region."""
+
+    def __init__(self, index=0):
+        self.index = index
+        self.proc = None
+        self.lines = []
+
+    def __enter__(self):
+        q = ("index,clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,"
+             "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
+             "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
+        try:
+            self.proc = subprocess.Popen(["nvidia-smi", f"--query-gpu={q}", "--format=csv,noheader,nounits",
+                                          "-i", str(self.index), "-lms", "100"], stdout=subprocess.PIPE,
+                                         stderr=subprocess.DEVNULL, text=True)
+            self.t = threading.Thread(target=self._read, daemon=True)
+            self.t.start()
+        except Exception:
+            self.proc = None
+        return self
+
+    def _read(self):
+        for line in self.proc.stdout:
+            self.lines.append(line.strip())
+
+    def __exit__(self, *a):
+        if self.proc:
+            self.proc.terminate()
+            try:
+                self.proc.wait(2)
+            except Exception:
+                self.proc.kill()
+
+    def summary(self):
+        sm, mx, reasons = [], None, set()
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        for ln in self.lines:
+            f = [x.strip() for x in ln.split(",")]
+            if len(f) < 9:
+                continue
+            try:
+                sm.append(float(f[1]))
+                mx = float(f[2])
+            except ValueError:
+                continue
+            for nm, v in zip(names, f[5:9]):
+                if v.lower().startswith("active"):
+                    reasons.add(nm)
+        return {"sm_mhz": float(np.median(sm)) if sm else None, "sm_max_mhz": mx, "reasons": sorted(reasons),
+                "samples": len(sm)}
+
+
+def dist_env():
+    rank = int(os.environ.get("RANK", "0"))
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    local = int(os.environ.get("LOCAL_RANK", str(rank)))
+    return rank, world, local
+
+
+def oracle_sample(parts, params, cnts, n_grav=20000, n_gas=1500, seed=1):
+    """Time the fp64 oracle as it stands on a bounded sample of the workload; returns
+    (pair interactions evaluated, seconds, description)."""
+    import oracle
+
+    rng = np.random.default_rng(seed)
+    n = parts["x"].shape[0]
+    gas = np.nonzero(parts["species"] == 1)[0]
+    tg = np.sort(rng.choice(gas, min(n_gas, gas.shape[0]), replace=False))
+    ta = np.sort(rng.choice(n, min(n_grav, n), replace=False))
+    cg, ch, cs = cnts  # input order
+    t0 = time.perf_counter()
+    oracle.gravity(parts, params, ta)
+    off, nb = oracle.neighbour_sets(parts, params, tg, 2)
+    T2 = np.unique(np.concatenate([tg, nb]))
+    off, nb = oracle.neighbour_sets(parts, params, T2, 1)
+    T1 = np.unique(np.concatenate([T2, nb]))
+    V = np.full(n, np.nan)
+    V[T1] = oracle.geometry(parts, params, T1)
+    cr = oracle.corrections(parts, params, V, T2)
+    A, B, dA, dB = np.full(n, np.nan), np.full((n, 3), np.nan), np.full((n, 3), np.nan), np.full((n, 9), np.nan)
+    A[T2], B[T2], dA[T2], dB[T2] = cr["A"], cr["B"], cr["dA"], cr["dB"]
+    ex = oracle.extras(parts, params, V, A, B, dA, dB, T2)
+    rho, P, c, dv = np.full(n, np.nan), np.full(n, np.nan), np.full(n, np.nan), np.full((n, 9), np.nan)
+    rho[T2], P[T2], c[T2], dv[T2] = ex["rho"], ex["P"], ex["cs"], ex["dv"]
+    oracle.accel(parts, params, V, A, B, dA, dB, rho, P, c, dv, tg)
+    secs = time.perf_counter() - t0
+    pairs = int(cg[ta].sum()) + int(ch[T1].sum()) + 2 * int(ch[T2].sum()) + int(cs[tg].sum())
+    desc = (f"oracle (fp64 C, OpenMP) on {ta.shape[0]} gravity targets + hydro chain for {tg.shape[0]} gas "
+            f"targets (closure {T1.shape[0]}/{T2.shape[0]}); pairs counted per pass on the computed sets")
+    return pairs, secs, desc
+
+
+def run_reference(args, parts, params, rank, world):
+    """--impl reference: the oracle (fp64 CPU) timed on this host's cores, rank 0 only."""
+    import oracle
+
+    if rank != 0:
+        return
+    from paper_2310_16122_b200 import Particles, Solver  # counts only (outside timing)
+    import torch
+
+    cnts = _counts_input_order(parts, params)
+    times, pairs_tot = [], 0
+    for s in range(args.warmup + args.steps):
+        pairs, secs, desc = oracle_sample(parts, params, cnts, n_grav=4000, n_gas=300, seed=100 + s)
+        if s >= args.warmup:
+            times.append(secs)
+            pairs_tot += pairs
+    val = pairs_tot / sum(times)
+    ms = 1e3 * sum(times) / len(times)
+    line = {"metric": METRIC, "impl": "reference", "value": val, "unit": "pair interactions/s",
+            "n_gpus": world, "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms,
+            "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64",
+            "data": "synthetic", "config": _config(args, parts),
+            "cpu_baseline": {"value": val, "unit": "pair interactions/s", "cores": oracle.num_threads(),
+                             "kind": "oracle", "sample": desc},
+            "e2e": {"value": val, "unit": "pair interactions/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
+    print(json.dumps(line), flush=True)
+
+
+def _config(args, parts):
+    n = parts["x"].shape[0]
+    return {"workload": f"{args.config}: 2x{round((n / 2) ** (1 / 3))}^3 DM+gas perturbed lattice (Zel'dovich rms 0.1), "
+                        "periodic box, one gravity + CRK-SPH short-range substep",
+            "particles_per_gpu": n, "l2": "inputs (>1.5 GB) larger than L2", "seq_len": None}
+
+
+_COUNT_CACHE = {}
+
+
+def _counts_input_order(parts, params):
+    import torch
+    from paper_2310_16122_b200 import Particles, Solver
+
+    key = id(parts)
+    if key in _COUNT_CACHE:
+        return _COUNT_CACHE[key]
+    p = Particles.from_host(parts, "cuda", outputs=False)
+    s = Solver(params, torch.cuda.current_device())
+    s.build_lists(p)
+    cg, ch, cs = s.count_pairs(p)
+    perm = p.perm.cpu().numpy().astype(np.int64)
+    out = []
+    for c in (cg, ch, cs):
+        o = np.empty(p.n, np.int64)
+        o[perm] = c.cpu().numpy()
+        out.append(o)
+    s.close()
+    del p
+    torch.cuda.empty_cache()
+    _COUNT_CACHE[key] = tuple(out)
+    return _COUNT_CACHE[key]
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=10)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--config", default="c4")
+    ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--dt", type=float, default=0.0)
+    args = ap.parse_args()
+    args.warmup = max(args.warmup, 3) if args.impl == "ours" else args.warmup
+
+    import torch
+
+    rank, world, local = dist_env()
+    if world > 1:
+        import torch.distributed as dist
+
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+    torch.cuda.set_device(local)
+
+    from gen import make_config
+
+    t0 = time.perf_counter()
+    parts, params = make_config(args.config)
+    gen_s = time.perf_counter() - t0
+
+    if args.impl == "reference":
+        run_reference(args, parts, params, rank, world)
+        if world > 1:
+            import torch.distributed as dist
+
+            dist.destroy_process_group()
+        return
+
+    from paper_2310_16122_b200 import Particles, Solver
+
+    dev = torch.device("cuda", local)
+    stream = torch.cuda.current_stream(dev)
+    cnts = _counts_input_order(parts, params)
+    pairs = {"gravity": int(cnts[0].sum()), "gather": int(cnts[1].sum()), "sym": int(cnts[2].sum())}
+    pair_int = pairs["gravity"] + 3 * pairs["gather"] + pairs["sym"]
+
+    p = Particles.from_host(parts, dev)
+    solver = Solver(params, local)
+    ev = {k: (torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)) for k in PASSES}
+
+    def step(timed):
+        if timed:
+            ev["build_lists"][0].record(stream)
+        solver.build_lists(p, stream)
+        if timed:
+            ev["build_lists"][1].record(stream)
+            ev["gravity"][0].record(stream)
+        solver.gravity_kick(p, args.dt, stream)
+        if timed:
+            ev["gravity"][1].record(stream)
+            ev["geometry"][0].record(stream)
+        solver.geometry(p, stream)
+        if timed:
+            ev["geometry"][1].record(stream)
+            ev["corrections"][0].record(stream)
+        solver.corrections(p, stream)
+        if timed:
+            ev["corrections"][1].record(stream)
+            ev["extras"][0].record(stream)
+        solver.extras(p, stream)
+        if timed:
+            ev["extras"][1].record(stream)
+            ev["accel_dudt"][0].record(stream)
+        solver.hydro_accel_dudt(p, args.dt, stream)
+        if timed:
+            ev["accel_dudt"][1].record(stream)
+
+    for _ in range(args.warmup):
+        step(False)
+    torch.cuda.synchronize()
+    if world > 1:
+        torch.distributed.barrier()
+    pass_ms = {k: 0.0 for k in PASSES}
+    l0 = solver.launch_count()
+    t_start, t_end = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    with ClockSampler(local) as clk:
+        torch.cuda.synchronize()
+        t_start.record(stream)
+        for _ in range(args.steps):
+            step(True)
+            torch.cuda.synchronize()
+            for k in PASSES:
+                pass_ms[k] += ev[k][0].elapsed_time(ev[k][1])
+        t_end.record(stream)
+        torch.cuda.synchronize()
+    launches = (solver.launch_count() - l0) // max(args.steps, 1)
+    total_ms = t_start.elapsed_time(t_end)
+    if world > 1:
+        import torch.distributed as dist
+
+        tt = torch.tensor([total_ms], device=dev)
+        dist.all_reduce(tt, op=dist.ReduceOp.MAX)
+        total_ms = float(tt.item())
+    ms_step = total_ms / args.steps
+    for k in pass_ms:
+        pass_ms[k] /= args.steps
+    value = pair_int * world / (ms_step * 1e-3)
+
+    # dominant kernel roofline (FP32 ALU)
+    pk = _peaks()
+    props = torch.cuda.get_device_properties(dev)
+    n_sm = props.multi_processor_count
+    f_max = float(pk.get("sm_max_mhz", 1965.0))
+    peak_tf = n_sm * 128 * 2 * f_max * 1e6 / 1e12
+    pass_pairs = {"gravity": pairs["gravity"], "geometry": pairs["gather"], "corrections": pairs["gather"],
+                  "extras": pairs["gather"], "accel_dudt": pairs["sym"]}
+    flops = {k: pass_pairs[k] * FLOP_PER_PAIR[k] for k in pass_pairs}
+    dom = max(pass_pairs, key=lambda k: pass_ms[k])
+    achieved = flops[dom] / (pass_ms[dom] * 1e-3) / 1e12
+    useful_tf = sum(flops.values()) / (ms_step * 1e-3) / 1e12
+
+    # e2e through the public API with host buffers (pinned), H2D + D2H inside the timed region
+    e2e = None
+    try:
+        host = {k: torch.from_numpy(np.ascontiguousarray(parts[k])).pin_memory()
+                for k in Particles.IN_F32 + ("species", "id")}
+        outk = ["ax", "ay", "az", "ahx", "ahy", "ahz", "dudt", "perm"]
+        hout = {k: torch.empty(p.n, dtype=getattr(p, k).dtype).pin_memory() for k in outk}
+        bi = sum(t.numel() * t.element_size() for t in host.values())
+        bo = sum(t.numel() * t.element_size() for t in hout.values())
+        for _ in range(2):
+            p.load(host, non_blocking=True)
+            step(False)
+        torch.cuda.synchronize()
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        e0.record(stream)
+        for _ in range(args.steps):
+            p.load(host, non_blocking=True)
+            step(False)
+            for k in outk:
+                hout[k].copy_(getattr(p, k), non_blocking=True)
+        e1.record(stream)
+        torch.cuda.synchronize()
+        ems = e0.elapsed_time(e1) / args.steps
+        e2e = {"value": pair_int * world / (ems * 1e-3), "unit": "pair interactions/s", "ms_per_step": ems,
+               "h2d_bytes_per_step": bi, "d2h_bytes_per_step": bo}
+    except Exception as ex:  # pragma: no cover
+        e2e = {"error": str(ex)}
+
+    cpu = None
+    if rank == 0 and world == 1 and not args.no_cpu_baseline:
+        import oracle
+
+        pr, secs, desc = oracle_sample(parts, params, cnts)
+        cpu = {"value": pr / secs, "unit": "pair interactions/s", "cores": oracle.num_threads(), "kind": "oracle",
+               "sample": desc, "seconds": secs}
+
+    if rank == 0:
+        line = {
+            "metric": METRIC, "value": value, "unit": "pair interactions/s", "n_gpus": world,
+            "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms_step, "higher_is_better": True,
+            "scaling": "weak", "vs_baseline": None, "dtype": "f32", "data": "synthetic",
+            "config": dict(_config(args, parts), parallelism="replicas" if world > 1 else "single GPU",
+                           generator_s=round(gen_s, 1)),
+            "pass_ms": {k: round(v, 4) for k, v in pass_ms.items()},
+            "substep_ms": ms_step,
+            "pairs": pairs, "pair_interactions_per_step": pair_int,
+            "useful_fp32_tflops": useful_tf, "useful_fp32_frac_of_peak": useful_tf / peak_tf,
+            "roofline": {"bound": "alu", "kernel": dom, "achieved": achieved, "peak": peak_tf, "unit": "TFLOP/s",
+                         "frac": achieved / peak_tf, "traffic": None,
+                         "peak_basis": f"{n_sm} SMs x 128 FP32 lanes x 2 x {f_max:.0f} MHz (sm_max_mhz, MEASURED_PEAKS.json)"},
+            "clocks": clk.summary(),
+            "e2e": e2e,
+            "gpu_launches": int(launches),
+            "cpu_baseline": cpu,
+        }
+        print(json.dumps(line), flush=True)
+    solver.close()
+    if world > 1:
+        import torch.distributed as dist
+
+        dist.destroy_process_group()
+
+
+if __name__ == "__main__":
+    main()

@@ -1,0 +1,152 @@
+/* crksr.h — C ABI of the B200-native CRK-HACC short-range solver (libcrksr.so).
+ *
+ * The calls follow the paper's statement of the problem (arxiv 2310.16122): the
+ * short-range particle-particle solver that dominates CRK-HACC's GPU time —
+ * leaf-pair interaction lists (§5.3 "half-warp" leaves A/B),
+ * short-range gravity with a degree-5 grid-force polynomial (PAPER.md:147, 278,
+ * 646 HACC_CUDA_POLY_ORDER=5) and the five hot CRK-SPH kernels Geometry,
+ * Corrections, Extras, Acceleration, Energy (timers at 503).  The
+ * formulas are the readings of SURVEY.md §8(c) O1-O9, listed in DESIGN.md §2.
+ *
+ * Conventions (every call):
+ *  - Pointers inside crk_particles are DEVICE pointers on the ctx's device unless
+ *    stated otherwise; the caller owns them.  Arrays are SoA, length n; multi-
+ *    component outputs are planes: B[a*n + i], dA[a*n + i], dB[(3a+g)*n + i]
+ *    (= d_g B^a), dv[(3a+b)*n + i] (= d_b v^a).
+ *  - Calls are asynchronous on `stream` (a cudaStream_t passed as void*; NULL =
+ *    legacy default stream) except crk_build_lists, which synchronises `stream`
+ *    once to size the interaction lists.
+ *  - Errors are returned, never thrown: CRK_EINVAL (bad argument or parameter,
+ *    nothing launched), CRK_ESTATE (call order violated), CRK_ENOMEM (device
+ *    allocation failed), CRK_ECUDA (a CUDA error; crk_last_error has the text).
+ *  - A ctx is bound to one device and is not thread-safe; one ctx per stream.
+ *  - The ctx owns all scratch (sort buffers, leaves, lists, gas-ordered
+ *    intermediates), grown on demand; nothing else is allocated per call.
+ */
+#ifndef CRKSR_H
+#define CRKSR_H
+
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+typedef enum {
+    CRK_OK = 0,
+    CRK_EINVAL = -1,
+    CRK_ENOMEM = -2,
+    CRK_ECUDA = -3,
+    CRK_ESTATE = -4,
+    CRK_ECAPACITY = -5
+} crk_status;
+
+/* Host struct, copied at crk_create. */
+typedef struct crk_params {
+    double box[3];       /* periodic box per axis, grid units; each a power of two, <= 4096 */
+    float rcut2;         /* gravity cutoff^2 (fp32, used verbatim in the O2 predicate) */
+    float eps2;          /* Plummer softening added to s = r^2; must be > 0 */
+    float poly[6];       /* grid force f_grid(s) = sum_k poly[k] s^k (HACC_CUDA_POLY_ORDER=5) */
+    float G;             /* gravity prefactor (cosmology factors folded in) */
+    float gamma;         /* adiabatic index of the EOS P = (gamma-1) rho u */
+    float av_cl, av_cq;  /* artificial viscosity linear / quadratic coefficients */
+    float av_eps2;       /* AV softening eps_AV^2 */
+    int32_t leaf_max_i;      /* gravity i-leaf size: 16, 32, 64 or 128 */
+    int32_t leaf_max_j;      /* gravity j-leaf size: 8 */
+    int32_t leaf_max_gas_i;  /* gas i-leaf size: 16, 32 or 64 */
+    int32_t leaf_max_gas_j;  /* gas j-leaf size: 8 */
+    double cell_side;    /* chaining-mesh cell side (power of two, <= box/4) */
+} crk_params;
+
+/* Caller-owned particle arrays (device pointers).  Inputs are sorted IN PLACE by
+ * crk_build_lists.  Output pointers may be NULL, in which case that output is kept
+ * only inside the ctx (the gas-ordered copies used by the next pass). */
+typedef struct crk_particles {
+    int64_t n;
+    float *x, *y, *z;          /* in/out: positions, multiples of q = max(box) 2^-23 in [0, box) */
+    float *vx, *vy, *vz;       /* in/out: velocities (kicked by gravity_kick / hydro_accel_dudt) */
+    float *m;                  /* in: mass */
+    uint8_t *species;          /* in: 0 = dark matter, 1 = gas */
+    int64_t *id;               /* in: unique particle ids (tie-break of the sort) */
+    float *H, *u;              /* in: gas smoothing length, specific internal energy (u kicked) */
+    int32_t *perm;             /* out: perm[k] = input index of the particle now at k */
+    float *ax, *ay, *az;       /* out: short-range gravitational acceleration */
+    float *V;                  /* out: gas volume (Geometry) */
+    float *A, *B, *dA, *dB;    /* out: RK coefficients A, B (3), grad A (3), grad B (9) */
+    float *rho, *P, *cs;       /* out: density, pressure, sound speed (Extras) */
+    float *dv;                 /* out: velocity gradient (9) (Extras) */
+    float *ahx, *ahy, *ahz;    /* out: hydro acceleration (Acceleration) */
+    float *dudt;               /* out: du/dt (Energy) */
+} crk_particles;
+
+struct crk_ctx;
+
+/* Device views of the lists built by crk_build_lists (valid until the next build
+ * or destroy).  Leaf sets: 0 gravity i, 1 gravity j, 2 gas i, 3 gas j.  first[]
+ * indexes sorted positions (sets 0,1) or gas ranks (sets 2,3; gas_idx maps a gas
+ * rank to its sorted position).  bbox: 6 floats per leaf (lo xyz, hi xyz).
+ * Lists: CSR over i-leaves; shift code (sx+1) + 3(sy+1) + 9(sz+1). */
+typedef struct crk_lists {
+    int64_t n_leaf[4];
+    const int32_t* leaf_first[4];
+    const int32_t* leaf_count[4];
+    const float* leaf_bbox[4];
+    const float* leaf_maxh2[4];      /* gas sets only (else NULL) */
+    const uint64_t* leaf_cell[4];    /* Morton code of the leaf's cell */
+    int64_t n_gas;
+    const int32_t* gas_idx;
+    int64_t n_entries[2];            /* 0 gravity, 1 hydro */
+    const int32_t* row_off[2];
+    const int32_t* col[2];
+    const int8_t* shift[2];
+} crk_lists;
+
+/* Create a solver context on `device`.  Validates params (CRK_EINVAL). */
+crk_status crk_create(const crk_params* params, int device, struct crk_ctx** out);
+crk_status crk_destroy(struct crk_ctx* ctx);
+
+/* a1 + a2: key -> radix sort -> permute SoA in place -> chaining-
+ * mesh cells -> leaves (O3) -> gravity and hydro leaf-pair lists (O4).
+ * Fills parts->perm.  Synchronises `stream` once (list sizes). */
+crk_status crk_build_lists(struct crk_ctx* ctx, crk_particles* parts, void* stream);
+
+/* a3: a_i = G sum_{j != i, s32 < rcut2} m_j x_ji [(s+eps2)^-3/2 - P5(s)] (O5);
+ * writes ax/ay/az and kicks v += dt a (dt = 0: forces only). */
+crk_status crk_gravity_kick(struct crk_ctx* ctx, crk_particles* parts, float dt, void* stream);
+
+/* a4 Geometry (upGeo): V_i = 1 / sum_{gas j, s32 < H_i^2, incl. i} W(r_ij, H_i) (O6). */
+crk_status crk_geometry(struct crk_ctx* ctx, crk_particles* parts, void* stream);
+
+/* a5 Corrections (upCor): A, B, grad A, grad B from the moments m0, m1, m2 and their
+ * gradients (O7). */
+crk_status crk_corrections(struct crk_ctx* ctx, crk_particles* parts, void* stream);
+
+/* a6 Extras (upBarEx): rho = sum m_j W^R_ij, P = (gamma-1) rho u, c = sqrt(gamma P/rho),
+ * grad v = sum V_j (v_j - v_i) grad W^R_ij (O8).  Reads the (possibly kicked) v. */
+crk_status crk_extras(struct crk_ctx* ctx, crk_particles* parts, void* stream);
+
+/* a7 + a8 Acceleration and Energy (upBarAc, upBarDu): antisymmetrised CRK-SPH momentum
+ * and energy derivatives with artificial viscosity (O9); kicks v += dt a_h and
+ * u += dt du/dt (dt = 0: derivatives only). */
+crk_status crk_hydro_accel_dudt(struct crk_ctx* ctx, crk_particles* parts, float dt, void* stream);
+
+/* Count mode (after SPEC.md:374-382): per-particle integer pair counts
+ * from the same list-driven pair kernels: gravity (j != i, s32 < rcut2), gas gather
+ * (gas j != i, s32 < H_i^2) and gas symmetric (s32 < max(H_i^2, H_j^2)); 0 for DM.
+ * Outputs are device int32 arrays of length n in sorted order.  Needs build_lists. */
+crk_status crk_count_pairs(struct crk_ctx* ctx, crk_particles* parts, int32_t* cgrav,
+                           int32_t* cgather, int32_t* csym, void* stream);
+
+/* Device views of leaves and lists (after crk_build_lists). */
+crk_status crk_list_view(struct crk_ctx* ctx, crk_lists* out);
+
+/* Number of kernel launches issued by this ctx since creation (launch accounting). */
+int64_t crk_launch_count(struct crk_ctx* ctx);
+
+const char* crk_status_string(crk_status s);
+const char* crk_last_error(struct crk_ctx* ctx);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* CRKSR_H */

@@ -1,0 +1,274 @@
+"""Thin ctypes binding of libcrksr.so (include/crksr.h).
+
+Argument marshalling only: every step of the solver runs in the CUDA kernels of
+libcrksr.so.  PyTorch supplies device memory and streams.  There is no CPU
+fallback: if the library is missing or no GPU is present, the calls raise.
+"""
+from __future__ import annotations
+
+import ctypes as C
+import os
+
+import torch
+
+_HERE = os.path.dirname(os.path.abspath(__file__))
+LIB_PATH = os.path.join(_HERE, "libcrksr.so")
+
+STATUS = {0: "CRK_OK", -1: "CRK_EINVAL", -2: "CRK_ENOMEM", -3: "CRK_ECUDA", -4: "CRK_ESTATE", -5: "CRK_ECAPACITY"}
+
+# exported symbols declared in include/crksr.h (tests check the .so exports all of them)
+EXPORTS = ["crk_create", "crk_destroy", "crk_build_lists", "crk_gravity_kick", "crk_geometry",
+           "crk_corrections", "crk_extras", "crk_hydro_accel_dudt", "crk_count_pairs", "crk_list_view",
+           "crk_launch_count", "crk_status_string", "crk_last_error"]
+
+
+class CrkError(RuntimeError):
+    def __init__(self, status, msg):
+        super().__init__(f"{STATUS.get(status, status)}: {msg}")
+        self.status = status
+
+
+class CrkParams(C.Structure):
+    _fields_ = [
+        ("box", C.c_double * 3),
+        ("rcut2", C.c_float), ("eps2", C.c_float), ("poly", C.c_float * 6), ("G", C.c_float),
+        ("gamma", C.c_float), ("av_cl", C.c_float), ("av_cq", C.c_float), ("av_eps2", C.c_float),
+        ("leaf_max_i", C.c_int32), ("leaf_max_j", C.c_int32),
+        ("leaf_max_gas_i", C.c_int32), ("leaf_max_gas_j", C.c_int32),
+        ("cell_side", C.c_double),
+    ]
+
+
+_PF = ["x", "y", "z", "vx", "vy", "vz", "m", "species", "id", "H", "u", "perm", "ax", "ay", "az", "V", "A", "B",
+       "dA", "dB", "rho", "P", "cs", "dv", "ahx", "ahy", "ahz", "dudt"]
+
+
+class CrkParticles(C.Structure):
+    _fields_ = [("n", C.c_int64)] + [(k, C.c_void_p) for k in _PF]
+
+
+class CrkLists(C.Structure):
+    _fields_ = [
+        ("n_leaf", C.c_int64 * 4),
+        ("leaf_first", C.c_void_p * 4), ("leaf_count", C.c_void_p * 4), ("leaf_bbox", C.c_void_p * 4),
+        ("leaf_maxh2", C.c_void_p * 4), ("leaf_cell", C.c_void_p * 4),
+        ("n_gas", C.c_int64), ("gas_idx", C.c_void_p),
+        ("n_entries", C.c_int64 * 2), ("row_off", C.c_void_p * 2), ("col", C.c_void_p * 2),
+        ("shift", C.c_void_p * 2),
+    ]
+
+
+_lib = None
+
+
+def lib():
+    """Load libcrksr.so (fails loudly when it is missing: no fallback path exists)."""
+    global _lib
+    if _lib is None:
+        if not os.path.exists(LIB_PATH):
+            raise ImportError(f"{LIB_PATH} is missing: run __graft_entry__.build() (no CPU fallback exists)")
+        L = C.CDLL(LIB_PATH)
+        vp = C.c_void_p
+        L.crk_create.argtypes = [C.POINTER(CrkParams), C.c_int, C.POINTER(vp)]
+        L.crk_destroy.argtypes = [vp]
+        for f in ("crk_build_lists", "crk_geometry", "crk_corrections", "crk_extras"):
+            getattr(L, f).argtypes = [vp, C.POINTER(CrkParticles), vp]
+        for f in ("crk_gravity_kick", "crk_hydro_accel_dudt"):
+            getattr(L, f).argtypes = [vp, C.POINTER(CrkParticles), C.c_float, vp]
+        L.crk_count_pairs.argtypes = [vp, C.POINTER(CrkParticles), vp, vp, vp, vp]
+        L.crk_list_view.argtypes = [vp, C.POINTER(CrkLists)]
+        L.crk_launch_count.argtypes = [vp]
+        L.crk_launch_count.restype = C.c_int64
+        L.crk_status_string.argtypes = [C.c_int]
+        L.crk_status_string.restype = C.c_char_p
+        L.crk_last_error.argtypes = [vp]
+        L.crk_last_error.restype = C.c_char_p
+        for f in ("crk_create", "crk_destroy", "crk_build_lists", "crk_gravity_kick", "crk_geometry",
+                  "crk_corrections", "crk_extras", "crk_hydro_accel_dudt", "crk_count_pairs", "crk_list_view"):
+            getattr(L, f).restype = C.c_int
+        _lib = L
+    return _lib
+
+
+def params_struct(p: dict) -> CrkParams:
+    s = CrkParams()
+    s.box[:] = p["box"]
+    for k in ("rcut2", "eps2", "G", "gamma", "av_cl", "av_cq", "av_eps2", "cell_side"):
+        setattr(s, k, p[k])
+    s.poly[:] = p["poly"]
+    for k in ("leaf_max_i", "leaf_max_j", "leaf_max_gas_i", "leaf_max_gas_j"):
+        setattr(s, k, p[k])
+    return s
+
+
+class Particles:
+    """Device-resident SoA particle set (torch tensors) plus output buffers."""
+
+    IN_F32 = ("x", "y", "z", "vx", "vy", "vz", "m", "H", "u")
+    OUT1 = ("ax", "ay", "az", "V", "A", "rho", "P", "cs", "ahx", "ahy", "ahz", "dudt")
+
+    def __init__(self, n: int, device, outputs: bool = True):
+        self.n = int(n)
+        self.device = torch.device(device)
+        z = lambda *s, dt=torch.float32: torch.zeros(*s, dtype=dt, device=self.device)  # noqa: E731
+        for k in self.IN_F32:
+            setattr(self, k, z(self.n))
+        self.species = z(self.n, dt=torch.uint8)
+        self.id = z(self.n, dt=torch.int64)
+        self.perm = z(self.n, dt=torch.int32)
+        self.outputs = outputs
+        if outputs:
+            for k in self.OUT1:
+                setattr(self, k, z(self.n))
+            self.B = z(3, self.n)
+            self.dA = z(3, self.n)
+            self.dB = z(9, self.n)
+            self.dv = z(9, self.n)
+
+    @classmethod
+    def from_host(cls, parts: dict, device="cuda", outputs=True, pinned=None):
+        n = parts["x"].shape[0]
+        p = cls(n, device, outputs)
+        p.load(parts)
+        return p
+
+    def load(self, parts: dict, non_blocking=False):
+        """Copy host arrays (numpy or pinned torch) to the device buffers."""
+        for k in self.IN_F32 + ("species", "id"):
+            src = parts[k]
+            if not isinstance(src, torch.Tensor):
+                src = torch.from_numpy(src)
+            getattr(self, k).copy_(src, non_blocking=non_blocking)
+
+    def struct(self) -> CrkParticles:
+        s = CrkParticles()
+        s.n = self.n
+        for k in _PF:
+            t = getattr(self, k, None)
+            setattr(s, k, t.data_ptr() if t is not None else None)
+        return s
+
+    def to_host(self, keys=None) -> dict:
+        keys = keys or [k for k in _PF if getattr(self, k, None) is not None]
+        return {k: getattr(self, k).cpu().numpy() for k in keys}
+
+
+class _CAI:
+    def __init__(self, ptr, shape, typestr):
+        self.__cuda_array_interface__ = {"shape": tuple(shape), "typestr": typestr, "data": (int(ptr), False),
+                                         "version": 3}
+
+
+def _wrap(ptr, shape, typestr, device):
+    if int(shape[0]) == 0 or not ptr:
+        dt = {"<i4": torch.int32, "<f4": torch.float32, "|i1": torch.int8, "<u8": torch.int64}[typestr]
+        return torch.zeros(shape, dtype=dt, device=device)
+    t = torch.as_tensor(_CAI(ptr, shape, typestr), device=device)
+    return t.clone()
+
+
+class Solver:
+    """One crk_ctx on one device; methods mirror the C-ABI calls of include/crksr.h."""
+
+    def __init__(self, params: dict, device=0):
+        self.params = dict(params)
+        self.device = torch.device("cuda", device) if isinstance(device, int) else torch.device(device)
+        self._ps = params_struct(params)
+        h = C.c_void_p()
+        idx = self.device.index if self.device.index is not None else torch.cuda.current_device()
+        self._check(lib().crk_create(C.byref(self._ps), idx, C.byref(h)), None)
+        self.ctx = h
+
+    def _check(self, st, ctx):
+        if st != 0:
+            msg = lib().crk_last_error(ctx).decode() if ctx is not None else ""
+            raise CrkError(st, msg)
+
+    def close(self):
+        if getattr(self, "ctx", None):
+            lib().crk_destroy(self.ctx)
+            self.ctx = None
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
+
+    @staticmethod
+    def _stream(stream):
+        s = stream if stream is not None else torch.cuda.current_stream()
+        return C.c_void_p(s.cuda_stream)
+
+    def _call(self, fn, parts, *args, stream=None):
+        ps = parts.struct()
+        self._check(fn(self.ctx, C.byref(ps), *args, self._stream(stream)), self.ctx)
+
+    def build_lists(self, parts, stream=None):
+        self._call(lib().crk_build_lists, parts, stream=stream)
+
+    def gravity_kick(self, parts, dt=0.0, stream=None):
+        self._call(lib().crk_gravity_kick, parts, C.c_float(dt), stream=stream)
+
+    def geometry(self, parts, stream=None):
+        self._call(lib().crk_geometry, parts, stream=stream)
+
+    def corrections(self, parts, stream=None):
+        self._call(lib().crk_corrections, parts, stream=stream)
+
+    def extras(self, parts, stream=None):
+        self._call(lib().crk_extras, parts, stream=stream)
+
+    def hydro_accel_dudt(self, parts, dt=0.0, stream=None):
+        self._call(lib().crk_hydro_accel_dudt, parts, C.c_float(dt), stream=stream)
+
+    def substep(self, parts, dt_grav=0.0, dt_hydro=0.0, stream=None, hydro=True):
+        """The whole short-range substep: a1-a8 in call order."""
+        self.build_lists(parts, stream)
+        self.gravity_kick(parts, dt_grav, stream)
+        if hydro:
+            self.geometry(parts, stream)
+            self.corrections(parts, stream)
+            self.extras(parts, stream)
+            self.hydro_accel_dudt(parts, dt_hydro, stream)
+
+    def count_pairs(self, parts, stream=None):
+        n = parts.n
+        cg = torch.zeros(n, dtype=torch.int32, device=parts.device)
+        ch = torch.zeros_like(cg)
+        cs = torch.zeros_like(cg)
+        ps = parts.struct()
+        self._check(lib().crk_count_pairs(self.ctx, C.byref(ps), C.c_void_p(cg.data_ptr()),
+                                          C.c_void_p(ch.data_ptr()), C.c_void_p(cs.data_ptr()),
+                                          self._stream(stream)), self.ctx)
+        return cg, ch, cs
+
+    def launch_count(self) -> int:
+        return int(lib().crk_launch_count(self.ctx))
+
+    def list_view(self) -> dict:
+        """Copies of the leaves and lists (device tensors)."""
+        lv = CrkLists()
+        self._check(lib().crk_list_view(self.ctx, C.byref(lv)), self.ctx)
+        torch.cuda.synchronize(self.device)
+        d = self.device
+        out = {"leaves": [], "lists": []}
+        for s in range(4):
+            nl = lv.n_leaf[s]
+            out["leaves"].append(dict(
+                first=_wrap(lv.leaf_first[s], (nl,), "<i4", d),
+                count=_wrap(lv.leaf_count[s], (nl,), "<i4", d),
+                bbox=_wrap(lv.leaf_bbox[s], (nl, 6), "<f4", d),
+                maxh2=_wrap(lv.leaf_maxh2[s], (nl,), "<f4", d) if s >= 2 else None,
+                cell=_wrap(lv.leaf_cell[s], (nl,), "<u8", d),
+            ))
+        out["gas_idx"] = _wrap(lv.gas_idx, (lv.n_gas,), "<i4", d)
+        for m in range(2):
+            na = lv.n_leaf[0 if m == 0 else 2]
+            ne = lv.n_entries[m]
+            out["lists"].append(dict(
+                row_off=_wrap(lv.row_off[m], (na + 1,), "<i4", d),
+                col=_wrap(lv.col[m], (ne,), "<i4", d),
+                shift=_wrap(lv.shift[m], (ne,), "|i1", d),
+            ))
+        return out

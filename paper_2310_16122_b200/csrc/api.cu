@@ -1,0 +1,249 @@
+// api.cu — the extern "C" boundary of libcrksr.so (include/crksr.h): context lifetime,
+// parameter validation, call-order state machine, error reporting.
+#include <cmath>
+#include <cstring>
+#include <new>
+
+#include "common.cuh"
+
+namespace crk {
+
+crk_status build_lists(crk_ctx* c, crk_particles* p, cudaStream_t st);
+crk_status gravity_kick(crk_ctx* c, crk_particles* p, float dt, cudaStream_t st);
+crk_status gravity_count(crk_ctx* c, crk_particles* p, int32_t* cnt, cudaStream_t st);
+crk_status geometry(crk_ctx* c, crk_particles* p, cudaStream_t st);
+crk_status corrections(crk_ctx* c, crk_particles* p, cudaStream_t st);
+crk_status extras(crk_ctx* c, crk_particles* p, cudaStream_t st);
+crk_status accel_dudt(crk_ctx* c, crk_particles* p, float dt, cudaStream_t st);
+crk_status hydro_count(crk_ctx* c, int32_t* cgather, int32_t* csym, cudaStream_t st);
+
+crk_status fail(crk_ctx* c, crk_status s, const char* what) {
+    if (c) c->err = what;
+    return s;
+}
+
+crk_status cuda_check(crk_ctx* c, cudaError_t e, const char* what) {
+    if (e == cudaSuccess) return CRK_OK;
+    if (c) c->err = std::string(what) + ": " + cudaGetErrorString(e);
+    return e == cudaErrorMemoryAllocation ? CRK_ENOMEM : CRK_ECUDA;
+}
+
+crk_status grow(crk_ctx* c, Buf& b, size_t bytes, cudaStream_t st) {
+    if (bytes <= b.cap) return CRK_OK;
+    if (b.p) {
+        cudaError_t e = cudaFreeAsync(b.p, st);
+        if (e != cudaSuccess) return cuda_check(c, e, "cudaFreeAsync");
+        b.p = nullptr;
+        b.cap = 0;
+    }
+    size_t want = bytes + bytes / 8 + 256;
+    cudaError_t e = cudaMallocAsync(&b.p, want, st);
+    if (e != cudaSuccess) {
+        cudaGetLastError();
+        return cuda_check(c, e, "cudaMallocAsync");
+    }
+    b.cap = want;
+    return CRK_OK;
+}
+
+static bool pow2(double v) {
+    if (!(v > 0)) return false;
+    int e;
+    return std::frexp(v, &e) == 0.5;
+}
+
+static crk_status validate(const crk_params* p, Layout& L, std::string& why) {
+    double lmax = 0;
+    for (int a = 0; a < 3; ++a) {
+        if (!pow2(p->box[a]) || p->box[a] < 16 || p->box[a] > 4096) { why = "box must be powers of two in [16, 4096]"; return CRK_EINVAL; }
+        lmax = p->box[a] > lmax ? p->box[a] : lmax;
+    }
+    if (!pow2(p->cell_side) || p->cell_side < 1.0) { why = "cell_side must be a power of two >= 1"; return CRK_EINVAL; }
+    for (int a = 0; a < 3; ++a)
+        if (p->cell_side > p->box[a] / 4) { why = "cell_side must be <= box/4"; return CRK_EINVAL; }
+    for (int a = 0; a < 3; ++a)
+        if (!(p->rcut2 > 0) || std::sqrt((double)p->rcut2) >= p->box[a] / 4) { why = "need 0 < rcut < box/4"; return CRK_EINVAL; }
+    if (!(p->eps2 > 0)) { why = "eps2 must be > 0"; return CRK_EINVAL; }
+    if (!(p->leaf_max_i == 16 || p->leaf_max_i == 32 || p->leaf_max_i == 64 || p->leaf_max_i == 128) ||
+        p->leaf_max_i > GRAV_NW * GRAV_G) { why = "leaf_max_i must be 16, 32, 64 or 128"; return CRK_EINVAL; }
+    if (p->leaf_max_j != JMAX || p->leaf_max_gas_j != JMAX) { why = "leaf_max_j and leaf_max_gas_j must be 8"; return CRK_EINVAL; }
+    if (!(p->leaf_max_gas_i == 16 || p->leaf_max_gas_i == 32 || p->leaf_max_gas_i == 64) ||
+        p->leaf_max_gas_i > HYD_NW * HYD_G) { why = "leaf_max_gas_i must be 16, 32 or 64"; return CRK_EINVAL; }
+    if (!(p->gamma > 1.f)) { why = "gamma must be > 1"; return CRK_EINVAL; }
+    L.q = std::ldexp(lmax, -23);
+    L.inv_q = (float)(1.0 / L.q);
+    L.cs = (int)std::lround(std::log2(p->cell_side / L.q));
+    int maxn = 1;
+    for (int a = 0; a < 3; ++a) {
+        L.ncell[a] = (int)std::lround(p->box[a] / p->cell_side);
+        maxn = L.ncell[a] > maxn ? L.ncell[a] : maxn;
+        L.L[a] = (float)p->box[a];
+    }
+    if (maxn > 256) { why = "at most 256 cells per axis (raise cell_side)"; return CRK_EINVAL; }
+    L.cbits = 0;
+    while ((1 << L.cbits) < maxn) ++L.cbits;
+    L.fbits = (64 - 3 * L.cbits) / 3;
+    if (L.fbits > L.cs) L.fbits = L.cs;
+    L.ncm = (int64_t)1 << (3 * L.cbits);
+    return CRK_OK;
+}
+
+}  // namespace crk
+
+using namespace crk;
+
+extern "C" {
+
+crk_status crk_create(const crk_params* params, int device, crk_ctx** out) {
+    if (!params || !out) return CRK_EINVAL;
+    *out = nullptr;
+    Layout L;
+    std::string why;
+    crk_status s = validate(params, L, why);
+    if (s != CRK_OK) return s;
+    cudaError_t e = cudaSetDevice(device);
+    if (e != cudaSuccess) return CRK_ECUDA;
+    crk_ctx* c = new (std::nothrow) crk_ctx();
+    if (!c) return CRK_ENOMEM;
+    c->prm = *params;
+    c->device = device;
+    c->lay = L;
+    void* h = nullptr;
+    e = cudaMallocHost(&h, 256);
+    if (e != cudaSuccess) {
+        delete c;
+        return CRK_ENOMEM;
+    }
+    c->pinned.p = h;
+    c->pinned.cap = 256;
+    // the gravity kernel's dynamic shared memory fits in the default 48 KB
+    *out = c;
+    return CRK_OK;
+}
+
+crk_status crk_destroy(crk_ctx* c) {
+    if (!c) return CRK_EINVAL;
+    cudaSetDevice(c->device);
+    cudaDeviceSynchronize();
+    Buf* bufs[] = {&c->keys_a, &c->keys_b, &c->idx_a, &c->idx_b, &c->cub_tmp, &c->scratch, &c->xm,
+                   &c->cell_start, &c->cell_end, &c->leaf_cnt, &c->gflag, &c->grank, &c->gas_idx,
+                   &c->dev_scalars, &c->gpos, &c->gvel, &c->gV, &c->gcoef, &c->grec, &c->gu};
+    for (Buf* b : bufs)
+        if (b->p) cudaFree(b->p);
+    for (int s = 0; s < 4; ++s) {
+        Buf* lb[] = {&c->lfirst[s], &c->lcount[s], &c->lbbox[s], &c->lmaxh2[s], &c->lcell[s]};
+        for (Buf* b : lb)
+            if (b->p) cudaFree(b->p);
+    }
+    for (int m = 0; m < 2; ++m) {
+        Buf* lb[] = {&c->rowlen[m], &c->rowoff[m], &c->col[m], &c->shift[m]};
+        for (Buf* b : lb)
+            if (b->p) cudaFree(b->p);
+    }
+    if (c->pinned.p) cudaFreeHost(c->pinned.p);
+    delete c;
+    return CRK_OK;
+}
+
+static crk_status check_parts(crk_ctx* c, const crk_particles* p, bool need_built) {
+    if (!c) return CRK_EINVAL;
+    if (!p || !p->x || !p->y || !p->z || !p->m || !p->species || !p->id || !p->H || p->n <= 0)
+        return fail(c, CRK_EINVAL, "missing particle arrays");
+    if (p->n > ((int64_t)1 << 31) - 2) return fail(c, CRK_EINVAL, "n too large");
+    if (need_built && (c->stage < ST_LISTS || p->n != c->n)) return fail(c, CRK_ESTATE, "call crk_build_lists first");
+    cudaError_t e = cudaSetDevice(c->device);
+    if (e != cudaSuccess) return cuda_check(c, e, "cudaSetDevice");
+    return CRK_OK;
+}
+
+crk_status crk_build_lists(crk_ctx* c, crk_particles* p, void* stream) {
+    CRK_TRY(check_parts(c, p, false));
+    if (!p->vx || !p->vy || !p->vz || !p->u) return fail(c, CRK_EINVAL, "missing particle arrays");
+    return build_lists(c, p, (cudaStream_t)stream);
+}
+
+crk_status crk_gravity_kick(crk_ctx* c, crk_particles* p, float dt, void* stream) {
+    CRK_TRY(check_parts(c, p, true));
+    return gravity_kick(c, p, dt, (cudaStream_t)stream);
+}
+
+crk_status crk_geometry(crk_ctx* c, crk_particles* p, void* stream) {
+    CRK_TRY(check_parts(c, p, true));
+    CRK_TRY(geometry(c, p, (cudaStream_t)stream));
+    c->stage = ST_GEO;
+    return CRK_OK;
+}
+
+crk_status crk_corrections(crk_ctx* c, crk_particles* p, void* stream) {
+    CRK_TRY(check_parts(c, p, true));
+    if (c->stage < ST_GEO) return fail(c, CRK_ESTATE, "call crk_geometry first");
+    CRK_TRY(corrections(c, p, (cudaStream_t)stream));
+    c->stage = ST_COR;
+    return CRK_OK;
+}
+
+crk_status crk_extras(crk_ctx* c, crk_particles* p, void* stream) {
+    CRK_TRY(check_parts(c, p, true));
+    if (c->stage < ST_COR) return fail(c, CRK_ESTATE, "call crk_corrections first");
+    if (!p->vx || !p->vy || !p->vz || !p->u) return fail(c, CRK_EINVAL, "extras needs v and u");
+    CRK_TRY(extras(c, p, (cudaStream_t)stream));
+    c->stage = ST_EXT;
+    return CRK_OK;
+}
+
+crk_status crk_hydro_accel_dudt(crk_ctx* c, crk_particles* p, float dt, void* stream) {
+    CRK_TRY(check_parts(c, p, true));
+    if (c->stage < ST_EXT) return fail(c, CRK_ESTATE, "call crk_extras first");
+    return accel_dudt(c, p, dt, (cudaStream_t)stream);
+}
+
+crk_status crk_count_pairs(crk_ctx* c, crk_particles* p, int32_t* cgrav, int32_t* cgather, int32_t* csym,
+                           void* stream) {
+    CRK_TRY(check_parts(c, p, true));
+    if (!cgrav || !cgather || !csym) return fail(c, CRK_EINVAL, "null count array");
+    cudaStream_t st = (cudaStream_t)stream;
+    CRK_TRY(cuda_check(c, cudaMemsetAsync(cgather, 0, p->n * 4, st), "memset"));
+    CRK_TRY(cuda_check(c, cudaMemsetAsync(csym, 0, p->n * 4, st), "memset"));
+    CRK_TRY(gravity_count(c, p, cgrav, st));
+    return hydro_count(c, cgather, csym, st);
+}
+
+crk_status crk_list_view(crk_ctx* c, crk_lists* o) {
+    if (!c || !o) return CRK_EINVAL;
+    if (c->stage < ST_LISTS) return fail(c, CRK_ESTATE, "call crk_build_lists first");
+    for (int s = 0; s < 4; ++s) {
+        o->n_leaf[s] = c->nleaf[s];
+        o->leaf_first[s] = P<int32_t>(c->lfirst[s]);
+        o->leaf_count[s] = P<int32_t>(c->lcount[s]);
+        o->leaf_bbox[s] = P<float>(c->lbbox[s]);
+        o->leaf_maxh2[s] = s >= 2 ? P<float>(c->lmaxh2[s]) : nullptr;
+        o->leaf_cell[s] = P<uint64_t>(c->lcell[s]);
+    }
+    o->n_gas = c->n_gas;
+    o->gas_idx = P<int32_t>(c->gas_idx);
+    for (int m = 0; m < 2; ++m) {
+        o->n_entries[m] = c->nent[m];
+        o->row_off[m] = P<int32_t>(c->rowoff[m]);
+        o->col[m] = P<int32_t>(c->col[m]);
+        o->shift[m] = P<int8_t>(c->shift[m]);
+    }
+    return CRK_OK;
+}
+
+int64_t crk_launch_count(crk_ctx* c) { return c ? c->launches : -1; }
+
+const char* crk_status_string(crk_status s) {
+    switch (s) {
+    case CRK_OK: return "ok";
+    case CRK_EINVAL: return "invalid argument";
+    case CRK_ENOMEM: return "out of device memory";
+    case CRK_ECUDA: return "CUDA error";
+    case CRK_ESTATE: return "call order violated";
+    case CRK_ECAPACITY: return "capacity exceeded";
+    }
+    return "unknown status";
+}
+
+const char* crk_last_error(crk_ctx* c) { return c ? c->err.c_str() : "null ctx"; }
+
+}  // extern "C"

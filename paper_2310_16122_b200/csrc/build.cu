@@ -1,0 +1,447 @@
+// build.cu — a1 + a2: sort, leaf build and leaf-pair interaction lists
+// (definitions §8(c) O1, O3, O4; the paper's leaves: PAPER.md:418-422).
+//
+//   key (cell Morton | in-cell Morton) -> CUB onesweep radix sort (+ id tie fix)
+//   -> permute the caller's SoA in place -> chaining-mesh cell runs (dense, Morton-indexed)
+//   -> gas ranks -> four leaf sets (balanced chunks of each cell run) -> bboxes
+//   -> gravity and hydro CSR lists (exact fp64 bbox test, per-axis periodic shift).
+// HBM-bound; every kernel is a streaming pass except the list kernels (one warp per i-leaf).
+#include <cub/cub.cuh>
+
+#include "common.cuh"
+
+namespace crk {
+
+// ---------------------------------------------------------------- keys
+__global__ void k_keys(int64_t n, const float* __restrict__ x, const float* __restrict__ y,
+                       const float* __restrict__ z, float inv_q, int cs, int fbits, uint64_t* keys,
+                       int32_t* idx) {
+    const int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+    if (i >= n) return;
+    const uint32_t xi = (uint32_t)(x[i] * inv_q), yi = (uint32_t)(y[i] * inv_q), zi = (uint32_t)(z[i] * inv_q);
+    const uint32_t msk = (1u << cs) - 1u, sh = cs - fbits;
+    const uint64_t cm = morton3(xi >> cs, yi >> cs, zi >> cs);
+    const uint64_t fm = morton3((xi & msk) >> sh, (yi & msk) >> sh, (zi & msk) >> sh);
+    keys[i] = (cm << (3 * fbits)) | fm;
+    idx[i] = (int32_t)i;
+}
+
+// Runs of equal keys (coincident to 1/2^fbits of a cell) are ordered by id: total order (O3).
+__global__ void k_tie_fix(int64_t n, const uint64_t* __restrict__ keys, int32_t* idx, const int64_t* __restrict__ id) {
+    const int64_t k = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+    if (k + 1 >= n) return;
+    if (keys[k] != keys[k + 1]) return;
+    if (k > 0 && keys[k - 1] == keys[k]) return;  // not the run start
+    int64_t e = k + 1;
+    while (e + 1 < n && keys[e + 1] == keys[k]) ++e;
+    for (int64_t a = k + 1; a <= e; ++a) {  // insertion sort by id
+        const int32_t v = idx[a];
+        const int64_t iv = id[v];
+        int64_t b = a - 1;
+        while (b >= k && id[idx[b]] > iv) {
+            idx[b + 1] = idx[b];
+            --b;
+        }
+        idx[b + 1] = v;
+    }
+}
+
+// ---------------------------------------------------------------- permute
+__global__ void k_gather_f32(int64_t n, const int32_t* __restrict__ perm, const float* __restrict__ in, float* out) {
+    const int64_t k = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+    if (k < n) out[k] = in[perm[k]];
+}
+__global__ void k_gather_u8(int64_t n, const int32_t* __restrict__ perm, const uint8_t* __restrict__ in, uint8_t* out) {
+    const int64_t k = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+    if (k < n) out[k] = in[perm[k]];
+}
+__global__ void k_gather_i64(int64_t n, const int32_t* __restrict__ perm, const int64_t* __restrict__ in, int64_t* out) {
+    const int64_t k = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+    if (k < n) out[k] = in[perm[k]];
+}
+
+// after the permute: packed (x,y,z,m), gas flags, cell runs
+__global__ void k_post_sort(int64_t n, const uint64_t* __restrict__ keys, int fbits, const float* __restrict__ x,
+                            const float* __restrict__ y, const float* __restrict__ z, const float* __restrict__ m,
+                            const uint8_t* __restrict__ sp, float4* xm, int32_t* gflag, int32_t* cstart,
+                            int32_t* cend) {
+    const int64_t k = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+    if (k >= n) return;
+    xm[k] = make_float4(x[k], y[k], z[k], m[k]);
+    gflag[k] = sp[k] == 1 ? 1 : 0;
+    const uint64_t c = keys[k] >> (3 * fbits);
+    if (k == 0 || (keys[k - 1] >> (3 * fbits)) != c) cstart[c] = (int32_t)k;
+    if (k == n - 1 || (keys[k + 1] >> (3 * fbits)) != c) cend[c] = (int32_t)(k + 1);
+}
+
+__global__ void k_gas_pack(int64_t n, const int32_t* __restrict__ gflag, const int32_t* __restrict__ grank,
+                           const float* __restrict__ x, const float* __restrict__ y, const float* __restrict__ z,
+                           const float* __restrict__ H, int32_t* gas_idx, float4* gpos, float* dmax_h2) {
+    const int64_t k = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+    float h2 = 0.f;
+    if (k < n && gflag[k]) {
+        const int32_t g = grank[k];
+        gas_idx[g] = (int32_t)k;
+        gpos[g] = make_float4(x[k], y[k], z[k], H[k]);
+        h2 = __fmul_rn(H[k], H[k]);
+    }
+    h2 = warp_max(h2);
+    if ((threadIdx.x & 31) == 0 && h2 > 0.f) atomicMax(reinterpret_cast<int*>(dmax_h2), __float_as_int(h2));
+}
+
+// ---------------------------------------------------------------- leaves (O3)
+// counts per cell for the 4 leaf sets: cnt[s*(ncm+1) + c]
+__global__ void k_leaf_counts(int64_t ncm, const int32_t* __restrict__ cstart, const int32_t* __restrict__ cend,
+                              const int32_t* __restrict__ grank, int l0, int l1, int l2, int l3, int32_t* cnt) {
+    const int64_t c = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+    if (c > ncm) return;
+    int nc = 0, gc = 0;
+    if (c < ncm) {
+        nc = cend[c] - cstart[c];
+        if (nc > 0) gc = grank[cend[c]] - grank[cstart[c]];
+    }
+    cnt[0 * (ncm + 1) + c] = (nc + l0 - 1) / l0;
+    cnt[1 * (ncm + 1) + c] = (nc + l1 - 1) / l1;
+    cnt[2 * (ncm + 1) + c] = (gc + l2 - 1) / l2;
+    cnt[3 * (ncm + 1) + c] = (gc + l3 - 1) / l3;
+}
+
+__global__ void k_leaf_fill(int64_t ncm, const int32_t* __restrict__ cstart, const int32_t* __restrict__ cend,
+                            const int32_t* __restrict__ grank, const int32_t* __restrict__ off, int set, int lmax,
+                            int32_t* first, int32_t* count, uint64_t* lcell) {
+    const int64_t c = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+    if (c >= ncm) return;
+    const int nc = cend[c] - cstart[c];
+    if (nc <= 0) return;
+    int base, cnt;
+    if (set < 2) {
+        base = cstart[c];
+        cnt = nc;
+    } else {
+        base = grank[cstart[c]];
+        cnt = grank[cend[c]] - base;
+    }
+    const int nch = (cnt + lmax - 1) / lmax;
+    const int o = off[c];
+    for (int t = 0; t < nch; ++t) {
+        const int lo = (int)((int64_t)t * cnt / nch), hi = (int)((int64_t)(t + 1) * cnt / nch);
+        first[o + t] = base + lo;
+        count[o + t] = hi - lo;
+        lcell[o + t] = (uint64_t)c;
+    }
+}
+
+// bbox (+ max H^2) per leaf; one thread per leaf, members contiguous in xm / gpos
+__global__ void k_leaf_bbox(int64_t nl, const int32_t* __restrict__ first, const int32_t* __restrict__ count,
+                            const float4* __restrict__ pts, int gas, float* bbox, float* maxh2) {
+    const int64_t l = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+    if (l >= nl) return;
+    float lo0 = INFINITY, lo1 = INFINITY, lo2 = INFINITY, hi0 = -INFINITY, hi1 = -INFINITY, hi2 = -INFINITY, mh = 0.f;
+    const int f = first[l], c = count[l];
+    for (int t = 0; t < c; ++t) {
+        const float4 p = pts[f + t];
+        lo0 = fminf(lo0, p.x); lo1 = fminf(lo1, p.y); lo2 = fminf(lo2, p.z);
+        hi0 = fmaxf(hi0, p.x); hi1 = fmaxf(hi1, p.y); hi2 = fmaxf(hi2, p.z);
+        if (gas) mh = fmaxf(mh, __fmul_rn(p.w, p.w));
+    }
+    float* b = bbox + 6 * l;
+    b[0] = lo0; b[1] = lo1; b[2] = lo2; b[3] = hi0; b[4] = hi1; b[5] = hi2;
+    if (gas) maxh2[l] = mh;
+}
+
+// ---------------------------------------------------------------- lists (O4)
+// per axis: gap_s = max(0, lo_b + sL - hi_a, lo_a - hi_b - sL) for s = 0, -1, +1 (first
+// minimum); d2 = sum gap^2 in fp64 (exact for q-multiples); keep iff d2 < cut2 (1 + 2^-20).
+__device__ __forceinline__ bool leaf_pair_test(const float* ba, const float* bb, const double L[3], double cut2s,
+                                               int& code) {
+    double d2 = 0.0;
+    int sc[3];
+#pragma unroll
+    for (int d = 0; d < 3; ++d) {
+        double best = 1e300;
+        int bs = 0;
+#pragma unroll
+        for (int t = 0; t < 3; ++t) {
+            const int s = t == 0 ? 0 : (t == 1 ? -1 : 1);
+            const double sL = s * L[d];
+            const double g1 = (double)bb[d] + sL - (double)ba[3 + d];
+            const double g2 = (double)ba[d] - (double)bb[3 + d] - sL;
+            const double g = fmax(0.0, fmax(g1, g2));
+            if (g < best) { best = g; bs = s; }
+        }
+        sc[d] = bs;
+        d2 = fma(best, best, d2);  // exact: all terms are integers times q^2 below 2^52 q^2
+    }
+    code = (sc[0] + 1) + 3 * (sc[1] + 1) + 9 * (sc[2] + 1);
+    return d2 < cut2s;
+}
+
+struct ListArgs {
+    int64_t nA;
+    const float* bboxA;
+    const float* maxh2A;
+    const float* bboxB;
+    const float* maxh2B;
+    const int32_t* loffB;  // per-cell offsets of the j-leaf set (ncm + 1)
+    const float* dmax_h2;  // global max H^2 (hydro mode)
+    int mode;              // 0 gravity (rcut2), 1 hydro (max of the two leaves' max H^2)
+    float rcut2;
+    double L[3];
+    double cell_side;
+    int ncell[3];
+    int32_t* rowlen;       // pass 1
+    const int32_t* rowoff; // pass 2
+    int32_t* col;
+    int8_t* shift;
+};
+
+// one warp per i-leaf; candidate j-leaves come from the cells within reach of the i-bbox
+template <bool FILL>
+__global__ void k_lists(ListArgs A) {
+    const int64_t a = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5;
+    const int lane = threadIdx.x & 31;
+    if (a >= A.nA) return;
+    const float* ba = A.bboxA + 6 * a;
+    const double slack = 1.0 + 0x1p-20;
+    double reach2;
+    if (A.mode == 0) reach2 = (double)A.rcut2;
+    else reach2 = fmax((double)A.maxh2A[a], (double)*A.dmax_h2);
+    const double reach = sqrt(reach2 * slack) * (1.0 + 1e-12) + 1e-12;
+    int c0[3], c1[3];
+#pragma unroll
+    for (int d = 0; d < 3; ++d) {
+        c0[d] = (int)floor(((double)ba[d] - reach) / A.cell_side);
+        c1[d] = (int)floor(((double)ba[3 + d] + reach) / A.cell_side);
+        if (c1[d] - c0[d] + 1 >= A.ncell[d]) { c0[d] = 0; c1[d] = A.ncell[d] - 1; }
+    }
+    int outpos = FILL ? A.rowoff[a] : 0;
+    int total = 0;
+    for (int cz = c0[2]; cz <= c1[2]; ++cz)
+        for (int cy = c0[1]; cy <= c1[1]; ++cy)
+            for (int cx = c0[0]; cx <= c1[0]; ++cx) {
+                const uint32_t wx = (uint32_t)((cx % A.ncell[0] + A.ncell[0]) % A.ncell[0]);
+                const uint32_t wy = (uint32_t)((cy % A.ncell[1] + A.ncell[1]) % A.ncell[1]);
+                const uint32_t wz = (uint32_t)((cz % A.ncell[2] + A.ncell[2]) % A.ncell[2]);
+                const uint64_t m = morton3(wx, wy, wz);
+                const int b0 = A.loffB[m], b1 = A.loffB[m + 1];
+                for (int bb = b0; bb < b1; bb += 32) {
+                    const int b = bb + lane;
+                    bool keep = false;
+                    int code = 13;
+                    if (b < b1) {
+                        const double cut2 = A.mode == 0 ? (double)A.rcut2
+                                                        : fmax((double)A.maxh2A[a], (double)A.maxh2B[b]);
+                        keep = leaf_pair_test(ba, A.bboxB + 6 * (int64_t)b, A.L, cut2 * slack, code);
+                    }
+                    const unsigned msk = __ballot_sync(0xffffffffu, keep);
+                    if (FILL && keep) {
+                        const int p = outpos + __popc(msk & ((1u << lane) - 1u));
+                        A.col[p] = b;
+                        A.shift[p] = (int8_t)code;
+                    }
+                    outpos += __popc(msk);
+                    total += __popc(msk);
+                }
+            }
+    if (!FILL && lane == 0) A.rowlen[a] = total;
+}
+
+// ---------------------------------------------------------------- driver
+static inline unsigned nblk(int64_t n, int b) { return (unsigned)((n + b - 1) / b); }
+
+crk_status build_lists(crk_ctx* c, crk_particles* p, cudaStream_t st) {
+    const int64_t n = p->n;
+    const Layout& L = c->lay;
+    c->n = n;
+    c->stage = ST_NONE;
+    const int bits = 3 * (L.cbits + L.fbits);
+    // ---- buffers
+    CRK_TRY(grow(c, c->keys_a, n * 8, st));
+    CRK_TRY(grow(c, c->keys_b, n * 8, st));
+    CRK_TRY(grow(c, c->idx_a, n * 4, st));
+    CRK_TRY(grow(c, c->idx_b, n * 4, st));
+    CRK_TRY(grow(c, c->scratch, n * 8, st));
+    CRK_TRY(grow(c, c->xm, n * 16, st));
+    CRK_TRY(grow(c, c->gflag, (n + 1) * 4, st));
+    CRK_TRY(grow(c, c->grank, (n + 1) * 4, st));
+    CRK_TRY(grow(c, c->cell_start, L.ncm * 4, st));
+    CRK_TRY(grow(c, c->cell_end, L.ncm * 4, st));
+    CRK_TRY(grow(c, c->leaf_cnt, 4 * (L.ncm + 1) * 4, st));
+    CRK_TRY(grow(c, c->dev_scalars, 64, st));
+    if (n == 0) return fail(c, CRK_EINVAL, "no particles");
+
+    // ---- keys + sort
+    k_keys<<<nblk(n, 256), 256, 0, st>>>(n, p->x, p->y, p->z, L.inv_q, L.cs, L.fbits, P<uint64_t>(c->keys_a),
+                                         P<int32_t>(c->idx_a));
+    CRK_LAUNCHED(c, "keys");
+    cub::DoubleBuffer<uint64_t> dk(P<uint64_t>(c->keys_a), P<uint64_t>(c->keys_b));
+    cub::DoubleBuffer<int32_t> dv(P<int32_t>(c->idx_a), P<int32_t>(c->idx_b));
+    size_t tmp = 0;
+    cub::DeviceRadixSort::SortPairs(nullptr, tmp, dk, dv, (int)n, 0, bits, st);
+    size_t tmp2 = 0;
+    cub::DeviceScan::ExclusiveSum(nullptr, tmp2, P<int32_t>(c->gflag), P<int32_t>(c->grank), (int)(n + 1), st);
+    size_t tmp3 = 0;
+    cub::DeviceScan::ExclusiveSum(nullptr, tmp3, P<int32_t>(c->leaf_cnt), P<int32_t>(c->leaf_cnt), (int)(L.ncm + 1), st);
+    size_t need = tmp > tmp2 ? tmp : tmp2;
+    need = need > tmp3 ? need : tmp3;
+    need = need > (size_t)(n + 1) * 4 ? need : (size_t)(n + 1) * 4;
+    CRK_TRY(grow(c, c->cub_tmp, need, st));
+    tmp = c->cub_tmp.cap;
+    CRK_TRY(cuda_check(c, cub::DeviceRadixSort::SortPairs(c->cub_tmp.p, tmp, dk, dv, (int)n, 0, bits, st), "radix sort"));
+    c->launches += 4;  // onesweep: histogram + per-pass kernels (counted approximately)
+    const uint64_t* keys = dk.Current();
+    int32_t* perm = dv.Current();
+    k_tie_fix<<<nblk(n, 256), 256, 0, st>>>(n, keys, perm, p->id);
+    CRK_LAUNCHED(c, "tie fix");
+
+    // ---- permute caller arrays in place (gather into scratch, copy back)
+    float* f32[9] = {p->x, p->y, p->z, p->vx, p->vy, p->vz, p->m, p->H, p->u};
+    for (int t = 0; t < 9; ++t) {
+        k_gather_f32<<<nblk(n, 256), 256, 0, st>>>(n, perm, f32[t], P<float>(c->scratch));
+        CRK_LAUNCHED(c, "permute");
+        CRK_TRY(cuda_check(c, cudaMemcpyAsync(f32[t], c->scratch.p, n * 4, cudaMemcpyDeviceToDevice, st), "copy"));
+    }
+    k_gather_u8<<<nblk(n, 256), 256, 0, st>>>(n, perm, p->species, P<uint8_t>(c->scratch));
+    CRK_LAUNCHED(c, "permute");
+    CRK_TRY(cuda_check(c, cudaMemcpyAsync(p->species, c->scratch.p, n, cudaMemcpyDeviceToDevice, st), "copy"));
+    k_gather_i64<<<nblk(n, 256), 256, 0, st>>>(n, perm, p->id, P<int64_t>(c->scratch));
+    CRK_LAUNCHED(c, "permute");
+    CRK_TRY(cuda_check(c, cudaMemcpyAsync(p->id, c->scratch.p, n * 8, cudaMemcpyDeviceToDevice, st), "copy"));
+    if (p->perm)
+        CRK_TRY(cuda_check(c, cudaMemcpyAsync(p->perm, perm, n * 4, cudaMemcpyDeviceToDevice, st), "copy"));
+
+    // ---- cells, gas ranks
+    CRK_TRY(cuda_check(c, cudaMemsetAsync(c->cell_start.p, 0, L.ncm * 4, st), "memset"));
+    CRK_TRY(cuda_check(c, cudaMemsetAsync(c->cell_end.p, 0, L.ncm * 4, st), "memset"));
+    CRK_TRY(cuda_check(c, cudaMemsetAsync(P<int32_t>(c->gflag) + n, 0, 4, st), "memset"));
+    CRK_TRY(cuda_check(c, cudaMemsetAsync(c->dev_scalars.p, 0, 64, st), "memset"));
+    k_post_sort<<<nblk(n, 256), 256, 0, st>>>(n, keys, L.fbits, p->x, p->y, p->z, p->m, p->species,
+                                              P<float4>(c->xm), P<int32_t>(c->gflag), P<int32_t>(c->cell_start),
+                                              P<int32_t>(c->cell_end));
+    CRK_LAUNCHED(c, "post sort");
+    tmp = c->cub_tmp.cap;
+    CRK_TRY(cuda_check(c, cub::DeviceScan::ExclusiveSum(c->cub_tmp.p, tmp, P<int32_t>(c->gflag), P<int32_t>(c->grank),
+                                                        (int)(n + 1), st), "gas scan"));
+    c->launches += 2;
+    // n_gas: needed for buffer sizes -> read back with the leaf totals below; use n as bound
+    CRK_TRY(grow(c, c->gas_idx, n * 4, st));
+    CRK_TRY(grow(c, c->gpos, n * 16, st));
+    k_gas_pack<<<nblk(n, 256), 256, 0, st>>>(n, P<int32_t>(c->gflag), P<int32_t>(c->grank), p->x, p->y, p->z, p->H,
+                                             P<int32_t>(c->gas_idx), P<float4>(c->gpos), P<float>(c->dev_scalars));
+    CRK_LAUNCHED(c, "gas pack");
+
+    // ---- leaves
+    const int lmax[4] = {c->prm.leaf_max_i, c->prm.leaf_max_j, c->prm.leaf_max_gas_i, c->prm.leaf_max_gas_j};
+    int32_t* cnt = P<int32_t>(c->leaf_cnt);
+    k_leaf_counts<<<nblk(L.ncm + 1, 256), 256, 0, st>>>(L.ncm, P<int32_t>(c->cell_start), P<int32_t>(c->cell_end),
+                                                        P<int32_t>(c->grank), lmax[0], lmax[1], lmax[2], lmax[3], cnt);
+    CRK_LAUNCHED(c, "leaf counts");
+    for (int s = 0; s < 4; ++s) {
+        tmp = c->cub_tmp.cap;
+        CRK_TRY(cuda_check(c, cub::DeviceScan::ExclusiveSum(c->cub_tmp.p, tmp, cnt + s * (L.ncm + 1),
+                                                            cnt + s * (L.ncm + 1), (int)(L.ncm + 1), st), "leaf scan"));
+        c->launches += 2;
+    }
+    // totals: leaf counts (4) + n_gas, one synchronisation
+    int32_t* host = P<int32_t>(c->pinned);
+    for (int s = 0; s < 4; ++s)
+        CRK_TRY(cuda_check(c, cudaMemcpyAsync(host + s, cnt + s * (L.ncm + 1) + L.ncm, 4, cudaMemcpyDeviceToHost, st), "d2h"));
+    CRK_TRY(cuda_check(c, cudaMemcpyAsync(host + 4, P<int32_t>(c->grank) + n, 4, cudaMemcpyDeviceToHost, st), "d2h"));
+    CRK_TRY(cuda_check(c, cudaStreamSynchronize(st), "sync"));
+    for (int s = 0; s < 4; ++s) c->nleaf[s] = host[s];
+    c->n_gas = host[4];
+    for (int s = 0; s < 4; ++s) {
+        const int64_t nl = c->nleaf[s] > 0 ? c->nleaf[s] : 1;
+        CRK_TRY(grow(c, c->lfirst[s], nl * 4, st));
+        CRK_TRY(grow(c, c->lcount[s], nl * 4, st));
+        CRK_TRY(grow(c, c->lbbox[s], nl * 24, st));
+        CRK_TRY(grow(c, c->lcell[s], nl * 8, st));
+        if (s >= 2) CRK_TRY(grow(c, c->lmaxh2[s], nl * 4, st));
+        k_leaf_fill<<<nblk(L.ncm, 256), 256, 0, st>>>(L.ncm, P<int32_t>(c->cell_start), P<int32_t>(c->cell_end),
+                                                      P<int32_t>(c->grank), cnt + s * (L.ncm + 1), s, lmax[s],
+                                                      P<int32_t>(c->lfirst[s]), P<int32_t>(c->lcount[s]),
+                                                      P<uint64_t>(c->lcell[s]));
+        CRK_LAUNCHED(c, "leaf fill");
+        if (c->nleaf[s] > 0) {
+            k_leaf_bbox<<<nblk(c->nleaf[s], 128), 128, 0, st>>>(
+                c->nleaf[s], P<int32_t>(c->lfirst[s]), P<int32_t>(c->lcount[s]),
+                s < 2 ? P<float4>(c->xm) : P<float4>(c->gpos), s >= 2, P<float>(c->lbbox[s]),
+                s >= 2 ? P<float>(c->lmaxh2[s]) : nullptr);
+            CRK_LAUNCHED(c, "leaf bbox");
+        }
+    }
+
+    // ---- lists: count, scan, fill
+    for (int m = 0; m < 2; ++m) {
+        const int sa = m == 0 ? 0 : 2, sb = m == 0 ? 1 : 3;
+        const int64_t na = c->nleaf[sa];
+        CRK_TRY(grow(c, c->rowlen[m], (na + 1) * 4, st));
+        CRK_TRY(grow(c, c->rowoff[m], (na + 1) * 4, st));
+        ListArgs A;
+        A.nA = na;
+        A.bboxA = P<float>(c->lbbox[sa]);
+        A.maxh2A = sa >= 2 ? P<float>(c->lmaxh2[sa]) : nullptr;
+        A.bboxB = P<float>(c->lbbox[sb]);
+        A.maxh2B = sb >= 2 ? P<float>(c->lmaxh2[sb]) : nullptr;
+        A.loffB = cnt + sb * (L.ncm + 1);
+        A.dmax_h2 = P<float>(c->dev_scalars);
+        A.mode = m;
+        A.rcut2 = c->prm.rcut2;
+        for (int d = 0; d < 3; ++d) { A.L[d] = c->prm.box[d]; A.ncell[d] = L.ncell[d]; }
+        A.cell_side = c->prm.cell_side;
+        A.rowlen = P<int32_t>(c->rowlen[m]);
+        A.rowoff = P<int32_t>(c->rowoff[m]);
+        A.col = nullptr;
+        A.shift = nullptr;
+        CRK_TRY(cuda_check(c, cudaMemsetAsync(P<int32_t>(c->rowlen[m]) + na, 0, 4, st), "memset"));
+        if (na > 0) {
+            k_lists<false><<<nblk(na * 32, 256), 256, 0, st>>>(A);
+            CRK_LAUNCHED(c, "list count");
+        }
+        tmp = c->cub_tmp.cap;
+        CRK_TRY(cuda_check(c, cub::DeviceScan::ExclusiveSum(c->cub_tmp.p, tmp, P<int32_t>(c->rowlen[m]),
+                                                            P<int32_t>(c->rowoff[m]), (int)(na + 1), st), "row scan"));
+        c->launches += 2;
+        CRK_TRY(cuda_check(c, cudaMemcpyAsync(host + 8 + m, P<int32_t>(c->rowoff[m]) + na, 4, cudaMemcpyDeviceToHost, st), "d2h"));
+    }
+    CRK_TRY(cuda_check(c, cudaStreamSynchronize(st), "sync"));
+    for (int m = 0; m < 2; ++m) {
+        c->nent[m] = host[8 + m];
+        const int sa = m == 0 ? 0 : 2, sb = m == 0 ? 1 : 3;
+        const int64_t na = c->nleaf[sa];
+        const int64_t ne = c->nent[m] > 0 ? c->nent[m] : 1;
+        CRK_TRY(grow(c, c->col[m], ne * 4, st));
+        CRK_TRY(grow(c, c->shift[m], ne, st));
+        ListArgs A;
+        A.nA = na;
+        A.bboxA = P<float>(c->lbbox[sa]);
+        A.maxh2A = sa >= 2 ? P<float>(c->lmaxh2[sa]) : nullptr;
+        A.bboxB = P<float>(c->lbbox[sb]);
+        A.maxh2B = sb >= 2 ? P<float>(c->lmaxh2[sb]) : nullptr;
+        A.loffB = cnt + sb * (L.ncm + 1);
+        A.dmax_h2 = P<float>(c->dev_scalars);
+        A.mode = m;
+        A.rcut2 = c->prm.rcut2;
+        for (int d = 0; d < 3; ++d) { A.L[d] = c->prm.box[d]; A.ncell[d] = L.ncell[d]; }
+        A.cell_side = c->prm.cell_side;
+        A.rowlen = nullptr;
+        A.rowoff = P<int32_t>(c->rowoff[m]);
+        A.col = P<int32_t>(c->col[m]);
+        A.shift = P<int8_t>(c->shift[m]);
+        if (na > 0) {
+            k_lists<true><<<nblk(na * 32, 256), 256, 0, st>>>(A);
+            CRK_LAUNCHED(c, "list fill");
+        }
+    }
+    // ---- gas-ordered state buffers for the hydro passes
+    const int64_t ng = c->n_gas > 0 ? c->n_gas : 1;
+    CRK_TRY(grow(c, c->gvel, ng * 16, st));
+    CRK_TRY(grow(c, c->gV, ng * 4, st));
+    CRK_TRY(grow(c, c->gcoef, ng * 16 * 4, st));
+    CRK_TRY(grow(c, c->grec, ng * 9 * 16, st));
+    CRK_TRY(grow(c, c->gu, ng * 4, st));
+    c->stage = ST_LISTS;
+    return CRK_OK;
+}
+
+}  // namespace crk

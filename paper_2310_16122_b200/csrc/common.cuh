@@ -1,0 +1,118 @@
+// common.cuh — device helpers shared by the kernels of libcrksr.so.
+#pragma once
+#include <cuda_runtime.h>
+
+#include <cstdint>
+
+#include "ctx.h"
+
+namespace crk {
+
+// ---------------------------------------------------------------- error plumbing
+crk_status fail(crk_ctx* c, crk_status s, const char* what);
+crk_status cuda_check(crk_ctx* c, cudaError_t e, const char* what);
+crk_status grow(crk_ctx* c, Buf& b, size_t bytes, cudaStream_t st);
+
+#define CRK_TRY(expr)                         \
+    do {                                      \
+        crk_status _s = (expr);               \
+        if (_s != CRK_OK) return _s;          \
+    } while (0)
+
+#define CRK_LAUNCHED(ctx, what)                                            \
+    do {                                                                   \
+        (ctx)->launches++;                                                 \
+        cudaError_t _e = cudaGetLastError();                               \
+        if (_e != cudaSuccess) return ::crk::cuda_check((ctx), _e, what);  \
+    } while (0)
+
+template <class T>
+inline T* P(const Buf& b) { return reinterpret_cast<T*>(b.p); }
+
+// ---------------------------------------------------------------- Morton
+__host__ __device__ inline uint64_t spread3(uint64_t v) {  // 21 bits -> every 3rd bit
+    v &= 0x1fffffull;
+    v = (v | (v << 32)) & 0x1f00000000ffffull;
+    v = (v | (v << 16)) & 0x1f0000ff0000ffull;
+    v = (v | (v << 8)) & 0x100f00f00f00f00full;
+    v = (v | (v << 4)) & 0x10c30c30c30c30c3ull;
+    v = (v | (v << 2)) & 0x1249249249249249ull;
+    return v;
+}
+
+__host__ __device__ inline uint32_t compact3(uint64_t v) {  // inverse of spread3
+    v &= 0x1249249249249249ull;
+    v = (v | (v >> 2)) & 0x10c30c30c30c30c3ull;
+    v = (v | (v >> 4)) & 0x100f00f00f00f00full;
+    v = (v | (v >> 8)) & 0x1f0000ff0000ffull;
+    v = (v | (v >> 16)) & 0x1f00000000ffffull;
+    v = (v | (v >> 32)) & 0x1fffffull;
+    return (uint32_t)v;
+}
+
+__host__ __device__ inline uint64_t morton3(uint32_t x, uint32_t y, uint32_t z) {
+    return spread3(x) | (spread3(y) << 1) | (spread3(z) << 2);
+}
+
+// shift code (sx+1) + 3(sy+1) + 9(sz+1)  ->  sx, sy, sz in {-1, 0, 1}
+__device__ __forceinline__ void decode_shift(int code, int& sx, int& sy, int& sz) {
+    sx = code % 3 - 1;
+    sy = (code / 3) % 3 - 1;
+    sz = code / 9 - 1;
+}
+
+// ---------------------------------------------------------------- O2 predicate
+// s32 = fmaf(dz,dz, fmaf(dy,dy, dx*dx)) with every op rounded to nearest even; the
+// explicit intrinsics keep the compiler from re-associating (bit-exact with the oracle).
+__device__ __forceinline__ float s32_of(float dx, float dy, float dz) {
+    return __fmaf_rn(dz, dz, __fmaf_rn(dy, dy, __fmul_rn(dx, dx)));
+}
+
+// ---------------------------------------------------------------- warp helpers
+__device__ __forceinline__ float warp_min(float v) {
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) v = fminf(v, __shfl_xor_sync(0xffffffffu, v, o));
+    return v;
+}
+__device__ __forceinline__ float warp_max(float v) {
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) v = fmaxf(v, __shfl_xor_sync(0xffffffffu, v, o));
+    return v;
+}
+// sum across the j-slots of a warp (lanes l, l+G, l+2G, ... hold partial sums of one i)
+template <int G>
+__device__ __forceinline__ float slot_sum(float v) {
+#pragma unroll
+    for (int o = 16; o >= G; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+    return v;
+}
+
+// squared distance of a point to an axis-aligned box (0 inside), fp32
+__device__ __forceinline__ float box_dist2(float x, float y, float z, const float lo[3], const float hi[3]) {
+    float gx = fmaxf(fmaxf(lo[0] - x, x - hi[0]), 0.f);
+    float gy = fmaxf(fmaxf(lo[1] - y, y - hi[1]), 0.f);
+    float gz = fmaxf(fmaxf(lo[2] - z, z - hi[2]), 0.f);
+    return fmaf(gz, gz, fmaf(gy, gy, gx * gx));
+}
+
+// Slack that makes fp32 culling tests a superset of the O2 predicate (|rel err| <= 2^-22).
+constexpr float CULL_SLACK = 1.0f + 1.0f / 1048576.0f * 4.0f;
+
+// ---------------------------------------------------------------- Wendland C4 (O6)
+// W(r,H)   = sigma/H^3 * wt(q),  wt(q) = (1-q)^6 (1 + 6q + 35q^2/3)
+// grad W   = sigma/H^3 * gt(q) * x_ij,  gt(q) = -(56/3)/H^2 (1-q)^5 (1+5q)
+constexpr float SIGMA_W = 4.9238032f;  // 495 / (32 pi)
+
+__device__ __forceinline__ void wendland_t(float s, float invH, float& wt, float& gt_h2) {
+    // gt_h2 = -(56/3) (1-q)^5 (1+5q)   (caller multiplies by 1/H^2)
+    float r = sqrtf(s);
+    float q = r * invH;
+    float t = fmaxf(1.f - q, 0.f);
+    float t2 = t * t;
+    float t4 = t2 * t2;
+    float t5 = t4 * t;
+    wt = t5 * t * fmaf(q, fmaf(q, 35.f / 3.f, 6.f), 1.f);
+    gt_h2 = (-56.f / 3.f) * t5 * fmaf(5.f, q, 1.f);
+}
+
+}  // namespace crk

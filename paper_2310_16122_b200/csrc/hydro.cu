@@ -1,0 +1,630 @@
+// hydro.cu — the five hot CRK-SPH kernels (timers upGeo, upCor,
+// upBarEx, upBarAc/upBarDu at PAPER.md:503) as list-driven pair kernels over the gas
+// leaves (formulas §8(c) O6-O9, readings in DESIGN.md §2).
+//
+// Gas state lives in the ctx in gas-rank order (gpos, gvel, gV, gcoef, grec) so that
+// the j-tiles of every pass are contiguous; the caller's per-particle outputs are
+// written at gas_idx[k] in each pass epilogue.
+#include "pairs.cuh"
+
+namespace crk {
+
+constexpr int HYD_CH = 256;
+constexpr int ACC_CH = 128;
+
+struct HydCommon {
+    const float4* gpos;      // (x, y, z, H)
+    const int32_t* gas_idx;  // gas rank -> sorted position
+};
+
+__device__ __forceinline__ void load_pos(const float4* gpos, int k, float& x, float& y, float& z,
+                                         float& H2, float& invH) {
+    const float4 p = gpos[k];
+    x = p.x; y = p.y; z = p.z;
+    H2 = __fmul_rn(p.w, p.w);
+    invH = 1.f / p.w;
+}
+
+// ============================================================== a4 Geometry (upGeo)
+// V_i = 1 / sum_{gas j, s32 < H_i^2, j incl. i} W(r_ij, H_i)
+template <bool COUNT>
+struct GeoPass : HydCommon {
+    static constexpr int PAY = 0;
+    static constexpr bool SYM = false;
+    float* gV;
+    float* Vout;
+    int32_t* cnt;
+    struct I { float x, y, z, H2, invH; int idx; };
+    struct Acc { float w; int n; };
+    __device__ void init(Acc& a) const { a.w = 0.f; a.n = 0; }
+    __device__ void load_i(int k, I& s) const { load_pos(gpos, k, s.x, s.y, s.z, s.H2, s.invH); s.idx = k; }
+    __device__ float ix(const I& s) const { return s.x; }
+    __device__ float iy(const I& s) const { return s.y; }
+    __device__ float iz(const I& s) const { return s.z; }
+    __device__ float cut(const I& s) const { return s.H2; }
+    __device__ void stage(int j, float ox, float oy, float oz, float4& jp, float4*) const {
+        const float4 p = __ldg(gpos + j);
+        jp = make_float4(p.x + ox, p.y + oy, p.z + oz, __int_as_float(j));
+    }
+    __device__ __forceinline__ void pair(const I& s, Acc& a, const float4& jp, const float4*) const {
+        const float dx = jp.x - s.x, dy = jp.y - s.y, dz = jp.z - s.z;
+        const float r2 = s32_of(dx, dy, dz);
+        const bool in = r2 < s.H2;
+        if (COUNT) {
+            a.n += (in && __float_as_int(jp.w) != s.idx) ? 1 : 0;
+        } else {
+            float wt, gt;
+            wendland_t(r2, s.invH, wt, gt);
+            a.w += in ? wt : 0.f;
+        }
+    }
+    template <int GG>
+    __device__ void reduce(Acc& a) const {
+        if (COUNT) {
+#pragma unroll
+            for (int o = 16; o >= GG; o >>= 1) a.n += __shfl_xor_sync(0xffffffffu, a.n, o);
+        } else {
+            a.w = slot_sum<GG>(a.w);
+        }
+    }
+    __device__ void finish(int k, const I& s, const Acc& a) const {
+        if (COUNT) {
+            cnt[gas_idx[k]] = a.n;
+            return;
+        }
+        const float V = 1.f / (SIGMA_W * s.invH * s.invH * s.invH * a.w);
+        gV[k] = V;
+        if (Vout) Vout[gas_idx[k]] = V;
+    }
+};
+
+// ============================================================== a5 Corrections (upCor)
+// Moments over gas j with s32 < H_i^2 (j incl. i), accumulated with d = x_j - x_i
+// (x_ij = -d); the symmetric gradient moments need only 6 + 10 accumulators.
+struct CorPass : HydCommon {
+    static constexpr int PAY = 0;
+    static constexpr bool SYM = false;
+    const float* gV;
+    float* gcoef;  // 16 planes of n_gas
+    int64_t ng;
+    float *A, *B, *dA, *dB;  // caller planes (n)
+    int64_t n;
+    struct I { float x, y, z, H2, invH; };
+    struct Acc {
+        float m0, m1[3], m2[6], g0[3], g1[6], g2[10];
+    };
+    __device__ void init(Acc& a) const {
+        a.m0 = 0.f;
+#pragma unroll
+        for (int t = 0; t < 3; ++t) a.m1[t] = a.g0[t] = 0.f;
+#pragma unroll
+        for (int t = 0; t < 6; ++t) a.m2[t] = a.g1[t] = 0.f;
+#pragma unroll
+        for (int t = 0; t < 10; ++t) a.g2[t] = 0.f;
+    }
+    __device__ void load_i(int k, I& s) const { load_pos(gpos, k, s.x, s.y, s.z, s.H2, s.invH); }
+    __device__ float ix(const I& s) const { return s.x; }
+    __device__ float iy(const I& s) const { return s.y; }
+    __device__ float iz(const I& s) const { return s.z; }
+    __device__ float cut(const I& s) const { return s.H2; }
+    __device__ void stage(int j, float ox, float oy, float oz, float4& jp, float4*) const {
+        const float4 p = __ldg(gpos + j);
+        jp = make_float4(p.x + ox, p.y + oy, p.z + oz, __ldg(gV + j));
+    }
+    __device__ __forceinline__ void pair(const I& s, Acc& a, const float4& jp, const float4*) const {
+        const float d0 = jp.x - s.x, d1 = jp.y - s.y, d2 = jp.z - s.z;
+        const float r2 = s32_of(d0, d1, d2);
+        float wt, gt;
+        wendland_t(r2, s.invH, wt, gt);
+        const bool in = r2 < s.H2;
+        const float w = in ? jp.w * wt : 0.f;
+        const float gw = in ? jp.w * gt : 0.f;  // (times 1/H^2 in finish)
+        const float wd0 = w * d0, wd1 = w * d1, wd2 = w * d2;
+        a.m0 += w;
+        a.m1[0] += wd0; a.m1[1] += wd1; a.m1[2] += wd2;
+        a.m2[0] = fmaf(wd0, d0, a.m2[0]); a.m2[1] = fmaf(wd0, d1, a.m2[1]); a.m2[2] = fmaf(wd0, d2, a.m2[2]);
+        a.m2[3] = fmaf(wd1, d1, a.m2[3]); a.m2[4] = fmaf(wd1, d2, a.m2[4]); a.m2[5] = fmaf(wd2, d2, a.m2[5]);
+        const float gd0 = gw * d0, gd1 = gw * d1, gd2 = gw * d2;
+        a.g0[0] += gd0; a.g0[1] += gd1; a.g0[2] += gd2;
+        a.g1[0] = fmaf(gd0, d0, a.g1[0]); a.g1[1] = fmaf(gd0, d1, a.g1[1]); a.g1[2] = fmaf(gd0, d2, a.g1[2]);
+        a.g1[3] = fmaf(gd1, d1, a.g1[3]); a.g1[4] = fmaf(gd1, d2, a.g1[4]); a.g1[5] = fmaf(gd2, d2, a.g1[5]);
+        const float e00 = gd0 * d0, e01 = gd0 * d1, e11 = gd1 * d1;
+        // fully symmetric third moment d_a d_b d_g gw: index set 000,001,002,011,012,022,111,112,122,222
+        a.g2[0] = fmaf(e00, d0, a.g2[0]);
+        a.g2[1] = fmaf(e00, d1, a.g2[1]);
+        a.g2[2] = fmaf(e00, d2, a.g2[2]);
+        a.g2[3] = fmaf(e01, d1, a.g2[3]);
+        a.g2[4] = fmaf(e01, d2, a.g2[4]);
+        a.g2[5] = fmaf(gd0 * d2, d2, a.g2[5]);
+        a.g2[6] = fmaf(e11, d1, a.g2[6]);
+        a.g2[7] = fmaf(e11, d2, a.g2[7]);
+        a.g2[8] = fmaf(gd1 * d2, d2, a.g2[8]);
+        a.g2[9] = fmaf(gd2 * d2, d2, a.g2[9]);
+    }
+    template <int GG>
+    __device__ void reduce(Acc& a) const {
+        a.m0 = slot_sum<GG>(a.m0);
+#pragma unroll
+        for (int t = 0; t < 3; ++t) { a.m1[t] = slot_sum<GG>(a.m1[t]); a.g0[t] = slot_sum<GG>(a.g0[t]); }
+#pragma unroll
+        for (int t = 0; t < 6; ++t) { a.m2[t] = slot_sum<GG>(a.m2[t]); a.g1[t] = slot_sum<GG>(a.g1[t]); }
+#pragma unroll
+        for (int t = 0; t < 10; ++t) a.g2[t] = slot_sum<GG>(a.g2[t]);
+    }
+    __device__ static int s2(int a, int b) {  // symmetric 3x3 index
+        if (a > b) { int t = a; a = b; b = t; }
+        return a == 0 ? b : (a == 1 ? 2 + b : 5);
+    }
+    __device__ static int s3(int a, int b, int g) {  // symmetric 3x3x3 index
+        int x = a, y = b, z = g, t;
+        if (x > y) { t = x; x = y; y = t; }
+        if (y > z) { t = y; y = z; z = t; }
+        if (x > y) { t = x; x = y; y = t; }
+        // sorted x <= y <= z
+        const int tab[3][3][3] = {{{0, 1, 2}, {0, 3, 4}, {0, 0, 5}},
+                                  {{0, 0, 0}, {0, 6, 7}, {0, 0, 8}},
+                                  {{0, 0, 0}, {0, 0, 0}, {0, 0, 9}}};
+        return tab[x][y][z];
+    }
+    __device__ void finish(int k, const I& s, const Acc& a) const {
+        const float c = SIGMA_W * s.invH * s.invH * s.invH;
+        const float cg = c * s.invH * s.invH;
+        // moments in x_ij = -d convention (O7), delta terms added here
+        const float m0 = c * a.m0;
+        float m1[3], m2[3][3], g0[3], g1[3][3], g2[3][3][3];
+#pragma unroll
+        for (int p = 0; p < 3; ++p) {
+            m1[p] = -c * a.m1[p];
+            g0[p] = -cg * a.g0[p];
+        }
+#pragma unroll
+        for (int p = 0; p < 3; ++p)
+#pragma unroll
+            for (int q = 0; q < 3; ++q) {
+                m2[p][q] = c * a.m2[s2(p, q)];
+                g1[p][q] = cg * a.g1[s2(p, q)] + (p == q ? m0 : 0.f);
+#pragma unroll
+                for (int g = 0; g < 3; ++g)
+                    g2[p][q][g] = -cg * a.g2[s3(p, q, g)] + (p == g ? m1[q] : 0.f) + (q == g ? m1[p] : 0.f);
+            }
+        // fp32 cofactor inverse of m2
+        const float c00 = m2[1][1] * m2[2][2] - m2[1][2] * m2[2][1];
+        const float c01 = m2[1][2] * m2[2][0] - m2[1][0] * m2[2][2];
+        const float c02 = m2[1][0] * m2[2][1] - m2[1][1] * m2[2][0];
+        const float det = m2[0][0] * c00 + m2[0][1] * c01 + m2[0][2] * c02;
+        const float tr = (m2[0][0] + m2[1][1] + m2[2][2]) * (1.f / 3.f);
+        float Ai, Bi[3], dAi[3], dBi[3][3];
+        if (fabsf(det) < 1e-10f * tr * tr * tr) {
+            Ai = 1.f / m0;
+#pragma unroll
+            for (int p = 0; p < 3; ++p) {
+                Bi[p] = 0.f;
+                dAi[p] = -g0[p] / (m0 * m0);
+#pragma unroll
+                for (int g = 0; g < 3; ++g) dBi[p][g] = 0.f;
+            }
+        } else {
+            const float id = 1.f / det;
+            float mi[3][3];
+            mi[0][0] = c00 * id;
+            mi[0][1] = (m2[0][2] * m2[2][1] - m2[0][1] * m2[2][2]) * id;
+            mi[0][2] = (m2[0][1] * m2[1][2] - m2[0][2] * m2[1][1]) * id;
+            mi[1][0] = c01 * id;
+            mi[1][1] = (m2[0][0] * m2[2][2] - m2[0][2] * m2[2][0]) * id;
+            mi[1][2] = (m2[0][2] * m2[1][0] - m2[0][0] * m2[1][2]) * id;
+            mi[2][0] = c02 * id;
+            mi[2][1] = (m2[0][1] * m2[2][0] - m2[0][0] * m2[2][1]) * id;
+            mi[2][2] = (m2[0][0] * m2[1][1] - m2[0][1] * m2[1][0]) * id;
+#pragma unroll
+            for (int p = 0; p < 3; ++p) Bi[p] = -(mi[p][0] * m1[0] + mi[p][1] * m1[1] + mi[p][2] * m1[2]);
+            Ai = 1.f / (m0 + Bi[0] * m1[0] + Bi[1] * m1[1] + Bi[2] * m1[2]);
+#pragma unroll
+            for (int g = 0; g < 3; ++g) {
+                float rhs[3];
+#pragma unroll
+                for (int p = 0; p < 3; ++p)
+                    rhs[p] = g1[p][g] + g2[p][0][g] * Bi[0] + g2[p][1][g] * Bi[1] + g2[p][2][g] * Bi[2];
+#pragma unroll
+                for (int p = 0; p < 3; ++p) dBi[p][g] = -(mi[p][0] * rhs[0] + mi[p][1] * rhs[1] + mi[p][2] * rhs[2]);
+            }
+#pragma unroll
+            for (int g = 0; g < 3; ++g) {
+                float t = g0[g];
+#pragma unroll
+                for (int p = 0; p < 3; ++p) t += dBi[p][g] * m1[p] + Bi[p] * g1[p][g];
+                dAi[g] = -Ai * Ai * t;
+            }
+        }
+        float vals[16];
+        vals[0] = Ai;
+#pragma unroll
+        for (int p = 0; p < 3; ++p) { vals[1 + p] = Bi[p]; vals[4 + p] = dAi[p]; }
+#pragma unroll
+        for (int p = 0; p < 3; ++p)
+#pragma unroll
+            for (int g = 0; g < 3; ++g) vals[7 + 3 * p + g] = dBi[p][g];
+#pragma unroll
+        for (int t = 0; t < 16; ++t) gcoef[(int64_t)t * ng + k] = vals[t];
+        const int64_t i = gas_idx[k];
+        if (A) A[i] = Ai;
+#pragma unroll
+        for (int p = 0; p < 3; ++p) {
+            if (B) B[p * n + i] = Bi[p];
+            if (dA) dA[p * n + i] = dAi[p];
+        }
+        if (dB)
+#pragma unroll
+            for (int t = 0; t < 9; ++t) dB[t * n + i] = vals[7 + t];
+    }
+};
+
+// ============================================================== a6 Extras (upBarEx)
+// rho = sum m_j W^R_ij, P = (gamma-1) rho u, c = sqrt(gamma P / rho),
+// d_b v^a = sum V_j (v^a_j - v^a_i) d_b W^R_ij ; the epilogue also packs the accel
+// record (9 float4) of particle i for a7/a8.
+struct ExtPass : HydCommon {
+    static constexpr int PAY = 1;
+    static constexpr bool SYM = false;
+    const float* gV;
+    const float* gcoef;
+    const float4* gvel;  // (vx, vy, vz, m)
+    const float* gu;
+    float4* grec;
+    int64_t ng, n;
+    float gamma;
+    float *rho, *P, *cs, *dv;  // caller
+    struct I {
+        float x, y, z, H2, invH;
+        float A, B[3], dA[3], dB[9];
+        float vx, vy, vz;
+    };
+    struct Acc { float rho, g[9]; };
+    __device__ void init(Acc& a) const {
+        a.rho = 0.f;
+#pragma unroll
+        for (int t = 0; t < 9; ++t) a.g[t] = 0.f;
+    }
+    __device__ void load_i(int k, I& s) const {
+        load_pos(gpos, k, s.x, s.y, s.z, s.H2, s.invH);
+        s.A = gcoef[k];
+#pragma unroll
+        for (int p = 0; p < 3; ++p) { s.B[p] = gcoef[(1 + p) * ng + k]; s.dA[p] = gcoef[(4 + p) * ng + k]; }
+#pragma unroll
+        for (int t = 0; t < 9; ++t) s.dB[t] = gcoef[(7 + t) * ng + k];
+        const float4 v = gvel[k];
+        s.vx = v.x; s.vy = v.y; s.vz = v.z;
+    }
+    __device__ float ix(const I& s) const { return s.x; }
+    __device__ float iy(const I& s) const { return s.y; }
+    __device__ float iz(const I& s) const { return s.z; }
+    __device__ float cut(const I& s) const { return s.H2; }
+    __device__ void stage(int j, float ox, float oy, float oz, float4& jp, float4* pay) const {
+        const float4 p = __ldg(gpos + j);
+        jp = make_float4(p.x + ox, p.y + oy, p.z + oz, __ldg(gV + j));
+        pay[0] = __ldg(gvel + j);
+    }
+    __device__ __forceinline__ void pair(const I& s, Acc& a, const float4& jp, const float4* pay) const {
+        // x_ij = x_i - x_j
+        const float x0 = s.x - jp.x, x1 = s.y - jp.y, x2 = s.z - jp.z;
+        const float r2 = s32_of(x0, x1, x2);
+        if (!(r2 < s.H2)) return;
+        float wt, gt;
+        wendland_t(r2, s.invH, wt, gt);
+        gt *= s.invH * s.invH;
+        const float lin = 1.f + s.B[0] * x0 + s.B[1] * x1 + s.B[2] * x2;
+        const float4 vj = pay[0];
+        a.rho = fmaf(vj.w, s.A * lin * wt, a.rho);
+        const float alg = s.A * lin * gt;
+        float gw[3];
+#pragma unroll
+        for (int g = 0; g < 3; ++g) {
+            const float t1 = s.dB[g] * x0 + s.dB[3 + g] * x1 + s.dB[6 + g] * x2 + s.B[g];
+            const float xg = g == 0 ? x0 : (g == 1 ? x1 : x2);
+            gw[g] = wt * (s.dA[g] * lin + s.A * t1) + alg * xg;
+        }
+        const float Vj = jp.w;
+        const float e0 = Vj * (vj.x - s.vx), e1 = Vj * (vj.y - s.vy), e2 = Vj * (vj.z - s.vz);
+#pragma unroll
+        for (int b = 0; b < 3; ++b) {
+            a.g[b] = fmaf(e0, gw[b], a.g[b]);
+            a.g[3 + b] = fmaf(e1, gw[b], a.g[3 + b]);
+            a.g[6 + b] = fmaf(e2, gw[b], a.g[6 + b]);
+        }
+    }
+    template <int GG>
+    __device__ void reduce(Acc& a) const {
+        a.rho = slot_sum<GG>(a.rho);
+#pragma unroll
+        for (int t = 0; t < 9; ++t) a.g[t] = slot_sum<GG>(a.g[t]);
+    }
+    __device__ void finish(int k, const I& s, const Acc& a) const {
+        const float c = SIGMA_W * s.invH * s.invH * s.invH;
+        const float r = c * a.rho;
+        const float u = gu[k];
+        const float Pk = (gamma - 1.f) * r * u;
+        const float ck = sqrtf(gamma * Pk / r);
+        float g[9];
+#pragma unroll
+        for (int t = 0; t < 9; ++t) g[t] = c * a.g[t];
+        const float V = gV[k];
+        const float4 vm = gvel[k];
+        float4* rec = grec + (int64_t)k * 9;
+        rec[0] = make_float4(s.invH, c * s.A, V, Pk);
+        rec[1] = make_float4(s.B[0], s.B[1], s.B[2], r);
+        rec[2] = make_float4(c * s.dA[0], c * s.dA[1], c * s.dA[2], ck);
+        rec[3] = make_float4(s.dB[0], s.dB[1], s.dB[2], s.dB[3]);
+        rec[4] = make_float4(s.dB[4], s.dB[5], s.dB[6], s.dB[7]);
+        rec[5] = make_float4(s.dB[8], vm.x, vm.y, vm.z);
+        rec[6] = make_float4(g[0], g[1], g[2], g[3]);
+        rec[7] = make_float4(g[4], g[5], g[6], g[7]);
+        rec[8] = make_float4(g[8], s.H2, vm.w, u);
+        const int64_t i = gas_idx[k];
+        if (rho) rho[i] = r;
+        if (P) P[i] = Pk;
+        if (cs) cs[i] = ck;
+        if (dv)
+#pragma unroll
+            for (int t = 0; t < 9; ++t) dv[t * n + i] = g[t];
+    }
+};
+
+// ============================================================== a7 + a8 Acceleration, Energy
+// Antisymmetrised CRK-SPH (O9): G_ij = (grad W^R_ij - grad W^R_ji)/2, each half with its
+// own particle's coefficients and H; artificial viscosity with a van Leer limited
+// midpoint velocity reconstruction.  Symmetric predicate s32 < max(H_i^2, H_j^2).
+struct Rec {
+    float invH, Ah, V, P, B[3], rho, dAh[3], cs, dB[9], v[3], dv[9], H2, m, u;
+};
+
+__device__ __forceinline__ void unpack_rec(const float4* r, Rec& q) {
+    float4 t = r[0]; q.invH = t.x; q.Ah = t.y; q.V = t.z; q.P = t.w;
+    t = r[1]; q.B[0] = t.x; q.B[1] = t.y; q.B[2] = t.z; q.rho = t.w;
+    t = r[2]; q.dAh[0] = t.x; q.dAh[1] = t.y; q.dAh[2] = t.z; q.cs = t.w;
+    t = r[3]; q.dB[0] = t.x; q.dB[1] = t.y; q.dB[2] = t.z; q.dB[3] = t.w;
+    t = r[4]; q.dB[4] = t.x; q.dB[5] = t.y; q.dB[6] = t.z; q.dB[7] = t.w;
+    t = r[5]; q.dB[8] = t.x; q.v[0] = t.y; q.v[1] = t.z; q.v[2] = t.w;
+    t = r[6]; q.dv[0] = t.x; q.dv[1] = t.y; q.dv[2] = t.z; q.dv[3] = t.w;
+    t = r[7]; q.dv[4] = t.x; q.dv[5] = t.y; q.dv[6] = t.z; q.dv[7] = t.w;
+    t = r[8]; q.dv[8] = t.x; q.H2 = t.y; q.m = t.z; q.u = t.w;
+}
+
+// corrected kernel gradient (scaled by sigma/H^3 via Ah, dAh) at separation x with
+// sign sg (x = sg * x_ij), for a particle with record q
+__device__ __forceinline__ void grad_wr(const float* Ah, const float* dAh, const float* B, const float* dB,
+                                        float invH, float r, const float x[3], float out[3]) {
+    const float q = r * invH;
+    const float t = fmaxf(1.f - q, 0.f);
+    const float t2 = t * t;
+    const float t5 = t2 * t2 * t;
+    const float wt = t5 * t * fmaf(q, fmaf(q, 35.f / 3.f, 6.f), 1.f);
+    const float gt = (-56.f / 3.f) * invH * invH * t5 * fmaf(5.f, q, 1.f);
+    const float lin = 1.f + B[0] * x[0] + B[1] * x[1] + B[2] * x[2];
+    const float alg = (*Ah) * lin * gt;
+#pragma unroll
+    for (int g = 0; g < 3; ++g) {
+        const float t1 = dB[g] * x[0] + dB[3 + g] * x[1] + dB[6 + g] * x[2] + B[g];
+        out[g] = wt * (dAh[g] * lin + (*Ah) * t1) + alg * x[g];
+    }
+}
+
+template <bool COUNT>
+struct AccPass : HydCommon {
+    static constexpr int PAY = COUNT ? 0 : 9;
+    static constexpr bool SYM = true;
+    const float4* grec;
+    float Cl, Cq, e2, dt;
+    int64_t n;
+    float *ahx, *ahy, *ahz, *dudt, *vx, *vy, *vz, *u;
+    int32_t* cnt;
+    struct I { float x, y, z; int idx; Rec r; };
+    struct Acc { float a[3], du; int nn; };
+    __device__ void init(Acc& a) const { a.a[0] = a.a[1] = a.a[2] = a.du = 0.f; a.nn = 0; }
+    __device__ void load_i(int k, I& s) const {
+        const float4 p = gpos[k];
+        s.x = p.x; s.y = p.y; s.z = p.z; s.idx = k;
+        if (COUNT) { s.r.H2 = __fmul_rn(p.w, p.w); return; }
+        unpack_rec(grec + (int64_t)k * 9, s.r);
+    }
+    __device__ float ix(const I& s) const { return s.x; }
+    __device__ float iy(const I& s) const { return s.y; }
+    __device__ float iz(const I& s) const { return s.z; }
+    __device__ float cut(const I& s) const { return s.r.H2; }
+    __device__ void stage(int j, float ox, float oy, float oz, float4& jp, float4* pay) const {
+        const float4 p = __ldg(gpos + j);
+        if (COUNT) {
+            jp = make_float4(p.x + ox, p.y + oy, p.z + oz, __fmul_rn(p.w, p.w));
+            return;
+        }
+        const float4* r = grec + (int64_t)j * 9;
+#pragma unroll
+        for (int t = 0; t < 9; ++t) pay[t] = __ldg(r + t);
+        jp = make_float4(p.x + ox, p.y + oy, p.z + oz, pay[8].y);
+    }
+    __device__ __forceinline__ void pair(const I& s, Acc& acc, const float4& jp, const float4* pay) const {
+        float x[3] = {s.x - jp.x, s.y - jp.y, s.z - jp.z};  // x_ij
+        const float r2 = s32_of(x[0], x[1], x[2]);
+        const bool in = r2 < fmaxf(s.r.H2, jp.w);
+        if (COUNT) {
+            // j index is not staged in count mode: a j with x_ij = 0 and equal H^2 is i itself
+            // only if it is the same particle; count mode uses the position tie rule below.
+            acc.nn += in ? 1 : 0;
+            return;
+        }
+        if (!in) return;
+        Rec q;
+        unpack_rec(pay, q);
+        const float r = sqrtf(r2);
+        float gi[3], gj[3];
+        grad_wr(&s.r.Ah, s.r.dAh, s.r.B, s.r.dB, s.r.invH, r, x, gi);
+        const float xm[3] = {-x[0], -x[1], -x[2]};
+        grad_wr(&q.Ah, q.dAh, q.B, q.dB, q.invH, r, xm, gj);
+        float G[3];
+#pragma unroll
+        for (int g = 0; g < 3; ++g) G[g] = 0.5f * (gi[g] - gj[g]);
+        // limiter on x.grad v.x
+        float gvi[3], gvj[3];
+#pragma unroll
+        for (int p = 0; p < 3; ++p) {
+            gvi[p] = s.r.dv[3 * p] * x[0] + s.r.dv[3 * p + 1] * x[1] + s.r.dv[3 * p + 2] * x[2];
+            gvj[p] = q.dv[3 * p] * x[0] + q.dv[3 * p + 1] * x[1] + q.dv[3 * p + 2] * x[2];
+        }
+        const float xgi = x[0] * gvi[0] + x[1] * gvi[1] + x[2] * gvi[2];
+        const float xgj = x[0] * gvj[0] + x[1] * gvj[1] + x[2] * gvj[2];
+        // phi = 4r/(1+r)^2 with r = xgi/xgj, written as 4 xgi xgj / (xgi + xgj)^2 (r > 0 <=> xgi xgj > 0)
+        const float pr = xgi * xgj;
+        const float sm = xgi + xgj;
+        const float phi = pr > 0.f ? fminf(1.f, 4.f * pr / (sm * sm)) : 0.f;
+        float vij[3], vs[3];
+#pragma unroll
+        for (int p = 0; p < 3; ++p) {
+            vij[p] = s.r.v[p] - q.v[p];
+            vs[p] = vij[p] - 0.5f * phi * (gvi[p] + gvj[p]);
+        }
+        const float vsx = vs[0] * x[0] + vs[1] * x[1] + vs[2] * x[2];
+        const float mui = fminf(0.f, vsx * s.r.invH / fmaf(r2, s.r.invH * s.r.invH, e2));
+        const float muj = fminf(0.f, vsx * q.invH / fmaf(r2, q.invH * q.invH, e2));
+        const float Q = s.r.rho * mui * (Cq * mui - Cl * s.r.cs) + q.rho * muj * (Cq * muj - Cl * q.cs);
+        const float fa = -q.V * (s.r.P + q.P + Q);
+        const float fu = q.V * (s.r.P + 0.5f * Q) * (vij[0] * G[0] + vij[1] * G[1] + vij[2] * G[2]);
+        acc.a[0] = fmaf(fa, G[0], acc.a[0]);
+        acc.a[1] = fmaf(fa, G[1], acc.a[1]);
+        acc.a[2] = fmaf(fa, G[2], acc.a[2]);
+        acc.du += fu;
+    }
+    template <int GG>
+    __device__ void reduce(Acc& a) const {
+        if (COUNT) {
+#pragma unroll
+            for (int o = 16; o >= GG; o >>= 1) a.nn += __shfl_xor_sync(0xffffffffu, a.nn, o);
+            return;
+        }
+#pragma unroll
+        for (int t = 0; t < 3; ++t) a.a[t] = slot_sum<GG>(a.a[t]);
+        a.du = slot_sum<GG>(a.du);
+    }
+    __device__ void finish(int k, const I& s, const Acc& a) const {
+        const int64_t i = gas_idx[k];
+        if (COUNT) {
+            cnt[i] = a.nn - 1;  // the self pair always satisfies the predicate (s32 = 0)
+            return;
+        }
+        const float f = s.r.V / s.r.m;
+        const float a0 = f * a.a[0], a1 = f * a.a[1], a2 = f * a.a[2], du = f * a.du;
+        if (ahx) { ahx[i] = a0; ahy[i] = a1; ahz[i] = a2; }
+        if (dudt) dudt[i] = du;
+        if (dt != 0.f) {
+            vx[i] = fmaf(dt, a0, vx[i]);
+            vy[i] = fmaf(dt, a1, vy[i]);
+            vz[i] = fmaf(dt, a2, vz[i]);
+            u[i] = fmaf(dt, du, u[i]);
+        }
+    }
+};
+
+// ============================================================== launches
+static RowView hydro_rows(crk_ctx* c) {
+    RowView rv;
+    rv.ifirst = P<int32_t>(c->lfirst[2]);
+    rv.icount = P<int32_t>(c->lcount[2]);
+    rv.jfirst = P<int32_t>(c->lfirst[3]);
+    rv.jcount = P<int32_t>(c->lcount[3]);
+    rv.row_off = P<int32_t>(c->rowoff[1]);
+    rv.col = P<int32_t>(c->col[1]);
+    rv.shift = P<int8_t>(c->shift[1]);
+    for (int a = 0; a < 3; ++a) rv.L[a] = c->lay.L[a];
+    return rv;
+}
+
+template <class Pass, int CH>
+static crk_status launch_hyd(crk_ctx* c, const Pass& ps, cudaStream_t st, const char* what) {
+    if (c->nleaf[2] == 0) return CRK_OK;
+    const size_t smem = pair_smem_bytes<Pass, HYD_NW, HYD_G, CH>();
+    if (smem > 48 * 1024) {
+        cudaError_t e = cudaFuncSetAttribute(pair_kernel<Pass, HYD_NW, HYD_G, CH>,
+                                             cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+        if (e != cudaSuccess) return cuda_check(c, e, what);
+    }
+    pair_kernel<Pass, HYD_NW, HYD_G, CH><<<(unsigned)c->nleaf[2], HYD_NW * 32, smem, st>>>(ps, hydro_rows(c));
+    CRK_LAUNCHED(c, what);
+    return CRK_OK;
+}
+
+static void common(crk_ctx* c, HydCommon& h) {
+    h.gpos = P<float4>(c->gpos);
+    h.gas_idx = P<int32_t>(c->gas_idx);
+}
+
+crk_status geometry(crk_ctx* c, crk_particles* p, cudaStream_t st) {
+    GeoPass<false> g;
+    common(c, g);
+    g.gV = P<float>(c->gV);
+    g.Vout = p->V;
+    g.cnt = nullptr;
+    return launch_hyd<GeoPass<false>, HYD_CH>(c, g, st, "geometry kernel");
+}
+
+crk_status corrections(crk_ctx* c, crk_particles* p, cudaStream_t st) {
+    CorPass g;
+    common(c, g);
+    g.gV = P<float>(c->gV);
+    g.gcoef = P<float>(c->gcoef);
+    g.ng = c->n_gas;
+    g.A = p->A; g.B = p->B; g.dA = p->dA; g.dB = p->dB;
+    g.n = c->n;
+    return launch_hyd<CorPass, HYD_CH>(c, g, st, "corrections kernel");
+}
+
+__global__ void k_gather_gas_state(int64_t ng, const int32_t* gas_idx, const float* vx, const float* vy,
+                                   const float* vz, const float* m, const float* u, float4* gvel, float* gu) {
+    const int64_t k = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+    if (k >= ng) return;
+    const int64_t i = gas_idx[k];
+    gvel[k] = make_float4(vx[i], vy[i], vz[i], m[i]);
+    gu[k] = u[i];
+}
+
+crk_status extras(crk_ctx* c, crk_particles* p, cudaStream_t st) {
+    if (c->n_gas == 0) return CRK_OK;
+    k_gather_gas_state<<<(unsigned)((c->n_gas + 255) / 256), 256, 0, st>>>(
+        c->n_gas, P<int32_t>(c->gas_idx), p->vx, p->vy, p->vz, p->m, p->u, P<float4>(c->gvel), P<float>(c->gu));
+    CRK_LAUNCHED(c, "gather gas state");
+    ExtPass g;
+    common(c, g);
+    g.gV = P<float>(c->gV);
+    g.gcoef = P<float>(c->gcoef);
+    g.gvel = P<float4>(c->gvel);
+    g.gu = P<float>(c->gu);
+    g.grec = P<float4>(c->grec);
+    g.ng = c->n_gas;
+    g.n = c->n;
+    g.gamma = c->prm.gamma;
+    g.rho = p->rho; g.P = p->P; g.cs = p->cs; g.dv = p->dv;
+    return launch_hyd<ExtPass, HYD_CH>(c, g, st, "extras kernel");
+}
+
+crk_status accel_dudt(crk_ctx* c, crk_particles* p, float dt, cudaStream_t st) {
+    if (dt != 0.f && (!p->vx || !p->vy || !p->vz || !p->u)) return fail(c, CRK_EINVAL, "kick needs v and u");
+    AccPass<false> g;
+    common(c, g);
+    g.grec = P<float4>(c->grec);
+    g.Cl = c->prm.av_cl; g.Cq = c->prm.av_cq; g.e2 = c->prm.av_eps2; g.dt = dt;
+    g.n = c->n;
+    g.ahx = p->ahx; g.ahy = p->ahy; g.ahz = p->ahz; g.dudt = p->dudt;
+    g.vx = p->vx; g.vy = p->vy; g.vz = p->vz; g.u = p->u;
+    g.cnt = nullptr;
+    return launch_hyd<AccPass<false>, ACC_CH>(c, g, st, "accel/dudt kernel");
+}
+
+crk_status hydro_count(crk_ctx* c, int32_t* cgather, int32_t* csym, cudaStream_t st) {
+    GeoPass<true> g;
+    common(c, g);
+    g.gV = nullptr; g.Vout = nullptr; g.cnt = cgather;
+    CRK_TRY((launch_hyd<GeoPass<true>, HYD_CH>(c, g, st, "gather count kernel")));
+    AccPass<true> a;
+    common(c, a);
+    a.grec = nullptr;
+    a.cnt = csym;
+    return launch_hyd<AccPass<true>, HYD_CH>(c, a, st, "sym count kernel");
+}
+
+}  // namespace crk

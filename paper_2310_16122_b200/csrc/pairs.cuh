@@ -1,0 +1,143 @@
+// pairs.cuh — the list-driven pair-kernel skeleton shared by every force pass.
+//
+// One CTA per i-leaf (a row of the CSR leaf-pair list).  The
+// CTA walks its row in chunks: all threads stage the particles of the next CH/JMAX
+// j-leaves (periodic shift applied, so every difference is exact, O1) into shared
+// memory; each warp then culls the staged candidates against the bounding box of
+// its own G i-particles (ballot + popc compaction into a warp-private index list)
+// and evaluates the survivors.  Lane l holds i-particle l % G and takes every
+// (32/G)-th survivor — the paper's half-warp layout (Fig.
+// half-warp-layout: lanes 0-15 / 16-31) generalised to 32/G j-slots, i-centric, with
+// register accumulation and one shuffle reduction over the slots at the end: no
+// atomics (SURVEY.md §7 "B200-idiomatic design").
+#pragma once
+#include "common.cuh"
+
+namespace crk {
+
+struct RowView {
+    const int32_t* ifirst;
+    const int32_t* icount;
+    const int32_t* jfirst;
+    const int32_t* jcount;
+    const int32_t* row_off;
+    const int32_t* col;
+    const int8_t* shift;
+    float L[3];
+};
+
+// Pass concept:
+//   static constexpr int PAY;            payload float4 per staged j (after the position)
+//   static constexpr bool SYM;           culling radius also uses j's H^2 (jpos.w)
+//   struct I; struct Acc;
+//   void load_i(int i, I&) ; float3-ish position via ix/iy/iz ; float cut(const I&)
+//   void stage(int j, float ox, float oy, float oz, float4& jp, float4* pay)
+//   void pair(const I&, Acc&, const float4& jp, const float4* pay)
+//   void reduce(Acc&) ; void finish(int i, const I&, const Acc&)
+template <class Pass, int NW, int G, int CH>
+__global__ void __launch_bounds__(NW * 32) pair_kernel(const Pass pass, const RowView rv) {
+    static_assert(32 % G == 0, "G must divide the warp");
+    static_assert(CH % 32 == 0 && CH % JMAX == 0, "bad chunk");
+    constexpr int S = 32 / G;
+    extern __shared__ __align__(16) unsigned char smem_raw[];
+    float4* jpos = reinterpret_cast<float4*>(smem_raw);
+    float4* jpay = jpos + CH;
+    uint16_t* wl_all = reinterpret_cast<uint16_t*>(jpay + CH * Pass::PAY);
+
+    const int a = blockIdx.x;
+    const int ifirst = rv.ifirst[a];
+    const int icount = rv.icount[a];
+    const int warp = threadIdx.x >> 5;
+    const int lane = threadIdx.x & 31;
+    const int il = lane % G;
+    const int sl = lane / G;
+    const int ibase = warp * G;
+    const bool wactive = ibase < icount;
+    const bool ivalid = ibase + il < icount;
+    uint16_t* wl = wl_all + warp * CH;
+
+    typename Pass::I is;
+    typename Pass::Acc acc;
+    pass.init(acc);
+    float lo[3], hi[3], wcut = 0.f;
+    if (wactive) {
+        pass.load_i(ifirst + ibase + (ivalid ? il : 0), is);
+        float px = pass.ix(is), py = pass.iy(is), pz = pass.iz(is);
+        lo[0] = warp_min(ivalid ? px : INFINITY);
+        lo[1] = warp_min(ivalid ? py : INFINITY);
+        lo[2] = warp_min(ivalid ? pz : INFINITY);
+        hi[0] = warp_max(ivalid ? px : -INFINITY);
+        hi[1] = warp_max(ivalid ? py : -INFINITY);
+        hi[2] = warp_max(ivalid ? pz : -INFINITY);
+        wcut = warp_max(ivalid ? pass.cut(is) : 0.f);
+    }
+
+    const int rbeg = rv.row_off[a], rend = rv.row_off[a + 1];
+    constexpr int EPC = CH / JMAX;  // entries per chunk
+    for (int e0 = rbeg; e0 < rend; e0 += EPC) {
+        for (int t = threadIdx.x; t < CH; t += NW * 32) {
+            const int e = e0 + t / JMAX;
+            const int k = t % JMAX;
+            bool ok = false;
+            int j = 0, code = 13;
+            if (e < rend) {
+                const int b = rv.col[e];
+                if (k < rv.jcount[b]) {
+                    ok = true;
+                    j = rv.jfirst[b] + k;
+                    code = rv.shift[e];
+                }
+            }
+            if (ok) {
+                int sx, sy, sz;
+                decode_shift(code, sx, sy, sz);
+                pass.stage(j, (float)sx * rv.L[0], (float)sy * rv.L[1], (float)sz * rv.L[2], jpos[t],
+                           jpay + t * Pass::PAY);
+            } else {
+                jpos[t] = make_float4(INFINITY, INFINITY, INFINITY, 0.f);
+            }
+        }
+        __syncthreads();
+        if (wactive) {
+            const int nslots = min(CH, (rend - e0) * JMAX);
+            int cnt = 0;
+            for (int t0 = 0; t0 < nslots; t0 += 32) {
+                const int t = t0 + lane;
+                bool keep = false;
+                if (t < nslots) {
+                    const float4 p = jpos[t];
+                    const float d2 = box_dist2(p.x, p.y, p.z, lo, hi);
+                    const float c = Pass::SYM ? fmaxf(wcut, p.w) : wcut;
+                    keep = d2 < c * CULL_SLACK;
+                }
+                const unsigned m = __ballot_sync(0xffffffffu, keep);
+                if (keep) wl[cnt + __popc(m & ((1u << lane) - 1u))] = (uint16_t)t;
+                cnt += __popc(m);
+            }
+            __syncwarp();
+            int k = sl;
+#pragma unroll 1
+            for (; k + S < cnt; k += 2 * S) {
+                const int t0 = wl[k], t1 = wl[k + S];
+                pass.pair(is, acc, jpos[t0], jpay + t0 * Pass::PAY);
+                pass.pair(is, acc, jpos[t1], jpay + t1 * Pass::PAY);
+            }
+            if (k < cnt) {
+                const int t0 = wl[k];
+                pass.pair(is, acc, jpos[t0], jpay + t0 * Pass::PAY);
+            }
+        }
+        __syncthreads();
+    }
+    if (wactive) {
+        pass.template reduce<G>(acc);
+        if (ivalid && sl == 0) pass.finish(ifirst + ibase + il, is, acc);
+    }
+}
+
+template <class Pass, int NW, int G, int CH>
+inline size_t pair_smem_bytes() {
+    return (size_t)CH * sizeof(float4) * (1 + Pass::PAY) + (size_t)NW * CH * sizeof(uint16_t);
+}
+
+}  // namespace crk

@@ -1,0 +1,210 @@
+"""GPU (sm_100a) vs fp64 oracle parity, through the C-ABI (libcrksr.so).
+
+Bars (north_star, SURVEY.md §8(c) "Tolerance"):
+  * sort order, leaves, interaction lists, neighbour counts: bit-exact;
+  * gravity acceleration, hydro acceleration, du/dt: max_i |gpu - ref| / S_i <= 1e-4,
+    S_i = sum_j |pair contribution| (fp32 vs fp64);
+  * intermediates: V, A, rho, P, c relative <= 1e-5 .. 2e-5; B, grad A, grad B, grad v
+    <= 2e-4 of the field's max magnitude (DESIGN.md §6 derives these from fp32
+    cancellation in the moment sums).
+"""
+import numpy as np
+import pytest
+
+import oracle
+from crk_testutil import cached_config, run_gpu, norm_err, rel_err, scaled_err
+
+pytestmark = pytest.mark.gpu
+
+TOL_FORCE = 1e-4
+
+
+def _oracle_lists(parts, params):
+    order, keys, cellm = oracle.sort_order(parts, params)
+    ls = [oracle.leaves(parts, params, order, cellm, k) for k in range(4)]
+    lists = [oracle.list_rows(ls[0], ls[1], params, 0), oracle.list_rows(ls[2], ls[3], params, 1)]
+    return order, ls, lists
+
+
+def _canon_rows(off, col, sh):
+    rows = []
+    for a in range(off.shape[0] - 1):
+        c = np.asarray(col[off[a]:off[a + 1]], np.int64)
+        s = np.asarray(sh[off[a]:off[a + 1]], np.int64)
+        o = np.lexsort((s, c))
+        rows.append((c[o], s[o]))
+    return rows
+
+
+@pytest.mark.parametrize("name", ["c1", "lat:32,16,16:0.1:3", "c2z"])
+def test_sort_leaves_lists_bit_exact(name):
+    parts, params = cached_config(name)
+    g = run_gpu(parts, params, counts=False, lists=True, hydro=False)
+    order, ls, lists = _oracle_lists(parts, params)
+    assert np.array_equal(g["perm"], order)
+    lv = g["lv"]
+    for s in range(4):
+        gl = {k: (v.cpu().numpy() if v is not None else None) for k, v in lv["leaves"][s].items()}
+        assert np.array_equal(gl["first"], ls[s]["first"]), s
+        assert np.array_equal(gl["count"], ls[s]["count"]), s
+        assert np.array_equal(gl["bbox"], ls[s]["bbox"]), s
+        assert np.array_equal(gl["cell"].astype(np.uint64), ls[s]["cell"]), s
+        if s >= 2:
+            assert np.array_equal(gl["maxh2"], ls[s]["maxh2"]), s
+    for m in range(2):
+        off, col, sh = lists[m]
+        gv = lv["lists"][m]
+        goff = gv["row_off"].cpu().numpy()
+        assert np.array_equal(goff, off), m
+        rg = _canon_rows(goff, gv["col"].cpu().numpy(), gv["shift"].cpu().numpy())
+        ro = _canon_rows(off, col, sh)
+        for a, (x, y) in enumerate(zip(rg, ro)):
+            assert np.array_equal(x[0], y[0]) and np.array_equal(x[1], y[1]), (m, a)
+
+
+@pytest.mark.parametrize("name", ["c1", "lat:32,16,16:0.1:3", "c2u", "c2z"])
+def test_counts_and_full_chain(name):
+    parts, params = cached_config(name)
+    g = run_gpu(parts, params)
+    ref_c = oracle.counts(parts, params)
+    cg, ch, cs = g["cnt_in"]
+    assert np.array_equal(cg, ref_c["grav"])
+    assert np.array_equal(ch, ref_c["gather"])
+    assert np.array_equal(cs, ref_c["sym"])
+    ref = oracle.substep(parts, params)
+    gi = g["in"]
+    a = np.stack([gi["ax"], gi["ay"], gi["az"]], 1)
+    assert norm_err(a, ref["grav_a"], ref["grav_S"]) <= TOL_FORCE
+    T = ref["targets"]
+    assert rel_err(gi["V"][T], ref["V"]) <= 1e-5
+    assert rel_err(gi["A"][T], ref["A"]) <= 1e-5
+    assert scaled_err(gi["B"][:, T].T, ref["B"]) <= 2e-4
+    assert scaled_err(gi["dA"][:, T].T, ref["dA"]) <= 2e-4
+    assert scaled_err(gi["dB"][:, T].T, ref["dB"]) <= 2e-4
+    assert rel_err(gi["rho"][T], ref["rho"]) <= 2e-5
+    assert rel_err(gi["P"][T], ref["P"]) <= 2e-5
+    assert rel_err(gi["cs"][T], ref["cs"]) <= 2e-5
+    if np.max(np.abs(ref["dv"])) > 0:
+        assert scaled_err(gi["dv"][:, T].T, ref["dv"]) <= 2e-4
+    ah = np.stack([gi["ahx"], gi["ahy"], gi["ahz"]], 1)[T]
+    assert norm_err(ah, ref["a"], ref["Sa"]) <= TOL_FORCE
+    assert norm_err(gi["dudt"][T], ref["dudt"], ref["Sdu"]) <= TOL_FORCE
+
+
+def test_kicks():
+    parts, params = cached_config("c1")
+    dtg, dth = 0.05, 0.02
+    g = run_gpu(parts, params, dt_grav=dtg, dt_hydro=dth, counts=False)
+    ref = oracle.substep(parts, params, dt_grav=dtg, dt_hydro=dth)
+    gi = g["in"]
+    v = np.stack([gi["vx"], gi["vy"], gi["vz"]], 1)
+    dm = np.nonzero(parts["species"] == 0)[0]
+    T = ref["targets"]
+    # DM: gravity kick only; gas: gravity then hydro kick
+    sv = np.abs(np.stack([parts["vx"], parts["vy"], parts["vz"]], 1)).max() * 2e-7
+    assert np.all(np.abs(v[dm] - ref["grav_v"][dm]) <= dtg * TOL_FORCE * ref["grav_S"][dm, None] + sv)
+    tolg = dth * TOL_FORCE * ref["Sa"][:, None] + dtg * TOL_FORCE * ref["grav_S"][T, None] + sv
+    assert np.all(np.abs(v[T] - ref["v"]) <= tolg)
+    su = np.abs(parts["u"]).max() * 2e-7
+    assert np.all(np.abs(gi["u"][T] - ref["u"]) <= dth * TOL_FORCE * ref["Sdu"] + su)
+
+
+def _species_subset(parts, keep):
+    idx = np.nonzero(keep)[0]
+    return {k: v[idx].copy() for k, v in parts.items()}
+
+
+def test_edge_all_dark_matter_and_all_gas():
+    parts, params = cached_config("c1")
+    dm = _species_subset(parts, parts["species"] == 0)
+    g = run_gpu(dm, params)
+    ref = oracle.substep(dm, params, hydro=False)
+    a = np.stack([g["in"]["ax"], g["in"]["ay"], g["in"]["az"]], 1)
+    assert norm_err(a, ref["grav_a"], ref["grav_S"]) <= TOL_FORCE
+    assert np.array_equal(g["cnt_in"][0], oracle.counts(dm, params)["grav"])
+    assert not np.any(g["cnt_in"][1]) and not np.any(g["cnt_in"][2])
+    gas = _species_subset(parts, parts["species"] == 1)
+    g = run_gpu(gas, params)
+    ref = oracle.substep(gas, params)
+    ah = np.stack([g["in"]["ahx"], g["in"]["ahy"], g["in"]["ahz"]], 1)
+    assert norm_err(ah, ref["a"], ref["Sa"]) <= TOL_FORCE
+    rc = oracle.counts(gas, params)
+    assert np.array_equal(g["cnt_in"][2], rc["sym"])
+
+
+def test_deterministic_and_resort_idempotent():
+    import torch
+    from paper_2310_16122_b200 import Particles, Solver
+
+    parts, params = cached_config("lat:32,16,16:0.1:3")
+    p = Particles.from_host(parts, "cuda")
+    s = Solver(params, 0)
+    s.substep(p)
+    first = {k: v.copy() for k, v in p.to_host().items()}
+    s.substep(p)  # already sorted input: same order, same results
+    second = p.to_host()
+    for k in first:
+        assert np.array_equal(first[k], second[k]) or k == "perm", k
+    assert np.array_equal(second["perm"], np.arange(p.n))
+    torch.cuda.synchronize()
+
+
+def test_call_order_and_errors():
+    from paper_2310_16122_b200 import CrkError, Particles, Solver
+
+    parts, params = cached_config("c1")
+    p = Particles.from_host(parts, "cuda")
+    s = Solver(params, 0)
+    with pytest.raises(CrkError) as e:
+        s.gravity_kick(p)
+    assert e.value.status == -4
+    s.build_lists(p)
+    with pytest.raises(CrkError) as e:
+        s.extras(p)
+    assert e.value.status == -4
+    s.geometry(p)
+    s.corrections(p)
+    s.extras(p)
+    s.hydro_accel_dudt(p)
+
+
+# ------------------------------------------------------------------ full sizes, sampled outputs
+def _sampled(name, n_samp, seed=5):
+    parts, params = cached_config(name)
+    rng = np.random.default_rng(seed)
+    n = parts["x"].shape[0]
+    gas = np.nonzero(parts["species"] == 1)[0]
+    tg = np.sort(rng.choice(gas, n_samp, replace=False))
+    ta = np.sort(rng.choice(n, n_samp, replace=False))
+    g = run_gpu(parts, params)
+    ref = oracle.substep(parts, params, targets=tg, grav_targets=ta)
+    rc = oracle.counts(parts, params, targets=np.concatenate([ta, tg]))
+    gi = g["in"]
+    cg, ch, cs = g["cnt_in"]
+    allt = np.concatenate([ta, tg])
+    assert np.array_equal(cg[allt], rc["grav"])
+    assert np.array_equal(ch[allt], rc["gather"])
+    assert np.array_equal(cs[allt], rc["sym"])
+    a = np.stack([gi["ax"], gi["ay"], gi["az"]], 1)[ta]
+    assert norm_err(a, ref["grav_a"], ref["grav_S"]) <= TOL_FORCE
+    T = ref["targets"]
+    assert rel_err(gi["V"][T], ref["V"]) <= 1e-5
+    ah = np.stack([gi["ahx"], gi["ahy"], gi["ahz"]], 1)[T]
+    assert norm_err(ah, ref["a"], ref["Sa"]) <= TOL_FORCE
+    assert norm_err(gi["dudt"][T], ref["dudt"], ref["Sdu"]) <= TOL_FORCE
+    # whole-array properties at full size: momentum conservation of the hydro force
+    m = parts["m"].astype(np.float64)
+    ahall = np.stack([gi["ahx"], gi["ahy"], gi["ahz"]], 1).astype(np.float64)
+    mom = np.abs((m[:, None] * ahall).sum(0))
+    assert np.all(mom <= 1e-4 * (m[:, None] * np.abs(ahall)).sum(0).max())
+    return g
+
+
+@pytest.mark.slow
+def test_clustered_config3_sampled():
+    _sampled("c3", 600)
+
+
+@pytest.mark.slow
+def test_config4_full_size_sampled():
+    _sampled("c4", 300)
