@@ -101,7 +101,7 @@ constexpr float CULL_SLACK = 1.0f + 1.0f / 1048576.0f * 4.0f;
 // ---------------------------------------------------------------- Wendland C4 (O6)
 // W(r,H)   = sigma/H^3 * wt(q),  wt(q) = (1-q)^6 (1 + 6q + 35q^2/3)
 // grad W   = sigma/H^3 * gt(q) * x_ij,  gt(q) = -(56/3)/H^2 (1-q)^5 (1+5q)
-constexpr float SIGMA_W = 4.9238032f;  // 495 / (32 pi)
+constexpr float SIGMA_W = 4.92385626f;  // 495 / (32 pi), fp32-rounded
 
 __device__ __forceinline__ void wendland_t(float s, float invH, float& wt, float& gt_h2) {
     // gt_h2 = -(56/3) (1-q)^5 (1+5q)   (caller multiplies by 1/H^2)

@@ -89,3 +89,10 @@ def scaled_err(gpu, ref):
     g = np.asarray(gpu, np.float64)
     r = np.asarray(ref, np.float64)
     return float(np.max(np.abs(g - r)) / max(np.max(np.abs(r)), 1e-300))
+
+
+def dimless_err(gpu, ref, scale):
+    """max |gpu - ref| * scale (scale makes the field dimensionless, e.g. H for B)."""
+    g = np.asarray(gpu, np.float64)
+    r = np.asarray(ref, np.float64)
+    return float(np.max(np.abs(g - r) * np.asarray(scale, np.float64)))
