@@ -92,7 +92,7 @@ static int layout_of(const orc_params* p, key_layout* k) {
     }
     k->cbits = 0;
     while ((1 << k->cbits) < maxn) ++k->cbits;
-    k->fbits = (64 - 3 * k->cbits) / 3;
+    k->fbits = (32 - 3 * k->cbits) / 3; /* the key fits 32 bits */
     if (k->fbits > k->cs) k->fbits = k->cs;
     return 0;
 }

@@ -82,7 +82,7 @@ static crk_status validate(const crk_params* p, Layout& L, std::string& why) {
     if (maxn > 256) { why = "at most 256 cells per axis (raise cell_side)"; return CRK_EINVAL; }
     L.cbits = 0;
     while ((1 << L.cbits) < maxn) ++L.cbits;
-    L.fbits = (64 - 3 * L.cbits) / 3;
+    L.fbits = (32 - 3 * L.cbits) / 3;  // 32-bit sort keys (DESIGN.md §2 O3)
     if (L.fbits > L.cs) L.fbits = L.cs;
     L.ncm = (int64_t)1 << (3 * L.cbits);
     return CRK_OK;

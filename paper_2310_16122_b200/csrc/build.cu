@@ -13,8 +13,9 @@
 namespace crk {
 
 // ---------------------------------------------------------------- keys
+// 32-bit key = Morton(cell) << 3 fbits | Morton(top fbits of the in-cell coordinate) (O3)
 __global__ void k_keys(int64_t n, const float* __restrict__ x, const float* __restrict__ y,
-                       const float* __restrict__ z, float inv_q, int cs, int fbits, uint64_t* keys,
+                       const float* __restrict__ z, float inv_q, int cs, int fbits, uint32_t* keys,
                        int32_t* idx) {
     const int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
     if (i >= n) return;
@@ -22,12 +23,12 @@ __global__ void k_keys(int64_t n, const float* __restrict__ x, const float* __re
     const uint32_t msk = (1u << cs) - 1u, sh = cs - fbits;
     const uint64_t cm = morton3(xi >> cs, yi >> cs, zi >> cs);
     const uint64_t fm = morton3((xi & msk) >> sh, (yi & msk) >> sh, (zi & msk) >> sh);
-    keys[i] = (cm << (3 * fbits)) | fm;
+    keys[i] = (uint32_t)((cm << (3 * fbits)) | fm);
     idx[i] = (int32_t)i;
 }
 
 // Runs of equal keys (coincident to 1/2^fbits of a cell) are ordered by id: total order (O3).
-__global__ void k_tie_fix(int64_t n, const uint64_t* __restrict__ keys, int32_t* idx, const int64_t* __restrict__ id) {
+__global__ void k_tie_fix(int64_t n, const uint32_t* __restrict__ keys, int32_t* idx, const int64_t* __restrict__ id) {
     const int64_t k = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
     if (k + 1 >= n) return;
     if (keys[k] != keys[k + 1]) return;
@@ -46,47 +47,66 @@ __global__ void k_tie_fix(int64_t n, const uint64_t* __restrict__ keys, int32_t*
     }
 }
 
-// ---------------------------------------------------------------- permute
-__global__ void k_gather_f32(int64_t n, const int32_t* __restrict__ perm, const float* __restrict__ in, float* out) {
-    const int64_t k = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
-    if (k < n) out[k] = in[perm[k]];
-}
-__global__ void k_gather_u8(int64_t n, const int32_t* __restrict__ perm, const uint8_t* __restrict__ in, uint8_t* out) {
-    const int64_t k = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
-    if (k < n) out[k] = in[perm[k]];
-}
-__global__ void k_gather_i64(int64_t n, const int32_t* __restrict__ perm, const int64_t* __restrict__ in, int64_t* out) {
-    const int64_t k = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
-    if (k < n) out[k] = in[perm[k]];
-}
+// ---------------------------------------------------------------- permute (one gather pass)
+struct SoA {
+    float* f[9];       // x y z vx vy vz m H u
+    uint8_t* sp;
+    int64_t* id;
+};
 
-// after the permute: packed (x,y,z,m), gas flags, cell runs
-__global__ void k_post_sort(int64_t n, const uint64_t* __restrict__ keys, int fbits, const float* __restrict__ x,
-                            const float* __restrict__ y, const float* __restrict__ z, const float* __restrict__ m,
-                            const uint8_t* __restrict__ sp, float4* xm, int32_t* gflag, int32_t* cstart,
-                            int32_t* cend) {
+__global__ void k_gather_all(int64_t n, const int32_t* __restrict__ perm, SoA in, SoA out) {
     const int64_t k = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
     if (k >= n) return;
-    xm[k] = make_float4(x[k], y[k], z[k], m[k]);
-    gflag[k] = sp[k] == 1 ? 1 : 0;
-    const uint64_t c = keys[k] >> (3 * fbits);
+    const int32_t s = perm[k];
+#pragma unroll
+    for (int t = 0; t < 9; ++t) out.f[t][k] = __ldg(in.f[t] + s);
+    out.sp[k] = __ldg(in.sp + s);
+    out.id[k] = __ldg(in.id + s);
+}
+
+// copy the sorted scratch back to the caller's arrays and derive xm, gas flags, cell runs
+__global__ void k_scatter_back(int64_t n, SoA tmp, SoA dst, const uint32_t* __restrict__ keys, int fbits, float4* xm,
+                               int32_t* gflag, int32_t* cstart, int32_t* cend) {
+    const int64_t k = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+    if (k >= n) return;
+    float v[9];
+#pragma unroll
+    for (int t = 0; t < 9; ++t) {
+        v[t] = tmp.f[t][k];
+        dst.f[t][k] = v[t];
+    }
+    const uint8_t s = tmp.sp[k];
+    dst.sp[k] = s;
+    dst.id[k] = tmp.id[k];
+    xm[k] = make_float4(v[0], v[1], v[2], v[6]);
+    gflag[k] = s == 1 ? 1 : 0;
+    const uint32_t c = keys[k] >> (3 * fbits);
     if (k == 0 || (keys[k - 1] >> (3 * fbits)) != c) cstart[c] = (int32_t)k;
     if (k == n - 1 || (keys[k + 1] >> (3 * fbits)) != c) cend[c] = (int32_t)(k + 1);
 }
 
 __global__ void k_gas_pack(int64_t n, const int32_t* __restrict__ gflag, const int32_t* __restrict__ grank,
-                           const float* __restrict__ x, const float* __restrict__ y, const float* __restrict__ z,
-                           const float* __restrict__ H, int32_t* gas_idx, float4* gpos, float* dmax_h2) {
+                           const float4* __restrict__ xm, const float* __restrict__ H, int32_t* gas_idx, float4* gpos,
+                           float* dmax_h2) {
+    __shared__ float wmax[32];
     const int64_t k = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
     float h2 = 0.f;
     if (k < n && gflag[k]) {
         const int32_t g = grank[k];
         gas_idx[g] = (int32_t)k;
-        gpos[g] = make_float4(x[k], y[k], z[k], H[k]);
-        h2 = __fmul_rn(H[k], H[k]);
+        const float4 p = xm[k];
+        const float h = H[k];
+        gpos[g] = make_float4(p.x, p.y, p.z, h);
+        h2 = __fmul_rn(h, h);
     }
     h2 = warp_max(h2);
-    if ((threadIdx.x & 31) == 0 && h2 > 0.f) atomicMax(reinterpret_cast<int*>(dmax_h2), __float_as_int(h2));
+    if ((threadIdx.x & 31) == 0) wmax[threadIdx.x >> 5] = h2;
+    __syncthreads();
+    if (threadIdx.x < 32) {
+        h2 = threadIdx.x < (blockDim.x >> 5) ? wmax[threadIdx.x] : 0.f;
+        h2 = warp_max(h2);
+        if (threadIdx.x == 0 && h2 > 0.f) atomicMax(reinterpret_cast<int*>(dmax_h2), __float_as_int(h2));
+    }
 }
 
 // ---------------------------------------------------------------- leaves (O3)
@@ -187,7 +207,10 @@ struct ListArgs {
     int mode;              // 0 gravity (rcut2), 1 hydro (max of the two leaves' max H^2)
     float rcut2;
     double L[3];
+    float Lf[3];
     double cell_side;
+    float inv_q;
+    double q2inv_slack;    // (1 + 2^-20) / q^2, exact
     int ncell[3];
     int32_t* rowlen;       // pass 1
     const int32_t* rowoff; // pass 2
@@ -195,11 +218,20 @@ struct ListArgs {
     int8_t* shift;
 };
 
-// one warp per i-leaf; candidate j-leaves come from the cells within reach of the i-bbox
+constexpr int LIST_WARPS = 8;
+
+// One warp per i-leaf.  Fast path (the usual case): the candidate cells around the
+// i-bbox do not wrap onto themselves, so each cell's periodic shift is known from the
+// wrap; cells whose box is out of reach are pruned; the j-leaves of the surviving
+// cells are flattened across the lanes (warp scan) and tested with the exact integer
+// form of O4 (gaps are multiples of q below 2^24 q).  Tiny boxes use the generic path
+// with the per-axis shift search.
 template <bool FILL>
-__global__ void k_lists(ListArgs A) {
+__global__ void __launch_bounds__(LIST_WARPS * 32) k_lists(ListArgs A) {
+    __shared__ int32_t s_b0[LIST_WARPS][32], s_ex[LIST_WARPS][32], s_code[LIST_WARPS][32];
     const int64_t a = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5;
     const int lane = threadIdx.x & 31;
+    const int w = threadIdx.x >> 5;
     if (a >= A.nA) return;
     const float* ba = A.bboxA + 6 * a;
     const double slack = 1.0 + 0x1p-20;
@@ -208,46 +240,156 @@ __global__ void k_lists(ListArgs A) {
     else reach2 = fmax((double)A.maxh2A[a], (double)*A.dmax_h2);
     const double reach = sqrt(reach2 * slack) * (1.0 + 1e-12) + 1e-12;
     int c0[3], c1[3];
+    bool generic = false;
 #pragma unroll
     for (int d = 0; d < 3; ++d) {
         c0[d] = (int)floor(((double)ba[d] - reach) / A.cell_side);
         c1[d] = (int)floor(((double)ba[3 + d] + reach) / A.cell_side);
-        if (c1[d] - c0[d] + 1 >= A.ncell[d]) { c0[d] = 0; c1[d] = A.ncell[d] - 1; }
+        if (c1[d] - c0[d] + 1 >= A.ncell[d]) { c0[d] = 0; c1[d] = A.ncell[d] - 1; generic = true; }
     }
     int outpos = FILL ? A.rowoff[a] : 0;
     int total = 0;
-    for (int cz = c0[2]; cz <= c1[2]; ++cz)
-        for (int cy = c0[1]; cy <= c1[1]; ++cy)
-            for (int cx = c0[0]; cx <= c1[0]; ++cx) {
-                const uint32_t wx = (uint32_t)((cx % A.ncell[0] + A.ncell[0]) % A.ncell[0]);
-                const uint32_t wy = (uint32_t)((cy % A.ncell[1] + A.ncell[1]) % A.ncell[1]);
-                const uint32_t wz = (uint32_t)((cz % A.ncell[2] + A.ncell[2]) % A.ncell[2]);
-                const uint64_t m = morton3(wx, wy, wz);
-                const int b0 = A.loffB[m], b1 = A.loffB[m + 1];
-                for (int bb = b0; bb < b1; bb += 32) {
-                    const int b = bb + lane;
-                    bool keep = false;
-                    int code = 13;
-                    if (b < b1) {
-                        const double cut2 = A.mode == 0 ? (double)A.rcut2
-                                                        : fmax((double)A.maxh2A[a], (double)A.maxh2B[b]);
-                        keep = leaf_pair_test(ba, A.bboxB + 6 * (int64_t)b, A.L, cut2 * slack, code);
-                    }
-                    const unsigned msk = __ballot_sync(0xffffffffu, keep);
-                    if (FILL && keep) {
-                        const int p = outpos + __popc(msk & ((1u << lane) - 1u));
-                        A.col[p] = b;
-                        A.shift[p] = (int8_t)code;
-                    }
-                    outpos += __popc(msk);
-                    total += __popc(msk);
+    const float mh2a = A.mode == 1 ? A.maxh2A[a] : 0.f;
+    if (!generic) {
+        const int nx = c1[0] - c0[0] + 1, ny = c1[1] - c0[1] + 1, nz = c1[2] - c0[2] + 1;
+        const int ncand = nx * ny * nz;
+        const double cs = A.cell_side;
+        for (int cb = 0; cb < ncand; cb += 32) {
+            const int t = cb + lane;
+            int nb = 0, b0 = 0, code = 13;
+            if (t < ncand) {
+                const int ix = t % nx, iy = (t / nx) % ny, iz = t / (nx * ny);
+                const int cc[3] = {c0[0] + ix, c0[1] + iy, c0[2] + iz};
+                double d2c = 0.0;
+                int wc[3], sc[3];
+#pragma unroll
+                for (int d = 0; d < 3; ++d) {
+                    const double lo = cc[d] * cs, hi = lo + cs;
+                    const double g = fmax(0.0, fmax(lo - (double)ba[3 + d], (double)ba[d] - hi));
+                    d2c += g * g;
+                    wc[d] = cc[d] < 0 ? cc[d] + A.ncell[d] : (cc[d] >= A.ncell[d] ? cc[d] - A.ncell[d] : cc[d]);
+                    sc[d] = cc[d] < 0 ? -1 : (cc[d] >= A.ncell[d] ? 1 : 0);
+                }
+                if (d2c < reach2 * slack) {
+                    const uint64_t m = morton3((uint32_t)wc[0], (uint32_t)wc[1], (uint32_t)wc[2]);
+                    b0 = A.loffB[m];
+                    nb = A.loffB[m + 1] - b0;
+                    code = (sc[0] + 1) + 3 * (sc[1] + 1) + 9 * (sc[2] + 1);
                 }
             }
+            int pre = nb;  // inclusive warp scan
+#pragma unroll
+            for (int o = 1; o < 32; o <<= 1) {
+                const int v = __shfl_up_sync(0xffffffffu, pre, o);
+                if (lane >= o) pre += v;
+            }
+            const int tot = __shfl_sync(0xffffffffu, pre, 31);
+            s_b0[w][lane] = b0;
+            s_ex[w][lane] = pre - nb;
+            s_code[w][lane] = code;
+            __syncwarp();
+            for (int u0 = 0; u0 < tot; u0 += 32) {
+                const int u = u0 + lane;
+                bool keep = false;
+                int b = 0, cd = 13;
+                if (u < tot) {
+                    int lo = 0, hi = 31;
+#pragma unroll
+                    for (int it = 0; it < 5; ++it) {
+                        const int mid = (lo + hi + 1) >> 1;
+                        if (s_ex[w][mid] <= u) lo = mid; else hi = mid - 1;
+                    }
+                    b = s_b0[w][lo] + (u - s_ex[w][lo]);
+                    cd = s_code[w][lo];
+                    const float* bb = A.bboxB + 6 * (int64_t)b;
+                    int sx, sy, sz;
+                    decode_shift(cd, sx, sy, sz);
+                    const float sL[3] = {(float)sx * A.Lf[0], (float)sy * A.Lf[1], (float)sz * A.Lf[2]};
+                    uint64_t K = 0;
+#pragma unroll
+                    for (int d = 0; d < 3; ++d) {
+                        const float g1 = (bb[d] + sL[d]) - ba[3 + d];   // exact (O1)
+                        const float g2 = ba[d] - (bb[3 + d] + sL[d]);
+                        const float g = fmaxf(0.f, fmaxf(g1, g2));
+                        const uint32_t k = (uint32_t)(g * A.inv_q);     // exact integer < 2^24
+                        K += (uint64_t)k * k;
+                    }
+                    const float cut2 = A.mode == 0 ? A.rcut2 : fmaxf(mh2a, A.maxh2B[b]);
+                    keep = (double)K < (double)cut2 * A.q2inv_slack;
+                }
+                const unsigned msk = __ballot_sync(0xffffffffu, keep);
+                if (FILL && keep) {
+                    const int p = outpos + __popc(msk & ((1u << lane) - 1u));
+                    A.col[p] = b;
+                    A.shift[p] = (int8_t)cd;
+                }
+                outpos += __popc(msk);
+                total += __popc(msk);
+            }
+            __syncwarp();
+        }
+    } else {
+        for (int cz = c0[2]; cz <= c1[2]; ++cz)
+            for (int cy = c0[1]; cy <= c1[1]; ++cy)
+                for (int cx = c0[0]; cx <= c1[0]; ++cx) {
+                    const uint32_t wx = (uint32_t)((cx % A.ncell[0] + A.ncell[0]) % A.ncell[0]);
+                    const uint32_t wy = (uint32_t)((cy % A.ncell[1] + A.ncell[1]) % A.ncell[1]);
+                    const uint32_t wz = (uint32_t)((cz % A.ncell[2] + A.ncell[2]) % A.ncell[2]);
+                    const uint64_t m = morton3(wx, wy, wz);
+                    const int b0 = A.loffB[m], b1 = A.loffB[m + 1];
+                    for (int bb = b0; bb < b1; bb += 32) {
+                        const int b = bb + lane;
+                        bool keep = false;
+                        int code = 13;
+                        if (b < b1) {
+                            const double cut2 = A.mode == 0 ? (double)A.rcut2
+                                                            : fmax((double)mh2a, (double)A.maxh2B[b]);
+                            keep = leaf_pair_test(ba, A.bboxB + 6 * (int64_t)b, A.L, cut2 * slack, code);
+                        }
+                        const unsigned msk = __ballot_sync(0xffffffffu, keep);
+                        if (FILL && keep) {
+                            const int p = outpos + __popc(msk & ((1u << lane) - 1u));
+                            A.col[p] = b;
+                            A.shift[p] = (int8_t)code;
+                        }
+                        outpos += __popc(msk);
+                        total += __popc(msk);
+                    }
+                }
+    }
     if (!FILL && lane == 0) A.rowlen[a] = total;
 }
 
 // ---------------------------------------------------------------- driver
 static inline unsigned nblk(int64_t n, int b) { return (unsigned)((n + b - 1) / b); }
+
+static ListArgs list_args(crk_ctx* c, int m) {
+    const Layout& L = c->lay;
+    const int sa = m == 0 ? 0 : 2, sb = m == 0 ? 1 : 3;
+    ListArgs A;
+    A.nA = c->nleaf[sa];
+    A.bboxA = P<float>(c->lbbox[sa]);
+    A.maxh2A = sa >= 2 ? P<float>(c->lmaxh2[sa]) : nullptr;
+    A.bboxB = P<float>(c->lbbox[sb]);
+    A.maxh2B = sb >= 2 ? P<float>(c->lmaxh2[sb]) : nullptr;
+    A.loffB = P<int32_t>(c->leaf_cnt) + sb * (L.ncm + 1);
+    A.dmax_h2 = P<float>(c->dev_scalars);
+    A.mode = m;
+    A.rcut2 = c->prm.rcut2;
+    for (int d = 0; d < 3; ++d) {
+        A.L[d] = c->prm.box[d];
+        A.Lf[d] = (float)c->prm.box[d];
+        A.ncell[d] = L.ncell[d];
+    }
+    A.cell_side = c->prm.cell_side;
+    A.inv_q = L.inv_q;
+    A.q2inv_slack = (1.0 + 0x1p-20) / (L.q * L.q);
+    A.rowlen = P<int32_t>(c->rowlen[m]);
+    A.rowoff = P<int32_t>(c->rowoff[m]);
+    A.col = P<int32_t>(c->col[m]);
+    A.shift = P<int8_t>(c->shift[m]);
+    return A;
+}
 
 crk_status build_lists(crk_ctx* c, crk_particles* p, cudaStream_t st) {
     const int64_t n = p->n;
@@ -256,11 +398,11 @@ crk_status build_lists(crk_ctx* c, crk_particles* p, cudaStream_t st) {
     c->stage = ST_NONE;
     const int bits = 3 * (L.cbits + L.fbits);
     // ---- buffers
-    CRK_TRY(grow(c, c->keys_a, n * 8, st));
-    CRK_TRY(grow(c, c->keys_b, n * 8, st));
+    CRK_TRY(grow(c, c->keys_a, n * 4, st));
+    CRK_TRY(grow(c, c->keys_b, n * 4, st));
     CRK_TRY(grow(c, c->idx_a, n * 4, st));
     CRK_TRY(grow(c, c->idx_b, n * 4, st));
-    CRK_TRY(grow(c, c->scratch, n * 8, st));
+    CRK_TRY(grow(c, c->scratch, n * 48 + 64, st));
     CRK_TRY(grow(c, c->xm, n * 16, st));
     CRK_TRY(grow(c, c->gflag, (n + 1) * 4, st));
     CRK_TRY(grow(c, c->grank, (n + 1) * 4, st));
@@ -268,13 +410,15 @@ crk_status build_lists(crk_ctx* c, crk_particles* p, cudaStream_t st) {
     CRK_TRY(grow(c, c->cell_end, L.ncm * 4, st));
     CRK_TRY(grow(c, c->leaf_cnt, 4 * (L.ncm + 1) * 4, st));
     CRK_TRY(grow(c, c->dev_scalars, 64, st));
+    CRK_TRY(grow(c, c->gas_idx, n * 4, st));
+    CRK_TRY(grow(c, c->gpos, n * 16, st));
     if (n == 0) return fail(c, CRK_EINVAL, "no particles");
 
-    // ---- keys + sort
-    k_keys<<<nblk(n, 256), 256, 0, st>>>(n, p->x, p->y, p->z, L.inv_q, L.cs, L.fbits, P<uint64_t>(c->keys_a),
+    // ---- keys + sort (32-bit keys, 3 (cbits + fbits) significant bits)
+    k_keys<<<nblk(n, 256), 256, 0, st>>>(n, p->x, p->y, p->z, L.inv_q, L.cs, L.fbits, P<uint32_t>(c->keys_a),
                                          P<int32_t>(c->idx_a));
     CRK_LAUNCHED(c, "keys");
-    cub::DoubleBuffer<uint64_t> dk(P<uint64_t>(c->keys_a), P<uint64_t>(c->keys_b));
+    cub::DoubleBuffer<uint32_t> dk(P<uint32_t>(c->keys_a), P<uint32_t>(c->keys_b));
     cub::DoubleBuffer<int32_t> dv(P<int32_t>(c->idx_a), P<int32_t>(c->idx_b));
     size_t tmp = 0;
     cub::DeviceRadixSort::SortPairs(nullptr, tmp, dk, dv, (int)n, 0, bits, st);
@@ -288,45 +432,40 @@ crk_status build_lists(crk_ctx* c, crk_particles* p, cudaStream_t st) {
     CRK_TRY(grow(c, c->cub_tmp, need, st));
     tmp = c->cub_tmp.cap;
     CRK_TRY(cuda_check(c, cub::DeviceRadixSort::SortPairs(c->cub_tmp.p, tmp, dk, dv, (int)n, 0, bits, st), "radix sort"));
-    c->launches += 4;  // onesweep: histogram + per-pass kernels (counted approximately)
-    const uint64_t* keys = dk.Current();
+    c->launches += 2 + (bits + 7) / 8;  // histogram, scan, one onesweep pass per 8 bits
+    const uint32_t* keys = dk.Current();
     int32_t* perm = dv.Current();
     k_tie_fix<<<nblk(n, 256), 256, 0, st>>>(n, keys, perm, p->id);
     CRK_LAUNCHED(c, "tie fix");
 
-    // ---- permute caller arrays in place (gather into scratch, copy back)
+    // ---- permute the caller's arrays in place: one gather pass into scratch, one pass back
+    SoA in, tmpS;
     float* f32[9] = {p->x, p->y, p->z, p->vx, p->vy, p->vz, p->m, p->H, p->u};
-    for (int t = 0; t < 9; ++t) {
-        k_gather_f32<<<nblk(n, 256), 256, 0, st>>>(n, perm, f32[t], P<float>(c->scratch));
-        CRK_LAUNCHED(c, "permute");
-        CRK_TRY(cuda_check(c, cudaMemcpyAsync(f32[t], c->scratch.p, n * 4, cudaMemcpyDeviceToDevice, st), "copy"));
-    }
-    k_gather_u8<<<nblk(n, 256), 256, 0, st>>>(n, perm, p->species, P<uint8_t>(c->scratch));
-    CRK_LAUNCHED(c, "permute");
-    CRK_TRY(cuda_check(c, cudaMemcpyAsync(p->species, c->scratch.p, n, cudaMemcpyDeviceToDevice, st), "copy"));
-    k_gather_i64<<<nblk(n, 256), 256, 0, st>>>(n, perm, p->id, P<int64_t>(c->scratch));
-    CRK_LAUNCHED(c, "permute");
-    CRK_TRY(cuda_check(c, cudaMemcpyAsync(p->id, c->scratch.p, n * 8, cudaMemcpyDeviceToDevice, st), "copy"));
+    for (int t = 0; t < 9; ++t) in.f[t] = f32[t];
+    in.sp = p->species;
+    in.id = p->id;
+    char* sbase = reinterpret_cast<char*>(c->scratch.p);
+    tmpS.id = reinterpret_cast<int64_t*>(sbase);
+    for (int t = 0; t < 9; ++t) tmpS.f[t] = reinterpret_cast<float*>(sbase + n * 8 + (int64_t)t * n * 4);
+    tmpS.sp = reinterpret_cast<uint8_t*>(sbase + n * 44);
+    k_gather_all<<<nblk(n, 256), 256, 0, st>>>(n, perm, in, tmpS);
+    CRK_LAUNCHED(c, "permute gather");
     if (p->perm)
         CRK_TRY(cuda_check(c, cudaMemcpyAsync(p->perm, perm, n * 4, cudaMemcpyDeviceToDevice, st), "copy"));
-
-    // ---- cells, gas ranks
     CRK_TRY(cuda_check(c, cudaMemsetAsync(c->cell_start.p, 0, L.ncm * 4, st), "memset"));
     CRK_TRY(cuda_check(c, cudaMemsetAsync(c->cell_end.p, 0, L.ncm * 4, st), "memset"));
     CRK_TRY(cuda_check(c, cudaMemsetAsync(P<int32_t>(c->gflag) + n, 0, 4, st), "memset"));
     CRK_TRY(cuda_check(c, cudaMemsetAsync(c->dev_scalars.p, 0, 64, st), "memset"));
-    k_post_sort<<<nblk(n, 256), 256, 0, st>>>(n, keys, L.fbits, p->x, p->y, p->z, p->m, p->species,
-                                              P<float4>(c->xm), P<int32_t>(c->gflag), P<int32_t>(c->cell_start),
-                                              P<int32_t>(c->cell_end));
-    CRK_LAUNCHED(c, "post sort");
+    k_scatter_back<<<nblk(n, 256), 256, 0, st>>>(n, tmpS, in, keys, L.fbits, P<float4>(c->xm), P<int32_t>(c->gflag),
+                                                 P<int32_t>(c->cell_start), P<int32_t>(c->cell_end));
+    CRK_LAUNCHED(c, "permute back");
+
+    // ---- gas ranks
     tmp = c->cub_tmp.cap;
     CRK_TRY(cuda_check(c, cub::DeviceScan::ExclusiveSum(c->cub_tmp.p, tmp, P<int32_t>(c->gflag), P<int32_t>(c->grank),
                                                         (int)(n + 1), st), "gas scan"));
     c->launches += 2;
-    // n_gas: needed for buffer sizes -> read back with the leaf totals below; use n as bound
-    CRK_TRY(grow(c, c->gas_idx, n * 4, st));
-    CRK_TRY(grow(c, c->gpos, n * 16, st));
-    k_gas_pack<<<nblk(n, 256), 256, 0, st>>>(n, P<int32_t>(c->gflag), P<int32_t>(c->grank), p->x, p->y, p->z, p->H,
+    k_gas_pack<<<nblk(n, 256), 256, 0, st>>>(n, P<int32_t>(c->gflag), P<int32_t>(c->grank), P<float4>(c->xm), p->H,
                                              P<int32_t>(c->gas_idx), P<float4>(c->gpos), P<float>(c->dev_scalars));
     CRK_LAUNCHED(c, "gas pack");
 
@@ -373,29 +512,13 @@ crk_status build_lists(crk_ctx* c, crk_particles* p, cudaStream_t st) {
 
     // ---- lists: count, scan, fill
     for (int m = 0; m < 2; ++m) {
-        const int sa = m == 0 ? 0 : 2, sb = m == 0 ? 1 : 3;
-        const int64_t na = c->nleaf[sa];
+        const int64_t na = c->nleaf[m == 0 ? 0 : 2];
         CRK_TRY(grow(c, c->rowlen[m], (na + 1) * 4, st));
         CRK_TRY(grow(c, c->rowoff[m], (na + 1) * 4, st));
-        ListArgs A;
-        A.nA = na;
-        A.bboxA = P<float>(c->lbbox[sa]);
-        A.maxh2A = sa >= 2 ? P<float>(c->lmaxh2[sa]) : nullptr;
-        A.bboxB = P<float>(c->lbbox[sb]);
-        A.maxh2B = sb >= 2 ? P<float>(c->lmaxh2[sb]) : nullptr;
-        A.loffB = cnt + sb * (L.ncm + 1);
-        A.dmax_h2 = P<float>(c->dev_scalars);
-        A.mode = m;
-        A.rcut2 = c->prm.rcut2;
-        for (int d = 0; d < 3; ++d) { A.L[d] = c->prm.box[d]; A.ncell[d] = L.ncell[d]; }
-        A.cell_side = c->prm.cell_side;
-        A.rowlen = P<int32_t>(c->rowlen[m]);
-        A.rowoff = P<int32_t>(c->rowoff[m]);
-        A.col = nullptr;
-        A.shift = nullptr;
+        ListArgs A = list_args(c, m);
         CRK_TRY(cuda_check(c, cudaMemsetAsync(P<int32_t>(c->rowlen[m]) + na, 0, 4, st), "memset"));
         if (na > 0) {
-            k_lists<false><<<nblk(na * 32, 256), 256, 0, st>>>(A);
+            k_lists<false><<<nblk(na * 32, LIST_WARPS * 32), LIST_WARPS * 32, 0, st>>>(A);
             CRK_LAUNCHED(c, "list count");
         }
         tmp = c->cub_tmp.cap;
@@ -407,29 +530,13 @@ crk_status build_lists(crk_ctx* c, crk_particles* p, cudaStream_t st) {
     CRK_TRY(cuda_check(c, cudaStreamSynchronize(st), "sync"));
     for (int m = 0; m < 2; ++m) {
         c->nent[m] = host[8 + m];
-        const int sa = m == 0 ? 0 : 2, sb = m == 0 ? 1 : 3;
-        const int64_t na = c->nleaf[sa];
+        const int64_t na = c->nleaf[m == 0 ? 0 : 2];
         const int64_t ne = c->nent[m] > 0 ? c->nent[m] : 1;
         CRK_TRY(grow(c, c->col[m], ne * 4, st));
         CRK_TRY(grow(c, c->shift[m], ne, st));
-        ListArgs A;
-        A.nA = na;
-        A.bboxA = P<float>(c->lbbox[sa]);
-        A.maxh2A = sa >= 2 ? P<float>(c->lmaxh2[sa]) : nullptr;
-        A.bboxB = P<float>(c->lbbox[sb]);
-        A.maxh2B = sb >= 2 ? P<float>(c->lmaxh2[sb]) : nullptr;
-        A.loffB = cnt + sb * (L.ncm + 1);
-        A.dmax_h2 = P<float>(c->dev_scalars);
-        A.mode = m;
-        A.rcut2 = c->prm.rcut2;
-        for (int d = 0; d < 3; ++d) { A.L[d] = c->prm.box[d]; A.ncell[d] = L.ncell[d]; }
-        A.cell_side = c->prm.cell_side;
-        A.rowlen = nullptr;
-        A.rowoff = P<int32_t>(c->rowoff[m]);
-        A.col = P<int32_t>(c->col[m]);
-        A.shift = P<int8_t>(c->shift[m]);
+        ListArgs A = list_args(c, m);
         if (na > 0) {
-            k_lists<true><<<nblk(na * 32, 256), 256, 0, st>>>(A);
+            k_lists<true><<<nblk(na * 32, LIST_WARPS * 32), LIST_WARPS * 32, 0, st>>>(A);
             CRK_LAUNCHED(c, "list fill");
         }
     }

@@ -101,9 +101,8 @@ static crk_status launch_grav(crk_ctx* c, crk_particles* p, float dt, int32_t* c
     rv.shift = P<int8_t>(c->shift[0]);
     for (int a = 0; a < 3; ++a) rv.L[a] = c->lay.L[a];
     if (c->nleaf[0] == 0) return CRK_OK;
-    const size_t smem = pair_smem_bytes<GravPass<COUNT>, GRAV_NW, GRAV_G, GRAV_CH>();
-    pair_kernel<GravPass<COUNT>, GRAV_NW, GRAV_G, GRAV_CH>
-        <<<(unsigned)c->nleaf[0], GRAV_NW * 32, smem, st>>>(g, rv);
+    pair_kernel<GravPass<COUNT>, GRAV_NW, GRAV_G, GRAV_CH, 1>
+        <<<(unsigned)c->nleaf[0], GRAV_NW * 32, 0, st>>>(g, rv);
     CRK_LAUNCHED(c, "gravity kernel");
     return CRK_OK;
 }

@@ -535,16 +535,10 @@ static RowView hydro_rows(crk_ctx* c) {
     return rv;
 }
 
-template <class Pass, int CH>
+template <class Pass, int CH, int MINB = 1>
 static crk_status launch_hyd(crk_ctx* c, const Pass& ps, cudaStream_t st, const char* what) {
     if (c->nleaf[2] == 0) return CRK_OK;
-    const size_t smem = pair_smem_bytes<Pass, HYD_NW, HYD_G, CH>();
-    if (smem > 48 * 1024) {
-        cudaError_t e = cudaFuncSetAttribute(pair_kernel<Pass, HYD_NW, HYD_G, CH>,
-                                             cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-        if (e != cudaSuccess) return cuda_check(c, e, what);
-    }
-    pair_kernel<Pass, HYD_NW, HYD_G, CH><<<(unsigned)c->nleaf[2], HYD_NW * 32, smem, st>>>(ps, hydro_rows(c));
+    pair_kernel<Pass, HYD_NW, HYD_G, CH, MINB><<<(unsigned)c->nleaf[2], HYD_NW * 32, 0, st>>>(ps, hydro_rows(c));
     CRK_LAUNCHED(c, what);
     return CRK_OK;
 }

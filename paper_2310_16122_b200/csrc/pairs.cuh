@@ -4,8 +4,9 @@
 // CTA walks its row in chunks: all threads stage the particles of the next CH/JMAX
 // j-leaves (periodic shift applied, so every difference is exact, O1) into shared
 // memory; each warp then culls the staged candidates against the bounding box of
-// its own G i-particles (ballot + popc compaction into a warp-private index list)
-// and evaluates the survivors.  Lane l holds i-particle l % G and takes every
+// its own G i-particles (ballot + popc compaction) and copies the survivors'
+// positions (plus a payload index) into a warp-private buffer, which it then
+// evaluates with a 4x unrolled loop.  Lane l holds i-particle l % G and takes every
 // (32/G)-th survivor — the paper's half-warp layout (Fig.
 // half-warp-layout: lanes 0-15 / 16-31) generalised to 32/G j-slots, i-centric, with
 // register accumulation and one shuffle reduction over the slots at the end: no
@@ -30,19 +31,25 @@ struct RowView {
 //   static constexpr int PAY;            payload float4 per staged j (after the position)
 //   static constexpr bool SYM;           culling radius also uses j's H^2 (jpos.w)
 //   struct I; struct Acc;
-//   void load_i(int i, I&) ; float3-ish position via ix/iy/iz ; float cut(const I&)
+//   void init(Acc&); void load_i(int i, I&); float ix/iy/iz(const I&); float cut(const I&)
 //   void stage(int j, float ox, float oy, float oz, float4& jp, float4* pay)
 //   void pair(const I&, Acc&, const float4& jp, const float4* pay)
-//   void reduce(Acc&) ; void finish(int i, const I&, const Acc&)
+//   template<int G> void reduce(Acc&) ; void finish(int i, const I&, const Acc&)
 template <class Pass, int NW, int G, int CH>
-__global__ void __launch_bounds__(NW * 32) pair_kernel(const Pass pass, const RowView rv) {
+struct PairSmem {
+    float4 jpos[CH];
+    float4 jpay[Pass::PAY > 0 ? CH * Pass::PAY : 1];
+    float4 wpos[NW][CH];
+    uint16_t widx[Pass::PAY > 0 ? NW : 1][Pass::PAY > 0 ? CH : 1];
+};
+
+template <class Pass, int NW, int G, int CH, int MINB>
+__global__ void __launch_bounds__(NW * 32, MINB) pair_kernel(const Pass pass, const RowView rv) {
     static_assert(32 % G == 0, "G must divide the warp");
     static_assert(CH % 32 == 0 && CH % JMAX == 0, "bad chunk");
     constexpr int S = 32 / G;
-    extern __shared__ __align__(16) unsigned char smem_raw[];
-    float4* jpos = reinterpret_cast<float4*>(smem_raw);
-    float4* jpay = jpos + CH;
-    uint16_t* wl_all = reinterpret_cast<uint16_t*>(jpay + CH * Pass::PAY);
+    constexpr bool HASPAY = Pass::PAY > 0;
+    __shared__ PairSmem<Pass, NW, G, CH> sm;
 
     const int a = blockIdx.x;
     const int ifirst = rv.ifirst[a];
@@ -54,7 +61,8 @@ __global__ void __launch_bounds__(NW * 32) pair_kernel(const Pass pass, const Ro
     const int ibase = warp * G;
     const bool wactive = ibase < icount;
     const bool ivalid = ibase + il < icount;
-    uint16_t* wl = wl_all + warp * CH;
+    float4* wpos = sm.wpos[warp];
+    uint16_t* widx = sm.widx[HASPAY ? warp : 0];
 
     typename Pass::I is;
     typename Pass::Acc acc;
@@ -62,14 +70,14 @@ __global__ void __launch_bounds__(NW * 32) pair_kernel(const Pass pass, const Ro
     float lo[3], hi[3], wcut = 0.f;
     if (wactive) {
         pass.load_i(ifirst + ibase + (ivalid ? il : 0), is);
-        float px = pass.ix(is), py = pass.iy(is), pz = pass.iz(is);
+        const float px = pass.ix(is), py = pass.iy(is), pz = pass.iz(is);
         lo[0] = warp_min(ivalid ? px : INFINITY);
         lo[1] = warp_min(ivalid ? py : INFINITY);
         lo[2] = warp_min(ivalid ? pz : INFINITY);
         hi[0] = warp_max(ivalid ? px : -INFINITY);
         hi[1] = warp_max(ivalid ? py : -INFINITY);
         hi[2] = warp_max(ivalid ? pz : -INFINITY);
-        wcut = warp_max(ivalid ? pass.cut(is) : 0.f);
+        wcut = warp_max(ivalid ? pass.cut(is) : 0.f) * CULL_SLACK;
     }
 
     const int rbeg = rv.row_off[a], rend = rv.row_off[a + 1];
@@ -81,20 +89,20 @@ __global__ void __launch_bounds__(NW * 32) pair_kernel(const Pass pass, const Ro
             bool ok = false;
             int j = 0, code = 13;
             if (e < rend) {
-                const int b = rv.col[e];
-                if (k < rv.jcount[b]) {
+                const int b = __ldg(rv.col + e);
+                if (k < __ldg(rv.jcount + b)) {
                     ok = true;
-                    j = rv.jfirst[b] + k;
-                    code = rv.shift[e];
+                    j = __ldg(rv.jfirst + b) + k;
+                    code = __ldg(rv.shift + e);
                 }
             }
             if (ok) {
                 int sx, sy, sz;
                 decode_shift(code, sx, sy, sz);
-                pass.stage(j, (float)sx * rv.L[0], (float)sy * rv.L[1], (float)sz * rv.L[2], jpos[t],
-                           jpay + t * Pass::PAY);
+                pass.stage(j, (float)sx * rv.L[0], (float)sy * rv.L[1], (float)sz * rv.L[2], sm.jpos[t],
+                           sm.jpay + (HASPAY ? t * Pass::PAY : 0));
             } else {
-                jpos[t] = make_float4(INFINITY, INFINITY, INFINITY, 0.f);
+                sm.jpos[t] = make_float4(INFINITY, INFINITY, INFINITY, 0.f);
             }
         }
         __syncthreads();
@@ -104,28 +112,32 @@ __global__ void __launch_bounds__(NW * 32) pair_kernel(const Pass pass, const Ro
             for (int t0 = 0; t0 < nslots; t0 += 32) {
                 const int t = t0 + lane;
                 bool keep = false;
+                float4 p = make_float4(INFINITY, INFINITY, INFINITY, 0.f);
                 if (t < nslots) {
-                    const float4 p = jpos[t];
+                    p = sm.jpos[t];
                     const float d2 = box_dist2(p.x, p.y, p.z, lo, hi);
-                    const float c = Pass::SYM ? fmaxf(wcut, p.w) : wcut;
-                    keep = d2 < c * CULL_SLACK;
+                    keep = d2 < (Pass::SYM ? fmaxf(wcut, p.w * CULL_SLACK) : wcut);
                 }
                 const unsigned m = __ballot_sync(0xffffffffu, keep);
-                if (keep) wl[cnt + __popc(m & ((1u << lane) - 1u))] = (uint16_t)t;
+                if (keep) {
+                    const int o = cnt + __popc(m & ((1u << lane) - 1u));
+                    wpos[o] = p;
+                    if (HASPAY) widx[o] = (uint16_t)t;
+                }
                 cnt += __popc(m);
             }
             __syncwarp();
             int k = sl;
 #pragma unroll 1
-            for (; k + S < cnt; k += 2 * S) {
-                const int t0 = wl[k], t1 = wl[k + S];
-                pass.pair(is, acc, jpos[t0], jpay + t0 * Pass::PAY);
-                pass.pair(is, acc, jpos[t1], jpay + t1 * Pass::PAY);
+            for (; k + 3 * S < cnt; k += 4 * S) {
+#pragma unroll
+                for (int u = 0; u < 4; ++u) {
+                    const int kk = k + u * S;
+                    pass.pair(is, acc, wpos[kk], sm.jpay + (HASPAY ? widx[kk] * Pass::PAY : 0));
+                }
             }
-            if (k < cnt) {
-                const int t0 = wl[k];
-                pass.pair(is, acc, jpos[t0], jpay + t0 * Pass::PAY);
-            }
+#pragma unroll 1
+            for (; k < cnt; k += S) pass.pair(is, acc, wpos[k], sm.jpay + (HASPAY ? widx[k] * Pass::PAY : 0));
         }
         __syncthreads();
     }
@@ -133,11 +145,6 @@ __global__ void __launch_bounds__(NW * 32) pair_kernel(const Pass pass, const Ro
         pass.template reduce<G>(acc);
         if (ivalid && sl == 0) pass.finish(ifirst + ibase + il, is, acc);
     }
-}
-
-template <class Pass, int NW, int G, int CH>
-inline size_t pair_smem_bytes() {
-    return (size_t)CH * sizeof(float4) * (1 + Pass::PAY) + (size_t)NW * CH * sizeof(uint16_t);
 }
 
 }  // namespace crk

@@ -93,7 +93,7 @@ def test_sort_order_matches_lexsort(c1):
     cs = int(round(math.log2(params["cell_side"] / q)))
     ncell = int(round(L / params["cell_side"]))
     cbits = max(1, int(math.ceil(math.log2(ncell))))
-    fbits = min(cs, (64 - 3 * cbits) // 3)
+    fbits = min(cs, (32 - 3 * cbits) // 3)
     cell = xi >> cs
     fine = (xi & ((1 << cs) - 1)) >> (cs - fbits)
     cm = _morton_np(cell, cbits)
