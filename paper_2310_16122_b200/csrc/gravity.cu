@@ -13,6 +13,7 @@ template <bool COUNT>
 struct GravPass {
     static constexpr int PAY = 0;
     static constexpr bool SYM = false;
+    static constexpr int UNROLL = 4;
     const float4* xm;  // sorted (x, y, z, m)
     float rcut2, eps2, G, dt;
     float c0, c1, c2, c3, c4, c5;
@@ -99,6 +100,8 @@ static crk_status launch_grav(crk_ctx* c, crk_particles* p, float dt, int32_t* c
     rv.row_off = P<int32_t>(c->rowoff[0]);
     rv.col = P<int32_t>(c->col[0]);
     rv.shift = P<int8_t>(c->shift[0]);
+    rv.jbbox = P<float>(c->lbbox[1]);
+    rv.jmaxh2 = nullptr;
     for (int a = 0; a < 3; ++a) rv.L[a] = c->lay.L[a];
     if (c->nleaf[0] == 0) return CRK_OK;
     pair_kernel<GravPass<COUNT>, GRAV_NW, GRAV_G, GRAV_CH, 1>

@@ -31,6 +31,7 @@ template <bool COUNT>
 struct GeoPass : HydCommon {
     static constexpr int PAY = 0;
     static constexpr bool SYM = false;
+    static constexpr int UNROLL = 4;
     float* gV;
     float* Vout;
     int32_t* cnt;
@@ -84,6 +85,7 @@ struct GeoPass : HydCommon {
 struct CorPass : HydCommon {
     static constexpr int PAY = 0;
     static constexpr bool SYM = false;
+    static constexpr int UNROLL = 2;
     const float* gV;
     float* gcoef;  // 16 planes of n_gas
     int64_t ng;
@@ -265,6 +267,7 @@ struct CorPass : HydCommon {
 struct ExtPass : HydCommon {
     static constexpr int PAY = 1;
     static constexpr bool SYM = false;
+    static constexpr int UNROLL = 2;
     const float* gV;
     const float* gcoef;
     const float4* gvel;  // (vx, vy, vz, m)
@@ -411,6 +414,7 @@ template <bool COUNT>
 struct AccPass : HydCommon {
     static constexpr int PAY = COUNT ? 0 : 9;
     static constexpr bool SYM = true;
+    static constexpr int UNROLL = 1;
     const float4* grec;
     float Cl, Cq, e2, dt;
     int64_t n;
@@ -531,6 +535,8 @@ static RowView hydro_rows(crk_ctx* c) {
     rv.row_off = P<int32_t>(c->rowoff[1]);
     rv.col = P<int32_t>(c->col[1]);
     rv.shift = P<int8_t>(c->shift[1]);
+    rv.jbbox = P<float>(c->lbbox[3]);
+    rv.jmaxh2 = P<float>(c->lmaxh2[3]);
     for (int a = 0; a < 3; ++a) rv.L[a] = c->lay.L[a];
     return rv;
 }
@@ -565,7 +571,7 @@ crk_status corrections(crk_ctx* c, crk_particles* p, cudaStream_t st) {
     g.ng = c->n_gas;
     g.A = p->A; g.B = p->B; g.dA = p->dA; g.dB = p->dB;
     g.n = c->n;
-    return launch_hyd<CorPass, HYD_CH>(c, g, st, "corrections kernel");
+    return launch_hyd<CorPass, HYD_CH, 3>(c, g, st, "corrections kernel");
 }
 
 __global__ void k_gather_gas_state(int64_t ng, const int32_t* gas_idx, const float* vx, const float* vy,
@@ -593,7 +599,7 @@ crk_status extras(crk_ctx* c, crk_particles* p, cudaStream_t st) {
     g.n = c->n;
     g.gamma = c->prm.gamma;
     g.rho = p->rho; g.P = p->P; g.cs = p->cs; g.dv = p->dv;
-    return launch_hyd<ExtPass, HYD_CH>(c, g, st, "extras kernel");
+    return launch_hyd<ExtPass, HYD_CH, 3>(c, g, st, "extras kernel");
 }
 
 crk_status accel_dudt(crk_ctx* c, crk_particles* p, float dt, cudaStream_t st) {
@@ -606,7 +612,7 @@ crk_status accel_dudt(crk_ctx* c, crk_particles* p, float dt, cudaStream_t st) {
     g.ahx = p->ahx; g.ahy = p->ahy; g.ahz = p->ahz; g.dudt = p->dudt;
     g.vx = p->vx; g.vy = p->vy; g.vz = p->vz; g.u = p->u;
     g.cnt = nullptr;
-    return launch_hyd<AccPass<false>, ACC_CH>(c, g, st, "accel/dudt kernel");
+    return launch_hyd<AccPass<false>, ACC_CH, 2>(c, g, st, "accel/dudt kernel");
 }
 
 crk_status hydro_count(crk_ctx* c, int32_t* cgather, int32_t* csym, cudaStream_t st) {

@@ -24,23 +24,30 @@ struct RowView {
     const int32_t* row_off;
     const int32_t* col;
     const int8_t* shift;
+    const float* jbbox;   // 6 floats per j-leaf (lo xyz, hi xyz)
+    const float* jmaxh2;  // per j-leaf max H^2 (SYM passes)
     float L[3];
 };
 
 // Pass concept:
 //   static constexpr int PAY;            payload float4 per staged j (after the position)
 //   static constexpr bool SYM;           culling radius also uses j's H^2 (jpos.w)
+//   static constexpr int UNROLL;         survivors per lane per loop iteration
 //   struct I; struct Acc;
 //   void init(Acc&); void load_i(int i, I&); float ix/iy/iz(const I&); float cut(const I&)
 //   void stage(int j, float ox, float oy, float oz, float4& jp, float4* pay)
 //   void pair(const I&, Acc&, const float4& jp, const float4* pay)
 //   template<int G> void reduce(Acc&) ; void finish(int i, const I&, const Acc&)
+// Passes without payload copy the survivors' float4 into the warp list (one LDS.128 per
+// pair); passes with a payload keep a u16 index list (the payload stays in the tile).
 template <class Pass, int NW, int G, int CH>
 struct PairSmem {
+    static constexpr bool COPY = Pass::PAY == 0;
     float4 jpos[CH];
-    float4 jpay[Pass::PAY > 0 ? CH * Pass::PAY : 1];
-    float4 wpos[NW][CH];
-    uint16_t widx[Pass::PAY > 0 ? NW : 1][Pass::PAY > 0 ? CH : 1];
+    float4 jpay[COPY ? 1 : CH * Pass::PAY];
+    float4 wpos[COPY ? NW : 1][COPY ? CH : 1];
+    uint16_t widx[COPY ? 1 : NW][COPY ? 1 : CH];
+    uint8_t went[NW][32];
 };
 
 template <class Pass, int NW, int G, int CH, int MINB>
@@ -49,7 +56,8 @@ __global__ void __launch_bounds__(NW * 32, MINB) pair_kernel(const Pass pass, co
     static_assert(CH % 32 == 0 && CH % JMAX == 0, "bad chunk");
     constexpr int S = 32 / G;
     constexpr bool HASPAY = Pass::PAY > 0;
-    __shared__ PairSmem<Pass, NW, G, CH> sm;
+    using SM = PairSmem<Pass, NW, G, CH>;
+    __shared__ SM sm;
 
     const int a = blockIdx.x;
     const int ifirst = rv.ifirst[a];
@@ -61,8 +69,10 @@ __global__ void __launch_bounds__(NW * 32, MINB) pair_kernel(const Pass pass, co
     const int ibase = warp * G;
     const bool wactive = ibase < icount;
     const bool ivalid = ibase + il < icount;
-    float4* wpos = sm.wpos[warp];
-    uint16_t* widx = sm.widx[HASPAY ? warp : 0];
+    float4* wpos = sm.wpos[SM::COPY ? warp : 0];
+    uint16_t* widx = sm.widx[SM::COPY ? 0 : warp];
+    uint8_t* went = sm.went[warp];
+    static_assert(CH / JMAX <= 32, "one lane per staged j-leaf");
 
     typename Pass::I is;
     typename Pass::Acc acc;
@@ -107,37 +117,70 @@ __global__ void __launch_bounds__(NW * 32, MINB) pair_kernel(const Pass pass, co
         }
         __syncthreads();
         if (wactive) {
-            const int nslots = min(CH, (rend - e0) * JMAX);
-            int cnt = 0;
-            for (int t0 = 0; t0 < nslots; t0 += 32) {
-                const int t = t0 + lane;
-                bool keep = false;
-                float4 p = make_float4(INFINITY, INFINITY, INFINITY, 0.f);
-                if (t < nslots) {
-                    p = sm.jpos[t];
-                    const float d2 = box_dist2(p.x, p.y, p.z, lo, hi);
-                    keep = d2 < (Pass::SYM ? fmaxf(wcut, p.w * CULL_SLACK) : wcut);
+            // (1) leaf-level prefilter: one lane per staged j-leaf, box-box distance
+            const int nent = min(EPC, rend - e0);
+            bool ek = false;
+            if (lane < nent) {
+                const int e = e0 + lane;
+                const int b = __ldg(rv.col + e);
+                int sx, sy, sz;
+                decode_shift(__ldg(rv.shift + e), sx, sy, sz);
+                const float o[3] = {(float)sx * rv.L[0], (float)sy * rv.L[1], (float)sz * rv.L[2]};
+                const float* bb = rv.jbbox + 6 * (int64_t)b;
+                float d2 = 0.f;
+#pragma unroll
+                for (int d = 0; d < 3; ++d) {
+                    const float g = fmaxf(fmaxf((__ldg(bb + d) + o[d]) - hi[d], lo[d] - (__ldg(bb + 3 + d) + o[d])), 0.f);
+                    d2 = fmaf(g, g, d2);
                 }
+                ek = d2 < (Pass::SYM ? fmaxf(wcut, __ldg(rv.jmaxh2 + b) * CULL_SLACK) : wcut);
+            }
+            const unsigned em = __ballot_sync(0xffffffffu, ek);
+            if (ek) went[__popc(em & ((1u << lane) - 1u))] = (uint8_t)lane;
+            const int nsurv = __popc(em);
+            __syncwarp();
+            // (2) particle-level filter over the surviving leaves, 32/JMAX leaves per step
+            int cnt = 0;
+            for (int q0 = 0; q0 < nsurv; q0 += 32 / JMAX) {
+                const int qe = q0 + lane / JMAX;
+                const int t = (qe < nsurv ? went[qe] : 0) * JMAX + lane % JMAX;
+                float4 p = sm.jpos[t];
+                if (qe >= nsurv) p.x = INFINITY;
+                const float d2 = box_dist2(p.x, p.y, p.z, lo, hi);
+                const bool keep = d2 < (Pass::SYM ? fmaxf(wcut, p.w * CULL_SLACK) : wcut);
                 const unsigned m = __ballot_sync(0xffffffffu, keep);
                 if (keep) {
                     const int o = cnt + __popc(m & ((1u << lane) - 1u));
-                    wpos[o] = p;
-                    if (HASPAY) widx[o] = (uint16_t)t;
+                    if (SM::COPY) wpos[o] = p;
+                    else widx[o] = (uint16_t)t;
                 }
                 cnt += __popc(m);
             }
             __syncwarp();
+            constexpr int U = Pass::UNROLL;
             int k = sl;
 #pragma unroll 1
-            for (; k + 3 * S < cnt; k += 4 * S) {
+            for (; k + (U - 1) * S < cnt; k += U * S) {
 #pragma unroll
-                for (int u = 0; u < 4; ++u) {
+                for (int u = 0; u < U; ++u) {
                     const int kk = k + u * S;
-                    pass.pair(is, acc, wpos[kk], sm.jpay + (HASPAY ? widx[kk] * Pass::PAY : 0));
+                    if (SM::COPY) {
+                        pass.pair(is, acc, wpos[kk], sm.jpay);
+                    } else {
+                        const int t = widx[kk];
+                        pass.pair(is, acc, sm.jpos[t], sm.jpay + t * Pass::PAY);
+                    }
                 }
             }
 #pragma unroll 1
-            for (; k < cnt; k += S) pass.pair(is, acc, wpos[k], sm.jpay + (HASPAY ? widx[k] * Pass::PAY : 0));
+            for (; k < cnt; k += S) {
+                if (SM::COPY) {
+                    pass.pair(is, acc, wpos[k], sm.jpay);
+                } else {
+                    const int t = widx[k];
+                    pass.pair(is, acc, sm.jpos[t], sm.jpay + t * Pass::PAY);
+                }
+            }
         }
         __syncthreads();
     }
