@@ -36,6 +36,7 @@ class CrkParams(C.Structure):
         ("leaf_max_i", C.c_int32), ("leaf_max_j", C.c_int32),
         ("leaf_max_gas_i", C.c_int32), ("leaf_max_gas_j", C.c_int32),
         ("cell_side", C.c_double),
+        ("symmetric", C.c_int32),
     ]
 
 
@@ -98,6 +99,7 @@ def params_struct(p: dict) -> CrkParams:
     s.poly[:] = p["poly"]
     for k in ("leaf_max_i", "leaf_max_j", "leaf_max_gas_i", "leaf_max_gas_j"):
         setattr(s, k, p[k])
+    s.symmetric = int(p.get("symmetric", 1))
     return s
 
 

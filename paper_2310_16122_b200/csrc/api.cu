@@ -127,7 +127,8 @@ crk_status crk_destroy(crk_ctx* c) {
     cudaDeviceSynchronize();
     Buf* bufs[] = {&c->keys_a, &c->keys_b, &c->idx_a, &c->idx_b, &c->cub_tmp, &c->scratch, &c->xm,
                    &c->cell_start, &c->cell_end, &c->leaf_cnt, &c->gflag, &c->grank, &c->gas_idx,
-                   &c->dev_scalars, &c->gpos, &c->gvel, &c->gV, &c->gcoef, &c->grec, &c->gu};
+                   &c->dev_scalars, &c->gpos, &c->gvel, &c->gV, &c->gcoef, &c->grec, &c->gu,
+                   &c->gacc, &c->gkey};
     for (Buf* b : bufs)
         if (b->p) cudaFree(b->p);
     for (int s = 0; s < 4; ++s) {
@@ -150,6 +151,7 @@ static crk_status check_parts(crk_ctx* c, const crk_particles* p, bool need_buil
     if (!p || !p->x || !p->y || !p->z || !p->m || !p->species || !p->id || !p->H || p->n <= 0)
         return fail(c, CRK_EINVAL, "missing particle arrays");
     if (p->n > ((int64_t)1 << 31) - 2) return fail(c, CRK_EINVAL, "n too large");
+    if (c->prm.symmetric && p->n >= ((int64_t)1 << 30)) return fail(c, CRK_EINVAL, "n too large for symmetric mode");
     if (need_built && (c->stage < ST_LISTS || p->n != c->n)) return fail(c, CRK_ESTATE, "call crk_build_lists first");
     cudaError_t e = cudaSetDevice(c->device);
     if (e != cudaSuccess) return cuda_check(c, e, "cudaSetDevice");

@@ -79,6 +79,11 @@ __device__ __forceinline__ float warp_max(float v) {
     for (int o = 16; o > 0; o >>= 1) v = fmaxf(v, __shfl_xor_sync(0xffffffffu, v, o));
     return v;
 }
+__device__ __forceinline__ float warp_sum(float v) {
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+    return v;
+}
 // sum across the j-slots of a warp (lanes l, l+G, l+2G, ... hold partial sums of one i)
 template <int G>
 __device__ __forceinline__ float slot_sum(float v) {

@@ -71,5 +71,7 @@ struct crk_ctx {
     crk::Buf gcoef;              // 16 planes: A, B(3), dA(3), dB(9)  (A, dA unscaled)
     crk::Buf grec;               // accel records: 9 float4 per gas particle
     crk::Buf gu;                 // float
+    crk::Buf gacc;               // float4 force accumulator (symmetric kernels)
+    crk::Buf gkey;               // int32 group key per particle (symmetric gravity)
     crk::Buf pinned;             // host pinned totals
 };

@@ -48,6 +48,7 @@ struct PairSmem {
     float4 wpos[COPY ? NW : 1][COPY ? CH : 1];
     uint16_t widx[COPY ? 1 : NW][COPY ? 1 : CH];
     uint8_t went[NW][32];
+    float4 elo[CH / JMAX], ehi[CH / JMAX];  // shifted j-leaf boxes (.w of elo: max H^2)
 };
 
 template <class Pass, int NW, int G, int CH, int MINB>
@@ -92,48 +93,51 @@ __global__ void __launch_bounds__(NW * 32, MINB) pair_kernel(const Pass pass, co
 
     const int rbeg = rv.row_off[a], rend = rv.row_off[a + 1];
     constexpr int EPC = CH / JMAX;  // entries per chunk
-    for (int e0 = rbeg; e0 < rend; e0 += EPC) {
+    // chunk c takes the row entries c, c + nch, c + 2 nch, ...: every chunk samples the
+    // whole neighbourhood, so the warps' per-chunk work (and the barrier wait) balances
+    const int nch = (rend - rbeg + EPC - 1) / EPC;
+    for (int c = 0; c < nch; ++c) {
+        const int nent = (rend - rbeg - c + nch - 1) / nch;  // entries in this chunk
         for (int t = threadIdx.x; t < CH; t += NW * 32) {
-            const int e = e0 + t / JMAX;
+            const int m = t / JMAX;
             const int k = t % JMAX;
+            const int e = rbeg + c + m * nch;
             bool ok = false;
-            int j = 0, code = 13;
-            if (e < rend) {
-                const int b = __ldg(rv.col + e);
+            int j = 0, code = 13, b = 0;
+            if (m < nent) {
+                b = __ldg(rv.col + e);
+                code = __ldg(rv.shift + e);
                 if (k < __ldg(rv.jcount + b)) {
                     ok = true;
                     j = __ldg(rv.jfirst + b) + k;
-                    code = __ldg(rv.shift + e);
                 }
             }
+            int sx, sy, sz;
+            decode_shift(code, sx, sy, sz);
+            const float ox = (float)sx * rv.L[0], oy = (float)sy * rv.L[1], oz = (float)sz * rv.L[2];
             if (ok) {
-                int sx, sy, sz;
-                decode_shift(code, sx, sy, sz);
-                pass.stage(j, (float)sx * rv.L[0], (float)sy * rv.L[1], (float)sz * rv.L[2], sm.jpos[t],
-                           sm.jpay + (HASPAY ? t * Pass::PAY : 0));
+                pass.stage(j, ox, oy, oz, sm.jpos[t], sm.jpay + (HASPAY ? t * Pass::PAY : 0));
             } else {
                 sm.jpos[t] = make_float4(INFINITY, INFINITY, INFINITY, 0.f);
+            }
+            if (k == 0 && m < nent) {
+                const float* bb = rv.jbbox + 6 * (int64_t)b;
+                sm.elo[m] = make_float4(__ldg(bb) + ox, __ldg(bb + 1) + oy, __ldg(bb + 2) + oz,
+                                        Pass::SYM ? __ldg(rv.jmaxh2 + b) * CULL_SLACK : 0.f);
+                sm.ehi[m] = make_float4(__ldg(bb + 3) + ox, __ldg(bb + 4) + oy, __ldg(bb + 5) + oz, 0.f);
             }
         }
         __syncthreads();
         if (wactive) {
             // (1) leaf-level prefilter: one lane per staged j-leaf, box-box distance
-            const int nent = min(EPC, rend - e0);
             bool ek = false;
             if (lane < nent) {
-                const int e = e0 + lane;
-                const int b = __ldg(rv.col + e);
-                int sx, sy, sz;
-                decode_shift(__ldg(rv.shift + e), sx, sy, sz);
-                const float o[3] = {(float)sx * rv.L[0], (float)sy * rv.L[1], (float)sz * rv.L[2]};
-                const float* bb = rv.jbbox + 6 * (int64_t)b;
-                float d2 = 0.f;
-#pragma unroll
-                for (int d = 0; d < 3; ++d) {
-                    const float g = fmaxf(fmaxf((__ldg(bb + d) + o[d]) - hi[d], lo[d] - (__ldg(bb + 3 + d) + o[d])), 0.f);
-                    d2 = fmaf(g, g, d2);
-                }
-                ek = d2 < (Pass::SYM ? fmaxf(wcut, __ldg(rv.jmaxh2 + b) * CULL_SLACK) : wcut);
+                const float4 bl = sm.elo[lane], bh = sm.ehi[lane];
+                const float gx = fmaxf(fmaxf(bl.x - hi[0], lo[0] - bh.x), 0.f);
+                const float gy = fmaxf(fmaxf(bl.y - hi[1], lo[1] - bh.y), 0.f);
+                const float gz = fmaxf(fmaxf(bl.z - hi[2], lo[2] - bh.z), 0.f);
+                const float d2 = fmaf(gz, gz, fmaf(gy, gy, gx * gx));
+                ek = d2 < (Pass::SYM ? fmaxf(wcut, bl.w) : wcut);
             }
             const unsigned em = __ballot_sync(0xffffffffu, ek);
             if (ek) went[__popc(em & ((1u << lane) - 1u))] = (uint8_t)lane;

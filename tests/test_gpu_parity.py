@@ -63,9 +63,11 @@ def test_sort_leaves_lists_bit_exact(name):
             assert np.array_equal(x[0], y[0]) and np.array_equal(x[1], y[1]), (m, a)
 
 
-@pytest.mark.parametrize("name", ["c1", "lat:32,16,16:0.1:3", "c2u", "c2z"])
-def test_counts_and_full_chain(name):
+@pytest.mark.parametrize("name,sym", [("c1", 1), ("c1", 0), ("lat:32,16,16:0.1:3", 1), ("c2u", 1), ("c2z", 1),
+                                      ("c2z", 0)])
+def test_counts_and_full_chain(name, sym):
     parts, params = cached_config(name)
+    params["symmetric"] = sym
     g = run_gpu(parts, params)
     ref_c = oracle.counts(parts, params)
     cg, ch, cs = g["cnt_in"]
@@ -94,8 +96,10 @@ def test_counts_and_full_chain(name):
     assert norm_err(gi["dudt"][T], ref["dudt"], ref["Sdu"]) <= TOL_FORCE
 
 
-def test_kicks():
+@pytest.mark.parametrize("sym", [1, 0])
+def test_kicks(sym):
     parts, params = cached_config("c1")
+    params["symmetric"] = sym
     dtg, dth = 0.05, 0.02
     g = run_gpu(parts, params, dt_grav=dtg, dt_hydro=dth, counts=False)
     ref = oracle.substep(parts, params, dt_grav=dtg, dt_hydro=dth)
@@ -136,10 +140,12 @@ def test_edge_all_dark_matter_and_all_gas():
 
 
 def test_deterministic_and_resort_idempotent():
+    """i-centric mode (symmetric=0) is bit-reproducible; the sort is idempotent."""
     import torch
     from paper_2310_16122_b200 import Particles, Solver
 
     parts, params = cached_config("lat:32,16,16:0.1:3")
+    params["symmetric"] = 0
     p = Particles.from_host(parts, "cuda")
     s = Solver(params, 0)
     s.substep(p)
