@@ -132,12 +132,12 @@ crk_status crk_destroy(crk_ctx* c) {
     for (Buf* b : bufs)
         if (b->p) cudaFree(b->p);
     for (int s = 0; s < 4; ++s) {
-        Buf* lb[] = {&c->lfirst[s], &c->lcount[s], &c->lbbox[s], &c->lmaxh2[s], &c->lcell[s]};
+        Buf* lb[] = {&c->lfirst[s], &c->lcount[s], &c->lbbox[s], &c->lmaxh2[s], &c->lcell[s], &c->lbox8[s]};
         for (Buf* b : lb)
             if (b->p) cudaFree(b->p);
     }
     for (int m = 0; m < 2; ++m) {
-        Buf* lb[] = {&c->rowlen[m], &c->rowoff[m], &c->col[m], &c->shift[m]};
+        Buf* lb[] = {&c->rowlen[m], &c->rowoff[m], &c->col[m], &c->shift[m], &c->erec[m]};
         for (Buf* b : lb)
             if (b->p) cudaFree(b->p);
     }
@@ -150,7 +150,7 @@ static crk_status check_parts(crk_ctx* c, const crk_particles* p, bool need_buil
     if (!c) return CRK_EINVAL;
     if (!p || !p->x || !p->y || !p->z || !p->m || !p->species || !p->id || !p->H || p->n <= 0)
         return fail(c, CRK_EINVAL, "missing particle arrays");
-    if (p->n > ((int64_t)1 << 31) - 2) return fail(c, CRK_EINVAL, "n too large");
+    if (p->n >= ((int64_t)1 << 29)) return fail(c, CRK_EINVAL, "n must be < 2^29 (packed list entries)");
     if (c->prm.symmetric && p->n >= ((int64_t)1 << 30)) return fail(c, CRK_EINVAL, "n too large for symmetric mode");
     if (need_built && (c->stage < ST_LISTS || p->n != c->n)) return fail(c, CRK_ESTATE, "call crk_build_lists first");
     cudaError_t e = cudaSetDevice(c->device);

@@ -153,7 +153,7 @@ __global__ void k_leaf_fill(int64_t ncm, const int32_t* __restrict__ cstart, con
 
 // bbox (+ max H^2) per leaf; one thread per leaf, members contiguous in xm / gpos
 __global__ void k_leaf_bbox(int64_t nl, const int32_t* __restrict__ first, const int32_t* __restrict__ count,
-                            const float4* __restrict__ pts, int gas, float* bbox, float* maxh2) {
+                            const float4* __restrict__ pts, int gas, float* bbox, float* maxh2, float4* box8) {
     const int64_t l = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
     if (l >= nl) return;
     float lo0 = INFINITY, lo1 = INFINITY, lo2 = INFINITY, hi0 = -INFINITY, hi1 = -INFINITY, hi2 = -INFINITY, mh = 0.f;
@@ -167,6 +167,8 @@ __global__ void k_leaf_bbox(int64_t nl, const int32_t* __restrict__ first, const
     float* b = bbox + 6 * l;
     b[0] = lo0; b[1] = lo1; b[2] = lo2; b[3] = hi0; b[4] = hi1; b[5] = hi2;
     if (gas) maxh2[l] = mh;
+    box8[2 * l] = make_float4(lo0, lo1, lo2, mh);  // 32-byte padded copy for TMA staging
+    box8[2 * l + 1] = make_float4(hi0, hi1, hi2, 0.f);
 }
 
 // ---------------------------------------------------------------- lists (O4)
@@ -216,7 +218,16 @@ struct ListArgs {
     const int32_t* rowoff; // pass 2
     int32_t* col;
     int8_t* shift;
+    const int32_t* jfirst;  // j-leaf first member / count (packed entry records)
+    const int32_t* jcount;
+    int2* erec;
 };
+
+__device__ __forceinline__ void put_entry(const ListArgs& A, int p, int b, int code) {
+    A.col[p] = b;
+    A.shift[p] = (int8_t)code;
+    A.erec[p] = make_int2(A.jfirst[b] | ((A.jcount[b] - 1) << 29), b | (code << 26));
+}
 
 constexpr int LIST_WARPS = 8;
 
@@ -318,11 +329,7 @@ __global__ void __launch_bounds__(LIST_WARPS * 32) k_lists(ListArgs A) {
                     keep = (double)K < (double)cut2 * A.q2inv_slack;
                 }
                 const unsigned msk = __ballot_sync(0xffffffffu, keep);
-                if (FILL && keep) {
-                    const int p = outpos + __popc(msk & ((1u << lane) - 1u));
-                    A.col[p] = b;
-                    A.shift[p] = (int8_t)cd;
-                }
+                if (FILL && keep) put_entry(A, outpos + __popc(msk & ((1u << lane) - 1u)), b, cd);
                 outpos += __popc(msk);
                 total += __popc(msk);
             }
@@ -347,11 +354,7 @@ __global__ void __launch_bounds__(LIST_WARPS * 32) k_lists(ListArgs A) {
                             keep = leaf_pair_test(ba, A.bboxB + 6 * (int64_t)b, A.L, cut2 * slack, code);
                         }
                         const unsigned msk = __ballot_sync(0xffffffffu, keep);
-                        if (FILL && keep) {
-                            const int p = outpos + __popc(msk & ((1u << lane) - 1u));
-                            A.col[p] = b;
-                            A.shift[p] = (int8_t)code;
-                        }
+                        if (FILL && keep) put_entry(A, outpos + __popc(msk & ((1u << lane) - 1u)), b, code);
                         outpos += __popc(msk);
                         total += __popc(msk);
                     }
@@ -388,6 +391,9 @@ static ListArgs list_args(crk_ctx* c, int m) {
     A.rowoff = P<int32_t>(c->rowoff[m]);
     A.col = P<int32_t>(c->col[m]);
     A.shift = P<int8_t>(c->shift[m]);
+    A.jfirst = P<int32_t>(c->lfirst[sb]);
+    A.jcount = P<int32_t>(c->lcount[sb]);
+    A.erec = P<int2>(c->erec[m]);
     return A;
 }
 
@@ -495,6 +501,7 @@ crk_status build_lists(crk_ctx* c, crk_particles* p, cudaStream_t st) {
         CRK_TRY(grow(c, c->lcount[s], nl * 4, st));
         CRK_TRY(grow(c, c->lbbox[s], nl * 24, st));
         CRK_TRY(grow(c, c->lcell[s], nl * 8, st));
+        CRK_TRY(grow(c, c->lbox8[s], nl * 32, st));
         if (s >= 2) CRK_TRY(grow(c, c->lmaxh2[s], nl * 4, st));
         k_leaf_fill<<<nblk(L.ncm, 256), 256, 0, st>>>(L.ncm, P<int32_t>(c->cell_start), P<int32_t>(c->cell_end),
                                                       P<int32_t>(c->grank), cnt + s * (L.ncm + 1), s, lmax[s],
@@ -505,7 +512,7 @@ crk_status build_lists(crk_ctx* c, crk_particles* p, cudaStream_t st) {
             k_leaf_bbox<<<nblk(c->nleaf[s], 128), 128, 0, st>>>(
                 c->nleaf[s], P<int32_t>(c->lfirst[s]), P<int32_t>(c->lcount[s]),
                 s < 2 ? P<float4>(c->xm) : P<float4>(c->gpos), s >= 2, P<float>(c->lbbox[s]),
-                s >= 2 ? P<float>(c->lmaxh2[s]) : nullptr);
+                s >= 2 ? P<float>(c->lmaxh2[s]) : nullptr, P<float4>(c->lbox8[s]));
             CRK_LAUNCHED(c, "leaf bbox");
         }
     }
@@ -534,6 +541,7 @@ crk_status build_lists(crk_ctx* c, crk_particles* p, cudaStream_t st) {
         const int64_t ne = c->nent[m] > 0 ? c->nent[m] : 1;
         CRK_TRY(grow(c, c->col[m], ne * 4, st));
         CRK_TRY(grow(c, c->shift[m], ne, st));
+        CRK_TRY(grow(c, c->erec[m], ne * 8, st));
         ListArgs A = list_args(c, m);
         if (na > 0) {
             k_lists<true><<<nblk(na * 32, LIST_WARPS * 32), LIST_WARPS * 32, 0, st>>>(A);

@@ -61,9 +61,11 @@ struct crk_ctx {
     crk::Buf gflag, grank, gas_idx;
     // leaves (4 sets)
     crk::Buf lfirst[4], lcount[4], lbbox[4], lmaxh2[4], lcell[4];
+    crk::Buf lbox8[4];           // padded boxes: (lo xyz, max H^2), (hi xyz, 0) per leaf
     crk::Buf dev_scalars;        // [0] float max H^2 ; [1..] int64 totals
     // lists (0 gravity, 1 hydro)
     crk::Buf rowlen[2], rowoff[2], col[2], shift[2];
+    crk::Buf erec[2];            // packed entries: int2 (first | (count-1) << 29, leaf | shift << 26)
     // gas-ordered state
     crk::Buf gpos;               // float4 (x, y, z, H)
     crk::Buf gvel;               // float4 (vx, vy, vz, m)

@@ -78,23 +78,28 @@ struct GravPass {
 };
 
 // ============================================================== symmetric (Newton-3) variant
-// Each unordered pair {i, j} is evaluated once, by the warp of the lower i-group.
-// gkey[j] = sorted index of the first particle of j's group (warp w of gravity i-leaf a
-// covers [first_a + 16w, first_a + 16w + 16)), so group order is a total order.  Lanes
-// own the j-survivors and loop over the warp's 16 i-particles (shared-memory
-// broadcast); the i-side sums stay in registers for the whole row and are reduced
-// once at the end; the j-side reactions (and the final i-side sums) go to a float4
-// accumulator with red.global.add.v4.f32 — the set of terms is fixed, their summation
-// order depends on scheduling.  Within the own group the pair is met from both sides,
-// so there only the survivor's (j-side) half is accumulated.  Survivors carry over
-// across chunks so that every warp step but the last is full.
+// Each unordered pair {i, j} is evaluated once, by the warp of the lower i-group.  Warp
+// w of gravity i-leaf a owns the group [gself, gself + ng) with gself = first_a + 16w;
+// groups are contiguous ranges of sorted positions, so "j belongs to this or a later
+// group" is simply j >= gself.  Lanes own the j-survivors and loop over the warp's 16
+// i-particles (shared-memory broadcast); the i-side sums stay in registers for the
+// whole row and are reduced once at the end; the j-side reactions (and the final
+// i-side sums) go to a float4 accumulator with red.global.add.v4.f32 — the set of
+// terms is fixed, their summation order depends on scheduling.  Inside the own group
+// the pair is met from both sides, so there only the survivor's (j-side) half counts.
+//
+// Staging is a two-stage TMA pipeline: for each chunk of 32 row entries, warp 0 issues
+// 1-D bulk copies (cp.async.bulk, mbarrier complete_tx) of the j-leaves' packed
+// (x, y, z, m) rows and of their padded boxes, one chunk ahead of the compute.
+// Survivors carry over across chunks so that every warp step but the last is full.
 namespace symg {
-constexpr int NW = 8, G = 16, CH = 256, CAP = CH + 32;
+constexpr int NW = 8, G = 16, EPC = 32, CH = EPC * JMAX, CAP = CH + 32;
 struct Smem {
-    float4 jpos[CH];
-    int jg[CH];
-    int jidx[CH];
-    float4 elo[CH / JMAX], ehi[CH / JMAX];
+    float4 raw[2][CH];       // TMA: xm rows of the chunk's j-leaves, JMAX slots per entry
+    float4 ebox[2][EPC][2];  // TMA: padded j-leaf boxes
+    float4 eoff[2][EPC];     // periodic offset of the entry (x, y, z), first (w, as int)
+    int ecnt[2][EPC];        // entry size (0: no entry)
+    uint64_t bar[2];
     float4 ipos[NW][G];
     float4 wpos[NW][CAP];
     int widx[NW][CAP];
@@ -109,25 +114,61 @@ __device__ __forceinline__ void red_add_v4(float4* p, float a, float b, float c)
 
 struct GravSymArgs {
     const float4* xm;
-    const int32_t* gkey;
+    const float4* box8;  // gravity j-leaf padded boxes
+    const int2* erec;    // packed list entries
+    const int32_t* row_off;
+    const int32_t* ifirst;
+    const int32_t* icount;
     float4* acc;
+    float L[3];
     float rcut2, eps2;
     float c0, c1, c2, c3, c4, c5;
 };
 
-__global__ void __launch_bounds__(symg::NW * 32, 2) grav_sym_kernel(const GravSymArgs A, const RowView rv) {
+// warp 0 issues the bulk copies of chunk c (entries rbeg + c + m nch) into buffer `buf`
+__device__ __forceinline__ void grav_issue(symg::Smem& sm, const GravSymArgs& A, int rbeg, int nent, int nch, int c,
+                                           int buf, int lane) {
+    int first = 0, count = 0, leaf = 0, code = 13;
+    if (lane < nent) unpack_entry(__ldg(A.erec + rbeg + c + lane * nch), first, count, leaf, code);
+    int sx, sy, sz;
+    decode_shift(code, sx, sy, sz);
+    sm.eoff[buf][lane] = make_float4((float)sx * A.L[0], (float)sy * A.L[1], (float)sz * A.L[2], __int_as_float(first));
+    sm.ecnt[buf][lane] = lane < nent ? count : 0;
+    uint32_t bytes = lane < nent ? (uint32_t)count * 16u + 32u : 0u;
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) bytes += __shfl_xor_sync(0xffffffffu, bytes, o);
+    if (lane == 0) mbar_arrive_expect_tx(&sm.bar[buf], bytes);
+    __syncwarp();
+    if (lane < nent) {
+        bulk_g2s(&sm.raw[buf][lane * JMAX], A.xm + first, (uint32_t)count * 16u, &sm.bar[buf]);
+        bulk_g2s(&sm.ebox[buf][lane][0], A.box8 + 2 * (int64_t)leaf, 32u, &sm.bar[buf]);
+    }
+}
+
+__global__ void __launch_bounds__(symg::NW * 32, 2) grav_sym_kernel(const GravSymArgs A) {
     using namespace symg;
-    extern __shared__ __align__(16) unsigned char smem_raw[];
+    extern __shared__ __align__(128) unsigned char smem_raw[];
     Smem& sm = *reinterpret_cast<Smem*>(smem_raw);
     const int a = blockIdx.x;
-    const int ifirst = rv.ifirst[a];
-    const int icount = rv.icount[a];
+    const int ifirst = A.ifirst[a];
+    const int icount = A.icount[a];
     const int warp = threadIdx.x >> 5;
     const int lane = threadIdx.x & 31;
     const int ibase = warp * G;
     const bool wactive = ibase < icount;
-    const int gself = ifirst + ibase;  // this warp's group key
+    const int gself = ifirst + ibase;  // this warp's group: [gself, gself + ng)
     const int ng = min(G, icount - ibase);
+    const int rbeg = A.row_off[a], rend = A.row_off[a + 1];
+    const int nch = (rend - rbeg + EPC - 1) / EPC;
+    auto nent_of = [&](int c) { return (rend - rbeg - c + nch - 1) / nch; };
+
+    if (threadIdx.x == 0) {
+        mbar_init(&sm.bar[0], 1);
+        mbar_init(&sm.bar[1], 1);
+        mbar_fence_init();
+    }
+    __syncthreads();
+    if (warp == 0 && nch > 0) grav_issue(sm, A, rbeg, nent_of(0), nch, 0, 0, lane);
 
     float lo[3] = {0.f, 0.f, 0.f}, hi[3] = {0.f, 0.f, 0.f};
     const float wcut = A.rcut2 * CULL_SLACK;
@@ -143,6 +184,7 @@ __global__ void __launch_bounds__(symg::NW * 32, 2) grav_sym_kernel(const GravSy
         hi[1] = warp_max(iv ? p.y : -INFINITY);
         hi[2] = warp_max(iv ? p.z : -INFINITY);
     }
+    __syncwarp();
     float ax[G], ay[G], az[G];
 #pragma unroll
     for (int i = 0; i < G; ++i) ax[i] = ay[i] = az[i] = 0.f;
@@ -156,13 +198,13 @@ __global__ void __launch_bounds__(symg::NW * 32, 2) grav_sym_kernel(const GravSy
     auto eval_step = [&](int k0, int kend) {
         const int k = k0 + lane;
         float4 jp = make_float4(1e18f, 1e18f, 1e18f, 0.f);
-        int j = -1;
+        int j = 0;
         if (k < kend) {
             jp = wpos[k];
             j = widx[k];
         }
-        const float mj = j < 0 ? 0.f : (j & 0x40000000 ? 0.f : jp.w);  // own group: j-side only
-        j &= 0x3fffffff;
+        // own group: the i-side half is counted when the partner is the survivor
+        const float mj = (j >= gself && j < gself + ng) ? 0.f : jp.w;
         float bx = 0.f, by = 0.f, bz = 0.f;
 #pragma unroll
         for (int i = 0; i < G; ++i) {
@@ -186,51 +228,19 @@ __global__ void __launch_bounds__(symg::NW * 32, 2) grav_sym_kernel(const GravSy
     };
 
     int cnt = 0;  // survivors waiting in the warp buffer
-    const int rbeg = rv.row_off[a], rend = rv.row_off[a + 1];
-    constexpr int EPC = CH / JMAX;
-    const int nch = (rend - rbeg + EPC - 1) / EPC;
     for (int c = 0; c < nch; ++c) {
-        const int nent = (rend - rbeg - c + nch - 1) / nch;
-        for (int t = threadIdx.x; t < CH; t += NW * 32) {
-            const int m = t / JMAX;
-            const int k = t % JMAX;
-            const int e = rbeg + c + m * nch;
-            bool ok = false;
-            int j = 0, code = 13, b = 0;
-            if (m < nent) {
-                b = __ldg(rv.col + e);
-                code = __ldg(rv.shift + e);
-                if (k < __ldg(rv.jcount + b)) {
-                    ok = true;
-                    j = __ldg(rv.jfirst + b) + k;
-                }
-            }
-            int sx, sy, sz;
-            decode_shift(code, sx, sy, sz);
-            const float ox = (float)sx * rv.L[0], oy = (float)sy * rv.L[1], oz = (float)sz * rv.L[2];
-            if (ok) {
-                const float4 p = __ldg(A.xm + j);
-                sm.jpos[t] = make_float4(p.x + ox, p.y + oy, p.z + oz, p.w);
-                sm.jg[t] = __ldg(A.gkey + j);
-                sm.jidx[t] = j;
-            } else {
-                sm.jpos[t] = make_float4(INFINITY, INFINITY, INFINITY, 0.f);
-                sm.jg[t] = -1;
-            }
-            if (k == 0 && m < nent) {
-                const float* bb = rv.jbbox + 6 * (int64_t)b;
-                sm.elo[m] = make_float4(__ldg(bb) + ox, __ldg(bb + 1) + oy, __ldg(bb + 2) + oz, 0.f);
-                sm.ehi[m] = make_float4(__ldg(bb + 3) + ox, __ldg(bb + 4) + oy, __ldg(bb + 5) + oz, 0.f);
-            }
-        }
-        __syncthreads();
+        const int buf = c & 1;
+        if (warp == 0 && c + 1 < nch) grav_issue(sm, A, rbeg, nent_of(c + 1), nch, c + 1, buf ^ 1, lane);
+        mbar_wait(&sm.bar[buf], (c >> 1) & 1);
         if (wactive) {
+            const int nent = nent_of(c);
             bool ek = false;
             if (lane < nent) {
-                const float4 bl = sm.elo[lane], bh = sm.ehi[lane];
-                const float gx = fmaxf(fmaxf(bl.x - hi[0], lo[0] - bh.x), 0.f);
-                const float gy = fmaxf(fmaxf(bl.y - hi[1], lo[1] - bh.y), 0.f);
-                const float gz = fmaxf(fmaxf(bl.z - hi[2], lo[2] - bh.z), 0.f);
+                const float4 o = sm.eoff[buf][lane];
+                const float4 bl = sm.ebox[buf][lane][0], bh = sm.ebox[buf][lane][1];
+                const float gx = fmaxf(fmaxf(bl.x + o.x - hi[0], lo[0] - bh.x - o.x), 0.f);
+                const float gy = fmaxf(fmaxf(bl.y + o.y - hi[1], lo[1] - bh.y - o.y), 0.f);
+                const float gz = fmaxf(fmaxf(bl.z + o.z - hi[2], lo[2] - bh.z - o.z), 0.f);
                 ek = fmaf(gz, gz, fmaf(gy, gy, gx * gx)) < wcut;
             }
             const unsigned em = __ballot_sync(0xffffffffu, ek);
@@ -239,16 +249,19 @@ __global__ void __launch_bounds__(symg::NW * 32, 2) grav_sym_kernel(const GravSy
             __syncwarp();
             for (int q0 = 0; q0 < nsurv; q0 += 32 / JMAX) {
                 const int qe = q0 + lane / JMAX;
-                const int t = (qe < nsurv ? went[qe] : 0) * JMAX + lane % JMAX;
-                const float4 p = sm.jpos[t];
-                const int jgk = sm.jg[t];
-                // pairs owned by this group: j in a later group, or j in this group
-                const bool keep = qe < nsurv && jgk >= gself && box_dist2(p.x, p.y, p.z, lo, hi) < wcut;
+                const int kk = lane % JMAX;
+                const int e = went[qe < nsurv ? qe : 0];
+                const float4 o = sm.eoff[buf][e];
+                float4 p = sm.raw[buf][e * JMAX + kk];
+                p.x += o.x; p.y += o.y; p.z += o.z;  // exact (O1)
+                const int j = __float_as_int(o.w) + kk;
+                const bool keep = qe < nsurv && kk < sm.ecnt[buf][e] && j >= gself &&
+                                  box_dist2(p.x, p.y, p.z, lo, hi) < wcut;
                 const unsigned msk = __ballot_sync(0xffffffffu, keep);
                 if (keep) {
-                    const int o = cnt + __popc(msk & ((1u << lane) - 1u));
-                    wpos[o] = p;
-                    widx[o] = sm.jidx[t] | (jgk == gself ? 0x40000000 : 0);
+                    const int o2 = cnt + __popc(msk & ((1u << lane) - 1u));
+                    wpos[o2] = p;
+                    widx[o2] = j;
                 }
                 cnt += __popc(msk);
             }
@@ -257,21 +270,21 @@ __global__ void __launch_bounds__(symg::NW * 32, 2) grav_sym_kernel(const GravSy
             for (int k0 = 0; k0 < nfull; k0 += 32) eval_step(k0, nfull);
             // move the remainder (< 32) to the front of the buffer
             const int rem = cnt - nfull;
-            float4 rp;
-            int ri = 0;
+            float4 rp = make_float4(0.f, 0.f, 0.f, 0.f);
+            int rj = 0;
             if (nfull > 0 && lane < rem) {
                 rp = wpos[nfull + lane];
-                ri = widx[nfull + lane];
+                rj = widx[nfull + lane];
             }
             __syncwarp();
             if (nfull > 0 && lane < rem) {
                 wpos[lane] = rp;
-                widx[lane] = ri;
+                widx[lane] = rj;
             }
             cnt = rem;
             __syncwarp();
         }
-        __syncthreads();
+        __syncthreads();  // buffer `buf` is free for chunk c + 2
     }
     if (wactive) {
         if (cnt > 0) eval_step(0, cnt);
@@ -296,15 +309,6 @@ __global__ void k_grav_finish(int64_t n, const float4* __restrict__ acc, float G
         vy[i] = fmaf(dt, gy, vy[i]);
         vz[i] = fmaf(dt, gz, vz[i]);
     }
-}
-
-// group keys: gkey[k] = first_a + 16 ((k - first_a) / 16) for k in gravity i-leaf a
-__global__ void k_group_keys(int64_t nl, const int32_t* __restrict__ first, const int32_t* __restrict__ count,
-                             int32_t* gkey) {
-    const int64_t l = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
-    if (l >= nl) return;
-    const int f = first[l], c = count[l];
-    for (int t = 0; t < c; ++t) gkey[f + t] = f + symg::G * (t / symg::G);
 }
 
 constexpr int GRAV_CH = 256;
@@ -358,16 +362,17 @@ static RowView grav_rows(crk_ctx* c) {
 static crk_status gravity_sym(crk_ctx* c, crk_particles* p, float dt, cudaStream_t st) {
     const int64_t n = c->n;
     CRK_TRY(grow(c, c->gacc, n * 16, st));
-    CRK_TRY(grow(c, c->gkey, n * 4, st));
     CRK_TRY(cuda_check(c, cudaMemsetAsync(c->gacc.p, 0, n * 16, st), "memset"));
     if (c->nleaf[0] > 0) {
-        k_group_keys<<<(unsigned)((c->nleaf[0] + 127) / 128), 128, 0, st>>>(
-            c->nleaf[0], P<int32_t>(c->lfirst[0]), P<int32_t>(c->lcount[0]), P<int32_t>(c->gkey));
-        CRK_LAUNCHED(c, "group keys");
         GravSymArgs A;
         A.xm = P<float4>(c->xm);
-        A.gkey = P<int32_t>(c->gkey);
+        A.box8 = P<float4>(c->lbox8[1]);
+        A.erec = P<int2>(c->erec[0]);
+        A.row_off = P<int32_t>(c->rowoff[0]);
+        A.ifirst = P<int32_t>(c->lfirst[0]);
+        A.icount = P<int32_t>(c->lcount[0]);
         A.acc = P<float4>(c->gacc);
+        for (int d = 0; d < 3; ++d) A.L[d] = c->lay.L[d];
         A.rcut2 = c->prm.rcut2;
         A.eps2 = c->prm.eps2;
         A.c0 = c->prm.poly[0]; A.c1 = c->prm.poly[1]; A.c2 = c->prm.poly[2];
@@ -375,7 +380,7 @@ static crk_status gravity_sym(crk_ctx* c, crk_particles* p, float dt, cudaStream
         const int smem = (int)sizeof(symg::Smem);
         cudaError_t e = cudaFuncSetAttribute(grav_sym_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
         if (e != cudaSuccess) return cuda_check(c, e, "smem attribute");
-        grav_sym_kernel<<<(unsigned)c->nleaf[0], symg::NW * 32, smem, st>>>(A, grav_rows(c));
+        grav_sym_kernel<<<(unsigned)c->nleaf[0], symg::NW * 32, smem, st>>>(A);
         CRK_LAUNCHED(c, "gravity (symmetric) kernel");
     }
     k_grav_finish<<<(unsigned)((n + 255) / 256), 256, 0, st>>>(n, P<float4>(c->gacc), c->prm.G, dt, p->ax, p->ay,
