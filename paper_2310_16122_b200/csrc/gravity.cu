@@ -88,22 +88,23 @@ struct GravPass {
 // terms is fixed, their summation order depends on scheduling.  Inside the own group
 // the pair is met from both sides, so there only the survivor's (j-side) half counts.
 //
-// Staging is a two-stage TMA pipeline: for each chunk of 32 row entries, warp 0 issues
-// 1-D bulk copies (cp.async.bulk, mbarrier complete_tx) of the j-leaves' packed
-// (x, y, z, m) rows and of their padded boxes, one chunk ahead of the compute.
-// Survivors carry over across chunks so that every warp step but the last is full.
+// Staging: the whole row (up to ENT entries; longer rows in several rounds) is copied
+// into shared memory with 1-D TMA bulk copies (cp.async.bulk, one per j-leaf row of
+// packed (x, y, z, m) and one per padded leaf box) completing on one mbarrier; after
+// that single wait every warp runs prefilter -> particle filter -> evaluation on its
+// own, feeding a 64-entry ring of survivors so that every warp step but the last is full.
 namespace symg {
-constexpr int NW = 8, G = 16, EPC = 32, CH = EPC * JMAX, CAP = CH + 32;
+constexpr int NW = 8, G = 16, ENT = 256, RING = 64;
 struct Smem {
-    float4 raw[2][CH];       // TMA: xm rows of the chunk's j-leaves, JMAX slots per entry
-    float4 ebox[2][EPC][2];  // TMA: padded j-leaf boxes
-    float4 eoff[2][EPC];     // periodic offset of the entry (x, y, z), first (w, as int)
-    int ecnt[2][EPC];        // entry size (0: no entry)
-    uint64_t bar[2];
+    float4 raw[ENT * JMAX];  // TMA: xm rows of the row's j-leaves, JMAX slots per entry
+    float4 ebox[ENT][2];     // TMA: padded j-leaf boxes
+    float4 eoff[ENT];        // periodic offset (x, y, z) and first (w, as int)
+    int ecnt[ENT];
+    uint64_t bar;
     float4 ipos[NW][G];
-    float4 wpos[NW][CAP];
-    int widx[NW][CAP];
-    uint8_t went[NW][32];
+    float4 wpos[NW][RING];
+    int widx[NW][RING];
+    uint16_t went[NW][ENT];
 };
 }  // namespace symg
 
@@ -125,26 +126,6 @@ struct GravSymArgs {
     float c0, c1, c2, c3, c4, c5;
 };
 
-// warp 0 issues the bulk copies of chunk c (entries rbeg + c + m nch) into buffer `buf`
-__device__ __forceinline__ void grav_issue(symg::Smem& sm, const GravSymArgs& A, int rbeg, int nent, int nch, int c,
-                                           int buf, int lane) {
-    int first = 0, count = 0, leaf = 0, code = 13;
-    if (lane < nent) unpack_entry(__ldg(A.erec + rbeg + c + lane * nch), first, count, leaf, code);
-    int sx, sy, sz;
-    decode_shift(code, sx, sy, sz);
-    sm.eoff[buf][lane] = make_float4((float)sx * A.L[0], (float)sy * A.L[1], (float)sz * A.L[2], __int_as_float(first));
-    sm.ecnt[buf][lane] = lane < nent ? count : 0;
-    uint32_t bytes = lane < nent ? (uint32_t)count * 16u + 32u : 0u;
-#pragma unroll
-    for (int o = 16; o > 0; o >>= 1) bytes += __shfl_xor_sync(0xffffffffu, bytes, o);
-    if (lane == 0) mbar_arrive_expect_tx(&sm.bar[buf], bytes);
-    __syncwarp();
-    if (lane < nent) {
-        bulk_g2s(&sm.raw[buf][lane * JMAX], A.xm + first, (uint32_t)count * 16u, &sm.bar[buf]);
-        bulk_g2s(&sm.ebox[buf][lane][0], A.box8 + 2 * (int64_t)leaf, 32u, &sm.bar[buf]);
-    }
-}
-
 __global__ void __launch_bounds__(symg::NW * 32, 2) grav_sym_kernel(const GravSymArgs A) {
     using namespace symg;
     extern __shared__ __align__(128) unsigned char smem_raw[];
@@ -159,17 +140,11 @@ __global__ void __launch_bounds__(symg::NW * 32, 2) grav_sym_kernel(const GravSy
     const int gself = ifirst + ibase;  // this warp's group: [gself, gself + ng)
     const int ng = min(G, icount - ibase);
     const int rbeg = A.row_off[a], rend = A.row_off[a + 1];
-    const int nch = (rend - rbeg + EPC - 1) / EPC;
-    auto nent_of = [&](int c) { return (rend - rbeg - c + nch - 1) / nch; };
 
     if (threadIdx.x == 0) {
-        mbar_init(&sm.bar[0], 1);
-        mbar_init(&sm.bar[1], 1);
+        mbar_init(&sm.bar, 1);
         mbar_fence_init();
     }
-    __syncthreads();
-    if (warp == 0 && nch > 0) grav_issue(sm, A, rbeg, nent_of(0), nch, 0, 0, lane);
-
     float lo[3] = {0.f, 0.f, 0.f}, hi[3] = {0.f, 0.f, 0.f};
     const float wcut = A.rcut2 * CULL_SLACK;
     if (wactive) {
@@ -184,24 +159,23 @@ __global__ void __launch_bounds__(symg::NW * 32, 2) grav_sym_kernel(const GravSy
         hi[1] = warp_max(iv ? p.y : -INFINITY);
         hi[2] = warp_max(iv ? p.z : -INFINITY);
     }
-    __syncwarp();
     float ax[G], ay[G], az[G];
 #pragma unroll
     for (int i = 0; i < G; ++i) ax[i] = ay[i] = az[i] = 0.f;
     float4* wpos = sm.wpos[warp];
     int* widx = sm.widx[warp];
-    uint8_t* went = sm.went[warp];
+    uint16_t* went = sm.went[warp];
     const float rc2 = A.rcut2, e2 = A.eps2;
     const float c0 = A.c0, c1 = A.c1, c2 = A.c2, c3 = A.c3, c4 = A.c4, c5 = A.c5;
 
-    // one warp step: lane owns survivor k0 + lane (or the far sentinel), loops over the group
-    auto eval_step = [&](int k0, int kend) {
-        const int k = k0 + lane;
+    // one warp step over ring slots [r0, r0 + n): lane owns one survivor, loops over the group
+    auto eval_step = [&](int r0, int n) {
         float4 jp = make_float4(1e18f, 1e18f, 1e18f, 0.f);
         int j = 0;
-        if (k < kend) {
-            jp = wpos[k];
-            j = widx[k];
+        if (lane < n) {
+            const int s = (r0 + lane) & (RING - 1);
+            jp = wpos[s];
+            j = widx[s];
         }
         // own group: the i-side half is counted when the partner is the survivor
         const float mj = (j >= gself && j < gself + ng) ? 0.f : jp.w;
@@ -224,70 +198,78 @@ __global__ void __launch_bounds__(symg::NW * 32, 2) grav_sym_kernel(const GravSy
             by = fmaf(-wj, dy, by);
             bz = fmaf(-wj, dz, bz);
         }
-        if (k < kend) red_add_v4(A.acc + j, bx, by, bz);
+        if (lane < n) red_add_v4(A.acc + j, bx, by, bz);
     };
 
-    int cnt = 0;  // survivors waiting in the warp buffer
-    for (int c = 0; c < nch; ++c) {
-        const int buf = c & 1;
-        if (warp == 0 && c + 1 < nch) grav_issue(sm, A, rbeg, nent_of(c + 1), nch, c + 1, buf ^ 1, lane);
-        mbar_wait(&sm.bar[buf], (c >> 1) & 1);
+    int wr = 0, rd = 0;  // ring write / read counters
+    uint32_t phase = 0;
+    for (int e0 = rbeg; e0 < rend; e0 += ENT) {
+        const int nent = min(ENT, rend - e0);
+        __syncthreads();  // mbarrier initialised / previous round consumed
+        for (int t = threadIdx.x; t < nent; t += NW * 32) {
+            int first, count, leaf, code;
+            unpack_entry(__ldg(A.erec + e0 + t), first, count, leaf, code);
+            int sx, sy, sz;
+            decode_shift(code, sx, sy, sz);
+            sm.eoff[t] = make_float4((float)sx * A.L[0], (float)sy * A.L[1], (float)sz * A.L[2], __int_as_float(first));
+            sm.ecnt[t] = count;
+            mbar_expect_tx(&sm.bar, (uint32_t)count * 16u + 32u);
+            bulk_g2s(&sm.raw[t * JMAX], A.xm + first, (uint32_t)count * 16u, &sm.bar);
+            bulk_g2s(&sm.ebox[t][0], A.box8 + 2 * (int64_t)leaf, 32u, &sm.bar);
+        }
+        __syncthreads();
+        if (threadIdx.x == 0) mbar_arrive(&sm.bar);
+        mbar_wait(&sm.bar, phase);
+        phase ^= 1u;
         if (wactive) {
-            const int nent = nent_of(c);
-            bool ek = false;
-            if (lane < nent) {
-                const float4 o = sm.eoff[buf][lane];
-                const float4 bl = sm.ebox[buf][lane][0], bh = sm.ebox[buf][lane][1];
-                const float gx = fmaxf(fmaxf(bl.x + o.x - hi[0], lo[0] - bh.x - o.x), 0.f);
-                const float gy = fmaxf(fmaxf(bl.y + o.y - hi[1], lo[1] - bh.y - o.y), 0.f);
-                const float gz = fmaxf(fmaxf(bl.z + o.z - hi[2], lo[2] - bh.z - o.z), 0.f);
-                ek = fmaf(gz, gz, fmaf(gy, gy, gx * gx)) < wcut;
+            // (1) leaf prefilter: box-box distance, one lane per entry
+            int nsurv = 0;
+            for (int e = lane; e - lane < nent; e += 32) {
+                bool ek = false;
+                if (e < nent) {
+                    const float4 o = sm.eoff[e];
+                    const float4 bl = sm.ebox[e][0], bh = sm.ebox[e][1];
+                    const float gx = fmaxf(fmaxf(bl.x + o.x - hi[0], lo[0] - bh.x - o.x), 0.f);
+                    const float gy = fmaxf(fmaxf(bl.y + o.y - hi[1], lo[1] - bh.y - o.y), 0.f);
+                    const float gz = fmaxf(fmaxf(bl.z + o.z - hi[2], lo[2] - bh.z - o.z), 0.f);
+                    // entries wholly below this group own no pair (j < gself)
+                    ek = fmaf(gz, gz, fmaf(gy, gy, gx * gx)) < wcut &&
+                         __float_as_int(o.w) + sm.ecnt[e] > gself;
+                }
+                const unsigned em = __ballot_sync(0xffffffffu, ek);
+                if (ek) went[nsurv + __popc(em & ((1u << lane) - 1u))] = (uint16_t)e;
+                nsurv += __popc(em);
             }
-            const unsigned em = __ballot_sync(0xffffffffu, ek);
-            if (ek) went[__popc(em & ((1u << lane) - 1u))] = (uint8_t)lane;
-            const int nsurv = __popc(em);
             __syncwarp();
+            // (2) particle filter, 32/JMAX entries per step, into the survivor ring
             for (int q0 = 0; q0 < nsurv; q0 += 32 / JMAX) {
                 const int qe = q0 + lane / JMAX;
                 const int kk = lane % JMAX;
                 const int e = went[qe < nsurv ? qe : 0];
-                const float4 o = sm.eoff[buf][e];
-                float4 p = sm.raw[buf][e * JMAX + kk];
+                const float4 o = sm.eoff[e];
+                float4 p = sm.raw[e * JMAX + kk];
                 p.x += o.x; p.y += o.y; p.z += o.z;  // exact (O1)
                 const int j = __float_as_int(o.w) + kk;
-                const bool keep = qe < nsurv && kk < sm.ecnt[buf][e] && j >= gself &&
+                const bool keep = qe < nsurv && kk < sm.ecnt[e] && j >= gself &&
                                   box_dist2(p.x, p.y, p.z, lo, hi) < wcut;
                 const unsigned msk = __ballot_sync(0xffffffffu, keep);
                 if (keep) {
-                    const int o2 = cnt + __popc(msk & ((1u << lane) - 1u));
-                    wpos[o2] = p;
-                    widx[o2] = j;
+                    const int s = (wr + __popc(msk & ((1u << lane) - 1u))) & (RING - 1);
+                    wpos[s] = p;
+                    widx[s] = j;
                 }
-                cnt += __popc(msk);
+                wr += __popc(msk);
+                __syncwarp();
+                if (wr - rd >= 32) {
+                    eval_step(rd, 32);
+                    rd += 32;
+                    __syncwarp();
+                }
             }
-            __syncwarp();
-            const int nfull = cnt & ~31;
-            for (int k0 = 0; k0 < nfull; k0 += 32) eval_step(k0, nfull);
-            // move the remainder (< 32) to the front of the buffer
-            const int rem = cnt - nfull;
-            float4 rp = make_float4(0.f, 0.f, 0.f, 0.f);
-            int rj = 0;
-            if (nfull > 0 && lane < rem) {
-                rp = wpos[nfull + lane];
-                rj = widx[nfull + lane];
-            }
-            __syncwarp();
-            if (nfull > 0 && lane < rem) {
-                wpos[lane] = rp;
-                widx[lane] = rj;
-            }
-            cnt = rem;
-            __syncwarp();
         }
-        __syncthreads();  // buffer `buf` is free for chunk c + 2
     }
     if (wactive) {
-        if (cnt > 0) eval_step(0, cnt);
+        if (wr > rd) eval_step(rd, wr - rd);
 #pragma unroll
         for (int i = 0; i < G; ++i) {
             const float sx = warp_sum(ax[i]), sy = warp_sum(ay[i]), sz = warp_sum(az[i]);
