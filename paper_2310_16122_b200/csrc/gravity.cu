@@ -94,7 +94,7 @@ struct GravPass {
 // that single wait every warp runs prefilter -> particle filter -> evaluation on its
 // own, feeding a 64-entry ring of survivors so that every warp step but the last is full.
 namespace symg {
-constexpr int NW = 8, G = 16, ENT = 256, RING = 64;
+constexpr int NW = 4, G = 16, ENT = 256, RING = 64;  // NW warps per CTA; two CTAs per 128-leaf
 struct Smem {
     float4 raw[ENT * JMAX];  // TMA: xm rows of the row's j-leaves, JMAX slots per entry
     float4 ebox[ENT][2];     // TMA: padded j-leaf boxes
@@ -121,21 +121,22 @@ struct GravSymArgs {
     const int32_t* ifirst;
     const int32_t* icount;
     float4* acc;
+    int split;  // CTAs per i-leaf
     float L[3];
     float rcut2, eps2;
     float c0, c1, c2, c3, c4, c5;
 };
 
-__global__ void __launch_bounds__(symg::NW * 32, 2) grav_sym_kernel(const GravSymArgs A) {
+__global__ void __launch_bounds__(symg::NW * 32, 4) grav_sym_kernel(const GravSymArgs A) {
     using namespace symg;
     extern __shared__ __align__(128) unsigned char smem_raw[];
     Smem& sm = *reinterpret_cast<Smem*>(smem_raw);
-    const int a = blockIdx.x;
+    const int a = blockIdx.x / A.split;  // i-leaf; CTA part blockIdx.x % split covers NW groups
     const int ifirst = A.ifirst[a];
     const int icount = A.icount[a];
     const int warp = threadIdx.x >> 5;
     const int lane = threadIdx.x & 31;
-    const int ibase = warp * G;
+    const int ibase = (blockIdx.x % A.split * NW + warp) * G;
     const bool wactive = ibase < icount;
     const int gself = ifirst + ibase;  // this warp's group: [gself, gself + ng)
     const int ng = min(G, icount - ibase);
@@ -362,7 +363,8 @@ static crk_status gravity_sym(crk_ctx* c, crk_particles* p, float dt, cudaStream
         const int smem = (int)sizeof(symg::Smem);
         cudaError_t e = cudaFuncSetAttribute(grav_sym_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
         if (e != cudaSuccess) return cuda_check(c, e, "smem attribute");
-        grav_sym_kernel<<<(unsigned)c->nleaf[0], symg::NW * 32, smem, st>>>(A);
+        A.split = (c->prm.leaf_max_i + symg::NW * symg::G - 1) / (symg::NW * symg::G);
+        grav_sym_kernel<<<(unsigned)(c->nleaf[0] * A.split), symg::NW * 32, smem, st>>>(A);
         CRK_LAUNCHED(c, "gravity (symmetric) kernel");
     }
     k_grav_finish<<<(unsigned)((n + 255) / 256), 256, 0, st>>>(n, P<float4>(c->gacc), c->prm.G, dt, p->ax, p->ay,
