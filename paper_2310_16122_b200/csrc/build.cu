@@ -552,6 +552,7 @@ crk_status build_lists(crk_ctx* c, crk_particles* p, cudaStream_t st) {
     const int64_t ng = c->n_gas > 0 ? c->n_gas : 1;
     CRK_TRY(grow(c, c->gvel, ng * 16, st));
     CRK_TRY(grow(c, c->gV, ng * 4, st));
+    CRK_TRY(grow(c, c->gposV, ng * 16, st));
     CRK_TRY(grow(c, c->gcoef, ng * 16 * 4, st));
     CRK_TRY(grow(c, c->grec, ng * 9 * 16, st));
     CRK_TRY(grow(c, c->gu, ng * 4, st));

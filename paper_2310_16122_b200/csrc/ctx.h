@@ -70,6 +70,7 @@ struct crk_ctx {
     crk::Buf gpos;               // float4 (x, y, z, H)
     crk::Buf gvel;               // float4 (vx, vy, vz, m)
     crk::Buf gV;                 // float
+    crk::Buf gposV;              // float4 (x, y, z, V) j-rows of corrections/extras
     crk::Buf gcoef;              // 16 planes: A, B(3), dA(3), dB(9)  (A, dA unscaled)
     crk::Buf grec;               // accel records: 9 float4 per gas particle
     crk::Buf gu;                 // float

@@ -14,7 +14,9 @@ struct GravPass {
     static constexpr int PAY = 0;
     static constexpr bool SYM = false;
     static constexpr int UNROLL = 4;
-    const float4* xm;  // sorted (x, y, z, m)
+    const float4* jrows;  // sorted (x, y, z, m)
+    const float4* jpay;
+    const float4* xm;
     float rcut2, eps2, G, dt;
     float c0, c1, c2, c3, c4, c5;
     float *ax, *ay, *az, *vx, *vy, *vz;
@@ -32,15 +34,12 @@ struct GravPass {
     __device__ float iy(const I& s) const { return s.y; }
     __device__ float iz(const I& s) const { return s.z; }
     __device__ float cut(const I&) const { return rcut2; }
-    __device__ void stage(int j, float ox, float oy, float oz, float4& jp, float4*) const {
-        const float4 p = __ldg(xm + j);
-        jp = make_float4(p.x + ox, p.y + oy, p.z + oz, COUNT ? __int_as_float(j) : p.w);
-    }
-    __device__ __forceinline__ void pair(const I& s, Acc& a, const float4& jp, const float4*) const {
+    __device__ float jcut(const float4&) const { return 0.f; }
+    __device__ __forceinline__ void pair(const I& s, Acc& a, const float4& jp, const float4*, int j) const {
         const float dx = jp.x - s.x, dy = jp.y - s.y, dz = jp.z - s.z;  // exact (O1)
         const float r2 = s32_of(dx, dy, dz);
         if (COUNT) {
-            a.n += (r2 < rcut2 && __float_as_int(jp.w) != s.idx) ? 1 : 0;
+            a.n += (r2 < rcut2 && j != s.idx) ? 1 : 0;
         } else {
             const float ri = rsqrtf(r2 + eps2);
             const float ri3 = ri * ri * ri;
@@ -294,12 +293,24 @@ __global__ void k_grav_finish(int64_t n, const float4* __restrict__ acc, float G
     }
 }
 
-constexpr int GRAV_CH = 256;
+
+static RowView grav_rows(crk_ctx* c) {
+    RowView rv;
+    rv.ifirst = P<int32_t>(c->lfirst[0]);
+    rv.icount = P<int32_t>(c->lcount[0]);
+    rv.row_off = P<int32_t>(c->rowoff[0]);
+    rv.erec = P<int2>(c->erec[0]);
+    rv.box8 = P<float4>(c->lbox8[1]);
+    for (int a = 0; a < 3; ++a) rv.L[a] = c->lay.L[a];
+    return rv;
+}
 
 template <bool COUNT>
 static crk_status launch_grav(crk_ctx* c, crk_particles* p, float dt, int32_t* cnt, cudaStream_t st) {
     GravPass<COUNT> g;
     g.xm = P<float4>(c->xm);
+    g.jrows = g.xm;
+    g.jpay = nullptr;
     g.rcut2 = c->prm.rcut2;
     g.eps2 = c->prm.eps2;
     g.G = c->prm.G;
@@ -309,37 +320,11 @@ static crk_status launch_grav(crk_ctx* c, crk_particles* p, float dt, int32_t* c
     g.ax = p->ax; g.ay = p->ay; g.az = p->az;
     g.vx = p->vx; g.vy = p->vy; g.vz = p->vz;
     g.cnt = cnt;
-    RowView rv;
-    rv.ifirst = P<int32_t>(c->lfirst[0]);
-    rv.icount = P<int32_t>(c->lcount[0]);
-    rv.jfirst = P<int32_t>(c->lfirst[1]);
-    rv.jcount = P<int32_t>(c->lcount[1]);
-    rv.row_off = P<int32_t>(c->rowoff[0]);
-    rv.col = P<int32_t>(c->col[0]);
-    rv.shift = P<int8_t>(c->shift[0]);
-    rv.jbbox = P<float>(c->lbbox[1]);
-    rv.jmaxh2 = nullptr;
-    for (int a = 0; a < 3; ++a) rv.L[a] = c->lay.L[a];
     if (c->nleaf[0] == 0) return CRK_OK;
-    pair_kernel<GravPass<COUNT>, GRAV_NW, GRAV_G, GRAV_CH, 1>
-        <<<(unsigned)c->nleaf[0], GRAV_NW * 32, 0, st>>>(g, rv);
-    CRK_LAUNCHED(c, "gravity kernel");
+    CRK_TRY(cuda_check(c, launch_pairs<GravPass<COUNT>, GRAV_NW, GRAV_G, 256, 2>(g, grav_rows(c), c->nleaf[0], st),
+                       "gravity kernel"));
+    c->launches++;
     return CRK_OK;
-}
-
-static RowView grav_rows(crk_ctx* c) {
-    RowView rv;
-    rv.ifirst = P<int32_t>(c->lfirst[0]);
-    rv.icount = P<int32_t>(c->lcount[0]);
-    rv.jfirst = P<int32_t>(c->lfirst[1]);
-    rv.jcount = P<int32_t>(c->lcount[1]);
-    rv.row_off = P<int32_t>(c->rowoff[0]);
-    rv.col = P<int32_t>(c->col[0]);
-    rv.shift = P<int8_t>(c->shift[0]);
-    rv.jbbox = P<float>(c->lbbox[1]);
-    rv.jmaxh2 = nullptr;
-    for (int a = 0; a < 3; ++a) rv.L[a] = c->lay.L[a];
-    return rv;
 }
 
 static crk_status gravity_sym(crk_ctx* c, crk_particles* p, float dt, cudaStream_t st) {

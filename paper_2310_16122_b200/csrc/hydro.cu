@@ -9,8 +9,6 @@
 
 namespace crk {
 
-constexpr int HYD_CH = 256;
-constexpr int ACC_CH = 128;
 
 struct HydCommon {
     const float4* gpos;      // (x, y, z, H)
@@ -32,7 +30,10 @@ struct GeoPass : HydCommon {
     static constexpr int PAY = 0;
     static constexpr bool SYM = false;
     static constexpr int UNROLL = 4;
+    const float4* jrows;  // gpos
+    const float4* jpay;
     float* gV;
+    float4* gposV;        // out: (x, y, z, V) rows for the next passes
     float* Vout;
     int32_t* cnt;
     struct I { float x, y, z, H2, invH; int idx; };
@@ -43,16 +44,13 @@ struct GeoPass : HydCommon {
     __device__ float iy(const I& s) const { return s.y; }
     __device__ float iz(const I& s) const { return s.z; }
     __device__ float cut(const I& s) const { return s.H2; }
-    __device__ void stage(int j, float ox, float oy, float oz, float4& jp, float4*) const {
-        const float4 p = __ldg(gpos + j);
-        jp = make_float4(p.x + ox, p.y + oy, p.z + oz, __int_as_float(j));
-    }
-    __device__ __forceinline__ void pair(const I& s, Acc& a, const float4& jp, const float4*) const {
+    __device__ float jcut(const float4&) const { return 0.f; }
+    __device__ __forceinline__ void pair(const I& s, Acc& a, const float4& jp, const float4*, int j) const {
         const float dx = jp.x - s.x, dy = jp.y - s.y, dz = jp.z - s.z;
         const float r2 = s32_of(dx, dy, dz);
         const bool in = r2 < s.H2;
         if (COUNT) {
-            a.n += (in && __float_as_int(jp.w) != s.idx) ? 1 : 0;
+            a.n += (in && j != s.idx) ? 1 : 0;
         } else {
             float wt, gt;
             wendland_t(r2, s.invH, wt, gt);
@@ -75,6 +73,7 @@ struct GeoPass : HydCommon {
         }
         const float V = 1.f / (SIGMA_W * s.invH * s.invH * s.invH * a.w);
         gV[k] = V;
+        gposV[k] = make_float4(s.x, s.y, s.z, V);
         if (Vout) Vout[gas_idx[k]] = V;
     }
 };
@@ -86,7 +85,8 @@ struct CorPass : HydCommon {
     static constexpr int PAY = 0;
     static constexpr bool SYM = false;
     static constexpr int UNROLL = 2;
-    const float* gV;
+    const float4* jrows;  // gposV (x, y, z, V)
+    const float4* jpay;
     float* gcoef;  // 16 planes of n_gas
     int64_t ng;
     float *A, *B, *dA, *dB;  // caller planes (n)
@@ -109,11 +109,8 @@ struct CorPass : HydCommon {
     __device__ float iy(const I& s) const { return s.y; }
     __device__ float iz(const I& s) const { return s.z; }
     __device__ float cut(const I& s) const { return s.H2; }
-    __device__ void stage(int j, float ox, float oy, float oz, float4& jp, float4*) const {
-        const float4 p = __ldg(gpos + j);
-        jp = make_float4(p.x + ox, p.y + oy, p.z + oz, __ldg(gV + j));
-    }
-    __device__ __forceinline__ void pair(const I& s, Acc& a, const float4& jp, const float4*) const {
+    __device__ float jcut(const float4&) const { return 0.f; }
+    __device__ __forceinline__ void pair(const I& s, Acc& a, const float4& jp, const float4*, int) const {
         const float d0 = jp.x - s.x, d1 = jp.y - s.y, d2 = jp.z - s.z;
         const float r2 = s32_of(d0, d1, d2);
         float wt, gt;
@@ -268,6 +265,8 @@ struct ExtPass : HydCommon {
     static constexpr int PAY = 1;
     static constexpr bool SYM = false;
     static constexpr int UNROLL = 2;
+    const float4* jrows;  // gposV (x, y, z, V)
+    const float4* jpay;   // gvel (vx, vy, vz, m)
     const float* gV;
     const float* gcoef;
     const float4* gvel;  // (vx, vy, vz, m)
@@ -301,12 +300,8 @@ struct ExtPass : HydCommon {
     __device__ float iy(const I& s) const { return s.y; }
     __device__ float iz(const I& s) const { return s.z; }
     __device__ float cut(const I& s) const { return s.H2; }
-    __device__ void stage(int j, float ox, float oy, float oz, float4& jp, float4* pay) const {
-        const float4 p = __ldg(gpos + j);
-        jp = make_float4(p.x + ox, p.y + oy, p.z + oz, __ldg(gV + j));
-        pay[0] = __ldg(gvel + j);
-    }
-    __device__ __forceinline__ void pair(const I& s, Acc& a, const float4& jp, const float4* pay) const {
+    __device__ float jcut(const float4&) const { return 0.f; }
+    __device__ __forceinline__ void pair(const I& s, Acc& a, const float4& jp, const float4* pay, int) const {
         // x_ij = x_i - x_j
         const float x0 = s.x - jp.x, x1 = s.y - jp.y, x2 = s.z - jp.z;
         const float r2 = s32_of(x0, x1, x2);
@@ -415,6 +410,8 @@ struct AccPass : HydCommon {
     static constexpr int PAY = COUNT ? 0 : 9;
     static constexpr bool SYM = true;
     static constexpr int UNROLL = 1;
+    const float4* jrows;  // gpos (x, y, z, H)
+    const float4* jpay;   // grec
     const float4* grec;
     float Cl, Cq, e2, dt;
     int64_t n;
@@ -433,25 +430,13 @@ struct AccPass : HydCommon {
     __device__ float iy(const I& s) const { return s.y; }
     __device__ float iz(const I& s) const { return s.z; }
     __device__ float cut(const I& s) const { return s.r.H2; }
-    __device__ void stage(int j, float ox, float oy, float oz, float4& jp, float4* pay) const {
-        const float4 p = __ldg(gpos + j);
-        if (COUNT) {
-            jp = make_float4(p.x + ox, p.y + oy, p.z + oz, __fmul_rn(p.w, p.w));
-            return;
-        }
-        const float4* r = grec + (int64_t)j * 9;
-#pragma unroll
-        for (int t = 0; t < 9; ++t) pay[t] = __ldg(r + t);
-        jp = make_float4(p.x + ox, p.y + oy, p.z + oz, pay[8].y);
-    }
-    __device__ __forceinline__ void pair(const I& s, Acc& acc, const float4& jp, const float4* pay) const {
+    __device__ float jcut(const float4& jp) const { return __fmul_rn(jp.w, jp.w); }
+    __device__ __forceinline__ void pair(const I& s, Acc& acc, const float4& jp, const float4* pay, int j) const {
         float x[3] = {s.x - jp.x, s.y - jp.y, s.z - jp.z};  // x_ij
         const float r2 = s32_of(x[0], x[1], x[2]);
-        const bool in = r2 < fmaxf(s.r.H2, jp.w);
+        const bool in = r2 < fmaxf(s.r.H2, __fmul_rn(jp.w, jp.w));
         if (COUNT) {
-            // j index is not staged in count mode: a j with x_ij = 0 and equal H^2 is i itself
-            // only if it is the same particle; count mode uses the position tie rule below.
-            acc.nn += in ? 1 : 0;
+            acc.nn += (in && j != s.idx) ? 1 : 0;
             return;
         }
         if (!in) return;
@@ -509,7 +494,7 @@ struct AccPass : HydCommon {
     __device__ void finish(int k, const I& s, const Acc& a) const {
         const int64_t i = gas_idx[k];
         if (COUNT) {
-            cnt[i] = a.nn - 1;  // the self pair always satisfies the predicate (s32 = 0)
+            cnt[i] = a.nn;
             return;
         }
         const float f = s.r.V / s.r.m;
@@ -530,22 +515,18 @@ static RowView hydro_rows(crk_ctx* c) {
     RowView rv;
     rv.ifirst = P<int32_t>(c->lfirst[2]);
     rv.icount = P<int32_t>(c->lcount[2]);
-    rv.jfirst = P<int32_t>(c->lfirst[3]);
-    rv.jcount = P<int32_t>(c->lcount[3]);
     rv.row_off = P<int32_t>(c->rowoff[1]);
-    rv.col = P<int32_t>(c->col[1]);
-    rv.shift = P<int8_t>(c->shift[1]);
-    rv.jbbox = P<float>(c->lbbox[3]);
-    rv.jmaxh2 = P<float>(c->lmaxh2[3]);
+    rv.erec = P<int2>(c->erec[1]);
+    rv.box8 = P<float4>(c->lbox8[3]);
     for (int a = 0; a < 3; ++a) rv.L[a] = c->lay.L[a];
     return rv;
 }
 
-template <class Pass, int CH, int MINB = 1>
+template <class Pass, int ENT, int MINB = 1>
 static crk_status launch_hyd(crk_ctx* c, const Pass& ps, cudaStream_t st, const char* what) {
     if (c->nleaf[2] == 0) return CRK_OK;
-    pair_kernel<Pass, HYD_NW, HYD_G, CH, MINB><<<(unsigned)c->nleaf[2], HYD_NW * 32, 0, st>>>(ps, hydro_rows(c));
-    CRK_LAUNCHED(c, what);
+    CRK_TRY(cuda_check(c, launch_pairs<Pass, HYD_NW, HYD_G, ENT, MINB>(ps, hydro_rows(c), c->nleaf[2], st), what));
+    c->launches++;
     return CRK_OK;
 }
 
@@ -557,21 +538,25 @@ static void common(crk_ctx* c, HydCommon& h) {
 crk_status geometry(crk_ctx* c, crk_particles* p, cudaStream_t st) {
     GeoPass<false> g;
     common(c, g);
+    g.jrows = P<float4>(c->gpos);
+    g.jpay = nullptr;
     g.gV = P<float>(c->gV);
+    g.gposV = P<float4>(c->gposV);
     g.Vout = p->V;
     g.cnt = nullptr;
-    return launch_hyd<GeoPass<false>, HYD_CH>(c, g, st, "geometry kernel");
+    return launch_hyd<GeoPass<false>, 128, 2>(c, g, st, "geometry kernel");
 }
 
 crk_status corrections(crk_ctx* c, crk_particles* p, cudaStream_t st) {
     CorPass g;
     common(c, g);
-    g.gV = P<float>(c->gV);
+    g.jrows = P<float4>(c->gposV);
+    g.jpay = nullptr;
     g.gcoef = P<float>(c->gcoef);
     g.ng = c->n_gas;
     g.A = p->A; g.B = p->B; g.dA = p->dA; g.dB = p->dB;
     g.n = c->n;
-    return launch_hyd<CorPass, HYD_CH, 3>(c, g, st, "corrections kernel");
+    return launch_hyd<CorPass, 128, 3>(c, g, st, "corrections kernel");
 }
 
 __global__ void k_gather_gas_state(int64_t ng, const int32_t* gas_idx, const float* vx, const float* vy,
@@ -590,6 +575,8 @@ crk_status extras(crk_ctx* c, crk_particles* p, cudaStream_t st) {
     CRK_LAUNCHED(c, "gather gas state");
     ExtPass g;
     common(c, g);
+    g.jrows = P<float4>(c->gposV);
+    g.jpay = P<float4>(c->gvel);
     g.gV = P<float>(c->gV);
     g.gcoef = P<float>(c->gcoef);
     g.gvel = P<float4>(c->gvel);
@@ -599,32 +586,38 @@ crk_status extras(crk_ctx* c, crk_particles* p, cudaStream_t st) {
     g.n = c->n;
     g.gamma = c->prm.gamma;
     g.rho = p->rho; g.P = p->P; g.cs = p->cs; g.dv = p->dv;
-    return launch_hyd<ExtPass, HYD_CH, 3>(c, g, st, "extras kernel");
+    return launch_hyd<ExtPass, 128, 3>(c, g, st, "extras kernel");
 }
 
 crk_status accel_dudt(crk_ctx* c, crk_particles* p, float dt, cudaStream_t st) {
     if (dt != 0.f && (!p->vx || !p->vy || !p->vz || !p->u)) return fail(c, CRK_EINVAL, "kick needs v and u");
     AccPass<false> g;
     common(c, g);
+    g.jrows = P<float4>(c->gpos);
+    g.jpay = P<float4>(c->grec);
     g.grec = P<float4>(c->grec);
     g.Cl = c->prm.av_cl; g.Cq = c->prm.av_cq; g.e2 = c->prm.av_eps2; g.dt = dt;
     g.n = c->n;
     g.ahx = p->ahx; g.ahy = p->ahy; g.ahz = p->ahz; g.dudt = p->dudt;
     g.vx = p->vx; g.vy = p->vy; g.vz = p->vz; g.u = p->u;
     g.cnt = nullptr;
-    return launch_hyd<AccPass<false>, ACC_CH, 2>(c, g, st, "accel/dudt kernel");
+    return launch_hyd<AccPass<false>, 72, 2>(c, g, st, "accel/dudt kernel");
 }
 
 crk_status hydro_count(crk_ctx* c, int32_t* cgather, int32_t* csym, cudaStream_t st) {
     GeoPass<true> g;
     common(c, g);
-    g.gV = nullptr; g.Vout = nullptr; g.cnt = cgather;
-    CRK_TRY((launch_hyd<GeoPass<true>, HYD_CH>(c, g, st, "gather count kernel")));
+    g.jrows = P<float4>(c->gpos);
+    g.jpay = nullptr;
+    g.gV = nullptr; g.gposV = nullptr; g.Vout = nullptr; g.cnt = cgather;
+    CRK_TRY((launch_hyd<GeoPass<true>, 128>(c, g, st, "gather count kernel")));
     AccPass<true> a;
     common(c, a);
+    a.jrows = P<float4>(c->gpos);
+    a.jpay = nullptr;
     a.grec = nullptr;
     a.cnt = csym;
-    return launch_hyd<AccPass<true>, HYD_CH>(c, a, st, "sym count kernel");
+    return launch_hyd<AccPass<true>, 128>(c, a, st, "sym count kernel");
 }
 
 }  // namespace crk

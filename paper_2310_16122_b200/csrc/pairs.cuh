@@ -1,16 +1,16 @@
-// pairs.cuh — the list-driven pair-kernel skeleton shared by every force pass.
+// pairs.cuh — the list-driven i-centric pair-kernel skeleton shared by the force passes.
 //
-// One CTA per i-leaf (a row of the CSR leaf-pair list).  The
-// CTA walks its row in chunks: all threads stage the particles of the next CH/JMAX
-// j-leaves (periodic shift applied, so every difference is exact, O1) into shared
-// memory; each warp then culls the staged candidates against the bounding box of
-// its own G i-particles (ballot + popc compaction) and copies the survivors'
-// positions (plus a payload index) into a warp-private buffer, which it then
-// evaluates with a 4x unrolled loop.  Lane l holds i-particle l % G and takes every
-// (32/G)-th survivor — the paper's half-warp layout (Fig.
-// half-warp-layout: lanes 0-15 / 16-31) generalised to 32/G j-slots, i-centric, with
-// register accumulation and one shuffle reduction over the slots at the end: no
-// atomics (SURVEY.md §7 "B200-idiomatic design").
+// One CTA per i-leaf (a row of the CSR leaf-pair list).  The CTA
+// copies its whole row — each j-leaf's packed position rows, payload rows and padded
+// bounding box — into shared memory with 1-D TMA bulk copies (cp.async.bulk completing
+// on one mbarrier; rows longer than ENT entries take several rounds).  After that single
+// wait every warp works on its own: a leaf-level prefilter (box-box distance to the
+// bounding box of its G i-particles), a particle-level filter (ballot + popc compaction
+// into a per-warp survivor ring) and the evaluation, in which lane l holds i-particle
+// l % G and takes every (32/G)-th survivor — the paper's half-warp layout (PAPER.md:418,
+// Fig. half-warp-layout: lanes 0-15 / 16-31) generalised to 32/G j-slots, i-centric,
+// register accumulation and one shuffle reduction over the slots at the end: no atomics.
+// Periodic shifts are added to the staged positions (exact, O1).
 #pragma once
 #include "common.cuh"
 
@@ -19,46 +19,45 @@ namespace crk {
 struct RowView {
     const int32_t* ifirst;
     const int32_t* icount;
-    const int32_t* jfirst;
-    const int32_t* jcount;
     const int32_t* row_off;
-    const int32_t* col;
-    const int8_t* shift;
-    const float* jbbox;   // 6 floats per j-leaf (lo xyz, hi xyz)
-    const float* jmaxh2;  // per j-leaf max H^2 (SYM passes)
+    const int2* erec;     // packed entries (first | (count-1) << 29, leaf | shift << 26)
+    const float4* box8;   // padded j-leaf boxes: (lo, max H^2), (hi, 0)
     float L[3];
 };
 
 // Pass concept:
-//   static constexpr int PAY;            payload float4 per staged j (after the position)
-//   static constexpr bool SYM;           culling radius also uses j's H^2 (jpos.w)
-//   static constexpr int UNROLL;         survivors per lane per loop iteration
+//   static constexpr int PAY;      payload float4 per j particle (contiguous rows in jpay)
+//   static constexpr bool SYM;     culling radius also uses j's H^2 (symmetric predicate)
+//   static constexpr int UNROLL;   survivors per lane per loop iteration
+//   const float4* jrows; const float4* jpay;   j position rows (x, y, z, w) / payload rows
 //   struct I; struct Acc;
 //   void init(Acc&); void load_i(int i, I&); float ix/iy/iz(const I&); float cut(const I&)
-//   void stage(int j, float ox, float oy, float oz, float4& jp, float4* pay)
-//   void pair(const I&, Acc&, const float4& jp, const float4* pay)
+//   float jcut(const float4& jp)   (SYM only: j's H^2 from its staged row)
+//   void pair(const I&, Acc&, const float4& jp, const float4* pay, int j)
 //   template<int G> void reduce(Acc&) ; void finish(int i, const I&, const Acc&)
-// Passes without payload copy the survivors' float4 into the warp list (one LDS.128 per
-// pair); passes with a payload keep a u16 index list (the payload stays in the tile).
-template <class Pass, int NW, int G, int CH>
+template <class Pass, int NW, int ENT>
 struct PairSmem {
-    static constexpr bool COPY = Pass::PAY == 0;
-    float4 jpos[CH];
-    float4 jpay[COPY ? 1 : CH * Pass::PAY];
-    float4 wpos[COPY ? NW : 1][COPY ? CH : 1];
-    uint16_t widx[COPY ? 1 : NW][COPY ? 1 : CH];
-    uint8_t went[NW][32];
-    float4 elo[CH / JMAX], ehi[CH / JMAX];  // shifted j-leaf boxes (.w of elo: max H^2)
+    static constexpr int RING = 64;
+    float4 raw[ENT * JMAX];
+    float4 pay[Pass::PAY > 0 ? ENT * JMAX * Pass::PAY : 1];
+    float4 ebox[ENT][2];
+    float4 eoff[ENT];  // shift offset (x, y, z), first (w, as int)
+    int ecnt[ENT];
+    uint64_t bar;
+    uint16_t went[NW][ENT];
+    float4 rpos[NW][RING];     // survivors: shifted position
+    uint16_t rslot[NW][RING];  // survivors: staged slot (payload, j index)
 };
 
-template <class Pass, int NW, int G, int CH, int MINB>
+template <class Pass, int NW, int G, int ENT, int MINB>
 __global__ void __launch_bounds__(NW * 32, MINB) pair_kernel(const Pass pass, const RowView rv) {
     static_assert(32 % G == 0, "G must divide the warp");
-    static_assert(CH % 32 == 0 && CH % JMAX == 0, "bad chunk");
+    static_assert(ENT * JMAX <= 65536, "slot index is 16 bits");
     constexpr int S = 32 / G;
-    constexpr bool HASPAY = Pass::PAY > 0;
-    using SM = PairSmem<Pass, NW, G, CH>;
-    __shared__ SM sm;
+    using SM = PairSmem<Pass, NW, ENT>;
+    constexpr int RING = SM::RING;
+    extern __shared__ __align__(128) unsigned char smem_raw[];
+    SM& sm = *reinterpret_cast<SM*>(smem_raw);
 
     const int a = blockIdx.x;
     const int ifirst = rv.ifirst[a];
@@ -70,15 +69,18 @@ __global__ void __launch_bounds__(NW * 32, MINB) pair_kernel(const Pass pass, co
     const int ibase = warp * G;
     const bool wactive = ibase < icount;
     const bool ivalid = ibase + il < icount;
-    float4* wpos = sm.wpos[SM::COPY ? warp : 0];
-    uint16_t* widx = sm.widx[SM::COPY ? 0 : warp];
-    uint8_t* went = sm.went[warp];
-    static_assert(CH / JMAX <= 32, "one lane per staged j-leaf");
+    float4* rpos = sm.rpos[warp];
+    uint16_t* rslot = sm.rslot[warp];
+    uint16_t* went = sm.went[warp];
 
+    if (threadIdx.x == 0) {
+        mbar_init(&sm.bar, 1);
+        mbar_fence_init();
+    }
     typename Pass::I is;
     typename Pass::Acc acc;
     pass.init(acc);
-    float lo[3], hi[3], wcut = 0.f;
+    float lo[3] = {0.f, 0.f, 0.f}, hi[3] = {0.f, 0.f, 0.f}, wcut = 0.f;
     if (wactive) {
         pass.load_i(ifirst + ibase + (ivalid ? il : 0), is);
         const float px = pass.ix(is), py = pass.iy(is), pz = pass.iz(is);
@@ -91,107 +93,123 @@ __global__ void __launch_bounds__(NW * 32, MINB) pair_kernel(const Pass pass, co
         wcut = warp_max(ivalid ? pass.cut(is) : 0.f) * CULL_SLACK;
     }
 
-    const int rbeg = rv.row_off[a], rend = rv.row_off[a + 1];
-    constexpr int EPC = CH / JMAX;  // entries per chunk
-    // chunk c takes the row entries c, c + nch, c + 2 nch, ...: every chunk samples the
-    // whole neighbourhood, so the warps' per-chunk work (and the barrier wait) balances
-    const int nch = (rend - rbeg + EPC - 1) / EPC;
-    for (int c = 0; c < nch; ++c) {
-        const int nent = (rend - rbeg - c + nch - 1) / nch;  // entries in this chunk
-        for (int t = threadIdx.x; t < CH; t += NW * 32) {
-            const int m = t / JMAX;
-            const int k = t % JMAX;
-            const int e = rbeg + c + m * nch;
-            bool ok = false;
-            int j = 0, code = 13, b = 0;
-            if (m < nent) {
-                b = __ldg(rv.col + e);
-                code = __ldg(rv.shift + e);
-                if (k < __ldg(rv.jcount + b)) {
-                    ok = true;
-                    j = __ldg(rv.jfirst + b) + k;
-                }
+    // evaluate ring survivors [rd, rd + n)
+    auto eval = [&](int rd, int n) {
+        constexpr int U = Pass::UNROLL;
+        int k = sl;
+#pragma unroll 1
+        for (; k + (U - 1) * S < n; k += U * S) {
+#pragma unroll
+            for (int u = 0; u < U; ++u) {
+                const int s = (rd + k + u * S) & (RING - 1);
+                const int t = rslot[s];
+                pass.pair(is, acc, rpos[s], sm.pay + t * Pass::PAY,
+                          __float_as_int(sm.eoff[t / JMAX].w) + t % JMAX);
             }
+        }
+#pragma unroll 1
+        for (; k < n; k += S) {
+            const int s = (rd + k) & (RING - 1);
+            const int t = rslot[s];
+            pass.pair(is, acc, rpos[s], sm.pay + t * Pass::PAY, __float_as_int(sm.eoff[t / JMAX].w) + t % JMAX);
+        }
+    };
+
+    int wr = 0, rd = 0;
+    uint32_t phase = 0;
+    const int rbeg = rv.row_off[a], rend = rv.row_off[a + 1];
+    for (int e0 = rbeg; e0 < rend; e0 += ENT) {
+        const int nent = min(ENT, rend - e0);
+        __syncthreads();  // barrier initialised / previous round consumed
+        for (int t = threadIdx.x; t < nent; t += NW * 32) {
+            int first, count, leaf, code;
+            unpack_entry(__ldg(rv.erec + e0 + t), first, count, leaf, code);
             int sx, sy, sz;
             decode_shift(code, sx, sy, sz);
-            const float ox = (float)sx * rv.L[0], oy = (float)sy * rv.L[1], oz = (float)sz * rv.L[2];
-            if (ok) {
-                pass.stage(j, ox, oy, oz, sm.jpos[t], sm.jpay + (HASPAY ? t * Pass::PAY : 0));
-            } else {
-                sm.jpos[t] = make_float4(INFINITY, INFINITY, INFINITY, 0.f);
-            }
-            if (k == 0 && m < nent) {
-                const float* bb = rv.jbbox + 6 * (int64_t)b;
-                sm.elo[m] = make_float4(__ldg(bb) + ox, __ldg(bb + 1) + oy, __ldg(bb + 2) + oz,
-                                        Pass::SYM ? __ldg(rv.jmaxh2 + b) * CULL_SLACK : 0.f);
-                sm.ehi[m] = make_float4(__ldg(bb + 3) + ox, __ldg(bb + 4) + oy, __ldg(bb + 5) + oz, 0.f);
-            }
+            sm.eoff[t] = make_float4((float)sx * rv.L[0], (float)sy * rv.L[1], (float)sz * rv.L[2],
+                                     __int_as_float(first));
+            sm.ecnt[t] = count;
+            const uint32_t pb = (uint32_t)count * 16u;
+            mbar_expect_tx(&sm.bar, pb * (1 + Pass::PAY) + 32u);
+            bulk_g2s(&sm.raw[t * JMAX], pass.jrows + first, pb, &sm.bar);
+            if (Pass::PAY > 0)
+                bulk_g2s(&sm.pay[t * JMAX * Pass::PAY], pass.jpay + (int64_t)first * Pass::PAY, pb * Pass::PAY,
+                         &sm.bar);
+            bulk_g2s(&sm.ebox[t][0], rv.box8 + 2 * (int64_t)leaf, 32u, &sm.bar);
         }
         __syncthreads();
+        if (threadIdx.x == 0) mbar_arrive(&sm.bar);
+        mbar_wait(&sm.bar, phase);
+        phase ^= 1u;
         if (wactive) {
-            // (1) leaf-level prefilter: one lane per staged j-leaf, box-box distance
-            bool ek = false;
-            if (lane < nent) {
-                const float4 bl = sm.elo[lane], bh = sm.ehi[lane];
-                const float gx = fmaxf(fmaxf(bl.x - hi[0], lo[0] - bh.x), 0.f);
-                const float gy = fmaxf(fmaxf(bl.y - hi[1], lo[1] - bh.y), 0.f);
-                const float gz = fmaxf(fmaxf(bl.z - hi[2], lo[2] - bh.z), 0.f);
-                const float d2 = fmaf(gz, gz, fmaf(gy, gy, gx * gx));
-                ek = d2 < (Pass::SYM ? fmaxf(wcut, bl.w) : wcut);
+            // (1) leaf prefilter
+            int nsurv = 0;
+            for (int e = lane; e - lane < nent; e += 32) {
+                bool ek = false;
+                if (e < nent) {
+                    const float4 o = sm.eoff[e];
+                    const float4 bl = sm.ebox[e][0], bh = sm.ebox[e][1];
+                    const float gx = fmaxf(fmaxf(bl.x + o.x - hi[0], lo[0] - bh.x - o.x), 0.f);
+                    const float gy = fmaxf(fmaxf(bl.y + o.y - hi[1], lo[1] - bh.y - o.y), 0.f);
+                    const float gz = fmaxf(fmaxf(bl.z + o.z - hi[2], lo[2] - bh.z - o.z), 0.f);
+                    const float d2 = fmaf(gz, gz, fmaf(gy, gy, gx * gx));
+                    ek = d2 < (Pass::SYM ? fmaxf(wcut, bl.w * CULL_SLACK) : wcut);
+                }
+                const unsigned em = __ballot_sync(0xffffffffu, ek);
+                if (ek) went[nsurv + __popc(em & ((1u << lane) - 1u))] = (uint16_t)e;
+                nsurv += __popc(em);
             }
-            const unsigned em = __ballot_sync(0xffffffffu, ek);
-            if (ek) went[__popc(em & ((1u << lane) - 1u))] = (uint8_t)lane;
-            const int nsurv = __popc(em);
             __syncwarp();
-            // (2) particle-level filter over the surviving leaves, 32/JMAX leaves per step
-            int cnt = 0;
+            // (2) particle filter into the survivor ring, evaluation whenever >= 32 wait
             for (int q0 = 0; q0 < nsurv; q0 += 32 / JMAX) {
                 const int qe = q0 + lane / JMAX;
-                const int t = (qe < nsurv ? went[qe] : 0) * JMAX + lane % JMAX;
-                float4 p = sm.jpos[t];
-                if (qe >= nsurv) p.x = INFINITY;
-                const float d2 = box_dist2(p.x, p.y, p.z, lo, hi);
-                const bool keep = d2 < (Pass::SYM ? fmaxf(wcut, p.w * CULL_SLACK) : wcut);
-                const unsigned m = __ballot_sync(0xffffffffu, keep);
+                const int kk = lane % JMAX;
+                const int e = went[qe < nsurv ? qe : 0];
+                const float4 o = sm.eoff[e];
+                const int t = e * JMAX + kk;
+                float4 p = sm.raw[t];
+                p.x += o.x; p.y += o.y; p.z += o.z;
+                bool keep = qe < nsurv && kk < sm.ecnt[e];
                 if (keep) {
-                    const int o = cnt + __popc(m & ((1u << lane) - 1u));
-                    if (SM::COPY) wpos[o] = p;
-                    else widx[o] = (uint16_t)t;
+                    const float d2 = box_dist2(p.x, p.y, p.z, lo, hi);
+                    keep = d2 < (Pass::SYM ? fmaxf(wcut, pass.jcut(p) * CULL_SLACK) : wcut);
                 }
-                cnt += __popc(m);
-            }
-            __syncwarp();
-            constexpr int U = Pass::UNROLL;
-            int k = sl;
-#pragma unroll 1
-            for (; k + (U - 1) * S < cnt; k += U * S) {
-#pragma unroll
-                for (int u = 0; u < U; ++u) {
-                    const int kk = k + u * S;
-                    if (SM::COPY) {
-                        pass.pair(is, acc, wpos[kk], sm.jpay);
-                    } else {
-                        const int t = widx[kk];
-                        pass.pair(is, acc, sm.jpos[t], sm.jpay + t * Pass::PAY);
-                    }
+                const unsigned msk = __ballot_sync(0xffffffffu, keep);
+                if (keep) {
+                    const int s = (wr + __popc(msk & ((1u << lane) - 1u))) & (RING - 1);
+                    rpos[s] = p;
+                    rslot[s] = (uint16_t)t;
+                }
+                wr += __popc(msk);
+                __syncwarp();
+                if (wr - rd >= 32) {
+                    eval(rd, 32);
+                    rd += 32;
+                    __syncwarp();
                 }
             }
-#pragma unroll 1
-            for (; k < cnt; k += S) {
-                if (SM::COPY) {
-                    pass.pair(is, acc, wpos[k], sm.jpay);
-                } else {
-                    const int t = widx[k];
-                    pass.pair(is, acc, sm.jpos[t], sm.jpay + t * Pass::PAY);
-                }
+            if (e0 + ENT < rend && wr > rd) {  // slots are restaged next round: flush the ring
+                eval(rd, wr - rd);
+                rd = wr;
+                __syncwarp();
             }
         }
-        __syncthreads();
     }
     if (wactive) {
+        if (wr > rd) eval(rd, wr - rd);
         pass.template reduce<G>(acc);
         if (ivalid && sl == 0) pass.finish(ifirst + ibase + il, is, acc);
     }
+}
+
+template <class Pass, int NW, int G, int ENT, int MINB>
+inline cudaError_t launch_pairs(const Pass& pass, const RowView& rv, int64_t nleaf, cudaStream_t st) {
+    const int smem = (int)sizeof(PairSmem<Pass, NW, ENT>);
+    cudaError_t e = cudaFuncSetAttribute(pair_kernel<Pass, NW, G, ENT, MINB>,
+                                         cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+    if (e != cudaSuccess) return e;
+    pair_kernel<Pass, NW, G, ENT, MINB><<<(unsigned)nleaf, NW * 32, smem, st>>>(pass, rv);
+    return cudaGetLastError();
 }
 
 }  // namespace crk
