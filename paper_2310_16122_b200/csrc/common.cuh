@@ -159,6 +159,11 @@ __device__ __forceinline__ void bulk_g2s(void* dst, const void* src, uint32_t by
                  "l"(src), "r"(bytes), "r"(smem_u32(bar))
                  : "memory");
 }
+// fire-and-forget vector atomic add (REDG.E.ADD.F32x4)
+__device__ __forceinline__ void red_add_v4(float4* p, float a, float b, float c, float d) {
+    asm volatile("red.global.add.v4.f32 [%0], {%1, %2, %3, %4};" ::"l"(p), "f"(a), "f"(b), "f"(c), "f"(d)
+                 : "memory");
+}
 // packed list entry: x = first | (count - 1) << 29, y = leaf | shift << 26
 __device__ __forceinline__ void unpack_entry(int2 r, int& first, int& count, int& leaf, int& code) {
     first = r.x & 0x1fffffff;

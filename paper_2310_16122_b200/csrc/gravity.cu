@@ -107,10 +107,6 @@ struct Smem {
 };
 }  // namespace symg
 
-__device__ __forceinline__ void red_add_v4(float4* p, float a, float b, float c) {
-    asm volatile("red.global.add.v4.f32 [%0], {%1, %2, %3, %4};" ::"l"(p), "f"(a), "f"(b), "f"(c), "f"(0.f)
-                 : "memory");
-}
 
 struct GravSymArgs {
     const float4* xm;
@@ -198,7 +194,7 @@ __global__ void __launch_bounds__(symg::NW * 32, 4) grav_sym_kernel(const GravSy
             by = fmaf(-wj, dy, by);
             bz = fmaf(-wj, dz, bz);
         }
-        if (lane < n) red_add_v4(A.acc + j, bx, by, bz);
+        if (lane < n) red_add_v4(A.acc + j, bx, by, bz, 0.f);
     };
 
     int wr = 0, rd = 0;  // ring write / read counters
@@ -273,7 +269,7 @@ __global__ void __launch_bounds__(symg::NW * 32, 4) grav_sym_kernel(const GravSy
 #pragma unroll
         for (int i = 0; i < G; ++i) {
             const float sx = warp_sum(ax[i]), sy = warp_sum(ay[i]), sz = warp_sum(az[i]);
-            if (lane == i && i < ng) red_add_v4(A.acc + gself + i, sx, sy, sz);
+            if (lane == i && i < ng) red_add_v4(A.acc + gself + i, sx, sy, sz, 0.f);
         }
     }
 }

@@ -510,6 +510,278 @@ struct AccPass : HydCommon {
     }
 };
 
+// ============================================================== a7 + a8, symmetric (Newton-3) variant
+// Every unordered gas pair is evaluated once (G_ij, Q_ij, the limiter and the pressure
+// terms are shared by both sides): by the warp of the lower 8-particle group (groups are
+// contiguous gas-rank ranges, so "j in this or a later group" is j >= gself).  Lanes own
+// the j-survivors and loop over the group's 8 i-records (shared-memory broadcast); the
+// i-side sums (a, du/dt) stay in registers and are reduced once; the j-side reactions
+// go to a float4 (a, du/dt) accumulator with red.global.add.v4.f32.  Inside the own group
+// the pair is met from both sides, so there only the survivor's half counts.
+// Row staging: TMA bulk copies of gpos rows, accel records and leaf boxes (one mbarrier).
+
+// F = V_a V_b (P_a + P_b + Q_ab) G_ab,  Ea = V_a V_b (P_a + Q/2) v_ab.G_ab,  Eb likewise with P_b
+// (x = x_a - x_b; m_a dv_a/dt gets -F, m_b dv_b/dt gets +F; m_a du_a/dt gets Ea, m_b du_b/dt Eb)
+__device__ __forceinline__ void pair_terms(const Rec& A, const Rec& B, const float x[3], float r2, float Cl,
+                                           float Cq, float e2, float F[3], float& Ea, float& Eb) {
+    const float r = sqrtf(r2);
+    float ga[3], gb[3];
+    grad_wr(&A.Ah, A.dAh, A.B, A.dB, A.invH, r, x, ga);
+    const float xm[3] = {-x[0], -x[1], -x[2]};
+    grad_wr(&B.Ah, B.dAh, B.B, B.dB, B.invH, r, xm, gb);
+    float G[3], gva[3], gvb[3];
+#pragma unroll
+    for (int g = 0; g < 3; ++g) G[g] = 0.5f * (ga[g] - gb[g]);
+#pragma unroll
+    for (int p = 0; p < 3; ++p) {
+        gva[p] = A.dv[3 * p] * x[0] + A.dv[3 * p + 1] * x[1] + A.dv[3 * p + 2] * x[2];
+        gvb[p] = B.dv[3 * p] * x[0] + B.dv[3 * p + 1] * x[1] + B.dv[3 * p + 2] * x[2];
+    }
+    const float xga = x[0] * gva[0] + x[1] * gva[1] + x[2] * gva[2];
+    const float xgb = x[0] * gvb[0] + x[1] * gvb[1] + x[2] * gvb[2];
+    const float pr = xga * xgb, sm = xga + xgb;
+    const float phi = pr > 0.f ? fminf(1.f, 4.f * pr / (sm * sm)) : 0.f;
+    float vab[3], vs[3];
+#pragma unroll
+    for (int p = 0; p < 3; ++p) {
+        vab[p] = A.v[p] - B.v[p];
+        vs[p] = vab[p] - 0.5f * phi * (gva[p] + gvb[p]);
+    }
+    const float vsx = vs[0] * x[0] + vs[1] * x[1] + vs[2] * x[2];
+    const float mua = fminf(0.f, vsx * A.invH / fmaf(r2, A.invH * A.invH, e2));
+    const float mub = fminf(0.f, vsx * B.invH / fmaf(r2, B.invH * B.invH, e2));
+    const float Q = A.rho * mua * (Cq * mua - Cl * A.cs) + B.rho * mub * (Cq * mub - Cl * B.cs);
+    const float VV = A.V * B.V;
+    const float PQ = VV * (A.P + B.P + Q);
+    F[0] = PQ * G[0];
+    F[1] = PQ * G[1];
+    F[2] = PQ * G[2];
+    const float vG = vab[0] * G[0] + vab[1] * G[1] + vab[2] * G[2];
+    Ea = VV * (A.P + 0.5f * Q) * vG;
+    Eb = VV * (B.P + 0.5f * Q) * vG;
+}
+
+namespace syma {
+constexpr int NW = 8, G = 8, ENT = 56, RING = 64, REC = 9;
+struct Smem {
+    float4 raw[ENT * JMAX];
+    float4 pay[ENT * JMAX * REC];
+    float4 ebox[ENT][2];
+    float4 eoff[ENT];
+    int ecnt[ENT];
+    uint64_t bar;
+    uint16_t went[NW][ENT];
+    float4 rpos[NW][RING];
+    uint16_t rslot[NW][RING];
+    float4 ipos[NW][G];
+    float4 irec[NW][G][REC];
+};
+}  // namespace syma
+
+struct AccSymArgs {
+    const float4* gpos;
+    const float4* grec;
+    const int32_t* ifirst;
+    const int32_t* icount;
+    const int32_t* row_off;
+    const int2* erec;
+    const float4* box8;
+    float4* acc;  // (a, du/dt) per gas rank
+    float L[3];
+    float Cl, Cq, e2;
+};
+
+__global__ void __launch_bounds__(syma::NW * 32, 2) acc_sym_kernel(const AccSymArgs A) {
+    using namespace syma;
+    extern __shared__ __align__(128) unsigned char smem_raw[];
+    Smem& sm = *reinterpret_cast<Smem*>(smem_raw);
+    const int a = blockIdx.x;
+    const int ifirst = A.ifirst[a];
+    const int icount = A.icount[a];
+    const int warp = threadIdx.x >> 5;
+    const int lane = threadIdx.x & 31;
+    const int ibase = warp * G;
+    const bool wactive = ibase < icount;
+    const int gself = ifirst + ibase;
+    const int ng = min(G, icount - ibase);
+    float4* rpos = sm.rpos[warp];
+    uint16_t* rslot = sm.rslot[warp];
+    uint16_t* went = sm.went[warp];
+
+    if (threadIdx.x == 0) {
+        mbar_init(&sm.bar, 1);
+        mbar_fence_init();
+    }
+    float lo[3] = {0.f, 0.f, 0.f}, hi[3] = {0.f, 0.f, 0.f}, wcut = 0.f;
+    if (wactive) {
+        const bool iv = lane < ng;
+        float4 p = make_float4(-1e18f, -1e18f, -1e18f, 1.f);
+        if (iv) p = A.gpos[gself + lane];
+        if (lane < G) sm.ipos[warp][lane] = p;
+        for (int t = lane; t < G * REC; t += 32) {
+            const int i = t / REC;
+            sm.irec[warp][i][t % REC] = i < ng ? A.grec[(int64_t)(gself + i) * REC + t % REC]
+                                               : make_float4(0.f, 0.f, 0.f, 0.f);
+        }
+        lo[0] = warp_min(iv ? p.x : INFINITY);
+        lo[1] = warp_min(iv ? p.y : INFINITY);
+        lo[2] = warp_min(iv ? p.z : INFINITY);
+        hi[0] = warp_max(iv ? p.x : -INFINITY);
+        hi[1] = warp_max(iv ? p.y : -INFINITY);
+        hi[2] = warp_max(iv ? p.z : -INFINITY);
+        wcut = warp_max(iv ? __fmul_rn(p.w, p.w) : 0.f) * CULL_SLACK;
+    }
+    float ia[G][4];
+#pragma unroll
+    for (int i = 0; i < G; ++i) ia[i][0] = ia[i][1] = ia[i][2] = ia[i][3] = 0.f;
+    const float Cl = A.Cl, Cq = A.Cq, e2 = A.e2;
+
+    auto eval_step = [&](int r0, int n) {
+        float4 jp = make_float4(1e18f, 1e18f, 1e18f, 1.f);
+        int t = 0;
+        const bool valid = lane < n;
+        if (valid) {
+            const int s = (r0 + lane) & (RING - 1);
+            jp = rpos[s];
+            t = rslot[s];
+        }
+        Rec rj;
+        unpack_rec(sm.pay + t * REC, rj);
+        const int j = __float_as_int(sm.eoff[t / JMAX].w) + t % JMAX;
+        const bool own = j >= gself && j < gself + ng;  // own group: j-side only
+        const float h2j = __fmul_rn(jp.w, jp.w);
+        float bj[4] = {0.f, 0.f, 0.f, 0.f};
+#pragma unroll
+        for (int i = 0; i < G; ++i) {
+            const float4 ip = sm.ipos[warp][i];
+            Rec ri;
+            unpack_rec(sm.irec[warp][i], ri);
+            const float x[3] = {ip.x - jp.x, ip.y - jp.y, ip.z - jp.z};  // x_ij
+            const float r2 = s32_of(x[0], x[1], x[2]);
+            const bool in = valid && r2 < fmaxf(ri.H2, h2j);
+            float F[3], Ei, Ej;
+            pair_terms(ri, rj, x, r2, Cl, Cq, e2, F, Ei, Ej);
+            const bool side_i = in && !own;
+            ia[i][0] -= side_i ? F[0] : 0.f;
+            ia[i][1] -= side_i ? F[1] : 0.f;
+            ia[i][2] -= side_i ? F[2] : 0.f;
+            ia[i][3] += side_i ? Ei : 0.f;
+            bj[0] += in ? F[0] : 0.f;
+            bj[1] += in ? F[1] : 0.f;
+            bj[2] += in ? F[2] : 0.f;
+            bj[3] += in ? Ej : 0.f;
+        }
+        if (valid) {
+            const float im = 1.f / rj.m;
+            red_add_v4(A.acc + j, bj[0] * im, bj[1] * im, bj[2] * im, bj[3] * im);
+        }
+    };
+
+    int wr = 0, rd = 0;
+    uint32_t phase = 0;
+    const int rbeg = A.row_off[a], rend = A.row_off[a + 1];
+    for (int e0 = rbeg; e0 < rend; e0 += ENT) {
+        const int nent = min(ENT, rend - e0);
+        __syncthreads();
+        for (int t = threadIdx.x; t < nent; t += NW * 32) {
+            int first, count, leaf, code;
+            unpack_entry(__ldg(A.erec + e0 + t), first, count, leaf, code);
+            int sx, sy, sz;
+            decode_shift(code, sx, sy, sz);
+            sm.eoff[t] = make_float4((float)sx * A.L[0], (float)sy * A.L[1], (float)sz * A.L[2], __int_as_float(first));
+            sm.ecnt[t] = count;
+            const uint32_t pb = (uint32_t)count * 16u;
+            mbar_expect_tx(&sm.bar, pb * (1 + REC) + 32u);
+            bulk_g2s(&sm.raw[t * JMAX], A.gpos + first, pb, &sm.bar);
+            bulk_g2s(&sm.pay[t * JMAX * REC], A.grec + (int64_t)first * REC, pb * REC, &sm.bar);
+            bulk_g2s(&sm.ebox[t][0], A.box8 + 2 * (int64_t)leaf, 32u, &sm.bar);
+        }
+        __syncthreads();
+        if (threadIdx.x == 0) mbar_arrive(&sm.bar);
+        mbar_wait(&sm.bar, phase);
+        phase ^= 1u;
+        if (wactive) {
+            int nsurv = 0;
+            for (int e = lane; e - lane < nent; e += 32) {
+                bool ek = false;
+                if (e < nent) {
+                    const float4 o = sm.eoff[e];
+                    const float4 bl = sm.ebox[e][0], bh = sm.ebox[e][1];
+                    const float gx = fmaxf(fmaxf(bl.x + o.x - hi[0], lo[0] - bh.x - o.x), 0.f);
+                    const float gy = fmaxf(fmaxf(bl.y + o.y - hi[1], lo[1] - bh.y - o.y), 0.f);
+                    const float gz = fmaxf(fmaxf(bl.z + o.z - hi[2], lo[2] - bh.z - o.z), 0.f);
+                    ek = fmaf(gz, gz, fmaf(gy, gy, gx * gx)) < fmaxf(wcut, bl.w * CULL_SLACK) &&
+                         __float_as_int(o.w) + sm.ecnt[e] > gself;
+                }
+                const unsigned em = __ballot_sync(0xffffffffu, ek);
+                if (ek) went[nsurv + __popc(em & ((1u << lane) - 1u))] = (uint16_t)e;
+                nsurv += __popc(em);
+            }
+            __syncwarp();
+            for (int q0 = 0; q0 < nsurv; q0 += 32 / JMAX) {
+                const int qe = q0 + lane / JMAX;
+                const int kk = lane % JMAX;
+                const int e = went[qe < nsurv ? qe : 0];
+                const float4 o = sm.eoff[e];
+                const int t = e * JMAX + kk;
+                float4 p = sm.raw[t];
+                p.x += o.x; p.y += o.y; p.z += o.z;
+                const int j = __float_as_int(o.w) + kk;
+                const bool keep = qe < nsurv && kk < sm.ecnt[e] && j >= gself &&
+                                  box_dist2(p.x, p.y, p.z, lo, hi) < fmaxf(wcut, __fmul_rn(p.w, p.w) * CULL_SLACK);
+                const unsigned msk = __ballot_sync(0xffffffffu, keep);
+                if (keep) {
+                    const int s = (wr + __popc(msk & ((1u << lane) - 1u))) & (RING - 1);
+                    rpos[s] = p;
+                    rslot[s] = (uint16_t)t;
+                }
+                wr += __popc(msk);
+                __syncwarp();
+                if (wr - rd >= 32) {
+                    eval_step(rd, 32);
+                    rd += 32;
+                    __syncwarp();
+                }
+            }
+            if (e0 + ENT < rend && wr > rd) {  // slots are restaged next round: flush
+                eval_step(rd, wr - rd);
+                rd = wr;
+                __syncwarp();
+            }
+        }
+    }
+    if (wactive) {
+        if (wr > rd) eval_step(rd, wr - rd);
+#pragma unroll
+        for (int i = 0; i < G; ++i) {
+            const float s0 = warp_sum(ia[i][0]), s1 = warp_sum(ia[i][1]), s2 = warp_sum(ia[i][2]),
+                        s3 = warp_sum(ia[i][3]);
+            if (lane == i && i < ng) {
+                const float im = 1.f / sm.irec[warp][i][8].z;  // 1 / m_i
+                red_add_v4(A.acc + gself + i, s0 * im, s1 * im, s2 * im, s3 * im);
+            }
+        }
+    }
+}
+
+// caller outputs and kicks from the (a, du/dt) accumulator (gas-rank order)
+__global__ void k_acc_finish(int64_t ng, const float4* __restrict__ acc, const int32_t* __restrict__ gas_idx, float dt,
+                             float* ahx, float* ahy, float* ahz, float* dudt, float* vx, float* vy, float* vz,
+                             float* u) {
+    const int64_t k = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+    if (k >= ng) return;
+    const float4 q = acc[k];
+    const int64_t i = gas_idx[k];
+    if (ahx) { ahx[i] = q.x; ahy[i] = q.y; ahz[i] = q.z; }
+    if (dudt) dudt[i] = q.w;
+    if (dt != 0.f) {
+        vx[i] = fmaf(dt, q.x, vx[i]);
+        vy[i] = fmaf(dt, q.y, vy[i]);
+        vz[i] = fmaf(dt, q.z, vz[i]);
+        u[i] = fmaf(dt, q.w, u[i]);
+    }
+}
+
 // ============================================================== launches
 static RowView hydro_rows(crk_ctx* c) {
     RowView rv;
@@ -589,8 +861,40 @@ crk_status extras(crk_ctx* c, crk_particles* p, cudaStream_t st) {
     return launch_hyd<ExtPass, 128, 3>(c, g, st, "extras kernel");
 }
 
+static crk_status accel_sym(crk_ctx* c, crk_particles* p, float dt, cudaStream_t st) {
+    const int64_t ng = c->n_gas;
+    CRK_TRY(grow(c, c->gacc, (ng > 0 ? ng : 1) * 16, st));
+    CRK_TRY(cuda_check(c, cudaMemsetAsync(c->gacc.p, 0, (ng > 0 ? ng : 1) * 16, st), "memset"));
+    if (c->nleaf[2] > 0) {
+        AccSymArgs A;
+        A.gpos = P<float4>(c->gpos);
+        A.grec = P<float4>(c->grec);
+        A.ifirst = P<int32_t>(c->lfirst[2]);
+        A.icount = P<int32_t>(c->lcount[2]);
+        A.row_off = P<int32_t>(c->rowoff[1]);
+        A.erec = P<int2>(c->erec[1]);
+        A.box8 = P<float4>(c->lbox8[3]);
+        A.acc = P<float4>(c->gacc);
+        for (int d = 0; d < 3; ++d) A.L[d] = c->lay.L[d];
+        A.Cl = c->prm.av_cl; A.Cq = c->prm.av_cq; A.e2 = c->prm.av_eps2;
+        const int smem = (int)sizeof(syma::Smem);
+        cudaError_t e = cudaFuncSetAttribute(acc_sym_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+        if (e != cudaSuccess) return cuda_check(c, e, "smem attribute");
+        acc_sym_kernel<<<(unsigned)c->nleaf[2], syma::NW * 32, smem, st>>>(A);
+        CRK_LAUNCHED(c, "accel/dudt (symmetric) kernel");
+    }
+    if (ng > 0) {
+        k_acc_finish<<<(unsigned)((ng + 255) / 256), 256, 0, st>>>(ng, P<float4>(c->gacc), P<int32_t>(c->gas_idx), dt,
+                                                                   p->ahx, p->ahy, p->ahz, p->dudt, p->vx, p->vy,
+                                                                   p->vz, p->u);
+        CRK_LAUNCHED(c, "accel finish");
+    }
+    return CRK_OK;
+}
+
 crk_status accel_dudt(crk_ctx* c, crk_particles* p, float dt, cudaStream_t st) {
     if (dt != 0.f && (!p->vx || !p->vy || !p->vz || !p->u)) return fail(c, CRK_EINVAL, "kick needs v and u");
+    if (c->prm.symmetric) return accel_sym(c, p, dt, st);
     AccPass<false> g;
     common(c, g);
     g.jrows = P<float4>(c->gpos);
