@@ -202,6 +202,8 @@ def main():
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--dt", type=float, default=0.0)
+    ap.add_argument("--symmetric", type=int, default=None,
+                    help="kernel variant bitmask: 1 = Newton-3 gravity, 2 = Newton-3 accel (default: library default)")
     args = ap.parse_args()
     args.warmup = max(args.warmup, 3) if args.impl == "ours" else args.warmup
 
@@ -218,6 +220,8 @@ def main():
 
     t0 = time.perf_counter()
     parts, params = make_config(args.config)
+    if args.symmetric is not None:
+        params["symmetric"] = args.symmetric
     gen_s = time.perf_counter() - t0
 
     if args.impl == "reference":

@@ -56,9 +56,10 @@ typedef struct crk_params {
     int32_t leaf_max_gas_i;  /* gas i-leaf size: 16, 32 or 64 */
     int32_t leaf_max_gas_j;  /* gas j-leaf size: 8 */
     double cell_side;    /* chaining-mesh cell side (power of two, <= box/4) */
-    int32_t symmetric;   /* 1: evaluate each unordered pair once (Newton's third law), reactions
-                            added with float atomics (summation order varies run to run);
-                            0: i-centric, every ordered pair, bit-reproducible */
+    int32_t symmetric;   /* bitmask, 0 = every kernel i-centric (each ordered pair evaluated by
+                            its i, bit-reproducible); bit 0: gravity, bit 1: accel/du-dt evaluate
+                            each unordered pair once (Newton's third law) and add the reactions
+                            with float atomics (summation order varies run to run) */
 } crk_params;
 
 /* Caller-owned particle arrays (device pointers).  Inputs are sorted IN PLACE by

@@ -63,7 +63,7 @@ def test_sort_leaves_lists_bit_exact(name):
             assert np.array_equal(x[0], y[0]) and np.array_equal(x[1], y[1]), (m, a)
 
 
-@pytest.mark.parametrize("name,sym", [("c1", 1), ("c1", 0), ("lat:32,16,16:0.1:3", 1), ("c2u", 1), ("c2z", 1),
+@pytest.mark.parametrize("name,sym", [("c1", 3), ("c1", 0), ("lat:32,16,16:0.1:3", 3), ("c2u", 0), ("c2z", 3),
                                       ("c2z", 0)])
 def test_counts_and_full_chain(name, sym):
     parts, params = cached_config(name)
@@ -96,7 +96,7 @@ def test_counts_and_full_chain(name, sym):
     assert norm_err(gi["dudt"][T], ref["dudt"], ref["Sdu"]) <= TOL_FORCE
 
 
-@pytest.mark.parametrize("sym", [1, 0])
+@pytest.mark.parametrize("sym", [3, 0])
 def test_kicks(sym):
     parts, params = cached_config("c1")
     params["symmetric"] = sym
