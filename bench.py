@@ -313,6 +313,14 @@ def main():
     flops = {k: pass_pairs[k] * FLOP_PER_PAIR[k] for k in pass_pairs}
     dom = max(pass_pairs, key=lambda k: pass_ms[k])
     achieved = flops[dom] / (pass_ms[dom] * 1e-3) / 1e12
+    traffic = None
+    try:  # dram bytes per launch of the same kernel from the committed ncu --set full capture
+        with open(os.path.join(ROOT, "profiles", "r01", "ncu_traffic.json")) as f:
+            tk = json.load(f)["kernels"].get(dom)
+        if tk and args.config == "c4":
+            traffic = tk["dram_bytes"]
+    except Exception:
+        pass
     useful_tf = sum(flops.values()) / (ms_step * 1e-3) / 1e12
 
     # e2e through the public API with host buffers (pinned), H2D + D2H inside the timed region
@@ -363,7 +371,8 @@ def main():
             "pairs": pairs, "pair_interactions_per_step": pair_int,
             "useful_fp32_tflops": useful_tf, "useful_fp32_frac_of_peak": useful_tf / peak_tf,
             "roofline": {"bound": "alu", "kernel": dom, "achieved": achieved, "peak": peak_tf, "unit": "TFLOP/s",
-                         "frac": achieved / peak_tf, "traffic": None,
+                         "frac": achieved / peak_tf, "traffic": traffic,
+                         "traffic_source": "profiles/r01/ncu_traffic.json (dram__bytes_read+write, one launch)",
                          "peak_basis": f"{n_sm} SMs x 128 FP32 lanes x 2 x {f_max:.0f} MHz (sm_max_mhz, MEASURED_PEAKS.json)"},
             "clocks": clk.summary(),
             "e2e": e2e,
