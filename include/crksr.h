@@ -60,6 +60,11 @@ typedef struct crk_params {
                             its i, bit-reproducible); bit 0: gravity, bit 1: accel/du-dt evaluate
                             each unordered pair once (Newton's third law) and add the reactions
                             with float atomics (summation order varies run to run) */
+    int32_t dom_lo[3], dom_hi[3];  /* owned chaining-mesh cells [dom_lo, dom_hi) per axis (3-D domain
+                                      decomposition); all-zero dom_hi = whole box.
+                                      With a partial domain, i-leaves (and so every output) exist
+                                      only for owned cells; particles in other cells are ghosts
+                                      (j-side only) and the kernels run i-centric. */
 } crk_params;
 
 /* Caller-owned particle arrays (device pointers).  Inputs are sorted IN PLACE by
@@ -140,6 +145,38 @@ crk_status crk_hydro_accel_dudt(struct crk_ctx* ctx, crk_particles* parts, float
  * Outputs are device int32 arrays of length n in sorted order.  Needs build_lists. */
 crk_status crk_count_pairs(struct crk_ctx* ctx, crk_particles* parts, int32_t* cgrav,
                            int32_t* cgather, int32_t* csym, void* stream);
+
+/* ---- ghost exchange support ----
+ * Cell masks are HOST arrays of ncell[a] bytes per axis; a particle is selected iff its
+ * cell (cx, cy, cz) has mask_x[cx] && mask_y[cy] && mask_z[cz].  Selections preserve
+ * order.  These calls synchronise `stream` (the count sizes the messages). */
+
+/* Indices (into the given x/y/z arrays, length n) of particles in the masked cells;
+ * gas_only != 0 restricts to species == 1.  idx_out: device, capacity n. */
+crk_status crk_select_cells(struct crk_ctx* ctx, const float* x, const float* y, const float* z,
+                            const uint8_t* species, int gas_only, int64_t n, const uint8_t* mask_x,
+                            const uint8_t* mask_y, const uint8_t* mask_z, int32_t* idx_out,
+                            int64_t* count_out, void* stream);
+
+/* Gas ranks (ascending) of the gas particles in the masked cells, after crk_build_lists:
+ * the same cells give the same particles in the same (key) order on every rank. */
+crk_status crk_select_gas(struct crk_ctx* ctx, const uint8_t* mask_x, const uint8_t* mask_y,
+                          const uint8_t* mask_z, int32_t* idx_out, int64_t* count_out, void* stream);
+
+/* R1: pack / unpack whole particles as 48-byte records (x y z vx vy vz m H u, species,
+ * id).  unpack writes records [0, n) to parts entries [offset, offset + n). */
+crk_status crk_pack_particles(struct crk_ctx* ctx, const crk_particles* parts, const int32_t* idx,
+                              int64_t n, void* out, void* stream);
+crk_status crk_unpack_particles(struct crk_ctx* ctx, crk_particles* parts, int64_t offset, int64_t n,
+                                const void* in, void* stream);
+
+/* R2 / R3: pack / unpack per-gas-rank state.  what = 0: volume V (4 bytes; updates the
+ * V column of the corrections/extras j-rows), what = 1: the accel record of a7/a8
+ * (144 bytes).  Call R2 after crk_geometry, R3 after crk_extras. */
+crk_status crk_pack_gas(struct crk_ctx* ctx, int what, const int32_t* idx, int64_t n, void* out,
+                        void* stream);
+crk_status crk_unpack_gas(struct crk_ctx* ctx, int what, const int32_t* idx, int64_t n, const void* in,
+                          void* stream);
 
 /* Device views of leaves and lists (after crk_build_lists). */
 crk_status crk_list_view(struct crk_ctx* ctx, crk_lists* out);

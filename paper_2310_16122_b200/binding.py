@@ -19,7 +19,8 @@ STATUS = {0: "CRK_OK", -1: "CRK_EINVAL", -2: "CRK_ENOMEM", -3: "CRK_ECUDA", -4: 
 # exported symbols declared in include/crksr.h (tests check the .so exports all of them)
 EXPORTS = ["crk_create", "crk_destroy", "crk_build_lists", "crk_gravity_kick", "crk_geometry",
            "crk_corrections", "crk_extras", "crk_hydro_accel_dudt", "crk_count_pairs", "crk_list_view",
-           "crk_launch_count", "crk_status_string", "crk_last_error"]
+           "crk_launch_count", "crk_status_string", "crk_last_error", "crk_select_cells", "crk_select_gas",
+           "crk_pack_particles", "crk_unpack_particles", "crk_pack_gas", "crk_unpack_gas"]
 
 
 class CrkError(RuntimeError):
@@ -37,6 +38,7 @@ class CrkParams(C.Structure):
         ("leaf_max_gas_i", C.c_int32), ("leaf_max_gas_j", C.c_int32),
         ("cell_side", C.c_double),
         ("symmetric", C.c_int32),
+        ("dom_lo", C.c_int32 * 3), ("dom_hi", C.c_int32 * 3),
     ]
 
 
@@ -84,8 +86,17 @@ def lib():
         L.crk_status_string.restype = C.c_char_p
         L.crk_last_error.argtypes = [vp]
         L.crk_last_error.restype = C.c_char_p
+        L.crk_select_cells.argtypes = [vp, vp, vp, vp, vp, C.c_int, C.c_int64, C.c_char_p, C.c_char_p, C.c_char_p,
+                                       vp, C.POINTER(C.c_int64), vp]
+        L.crk_select_gas.argtypes = [vp, C.c_char_p, C.c_char_p, C.c_char_p, vp, C.POINTER(C.c_int64), vp]
+        L.crk_pack_particles.argtypes = [vp, C.POINTER(CrkParticles), vp, C.c_int64, vp, vp]
+        L.crk_unpack_particles.argtypes = [vp, C.POINTER(CrkParticles), C.c_int64, C.c_int64, vp, vp]
+        L.crk_pack_gas.argtypes = [vp, C.c_int, vp, C.c_int64, vp, vp]
+        L.crk_unpack_gas.argtypes = [vp, C.c_int, vp, C.c_int64, vp, vp]
         for f in ("crk_create", "crk_destroy", "crk_build_lists", "crk_gravity_kick", "crk_geometry",
-                  "crk_corrections", "crk_extras", "crk_hydro_accel_dudt", "crk_count_pairs", "crk_list_view"):
+                  "crk_corrections", "crk_extras", "crk_hydro_accel_dudt", "crk_count_pairs", "crk_list_view",
+                  "crk_select_cells", "crk_select_gas", "crk_pack_particles", "crk_unpack_particles",
+                  "crk_pack_gas", "crk_unpack_gas"):
             getattr(L, f).restype = C.c_int
         _lib = L
     return _lib
@@ -100,6 +111,8 @@ def params_struct(p: dict) -> CrkParams:
     for k in ("leaf_max_i", "leaf_max_j", "leaf_max_gas_i", "leaf_max_gas_j"):
         setattr(s, k, p[k])
     s.symmetric = int(p.get("symmetric", 1))
+    s.dom_lo[:] = list(p.get("dom_lo", (0, 0, 0)))
+    s.dom_hi[:] = list(p.get("dom_hi", (0, 0, 0)))
     return s
 
 
@@ -244,6 +257,56 @@ class Solver:
                                           C.c_void_p(ch.data_ptr()), C.c_void_p(cs.data_ptr()),
                                           self._stream(stream)), self.ctx)
         return cg, ch, cs
+
+    # ---- ghost exchange (a9) ----
+    @staticmethod
+    def _mask(m):
+        import numpy as np
+
+        return np.ascontiguousarray(m, dtype=np.uint8).tobytes()
+
+    def select_cells(self, parts, masks, gas_only=False, n=None, stream=None):
+        """Indices (device int32) of parts[:n] in the masked cells (masks: 3 uint8 arrays)."""
+        n = parts.n if n is None else n
+        out = torch.empty(max(n, 1), dtype=torch.int32, device=parts.device)
+        cnt = C.c_int64()
+        mx, my, mz = (self._mask(m) for m in masks)
+        self._check(lib().crk_select_cells(self.ctx, C.c_void_p(parts.x.data_ptr()), C.c_void_p(parts.y.data_ptr()),
+                                           C.c_void_p(parts.z.data_ptr()), C.c_void_p(parts.species.data_ptr()),
+                                           int(gas_only), n, mx, my, mz, C.c_void_p(out.data_ptr()), C.byref(cnt),
+                                           self._stream(stream)), self.ctx)
+        return out[: cnt.value]
+
+    def select_gas(self, masks, device, stream=None, n_gas=None):
+        out = torch.empty(max(int(n_gas or 1), 1), dtype=torch.int32, device=device)
+        cnt = C.c_int64()
+        mx, my, mz = (self._mask(m) for m in masks)
+        self._check(lib().crk_select_gas(self.ctx, mx, my, mz, C.c_void_p(out.data_ptr()), C.byref(cnt),
+                                         self._stream(stream)), self.ctx)
+        return out[: cnt.value]
+
+    def pack_particles(self, parts, idx, stream=None):
+        out = torch.empty((idx.numel(), 12), dtype=torch.float32, device=parts.device)
+        ps = parts.struct()
+        self._check(lib().crk_pack_particles(self.ctx, C.byref(ps), C.c_void_p(idx.data_ptr()), idx.numel(),
+                                             C.c_void_p(out.data_ptr()), self._stream(stream)), self.ctx)
+        return out
+
+    def unpack_particles(self, parts, offset, buf, stream=None):
+        ps = parts.struct()
+        self._check(lib().crk_unpack_particles(self.ctx, C.byref(ps), int(offset), buf.shape[0],
+                                               C.c_void_p(buf.data_ptr()), self._stream(stream)), self.ctx)
+
+    def pack_gas(self, what, idx, stream=None):
+        w = 1 if what == 0 else 36
+        out = torch.empty((idx.numel(), w), dtype=torch.float32, device=idx.device)
+        self._check(lib().crk_pack_gas(self.ctx, int(what), C.c_void_p(idx.data_ptr()), idx.numel(),
+                                       C.c_void_p(out.data_ptr()), self._stream(stream)), self.ctx)
+        return out
+
+    def unpack_gas(self, what, idx, buf, stream=None):
+        self._check(lib().crk_unpack_gas(self.ctx, int(what), C.c_void_p(idx.data_ptr()), idx.numel(),
+                                         C.c_void_p(buf.data_ptr()), self._stream(stream)), self.ctx)
 
     def launch_count(self) -> int:
         return int(lib().crk_launch_count(self.ctx))

@@ -85,6 +85,14 @@ static crk_status validate(const crk_params* p, Layout& L, std::string& why) {
     L.fbits = (32 - 3 * L.cbits) / 3;  // 32-bit sort keys (DESIGN.md §2 O3)
     if (L.fbits > L.cs) L.fbits = L.cs;
     L.ncm = (int64_t)1 << (3 * L.cbits);
+    bool whole = p->dom_hi[0] == 0 && p->dom_hi[1] == 0 && p->dom_hi[2] == 0;
+    L.partial = false;
+    for (int a = 0; a < 3; ++a) {
+        L.dlo[a] = whole ? 0 : p->dom_lo[a];
+        L.dhi[a] = whole ? L.ncell[a] : p->dom_hi[a];
+        if (L.dlo[a] < 0 || L.dhi[a] > L.ncell[a] || L.dlo[a] >= L.dhi[a]) { why = "bad domain cell range"; return CRK_EINVAL; }
+        if (L.dlo[a] != 0 || L.dhi[a] != L.ncell[a]) L.partial = true;
+    }
     return CRK_OK;
 }
 
@@ -128,7 +136,7 @@ crk_status crk_destroy(crk_ctx* c) {
     Buf* bufs[] = {&c->keys_a, &c->keys_b, &c->idx_a, &c->idx_b, &c->cub_tmp, &c->scratch, &c->xm,
                    &c->cell_start, &c->cell_end, &c->leaf_cnt, &c->gflag, &c->grank, &c->gas_idx,
                    &c->dev_scalars, &c->gpos, &c->gvel, &c->gV, &c->gcoef, &c->grec, &c->gu,
-                   &c->gacc, &c->gkey, &c->gposV};
+                   &c->gacc, &c->gkey, &c->gposV, &c->sel_flag, &c->sel_mask};
     for (Buf* b : bufs)
         if (b->p) cudaFree(b->p);
     for (int s = 0; s < 4; ++s) {
@@ -204,6 +212,7 @@ crk_status crk_count_pairs(crk_ctx* c, crk_particles* p, int32_t* cgrav, int32_t
     CRK_TRY(check_parts(c, p, true));
     if (!cgrav || !cgather || !csym) return fail(c, CRK_EINVAL, "null count array");
     cudaStream_t st = (cudaStream_t)stream;
+    CRK_TRY(cuda_check(c, cudaMemsetAsync(cgrav, 0, p->n * 4, st), "memset"));
     CRK_TRY(cuda_check(c, cudaMemsetAsync(cgather, 0, p->n * 4, st), "memset"));
     CRK_TRY(cuda_check(c, cudaMemsetAsync(csym, 0, p->n * 4, st), "memset"));
     CRK_TRY(gravity_count(c, p, cgrav, st));

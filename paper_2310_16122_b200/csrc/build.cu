@@ -111,28 +111,42 @@ __global__ void k_gas_pack(int64_t n, const int32_t* __restrict__ gflag, const i
 
 // ---------------------------------------------------------------- leaves (O3)
 // counts per cell for the 4 leaf sets: cnt[s*(ncm+1) + c]
+struct Dom {
+    int lo[3], hi[3];
+};
+// is Morton-indexed cell c owned by this domain?
+__device__ __forceinline__ bool owned(uint64_t c, const Dom& d) {
+    const int cx = (int)compact3(c), cy = (int)compact3(c >> 1), cz = (int)compact3(c >> 2);
+    return cx >= d.lo[0] && cx < d.hi[0] && cy >= d.lo[1] && cy < d.hi[1] && cz >= d.lo[2] && cz < d.hi[2];
+}
+
+// i-leaf sets (0, 2) only in owned cells; j-leaf sets (1, 3) in every populated cell
 __global__ void k_leaf_counts(int64_t ncm, const int32_t* __restrict__ cstart, const int32_t* __restrict__ cend,
-                              const int32_t* __restrict__ grank, int l0, int l1, int l2, int l3, int32_t* cnt) {
+                              const int32_t* __restrict__ grank, int l0, int l1, int l2, int l3, Dom dom,
+                              int32_t* cnt) {
     const int64_t c = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
     if (c > ncm) return;
     int nc = 0, gc = 0;
+    bool own = false;
     if (c < ncm) {
         nc = cend[c] - cstart[c];
         if (nc > 0) gc = grank[cend[c]] - grank[cstart[c]];
+        own = owned((uint64_t)c, dom);
     }
-    cnt[0 * (ncm + 1) + c] = (nc + l0 - 1) / l0;
+    cnt[0 * (ncm + 1) + c] = own ? (nc + l0 - 1) / l0 : 0;
     cnt[1 * (ncm + 1) + c] = (nc + l1 - 1) / l1;
-    cnt[2 * (ncm + 1) + c] = (gc + l2 - 1) / l2;
+    cnt[2 * (ncm + 1) + c] = own ? (gc + l2 - 1) / l2 : 0;
     cnt[3 * (ncm + 1) + c] = (gc + l3 - 1) / l3;
 }
 
 __global__ void k_leaf_fill(int64_t ncm, const int32_t* __restrict__ cstart, const int32_t* __restrict__ cend,
                             const int32_t* __restrict__ grank, const int32_t* __restrict__ off, int set, int lmax,
-                            int32_t* first, int32_t* count, uint64_t* lcell) {
+                            Dom dom, int32_t* first, int32_t* count, uint64_t* lcell) {
     const int64_t c = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
     if (c >= ncm) return;
     const int nc = cend[c] - cstart[c];
     if (nc <= 0) return;
+    if ((set == 0 || set == 2) && !owned((uint64_t)c, dom)) return;
     int base, cnt;
     if (set < 2) {
         base = cstart[c];
@@ -478,8 +492,11 @@ crk_status build_lists(crk_ctx* c, crk_particles* p, cudaStream_t st) {
     // ---- leaves
     const int lmax[4] = {c->prm.leaf_max_i, c->prm.leaf_max_j, c->prm.leaf_max_gas_i, c->prm.leaf_max_gas_j};
     int32_t* cnt = P<int32_t>(c->leaf_cnt);
+    Dom dom;
+    for (int d = 0; d < 3; ++d) { dom.lo[d] = L.dlo[d]; dom.hi[d] = L.dhi[d]; }
     k_leaf_counts<<<nblk(L.ncm + 1, 256), 256, 0, st>>>(L.ncm, P<int32_t>(c->cell_start), P<int32_t>(c->cell_end),
-                                                        P<int32_t>(c->grank), lmax[0], lmax[1], lmax[2], lmax[3], cnt);
+                                                        P<int32_t>(c->grank), lmax[0], lmax[1], lmax[2], lmax[3], dom,
+                                                        cnt);
     CRK_LAUNCHED(c, "leaf counts");
     for (int s = 0; s < 4; ++s) {
         tmp = c->cub_tmp.cap;
@@ -505,7 +522,7 @@ crk_status build_lists(crk_ctx* c, crk_particles* p, cudaStream_t st) {
         if (s >= 2) CRK_TRY(grow(c, c->lmaxh2[s], nl * 4, st));
         k_leaf_fill<<<nblk(L.ncm, 256), 256, 0, st>>>(L.ncm, P<int32_t>(c->cell_start), P<int32_t>(c->cell_end),
                                                       P<int32_t>(c->grank), cnt + s * (L.ncm + 1), s, lmax[s],
-                                                      P<int32_t>(c->lfirst[s]), P<int32_t>(c->lcount[s]),
+                                                      dom, P<int32_t>(c->lfirst[s]), P<int32_t>(c->lcount[s]),
                                                       P<uint64_t>(c->lcell[s]));
         CRK_LAUNCHED(c, "leaf fill");
         if (c->nleaf[s] > 0) {

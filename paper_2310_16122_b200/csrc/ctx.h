@@ -33,6 +33,8 @@ struct Layout {
     int ncell[3];
     int64_t ncm;     // size of the dense Morton-indexed cell arrays = 2^(3 cbits)
     float L[3];      // box as fp32 (exact: powers of two)
+    int dlo[3], dhi[3];  // owned cells [dlo, dhi)
+    bool partial;        // domain smaller than the box (ghosts present)
 };
 
 }  // namespace crk
@@ -77,4 +79,5 @@ struct crk_ctx {
     crk::Buf gacc;               // float4 force accumulator (symmetric kernels)
     crk::Buf gkey;               // int32 group key per particle (symmetric gravity)
     crk::Buf pinned;             // host pinned totals
+    crk::Buf sel_flag, sel_mask; // selection scratch
 };

@@ -356,7 +356,7 @@ static crk_status gravity_sym(crk_ctx* c, crk_particles* p, float dt, cudaStream
 
 crk_status gravity_kick(crk_ctx* c, crk_particles* p, float dt, cudaStream_t st) {
     if (dt != 0.f && (!p->vx || !p->vy || !p->vz)) return fail(c, CRK_EINVAL, "kick needs vx, vy, vz");
-    if (c->prm.symmetric & 1) return gravity_sym(c, p, dt, st);
+    if ((c->prm.symmetric & 1) && !c->lay.partial) return gravity_sym(c, p, dt, st);
     return launch_grav<false>(c, p, dt, nullptr, st);
 }
 

@@ -894,7 +894,7 @@ static crk_status accel_sym(crk_ctx* c, crk_particles* p, float dt, cudaStream_t
 
 crk_status accel_dudt(crk_ctx* c, crk_particles* p, float dt, cudaStream_t st) {
     if (dt != 0.f && (!p->vx || !p->vy || !p->vz || !p->u)) return fail(c, CRK_EINVAL, "kick needs v and u");
-    if (c->prm.symmetric & 2) return accel_sym(c, p, dt, st);
+    if ((c->prm.symmetric & 2) && !c->lay.partial) return accel_sym(c, p, dt, st);
     AccPass<false> g;
     common(c, g);
     g.jrows = P<float4>(c->gpos);
