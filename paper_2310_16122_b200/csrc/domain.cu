@@ -82,15 +82,16 @@ __global__ void k_pack_gas(int64_t n, int what, const int32_t* __restrict__ idx,
     }
 }
 
-__global__ void k_unpack_gas(int64_t n, int what, const int32_t* __restrict__ idx, const void* in, float* gV,
-                             float4* gposV, float4* grec) {
+__global__ void k_unpack_gas(int64_t n, int what, const int32_t* __restrict__ idx, const void* in,
+                             const float4* __restrict__ gpos, float* gV, float4* gposV, float4* grec) {
     const int64_t t = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
     if (what == 0) {
         if (t >= n) return;
         const float V = reinterpret_cast<const float*>(in)[t];
         const int32_t k = idx[t];
+        const float4 p = gpos[k];  // ghost rows of the corrections/extras j-tiles: (x, y, z, V)
         gV[k] = V;
-        gposV[k].w = V;
+        gposV[k] = make_float4(p.x, p.y, p.z, V);
     } else {
         if (t >= n * 9) return;
         const int64_t k = t / 9;
@@ -219,8 +220,8 @@ crk_status crk_unpack_gas(crk_ctx* c, int what, const int32_t* idx, int64_t n, c
     if (what == 1 && c->stage < ST_EXT) return fail(c, CRK_ESTATE, "records are unpacked after crk_extras");
     if (n == 0) return CRK_OK;
     CRK_TRY(cuda_check(c, cudaSetDevice(c->device), "cudaSetDevice"));
-    k_unpack_gas<<<nb(what == 0 ? n : n * 9), 256, 0, (cudaStream_t)stream>>>(n, what, idx, in, P<float>(c->gV),
-                                                                              P<float4>(c->gposV), P<float4>(c->grec));
+    k_unpack_gas<<<nb(what == 0 ? n : n * 9), 256, 0, (cudaStream_t)stream>>>(
+        n, what, idx, in, P<float4>(c->gpos), P<float>(c->gV), P<float4>(c->gposV), P<float4>(c->grec));
     CRK_LAUNCHED(c, "unpack gas");
     return CRK_OK;
 }
