@@ -193,6 +193,77 @@ def _counts_input_order(parts, params):
     return _COUNT_CACHE[key]
 
 
+def tile_config(parts, params, P, r):
+    """Weak scaling: the single-GPU workload tiled over the 2x1x1 / 2x2x1 / 2x2x2 rank grid
+    (periodic replicas, so the generator's H stays exact); rank r gets tile r, re-quantised
+    to q = L_max 2^-23 of the global box, ids offset by r n."""
+    from gen.configs import make_params, quantise
+    from paper_2310_16122_b200.domain import grid_dims
+
+    dims = grid_dims(P)
+    box = [params["box"][a] * dims[a] for a in range(3)]
+    gp = make_params(box, poly=params["poly"], symmetric=params.get("symmetric", 1))
+    c = (r % dims[0], (r // dims[0]) % dims[1], r // (dims[0] * dims[1]))
+    pos = np.stack([parts[k].astype(np.float64) + c[a] * params["box"][a] for a, k in enumerate("xyz")], 1)
+    pos = quantise(pos, box)
+    own = dict(parts)
+    own["x"], own["y"], own["z"] = (np.ascontiguousarray(pos[:, a]) for a in range(3))
+    own["id"] = parts["id"] + r * parts["x"].shape[0]
+    return own, gp
+
+
+def run_multi(args, parts, params, rank, world, local, gen_s):
+    """N > 1: 3-D domain decomposition, ghost exchange over NCCL, weak scaling."""
+    import torch
+    import torch.distributed as dist
+    from paper_2310_16122_b200.domain import Decomposition, DistExchange, DomainRank, substep_dist
+
+    own, gp = tile_config(parts, params, world, rank)
+    d = Decomposition(gp, world)
+    dev = torch.device("cuda", local)
+    rk = DomainRank(d, rank, own, dev)
+    ex = DistExchange(rank, world, dev)
+    hmax2 = ex.allreduce_max(rk.local_hmax2())
+    for _ in range(args.warmup):
+        substep_dist(rk, ex, args.dt, args.dt, hmax2)
+    torch.cuda.synchronize()
+    dist.barrier()
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    l0 = rk.solver.launch_count()
+    with ClockSampler(local) as clk:
+        e0.record()
+        for _ in range(args.steps):
+            substep_dist(rk, ex, args.dt, args.dt, hmax2)
+        e1.record()
+        torch.cuda.synchronize()
+    red_dev = "cpu" if dist.get_backend() == "gloo" else dev
+    ms = torch.tensor([e0.elapsed_time(e1) / args.steps], device=red_dev)
+    dist.all_reduce(ms, op=dist.ReduceOp.MAX)
+    launches = (rk.solver.launch_count() - l0) // max(args.steps, 1)
+    cg, ch, cs = rk.solver.count_pairs(rk.p)
+    own_m = rk.own_mask()
+    pr = torch.tensor([int(cg[own_m].sum()), int(ch[own_m].sum()), int(cs[own_m].sum()),
+                       int(rk.n_total - rk.n_own)], dtype=torch.float64, device=red_dev)
+    dist.all_reduce(pr)
+    pair_int = pr[0].item() + 3 * pr[1].item() + pr[2].item()
+    ms_step = float(ms.item())
+    if rank == 0:
+        line = {"metric": METRIC, "value": pair_int / (ms_step * 1e-3), "unit": "pair interactions/s",
+                "n_gpus": world, "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms_step,
+                "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f32",
+                "data": "synthetic",
+                "config": dict(_config(args, parts), parallelism=f"3-D domain decomposition {d.dims}, "
+                               "ghost exchange R1/R2/R3 over NCCL send/recv", global_box=gp["box"],
+                               ghost_particles_total=int(pr[3].item()), generator_s=round(gen_s, 1)),
+                "substep_ms": ms_step,
+                "pairs": {"gravity": int(pr[0].item()), "gather": int(pr[1].item()), "sym": int(pr[2].item())},
+                "pair_interactions_per_step": int(pair_int),
+                "clocks": clk.summary(), "gpu_launches": int(launches),
+                "e2e": None, "cpu_baseline": None, "roofline": None}
+        print(json.dumps(line), flush=True)
+    rk.close()
+
+
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
@@ -213,7 +284,13 @@ def main():
     if world > 1:
         import torch.distributed as dist
 
-        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+        backend = os.environ.get("CRK_DIST_BACKEND", "nccl")  # gloo: ranks sharing one GPU (tests)
+        if backend == "nccl":
+            dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+        else:
+            dist.init_process_group(backend)
+    if os.environ.get("CRK_SHARE_GPU"):
+        local = 0
     torch.cuda.set_device(local)
 
     from gen import make_config
@@ -230,6 +307,12 @@ def main():
             import torch.distributed as dist
 
             dist.destroy_process_group()
+        return
+    if world > 1:
+        run_multi(args, parts, params, rank, world, local, gen_s)
+        import torch.distributed as dist
+
+        dist.destroy_process_group()
         return
 
     from paper_2310_16122_b200 import Particles, Solver

@@ -108,6 +108,10 @@ class DistExchange:
     def _p2p(self, sends: dict, recvs: dict):
         import torch.distributed as dist
 
+        host = dist.get_backend() == "gloo" and self.device.type == "cuda"  # gloo moves host tensors
+        if host:
+            sends = {s: t.cpu() for s, t in sends.items()}
+            dev_recvs, recvs = recvs, {s: torch.empty(t.shape, dtype=t.dtype) for s, t in recvs.items()}
         ops = []
         for s, t in sends.items():
             ops.append(dist.P2POp(dist.isend, t, s))
@@ -116,6 +120,9 @@ class DistExchange:
         if ops:
             for w in dist.batch_isend_irecv(ops):
                 w.wait()
+        if host:
+            for s, t in recvs.items():
+                dev_recvs[s].copy_(t)
 
     def alltoallv(self, sends: dict, width: int, dtype=torch.float32) -> dict:
         """sends: {peer: tensor (n, width)} -> {peer: tensor (m, width)} (counts exchanged first)."""
@@ -133,7 +140,8 @@ class DistExchange:
     def allreduce_max(self, v: float) -> float:
         import torch.distributed as dist
 
-        t = torch.tensor([v], dtype=torch.float64, device=self.device)
+        dev = "cpu" if dist.get_backend() == "gloo" else self.device
+        t = torch.tensor([v], dtype=torch.float64, device=dev)
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
         return float(t.item())
 
