@@ -253,7 +253,7 @@ def run_multi(args, parts, params, rank, world, local, gen_s):
                 "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f32",
                 "data": "synthetic",
                 "config": dict(_config(args, parts), parallelism=f"3-D domain decomposition {d.dims}, "
-                               "ghost exchange R1/R2/R3 over NCCL send/recv", global_box=gp["box"],
+                               f"ghost exchange R1/R2/R3 over {dist.get_backend()} send/recv", global_box=gp["box"],
                                ghost_particles_total=int(pr[3].item()), generator_s=round(gen_s, 1)),
                 "substep_ms": ms_step,
                 "pairs": {"gravity": int(pr[0].item()), "gather": int(pr[1].item()), "sym": int(pr[2].item())},
