@@ -631,9 +631,8 @@ __global__ void __launch_bounds__(syma::NW * 32, 2) acc_sym_kernel(const AccSymA
         hi[2] = warp_max(iv ? p.z : -INFINITY);
         wcut = warp_max(iv ? __fmul_rn(p.w, p.w) : 0.f) * CULL_SLACK;
     }
-    float ia[G][4];
-#pragma unroll
-    for (int i = 0; i < G; ++i) ia[i][0] = ia[i][1] = ia[i][2] = ia[i][3] = 0.f;
+    // i-side sums of group particle `lane` (lanes < G), reduced over the warp per i
+    float ia0 = 0.f, ia1 = 0.f, ia2 = 0.f, ia3 = 0.f;
     const float Cl = A.Cl, Cq = A.Cq, e2 = A.e2;
 
     auto eval_step = [&](int r0, int n) {
@@ -650,30 +649,33 @@ __global__ void __launch_bounds__(syma::NW * 32, 2) acc_sym_kernel(const AccSymA
         const int j = __float_as_int(sm.eoff[t / JMAX].w) + t % JMAX;
         const bool own = j >= gself && j < gself + ng;  // own group: j-side only
         const float h2j = __fmul_rn(jp.w, jp.w);
-        float bj[4] = {0.f, 0.f, 0.f, 0.f};
-#pragma unroll
-        for (int i = 0; i < G; ++i) {
+        float bj0 = 0.f, bj1 = 0.f, bj2 = 0.f, bj3 = 0.f;
+#pragma unroll 1
+        for (int i = 0; i < ng; ++i) {
             const float4 ip = sm.ipos[warp][i];
-            Rec ri;
-            unpack_rec(sm.irec[warp][i], ri);
             const float x[3] = {ip.x - jp.x, ip.y - jp.y, ip.z - jp.z};  // x_ij
             const float r2 = s32_of(x[0], x[1], x[2]);
-            const bool in = valid && r2 < fmaxf(ri.H2, h2j);
+            const float h2i = __fmul_rn(ip.w, ip.w);
+            const bool in = valid && r2 < fmaxf(h2i, h2j);
+            if (__ballot_sync(0xffffffffu, in) == 0u) continue;  // no lane pairs with this i
+            Rec ri;
+            unpack_rec(sm.irec[warp][i], ri);
             float F[3], Ei, Ej;
             pair_terms(ri, rj, x, r2, Cl, Cq, e2, F, Ei, Ej);
             const bool side_i = in && !own;
-            ia[i][0] -= side_i ? F[0] : 0.f;
-            ia[i][1] -= side_i ? F[1] : 0.f;
-            ia[i][2] -= side_i ? F[2] : 0.f;
-            ia[i][3] += side_i ? Ei : 0.f;
-            bj[0] += in ? F[0] : 0.f;
-            bj[1] += in ? F[1] : 0.f;
-            bj[2] += in ? F[2] : 0.f;
-            bj[3] += in ? Ej : 0.f;
+            const float s0 = warp_sum(side_i ? -F[0] : 0.f), s1 = warp_sum(side_i ? -F[1] : 0.f),
+                        s2 = warp_sum(side_i ? -F[2] : 0.f), s3 = warp_sum(side_i ? Ei : 0.f);
+            if (lane == i) {
+                ia0 += s0; ia1 += s1; ia2 += s2; ia3 += s3;
+            }
+            bj0 += in ? F[0] : 0.f;
+            bj1 += in ? F[1] : 0.f;
+            bj2 += in ? F[2] : 0.f;
+            bj3 += in ? Ej : 0.f;
         }
         if (valid) {
             const float im = 1.f / rj.m;
-            red_add_v4(A.acc + j, bj[0] * im, bj[1] * im, bj[2] * im, bj[3] * im);
+            red_add_v4(A.acc + j, bj0 * im, bj1 * im, bj2 * im, bj3 * im);
         }
     };
 
@@ -752,14 +754,9 @@ __global__ void __launch_bounds__(syma::NW * 32, 2) acc_sym_kernel(const AccSymA
     }
     if (wactive) {
         if (wr > rd) eval_step(rd, wr - rd);
-#pragma unroll
-        for (int i = 0; i < G; ++i) {
-            const float s0 = warp_sum(ia[i][0]), s1 = warp_sum(ia[i][1]), s2 = warp_sum(ia[i][2]),
-                        s3 = warp_sum(ia[i][3]);
-            if (lane == i && i < ng) {
-                const float im = 1.f / sm.irec[warp][i][8].z;  // 1 / m_i
-                red_add_v4(A.acc + gself + i, s0 * im, s1 * im, s2 * im, s3 * im);
-            }
+        if (lane < ng) {
+            const float im = 1.f / sm.irec[warp][lane][8].z;  // 1 / m_i
+            red_add_v4(A.acc + gself + lane, ia0 * im, ia1 * im, ia2 * im, ia3 * im);
         }
     }
 }
