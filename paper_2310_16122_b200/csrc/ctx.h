@@ -80,4 +80,5 @@ struct crk_ctx {
     crk::Buf gkey;               // int32 group key per particle (symmetric gravity)
     crk::Buf pinned;             // host pinned totals
     crk::Buf sel_flag, sel_mask; // selection scratch
+    crk::Buf work;               // dynamic work counters of the persistent kernels
 };

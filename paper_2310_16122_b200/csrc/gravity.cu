@@ -5,6 +5,9 @@
 // Newtonian minus the fitted grid-force polynomial of order 5 (PAPER.md:147, 278,
 // 646 HACC_CUDA_POLY_ORDER=5), Plummer-softened, inside the cutoff.  Per pair: one
 // MUFU rsqrt and ~19 FP32 FMA-pipe instructions; FP32-ALU bound.
+#include <algorithm>
+#include <cstdlib>
+
 #include "pairs.cuh"
 
 namespace crk {
@@ -93,20 +96,26 @@ struct GravPass {
 // that single wait every warp runs prefilter -> particle filter -> evaluation on its
 // own, feeding a 64-entry ring of survivors so that every warp step but the last is full.
 namespace symg {
-constexpr int NW = 4, G = 16, ENT = 256, RING = 64;  // NW warps per CTA; two CTAs per 128-leaf
-struct Smem {
+constexpr int G = 16, RING = 64;
+template <int NW, int ENT, int NB>  // warps per CTA, row entries per round, row buffers (2 = prefetch)
+struct Cfg {
+struct RowBuf {
     float4 raw[ENT * JMAX];  // TMA: xm rows of the row's j-leaves, JMAX slots per entry
     float4 ebox[ENT][2];     // TMA: padded j-leaf boxes
     float4 eoff[ENT];        // periodic offset (x, y, z) and first (w, as int)
     int ecnt[ENT];
-    uint64_t bar;
+};
+struct Smem {
+    RowBuf rb[NB];           // NB = 2: the next work item's row streams in during this one
+    uint64_t bar[2];
+    int next_item;
     float4 ipos[NW][G];
     float4 wpos[NW][RING];
     int widx[NW][RING];
     uint16_t went[NW][ENT];
 };
+};
 }  // namespace symg
-
 
 struct GravSymArgs {
     const float4* xm;
@@ -116,161 +125,205 @@ struct GravSymArgs {
     const int32_t* ifirst;
     const int32_t* icount;
     float4* acc;
-    int split;  // CTAs per i-leaf
+    int* work;           // dynamic work counter (zeroed before the launch)
+    int split;           // work items per i-leaf
+    int nitems;
     float L[3];
     float rcut2, eps2;
     float c0, c1, c2, c3, c4, c5;
 };
 
-__global__ void __launch_bounds__(symg::NW * 32, 4) grav_sym_kernel(const GravSymArgs A) {
+// all threads: stage row entries [e0, e0 + nent) of leaf a into buffer rb; every thread
+// arrives once on `bar` with the bytes of the copies it issued (barrier count = CTA size)
+template <int NW, int ENT, int NB>
+__device__ __forceinline__ void grav_stage(typename symg::Cfg<NW, ENT, NB>::Smem& sm, const GravSymArgs& A, int b, int e0,
+                                           int nent) {
+    uint32_t bytes = 0;
+    for (int t = threadIdx.x; t < nent; t += NW * 32) {
+        int first, count, leaf, code;
+        unpack_entry(__ldg(A.erec + e0 + t), first, count, leaf, code);
+        int sx, sy, sz;
+        decode_shift(code, sx, sy, sz);
+        sm.rb[b].eoff[t] = make_float4((float)sx * A.L[0], (float)sy * A.L[1], (float)sz * A.L[2], __int_as_float(first));
+        sm.rb[b].ecnt[t] = count;
+        bulk_g2s(&sm.rb[b].raw[t * JMAX], A.xm + first, (uint32_t)count * 16u, &sm.bar[b]);
+        bulk_g2s(&sm.rb[b].ebox[t][0], A.box8 + 2 * (int64_t)leaf, 32u, &sm.bar[b]);
+        bytes += (uint32_t)count * 16u + 32u;
+    }
+    mbar_arrive_expect_tx(&sm.bar[b], bytes);
+}
+
+template <int NW, int ENT, int NB>
+__global__ void __launch_bounds__(NW * 32, 16 / NW) grav_sym_kernel(const GravSymArgs A) {
     using namespace symg;
+    using Smem = typename Cfg<NW, ENT, NB>::Smem;
+    using RowBuf = typename Cfg<NW, ENT, NB>::RowBuf;
     extern __shared__ __align__(128) unsigned char smem_raw[];
     Smem& sm = *reinterpret_cast<Smem*>(smem_raw);
-    const int a = blockIdx.x / A.split;  // i-leaf; CTA part blockIdx.x % split covers NW groups
-    const int ifirst = A.ifirst[a];
-    const int icount = A.icount[a];
     const int warp = threadIdx.x >> 5;
     const int lane = threadIdx.x & 31;
-    const int ibase = (blockIdx.x % A.split * NW + warp) * G;
-    const bool wactive = ibase < icount;
-    const int gself = ifirst + ibase;  // this warp's group: [gself, gself + ng)
-    const int ng = min(G, icount - ibase);
-    const int rbeg = A.row_off[a], rend = A.row_off[a + 1];
-
-    if (threadIdx.x == 0) {
-        mbar_init(&sm.bar, 1);
-        mbar_fence_init();
-    }
-    float lo[3] = {0.f, 0.f, 0.f}, hi[3] = {0.f, 0.f, 0.f};
     const float wcut = A.rcut2 * CULL_SLACK;
-    if (wactive) {
-        const bool iv = lane < ng;
-        float4 p = make_float4(-1e18f, -1e18f, -1e18f, 0.f);  // far sentinel: finite products
-        if (iv) p = A.xm[gself + lane];
-        if (lane < G) sm.ipos[warp][lane] = p;
-        lo[0] = warp_min(iv ? p.x : INFINITY);
-        lo[1] = warp_min(iv ? p.y : INFINITY);
-        lo[2] = warp_min(iv ? p.z : INFINITY);
-        hi[0] = warp_max(iv ? p.x : -INFINITY);
-        hi[1] = warp_max(iv ? p.y : -INFINITY);
-        hi[2] = warp_max(iv ? p.z : -INFINITY);
-    }
-    float ax[G], ay[G], az[G];
-#pragma unroll
-    for (int i = 0; i < G; ++i) ax[i] = ay[i] = az[i] = 0.f;
+    const float rc2 = A.rcut2, e2 = A.eps2;
+    const float c0 = A.c0, c1 = A.c1, c2 = A.c2, c3 = A.c3, c4 = A.c4, c5 = A.c5;
     float4* wpos = sm.wpos[warp];
     int* widx = sm.widx[warp];
     uint16_t* went = sm.went[warp];
-    const float rc2 = A.rcut2, e2 = A.eps2;
-    const float c0 = A.c0, c1 = A.c1, c2 = A.c2, c3 = A.c3, c4 = A.c4, c5 = A.c5;
 
-    // one warp step over ring slots [r0, r0 + n): lane owns one survivor, loops over the group
-    auto eval_step = [&](int r0, int n) {
-        float4 jp = make_float4(1e18f, 1e18f, 1e18f, 0.f);
-        int j = 0;
-        if (lane < n) {
-            const int s = (r0 + lane) & (RING - 1);
-            jp = wpos[s];
-            j = widx[s];
-        }
-        // own group: the i-side half is counted when the partner is the survivor
-        const float mj = (j >= gself && j < gself + ng) ? 0.f : jp.w;
-        float bx = 0.f, by = 0.f, bz = 0.f;
-#pragma unroll
-        for (int i = 0; i < G; ++i) {
-            const float4 ip = sm.ipos[warp][i];
-            const float dx = jp.x - ip.x, dy = jp.y - ip.y, dz = jp.z - ip.z;  // x_j - x_i
-            const float r2 = s32_of(dx, dy, dz);
-            const float ri = rsqrtf(r2 + e2);
-            const float ri3 = ri * ri * ri;
-            const float p5 = fmaf(fmaf(fmaf(fmaf(fmaf(c5, r2, c4), r2, c3), r2, c2), r2, c1), r2, c0);
-            const float w = r2 < rc2 ? ri3 - p5 : 0.f;
-            const float wi = mj * w;  // i-side: a_i += m_j w x_ji
-            ax[i] = fmaf(wi, dx, ax[i]);
-            ay[i] = fmaf(wi, dy, ay[i]);
-            az[i] = fmaf(wi, dz, az[i]);
-            const float wj = ip.w * w;  // j-side: a_j += m_i w x_ij
-            bx = fmaf(-wj, dx, bx);
-            by = fmaf(-wj, dy, by);
-            bz = fmaf(-wj, dz, bz);
-        }
-        if (lane < n) red_add_v4(A.acc + j, bx, by, bz, 0.f);
-    };
-
-    int wr = 0, rd = 0;  // ring write / read counters
-    uint32_t phase = 0;
-    for (int e0 = rbeg; e0 < rend; e0 += ENT) {
-        const int nent = min(ENT, rend - e0);
-        __syncthreads();  // mbarrier initialised / previous round consumed
-        for (int t = threadIdx.x; t < nent; t += NW * 32) {
-            int first, count, leaf, code;
-            unpack_entry(__ldg(A.erec + e0 + t), first, count, leaf, code);
-            int sx, sy, sz;
-            decode_shift(code, sx, sy, sz);
-            sm.eoff[t] = make_float4((float)sx * A.L[0], (float)sy * A.L[1], (float)sz * A.L[2], __int_as_float(first));
-            sm.ecnt[t] = count;
-            mbar_expect_tx(&sm.bar, (uint32_t)count * 16u + 32u);
-            bulk_g2s(&sm.raw[t * JMAX], A.xm + first, (uint32_t)count * 16u, &sm.bar);
-            bulk_g2s(&sm.ebox[t][0], A.box8 + 2 * (int64_t)leaf, 32u, &sm.bar);
-        }
-        __syncthreads();
-        if (threadIdx.x == 0) mbar_arrive(&sm.bar);
-        mbar_wait(&sm.bar, phase);
-        phase ^= 1u;
-        if (wactive) {
-            // (1) leaf prefilter: box-box distance, one lane per entry
-            int nsurv = 0;
-            for (int e = lane; e - lane < nent; e += 32) {
-                bool ek = false;
-                if (e < nent) {
-                    const float4 o = sm.eoff[e];
-                    const float4 bl = sm.ebox[e][0], bh = sm.ebox[e][1];
-                    const float gx = fmaxf(fmaxf(bl.x + o.x - hi[0], lo[0] - bh.x - o.x), 0.f);
-                    const float gy = fmaxf(fmaxf(bl.y + o.y - hi[1], lo[1] - bh.y - o.y), 0.f);
-                    const float gz = fmaxf(fmaxf(bl.z + o.z - hi[2], lo[2] - bh.z - o.z), 0.f);
-                    // entries wholly below this group own no pair (j < gself)
-                    ek = fmaf(gz, gz, fmaf(gy, gy, gx * gx)) < wcut &&
-                         __float_as_int(o.w) + sm.ecnt[e] > gself;
-                }
-                const unsigned em = __ballot_sync(0xffffffffu, ek);
-                if (ek) went[nsurv + __popc(em & ((1u << lane) - 1u))] = (uint16_t)e;
-                nsurv += __popc(em);
-            }
-            __syncwarp();
-            // (2) particle filter, 32/JMAX entries per step, into the survivor ring
-            for (int q0 = 0; q0 < nsurv; q0 += 32 / JMAX) {
-                const int qe = q0 + lane / JMAX;
-                const int kk = lane % JMAX;
-                const int e = went[qe < nsurv ? qe : 0];
-                const float4 o = sm.eoff[e];
-                float4 p = sm.raw[e * JMAX + kk];
-                p.x += o.x; p.y += o.y; p.z += o.z;  // exact (O1)
-                const int j = __float_as_int(o.w) + kk;
-                const bool keep = qe < nsurv && kk < sm.ecnt[e] && j >= gself &&
-                                  box_dist2(p.x, p.y, p.z, lo, hi) < wcut;
-                const unsigned msk = __ballot_sync(0xffffffffu, keep);
-                if (keep) {
-                    const int s = (wr + __popc(msk & ((1u << lane) - 1u))) & (RING - 1);
-                    wpos[s] = p;
-                    widx[s] = j;
-                }
-                wr += __popc(msk);
-                __syncwarp();
-                if (wr - rd >= 32) {
-                    eval_step(rd, 32);
-                    rd += 32;
-                    __syncwarp();
-                }
-            }
-        }
+    if (threadIdx.x == 0) {
+        mbar_init(&sm.bar[0], NW * 32);
+        mbar_init(&sm.bar[1], NW * 32);
+        mbar_fence_init();
+        sm.next_item = atomicAdd(A.work, 1);
     }
-    if (wactive) {
-        if (wr > rd) eval_step(rd, wr - rd);
-#pragma unroll
-        for (int i = 0; i < G; ++i) {
-            const float sx = warp_sum(ax[i]), sy = warp_sum(ay[i]), sz = warp_sum(az[i]);
-            if (lane == i && i < ng) red_add_v4(A.acc + gself + i, sx, sy, sz, 0.f);
+    __syncthreads();
+    int w = sm.next_item;
+    const int first_w = w;
+    uint32_t ph[2] = {0u, 0u};
+    int b = 0;
+    if (w < A.nitems) {
+        const int a0 = w / A.split;
+        const int r0 = A.row_off[a0];
+        grav_stage<NW, ENT, NB>(sm, A, 0, r0, min(ENT, A.row_off[a0 + 1] - r0));
+    }
+    while (w < A.nitems) {
+        // claim and prefetch the next work item into the other buffer (free since the
+        // barrier that ended the previous item)
+        if (threadIdx.x == 0) sm.next_item = atomicAdd(A.work, 1);
+        __syncthreads();
+        const int wn = sm.next_item;
+        if (NB == 2 && wn < A.nitems) {
+            const int an = wn / A.split;
+            const int rn = A.row_off[an];
+            grav_stage<NW, ENT, NB>(sm, A, b ^ 1, rn, min(ENT, A.row_off[an + 1] - rn));
         }
+
+        const int a = w / A.split;
+        const int ifirst = A.ifirst[a];
+        const int icount = A.icount[a];
+        const int ibase = (w % A.split * NW + warp) * G;
+        const bool wactive = ibase < icount;
+        const int gself = ifirst + ibase;  // this warp's group: [gself, gself + ng)
+        const int ng = min(G, icount - ibase);
+        const int rbeg = A.row_off[a], rend = A.row_off[a + 1];
+
+        float lo[3] = {0.f, 0.f, 0.f}, hi[3] = {0.f, 0.f, 0.f};
+        if (wactive) {
+            const bool iv = lane < ng;
+            float4 p = make_float4(-1e18f, -1e18f, -1e18f, 0.f);  // far sentinel: finite products
+            if (iv) p = A.xm[gself + lane];
+            if (lane < G) sm.ipos[warp][lane] = p;
+            lo[0] = warp_min(iv ? p.x : INFINITY);
+            lo[1] = warp_min(iv ? p.y : INFINITY);
+            lo[2] = warp_min(iv ? p.z : INFINITY);
+            hi[0] = warp_max(iv ? p.x : -INFINITY);
+            hi[1] = warp_max(iv ? p.y : -INFINITY);
+            hi[2] = warp_max(iv ? p.z : -INFINITY);
+        }
+        __syncwarp();
+        float ax[G], ay[G], az[G];
+#pragma unroll
+        for (int i = 0; i < G; ++i) ax[i] = ay[i] = az[i] = 0.f;
+
+        // one warp step over ring slots [r0, r0 + n): lane owns one survivor, loops over the group
+        auto eval_step = [&](int r0, int n) {
+            float4 jp = make_float4(1e18f, 1e18f, 1e18f, 0.f);
+            int j = 0;
+            if (lane < n) {
+                const int s = (r0 + lane) & (RING - 1);
+                jp = wpos[s];
+                j = widx[s];
+            }
+            // own group: the i-side half is counted when the partner is the survivor
+            const float mj = (j >= gself && j < gself + ng) ? 0.f : jp.w;
+            float bx = 0.f, by = 0.f, bz = 0.f;
+#pragma unroll
+            for (int i = 0; i < G; ++i) {
+                const float4 ip = sm.ipos[warp][i];
+                const float dx = jp.x - ip.x, dy = jp.y - ip.y, dz = jp.z - ip.z;  // x_j - x_i
+                const float r2 = s32_of(dx, dy, dz);
+                const float ri = rsqrtf(r2 + e2);
+                const float ri3 = ri * ri * ri;
+                const float p5 = fmaf(fmaf(fmaf(fmaf(fmaf(c5, r2, c4), r2, c3), r2, c2), r2, c1), r2, c0);
+                const float wgt = r2 < rc2 ? ri3 - p5 : 0.f;
+                const float wi = mj * wgt;  // i-side: a_i += m_j w x_ji
+                ax[i] = fmaf(wi, dx, ax[i]);
+                ay[i] = fmaf(wi, dy, ay[i]);
+                az[i] = fmaf(wi, dz, az[i]);
+                const float wj = ip.w * wgt;  // j-side: a_j += m_i w x_ij
+                bx = fmaf(-wj, dx, bx);
+                by = fmaf(-wj, dy, by);
+                bz = fmaf(-wj, dz, bz);
+            }
+            if (lane < n) red_add_v4(A.acc + j, bx, by, bz, 0.f);
+        };
+
+        int wr = 0, rd = 0;  // ring write / read counters
+        for (int e0 = rbeg; e0 < rend; e0 += ENT) {
+            const int nent = min(ENT, rend - e0);
+            if (e0 > rbeg || (NB == 1 && e0 == rbeg && w != first_w)) {  // rounds staged in place
+                __syncthreads();
+                grav_stage<NW, ENT, NB>(sm, A, b, e0, nent);
+            }
+            mbar_wait(&sm.bar[b], ph[b]);
+            ph[b] ^= 1u;
+            const RowBuf& R = sm.rb[b];
+            if (wactive) {
+                // (1) leaf prefilter: box-box distance, one lane per entry
+                int nsurv = 0;
+                for (int e = lane; e - lane < nent; e += 32) {
+                    bool ek = false;
+                    if (e < nent) {
+                        const float4 o = R.eoff[e];
+                        const float4 bl = R.ebox[e][0], bh = R.ebox[e][1];
+                        const float gx = fmaxf(fmaxf(bl.x + o.x - hi[0], lo[0] - bh.x - o.x), 0.f);
+                        const float gy = fmaxf(fmaxf(bl.y + o.y - hi[1], lo[1] - bh.y - o.y), 0.f);
+                        const float gz = fmaxf(fmaxf(bl.z + o.z - hi[2], lo[2] - bh.z - o.z), 0.f);
+                        // entries wholly below this group own no pair (j < gself)
+                        ek = fmaf(gz, gz, fmaf(gy, gy, gx * gx)) < wcut && __float_as_int(o.w) + R.ecnt[e] > gself;
+                    }
+                    const unsigned em = __ballot_sync(0xffffffffu, ek);
+                    if (ek) went[nsurv + __popc(em & ((1u << lane) - 1u))] = (uint16_t)e;
+                    nsurv += __popc(em);
+                }
+                __syncwarp();
+                // (2) particle filter, 32/JMAX entries per step, into the survivor ring
+                for (int q0 = 0; q0 < nsurv; q0 += 32 / JMAX) {
+                    const int qe = q0 + lane / JMAX;
+                    const int kk = lane % JMAX;
+                    const int e = went[qe < nsurv ? qe : 0];
+                    const float4 o = R.eoff[e];
+                    float4 p = R.raw[e * JMAX + kk];
+                    p.x += o.x; p.y += o.y; p.z += o.z;  // exact (O1)
+                    const int j = __float_as_int(o.w) + kk;
+                    const bool keep = qe < nsurv && kk < R.ecnt[e] && j >= gself &&
+                                      box_dist2(p.x, p.y, p.z, lo, hi) < wcut;
+                    const unsigned msk = __ballot_sync(0xffffffffu, keep);
+                    if (keep) {
+                        const int s = (wr + __popc(msk & ((1u << lane) - 1u))) & (RING - 1);
+                        wpos[s] = p;
+                        widx[s] = j;
+                    }
+                    wr += __popc(msk);
+                    __syncwarp();
+                    if (wr - rd >= 32) {
+                        eval_step(rd, 32);
+                        rd += 32;
+                        __syncwarp();
+                    }
+                }
+            }
+        }
+        if (wactive) {
+            if (wr > rd) eval_step(rd, wr - rd);
+#pragma unroll
+            for (int i = 0; i < G; ++i) {
+                const float sx = warp_sum(ax[i]), sy = warp_sum(ay[i]), sz = warp_sum(az[i]);
+                if (lane == i && i < ng) red_add_v4(A.acc + gself + i, sx, sy, sz, 0.f);
+            }
+        }
+        __syncthreads();  // buffer b is free for the item after next
+        if (NB == 2) b ^= 1;
+        w = wn;
     }
 }
 
@@ -323,6 +376,22 @@ static crk_status launch_grav(crk_ctx* c, crk_particles* p, float dt, int32_t* c
     return CRK_OK;
 }
 
+template <int NW, int ENT, int NB>
+static cudaError_t launch_grav_sym(crk_ctx* c, GravSymArgs& A, cudaStream_t st) {
+    using Smem = typename symg::Cfg<NW, ENT, NB>::Smem;
+    const int smem = (int)sizeof(Smem);
+    cudaError_t e = cudaFuncSetAttribute(grav_sym_kernel<NW, ENT, NB>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+    if (e != cudaSuccess) return e;
+    A.split = (c->prm.leaf_max_i + NW * symg::G - 1) / (NW * symg::G);
+    A.nitems = (int)(c->nleaf[0] * A.split);
+    int per_sm = 0, nsm = 0;
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, grav_sym_kernel<NW, ENT, NB>, NW * 32, smem);
+    cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, c->device);
+    const int grid = (int)std::min<int64_t>(A.nitems, (int64_t)std::max(1, per_sm) * nsm);
+    grav_sym_kernel<NW, ENT, NB><<<grid, NW * 32, smem, st>>>(A);
+    return cudaGetLastError();
+}
+
 static crk_status gravity_sym(crk_ctx* c, crk_particles* p, float dt, cudaStream_t st) {
     const int64_t n = c->n;
     CRK_TRY(grow(c, c->gacc, n * 16, st));
@@ -341,11 +410,20 @@ static crk_status gravity_sym(crk_ctx* c, crk_particles* p, float dt, cudaStream
         A.eps2 = c->prm.eps2;
         A.c0 = c->prm.poly[0]; A.c1 = c->prm.poly[1]; A.c2 = c->prm.poly[2];
         A.c3 = c->prm.poly[3]; A.c4 = c->prm.poly[4]; A.c5 = c->prm.poly[5];
-        const int smem = (int)sizeof(symg::Smem);
-        cudaError_t e = cudaFuncSetAttribute(grav_sym_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
-        if (e != cudaSuccess) return cuda_check(c, e, "smem attribute");
-        A.split = (c->prm.leaf_max_i + symg::NW * symg::G - 1) / (symg::NW * symg::G);
-        grav_sym_kernel<<<(unsigned)(c->nleaf[0] * A.split), symg::NW * 32, smem, st>>>(A);
+        const char* gv = getenv("CRK_GRAV_VARIANT");
+        const int var = gv ? atoi(gv) : 0;
+        CRK_TRY(grow(c, c->work, 16, st));
+        CRK_TRY(cuda_check(c, cudaMemsetAsync(c->work.p, 0, 16, st), "memset"));
+        A.work = P<int>(c->work);
+        cudaError_t e;
+        // measured on c4 (profiles/r01): <8 warps, 320 entries, 1 buffer> 24.6 ms, <4, 320, 1> 30.3,
+        // <8, 320, 2> 36.2, <4, 256, 2> 41.9 (the second row buffer costs occupancy)
+        switch (var) {
+        case 1: e = launch_grav_sym<4, 320, 1>(c, A, st); break;
+        case 2: e = launch_grav_sym<8, 320, 2>(c, A, st); break;
+        default: e = launch_grav_sym<8, 320, 1>(c, A, st); break;
+        }
+        if (e != cudaSuccess) return cuda_check(c, e, "gravity (symmetric) kernel");
         CRK_LAUNCHED(c, "gravity (symmetric) kernel");
     }
     k_grav_finish<<<(unsigned)((n + 255) / 256), 256, 0, st>>>(n, P<float4>(c->gacc), c->prm.G, dt, p->ax, p->ay,

@@ -5,6 +5,9 @@
 // Gas state lives in the ctx in gas-rank order (gpos, gvel, gV, gcoef, grec) so that
 // the j-tiles of every pass are contiguous; the caller's per-particle outputs are
 // written at gas_idx[k] in each pass epilogue.
+#include <cstdlib>
+#include <cstring>
+
 #include "pairs.cuh"
 
 namespace crk {
@@ -791,12 +794,20 @@ static RowView hydro_rows(crk_ctx* c) {
     return rv;
 }
 
-template <class Pass, int ENT, int MINB = 1>
+template <class Pass, int ENT, int MINB = 1, int NW = HYD_NW, int G = HYD_G>
 static crk_status launch_hyd(crk_ctx* c, const Pass& ps, cudaStream_t st, const char* what) {
     if (c->nleaf[2] == 0) return CRK_OK;
-    CRK_TRY(cuda_check(c, launch_pairs<Pass, HYD_NW, HYD_G, ENT, MINB>(ps, hydro_rows(c), c->nleaf[2], st), what));
+    static_assert(NW * G >= 64, "a CTA covers a whole gas i-leaf (<= 64)");
+    CRK_TRY(cuda_check(c, launch_pairs<Pass, NW, G, ENT, MINB>(ps, hydro_rows(c), c->nleaf[2], st), what));
     c->launches++;
     return CRK_OK;
+}
+
+// tuning hook (experiments only): CRK_HYD_VARIANT=<digit per pass: geo cor ext acc>, 0 = default, 1 = G4
+static int hyd_variant(int pass) {
+    const char* v = getenv("CRK_HYD_VARIANT");
+    if (!v || (int)strlen(v) <= pass) return 0;
+    return v[pass] - '0';
 }
 
 static void common(crk_ctx* c, HydCommon& h) {
@@ -813,6 +824,7 @@ crk_status geometry(crk_ctx* c, crk_particles* p, cudaStream_t st) {
     g.gposV = P<float4>(c->gposV);
     g.Vout = p->V;
     g.cnt = nullptr;
+    if (hyd_variant(0) == 1) return launch_hyd<GeoPass<false>, 128, 1, 16, 4>(c, g, st, "geometry kernel");
     return launch_hyd<GeoPass<false>, 128, 2>(c, g, st, "geometry kernel");
 }
 
@@ -825,6 +837,7 @@ crk_status corrections(crk_ctx* c, crk_particles* p, cudaStream_t st) {
     g.ng = c->n_gas;
     g.A = p->A; g.B = p->B; g.dA = p->dA; g.dB = p->dB;
     g.n = c->n;
+    if (hyd_variant(1) == 1) return launch_hyd<CorPass, 128, 1, 16, 4>(c, g, st, "corrections kernel");
     return launch_hyd<CorPass, 128, 3>(c, g, st, "corrections kernel");
 }
 
@@ -855,6 +868,7 @@ crk_status extras(crk_ctx* c, crk_particles* p, cudaStream_t st) {
     g.n = c->n;
     g.gamma = c->prm.gamma;
     g.rho = p->rho; g.P = p->P; g.cs = p->cs; g.dv = p->dv;
+    if (hyd_variant(2) == 1) return launch_hyd<ExtPass, 128, 1, 16, 4>(c, g, st, "extras kernel");
     return launch_hyd<ExtPass, 128, 3>(c, g, st, "extras kernel");
 }
 
@@ -902,6 +916,7 @@ crk_status accel_dudt(crk_ctx* c, crk_particles* p, float dt, cudaStream_t st) {
     g.ahx = p->ahx; g.ahy = p->ahy; g.ahz = p->ahz; g.dudt = p->dudt;
     g.vx = p->vx; g.vy = p->vy; g.vz = p->vz; g.u = p->u;
     g.cnt = nullptr;
+    if (hyd_variant(3) == 1) return launch_hyd<AccPass<false>, 72, 1, 16, 4>(c, g, st, "accel/dudt kernel");
     return launch_hyd<AccPass<false>, 72, 2>(c, g, st, "accel/dudt kernel");
 }
 
