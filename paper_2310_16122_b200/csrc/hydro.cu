@@ -653,7 +653,7 @@ __global__ void __launch_bounds__(syma::NW * 32, 2) acc_sym_kernel(const AccSymA
         const bool own = j >= gself && j < gself + ng;  // own group: j-side only
         const float h2j = __fmul_rn(jp.w, jp.w);
         float bj0 = 0.f, bj1 = 0.f, bj2 = 0.f, bj3 = 0.f;
-#pragma unroll 1
+#pragma unroll 2
         for (int i = 0; i < ng; ++i) {
             const float4 ip = sm.ipos[warp][i];
             const float x[3] = {ip.x - jp.x, ip.y - jp.y, ip.z - jp.z};  // x_ij

@@ -217,3 +217,97 @@ def test_clustered_config3_sampled():
 @pytest.mark.slow
 def test_config4_full_size_sampled():
     _sampled("c4", 300)
+
+
+# ------------------------------------------------------------------ parameter / input edge cases
+@pytest.mark.parametrize("li,lg", [(32, 16), (64, 32), (16, 64)])
+def test_leaf_size_variants(li, lg):
+    """Other compiled leaf sizes: lists, counts and forces still match the oracle."""
+    from gen import make_config
+
+    parts, params = make_config("lat:32,16,16:0.12:9", leaf_max_i=li, leaf_max_gas_i=lg)
+    g = run_gpu(parts, params, lists=True)
+    order, ls, lists = _oracle_lists(parts, params)
+    assert np.array_equal(g["perm"], order)
+    for m in range(2):
+        off, col, sh = lists[m]
+        gv = g["lv"]["lists"][m]
+        assert np.array_equal(gv["row_off"].cpu().numpy(), off)
+    ref_c = oracle.counts(parts, params)
+    assert np.array_equal(g["cnt_in"][0], ref_c["grav"])
+    assert np.array_equal(g["cnt_in"][2], ref_c["sym"])
+    ref = oracle.substep(parts, params)
+    gi = g["in"]
+    assert norm_err(np.stack([gi["ax"], gi["ay"], gi["az"]], 1), ref["grav_a"], ref["grav_S"]) <= TOL_FORCE
+    T = ref["targets"]
+    assert norm_err(np.stack([gi["ahx"], gi["ahy"], gi["ahz"]], 1)[T], ref["a"], ref["Sa"]) <= TOL_FORCE
+
+
+def test_coincident_particles_and_tiny_input():
+    """Distinct particles at identical positions (s = 0 pairs), and a box with very few
+    particles per cell: counts exact, results finite and within the bar."""
+    parts, params = cached_config("c1")
+    parts = {k: v.copy() for k, v in parts.items()}
+    # move every 97th particle onto its predecessor's position
+    for i in range(1, parts["x"].shape[0], 97):
+        for k in "xyz":
+            parts[k][i] = parts[k][i - 1]
+    for sym in (1, 0):
+        params["symmetric"] = sym
+        g = run_gpu(parts, params)
+        ref_c = oracle.counts(parts, params)
+        assert np.array_equal(g["cnt_in"][0], ref_c["grav"])
+        assert np.array_equal(g["cnt_in"][1], ref_c["gather"])
+        assert np.array_equal(g["cnt_in"][2], ref_c["sym"])
+        ref = oracle.substep(parts, params)
+        gi = g["in"]
+        a = np.stack([gi["ax"], gi["ay"], gi["az"]], 1)
+        assert np.all(np.isfinite(a))
+        assert norm_err(a, ref["grav_a"], ref["grav_S"]) <= TOL_FORCE
+        T = ref["targets"]
+        assert norm_err(np.stack([gi["ahx"], gi["ahy"], gi["ahz"]], 1)[T], ref["a"], ref["Sa"]) <= TOL_FORCE
+    # tiny: 2x4^3 particles in a 16^3 box (mostly empty cells)
+    from gen.configs import make_lattice, make_params
+    from crk_testutil import cached_config as _cc  # noqa: F401
+
+    rng = np.random.default_rng(3)
+    n = 128
+    tiny = {k: v[:0] for k, v in parts.items()}
+    pos = (rng.random((n, 3)) * 16.0).astype(np.float64)
+    from gen.configs import quantise
+
+    pos = quantise(pos, [16.0] * 3)
+    tiny = dict(x=pos[:, 0].copy(), y=pos[:, 1].copy(), z=pos[:, 2].copy(),
+                vx=np.zeros(n, np.float32), vy=np.zeros(n, np.float32), vz=np.zeros(n, np.float32),
+                m=np.full(n, 0.5, np.float32), species=(np.arange(n) % 2).astype(np.uint8),
+                id=np.arange(n, dtype=np.int64), H=np.where(np.arange(n) % 2 == 1, 3.5, 0.0).astype(np.float32),
+                u=np.ones(n, np.float32))
+    tp = make_params([16.0] * 3)
+    g = run_gpu(tiny, tp)
+    ref_c = oracle.counts(tiny, tp)
+    assert np.array_equal(g["cnt_in"][0], ref_c["grav"]) and np.array_equal(g["cnt_in"][2], ref_c["sym"])
+    ref = oracle.substep(tiny, tp)
+    gi = g["in"]
+    assert norm_err(np.stack([gi["ax"], gi["ay"], gi["az"]], 1), ref["grav_a"], ref["grav_S"]) <= TOL_FORCE
+
+
+@pytest.mark.slow
+def test_clustered_config3_full_chain_sampled_symmetric_modes():
+    """Config 3 (clustered, dense cells chunked into many leaves, long rows staged in
+    several TMA rounds) with both kernel variants."""
+    for sym in (0, 3):
+        parts, params = cached_config("c3")
+        params["symmetric"] = sym
+        rng = np.random.default_rng(11)
+        gas = np.nonzero(parts["species"] == 1)[0]
+        # bias the sample to the densest particles (smallest H)
+        dense = gas[np.argsort(parts["H"][gas])[:2000]]
+        tg = np.sort(rng.choice(dense, 150, replace=False))
+        g = run_gpu(parts, params, counts=False)
+        ref = oracle.substep(parts, params, targets=tg, grav_targets=tg)
+        gi = g["in"]
+        a = np.stack([gi["ax"], gi["ay"], gi["az"]], 1)[tg]
+        assert norm_err(a, ref["grav_a"], ref["grav_S"]) <= TOL_FORCE
+        T = ref["targets"]
+        assert norm_err(np.stack([gi["ahx"], gi["ahy"], gi["ahz"]], 1)[T], ref["a"], ref["Sa"]) <= TOL_FORCE
+        assert norm_err(gi["dudt"][T], ref["dudt"], ref["Sdu"]) <= TOL_FORCE
