@@ -764,6 +764,225 @@ __global__ void __launch_bounds__(syma::NW * 32, 2) acc_sym_kernel(const AccSymA
     }
 }
 
+// ============================================================== a7 + a8, pair-compacted i-centric variant
+// Same arithmetic as AccPass (each ordered pair once, by its i), but the lanes never idle
+// on out-of-range pairs: a warp tests the exact symmetric predicate for (i, survivor)
+// pairs of its 8 i-particles (cheap), compacts the passing pairs into a per-warp pair
+// ring and evaluates 32 real pairs per step, each lane with its own (i, j); the per-i
+// sums go to shared memory with red.shared.add.f32 (4 per pair).  Summation order
+// within a warp is scheduling dependent (float shared atomics).
+namespace accc {
+constexpr int NW = 8, G = 8, ENT = 64, RING = 64, PRING = 64, REC = 9;
+struct Smem {
+    float4 raw[ENT * JMAX];
+    float4 pay[ENT * JMAX * REC];
+    float4 ebox[ENT][2];
+    float4 eoff[ENT];
+    int ecnt[ENT];
+    uint64_t bar;
+    uint16_t went[NW][ENT];
+    uint16_t rslot[NW][RING];
+    uint32_t pring[NW][PRING];
+    float4 ipos[NW][G];
+    float4 irec[NW][G][REC];
+    float acc[NW][G][4];
+};
+}  // namespace accc
+
+struct AccCmpArgs {
+    const float4* gpos;
+    const float4* grec;
+    const int32_t* gas_idx;
+    const int32_t* ifirst;
+    const int32_t* icount;
+    const int32_t* row_off;
+    const int2* erec;
+    const float4* box8;
+    float L[3];
+    float Cl, Cq, e2, dt;
+    float *ahx, *ahy, *ahz, *dudt, *vx, *vy, *vz, *u;
+};
+
+__device__ __forceinline__ void red_shared_add(float* p, float v) {
+    asm volatile("red.shared.add.f32 [%0], %1;" ::"r"(smem_u32(p)), "f"(v) : "memory");
+}
+
+__global__ void __launch_bounds__(accc::NW * 32, 2) acc_cmp_kernel(const AccCmpArgs A) {
+    using namespace accc;
+    extern __shared__ __align__(128) unsigned char smem_raw[];
+    Smem& sm = *reinterpret_cast<Smem*>(smem_raw);
+    const int a = blockIdx.x;
+    const int ifirst = A.ifirst[a];
+    const int icount = A.icount[a];
+    const int warp = threadIdx.x >> 5;
+    const int lane = threadIdx.x & 31;
+    const int ibase = warp * G;
+    const bool wactive = ibase < icount;
+    const int gself = ifirst + ibase;
+    const int ng = min(G, icount - ibase);
+    uint16_t* rslot = sm.rslot[warp];
+    uint16_t* went = sm.went[warp];
+    uint32_t* pring = sm.pring[warp];
+
+    if (threadIdx.x == 0) {
+        mbar_init(&sm.bar, 1);
+        mbar_fence_init();
+    }
+    float lo[3] = {0.f, 0.f, 0.f}, hi[3] = {0.f, 0.f, 0.f}, wcut = 0.f;
+    if (wactive) {
+        const bool iv = lane < ng;
+        float4 p = make_float4(-1e18f, -1e18f, -1e18f, 1.f);
+        if (iv) p = A.gpos[gself + lane];
+        if (lane < G) sm.ipos[warp][lane] = p;
+        for (int t = lane; t < G * REC; t += 32) {
+            const int i = t / REC;
+            sm.irec[warp][i][t % REC] = i < ng ? A.grec[(int64_t)(gself + i) * REC + t % REC]
+                                               : make_float4(0.f, 0.f, 0.f, 0.f);
+        }
+        sm.acc[warp][lane >> 2][lane & 3] = 0.f;
+        lo[0] = warp_min(iv ? p.x : INFINITY);
+        lo[1] = warp_min(iv ? p.y : INFINITY);
+        lo[2] = warp_min(iv ? p.z : INFINITY);
+        hi[0] = warp_max(iv ? p.x : -INFINITY);
+        hi[1] = warp_max(iv ? p.y : -INFINITY);
+        hi[2] = warp_max(iv ? p.z : -INFINITY);
+        wcut = warp_max(iv ? __fmul_rn(p.w, p.w) : 0.f) * CULL_SLACK;
+    }
+    const float Cl = A.Cl, Cq = A.Cq, e2 = A.e2;
+
+    // evaluate pairs [prd, prd + n) of the pair ring, one per lane
+    auto eval_pairs = [&](int prd, int n) {
+        if (lane < n) {
+            const uint32_t pr = pring[(prd + lane) & (PRING - 1)];
+            const int i = pr & 7;
+            const int t = pr >> 3;
+            const float4 o = sm.eoff[t / JMAX];
+            const float4 jr = sm.raw[t];
+            const float4 ip = sm.ipos[warp][i];
+            const float x[3] = {ip.x - (jr.x + o.x), ip.y - (jr.y + o.y), ip.z - (jr.z + o.z)};  // x_ij
+            const float r2 = s32_of(x[0], x[1], x[2]);
+            Rec ri, rj;
+            unpack_rec(sm.irec[warp][i], ri);
+            unpack_rec(sm.pay + t * REC, rj);
+            float F[3], Ei, Ej;
+            pair_terms(ri, rj, x, r2, Cl, Cq, e2, F, Ei, Ej);
+            float* ac = sm.acc[warp][i];
+            red_shared_add(ac + 0, -F[0]);
+            red_shared_add(ac + 1, -F[1]);
+            red_shared_add(ac + 2, -F[2]);
+            red_shared_add(ac + 3, Ei);
+        }
+    };
+
+    int wr = 0, rd = 0, pw = 0, prd = 0;
+    // test up to 4 survivors [rd, rd + ns) against the 8 i's: lane = i + 8 s
+    auto test_pairs = [&](int ns) {
+        const int i = lane & 7, s = lane >> 3;
+        bool keep = false;
+        int t = 0;
+        if (s < ns && i < ng) {
+            t = rslot[(rd + s) & (RING - 1)];
+            const float4 o = sm.eoff[t / JMAX];
+            const float4 jr = sm.raw[t];
+            const float4 ip = sm.ipos[warp][i];
+            const float dx = ip.x - (jr.x + o.x), dy = ip.y - (jr.y + o.y), dz = ip.z - (jr.z + o.z);
+            const float r2 = s32_of(dx, dy, dz);
+            const int j = __float_as_int(o.w) + t % JMAX;
+            keep = j != gself + i && r2 < fmaxf(__fmul_rn(ip.w, ip.w), __fmul_rn(jr.w, jr.w));
+        }
+        const unsigned m = __ballot_sync(0xffffffffu, keep);
+        if (keep) pring[(pw + __popc(m & ((1u << lane) - 1u))) & (PRING - 1)] = (uint32_t)i | ((uint32_t)t << 3);
+        pw += __popc(m);
+        rd += ns;
+        __syncwarp();
+        if (pw - prd >= 32) {
+            eval_pairs(prd, 32);
+            prd += 32;
+        }
+        __syncwarp();
+    };
+
+    uint32_t phase = 0;
+    const int rbeg = A.row_off[a], rend = A.row_off[a + 1];
+    for (int e0 = rbeg; e0 < rend; e0 += ENT) {
+        const int nent = min(ENT, rend - e0);
+        __syncthreads();
+        for (int t = threadIdx.x; t < nent; t += NW * 32) {
+            int first, count, leaf, code;
+            unpack_entry(__ldg(A.erec + e0 + t), first, count, leaf, code);
+            int sx, sy, sz;
+            decode_shift(code, sx, sy, sz);
+            sm.eoff[t] = make_float4((float)sx * A.L[0], (float)sy * A.L[1], (float)sz * A.L[2], __int_as_float(first));
+            sm.ecnt[t] = count;
+            const uint32_t pb = (uint32_t)count * 16u;
+            mbar_expect_tx(&sm.bar, pb * (1 + REC) + 32u);
+            bulk_g2s(&sm.raw[t * JMAX], A.gpos + first, pb, &sm.bar);
+            bulk_g2s(&sm.pay[t * JMAX * REC], A.grec + (int64_t)first * REC, pb * REC, &sm.bar);
+            bulk_g2s(&sm.ebox[t][0], A.box8 + 2 * (int64_t)leaf, 32u, &sm.bar);
+        }
+        __syncthreads();
+        if (threadIdx.x == 0) mbar_arrive(&sm.bar);
+        mbar_wait(&sm.bar, phase);
+        phase ^= 1u;
+        if (wactive) {
+            int nsurv = 0;
+            for (int e = lane; e - lane < nent; e += 32) {
+                bool ek = false;
+                if (e < nent) {
+                    const float4 o = sm.eoff[e];
+                    const float4 bl = sm.ebox[e][0], bh = sm.ebox[e][1];
+                    const float gx = fmaxf(fmaxf(bl.x + o.x - hi[0], lo[0] - bh.x - o.x), 0.f);
+                    const float gy = fmaxf(fmaxf(bl.y + o.y - hi[1], lo[1] - bh.y - o.y), 0.f);
+                    const float gz = fmaxf(fmaxf(bl.z + o.z - hi[2], lo[2] - bh.z - o.z), 0.f);
+                    ek = fmaf(gz, gz, fmaf(gy, gy, gx * gx)) < fmaxf(wcut, bl.w * CULL_SLACK);
+                }
+                const unsigned em = __ballot_sync(0xffffffffu, ek);
+                if (ek) went[nsurv + __popc(em & ((1u << lane) - 1u))] = (uint16_t)e;
+                nsurv += __popc(em);
+            }
+            __syncwarp();
+            for (int q0 = 0; q0 < nsurv; q0 += 32 / JMAX) {
+                const int qe = q0 + lane / JMAX;
+                const int kk = lane % JMAX;
+                const int e = went[qe < nsurv ? qe : 0];
+                const float4 o = sm.eoff[e];
+                const int t = e * JMAX + kk;
+                float4 p = sm.raw[t];
+                p.x += o.x; p.y += o.y; p.z += o.z;
+                const bool keep = qe < nsurv && kk < sm.ecnt[e] &&
+                                  box_dist2(p.x, p.y, p.z, lo, hi) < fmaxf(wcut, __fmul_rn(p.w, p.w) * CULL_SLACK);
+                const unsigned msk = __ballot_sync(0xffffffffu, keep);
+                if (keep) rslot[(wr + __popc(msk & ((1u << lane) - 1u))) & (RING - 1)] = (uint16_t)t;
+                wr += __popc(msk);
+                __syncwarp();
+                while (wr - rd >= 4) test_pairs(4);
+            }
+            if (wr > rd) test_pairs(wr - rd);  // slots are restaged next round: drain everything
+            if (pw > prd) {
+                eval_pairs(prd, pw - prd);
+                prd = pw;
+            }
+            __syncwarp();
+        }
+    }
+    if (wactive && lane < ng) {
+        __syncwarp(__activemask());
+        const int k = gself + lane;
+        const float im = 1.f / sm.irec[warp][lane][8].z;  // 1 / m_i
+        const float a0 = sm.acc[warp][lane][0] * im, a1 = sm.acc[warp][lane][1] * im;
+        const float a2 = sm.acc[warp][lane][2] * im, du = sm.acc[warp][lane][3] * im;
+        const int64_t i = A.gas_idx[k];
+        if (A.ahx) { A.ahx[i] = a0; A.ahy[i] = a1; A.ahz[i] = a2; }
+        if (A.dudt) A.dudt[i] = du;
+        if (A.dt != 0.f) {
+            A.vx[i] = fmaf(A.dt, a0, A.vx[i]);
+            A.vy[i] = fmaf(A.dt, a1, A.vy[i]);
+            A.vz[i] = fmaf(A.dt, a2, A.vz[i]);
+            A.u[i] = fmaf(A.dt, du, A.u[i]);
+        }
+    }
+}
+
 // caller outputs and kicks from the (a, du/dt) accumulator (gas-rank order)
 __global__ void k_acc_finish(int64_t ng, const float4* __restrict__ acc, const int32_t* __restrict__ gas_idx, float dt,
                              float* ahx, float* ahy, float* ahz, float* dudt, float* vx, float* vy, float* vz,
@@ -903,8 +1122,32 @@ static crk_status accel_sym(crk_ctx* c, crk_particles* p, float dt, cudaStream_t
     return CRK_OK;
 }
 
+static crk_status accel_cmp(crk_ctx* c, crk_particles* p, float dt, cudaStream_t st) {
+    if (c->nleaf[2] == 0) return CRK_OK;
+    AccCmpArgs A;
+    A.gpos = P<float4>(c->gpos);
+    A.grec = P<float4>(c->grec);
+    A.gas_idx = P<int32_t>(c->gas_idx);
+    A.ifirst = P<int32_t>(c->lfirst[2]);
+    A.icount = P<int32_t>(c->lcount[2]);
+    A.row_off = P<int32_t>(c->rowoff[1]);
+    A.erec = P<int2>(c->erec[1]);
+    A.box8 = P<float4>(c->lbox8[3]);
+    for (int d = 0; d < 3; ++d) A.L[d] = c->lay.L[d];
+    A.Cl = c->prm.av_cl; A.Cq = c->prm.av_cq; A.e2 = c->prm.av_eps2; A.dt = dt;
+    A.ahx = p->ahx; A.ahy = p->ahy; A.ahz = p->ahz; A.dudt = p->dudt;
+    A.vx = p->vx; A.vy = p->vy; A.vz = p->vz; A.u = p->u;
+    const int smem = (int)sizeof(accc::Smem);
+    cudaError_t e = cudaFuncSetAttribute(acc_cmp_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+    if (e != cudaSuccess) return cuda_check(c, e, "smem attribute");
+    acc_cmp_kernel<<<(unsigned)c->nleaf[2], accc::NW * 32, smem, st>>>(A);
+    CRK_LAUNCHED(c, "accel/dudt (pair-compacted) kernel");
+    return CRK_OK;
+}
+
 crk_status accel_dudt(crk_ctx* c, crk_particles* p, float dt, cudaStream_t st) {
     if (dt != 0.f && (!p->vx || !p->vy || !p->vz || !p->u)) return fail(c, CRK_EINVAL, "kick needs v and u");
+    if (c->prm.symmetric & 4) return accel_cmp(c, p, dt, st);
     if ((c->prm.symmetric & 2) && !c->lay.partial) return accel_sym(c, p, dt, st);
     AccPass<false> g;
     common(c, g);

@@ -63,8 +63,8 @@ def test_sort_leaves_lists_bit_exact(name):
             assert np.array_equal(x[0], y[0]) and np.array_equal(x[1], y[1]), (m, a)
 
 
-@pytest.mark.parametrize("name,sym", [("c1", 3), ("c1", 0), ("lat:32,16,16:0.1:3", 3), ("c2u", 0), ("c2z", 3),
-                                      ("c2z", 0)])
+@pytest.mark.parametrize("name,sym", [("c1", 3), ("c1", 0), ("c1", 4), ("lat:32,16,16:0.1:3", 3), ("c2u", 0),
+                                      ("c2z", 3), ("c2z", 0), ("c2z", 5)])
 def test_counts_and_full_chain(name, sym):
     parts, params = cached_config(name)
     params["symmetric"] = sym
