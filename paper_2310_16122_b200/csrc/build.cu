@@ -165,6 +165,32 @@ __global__ void k_leaf_fill(int64_t ncm, const int32_t* __restrict__ cstart, con
     }
 }
 
+// bbox (+ max H^2) of big leaves (i-leaf sets): one warp per leaf, lanes stride the members
+__global__ void k_leaf_bbox_warp(int64_t nl, const int32_t* __restrict__ first, const int32_t* __restrict__ count,
+                                 const float4* __restrict__ pts, int gas, float* bbox, float* maxh2, float4* box8) {
+    const int64_t l = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5;
+    const int lane = threadIdx.x & 31;
+    if (l >= nl) return;
+    float lo0 = INFINITY, lo1 = INFINITY, lo2 = INFINITY, hi0 = -INFINITY, hi1 = -INFINITY, hi2 = -INFINITY, mh = 0.f;
+    const int f = first[l], c = count[l];
+    for (int t = lane; t < c; t += 32) {
+        const float4 p = pts[f + t];
+        lo0 = fminf(lo0, p.x); lo1 = fminf(lo1, p.y); lo2 = fminf(lo2, p.z);
+        hi0 = fmaxf(hi0, p.x); hi1 = fmaxf(hi1, p.y); hi2 = fmaxf(hi2, p.z);
+        if (gas) mh = fmaxf(mh, __fmul_rn(p.w, p.w));
+    }
+    lo0 = warp_min(lo0); lo1 = warp_min(lo1); lo2 = warp_min(lo2);
+    hi0 = warp_max(hi0); hi1 = warp_max(hi1); hi2 = warp_max(hi2);
+    mh = warp_max(mh);
+    if (lane == 0) {
+        float* b = bbox + 6 * l;
+        b[0] = lo0; b[1] = lo1; b[2] = lo2; b[3] = hi0; b[4] = hi1; b[5] = hi2;
+        if (gas) maxh2[l] = mh;
+        box8[2 * l] = make_float4(lo0, lo1, lo2, mh);
+        box8[2 * l + 1] = make_float4(hi0, hi1, hi2, 0.f);
+    }
+}
+
 // bbox (+ max H^2) per leaf; one thread per leaf, members contiguous in xm / gpos
 __global__ void k_leaf_bbox(int64_t nl, const int32_t* __restrict__ first, const int32_t* __restrict__ count,
                             const float4* __restrict__ pts, int gas, float* bbox, float* maxh2, float4* box8) {
@@ -326,7 +352,8 @@ __global__ void __launch_bounds__(LIST_WARPS * 32) k_lists(ListArgs A) {
                     }
                     b = s_b0[w][lo] + (u - s_ex[w][lo]);
                     cd = s_code[w][lo];
-                    const float* bb = A.bboxB + 6 * (int64_t)b;
+                    const float4 blo = __ldg(A.box8B + 2 * (int64_t)b), bhi = __ldg(A.box8B + 2 * (int64_t)b + 1);
+                    const float bb[6] = {blo.x, blo.y, blo.z, bhi.x, bhi.y, bhi.z};
                     int sx, sy, sz;
                     decode_shift(cd, sx, sy, sz);
                     const float sL[3] = {(float)sx * A.Lf[0], (float)sy * A.Lf[1], (float)sz * A.Lf[2]};
@@ -339,7 +366,7 @@ __global__ void __launch_bounds__(LIST_WARPS * 32) k_lists(ListArgs A) {
                         const uint32_t k = (uint32_t)(g * A.inv_q);     // exact integer < 2^24
                         K += (uint64_t)k * k;
                     }
-                    const float cut2 = A.mode == 0 ? A.rcut2 : fmaxf(mh2a, A.maxh2B[b]);
+                    const float cut2 = A.mode == 0 ? A.rcut2 : fmaxf(mh2a, blo.w);
                     keep = (double)K < (double)cut2 * A.q2inv_slack;
                 }
                 const unsigned msk = __ballot_sync(0xffffffffu, keep);
@@ -408,6 +435,7 @@ static ListArgs list_args(crk_ctx* c, int m) {
     A.jfirst = P<int32_t>(c->lfirst[sb]);
     A.jcount = P<int32_t>(c->lcount[sb]);
     A.erec = P<int2>(c->erec[m]);
+    A.box8B = P<float4>(c->lbox8[sb]);
     return A;
 }
 
@@ -525,7 +553,13 @@ crk_status build_lists(crk_ctx* c, crk_particles* p, cudaStream_t st) {
                                                       dom, P<int32_t>(c->lfirst[s]), P<int32_t>(c->lcount[s]),
                                                       P<uint64_t>(c->lcell[s]));
         CRK_LAUNCHED(c, "leaf fill");
-        if (c->nleaf[s] > 0) {
+        if (c->nleaf[s] > 0 && (s == 0 || s == 2)) {
+            k_leaf_bbox_warp<<<nblk(c->nleaf[s] * 32, 256), 256, 0, st>>>(
+                c->nleaf[s], P<int32_t>(c->lfirst[s]), P<int32_t>(c->lcount[s]),
+                s < 2 ? P<float4>(c->xm) : P<float4>(c->gpos), s >= 2, P<float>(c->lbbox[s]),
+                s >= 2 ? P<float>(c->lmaxh2[s]) : nullptr, P<float4>(c->lbox8[s]));
+            CRK_LAUNCHED(c, "leaf bbox");
+        } else if (c->nleaf[s] > 0) {
             k_leaf_bbox<<<nblk(c->nleaf[s], 128), 128, 0, st>>>(
                 c->nleaf[s], P<int32_t>(c->lfirst[s]), P<int32_t>(c->lcount[s]),
                 s < 2 ? P<float4>(c->xm) : P<float4>(c->gpos), s >= 2, P<float>(c->lbbox[s]),
