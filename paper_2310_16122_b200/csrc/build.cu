@@ -261,6 +261,7 @@ struct ListArgs {
     const int32_t* jfirst;  // j-leaf first member / count (packed entry records)
     const int32_t* jcount;
     int2* erec;
+    const float4* box8B;    // padded j-leaf boxes (lo, max H^2), (hi, 0)
 };
 
 __device__ __forceinline__ void put_entry(const ListArgs& A, int p, int b, int code) {
