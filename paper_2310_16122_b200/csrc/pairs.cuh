@@ -43,8 +43,8 @@ struct PairSmem {
     float4 ebox[ENT][2];
     float4 eoff[ENT];  // shift offset (x, y, z), first (w, as int)
     int ecnt[ENT];
-    uint64_t bar[(ENT + 31) / 32];  // one per 32-entry block: warps start on block 0 while the rest lands
-    uint16_t went[NW][32];
+    uint64_t bar;
+    uint16_t went[NW][ENT];
     float4 rpos[NW][RING];     // survivors: shifted position
     uint16_t rslot[NW][RING];  // survivors: staged slot (payload, j index)
 };
@@ -73,9 +73,8 @@ __global__ void __launch_bounds__(NW * 32, MINB) pair_kernel(const Pass pass, co
     uint16_t* rslot = sm.rslot[warp];
     uint16_t* went = sm.went[warp];
 
-    constexpr int NBLK = (ENT + 31) / 32;
     if (threadIdx.x == 0) {
-        for (int b = 0; b < NBLK; ++b) mbar_init(&sm.bar[b], 1);
+        mbar_init(&sm.bar, 1);
         mbar_fence_init();
     }
     typename Pass::I is;
@@ -117,7 +116,7 @@ __global__ void __launch_bounds__(NW * 32, MINB) pair_kernel(const Pass pass, co
     };
 
     int wr = 0, rd = 0;
-    uint32_t phase = 0;  // one parity bit per block barrier
+    uint32_t phase = 0;
     const int rbeg = rv.row_off[a], rend = rv.row_off[a + 1];
     for (int e0 = rbeg; e0 < rend; e0 += ENT) {
         const int nent = min(ENT, rend - e0);
@@ -131,44 +130,46 @@ __global__ void __launch_bounds__(NW * 32, MINB) pair_kernel(const Pass pass, co
                                      __int_as_float(first));
             sm.ecnt[t] = count;
             const uint32_t pb = (uint32_t)count * 16u;
-            uint64_t* bar = &sm.bar[t >> 5];
-            mbar_expect_tx(bar, pb * (1 + Pass::PAY) + 32u);
-            bulk_g2s(&sm.raw[t * JMAX], pass.jrows + first, pb, bar);
+            mbar_expect_tx(&sm.bar, pb * (1 + Pass::PAY) + 32u);
+            bulk_g2s(&sm.raw[t * JMAX], pass.jrows + first, pb, &sm.bar);
             if (Pass::PAY > 0)
-                bulk_g2s(&sm.pay[t * JMAX * Pass::PAY], pass.jpay + (int64_t)first * Pass::PAY, pb * Pass::PAY, bar);
-            bulk_g2s(&sm.ebox[t][0], rv.box8 + 2 * (int64_t)leaf, 32u, bar);
+                bulk_g2s(&sm.pay[t * JMAX * Pass::PAY], pass.jpay + (int64_t)first * Pass::PAY, pb * Pass::PAY,
+                         &sm.bar);
+            bulk_g2s(&sm.ebox[t][0], rv.box8 + 2 * (int64_t)leaf, 32u, &sm.bar);
         }
         __syncthreads();
-        if (threadIdx.x < (nent + 31) / 32) mbar_arrive(&sm.bar[threadIdx.x]);
-        for (int b0 = 0; b0 < nent; b0 += 32) {  // block by block, as the copies land
-            mbar_wait(&sm.bar[b0 >> 5], (phase >> (b0 >> 5)) & 1u);
-            if (!wactive) continue;
-            // (1) leaf prefilter over this block
-            const int e = b0 + lane;
-            bool ek = false;
-            if (e < nent) {
-                const float4 o = sm.eoff[e];
-                const float4 bl = sm.ebox[e][0], bh = sm.ebox[e][1];
-                const float gx = fmaxf(fmaxf(bl.x + o.x - hi[0], lo[0] - bh.x - o.x), 0.f);
-                const float gy = fmaxf(fmaxf(bl.y + o.y - hi[1], lo[1] - bh.y - o.y), 0.f);
-                const float gz = fmaxf(fmaxf(bl.z + o.z - hi[2], lo[2] - bh.z - o.z), 0.f);
-                const float d2 = fmaf(gz, gz, fmaf(gy, gy, gx * gx));
-                ek = d2 < (Pass::SYM ? fmaxf(wcut, bl.w * CULL_SLACK) : wcut);
+        if (threadIdx.x == 0) mbar_arrive(&sm.bar);
+        mbar_wait(&sm.bar, phase);
+        phase ^= 1u;
+        if (wactive) {
+            // (1) leaf prefilter
+            int nsurv = 0;
+            for (int e = lane; e - lane < nent; e += 32) {
+                bool ek = false;
+                if (e < nent) {
+                    const float4 o = sm.eoff[e];
+                    const float4 bl = sm.ebox[e][0], bh = sm.ebox[e][1];
+                    const float gx = fmaxf(fmaxf(bl.x + o.x - hi[0], lo[0] - bh.x - o.x), 0.f);
+                    const float gy = fmaxf(fmaxf(bl.y + o.y - hi[1], lo[1] - bh.y - o.y), 0.f);
+                    const float gz = fmaxf(fmaxf(bl.z + o.z - hi[2], lo[2] - bh.z - o.z), 0.f);
+                    const float d2 = fmaf(gz, gz, fmaf(gy, gy, gx * gx));
+                    ek = d2 < (Pass::SYM ? fmaxf(wcut, bl.w * CULL_SLACK) : wcut);
+                }
+                const unsigned em = __ballot_sync(0xffffffffu, ek);
+                if (ek) went[nsurv + __popc(em & ((1u << lane) - 1u))] = (uint16_t)e;
+                nsurv += __popc(em);
             }
-            const unsigned em = __ballot_sync(0xffffffffu, ek);
-            if (ek) went[__popc(em & ((1u << lane) - 1u))] = (uint16_t)e;
-            const int nsurv = __popc(em);
             __syncwarp();
             // (2) particle filter into the survivor ring, evaluation whenever >= 32 wait
             for (int q0 = 0; q0 < nsurv; q0 += 32 / JMAX) {
                 const int qe = q0 + lane / JMAX;
                 const int kk = lane % JMAX;
-                const int ee = went[qe < nsurv ? qe : 0];
-                const float4 o = sm.eoff[ee];
-                const int t = ee * JMAX + kk;
+                const int e = went[qe < nsurv ? qe : 0];
+                const float4 o = sm.eoff[e];
+                const int t = e * JMAX + kk;
                 float4 p = sm.raw[t];
                 p.x += o.x; p.y += o.y; p.z += o.z;
-                bool keep = qe < nsurv && kk < sm.ecnt[ee];
+                bool keep = qe < nsurv && kk < sm.ecnt[e];
                 if (keep) {
                     const float d2 = box_dist2(p.x, p.y, p.z, lo, hi);
                     keep = d2 < (Pass::SYM ? fmaxf(wcut, pass.jcut(p) * CULL_SLACK) : wcut);
@@ -187,13 +188,11 @@ __global__ void __launch_bounds__(NW * 32, MINB) pair_kernel(const Pass pass, co
                     __syncwarp();
                 }
             }
-            __syncwarp();
-        }
-        phase ^= (nent + 31) / 32 >= 32 ? 0xffffffffu : ((1u << ((nent + 31) / 32)) - 1u);  // blocks used
-        if (wactive && e0 + ENT < rend && wr > rd) {  // slots are restaged next round: flush the ring
-            eval(rd, wr - rd);
-            rd = wr;
-            __syncwarp();
+            if (e0 + ENT < rend && wr > rd) {  // slots are restaged next round: flush the ring
+                eval(rd, wr - rd);
+                rd = wr;
+                __syncwarp();
+            }
         }
     }
     if (wactive) {
