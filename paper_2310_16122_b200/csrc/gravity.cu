@@ -109,7 +109,7 @@ struct Smem {
     RowBuf rb[NB];           // NB = 2: the next work item's row streams in during this one
     uint64_t bar[2];
     int next_item;
-    float4 ipos[NW][G];
+    float2 inx[NW][G / 2], iny[NW][G / 2], inz[NW][G / 2], im[NW][G / 2];  // (i, i + 8) pairs, -x
     float4 wpos[NW][RING];
     int widx[NW][RING];
     uint16_t went[NW][ENT];
@@ -211,7 +211,13 @@ __global__ void __launch_bounds__(NW * 32, 16 / NW) grav_sym_kernel(const GravSy
             const bool iv = lane < ng;
             float4 p = make_float4(-1e18f, -1e18f, -1e18f, 0.f);  // far sentinel: finite products
             if (iv) p = A.xm[gself + lane];
-            if (lane < G) sm.ipos[warp][lane] = p;
+            if (lane < G) {  // packed (i, i + G/2) pairs of negated positions for FADD2
+                const int k = 2 * (lane % (G / 2)) + lane / (G / 2);
+                reinterpret_cast<float*>(sm.inx[warp])[k] = -p.x;
+                reinterpret_cast<float*>(sm.iny[warp])[k] = -p.y;
+                reinterpret_cast<float*>(sm.inz[warp])[k] = -p.z;
+                reinterpret_cast<float*>(sm.im[warp])[k] = p.w;
+            }
             lo[0] = warp_min(iv ? p.x : INFINITY);
             lo[1] = warp_min(iv ? p.y : INFINITY);
             lo[2] = warp_min(iv ? p.z : INFINITY);
@@ -220,11 +226,15 @@ __global__ void __launch_bounds__(NW * 32, 16 / NW) grav_sym_kernel(const GravSy
             hi[2] = warp_max(iv ? p.z : -INFINITY);
         }
         __syncwarp();
-        float ax[G], ay[G], az[G];
+        // i-side sums, packed: component .x is i = k, .y is i = k + G/2
+        float2 ax[G / 2], ay[G / 2], az[G / 2];
 #pragma unroll
-        for (int i = 0; i < G; ++i) ax[i] = ay[i] = az[i] = 0.f;
+        for (int k = 0; k < G / 2; ++k) ax[k] = ay[k] = az[k] = make_float2(0.f, 0.f);
 
-        // one warp step over ring slots [r0, r0 + n): lane owns one survivor, loops over the group
+        // one warp step over ring slots [r0, r0 + n): lane owns one survivor and evaluates
+        // its pairs with the group two at a time in packed FP32 (FFMA2 / FADD2 / FMUL2: one
+        // issue slot per two pairs; every op still rounds per component, so the O2 predicate
+        // is bit-identical to the scalar form)
         auto eval_step = [&](int r0, int n) {
             float4 jp = make_float4(1e18f, 1e18f, 1e18f, 0.f);
             int j = 0;
@@ -235,26 +245,38 @@ __global__ void __launch_bounds__(NW * 32, 16 / NW) grav_sym_kernel(const GravSy
             }
             // own group: the i-side half is counted when the partner is the survivor
             const float mj = (j >= gself && j < gself + ng) ? 0.f : jp.w;
-            float bx = 0.f, by = 0.f, bz = 0.f;
+            const float2 jx = make_float2(jp.x, jp.x), jy = make_float2(jp.y, jp.y), jz = make_float2(jp.z, jp.z);
+            const float2 mj2 = make_float2(mj, mj), e22 = make_float2(e2, e2);
+            const float2 n0 = make_float2(-c0, -c0), n1 = make_float2(-c1, -c1), n2 = make_float2(-c2, -c2);
+            const float2 n3 = make_float2(-c3, -c3), n4 = make_float2(-c4, -c4), n5 = make_float2(-c5, -c5);
+            float2 bx = make_float2(0.f, 0.f), by = bx, bz = bx;
 #pragma unroll
-            for (int i = 0; i < G; ++i) {
-                const float4 ip = sm.ipos[warp][i];
-                const float dx = jp.x - ip.x, dy = jp.y - ip.y, dz = jp.z - ip.z;  // x_j - x_i
-                const float r2 = s32_of(dx, dy, dz);
-                const float ri = rsqrtf(r2 + e2);
-                const float ri3 = ri * ri * ri;
-                const float p5 = fmaf(fmaf(fmaf(fmaf(fmaf(c5, r2, c4), r2, c3), r2, c2), r2, c1), r2, c0);
-                const float wgt = r2 < rc2 ? ri3 - p5 : 0.f;
-                const float wi = mj * wgt;  // i-side: a_i += m_j w x_ji
-                ax[i] = fmaf(wi, dx, ax[i]);
-                ay[i] = fmaf(wi, dy, ay[i]);
-                az[i] = fmaf(wi, dz, az[i]);
-                const float wj = ip.w * wgt;  // j-side: a_j += m_i w x_ij
-                bx = fmaf(-wj, dx, bx);
-                by = fmaf(-wj, dy, by);
-                bz = fmaf(-wj, dz, bz);
+            for (int k = 0; k < G / 2; ++k) {
+                const float2 dx = __fadd2_rn(jx, sm.inx[warp][k]);  // x_j - x_i, exact (O1)
+                const float2 dy = __fadd2_rn(jy, sm.iny[warp][k]);
+                const float2 dz = __fadd2_rn(jz, sm.inz[warp][k]);
+                const float2 r2 = __ffma2_rn(dz, dz, __ffma2_rn(dy, dy, __fmul2_rn(dx, dx)));  // O2 order
+                const float2 re = __fadd2_rn(r2, e22);
+                const float2 ri = make_float2(rsqrtf(re.x), rsqrtf(re.y));
+                const float2 ri2 = __fmul2_rn(ri, ri);
+                float2 np5 = __ffma2_rn(n5, r2, n4);  // -P5(s)
+                np5 = __ffma2_rn(np5, r2, n3);
+                np5 = __ffma2_rn(np5, r2, n2);
+                np5 = __ffma2_rn(np5, r2, n1);
+                np5 = __ffma2_rn(np5, r2, n0);
+                float2 w = __ffma2_rn(ri2, ri, np5);  // (s + eps2)^-3/2 - P5(s)
+                w.x = r2.x < rc2 ? w.x : 0.f;
+                w.y = r2.y < rc2 ? w.y : 0.f;
+                const float2 wi = __fmul2_rn(mj2, w);  // i-side: a_i += m_j w x_ji
+                ax[k] = __ffma2_rn(wi, dx, ax[k]);
+                ay[k] = __ffma2_rn(wi, dy, ay[k]);
+                az[k] = __ffma2_rn(wi, dz, az[k]);
+                const float2 wj = __fmul2_rn(sm.im[warp][k], w);  // j-side: a_j -= m_i w x_ji
+                bx = __ffma2_rn(wj, dx, bx);
+                by = __ffma2_rn(wj, dy, by);
+                bz = __ffma2_rn(wj, dz, bz);
             }
-            if (lane < n) red_add_v4(A.acc + j, bx, by, bz, 0.f);
+            if (lane < n) red_add_v4(A.acc + j, -(bx.x + bx.y), -(by.x + by.y), -(bz.x + bz.y), 0.f);
         };
 
         int wr = 0, rd = 0;  // ring write / read counters
@@ -316,9 +338,11 @@ __global__ void __launch_bounds__(NW * 32, 16 / NW) grav_sym_kernel(const GravSy
         if (wactive) {
             if (wr > rd) eval_step(rd, wr - rd);
 #pragma unroll
-            for (int i = 0; i < G; ++i) {
-                const float sx = warp_sum(ax[i]), sy = warp_sum(ay[i]), sz = warp_sum(az[i]);
-                if (lane == i && i < ng) red_add_v4(A.acc + gself + i, sx, sy, sz, 0.f);
+            for (int k = 0; k < G / 2; ++k) {
+                const float sx0 = warp_sum(ax[k].x), sy0 = warp_sum(ay[k].x), sz0 = warp_sum(az[k].x);
+                const float sx1 = warp_sum(ax[k].y), sy1 = warp_sum(ay[k].y), sz1 = warp_sum(az[k].y);
+                if (lane == k && k < ng) red_add_v4(A.acc + gself + k, sx0, sy0, sz0, 0.f);
+                if (lane == k + G / 2 && k + G / 2 < ng) red_add_v4(A.acc + gself + k + G / 2, sx1, sy1, sz1, 0.f);
             }
         }
         __syncthreads();  // buffer b is free for the item after next
