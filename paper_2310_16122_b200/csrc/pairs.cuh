@@ -12,6 +12,8 @@
 // register accumulation and one shuffle reduction over the slots at the end: no atomics.
 // Periodic shifts are added to the staged positions (exact, O1).
 #pragma once
+#include <type_traits>
+
 #include "common.cuh"
 
 namespace crk {
@@ -35,6 +37,12 @@ struct RowView {
 //   float jcut(const float4& jp)   (SYM only: j's H^2 from its staged row)
 //   void pair(const I&, Acc&, const float4& jp, const float4* pay, int j)
 //   template<int G> void reduce(Acc&) ; void finish(int i, const I&, const Acc&)
+// passes that declare `static constexpr bool PAIR2 = true` provide pair2(): two survivors at once
+template <class Pass, class = void>
+struct has_pair2 : std::false_type {};
+template <class Pass>
+struct has_pair2<Pass, std::enable_if_t<Pass::PAIR2>> : std::true_type {};
+
 template <class Pass, int NW, int ENT>
 struct PairSmem {
     static constexpr int RING = 64;
@@ -97,14 +105,24 @@ __global__ void __launch_bounds__(NW * 32, MINB) pair_kernel(const Pass pass, co
     auto eval = [&](int rd, int n) {
         constexpr int U = Pass::UNROLL;
         int k = sl;
+        if constexpr (has_pair2<Pass>::value) {  // two survivors per packed-FP32 evaluation
 #pragma unroll 1
-        for (; k + (U - 1) * S < n; k += U * S) {
+            for (; k + S < n; k += 2 * S) {
+                const int s0 = (rd + k) & (RING - 1), s1 = (rd + k + S) & (RING - 1);
+                const int t0 = rslot[s0], t1 = rslot[s1];
+                pass.pair2(is, acc, rpos[s0], sm.pay + t0 * Pass::PAY, __float_as_int(sm.eoff[t0 / JMAX].w) + t0 % JMAX,
+                           rpos[s1], sm.pay + t1 * Pass::PAY, __float_as_int(sm.eoff[t1 / JMAX].w) + t1 % JMAX);
+            }
+        } else {
+#pragma unroll 1
+            for (; k + (U - 1) * S < n; k += U * S) {
 #pragma unroll
-            for (int u = 0; u < U; ++u) {
-                const int s = (rd + k + u * S) & (RING - 1);
-                const int t = rslot[s];
-                pass.pair(is, acc, rpos[s], sm.pay + t * Pass::PAY,
-                          __float_as_int(sm.eoff[t / JMAX].w) + t % JMAX);
+                for (int u = 0; u < U; ++u) {
+                    const int s = (rd + k + u * S) & (RING - 1);
+                    const int t = rslot[s];
+                    pass.pair(is, acc, rpos[s], sm.pay + t * Pass::PAY,
+                              __float_as_int(sm.eoff[t / JMAX].w) + t % JMAX);
+                }
             }
         }
 #pragma unroll 1
