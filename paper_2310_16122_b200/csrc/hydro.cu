@@ -125,21 +125,18 @@ struct CorPass : HydCommon {
     int64_t ng;
     float *A, *B, *dA, *dB;  // caller planes (n)
     int64_t n;
-    static constexpr bool PAIR2 = true;
     struct I { float x, y, z, H2, invH; };
-    // packed partial sums: component .x from the first of two pairs, .y from the second
     struct Acc {
-        float2 m0, m1[3], m2[6], g0[3], g1[6], g2[10];
+        float m0, m1[3], m2[6], g0[3], g1[6], g2[10];
     };
     __device__ void init(Acc& a) const {
-        const float2 z = make_float2(0.f, 0.f);
-        a.m0 = z;
+        a.m0 = 0.f;
 #pragma unroll
-        for (int t = 0; t < 3; ++t) a.m1[t] = a.g0[t] = z;
+        for (int t = 0; t < 3; ++t) a.m1[t] = a.g0[t] = 0.f;
 #pragma unroll
-        for (int t = 0; t < 6; ++t) a.m2[t] = a.g1[t] = z;
+        for (int t = 0; t < 6; ++t) a.m2[t] = a.g1[t] = 0.f;
 #pragma unroll
-        for (int t = 0; t < 10; ++t) a.g2[t] = z;
+        for (int t = 0; t < 10; ++t) a.g2[t] = 0.f;
     }
     __device__ void load_i(int k, I& s) const { load_pos(gpos, k, s.x, s.y, s.z, s.H2, s.invH); }
     __device__ float ix(const I& s) const { return s.x; }
@@ -147,33 +144,6 @@ struct CorPass : HydCommon {
     __device__ float iz(const I& s) const { return s.z; }
     __device__ float cut(const I& s) const { return s.H2; }
     __device__ float jcut(const float4&) const { return 0.f; }
-    // moment sums with d = x_j - x_i for w = V_j W~ and gw = V_j g~ (both packed)
-    __device__ __forceinline__ void accum(Acc& a, float2 w, float2 gw, float2 d0, float2 d1, float2 d2) const {
-        const float2 wd0 = __fmul2_rn(w, d0), wd1 = __fmul2_rn(w, d1), wd2 = __fmul2_rn(w, d2);
-        a.m0 = __fadd2_rn(a.m0, w);
-        a.m1[0] = __fadd2_rn(a.m1[0], wd0); a.m1[1] = __fadd2_rn(a.m1[1], wd1); a.m1[2] = __fadd2_rn(a.m1[2], wd2);
-        a.m2[0] = __ffma2_rn(wd0, d0, a.m2[0]); a.m2[1] = __ffma2_rn(wd0, d1, a.m2[1]);
-        a.m2[2] = __ffma2_rn(wd0, d2, a.m2[2]); a.m2[3] = __ffma2_rn(wd1, d1, a.m2[3]);
-        a.m2[4] = __ffma2_rn(wd1, d2, a.m2[4]); a.m2[5] = __ffma2_rn(wd2, d2, a.m2[5]);
-        const float2 gd0 = __fmul2_rn(gw, d0), gd1 = __fmul2_rn(gw, d1), gd2 = __fmul2_rn(gw, d2);
-        a.g0[0] = __fadd2_rn(a.g0[0], gd0); a.g0[1] = __fadd2_rn(a.g0[1], gd1); a.g0[2] = __fadd2_rn(a.g0[2], gd2);
-        a.g1[0] = __ffma2_rn(gd0, d0, a.g1[0]); a.g1[1] = __ffma2_rn(gd0, d1, a.g1[1]);
-        a.g1[2] = __ffma2_rn(gd0, d2, a.g1[2]); a.g1[3] = __ffma2_rn(gd1, d1, a.g1[3]);
-        a.g1[4] = __ffma2_rn(gd1, d2, a.g1[4]); a.g1[5] = __ffma2_rn(gd2, d2, a.g1[5]);
-        const float2 e00 = __fmul2_rn(gd0, d0), e01 = __fmul2_rn(gd0, d1), e11 = __fmul2_rn(gd1, d1);
-        const float2 e02 = __fmul2_rn(gd0, d2), e12 = __fmul2_rn(gd1, d2), e22 = __fmul2_rn(gd2, d2);
-        // fully symmetric third moment d_a d_b d_g gw: index set 000,001,002,011,012,022,111,112,122,222
-        a.g2[0] = __ffma2_rn(e00, d0, a.g2[0]);
-        a.g2[1] = __ffma2_rn(e00, d1, a.g2[1]);
-        a.g2[2] = __ffma2_rn(e00, d2, a.g2[2]);
-        a.g2[3] = __ffma2_rn(e01, d1, a.g2[3]);
-        a.g2[4] = __ffma2_rn(e01, d2, a.g2[4]);
-        a.g2[5] = __ffma2_rn(e02, d2, a.g2[5]);
-        a.g2[6] = __ffma2_rn(e11, d1, a.g2[6]);
-        a.g2[7] = __ffma2_rn(e11, d2, a.g2[7]);
-        a.g2[8] = __ffma2_rn(e12, d2, a.g2[8]);
-        a.g2[9] = __ffma2_rn(e22, d2, a.g2[9]);
-    }
     __device__ __forceinline__ void pair(const I& s, Acc& a, const float4& jp, const float4*, int) const {
         const float d0 = jp.x - s.x, d1 = jp.y - s.y, d2 = jp.z - s.z;
         const float r2 = s32_of(d0, d1, d2);
@@ -182,35 +152,37 @@ struct CorPass : HydCommon {
         const bool in = r2 < s.H2;
         const float w = in ? jp.w * wt : 0.f;
         const float gw = in ? jp.w * gt : 0.f;  // (times 1/H^2 in finish)
-        accum(a, make_float2(w, 0.f), make_float2(gw, 0.f), make_float2(d0, 0.f), make_float2(d1, 0.f),
-              make_float2(d2, 0.f));
-    }
-    __device__ __forceinline__ void pair2(const I& s, Acc& a, const float4& p0, const float4*, int,
-                                          const float4& p1, const float4*, int) const {
-        const float2 d0 = make_float2(p0.x - s.x, p1.x - s.x), d1 = make_float2(p0.y - s.y, p1.y - s.y),
-                     d2 = make_float2(p0.z - s.z, p1.z - s.z);
-        const float2 r2 = s32_of2(d0, d1, d2);
-        float2 wt, gt;
-        wendland_t2(r2, s.invH, wt, gt);
-        const bool in0 = r2.x < s.H2, in1 = r2.y < s.H2;
-        const float2 V = make_float2(p0.w, p1.w);
-        accum(a, f2sel(in0, in1, __fmul2_rn(V, wt)), f2sel(in0, in1, __fmul2_rn(V, gt)), d0, d1, d2);
+        const float wd0 = w * d0, wd1 = w * d1, wd2 = w * d2;
+        a.m0 += w;
+        a.m1[0] += wd0; a.m1[1] += wd1; a.m1[2] += wd2;
+        a.m2[0] = fmaf(wd0, d0, a.m2[0]); a.m2[1] = fmaf(wd0, d1, a.m2[1]); a.m2[2] = fmaf(wd0, d2, a.m2[2]);
+        a.m2[3] = fmaf(wd1, d1, a.m2[3]); a.m2[4] = fmaf(wd1, d2, a.m2[4]); a.m2[5] = fmaf(wd2, d2, a.m2[5]);
+        const float gd0 = gw * d0, gd1 = gw * d1, gd2 = gw * d2;
+        a.g0[0] += gd0; a.g0[1] += gd1; a.g0[2] += gd2;
+        a.g1[0] = fmaf(gd0, d0, a.g1[0]); a.g1[1] = fmaf(gd0, d1, a.g1[1]); a.g1[2] = fmaf(gd0, d2, a.g1[2]);
+        a.g1[3] = fmaf(gd1, d1, a.g1[3]); a.g1[4] = fmaf(gd1, d2, a.g1[4]); a.g1[5] = fmaf(gd2, d2, a.g1[5]);
+        const float e00 = gd0 * d0, e01 = gd0 * d1, e11 = gd1 * d1;
+        // fully symmetric third moment d_a d_b d_g gw: index set 000,001,002,011,012,022,111,112,122,222
+        a.g2[0] = fmaf(e00, d0, a.g2[0]);
+        a.g2[1] = fmaf(e00, d1, a.g2[1]);
+        a.g2[2] = fmaf(e00, d2, a.g2[2]);
+        a.g2[3] = fmaf(e01, d1, a.g2[3]);
+        a.g2[4] = fmaf(e01, d2, a.g2[4]);
+        a.g2[5] = fmaf(gd0 * d2, d2, a.g2[5]);
+        a.g2[6] = fmaf(e11, d1, a.g2[6]);
+        a.g2[7] = fmaf(e11, d2, a.g2[7]);
+        a.g2[8] = fmaf(gd1 * d2, d2, a.g2[8]);
+        a.g2[9] = fmaf(gd2 * d2, d2, a.g2[9]);
     }
     template <int GG>
     __device__ void reduce(Acc& a) const {
-        a.m0.x = slot_sum<GG>(a.m0.x + a.m0.y);
+        a.m0 = slot_sum<GG>(a.m0);
 #pragma unroll
-        for (int t = 0; t < 3; ++t) {
-            a.m1[t].x = slot_sum<GG>(a.m1[t].x + a.m1[t].y);
-            a.g0[t].x = slot_sum<GG>(a.g0[t].x + a.g0[t].y);
-        }
+        for (int t = 0; t < 3; ++t) { a.m1[t] = slot_sum<GG>(a.m1[t]); a.g0[t] = slot_sum<GG>(a.g0[t]); }
 #pragma unroll
-        for (int t = 0; t < 6; ++t) {
-            a.m2[t].x = slot_sum<GG>(a.m2[t].x + a.m2[t].y);
-            a.g1[t].x = slot_sum<GG>(a.g1[t].x + a.g1[t].y);
-        }
+        for (int t = 0; t < 6; ++t) { a.m2[t] = slot_sum<GG>(a.m2[t]); a.g1[t] = slot_sum<GG>(a.g1[t]); }
 #pragma unroll
-        for (int t = 0; t < 10; ++t) a.g2[t].x = slot_sum<GG>(a.g2[t].x + a.g2[t].y);
+        for (int t = 0; t < 10; ++t) a.g2[t] = slot_sum<GG>(a.g2[t]);
     }
     __device__ static int s2(int a, int b) {  // symmetric 3x3 index
         if (a > b) { int t = a; a = b; b = t; }
@@ -231,22 +203,22 @@ struct CorPass : HydCommon {
         const float c = SIGMA_W * s.invH * s.invH * s.invH;
         const float cg = c * s.invH * s.invH;
         // moments in x_ij = -d convention (O7), delta terms added here
-        const float m0 = c * a.m0.x;
+        const float m0 = c * a.m0;
         float m1[3], m2[3][3], g0[3], g1[3][3], g2[3][3][3];
 #pragma unroll
         for (int p = 0; p < 3; ++p) {
-            m1[p] = -c * a.m1[p].x;
-            g0[p] = -cg * a.g0[p].x;
+            m1[p] = -c * a.m1[p];
+            g0[p] = -cg * a.g0[p];
         }
 #pragma unroll
         for (int p = 0; p < 3; ++p)
 #pragma unroll
             for (int q = 0; q < 3; ++q) {
-                m2[p][q] = c * a.m2[s2(p, q)].x;
-                g1[p][q] = cg * a.g1[s2(p, q)].x + (p == q ? m0 : 0.f);
+                m2[p][q] = c * a.m2[s2(p, q)];
+                g1[p][q] = cg * a.g1[s2(p, q)] + (p == q ? m0 : 0.f);
 #pragma unroll
                 for (int g = 0; g < 3; ++g)
-                    g2[p][q][g] = -cg * a.g2[s3(p, q, g)].x + (p == g ? m1[q] : 0.f) + (q == g ? m1[p] : 0.f);
+                    g2[p][q][g] = -cg * a.g2[s3(p, q, g)] + (p == g ? m1[q] : 0.f) + (q == g ? m1[p] : 0.f);
             }
         // fp32 cofactor inverse of m2
         const float c00 = m2[1][1] * m2[2][2] - m2[1][2] * m2[2][1];
@@ -1116,7 +1088,7 @@ crk_status corrections(crk_ctx* c, crk_particles* p, cudaStream_t st) {
     g.A = p->A; g.B = p->B; g.dA = p->dA; g.dB = p->dB;
     g.n = c->n;
     if (hyd_variant(1) == 1) return launch_hyd<CorPass, 128, 1, 16, 4>(c, g, st, "corrections kernel");
-    return launch_hyd<CorPass, 128, 2>(c, g, st, "corrections kernel");
+    return launch_hyd<CorPass, 128, 3>(c, g, st, "corrections kernel");
 }
 
 __global__ void k_gather_gas_state(int64_t ng, const int32_t* gas_idx, const float* vx, const float* vy,
