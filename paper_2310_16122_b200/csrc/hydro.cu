@@ -544,137 +544,6 @@ struct AccPass : HydCommon {
     }
 };
 
-// ============================================================== a7 + a8, packed i/j halves (default)
-// Same pairs and arithmetic as AccPass, but the pair's two symmetric halves — the i-side
-// gradient with i's coefficients and the j-side gradient with j's, the two limiter
-// projections, the two AV terms — are evaluated together in packed FP32 (FFMA2 / FADD2 /
-// FMUL2): component .x carries i (set once per lane), .y carries j (loaded per pair).
-struct RP2 {  // accel record, packed: .x = i, .y = j
-    float2 invH, Ah, V, P, B[3], rho, dAh[3], cs, dB[9], v[3], dv[9];
-};
-
-__device__ __forceinline__ void load_y(const float4* r, RP2& q) {  // j's record into the .y halves
-    const float* f = reinterpret_cast<const float*>(r);
-    q.invH.y = f[0]; q.Ah.y = f[1]; q.V.y = f[2]; q.P.y = f[3];
-    q.B[0].y = f[4]; q.B[1].y = f[5]; q.B[2].y = f[6]; q.rho.y = f[7];
-    q.dAh[0].y = f[8]; q.dAh[1].y = f[9]; q.dAh[2].y = f[10]; q.cs.y = f[11];
-#pragma unroll
-    for (int t = 0; t < 9; ++t) q.dB[t].y = f[12 + t];
-    q.v[0].y = f[21]; q.v[1].y = f[22]; q.v[2].y = f[23];
-#pragma unroll
-    for (int t = 0; t < 9; ++t) q.dv[t].y = f[24 + t];
-}
-
-template <bool DUMMY = false>
-struct AccPass2 : HydCommon {
-    static constexpr int PAY = 9;
-    static constexpr bool SYM = true;
-    static constexpr int UNROLL = 1;
-    const float4* jrows;  // gpos (x, y, z, H)
-    const float4* jpay;   // grec
-    const float4* grec;
-    float Cl, Cq, e2, dt;
-    int64_t n;
-    float *ahx, *ahy, *ahz, *dudt, *vx, *vy, *vz, *u;
-    struct I { float x, y, z, H2, m; RP2 r; };
-    struct Acc { float a[3], du; };
-    __device__ void init(Acc& a) const { a.a[0] = a.a[1] = a.a[2] = a.du = 0.f; }
-    __device__ void load_i(int k, I& s) const {
-        const float4 p = gpos[k];
-        s.x = p.x; s.y = p.y; s.z = p.z;
-        const float* f = reinterpret_cast<const float*>(grec + (int64_t)k * 9);
-        RP2& q = s.r;
-        q.invH.x = f[0]; q.Ah.x = f[1]; q.V.x = f[2]; q.P.x = f[3];
-        q.B[0].x = f[4]; q.B[1].x = f[5]; q.B[2].x = f[6]; q.rho.x = f[7];
-        q.dAh[0].x = f[8]; q.dAh[1].x = f[9]; q.dAh[2].x = f[10]; q.cs.x = f[11];
-#pragma unroll
-        for (int t = 0; t < 9; ++t) q.dB[t].x = f[12 + t];
-        q.v[0].x = f[21]; q.v[1].x = f[22]; q.v[2].x = f[23];
-#pragma unroll
-        for (int t = 0; t < 9; ++t) q.dv[t].x = f[24 + t];
-        s.H2 = f[33];
-        s.m = f[34];
-    }
-    __device__ float ix(const I& s) const { return s.x; }
-    __device__ float iy(const I& s) const { return s.y; }
-    __device__ float iz(const I& s) const { return s.z; }
-    __device__ float cut(const I& s) const { return s.H2; }
-    __device__ float jcut(const float4& jp) const { return __fmul_rn(jp.w, jp.w); }
-    __device__ __forceinline__ void pair(I& s, Acc& acc, const float4& jp, const float4* pay, int) const {
-        const float x0 = s.x - jp.x, x1 = s.y - jp.y, x2 = s.z - jp.z;  // x_ij
-        const float r2 = s32_of(x0, x1, x2);
-        if (!(r2 < fmaxf(s.H2, __fmul_rn(jp.w, jp.w)))) return;
-        RP2& q = s.r;
-        load_y(pay, q);
-        const float r = sqrtf(r2);
-        // the two corrected-kernel gradients: i at x_ij (.x), j at x_ji = -x_ij (.y)
-        const float2 X0 = make_float2(x0, -x0), X1 = make_float2(x1, -x1), X2 = make_float2(x2, -x2);
-        const float2 qq = __fmul2_rn(f2(r), q.invH);
-        const float2 t = make_float2(fmaxf(1.f - qq.x, 0.f), fmaxf(1.f - qq.y, 0.f));
-        const float2 t2 = __fmul2_rn(t, t);
-        const float2 t5 = __fmul2_rn(__fmul2_rn(t2, t2), t);
-        const float2 wt = __fmul2_rn(__fmul2_rn(t5, t), __ffma2_rn(qq, __ffma2_rn(qq, f2(35.f / 3.f), f2(6.f)), f2(1.f)));
-        const float2 gt = __fmul2_rn(__fmul2_rn(__fmul2_rn(f2(-56.f / 3.f), __fmul2_rn(q.invH, q.invH)), t5),
-                                     __ffma2_rn(f2(5.f), qq, f2(1.f)));
-        const float2 lin = __ffma2_rn(q.B[2], X2, __ffma2_rn(q.B[1], X1, __ffma2_rn(q.B[0], X0, f2(1.f))));
-        const float2 alg = __fmul2_rn(__fmul2_rn(q.Ah, lin), gt);
-        const float2 Xg[3] = {X0, X1, X2};
-        float G[3];
-#pragma unroll
-        for (int g = 0; g < 3; ++g) {
-            const float2 t1 = __ffma2_rn(q.dB[6 + g], X2, __ffma2_rn(q.dB[3 + g], X1, __ffma2_rn(q.dB[g], X0, q.B[g])));
-            const float2 o = __ffma2_rn(wt, __ffma2_rn(q.dAh[g], lin, __fmul2_rn(q.Ah, t1)), __fmul2_rn(alg, Xg[g]));
-            G[g] = 0.5f * (o.x - o.y);
-        }
-        // limiter on x.grad v.x (both with x_ij)
-        const float2 xx0 = f2(x0), xx1 = f2(x1), xx2 = f2(x2);
-        float2 gv[3];
-#pragma unroll
-        for (int p = 0; p < 3; ++p)
-            gv[p] = __ffma2_rn(q.dv[3 * p + 2], xx2, __ffma2_rn(q.dv[3 * p + 1], xx1, __fmul2_rn(q.dv[3 * p], xx0)));
-        const float2 xg = __ffma2_rn(xx2, gv[2], __ffma2_rn(xx1, gv[1], __fmul2_rn(xx0, gv[0])));
-        const float pr = xg.x * xg.y, sm = xg.x + xg.y;
-        const float phi = pr > 0.f ? fminf(1.f, 4.f * pr / (sm * sm)) : 0.f;
-        float vij[3], vs[3];
-#pragma unroll
-        for (int p = 0; p < 3; ++p) {
-            vij[p] = q.v[p].x - q.v[p].y;
-            vs[p] = vij[p] - 0.5f * phi * (gv[p].x + gv[p].y);
-        }
-        const float vsx = vs[0] * x0 + vs[1] * x1 + vs[2] * x2;
-        const float2 den = __ffma2_rn(f2(r2), __fmul2_rn(q.invH, q.invH), f2(e2));
-        const float2 num = __fmul2_rn(f2(vsx), q.invH);
-        const float2 mu = make_float2(fminf(0.f, num.x / den.x), fminf(0.f, num.y / den.y));
-        const float2 Qk = __fmul2_rn(__fmul2_rn(q.rho, mu), __ffma2_rn(f2(Cq), mu, __fmul2_rn(f2(-Cl), q.cs)));
-        const float Q = Qk.x + Qk.y;
-        const float fa = -q.V.y * (q.P.x + q.P.y + Q);
-        const float fu = q.V.y * (q.P.x + 0.5f * Q) * (vij[0] * G[0] + vij[1] * G[1] + vij[2] * G[2]);
-        acc.a[0] = fmaf(fa, G[0], acc.a[0]);
-        acc.a[1] = fmaf(fa, G[1], acc.a[1]);
-        acc.a[2] = fmaf(fa, G[2], acc.a[2]);
-        acc.du += fu;
-    }
-    template <int GG>
-    __device__ void reduce(Acc& a) const {
-#pragma unroll
-        for (int t = 0; t < 3; ++t) a.a[t] = slot_sum<GG>(a.a[t]);
-        a.du = slot_sum<GG>(a.du);
-    }
-    __device__ void finish(int k, const I& s, const Acc& a) const {
-        const int64_t i = gas_idx[k];
-        const float f = s.r.V.x / s.m;
-        const float a0 = f * a.a[0], a1 = f * a.a[1], a2 = f * a.a[2], du = f * a.du;
-        if (ahx) { ahx[i] = a0; ahy[i] = a1; ahz[i] = a2; }
-        if (dudt) dudt[i] = du;
-        if (dt != 0.f) {
-            vx[i] = fmaf(dt, a0, vx[i]);
-            vy[i] = fmaf(dt, a1, vy[i]);
-            vz[i] = fmaf(dt, a2, vz[i]);
-            u[i] = fmaf(dt, du, u[i]);
-        }
-    }
-};
-
 // ============================================================== a7 + a8, symmetric (Newton-3) variant
 // Every unordered gas pair is evaluated once (G_ij, Q_ij, the limiter and the pressure
 // terms are shared by both sides): by the warp of the lower 8-particle group (groups are
@@ -1311,18 +1180,6 @@ crk_status accel_dudt(crk_ctx* c, crk_particles* p, float dt, cudaStream_t st) {
     if (dt != 0.f && (!p->vx || !p->vy || !p->vz || !p->u)) return fail(c, CRK_EINVAL, "kick needs v and u");
     if (c->prm.symmetric & 4) return accel_cmp(c, p, dt, st);
     if ((c->prm.symmetric & 2) && !c->lay.partial) return accel_sym(c, p, dt, st);
-    if (!getenv("CRK_ACC_SCALAR")) {
-        AccPass2<> g2;
-        common(c, g2);
-        g2.jrows = P<float4>(c->gpos);
-        g2.jpay = P<float4>(c->grec);
-        g2.grec = P<float4>(c->grec);
-        g2.Cl = c->prm.av_cl; g2.Cq = c->prm.av_cq; g2.e2 = c->prm.av_eps2; g2.dt = dt;
-        g2.n = c->n;
-        g2.ahx = p->ahx; g2.ahy = p->ahy; g2.ahz = p->ahz; g2.dudt = p->dudt;
-        g2.vx = p->vx; g2.vy = p->vy; g2.vz = p->vz; g2.u = p->u;
-        return launch_hyd<AccPass2<>, 72, 2>(c, g2, st, "accel/dudt kernel");
-    }
     AccPass<false> g;
     common(c, g);
     g.jrows = P<float4>(c->gpos);
