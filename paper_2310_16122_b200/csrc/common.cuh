@@ -171,4 +171,25 @@ __device__ __forceinline__ void unpack_entry(int2 r, int& first, int& count, int
     leaf = r.y & 0x03ffffff;
     code = (unsigned)r.y >> 26;
 }
+// Row staging in runs: consecutive list entries that are consecutive full j-leaves of the
+// same cell under the same shift are contiguous in memory (and their slots contiguous in
+// the staged tile), so one bulk copy serves the whole run.  Returns the run length of
+// the run starting at entry e (e must be a run start) and whether e starts a run.
+__device__ __forceinline__ bool entry_continues(int2 prev, int2 cur) {
+    int pf, pc, pl, ps, cf, cc, cl, cx;
+    unpack_entry(prev, pf, pc, pl, ps);
+    unpack_entry(cur, cf, cc, cl, cx);
+    return pc == JMAX && ps == cx && cl == pl + 1 && cf == pf + JMAX;
+}
+__device__ __forceinline__ int run_length(const int2* erec, int e, int end) {
+    int len = 1;
+    int2 prev = __ldg(erec + e);
+    while (e + len < end) {
+        const int2 cur = __ldg(erec + e + len);
+        if (!entry_continues(prev, cur)) break;
+        prev = cur;
+        ++len;
+    }
+    return len;
+}
 }  // namespace crk

@@ -146,9 +146,14 @@ __device__ __forceinline__ void grav_stage(typename symg::Cfg<NW, ENT, NB>::Smem
         decode_shift(code, sx, sy, sz);
         sm.rb[b].eoff[t] = make_float4((float)sx * A.L[0], (float)sy * A.L[1], (float)sz * A.L[2], __int_as_float(first));
         sm.rb[b].ecnt[t] = count;
-        bulk_g2s(&sm.rb[b].raw[t * JMAX], A.xm + first, (uint32_t)count * 16u, &sm.bar[b]);
-        bulk_g2s(&sm.rb[b].ebox[t][0], A.box8 + 2 * (int64_t)leaf, 32u, &sm.bar[b]);
-        bytes += (uint32_t)count * 16u + 32u;
+        if (t > 0 && entry_continues(__ldg(A.erec + e0 + t - 1), __ldg(A.erec + e0 + t))) continue;
+        const int len = run_length(A.erec, e0 + t, e0 + nent);  // one copy per contiguous run
+        int lf, lc, ll, lx;
+        unpack_entry(__ldg(A.erec + e0 + t + len - 1), lf, lc, ll, lx);
+        const uint32_t pb = (uint32_t)(JMAX * (len - 1) + lc) * 16u;
+        bulk_g2s(&sm.rb[b].raw[t * JMAX], A.xm + first, pb, &sm.bar[b]);
+        bulk_g2s(&sm.rb[b].ebox[t][0], A.box8 + 2 * (int64_t)leaf, 32u * len, &sm.bar[b]);
+        bytes += pb + 32u * len;
     }
     mbar_arrive_expect_tx(&sm.bar[b], bytes);
 }
