@@ -147,17 +147,13 @@ __global__ void __launch_bounds__(NW * 32, MINB) pair_kernel(const Pass pass, co
             sm.eoff[t] = make_float4((float)sx * rv.L[0], (float)sy * rv.L[1], (float)sz * rv.L[2],
                                      __int_as_float(first));
             sm.ecnt[t] = count;
-            if (t > 0 && entry_continues(__ldg(rv.erec + e0 + t - 1), __ldg(rv.erec + e0 + t))) continue;
-            const int len = run_length(rv.erec, e0 + t, e0 + nent);  // one copy per contiguous run
-            int lf, lc, ll, lx;
-            unpack_entry(__ldg(rv.erec + e0 + t + len - 1), lf, lc, ll, lx);
-            const uint32_t pb = (uint32_t)(JMAX * (len - 1) + lc) * 16u;
-            mbar_expect_tx(&sm.bar, pb * (1 + Pass::PAY) + 32u * len);
+            const uint32_t pb = (uint32_t)count * 16u;
+            mbar_expect_tx(&sm.bar, pb * (1 + Pass::PAY) + 32u);
             bulk_g2s(&sm.raw[t * JMAX], pass.jrows + first, pb, &sm.bar);
             if (Pass::PAY > 0)
                 bulk_g2s(&sm.pay[t * JMAX * Pass::PAY], pass.jpay + (int64_t)first * Pass::PAY, pb * Pass::PAY,
                          &sm.bar);
-            bulk_g2s(&sm.ebox[t][0], rv.box8 + 2 * (int64_t)leaf, 32u * len, &sm.bar);
+            bulk_g2s(&sm.ebox[t][0], rv.box8 + 2 * (int64_t)leaf, 32u, &sm.bar);
         }
         __syncthreads();
         if (threadIdx.x == 0) mbar_arrive(&sm.bar);
