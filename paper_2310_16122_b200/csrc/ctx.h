@@ -77,7 +77,6 @@ struct crk_ctx {
     crk::Buf grec;               // accel records: 9 float4 per gas particle
     crk::Buf gu;                 // float
     crk::Buf gacc;               // float4 force accumulator (symmetric kernels)
-    crk::Buf gkey;               // int32 group key per particle (symmetric gravity)
     crk::Buf pinned;             // host pinned totals
     crk::Buf sel_flag, sel_mask; // selection scratch
     crk::Buf work;               // dynamic work counters of the persistent kernels
