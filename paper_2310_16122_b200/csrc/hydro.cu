@@ -339,10 +339,11 @@ struct ExtPass : HydCommon {
         // x_ij = x_i - x_j
         const float x0 = s.x - jp.x, x1 = s.y - jp.y, x2 = s.z - jp.z;
         const float r2 = s32_of(x0, x1, x2);
-        if (!(r2 < s.H2)) return;
+        const bool in = r2 < s.H2;  // branch-free: out-of-range pairs add exact zeros
         float wt, gt;
         wendland_t(r2, s.invH, wt, gt);
-        gt *= s.invH * s.invH;
+        wt = in ? wt : 0.f;
+        gt = in ? gt * (s.invH * s.invH) : 0.f;
         const float lin = 1.f + s.B[0] * x0 + s.B[1] * x1 + s.B[2] * x2;
         const float4 vj = pay[0];
         a.rho = fmaf(vj.w, s.A * lin * wt, a.rho);
