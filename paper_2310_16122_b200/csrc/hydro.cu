@@ -440,11 +440,22 @@ __device__ __forceinline__ void grad_wr(const float* Ah, const float* dAh, const
     }
 }
 
-template <bool COUNT>
+// pair-compacted variants of the gather passes (pairs.cuh batch_of): same arithmetic, the
+// in-range test is the passes' own (s32 < H_i^2)
+template <class Base, int BT>
+struct Compacted : Base {
+    static constexpr int BATCH = BT;
+    __device__ __forceinline__ bool in(const typename Base::I& s, const float4& jp) const {
+        return s32_of(s.x - jp.x, s.y - jp.y, s.z - jp.z) < s.H2;
+    }
+};
+
+template <bool COUNT, int BATCH_ = 32>
 struct AccPass : HydCommon {
     static constexpr int PAY = COUNT ? 0 : 9;
     static constexpr bool SYM = true;
     static constexpr int UNROLL = 1;
+    static constexpr int BATCH = COUNT ? 0 : BATCH_;
     const float4* jrows;  // gpos (x, y, z, H)
     const float4* jpay;   // grec
     const float4* grec;
@@ -466,6 +477,9 @@ struct AccPass : HydCommon {
     __device__ float iz(const I& s) const { return s.z; }
     __device__ float cut(const I& s) const { return s.r.H2; }
     __device__ float jcut(const float4& jp) const { return __fmul_rn(jp.w, jp.w); }
+    __device__ __forceinline__ bool in(const I& s, const float4& jp) const {
+        return s32_of(s.x - jp.x, s.y - jp.y, s.z - jp.z) < fmaxf(s.r.H2, __fmul_rn(jp.w, jp.w));
+    }
     __device__ __forceinline__ void pair(const I& s, Acc& acc, const float4& jp, const float4* pay, int j) const {
         float x[3] = {s.x - jp.x, s.y - jp.y, s.z - jp.z};  // x_ij
         const float r2 = s32_of(x[0], x[1], x[2]);
@@ -1088,8 +1102,12 @@ crk_status corrections(crk_ctx* c, crk_particles* p, cudaStream_t st) {
     g.ng = c->n_gas;
     g.A = p->A; g.B = p->B; g.dA = p->dA; g.dB = p->dB;
     g.n = c->n;
-    if (hyd_variant(1) == 1) return launch_hyd<CorPass, 128, 1, 16, 4>(c, g, st, "corrections kernel");
-    return launch_hyd<CorPass, 128, 3>(c, g, st, "corrections kernel");
+    switch (hyd_variant(1)) {
+        case 1: return launch_hyd<CorPass, 128, 1, 16, 4>(c, g, st, "corrections kernel");
+        case 2: return launch_hyd<Compacted<CorPass, 32>, 128, 3>(c, {g}, st, "corrections kernel");
+        case 3: return launch_hyd<Compacted<CorPass, 64>, 128, 3>(c, {g}, st, "corrections kernel");
+        default: return launch_hyd<CorPass, 128, 3>(c, g, st, "corrections kernel");
+    }
 }
 
 __global__ void k_gather_gas_state(int64_t ng, const int32_t* gas_idx, const float* vx, const float* vy,
@@ -1119,8 +1137,12 @@ crk_status extras(crk_ctx* c, crk_particles* p, cudaStream_t st) {
     g.n = c->n;
     g.gamma = c->prm.gamma;
     g.rho = p->rho; g.P = p->P; g.cs = p->cs; g.dv = p->dv;
-    if (hyd_variant(2) == 1) return launch_hyd<ExtPass, 128, 1, 16, 4>(c, g, st, "extras kernel");
-    return launch_hyd<ExtPass, 128, 3>(c, g, st, "extras kernel");
+    switch (hyd_variant(2)) {
+        case 1: return launch_hyd<ExtPass, 128, 1, 16, 4>(c, g, st, "extras kernel");
+        case 2: return launch_hyd<Compacted<ExtPass, 32>, 128, 3>(c, {g}, st, "extras kernel");
+        case 3: return launch_hyd<Compacted<ExtPass, 64>, 128, 3>(c, {g}, st, "extras kernel");
+        default: return launch_hyd<ExtPass, 128, 3>(c, g, st, "extras kernel");
+    }
 }
 
 static crk_status accel_sym(crk_ctx* c, crk_particles* p, float dt, cudaStream_t st) {
@@ -1177,11 +1199,9 @@ static crk_status accel_cmp(crk_ctx* c, crk_particles* p, float dt, cudaStream_t
     return CRK_OK;
 }
 
-crk_status accel_dudt(crk_ctx* c, crk_particles* p, float dt, cudaStream_t st) {
-    if (dt != 0.f && (!p->vx || !p->vy || !p->vz || !p->u)) return fail(c, CRK_EINVAL, "kick needs v and u");
-    if (c->prm.symmetric & 4) return accel_cmp(c, p, dt, st);
-    if ((c->prm.symmetric & 2) && !c->lay.partial) return accel_sym(c, p, dt, st);
-    AccPass<false> g;
+template <int BT, int ENT>
+static crk_status accel_gather(crk_ctx* c, crk_particles* p, float dt, cudaStream_t st) {
+    AccPass<false, BT> g;
     common(c, g);
     g.jrows = P<float4>(c->gpos);
     g.jpay = P<float4>(c->grec);
@@ -1191,8 +1211,19 @@ crk_status accel_dudt(crk_ctx* c, crk_particles* p, float dt, cudaStream_t st) {
     g.ahx = p->ahx; g.ahy = p->ahy; g.ahz = p->ahz; g.dudt = p->dudt;
     g.vx = p->vx; g.vy = p->vy; g.vz = p->vz; g.u = p->u;
     g.cnt = nullptr;
-    if (hyd_variant(3) == 1) return launch_hyd<AccPass<false>, 72, 1, 16, 4>(c, g, st, "accel/dudt kernel");
-    return launch_hyd<AccPass<false>, 72, 2>(c, g, st, "accel/dudt kernel");
+    return launch_hyd<AccPass<false, BT>, ENT, 2>(c, g, st, "accel/dudt kernel");
+}
+
+crk_status accel_dudt(crk_ctx* c, crk_particles* p, float dt, cudaStream_t st) {
+    if (dt != 0.f && (!p->vx || !p->vy || !p->vz || !p->u)) return fail(c, CRK_EINVAL, "kick needs v and u");
+    if (c->prm.symmetric & 4) return accel_cmp(c, p, dt, st);
+    if ((c->prm.symmetric & 2) && !c->lay.partial) return accel_sym(c, p, dt, st);
+    // gather variant: batch-32 pair-compacted evaluation (2: batch 64, 3: uncompacted)
+    switch (hyd_variant(3)) {
+        case 2: return accel_gather<64, 64>(c, p, dt, st);
+        case 3: return accel_gather<0, 72>(c, p, dt, st);
+        default: return accel_gather<32, 72>(c, p, dt, st);
+    }
 }
 
 crk_status hydro_count(crk_ctx* c, int32_t* cgather, int32_t* csym, cudaStream_t st) {

@@ -42,10 +42,19 @@ template <class Pass, class = void>
 struct has_pair2 : std::false_type {};
 template <class Pass>
 struct has_pair2<Pass, std::enable_if_t<Pass::PAIR2>> : std::true_type {};
+// passes that declare `static constexpr int BATCH` (32 or 64) and provide `bool in(const I&, float4 jp)`
+// are evaluated pair-compacted: each batch of ring survivors is first tested against every
+// i-particle of the warp (cheap), and the lanes of i-particle il then share only its in-range
+// survivors, so a warp step does full work on (nearly) every lane instead of idling on
+// out-of-range pairs.
+template <class Pass, class = void>
+struct batch_of : std::integral_constant<int, 0> {};
+template <class Pass>
+struct batch_of<Pass, std::enable_if_t<(Pass::BATCH > 0)>> : std::integral_constant<int, Pass::BATCH> {};
 
 template <class Pass, int NW, int ENT>
 struct PairSmem {
-    static constexpr int RING = 64;
+    static constexpr int RING = batch_of<Pass>::value > 32 ? 128 : 64;
     float4 raw[ENT * JMAX];
     float4 pay[Pass::PAY > 0 ? ENT * JMAX * Pass::PAY : 1];
     float4 ebox[ENT][2];
@@ -101,11 +110,35 @@ __global__ void __launch_bounds__(NW * 32, MINB) pair_kernel(const Pass pass, co
         wcut = warp_max(ivalid ? pass.cut(is) : 0.f) * CULL_SLACK;
     }
 
+    constexpr int BATCH = batch_of<Pass>::value;
+    constexpr int TRIG = BATCH > 32 ? BATCH : 32;  // ring fill that triggers an evaluation
     // evaluate ring survivors [rd, rd + n)
     auto eval = [&](int rd, int n) {
         constexpr int U = Pass::UNROLL;
         int k = sl;
-        if constexpr (has_pair2<Pass>::value) {  // two survivors per packed-FP32 evaluation
+        if constexpr (BATCH > 0) {  // pair-compacted (n <= BATCH)
+            using M = std::conditional_t<(BATCH > 32), unsigned long long, unsigned>;
+            M m = 0;
+            if (ivalid)
+                for (; k < n; k += S)
+                    if (pass.in(is, rpos[(rd + k) & (RING - 1)])) m |= (M)1 << k;
+#pragma unroll
+            for (int o = G; o < 32; o <<= 1) m |= __shfl_xor_sync(0xffffffffu, m, o);
+            // in-range survivors of i-particle il, shared round-robin by its S lanes
+#pragma unroll
+            for (int q = 0; q < S - 1; ++q)
+                if (q < sl) m &= m - 1;
+#pragma unroll 1
+            while (m) {
+                const int kk = (BATCH > 32 ? __ffsll((long long)m) : __ffs((int)m)) - 1;
+#pragma unroll
+                for (int q = 0; q < S; ++q) m &= m - 1;
+                const int s = (rd + kk) & (RING - 1);
+                const int t = rslot[s];
+                pass.pair(is, acc, rpos[s], sm.pay + t * Pass::PAY, __float_as_int(sm.eoff[t / JMAX].w) + t % JMAX);
+            }
+            return;
+        } else if constexpr (has_pair2<Pass>::value) {  // two survivors per packed-FP32 evaluation
 #pragma unroll 1
             for (; k + S < n; k += 2 * S) {
                 const int s0 = (rd + k) & (RING - 1), s1 = (rd + k + S) & (RING - 1);
@@ -139,7 +172,11 @@ __global__ void __launch_bounds__(NW * 32, MINB) pair_kernel(const Pass pass, co
     for (int e0 = rbeg; e0 < rend; e0 += ENT) {
         const int nent = min(ENT, rend - e0);
         __syncthreads();  // barrier initialised / previous round consumed
-        for (int t = threadIdx.x; t < nent; t += NW * 32) {
+        // entry t is issued by warp t % NW: the bulk copies of one warp are issued lane by lane
+        // (uniform operands), so spreading the row over all warps shortens the issue chain NW-fold.
+        // (Merging runs of contiguous full leaves into one copy, as gravity does, measured slower
+        // here: the serial run-length scan sits on the critical path of a one-round row.)
+        for (int t = lane * NW + warp; t < nent; t += NW * 32) {
             int first, count, leaf, code;
             unpack_entry(__ldg(rv.erec + e0 + t), first, count, leaf, code);
             int sx, sy, sz;
@@ -200,9 +237,9 @@ __global__ void __launch_bounds__(NW * 32, MINB) pair_kernel(const Pass pass, co
                 }
                 wr += __popc(msk);
                 __syncwarp();
-                if (wr - rd >= 32) {
-                    eval(rd, 32);
-                    rd += 32;
+                if (wr - rd >= TRIG) {
+                    eval(rd, TRIG);
+                    rd += TRIG;
                     __syncwarp();
                 }
             }
