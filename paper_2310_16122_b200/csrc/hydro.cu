@@ -734,7 +734,7 @@ __global__ void __launch_bounds__(syma::NW * 32, 2) acc_sym_kernel(const AccSymA
     for (int e0 = rbeg; e0 < rend; e0 += ENT) {
         const int nent = min(ENT, rend - e0);
         __syncthreads();
-        for (int t = threadIdx.x; t < nent; t += NW * 32) {
+        for (int t = lane * NW + warp; t < nent; t += NW * 32) {  // spread over warps (pairs.cuh)
             int first, count, leaf, code;
             unpack_entry(__ldg(A.erec + e0 + t), first, count, leaf, code);
             int sx, sy, sz;
@@ -953,7 +953,7 @@ __global__ void __launch_bounds__(accc::NW * 32, 2) acc_cmp_kernel(const AccCmpA
     for (int e0 = rbeg; e0 < rend; e0 += ENT) {
         const int nent = min(ENT, rend - e0);
         __syncthreads();
-        for (int t = threadIdx.x; t < nent; t += NW * 32) {
+        for (int t = lane * NW + warp; t < nent; t += NW * 32) {  // spread over warps (pairs.cuh)
             int first, count, leaf, code;
             unpack_entry(__ldg(A.erec + e0 + t), first, count, leaf, code);
             int sx, sy, sz;
