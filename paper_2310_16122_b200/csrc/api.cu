@@ -4,6 +4,8 @@
 #include <cstring>
 #include <new>
 
+#include <cstdlib>
+
 #include "common.cuh"
 
 namespace crk {
@@ -124,6 +126,10 @@ crk_status crk_create(const crk_params* params, int device, crk_ctx** out) {
     }
     c->pinned.p = h;
     c->pinned.cap = 256;
+    // gas neighbour-list capacity per particle (CRK_NBR_CAP: tests force overflow / 0 = off)
+    const char* nc = getenv("CRK_NBR_CAP");
+    c->nbr_cap = nc ? atoi(nc) : 128;
+    if (c->nbr_cap < 0) c->nbr_cap = 0;
     // the gravity kernel's dynamic shared memory fits in the default 48 KB
     *out = c;
     return CRK_OK;
@@ -136,7 +142,7 @@ crk_status crk_destroy(crk_ctx* c) {
     Buf* bufs[] = {&c->keys_a, &c->keys_b, &c->idx_a, &c->idx_b, &c->cub_tmp, &c->scratch, &c->xm,
                    &c->cell_start, &c->cell_end, &c->leaf_cnt, &c->gflag, &c->grank, &c->gas_idx,
                    &c->dev_scalars, &c->gpos, &c->gvel, &c->gV, &c->gcoef, &c->grec, &c->gu,
-                   &c->gacc, &c->gposV, &c->sel_flag, &c->sel_mask, &c->work};
+                   &c->gacc, &c->gposV, &c->sel_flag, &c->sel_mask, &c->work, &c->nbr, &c->ncnt, &c->lflag};
     for (Buf* b : bufs)
         if (b->p) cudaFree(b->p);
     for (int s = 0; s < 4; ++s) {

@@ -80,4 +80,7 @@ struct crk_ctx {
     crk::Buf pinned;             // host pinned totals
     crk::Buf sel_flag, sel_mask; // selection scratch
     crk::Buf work;               // dynamic work counters of the persistent kernels
+    // gas neighbour lists (geometry -> corrections, extras, accel): pairs.cuh ListView
+    crk::Buf nbr, ncnt, lflag;
+    int nbr_cap = 0;             // entries per gas particle (0: lists off)
 };

@@ -342,13 +342,31 @@ __global__ void __launch_bounds__(NW * 32, 16 / NW) grav_sym_kernel(const GravSy
         }
         if (wactive) {
             if (wr > rd) eval_step(rd, wr - rd);
+            // transposed (reduce-scatter) sum of the 16 x 3 i-side values over the warp:
+            // after the halving steps over lane bits 4..1, lane l holds i = l >> 1 (48 shuffles
+            // instead of 48 full warp sums)
+            float v[3][G];
 #pragma unroll
             for (int k = 0; k < G / 2; ++k) {
-                const float sx0 = warp_sum(ax[k].x), sy0 = warp_sum(ay[k].x), sz0 = warp_sum(az[k].x);
-                const float sx1 = warp_sum(ax[k].y), sy1 = warp_sum(ay[k].y), sz1 = warp_sum(az[k].y);
-                if (lane == k && k < ng) red_add_v4(A.acc + gself + k, sx0, sy0, sz0, 0.f);
-                if (lane == k + G / 2 && k + G / 2 < ng) red_add_v4(A.acc + gself + k + G / 2, sx1, sy1, sz1, 0.f);
+                v[0][k] = ax[k].x; v[0][k + G / 2] = ax[k].y;
+                v[1][k] = ay[k].x; v[1][k + G / 2] = ay[k].y;
+                v[2][k] = az[k].x; v[2][k + G / 2] = az[k].y;
             }
+#pragma unroll
+            for (int h = G / 2; h >= 1; h >>= 1) {  // lane bit (16, 8, 4, 2) <-> i bit (8, 4, 2, 1)
+                const bool up = lane & (2 * h);
+#pragma unroll
+                for (int c = 0; c < 3; ++c)
+#pragma unroll
+                    for (int k = 0; k < h; ++k) {
+                        const float send = up ? v[c][k] : v[c][k + h];
+                        const float keep = up ? v[c][k + h] : v[c][k];
+                        v[c][k] = keep + __shfl_xor_sync(0xffffffffu, send, 2 * h);
+                    }
+            }
+#pragma unroll
+            for (int c = 0; c < 3; ++c) v[c][0] += __shfl_xor_sync(0xffffffffu, v[c][0], 1);
+            if ((lane & 1) == 0 && (lane >> 1) < ng) red_add_v4(A.acc + gself + (lane >> 1), v[0][0], v[1][0], v[2][0], 0.f);
         }
         __syncthreads();  // buffer b is free for the item after next
         if (NB == 2) b ^= 1;

@@ -49,10 +49,14 @@ __device__ __forceinline__ float2 s32_of2(float2 dx, float2 dy, float2 dz) {
 
 // ============================================================== a4 Geometry (upGeo)
 // V_i = 1 / sum_{gas j, s32 < H_i^2, j incl. i} W(r_ij, H_i)
-template <bool COUNT>
+// LIST: also build the gas neighbour lists (pairs.cuh ListView): culling and list use the
+// symmetric predicate s32 < max(H_i^2, H_j^2); V sums only the gather pairs.
+template <bool COUNT, bool LIST = false>
 struct GeoPass : HydCommon {
     static constexpr int PAY = 0;
-    static constexpr bool SYM = false;
+    static constexpr bool SYM = LIST;
+    static constexpr bool BUILD = LIST;
+    ListView lv;
     static constexpr int UNROLL = 4;
     const float4* jrows;  // gpos
     const float4* jpay;
@@ -62,14 +66,22 @@ struct GeoPass : HydCommon {
     int32_t* cnt;
     static constexpr bool PAIR2 = !COUNT;
     struct I { float x, y, z, H2, invH; int idx; };
-    struct Acc { float2 w; int n; };
-    __device__ void init(Acc& a) const { a.w = make_float2(0.f, 0.f); a.n = 0; }
+    struct Acc { float2 w; int n, nl; };
+    __device__ void init(Acc& a) const { a.w = make_float2(0.f, 0.f); a.n = 0; a.nl = 0; }
     __device__ void load_i(int k, I& s) const { load_pos(gpos, k, s.x, s.y, s.z, s.H2, s.invH); s.idx = k; }
     __device__ float ix(const I& s) const { return s.x; }
     __device__ float iy(const I& s) const { return s.y; }
     __device__ float iz(const I& s) const { return s.z; }
     __device__ float cut(const I& s) const { return s.H2; }
-    __device__ float jcut(const float4&) const { return 0.f; }
+    __device__ float jcut(const float4& jp) const { return __fmul_rn(jp.w, jp.w); }
+    __device__ __forceinline__ bool pair_list(const I& s, Acc& a, const float4& jp, int) const {
+        const float dx = jp.x - s.x, dy = jp.y - s.y, dz = jp.z - s.z;
+        const float r2 = s32_of(dx, dy, dz);
+        float wt, gt;
+        wendland_t(r2, s.invH, wt, gt);
+        a.w.x += r2 < s.H2 ? wt : 0.f;
+        return r2 < fmaxf(s.H2, __fmul_rn(jp.w, jp.w));
+    }
     __device__ __forceinline__ void pair(const I& s, Acc& a, const float4& jp, const float4*, int j) const {
         const float dx = jp.x - s.x, dy = jp.y - s.y, dz = jp.z - s.z;
         const float r2 = s32_of(dx, dy, dz);
@@ -1080,7 +1092,48 @@ static void common(crk_ctx* c, HydCommon& h) {
     h.gas_idx = P<int32_t>(c->gas_idx);
 }
 
+static ListView list_view(crk_ctx* c) {
+    ListView lv;
+    lv.nbr = P<uint16_t>(c->nbr);
+    lv.ncnt = P<int32_t>(c->ncnt);
+    lv.lflag = P<uint8_t>(c->lflag);
+    lv.cap = c->nbr_cap;
+    return lv;
+}
+static bool lists_on(crk_ctx* c) { return c->nbr_cap > 0 && c->nleaf[2] > 0; }
+
+// list-driven launch of a gather/accel pass, then the on-the-fly kernel over the rows whose
+// lists are incomplete (flagged by the builder; usually none: those CTAs exit at once)
+template <class Pass, int ENT, int MINB, int FENT, int FMINB>
+static crk_status launch_listed(crk_ctx* c, const Pass& ps, cudaStream_t st, const char* what) {
+    if (c->nleaf[2] == 0) return CRK_OK;
+    RowView rv = hydro_rows(c);
+    CRK_TRY(cuda_check(c, launch_list<Pass, HYD_NW, HYD_G, ENT, MINB>(ps, rv, list_view(c), c->nleaf[2], st), what));
+    c->launches++;
+    rv.only = P<uint8_t>(c->lflag);
+    CRK_TRY(cuda_check(c, launch_pairs<Pass, HYD_NW, HYD_G, FENT, FMINB>(ps, rv, c->nleaf[2], st), what));
+    c->launches++;
+    return CRK_OK;
+}
+
 crk_status geometry(crk_ctx* c, crk_particles* p, cudaStream_t st) {
+    if (lists_on(c)) {
+        GeoPass<false, true> g;
+        common(c, g);
+        g.jrows = P<float4>(c->gpos);
+        g.jpay = nullptr;
+        g.gV = P<float>(c->gV);
+        g.gposV = P<float4>(c->gposV);
+        g.Vout = p->V;
+        g.cnt = nullptr;
+        const int64_t ng = c->n_gas > 0 ? c->n_gas : 1;
+        CRK_TRY(grow(c, c->nbr, (size_t)ng * c->nbr_cap * sizeof(uint16_t), st));
+        CRK_TRY(grow(c, c->ncnt, (size_t)ng * sizeof(int32_t), st));
+        CRK_TRY(grow(c, c->lflag, (size_t)c->nleaf[2], st));
+        CRK_TRY(cuda_check(c, cudaMemsetAsync(c->lflag.p, 0, (size_t)c->nleaf[2], st), "memset"));
+        g.lv = list_view(c);
+        return launch_hyd<GeoPass<false, true>, 128, 2>(c, g, st, "geometry (list build) kernel");
+    }
     GeoPass<false> g;
     common(c, g);
     g.jrows = P<float4>(c->gpos);
@@ -1102,6 +1155,7 @@ crk_status corrections(crk_ctx* c, crk_particles* p, cudaStream_t st) {
     g.ng = c->n_gas;
     g.A = p->A; g.B = p->B; g.dA = p->dA; g.dB = p->dB;
     g.n = c->n;
+    if (lists_on(c)) return launch_listed<CorPass, 128, 3, 128, 3>(c, g, st, "corrections kernel");
     switch (hyd_variant(1)) {
         case 1: return launch_hyd<CorPass, 128, 1, 16, 4>(c, g, st, "corrections kernel");
         case 2: return launch_hyd<Compacted<CorPass, 32>, 128, 3>(c, {g}, st, "corrections kernel");
@@ -1137,6 +1191,7 @@ crk_status extras(crk_ctx* c, crk_particles* p, cudaStream_t st) {
     g.n = c->n;
     g.gamma = c->prm.gamma;
     g.rho = p->rho; g.P = p->P; g.cs = p->cs; g.dv = p->dv;
+    if (lists_on(c)) return launch_listed<ExtPass, 128, 3, 128, 3>(c, g, st, "extras kernel");
     switch (hyd_variant(2)) {
         case 1: return launch_hyd<ExtPass, 128, 1, 16, 4>(c, g, st, "extras kernel");
         case 2: return launch_hyd<Compacted<ExtPass, 32>, 128, 3>(c, {g}, st, "extras kernel");
@@ -1211,6 +1266,7 @@ static crk_status accel_gather(crk_ctx* c, crk_particles* p, float dt, cudaStrea
     g.ahx = p->ahx; g.ahy = p->ahy; g.ahz = p->ahz; g.dudt = p->dudt;
     g.vx = p->vx; g.vy = p->vy; g.vz = p->vz; g.u = p->u;
     g.cnt = nullptr;
+    if (lists_on(c)) return launch_listed<AccPass<false, BT>, 72, 2, ENT, 2>(c, g, st, "accel/dudt kernel");
     return launch_hyd<AccPass<false, BT>, ENT, 2>(c, g, st, "accel/dudt kernel");
 }
 

@@ -25,7 +25,28 @@ struct RowView {
     const int2* erec;     // packed entries (first | (count-1) << 29, leaf | shift << 26)
     const float4* box8;   // padded j-leaf boxes: (lo, max H^2), (hi, 0)
     float L[3];
+    const uint8_t* only = nullptr;  // non-null: run only the rows a with only[a] != 0 (list fallback)
 };
+
+// Per-particle neighbour lists of the gas passes: row-relative staging
+// slots (entry index within the i-leaf's CSR row * JMAX + member), ascending, of every
+// gas j (self included) with s32 < max(H_i^2, H_j^2) — the symmetric predicate, a
+// superset of the gather predicate.  Written by the geometry pass, read by corrections,
+// extras and accel/du-dt.  Rows whose lists overflow `cap` (or whose slots exceed 16
+// bits) are flagged; those rows run the on-the-fly kernels instead.
+struct ListView {
+    uint16_t* nbr;     // [n_gas * cap]
+    int32_t* ncnt;     // [n_gas]
+    uint8_t* lflag;    // [n gas i-leaves]: 1 = lists incomplete, use the on-the-fly path
+    int cap;
+};
+template <int G>
+__device__ __forceinline__ unsigned same_i_lanes(int il) {  // lanes l with l % G == il
+    unsigned m = 0;
+#pragma unroll
+    for (int q = 0; q < 32 / G; ++q) m |= 1u << (il + G * q);
+    return m;
+}
 
 // Pass concept:
 //   static constexpr int PAY;      payload float4 per j particle (contiguous rows in jpay)
@@ -47,6 +68,13 @@ struct has_pair2<Pass, std::enable_if_t<Pass::PAIR2>> : std::true_type {};
 // i-particle of the warp (cheap), and the lanes of i-particle il then share only its in-range
 // survivors, so a warp step does full work on (nearly) every lane instead of idling on
 // out-of-range pairs.
+// passes that declare `static constexpr bool BUILD = true` build the neighbour lists
+// (ListView) while they evaluate: bool pair_list(const I&, Acc&, float4 jp, int j) returns
+// the symmetric predicate of the pair, and Acc has an int `nl` (list length so far)
+template <class Pass, class = void>
+struct is_build : std::false_type {};
+template <class Pass>
+struct is_build<Pass, std::enable_if_t<Pass::BUILD>> : std::true_type {};
 template <class Pass, class = void>
 struct batch_of : std::integral_constant<int, 0> {};
 template <class Pass>
@@ -77,6 +105,7 @@ __global__ void __launch_bounds__(NW * 32, MINB) pair_kernel(const Pass pass, co
     SM& sm = *reinterpret_cast<SM*>(smem_raw);
 
     const int a = blockIdx.x;
+    if (rv.only && !rv.only[a]) return;
     const int ifirst = rv.ifirst[a];
     const int icount = rv.icount[a];
     const int warp = threadIdx.x >> 5;
@@ -86,6 +115,11 @@ __global__ void __launch_bounds__(NW * 32, MINB) pair_kernel(const Pass pass, co
     const int ibase = warp * G;
     const bool wactive = ibase < icount;
     const bool ivalid = ibase + il < icount;
+    const int rbeg = rv.row_off[a], rend = rv.row_off[a + 1];
+    int rbase = 0;  // row-relative slot of the current round's first entry
+    [[maybe_unused]] int lcap = 0;
+    if constexpr (is_build<Pass>::value)  // slots are 16-bit: longer rows get no lists
+        lcap = (rend - rbeg) * JMAX <= 65536 ? pass.lv.cap : 0;
     float4* rpos = sm.rpos[warp];
     uint16_t* rslot = sm.rslot[warp];
     uint16_t* went = sm.went[warp];
@@ -116,7 +150,29 @@ __global__ void __launch_bounds__(NW * 32, MINB) pair_kernel(const Pass pass, co
     auto eval = [&](int rd, int n) {
         constexpr int U = Pass::UNROLL;
         int k = sl;
-        if constexpr (BATCH > 0) {  // pair-compacted (n <= BATCH)
+        if constexpr (is_build<Pass>::value) {  // every (i, survivor) pair tested, lists appended
+            const unsigned own = same_i_lanes<G>(il);
+            const int64_t lbase = (int64_t)(ifirst + ibase + il) * lcap;
+#pragma unroll 1
+            for (int k0 = 0; k0 < n; k0 += S) {
+                const int kk = k0 + sl;
+                bool ok = false;
+                int gs = 0;
+                if (ivalid && kk < n) {
+                    const int s = (rd + kk) & (RING - 1);
+                    const int t = rslot[s];
+                    ok = pass.pair_list(is, acc, rpos[s], __float_as_int(sm.eoff[t / JMAX].w) + t % JMAX);
+                    gs = rbase + t;
+                }
+                const unsigned b = __ballot_sync(0xffffffffu, ok) & own;
+                if (ok) {
+                    const int pos = acc.nl + __popc(b & ((1u << lane) - 1u));
+                    if (pos < lcap) pass.lv.nbr[lbase + pos] = (uint16_t)gs;
+                }
+                acc.nl += __popc(b);
+            }
+            return;
+        } else if constexpr (BATCH > 0) {  // pair-compacted (n <= BATCH)
             using M = std::conditional_t<(BATCH > 32), unsigned long long, unsigned>;
             M m = 0;
             if (ivalid)
@@ -168,9 +224,9 @@ __global__ void __launch_bounds__(NW * 32, MINB) pair_kernel(const Pass pass, co
 
     int wr = 0, rd = 0;
     uint32_t phase = 0;
-    const int rbeg = rv.row_off[a], rend = rv.row_off[a + 1];
     for (int e0 = rbeg; e0 < rend; e0 += ENT) {
         const int nent = min(ENT, rend - e0);
+        rbase = (e0 - rbeg) * JMAX;
         __syncthreads();  // barrier initialised / previous round consumed
         // entry t is issued by warp t % NW: the bulk copies of one warp are issued lane by lane
         // (uniform operands), so spreading the row over all warps shortens the issue chain NW-fold.
@@ -253,8 +309,121 @@ __global__ void __launch_bounds__(NW * 32, MINB) pair_kernel(const Pass pass, co
     if (wactive) {
         if (wr > rd) eval(rd, wr - rd);
         pass.template reduce<G>(acc);
-        if (ivalid && sl == 0) pass.finish(ifirst + ibase + il, is, acc);
+        if (ivalid && sl == 0) {
+            pass.finish(ifirst + ibase + il, is, acc);
+            if constexpr (is_build<Pass>::value) {
+                pass.lv.ncnt[ifirst + ibase + il] = acc.nl;
+                if (acc.nl > lcap) pass.lv.lflag[a] = 1;
+            }
+        }
     }
+}
+
+// ---------------------------------------------------------------- list-driven consumer
+// Same row staging (positions and payload rows only: no boxes, no culling); lane l holds
+// i-particle l % G and walks every (32/G)-th entry of i's neighbour list, so every
+// evaluated pair is in the symmetric predicate (the gather passes still apply their own
+// s32 < H_i^2 select).  Rows flagged by the list builder exit here and run pair_kernel
+// with RowView::only.
+template <class Pass, int ENT>
+struct ListSmem {
+    float4 raw[ENT * JMAX];
+    float4 pay[Pass::PAY > 0 ? ENT * JMAX * Pass::PAY : 1];
+    float4 eoff[ENT];  // shift offset (x, y, z), first (w, as int)
+    uint64_t bar;
+};
+
+template <class Pass, int NW, int G, int ENT, int MINB>
+__global__ void __launch_bounds__(NW * 32, MINB) list_kernel(const Pass pass, const RowView rv, const ListView lv) {
+    static_assert(32 % G == 0, "G must divide the warp");
+    constexpr int S = 32 / G;
+    using SM = ListSmem<Pass, ENT>;
+    extern __shared__ __align__(128) unsigned char smem_raw[];
+    SM& sm = *reinterpret_cast<SM*>(smem_raw);
+
+    const int a = blockIdx.x;
+    if (lv.lflag[a]) return;
+    const int ifirst = rv.ifirst[a];
+    const int icount = rv.icount[a];
+    const int warp = threadIdx.x >> 5;
+    const int lane = threadIdx.x & 31;
+    const int il = lane % G;
+    const int sl = lane / G;
+    const int ibase = warp * G;
+    const bool wactive = ibase < icount;
+    const bool ivalid = ibase + il < icount;
+    const int rbeg = rv.row_off[a], rend = rv.row_off[a + 1];
+
+    if (threadIdx.x == 0) {
+        mbar_init(&sm.bar, 1);
+        mbar_fence_init();
+    }
+    typename Pass::I is;
+    typename Pass::Acc acc;
+    pass.init(acc);
+    const int ki = ifirst + ibase + (ivalid ? il : 0);
+    int nl = 0;
+    if (wactive) {
+        pass.load_i(ki, is);
+        if (ivalid) nl = lv.ncnt[ki];
+    }
+    const uint16_t* L = lv.nbr + (int64_t)ki * lv.cap;
+    int p = sl;
+    int tn = p < nl ? (int)L[p] : 0x7fffffff;  // next slot of this lane
+
+    uint32_t phase = 0;
+    for (int e0 = rbeg; e0 < rend; e0 += ENT) {
+        const int nent = min(ENT, rend - e0);
+        __syncthreads();  // barrier initialised / previous round consumed
+        for (int t = lane * NW + warp; t < nent; t += NW * 32) {
+            int first, count, leaf, code;
+            unpack_entry(__ldg(rv.erec + e0 + t), first, count, leaf, code);
+            int sx, sy, sz;
+            decode_shift(code, sx, sy, sz);
+            sm.eoff[t] = make_float4((float)sx * rv.L[0], (float)sy * rv.L[1], (float)sz * rv.L[2],
+                                     __int_as_float(first));
+            const uint32_t pb = (uint32_t)count * 16u;
+            mbar_expect_tx(&sm.bar, pb * (1 + Pass::PAY));
+            bulk_g2s(&sm.raw[t * JMAX], pass.jrows + first, pb, &sm.bar);
+            if (Pass::PAY > 0)
+                bulk_g2s(&sm.pay[t * JMAX * Pass::PAY], pass.jpay + (int64_t)first * Pass::PAY, pb * Pass::PAY,
+                         &sm.bar);
+        }
+        __syncthreads();
+        if (threadIdx.x == 0) mbar_arrive(&sm.bar);
+        mbar_wait(&sm.bar, phase);
+        phase ^= 1u;
+        if (wactive) {
+            const int rs = (e0 - rbeg) * JMAX, re = rs + nent * JMAX;
+#pragma unroll 1
+            while (__any_sync(0xffffffffu, tn < re)) {
+                if (tn < re) {
+                    const int tl = tn - rs;
+                    const float4 o = sm.eoff[tl / JMAX];
+                    float4 jp = sm.raw[tl];
+                    jp.x += o.x; jp.y += o.y; jp.z += o.z;  // exact (O1)
+                    p += S;
+                    tn = p < nl ? (int)L[p] : 0x7fffffff;
+                    pass.pair(is, acc, jp, sm.pay + tl * Pass::PAY, __float_as_int(o.w) + tl % JMAX);
+                }
+            }
+        }
+    }
+    if (wactive) {
+        pass.template reduce<G>(acc);
+        if (ivalid && sl == 0) pass.finish(ki, is, acc);
+    }
+}
+
+template <class Pass, int NW, int G, int ENT, int MINB>
+inline cudaError_t launch_list(const Pass& pass, const RowView& rv, const ListView& lv, int64_t nleaf,
+                               cudaStream_t st) {
+    const int smem = (int)sizeof(ListSmem<Pass, ENT>);
+    cudaError_t e = cudaFuncSetAttribute(list_kernel<Pass, NW, G, ENT, MINB>,
+                                         cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+    if (e != cudaSuccess) return e;
+    list_kernel<Pass, NW, G, ENT, MINB><<<(unsigned)nleaf, NW * 32, smem, st>>>(pass, rv, lv);
+    return cudaGetLastError();
 }
 
 template <class Pass, int NW, int G, int ENT, int MINB>

@@ -311,3 +311,27 @@ def test_clustered_config3_full_chain_sampled_symmetric_modes():
         T = ref["targets"]
         assert norm_err(np.stack([gi["ahx"], gi["ahy"], gi["ahz"]], 1)[T], ref["a"], ref["Sa"]) <= TOL_FORCE
         assert norm_err(gi["dudt"][T], ref["dudt"], ref["Sdu"]) <= TOL_FORCE
+
+
+@pytest.mark.parametrize("cap", [0, 16, 70, 128])
+def test_neighbour_list_capacities(cap, monkeypatch):
+    """The gas passes read the neighbour lists built by geometry; rows whose lists overflow
+    the per-particle capacity run the on-the-fly kernels.  cap 0: lists off; 16: every row
+    overflows; 70: a mix (sym counts ~64-80 on c2z); 128: no overflow."""
+    monkeypatch.setenv("CRK_NBR_CAP", str(cap))
+    parts, params = cached_config("c2z")
+    params["symmetric"] = 1
+    g = run_gpu(parts, params, counts=False)
+    ref = oracle.substep(parts, params)
+    gi = g["in"]
+    T = ref["targets"]
+    assert rel_err(gi["V"][T], ref["V"]) <= 1e-5
+    assert rel_err(gi["A"][T], ref["A"]) <= 1e-5
+    H = parts["H"][T].astype(np.float64)[:, None]
+    assert dimless_err(gi["dB"][:, T].T, ref["dB"], H * H) <= 1e-4
+    assert rel_err(gi["rho"][T], ref["rho"]) <= 1e-5
+    vrms = np.sqrt(np.mean(parts["vx"] ** 2 + parts["vy"] ** 2 + parts["vz"] ** 2))
+    assert dimless_err(gi["dv"][:, T].T, ref["dv"], H / vrms) <= 2e-5
+    ah = np.stack([gi["ahx"], gi["ahy"], gi["ahz"]], 1)[T]
+    assert norm_err(ah, ref["a"], ref["Sa"]) <= TOL_FORCE
+    assert norm_err(gi["dudt"][T], ref["dudt"], ref["Sdu"]) <= TOL_FORCE
