@@ -84,11 +84,28 @@ __device__ __forceinline__ float warp_sum(float v) {
     for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
     return v;
 }
-// sum across the j-slots of a warp (lanes l, l+G, l+2G, ... hold partial sums of one i)
+// sum across the j-slots of a warp.  G > 0: lanes l, l+G, l+2G, ... hold partial sums of
+// one i (i = l % G); G = -S < 0: runs of S consecutive lanes hold one i (i = l / S)
 template <int G>
 __device__ __forceinline__ float slot_sum(float v) {
+    if constexpr (G > 0) {
 #pragma unroll
-    for (int o = 16; o >= G; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+        for (int o = 16; o >= G; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+    } else {
+#pragma unroll
+        for (int o = 1; o < -G; o <<= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+    }
+    return v;
+}
+template <int G>
+__device__ __forceinline__ int slot_sum_i(int v) {
+    if constexpr (G > 0) {
+#pragma unroll
+        for (int o = 16; o >= G; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+    } else {
+#pragma unroll
+        for (int o = 1; o < -G; o <<= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+    }
     return v;
 }
 

@@ -56,8 +56,7 @@ struct GravPass {
     template <int GG>
     __device__ void reduce(Acc& a) const {
         if (COUNT) {
-#pragma unroll
-            for (int o = 16; o >= GG; o >>= 1) a.n += __shfl_xor_sync(0xffffffffu, a.n, o);
+            a.n = slot_sum_i<GG>(a.n);
         } else {
             a.ax = slot_sum<GG>(a.ax);
             a.ay = slot_sum<GG>(a.ay);

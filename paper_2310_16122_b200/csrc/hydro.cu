@@ -82,6 +82,17 @@ struct GeoPass : HydCommon {
         a.w.x += r2 < s.H2 ? wt : 0.f;
         return r2 < fmaxf(s.H2, __fmul_rn(jp.w, jp.w));
     }
+    __device__ __forceinline__ void pair_list2(const I& s, Acc& a, const float4& p0, const float4& p1, bool& ok0,
+                                               bool& ok1) const {
+        const float2 dx = make_float2(p0.x - s.x, p1.x - s.x), dy = make_float2(p0.y - s.y, p1.y - s.y),
+                     dz = make_float2(p0.z - s.z, p1.z - s.z);
+        const float2 r2 = s32_of2(dx, dy, dz);
+        float2 wt, gt;
+        wendland_t2(r2, s.invH, wt, gt);
+        a.w = __fadd2_rn(a.w, f2sel(r2.x < s.H2, r2.y < s.H2, wt));
+        ok0 = r2.x < fmaxf(s.H2, __fmul_rn(p0.w, p0.w));
+        ok1 = r2.y < fmaxf(s.H2, __fmul_rn(p1.w, p1.w));
+    }
     __device__ __forceinline__ void pair(const I& s, Acc& a, const float4& jp, const float4*, int j) const {
         const float dx = jp.x - s.x, dy = jp.y - s.y, dz = jp.z - s.z;
         const float r2 = s32_of(dx, dy, dz);
@@ -106,8 +117,7 @@ struct GeoPass : HydCommon {
     template <int GG>
     __device__ void reduce(Acc& a) const {
         if (COUNT) {
-#pragma unroll
-            for (int o = 16; o >= GG; o >>= 1) a.n += __shfl_xor_sync(0xffffffffu, a.n, o);
+            a.n = slot_sum_i<GG>(a.n);
         } else {
             a.w.x = slot_sum<GG>(a.w.x + a.w.y);
         }
@@ -544,8 +554,7 @@ struct AccPass : HydCommon {
     template <int GG>
     __device__ void reduce(Acc& a) const {
         if (COUNT) {
-#pragma unroll
-            for (int o = 16; o >= GG; o >>= 1) a.nn += __shfl_xor_sync(0xffffffffu, a.nn, o);
+            a.nn = slot_sum_i<GG>(a.nn);
             return;
         }
 #pragma unroll

@@ -153,8 +153,26 @@ __global__ void __launch_bounds__(NW * 32, MINB) pair_kernel(const Pass pass, co
         if constexpr (is_build<Pass>::value) {  // every (i, survivor) pair tested, lists appended
             const unsigned own = same_i_lanes<G>(il);
             const int64_t lbase = (int64_t)(ifirst + ibase + il) * lcap;
+            auto append = [&](bool ok, int gs) {
+                const unsigned b = __ballot_sync(0xffffffffu, ok) & own;
+                if (ok) {
+                    const int pos = acc.nl + __popc(b & ((1u << lane) - 1u));
+                    if (pos < lcap) pass.lv.nbr[lbase + pos] = (uint16_t)gs;
+                }
+                acc.nl += __popc(b);
+            };
+            int k0 = 0;
 #pragma unroll 1
-            for (int k0 = 0; k0 < n; k0 += S) {
+            for (; k0 + 2 * S <= n; k0 += 2 * S) {  // two survivors per lane (packed FP32)
+                bool ok0 = false, ok1 = false;
+                const int s0 = (rd + k0 + sl) & (RING - 1), s1 = (rd + k0 + S + sl) & (RING - 1);
+                const int t0 = rslot[s0], t1 = rslot[s1];
+                if (ivalid) pass.pair_list2(is, acc, rpos[s0], rpos[s1], ok0, ok1);
+                append(ok0, rbase + t0);
+                append(ok1, rbase + t1);
+            }
+#pragma unroll 1
+            for (; k0 < n; k0 += S) {
                 const int kk = k0 + sl;
                 bool ok = false;
                 int gs = 0;
@@ -164,12 +182,7 @@ __global__ void __launch_bounds__(NW * 32, MINB) pair_kernel(const Pass pass, co
                     ok = pass.pair_list(is, acc, rpos[s], __float_as_int(sm.eoff[t / JMAX].w) + t % JMAX);
                     gs = rbase + t;
                 }
-                const unsigned b = __ballot_sync(0xffffffffu, ok) & own;
-                if (ok) {
-                    const int pos = acc.nl + __popc(b & ((1u << lane) - 1u));
-                    if (pos < lcap) pass.lv.nbr[lbase + pos] = (uint16_t)gs;
-                }
-                acc.nl += __popc(b);
+                append(ok, gs);
             }
             return;
         } else if constexpr (BATCH > 0) {  // pair-compacted (n <= BATCH)
@@ -347,8 +360,10 @@ __global__ void __launch_bounds__(NW * 32, MINB) list_kernel(const Pass pass, co
     const int icount = rv.icount[a];
     const int warp = threadIdx.x >> 5;
     const int lane = threadIdx.x & 31;
-    const int il = lane % G;
-    const int sl = lane / G;
+    // runs of S consecutive lanes share one i: the S lanes read consecutive list entries,
+    // usually consecutive staged slots, so their shared-memory loads fall in distinct banks
+    const int il = lane / S;
+    const int sl = lane % S;
     const int ibase = warp * G;
     const bool wactive = ibase < icount;
     const bool ivalid = ibase + il < icount;
@@ -410,7 +425,7 @@ __global__ void __launch_bounds__(NW * 32, MINB) list_kernel(const Pass pass, co
         }
     }
     if (wactive) {
-        pass.template reduce<G>(acc);
+        pass.template reduce<-S>(acc);
         if (ivalid && sl == 0) pass.finish(ki, is, acc);
     }
 }
