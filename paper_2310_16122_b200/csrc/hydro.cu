@@ -1105,7 +1105,9 @@ static ListView list_view(crk_ctx* c) {
     ListView lv;
     lv.nbr = P<uint16_t>(c->nbr);
     lv.ncnt = P<int32_t>(c->ncnt);
-    lv.lflag = P<uint8_t>(c->lflag);
+    lv.lflag = P<uint32_t>(c->lflag);
+    lv.frows = P<int32_t>(c->lflag) + c->nleaf[2];
+    lv.nfrows = P<int32_t>(c->lflag) + 2 * c->nleaf[2];
     lv.cap = c->nbr_cap;
     return lv;
 }
@@ -1119,7 +1121,9 @@ static crk_status launch_listed(crk_ctx* c, const Pass& ps, cudaStream_t st, con
     RowView rv = hydro_rows(c);
     CRK_TRY(cuda_check(c, launch_list<Pass, HYD_NW, HYD_G, ENT, MINB>(ps, rv, list_view(c), c->nleaf[2], st), what));
     c->launches++;
-    rv.only = P<uint8_t>(c->lflag);
+    const ListView lv = list_view(c);
+    rv.rows = lv.frows;
+    rv.nrows = lv.nfrows;
     CRK_TRY(cuda_check(c, launch_pairs<Pass, HYD_NW, HYD_G, FENT, FMINB>(ps, rv, c->nleaf[2], st), what));
     c->launches++;
     return CRK_OK;
@@ -1138,8 +1142,10 @@ crk_status geometry(crk_ctx* c, crk_particles* p, cudaStream_t st) {
         const int64_t ng = c->n_gas > 0 ? c->n_gas : 1;
         CRK_TRY(grow(c, c->nbr, (size_t)ng * c->nbr_cap * sizeof(uint16_t), st));
         CRK_TRY(grow(c, c->ncnt, (size_t)ng * sizeof(int32_t), st));
-        CRK_TRY(grow(c, c->lflag, (size_t)c->nleaf[2], st));
-        CRK_TRY(cuda_check(c, cudaMemsetAsync(c->lflag.p, 0, (size_t)c->nleaf[2], st), "memset"));
+        // lflag: per-row flags, then the compact flagged-row list, then its length
+        const size_t fl = (size_t)(2 * c->nleaf[2] + 1) * sizeof(int32_t);
+        CRK_TRY(grow(c, c->lflag, fl, st));
+        CRK_TRY(cuda_check(c, cudaMemsetAsync(c->lflag.p, 0, fl, st), "memset"));
         g.lv = list_view(c);
         return launch_hyd<GeoPass<false, true>, 128, 2>(c, g, st, "geometry (list build) kernel");
     }

@@ -12,6 +12,7 @@
 // register accumulation and one shuffle reduction over the slots at the end: no atomics.
 // Periodic shifts are added to the staged positions (exact, O1).
 #pragma once
+#include <algorithm>
 #include <type_traits>
 
 #include "common.cuh"
@@ -25,7 +26,8 @@ struct RowView {
     const int2* erec;     // packed entries (first | (count-1) << 29, leaf | shift << 26)
     const float4* box8;   // padded j-leaf boxes: (lo, max H^2), (hi, 0)
     float L[3];
-    const uint8_t* only = nullptr;  // non-null: run only the rows a with only[a] != 0 (list fallback)
+    const int32_t* rows = nullptr;  // non-null: run only rows[0 .. *nrows) (list fallback), grid-strided
+    const int32_t* nrows = nullptr;
 };
 
 // Per-particle neighbour lists of the gas passes: row-relative staging
@@ -37,7 +39,9 @@ struct RowView {
 struct ListView {
     uint16_t* nbr;     // [n_gas * cap]
     int32_t* ncnt;     // [n_gas]
-    uint8_t* lflag;    // [n gas i-leaves]: 1 = lists incomplete, use the on-the-fly path
+    uint32_t* lflag;   // [n gas i-leaves]: 1 = lists incomplete, use the on-the-fly path
+    int32_t* frows;    // compact list of the flagged rows ...
+    int32_t* nfrows;   // ... and their number (zeroed before the build)
     int cap;
 };
 template <int G>
@@ -94,18 +98,14 @@ struct PairSmem {
     uint16_t rslot[NW][RING];  // survivors: staged slot (payload, j index)
 };
 
-template <class Pass, int NW, int G, int ENT, int MINB>
-__global__ void __launch_bounds__(NW * 32, MINB) pair_kernel(const Pass pass, const RowView rv) {
+template <class Pass, int NW, int G, int ENT>
+__device__ __forceinline__ void pair_row(const Pass& pass, const RowView& rv, PairSmem<Pass, NW, ENT>& sm, const int a,
+                                         uint32_t& phase) {
     static_assert(32 % G == 0, "G must divide the warp");
     static_assert(ENT * JMAX <= 65536, "slot index is 16 bits");
     constexpr int S = 32 / G;
     using SM = PairSmem<Pass, NW, ENT>;
     constexpr int RING = SM::RING;
-    extern __shared__ __align__(128) unsigned char smem_raw[];
-    SM& sm = *reinterpret_cast<SM*>(smem_raw);
-
-    const int a = blockIdx.x;
-    if (rv.only && !rv.only[a]) return;
     const int ifirst = rv.ifirst[a];
     const int icount = rv.icount[a];
     const int warp = threadIdx.x >> 5;
@@ -124,10 +124,6 @@ __global__ void __launch_bounds__(NW * 32, MINB) pair_kernel(const Pass pass, co
     uint16_t* rslot = sm.rslot[warp];
     uint16_t* went = sm.went[warp];
 
-    if (threadIdx.x == 0) {
-        mbar_init(&sm.bar, 1);
-        mbar_fence_init();
-    }
     typename Pass::I is;
     typename Pass::Acc acc;
     pass.init(acc);
@@ -153,14 +149,8 @@ __global__ void __launch_bounds__(NW * 32, MINB) pair_kernel(const Pass pass, co
         if constexpr (is_build<Pass>::value) {  // every (i, survivor) pair tested, lists appended
             const unsigned own = same_i_lanes<G>(il);
             const int64_t lbase = (int64_t)(ifirst + ibase + il) * lcap;
-            auto append = [&](bool ok, int gs) {
-                const unsigned b = __ballot_sync(0xffffffffu, ok) & own;
-                if (ok) {
-                    const int pos = acc.nl + __popc(b & ((1u << lane) - 1u));
-                    if (pos < lcap) pass.lv.nbr[lbase + pos] = (uint16_t)gs;
-                }
-                acc.nl += __popc(b);
-            };
+            const unsigned below = own & ((1u << lane) - 1u);
+            uint16_t* const lp = pass.lv.nbr + lbase;
             int k0 = 0;
 #pragma unroll 1
             for (; k0 + 2 * S <= n; k0 += 2 * S) {  // two survivors per lane (packed FP32)
@@ -168,21 +158,27 @@ __global__ void __launch_bounds__(NW * 32, MINB) pair_kernel(const Pass pass, co
                 const int s0 = (rd + k0 + sl) & (RING - 1), s1 = (rd + k0 + S + sl) & (RING - 1);
                 const int t0 = rslot[s0], t1 = rslot[s1];
                 if (ivalid) pass.pair_list2(is, acc, rpos[s0], rpos[s1], ok0, ok1);
-                append(ok0, rbase + t0);
-                append(ok1, rbase + t1);
+                const unsigned b0 = __ballot_sync(0xffffffffu, ok0), b1 = __ballot_sync(0xffffffffu, ok1);
+                const int n0 = __popc(b0 & own);
+                const int pos0 = acc.nl + __popc(b0 & below), pos1 = acc.nl + n0 + __popc(b1 & below);
+                if (ok0 && pos0 < lcap) lp[pos0] = (uint16_t)(rbase + t0);
+                if (ok1 && pos1 < lcap) lp[pos1] = (uint16_t)(rbase + t1);
+                acc.nl += n0 + __popc(b1 & own);
             }
 #pragma unroll 1
             for (; k0 < n; k0 += S) {
                 const int kk = k0 + sl;
                 bool ok = false;
-                int gs = 0;
+                int t = 0;
                 if (ivalid && kk < n) {
                     const int s = (rd + kk) & (RING - 1);
-                    const int t = rslot[s];
+                    t = rslot[s];
                     ok = pass.pair_list(is, acc, rpos[s], __float_as_int(sm.eoff[t / JMAX].w) + t % JMAX);
-                    gs = rbase + t;
                 }
-                append(ok, gs);
+                const unsigned b = __ballot_sync(0xffffffffu, ok);
+                const int pos = acc.nl + __popc(b & below);
+                if (ok && pos < lcap) lp[pos] = (uint16_t)(rbase + t);
+                acc.nl += __popc(b & own);
             }
             return;
         } else if constexpr (BATCH > 0) {  // pair-compacted (n <= BATCH)
@@ -236,7 +232,6 @@ __global__ void __launch_bounds__(NW * 32, MINB) pair_kernel(const Pass pass, co
     };
 
     int wr = 0, rd = 0;
-    uint32_t phase = 0;
     for (int e0 = rbeg; e0 < rend; e0 += ENT) {
         const int nent = min(ENT, rend - e0);
         rbase = (e0 - rbeg) * JMAX;
@@ -326,10 +321,29 @@ __global__ void __launch_bounds__(NW * 32, MINB) pair_kernel(const Pass pass, co
             pass.finish(ifirst + ibase + il, is, acc);
             if constexpr (is_build<Pass>::value) {
                 pass.lv.ncnt[ifirst + ibase + il] = acc.nl;
-                if (acc.nl > lcap) pass.lv.lflag[a] = 1;
+                if (acc.nl > lcap && atomicExch(pass.lv.lflag + a, 1u) == 0u)
+                    pass.lv.frows[atomicAdd(pass.lv.nfrows, 1)] = a;
             }
         }
     }
+}
+
+template <class Pass, int NW, int G, int ENT, int MINB>
+__global__ void __launch_bounds__(NW * 32, MINB) pair_kernel(const Pass pass, const RowView rv) {
+    using SM = PairSmem<Pass, NW, ENT>;
+    extern __shared__ __align__(128) unsigned char smem_raw[];
+    SM& sm = *reinterpret_cast<SM*>(smem_raw);
+    if (threadIdx.x == 0) {
+        mbar_init(&sm.bar, 1);
+        mbar_fence_init();
+    }
+    uint32_t phase = 0;
+    if (!rv.rows) {
+        pair_row<Pass, NW, G, ENT>(pass, rv, sm, blockIdx.x, phase);
+        return;
+    }
+    const int nrows = *rv.nrows;
+    for (int w = blockIdx.x; w < nrows; w += gridDim.x) pair_row<Pass, NW, G, ENT>(pass, rv, sm, rv.rows[w], phase);
 }
 
 // ---------------------------------------------------------------- list-driven consumer
@@ -337,7 +351,7 @@ __global__ void __launch_bounds__(NW * 32, MINB) pair_kernel(const Pass pass, co
 // i-particle l % G and walks every (32/G)-th entry of i's neighbour list, so every
 // evaluated pair is in the symmetric predicate (the gather passes still apply their own
 // s32 < H_i^2 select).  Rows flagged by the list builder exit here and run pair_kernel
-// with RowView::only.
+// with RowView::rows = the builder's flagged-row list.
 template <class Pass, int ENT>
 struct ListSmem {
     float4 raw[ENT * JMAX];
@@ -382,9 +396,9 @@ __global__ void __launch_bounds__(NW * 32, MINB) list_kernel(const Pass pass, co
         pass.load_i(ki, is);
         if (ivalid) nl = lv.ncnt[ki];
     }
-    const uint16_t* L = lv.nbr + (int64_t)ki * lv.cap;
-    int p = sl;
-    int tn = p < nl ? (int)L[p] : 0x7fffffff;  // next slot of this lane
+    const uint16_t* lp = lv.nbr + (int64_t)ki * lv.cap + sl;  // this lane's next list entry
+    const uint16_t* const lend = lv.nbr + (int64_t)ki * lv.cap + nl;
+    int tn = lp < lend ? (int)*lp : 0x7fffffff;  // next slot of this lane
 
     uint32_t phase = 0;
     for (int e0 = rbeg; e0 < rend; e0 += ENT) {
@@ -408,18 +422,27 @@ __global__ void __launch_bounds__(NW * 32, MINB) list_kernel(const Pass pass, co
         if (threadIdx.x == 0) mbar_arrive(&sm.bar);
         mbar_wait(&sm.bar, phase);
         phase ^= 1u;
+        // periodic shifts applied once per staged slot (exact, O1), not once per pair
+        for (int t = threadIdx.x; t < nent * JMAX; t += NW * 32) {
+            const float4 o = sm.eoff[t / JMAX];
+            if (o.x != 0.f || o.y != 0.f || o.z != 0.f) {
+                float4 q = sm.raw[t];
+                q.x += o.x; q.y += o.y; q.z += o.z;
+                sm.raw[t] = q;
+            }
+        }
+        fence_proxy_async_smem();  // generic writes before the next round's TMA overwrites
+        __syncthreads();
         if (wactive) {
             const int rs = (e0 - rbeg) * JMAX, re = rs + nent * JMAX;
 #pragma unroll 1
             while (__any_sync(0xffffffffu, tn < re)) {
                 if (tn < re) {
                     const int tl = tn - rs;
-                    const float4 o = sm.eoff[tl / JMAX];
-                    float4 jp = sm.raw[tl];
-                    jp.x += o.x; jp.y += o.y; jp.z += o.z;  // exact (O1)
-                    p += S;
-                    tn = p < nl ? (int)L[p] : 0x7fffffff;
-                    pass.pair(is, acc, jp, sm.pay + tl * Pass::PAY, __float_as_int(o.w) + tl % JMAX);
+                    const float4 jp = sm.raw[tl];
+                    lp += S;
+                    tn = lp < lend ? (int)*lp : 0x7fffffff;
+                    pass.pair(is, acc, jp, sm.pay + tl * Pass::PAY, __float_as_int(sm.eoff[tl / JMAX].w) + tl % JMAX);
                 }
             }
         }
@@ -447,7 +470,10 @@ inline cudaError_t launch_pairs(const Pass& pass, const RowView& rv, int64_t nle
     cudaError_t e = cudaFuncSetAttribute(pair_kernel<Pass, NW, G, ENT, MINB>,
                                          cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
     if (e != cudaSuccess) return e;
-    pair_kernel<Pass, NW, G, ENT, MINB><<<(unsigned)nleaf, NW * 32, smem, st>>>(pass, rv);
+    // rows mode: a few CTAs per SM walk the (device-counted) row list
+    const int64_t grid = rv.rows ? std::min<int64_t>(nleaf, 148 * MINB) : nleaf;
+    if (grid <= 0) return cudaSuccess;
+    pair_kernel<Pass, NW, G, ENT, MINB><<<(unsigned)grid, NW * 32, smem, st>>>(pass, rv);
     return cudaGetLastError();
 }
 
