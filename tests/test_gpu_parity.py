@@ -335,3 +335,17 @@ def test_neighbour_list_capacities(cap, monkeypatch):
     ah = np.stack([gi["ahx"], gi["ahy"], gi["ahz"]], 1)[T]
     assert norm_err(ah, ref["a"], ref["Sa"]) <= TOL_FORCE
     assert norm_err(gi["dudt"][T], ref["dudt"], ref["Sdu"]) <= TOL_FORCE
+
+
+@pytest.mark.parametrize("var", ["0", "1", "7"])
+@pytest.mark.parametrize("name", ["c1", "c2z"])
+def test_gravity_symmetric_variants(var, name, monkeypatch):
+    """Every Newton-3 gravity kernel variant (CRK_GRAV_VARIANT) against the oracle."""
+    monkeypatch.setenv("CRK_GRAV_VARIANT", var)
+    parts, params = cached_config(name)
+    params["symmetric"] = 1
+    g = run_gpu(parts, params, counts=False, hydro=False)
+    ref = oracle.substep(parts, params)
+    gi = g["in"]
+    a = np.stack([gi["ax"], gi["ay"], gi["az"]], 1)
+    assert norm_err(a, ref["grav_a"], ref["grav_S"]) <= TOL_FORCE
