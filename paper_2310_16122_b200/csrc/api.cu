@@ -142,7 +142,7 @@ crk_status crk_destroy(crk_ctx* c) {
     Buf* bufs[] = {&c->keys_a, &c->keys_b, &c->idx_a, &c->idx_b, &c->cub_tmp, &c->scratch, &c->xm,
                    &c->cell_start, &c->cell_end, &c->leaf_cnt, &c->gflag, &c->grank, &c->gas_idx,
                    &c->dev_scalars, &c->gpos, &c->gvel, &c->gV, &c->gcoef, &c->grec, &c->gu,
-                   &c->gacc, &c->gposV, &c->sel_flag, &c->sel_mask, &c->work, &c->nbr, &c->ncnt, &c->lflag};
+                   &c->gacc, &c->gposV, &c->sel_flag, &c->sel_mask, &c->work, &c->nbr, &c->ncnt, &c->lflag, &c->gebox};
     for (Buf* b : bufs)
         if (b->p) cudaFree(b->p);
     for (int s = 0; s < 4; ++s) {

@@ -262,12 +262,20 @@ struct ListArgs {
     const int32_t* jcount;
     int2* erec;
     const float4* box8B;    // padded j-leaf boxes (lo, max H^2), (hi, 0)
+    float4* ebox;           // gravity only (else null): per entry (lo + shift, first), (hi + shift, count | code << 8)
 };
 
 __device__ __forceinline__ void put_entry(const ListArgs& A, int p, int b, int code) {
     A.col[p] = b;
     A.shift[p] = (int8_t)code;
     A.erec[p] = make_int2(A.jfirst[b] | ((A.jcount[b] - 1) << 29), b | (code << 26));
+    if (A.ebox) {  // the j-leaf box with the periodic shift applied (exact, O1), next to first / count
+        const float ox = (float)(code % 3 - 1) * A.Lf[0], oy = (float)((code / 3) % 3 - 1) * A.Lf[1],
+                    oz = (float)(code / 9 - 1) * A.Lf[2];
+        const float4 bl = A.box8B[2 * (int64_t)b], bh = A.box8B[2 * (int64_t)b + 1];
+        A.ebox[2 * (int64_t)p] = make_float4(bl.x + ox, bl.y + oy, bl.z + oz, __int_as_float(A.jfirst[b]));
+        A.ebox[2 * (int64_t)p + 1] = make_float4(bh.x + ox, bh.y + oy, bh.z + oz, __int_as_float(A.jcount[b] | (code << 8)));
+    }
 }
 
 constexpr int LIST_WARPS = 8;
@@ -437,6 +445,7 @@ static ListArgs list_args(crk_ctx* c, int m) {
     A.jcount = P<int32_t>(c->lcount[sb]);
     A.erec = P<int2>(c->erec[m]);
     A.box8B = P<float4>(c->lbox8[sb]);
+    A.ebox = m == 0 ? P<float4>(c->gebox) : nullptr;
     return A;
 }
 
@@ -594,6 +603,7 @@ crk_status build_lists(crk_ctx* c, crk_particles* p, cudaStream_t st) {
         CRK_TRY(grow(c, c->col[m], ne * 4, st));
         CRK_TRY(grow(c, c->shift[m], ne, st));
         CRK_TRY(grow(c, c->erec[m], ne * 8, st));
+        if (m == 0) CRK_TRY(grow(c, c->gebox, ne * 32, st));
         ListArgs A = list_args(c, m);
         if (na > 0) {
             k_lists<true><<<nblk(na * 32, LIST_WARPS * 32), LIST_WARPS * 32, 0, st>>>(A);

@@ -68,6 +68,7 @@ struct crk_ctx {
     // lists (0 gravity, 1 hydro)
     crk::Buf rowlen[2], rowoff[2], col[2], shift[2];
     crk::Buf erec[2];            // packed entries: int2 (first | (count-1) << 29, leaf | shift << 26)
+    crk::Buf gebox;              // gravity entries: float4 (lo + shift, first), (hi + shift, count)
     // gas-ordered state
     crk::Buf gpos;               // float4 (x, y, z, H)
     crk::Buf gvel;               // float4 (vx, vy, vz, m)

@@ -119,6 +119,7 @@ struct Smem {
 
 struct GravSymArgs {
     const float4* xm;
+    const float4* ebox;  // per list entry: (lo + shift, first), (hi + shift, count | shift code << 8)
     const float4* box8;  // gravity j-leaf padded boxes
     const int2* erec;    // packed list entries
     const int32_t* row_off;
@@ -584,6 +585,237 @@ __global__ void __launch_bounds__(symw::NW * 32, 16 / symw::NW) grav_warp_kernel
     }
 }
 
+// ------------------------------------------------------------ pipelined warp-independent variant
+// grav_warp_kernel with the L2 latency taken off the critical path: per warp a two-deep
+// software pipeline of async copies (cp.async, no registers held) — the entry records
+// (shifted leaf box + first/count, written by the list build) of chunk c+2 and the
+// particles of the surviving leaves of chunk c+1 are in flight while chunk c is culled
+// and evaluated from shared memory.
+namespace symp {
+constexpr int G = 16, RING = 64, NW = 4, CH = 32;
+struct WarpSm {
+    float4 er[2][CH][2];      // entry records of two chunks
+    float4 pp[2][CH * JMAX];  // particles of the surviving leaves of two chunks
+    float4 woff[2][CH];       // surviving entries: shift offset, first (w)
+    int wcnt[2][CH];
+    float4 wpos[RING];
+    int widx[RING];
+    float2 inx[G / 2], iny[G / 2], inz[G / 2], im[G / 2];
+};
+}  // namespace symp
+
+__global__ void __launch_bounds__(symp::NW * 32, 16 / symp::NW) grav_pipe_kernel(const GravSymArgs A) {
+    using namespace symp;
+    extern __shared__ __align__(128) unsigned char smem_raw[];
+    const int warp = threadIdx.x >> 5;
+    const int lane = threadIdx.x & 31;
+    WarpSm& S = reinterpret_cast<WarpSm*>(smem_raw)[warp];
+    const float wcut = A.rcut2 * CULL_SLACK;
+    const float rc2 = A.rcut2, e2 = A.eps2;
+    const float c0 = A.c0, c1 = A.c1, c2 = A.c2, c3 = A.c3, c4 = A.c4, c5 = A.c5;
+    const unsigned below = (1u << lane) - 1u;
+    const float4* __restrict__ xm = A.xm;
+
+    while (true) {
+        int w = 0;
+        if (lane == 0) w = atomicAdd(A.work, 1);
+        w = __shfl_sync(0xffffffffu, w, 0);
+        if (w >= A.nitems) break;
+        const int a = w / A.split;
+        const int icount = __ldg(A.icount + a);
+        const int ibase = (w % A.split) * G;
+        if (ibase >= icount) continue;
+        const int gself = __ldg(A.ifirst + a) + ibase;
+        const int ng = min(G, icount - ibase);
+        const int rbeg = __ldg(A.row_off + a), rend = __ldg(A.row_off + a + 1);
+        const int nch = (rend - rbeg + CH - 1) / CH;
+
+        auto issue_entries = [&](int c) {  // entry records of chunk c -> er[c & 1]
+            const int e = rbeg + c * CH + lane;
+            if (c < nch && e < rend) {
+                cp_async16(&S.er[c & 1][lane][0], A.ebox + 2 * (int64_t)e);
+                cp_async16(&S.er[c & 1][lane][1], A.ebox + 2 * (int64_t)e + 1);
+            }
+            cp_async_commit();
+        };
+        issue_entries(0);
+        issue_entries(1);
+
+        float lo[3], hi[3];
+        {
+            const bool iv = lane < ng;
+            float4 p = make_float4(-1e18f, -1e18f, -1e18f, 0.f);
+            if (iv) p = __ldg(xm + gself + lane);
+            if (lane < G) {
+                const int k = 2 * (lane % (G / 2)) + lane / (G / 2);
+                reinterpret_cast<float*>(S.inx)[k] = -p.x;
+                reinterpret_cast<float*>(S.iny)[k] = -p.y;
+                reinterpret_cast<float*>(S.inz)[k] = -p.z;
+                reinterpret_cast<float*>(S.im)[k] = p.w;
+            }
+            lo[0] = warp_min(iv ? p.x : INFINITY);
+            lo[1] = warp_min(iv ? p.y : INFINITY);
+            lo[2] = warp_min(iv ? p.z : INFINITY);
+            hi[0] = warp_max(iv ? p.x : -INFINITY);
+            hi[1] = warp_max(iv ? p.y : -INFINITY);
+            hi[2] = warp_max(iv ? p.z : -INFINITY);
+        }
+
+        int nsurv[2] = {0, 0};
+        // entry cull of chunk c (records landed) and async copies of its surviving leaves
+        auto cull_entries = [&](int c) {
+            const int b = c & 1;
+            bool ek = false;
+            float4 off = make_float4(0.f, 0.f, 0.f, 0.f);
+            int cnt = 0;
+            if (c < nch && rbeg + c * CH + lane < rend) {
+                const float4 bl = S.er[b][lane][0], bh = S.er[b][lane][1];
+                const int first = __float_as_int(bl.w);
+                const int cc = __float_as_int(bh.w);
+                cnt = cc & 0xff;
+                int sx, sy, sz;
+                decode_shift(cc >> 8, sx, sy, sz);
+                off = make_float4((float)sx * A.L[0], (float)sy * A.L[1], (float)sz * A.L[2], bl.w);
+                if (first + cnt > gself) {  // entries wholly below this group own no pair
+                    const float gx = fmaxf(fmaxf(bl.x - hi[0], lo[0] - bh.x), 0.f);
+                    const float gy = fmaxf(fmaxf(bl.y - hi[1], lo[1] - bh.y), 0.f);
+                    const float gz = fmaxf(fmaxf(bl.z - hi[2], lo[2] - bh.z), 0.f);
+                    ek = fmaf(gz, gz, fmaf(gy, gy, gx * gx)) < wcut;
+                }
+            }
+            const unsigned em = __ballot_sync(0xffffffffu, ek);
+            const int ns = __popc(em);
+            nsurv[b] = ns;
+            if (ek) {
+                const int q = __popc(em & below);
+                S.wcnt[b][q] = cnt;
+                S.woff[b][q] = off;
+            }
+            __syncwarp();
+            // particles: lane -> (entry q0 + lane / 8, member lane % 8)
+            for (int q0 = 0; q0 < ns; q0 += 32 / JMAX) {
+                const int q = q0 + lane / JMAX, kk = lane % JMAX;
+                if (q < ns && kk < S.wcnt[b][q])
+                    cp_async16(&S.pp[b][q * JMAX + kk], xm + __float_as_int(S.woff[b][q].w) + kk);
+            }
+            cp_async_commit();
+        };
+        cp_async_wait<1>();  // entries(0)
+        __syncwarp();
+        cull_entries(0);
+
+        float2 ax[G / 2], ay[G / 2], az[G / 2];
+#pragma unroll
+        for (int k = 0; k < G / 2; ++k) ax[k] = ay[k] = az[k] = make_float2(0.f, 0.f);
+
+        auto eval_step = [&](int r0, int n) {
+            float4 jp = make_float4(1e18f, 1e18f, 1e18f, 0.f);
+            int j = 0;
+            if (lane < n) {
+                const int s = (r0 + lane) & (RING - 1);
+                jp = S.wpos[s];
+                j = S.widx[s];
+            }
+            const float mj = (j >= gself && j < gself + ng) ? 0.f : jp.w;
+            const float2 jx = make_float2(jp.x, jp.x), jy = make_float2(jp.y, jp.y), jz = make_float2(jp.z, jp.z);
+            const float2 mj2 = make_float2(mj, mj), e22 = make_float2(e2, e2);
+            const float2 n0 = make_float2(-c0, -c0), n1 = make_float2(-c1, -c1), n2 = make_float2(-c2, -c2);
+            const float2 n3 = make_float2(-c3, -c3), n4 = make_float2(-c4, -c4), n5 = make_float2(-c5, -c5);
+            float2 bx = make_float2(0.f, 0.f), by = bx, bz = bx;
+#pragma unroll
+            for (int k = 0; k < G / 2; ++k) {
+                const float2 dx = __fadd2_rn(jx, S.inx[k]);
+                const float2 dy = __fadd2_rn(jy, S.iny[k]);
+                const float2 dz = __fadd2_rn(jz, S.inz[k]);
+                const float2 r2 = __ffma2_rn(dz, dz, __ffma2_rn(dy, dy, __fmul2_rn(dx, dx)));
+                const float2 re = __fadd2_rn(r2, e22);
+                const float2 ri = make_float2(rsqrtf(re.x), rsqrtf(re.y));
+                const float2 ri2 = __fmul2_rn(ri, ri);
+                float2 np5 = __ffma2_rn(n5, r2, n4);
+                np5 = __ffma2_rn(np5, r2, n3);
+                np5 = __ffma2_rn(np5, r2, n2);
+                np5 = __ffma2_rn(np5, r2, n1);
+                np5 = __ffma2_rn(np5, r2, n0);
+                float2 wv = __ffma2_rn(ri2, ri, np5);
+                wv.x = r2.x < rc2 ? wv.x : 0.f;
+                wv.y = r2.y < rc2 ? wv.y : 0.f;
+                const float2 wi = __fmul2_rn(mj2, wv);
+                ax[k] = __ffma2_rn(wi, dx, ax[k]);
+                ay[k] = __ffma2_rn(wi, dy, ay[k]);
+                az[k] = __ffma2_rn(wi, dz, az[k]);
+                const float2 wj = __fmul2_rn(S.im[k], wv);
+                bx = __ffma2_rn(wj, dx, bx);
+                by = __ffma2_rn(wj, dy, by);
+                bz = __ffma2_rn(wj, dz, bz);
+            }
+            if (lane < n) red_add_v4(A.acc + j, -(bx.x + bx.y), -(by.x + by.y), -(bz.x + bz.y), 0.f);
+        };
+
+        int wr = 0, rd = 0;
+        for (int c = 0; c < nch; ++c) {
+            const int b = c & 1;
+            issue_entries(c + 2);  // into er[b]: chunk c's records were consumed by cull_entries(c)
+            cp_async_wait<2>();    // entries(c + 1)
+            __syncwarp();
+            cull_entries(c + 1);   // its particles go to pp[b ^ 1] (chunk c - 1's, consumed)
+            cp_async_wait<2>();    // particles(c)
+            __syncwarp();
+            // particle cull of chunk c from shared memory, then evaluation
+            const int ns = nsurv[b];
+            for (int q0 = 0; q0 < ns; q0 += 32 / JMAX) {
+                const int q = q0 + lane / JMAX, kk = lane % JMAX;
+                const int qc = q < ns ? q : 0;
+                const int cnt = S.wcnt[b][qc];
+                const float4 o = S.woff[b][qc];
+                const int j = __float_as_int(o.w) + kk;
+                float4 p = S.pp[b][qc * JMAX + kk];
+                p.x += o.x; p.y += o.y; p.z += o.z;  // exact (O1)
+                bool keep = q < ns && kk < cnt && j >= gself;
+                if (keep) keep = box_dist2(p.x, p.y, p.z, lo, hi) < wcut;
+                const unsigned msk = __ballot_sync(0xffffffffu, keep);
+                if (keep) {
+                    const int s = (wr + __popc(msk & below)) & (RING - 1);
+                    S.wpos[s] = p;
+                    S.widx[s] = j;
+                }
+                wr += __popc(msk);
+                __syncwarp();
+                if (wr - rd >= 32) {
+                    eval_step(rd, 32);
+                    rd += 32;
+                    __syncwarp();
+                }
+            }
+            __syncwarp();
+        }
+        cp_async_wait<0>();
+        if (wr > rd) eval_step(rd, wr - rd);
+        float v[3][G];
+#pragma unroll
+        for (int k = 0; k < G / 2; ++k) {
+            v[0][k] = ax[k].x; v[0][k + G / 2] = ax[k].y;
+            v[1][k] = ay[k].x; v[1][k + G / 2] = ay[k].y;
+            v[2][k] = az[k].x; v[2][k + G / 2] = az[k].y;
+        }
+#pragma unroll
+        for (int h = G / 2; h >= 1; h >>= 1) {
+            const bool up = lane & (2 * h);
+#pragma unroll
+            for (int cc = 0; cc < 3; ++cc)
+#pragma unroll
+                for (int k = 0; k < h; ++k) {
+                    const float send = up ? v[cc][k] : v[cc][k + h];
+                    const float keep = up ? v[cc][k + h] : v[cc][k];
+                    v[cc][k] = keep + __shfl_xor_sync(0xffffffffu, send, 2 * h);
+                }
+        }
+#pragma unroll
+        for (int cc = 0; cc < 3; ++cc) v[cc][0] += __shfl_xor_sync(0xffffffffu, v[cc][0], 1);
+        if ((lane & 1) == 0 && (lane >> 1) < ng) red_add_v4(A.acc + gself + (lane >> 1), v[0][0], v[1][0], v[2][0], 0.f);
+        __syncwarp();
+    }
+}
+
 // a = G acc (written to the caller), v += dt a
 __global__ void k_grav_finish(int64_t n, const float4* __restrict__ acc, float G, float dt, float* ax, float* ay,
                               float* az, float* vx, float* vy, float* vz) {
@@ -656,6 +888,7 @@ static crk_status gravity_sym(crk_ctx* c, crk_particles* p, float dt, cudaStream
     if (c->nleaf[0] > 0) {
         GravSymArgs A;
         A.xm = P<float4>(c->xm);
+        A.ebox = P<float4>(c->gebox);
         A.box8 = P<float4>(c->lbox8[1]);
         A.erec = P<int2>(c->erec[0]);
         A.row_off = P<int32_t>(c->rowoff[0]);
@@ -668,7 +901,7 @@ static crk_status gravity_sym(crk_ctx* c, crk_particles* p, float dt, cudaStream
         A.c0 = c->prm.poly[0]; A.c1 = c->prm.poly[1]; A.c2 = c->prm.poly[2];
         A.c3 = c->prm.poly[3]; A.c4 = c->prm.poly[4]; A.c5 = c->prm.poly[5];
         const char* gv = getenv("CRK_GRAV_VARIANT");
-        const int var = gv ? atoi(gv) : 0;  // 0: warp-independent kernel; 1-5, 7: CTA-staged variants
+        const int var = gv ? atoi(gv) : 0;  // 0: pipelined warp-independent kernel; 6: unpipelined; 1-5, 7: CTA-staged
         CRK_TRY(grow(c, c->work, 16, st));
         CRK_TRY(cuda_check(c, cudaMemsetAsync(c->work.p, 0, 16, st), "memset"));
         A.work = P<int>(c->work);
@@ -681,7 +914,7 @@ static crk_status gravity_sym(crk_ctx* c, crk_particles* p, float dt, cudaStream
         case 3: e = launch_grav_sym<8, 320, 1, 8, 3>(c, A, st); break;
         case 4: e = launch_grav_sym<16, 320, 1, 8, 1>(c, A, st); break;
         case 5: e = launch_grav_sym<8, 256, 1, 8, 3>(c, A, st); break;
-        default: {  // warp-independent (c4: 17.3 ms vs 20.4 for <8, 320, 1>)
+        case 6: {  // warp-independent (c4: 17.3 ms vs 20.4 for <8, 320, 1>)
             A.split = (c->prm.leaf_max_i + symw::G - 1) / symw::G;
             A.nitems = (int)(c->nleaf[0] * A.split);
             int nsm = 0;
@@ -691,6 +924,19 @@ static crk_status gravity_sym(crk_ctx* c, crk_particles* p, float dt, cudaStream
             break;
         }
         case 7: e = launch_grav_sym<8, 320, 1>(c, A, st); break;
+        default: {  // pipelined warp-independent (c4: 16.0 ms)
+            A.split = (c->prm.leaf_max_i + symp::G - 1) / symp::G;
+            A.nitems = (int)(c->nleaf[0] * A.split);
+            int nsm = 0;
+            cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, c->device);
+            const int smem = (int)sizeof(symp::WarpSm) * symp::NW;
+            e = cudaFuncSetAttribute(grav_pipe_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+            if (e == cudaSuccess) {
+                grav_pipe_kernel<<<nsm * (16 / symp::NW), symp::NW * 32, smem, st>>>(A);
+                e = cudaGetLastError();
+            }
+            break;
+        }
         }
         if (e != cudaSuccess) return cuda_check(c, e, "gravity (symmetric) kernel");
         CRK_LAUNCHED(c, "gravity (symmetric) kernel");
