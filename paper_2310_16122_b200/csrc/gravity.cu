@@ -902,7 +902,7 @@ static crk_status gravity_sym(crk_ctx* c, crk_particles* p, float dt, cudaStream
         A.c3 = c->prm.poly[3]; A.c4 = c->prm.poly[4]; A.c5 = c->prm.poly[5];
         const char* gv = getenv("CRK_GRAV_VARIANT");
         const int var = gv ? atoi(gv) : 0;  // 0: pipelined warp-independent kernel; 6: unpipelined; 1-5, 7: CTA-staged
-        CRK_TRY(grow(c, c->work, 16, st));
+        CRK_TRY(grow(c, c->work, 64, st));
         CRK_TRY(cuda_check(c, cudaMemsetAsync(c->work.p, 0, 16, st), "memset"));
         A.work = P<int>(c->work);
         cudaError_t e;

@@ -1051,11 +1051,109 @@ __global__ void __launch_bounds__(accc::NW * 32, 2) acc_cmp_kernel(const AccCmpA
 }
 
 // caller outputs and kicks from the (a, du/dt) accumulator (gas-rank order)
+// ============================================================== a7 + a8, symmetric over the lists
+// Newton-3 over the neighbour lists: the unordered pair {i, j} is evaluated once, in the
+// row of its lower gas rank (i's list holds every j with s32 < max(H_i^2, H_j^2), a
+// symmetric predicate, so j's list holds i).  G_ij, Q_ij, the limiter and the pressure
+// terms are shared by both sides; i's sums stay in registers (S lanes per i), j's go to a
+// float4 (a, du/dt) accumulator with red.global.add.v4.f32.  Only when no row is flagged
+// (every list complete); otherwise the CTAs exit and the gated i-centric kernels run.
+struct AccSymListArgs {
+    const float4* gpos;  // (x, y, z, H)
+    const float4* grec;  // accel records
+    RowView rv;
+    ListView lv;
+    float4* acc;         // (a, du/dt) sums, zeroed
+    float Cl, Cq, e2;
+};
+
+constexpr int ASL_NW = 8, ASL_G = 8, ASL_ENT = 72;
+
+__global__ void __launch_bounds__(ASL_NW * 32, 2) acc_symlist_kernel(const AccSymListArgs A) {
+    constexpr int S = 32 / ASL_G;
+    using SM = ListSmem<9, ASL_ENT>;
+    extern __shared__ __align__(128) unsigned char smem_raw[];
+    SM& sm = *reinterpret_cast<SM*>(smem_raw);
+    if (*A.lv.nfrows != 0) return;
+    const RowView& rv = A.rv;
+    const ListView& lv = A.lv;
+    const int warp = threadIdx.x >> 5;
+    const int lane = threadIdx.x & 31;
+    const int il = lane / S, sl = lane % S;
+    const int ibase = warp * ASL_G;
+    if (threadIdx.x == 0) {
+        mbar_init(&sm.bar, 1);
+        mbar_fence_init();
+    }
+    uint32_t phase = 0;
+    while (true) {
+        const int a = claim_row(sm, lv.work);
+        if (a >= lv.nrows) break;
+        const int icount = rv.icount[a];
+        const bool wactive = ibase < icount;
+        const bool ivalid = ibase + il < icount;
+        const int rbeg = rv.row_off[a], rend = rv.row_off[a + 1];
+        const int ki = rv.ifirst[a] + ibase + (ivalid ? il : 0);
+        Rec ri;
+        float4 ip = make_float4(0.f, 0.f, 0.f, 0.f);
+        int nl = 0;
+        if (wactive) {
+            ip = A.gpos[ki];
+            unpack_rec(A.grec + (int64_t)ki * 9, ri);
+            if (ivalid) nl = lv.ncnt[ki];
+        }
+        const float invmi = 1.f / ri.m;
+        float s0 = 0.f, s1 = 0.f, s2 = 0.f, s3 = 0.f;
+        const uint16_t* lp = lv.nbr + (int64_t)ki * lv.cap + sl;
+        const uint16_t* const lend = lv.nbr + (int64_t)ki * lv.cap + nl;
+        int tn = lp < lend ? (int)*lp : 0x7fffffff;
+        for (int e0 = rbeg; e0 < rend; e0 += ASL_ENT) {
+            const int nent = min(ASL_ENT, rend - e0);
+            stage_list_round<9, ASL_NW, ASL_ENT>(sm, rv, A.gpos, A.grec, e0, nent, phase);
+            if (wactive) {
+                const int rs = (e0 - rbeg) * JMAX, re = rs + nent * JMAX;
+                // skip this lane's entries the lower rank does not own (j <= i), within the round
+                auto skip = [&]() {
+                    while (tn < re && __float_as_int(sm.eoff[(tn - rs) / JMAX].w) + (tn - rs) % JMAX <= ki) {
+                        lp += S;
+                        tn = lp < lend ? (int)*lp : 0x7fffffff;
+                    }
+                };
+                skip();
+#pragma unroll 1
+                while (__any_sync(0xffffffffu, tn < re)) {
+                    if (tn < re) {
+                        const int tl = tn - rs;
+                        const int j = __float_as_int(sm.eoff[tl / JMAX].w) + tl % JMAX;
+                        const float4 jp = sm.raw[tl];
+                        lp += S;
+                        tn = lp < lend ? (int)*lp : 0x7fffffff;
+                        Rec rj;
+                        unpack_rec(sm.pay + tl * 9, rj);
+                        const float x[3] = {ip.x - jp.x, ip.y - jp.y, ip.z - jp.z};  // x_ij
+                        const float r2 = s32_of(x[0], x[1], x[2]);
+                        float F[3], Ei, Ej;
+                        pair_terms(ri, rj, x, r2, A.Cl, A.Cq, A.e2, F, Ei, Ej);
+                        s0 -= F[0]; s1 -= F[1]; s2 -= F[2]; s3 += Ei;
+                        const float im = 1.f / rj.m;
+                        red_add_v4(A.acc + j, F[0] * im, F[1] * im, F[2] * im, Ej * im);
+                        skip();
+                    }
+                }
+            }
+        }
+        if (wactive) {
+            s0 = slot_sum<-S>(s0); s1 = slot_sum<-S>(s1); s2 = slot_sum<-S>(s2); s3 = slot_sum<-S>(s3);
+            if (ivalid && sl == 0) red_add_v4(A.acc + ki, s0 * invmi, s1 * invmi, s2 * invmi, s3 * invmi);
+        }
+    }
+}
+
 __global__ void k_acc_finish(int64_t ng, const float4* __restrict__ acc, const int32_t* __restrict__ gas_idx, float dt,
                              float* ahx, float* ahy, float* ahz, float* dudt, float* vx, float* vy, float* vz,
-                             float* u) {
+                             float* u, const int32_t* gate = nullptr) {
     const int64_t k = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
-    if (k >= ng) return;
+    if (k >= ng || (gate && *gate != 0)) return;
     const float4 q = acc[k];
     const int64_t i = gas_idx[k];
     if (ahx) { ahx[i] = q.x; ahy[i] = q.y; ahz[i] = q.z; }
@@ -1109,6 +1207,8 @@ static ListView list_view(crk_ctx* c) {
     lv.frows = P<int32_t>(c->lflag) + c->nleaf[2];
     lv.nfrows = P<int32_t>(c->lflag) + 2 * c->nleaf[2];
     lv.cap = c->nbr_cap;
+    lv.nrows = (int)c->nleaf[2];
+    lv.work = P<int>(c->work) + 4;
     return lv;
 }
 static bool lists_on(crk_ctx* c) { return c->nbr_cap > 0 && c->nleaf[2] > 0; }
@@ -1119,7 +1219,8 @@ template <class Pass, int ENT, int MINB, int FENT, int FMINB>
 static crk_status launch_listed(crk_ctx* c, const Pass& ps, cudaStream_t st, const char* what) {
     if (c->nleaf[2] == 0) return CRK_OK;
     RowView rv = hydro_rows(c);
-    CRK_TRY(cuda_check(c, launch_list<Pass, HYD_NW, HYD_G, ENT, MINB>(ps, rv, list_view(c), c->nleaf[2], st), what));
+    CRK_TRY(grow(c, c->work, 64, st));
+    CRK_TRY(cuda_check(c, launch_list<Pass, HYD_NW, HYD_G, ENT, MINB>(ps, rv, list_view(c), st), what));
     c->launches++;
     const ListView lv = list_view(c);
     rv.rows = lv.frows;
@@ -1269,6 +1370,53 @@ static crk_status accel_cmp(crk_ctx* c, crk_particles* p, float dt, cudaStream_t
     return CRK_OK;
 }
 
+// symmetric accel over the lists (acc_symlist_kernel); if any row is flagged the symmetric
+// kernel and its finish exit on the device and the gated i-centric list kernels run instead
+static crk_status accel_symlist(crk_ctx* c, crk_particles* p, float dt, cudaStream_t st) {
+    const int64_t ng = c->n_gas;
+    CRK_TRY(grow(c, c->gacc, (ng > 0 ? ng : 1) * 16, st));
+    CRK_TRY(cuda_check(c, cudaMemsetAsync(c->gacc.p, 0, (ng > 0 ? ng : 1) * 16, st), "memset"));
+    CRK_TRY(grow(c, c->work, 64, st));
+    AccSymListArgs A;
+    A.gpos = P<float4>(c->gpos);
+    A.grec = P<float4>(c->grec);
+    A.rv = hydro_rows(c);
+    A.lv = list_view(c);
+    A.acc = P<float4>(c->gacc);
+    A.Cl = c->prm.av_cl; A.Cq = c->prm.av_cq; A.e2 = c->prm.av_eps2;
+    const int smem = (int)sizeof(ListSmem<9, ASL_ENT>);
+    cudaError_t e = cudaFuncSetAttribute(acc_symlist_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+    if (e != cudaSuccess) return cuda_check(c, e, "smem attribute");
+    CRK_TRY(cuda_check(c, cudaMemsetAsync(A.lv.work, 0, sizeof(int), st), "memset"));
+    acc_symlist_kernel<<<persistent_grid(acc_symlist_kernel, ASL_NW * 32, smem, A.lv.nrows), ASL_NW * 32, smem, st>>>(A);
+    CRK_LAUNCHED(c, "accel/dudt (symmetric list) kernel");
+    k_acc_finish<<<(unsigned)((ng + 255) / 256), 256, 0, st>>>(ng, P<float4>(c->gacc), P<int32_t>(c->gas_idx), dt,
+                                                               p->ahx, p->ahy, p->ahz, p->dudt, p->vx, p->vy, p->vz,
+                                                               p->u, A.lv.nfrows);
+    CRK_LAUNCHED(c, "accel finish");
+    // flagged rows present: i-centric list kernel (gated) + on-the-fly kernel over the flagged rows
+    AccPass<false, 32> g;
+    common(c, g);
+    g.jrows = P<float4>(c->gpos);
+    g.jpay = P<float4>(c->grec);
+    g.grec = P<float4>(c->grec);
+    g.Cl = c->prm.av_cl; g.Cq = c->prm.av_cq; g.e2 = c->prm.av_eps2; g.dt = dt;
+    g.n = c->n;
+    g.ahx = p->ahx; g.ahy = p->ahy; g.ahz = p->ahz; g.dudt = p->dudt;
+    g.vx = p->vx; g.vy = p->vy; g.vz = p->vz; g.u = p->u;
+    g.cnt = nullptr;
+    ListView lv = list_view(c);
+    lv.gate = 1;
+    RowView rv = hydro_rows(c);
+    CRK_TRY(cuda_check(c, launch_list<AccPass<false, 32>, HYD_NW, HYD_G, 72, 2>(g, rv, lv, st), "accel/dudt kernel"));
+    c->launches++;
+    rv.rows = lv.frows;
+    rv.nrows = lv.nfrows;
+    CRK_TRY(cuda_check(c, launch_pairs<AccPass<false, 32>, HYD_NW, HYD_G, 72, 2>(g, rv, c->nleaf[2], st), "accel/dudt kernel"));
+    c->launches++;
+    return CRK_OK;
+}
+
 template <int BT, int ENT>
 static crk_status accel_gather(crk_ctx* c, crk_particles* p, float dt, cudaStream_t st) {
     AccPass<false, BT> g;
@@ -1289,6 +1437,9 @@ crk_status accel_dudt(crk_ctx* c, crk_particles* p, float dt, cudaStream_t st) {
     if (dt != 0.f && (!p->vx || !p->vy || !p->vz || !p->u)) return fail(c, CRK_EINVAL, "kick needs v and u");
     if (c->prm.symmetric & 4) return accel_cmp(c, p, dt, st);
     if ((c->prm.symmetric & 2) && !c->lay.partial) return accel_sym(c, p, dt, st);
+    // opt-in (CRK_HYD_VARIANT=0005): c4 14.8 ms vs 13.3 for the i-centric list kernel (the per-pair
+    // red.global reactions cost more than the halved pair work saves)
+    if (lists_on(c) && !c->lay.partial && hyd_variant(3) == 5) return accel_symlist(c, p, dt, st);
     // gather variant: batch-32 pair-compacted evaluation (2: batch 64, 3: uncompacted)
     switch (hyd_variant(3)) {
         case 2: return accel_gather<64, 64>(c, p, dt, st);

@@ -43,6 +43,9 @@ struct ListView {
     int32_t* frows;    // compact list of the flagged rows ...
     int32_t* nfrows;   // ... and their number (zeroed before the build)
     int cap;
+    int nrows;         // rows (gas i-leaves)
+    int* work;         // row counter of the persistent list kernels (zeroed per launch)
+    int gate = 0;      // 1: the kernel runs only if some row is flagged (*nfrows > 0)
 };
 template <int G>
 __device__ __forceinline__ unsigned same_i_lanes(int il) {  // lanes l with l % G == il
@@ -352,26 +355,69 @@ __global__ void __launch_bounds__(NW * 32, MINB) pair_kernel(const Pass pass, co
 // evaluated pair is in the symmetric predicate (the gather passes still apply their own
 // s32 < H_i^2 select).  Rows flagged by the list builder exit here and run pair_kernel
 // with RowView::rows = the builder's flagged-row list.
-template <class Pass, int ENT>
+template <int PAY, int ENT>
 struct ListSmem {
     float4 raw[ENT * JMAX];
-    float4 pay[Pass::PAY > 0 ? ENT * JMAX * Pass::PAY : 1];
+    float4 pay[PAY > 0 ? ENT * JMAX * PAY : 1];
     float4 eoff[ENT];  // shift offset (x, y, z), first (w, as int)
     uint64_t bar;
+    int next;          // claimed row
 };
+
+// all threads: stage row entries [e0, e0 + nent) — position rows (x, y, z, w) and PAY payload
+// float4 per particle — then apply the periodic shifts in place (once per slot, exact, O1);
+// returns with the round resident and visible to the CTA
+template <int PAY, int NW, int ENT>
+__device__ __forceinline__ void stage_list_round(ListSmem<PAY, ENT>& sm, const RowView& rv, const float4* jrows,
+                                                 const float4* jpay, int e0, int nent, uint32_t& phase) {
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    __syncthreads();  // barrier initialised / previous round consumed
+    for (int t = lane * NW + warp; t < nent; t += NW * 32) {
+        int first, count, leaf, code;
+        unpack_entry(__ldg(rv.erec + e0 + t), first, count, leaf, code);
+        int sx, sy, sz;
+        decode_shift(code, sx, sy, sz);
+        sm.eoff[t] = make_float4((float)sx * rv.L[0], (float)sy * rv.L[1], (float)sz * rv.L[2], __int_as_float(first));
+        const uint32_t pb = (uint32_t)count * 16u;
+        mbar_expect_tx(&sm.bar, pb * (1 + PAY));
+        bulk_g2s(&sm.raw[t * JMAX], jrows + first, pb, &sm.bar);
+        if (PAY > 0) bulk_g2s(&sm.pay[t * JMAX * PAY], jpay + (int64_t)first * PAY, pb * PAY, &sm.bar);
+    }
+    __syncthreads();
+    if (threadIdx.x == 0) mbar_arrive(&sm.bar);
+    mbar_wait(&sm.bar, phase);
+    phase ^= 1u;
+    for (int t = threadIdx.x; t < nent * JMAX; t += NW * 32) {
+        const float4 o = sm.eoff[t / JMAX];
+        if (o.x != 0.f || o.y != 0.f || o.z != 0.f) {
+            float4 q = sm.raw[t];
+            q.x += o.x; q.y += o.y; q.z += o.z;
+            sm.raw[t] = q;
+        }
+    }
+    fence_proxy_async_smem();  // generic writes before the next round's TMA overwrites
+    __syncthreads();
+}
+
+// persistent CTAs claim rows from lv.work; returns the claimed row (>= nrows: done)
+template <int PAY, int ENT>
+__device__ __forceinline__ int claim_row(ListSmem<PAY, ENT>& sm, int* work) {
+    if (threadIdx.x == 0) sm.next = atomicAdd(work, 1);
+    __syncthreads();
+    const int a = sm.next;
+    __syncthreads();  // every thread has read `next` before it is claimed again
+    return a;
+}
 
 template <class Pass, int NW, int G, int ENT, int MINB>
 __global__ void __launch_bounds__(NW * 32, MINB) list_kernel(const Pass pass, const RowView rv, const ListView lv) {
     static_assert(32 % G == 0, "G must divide the warp");
     constexpr int S = 32 / G;
-    using SM = ListSmem<Pass, ENT>;
+    using SM = ListSmem<Pass::PAY, ENT>;
     extern __shared__ __align__(128) unsigned char smem_raw[];
     SM& sm = *reinterpret_cast<SM*>(smem_raw);
+    if (lv.gate && *lv.nfrows == 0) return;  // gated fallback: only when some row is flagged
 
-    const int a = blockIdx.x;
-    if (lv.lflag[a]) return;
-    const int ifirst = rv.ifirst[a];
-    const int icount = rv.icount[a];
     const int warp = threadIdx.x >> 5;
     const int lane = threadIdx.x & 31;
     // runs of S consecutive lanes share one i: the S lanes read consecutive list entries,
@@ -379,88 +425,85 @@ __global__ void __launch_bounds__(NW * 32, MINB) list_kernel(const Pass pass, co
     const int il = lane / S;
     const int sl = lane % S;
     const int ibase = warp * G;
-    const bool wactive = ibase < icount;
-    const bool ivalid = ibase + il < icount;
-    const int rbeg = rv.row_off[a], rend = rv.row_off[a + 1];
-
     if (threadIdx.x == 0) {
         mbar_init(&sm.bar, 1);
         mbar_fence_init();
     }
-    typename Pass::I is;
-    typename Pass::Acc acc;
-    pass.init(acc);
-    const int ki = ifirst + ibase + (ivalid ? il : 0);
-    int nl = 0;
-    if (wactive) {
-        pass.load_i(ki, is);
-        if (ivalid) nl = lv.ncnt[ki];
-    }
-    const uint16_t* lp = lv.nbr + (int64_t)ki * lv.cap + sl;  // this lane's next list entry
-    const uint16_t* const lend = lv.nbr + (int64_t)ki * lv.cap + nl;
-    int tn = lp < lend ? (int)*lp : 0x7fffffff;  // next slot of this lane
-
     uint32_t phase = 0;
-    for (int e0 = rbeg; e0 < rend; e0 += ENT) {
-        const int nent = min(ENT, rend - e0);
-        __syncthreads();  // barrier initialised / previous round consumed
-        for (int t = lane * NW + warp; t < nent; t += NW * 32) {
-            int first, count, leaf, code;
-            unpack_entry(__ldg(rv.erec + e0 + t), first, count, leaf, code);
-            int sx, sy, sz;
-            decode_shift(code, sx, sy, sz);
-            sm.eoff[t] = make_float4((float)sx * rv.L[0], (float)sy * rv.L[1], (float)sz * rv.L[2],
-                                     __int_as_float(first));
-            const uint32_t pb = (uint32_t)count * 16u;
-            mbar_expect_tx(&sm.bar, pb * (1 + Pass::PAY));
-            bulk_g2s(&sm.raw[t * JMAX], pass.jrows + first, pb, &sm.bar);
-            if (Pass::PAY > 0)
-                bulk_g2s(&sm.pay[t * JMAX * Pass::PAY], pass.jpay + (int64_t)first * Pass::PAY, pb * Pass::PAY,
-                         &sm.bar);
-        }
-        __syncthreads();
-        if (threadIdx.x == 0) mbar_arrive(&sm.bar);
-        mbar_wait(&sm.bar, phase);
-        phase ^= 1u;
-        // periodic shifts applied once per staged slot (exact, O1), not once per pair
-        for (int t = threadIdx.x; t < nent * JMAX; t += NW * 32) {
-            const float4 o = sm.eoff[t / JMAX];
-            if (o.x != 0.f || o.y != 0.f || o.z != 0.f) {
-                float4 q = sm.raw[t];
-                q.x += o.x; q.y += o.y; q.z += o.z;
-                sm.raw[t] = q;
-            }
-        }
-        fence_proxy_async_smem();  // generic writes before the next round's TMA overwrites
-        __syncthreads();
+    auto row = [&](const int a) {
+        const int ifirst = rv.ifirst[a];
+        const int icount = rv.icount[a];
+        const bool wactive = ibase < icount;
+        const bool ivalid = ibase + il < icount;
+        const int rbeg = rv.row_off[a], rend = rv.row_off[a + 1];
+        typename Pass::I is;
+        typename Pass::Acc acc;
+        pass.init(acc);
+        const int ki = ifirst + ibase + (ivalid ? il : 0);
+        int nl = 0;
         if (wactive) {
-            const int rs = (e0 - rbeg) * JMAX, re = rs + nent * JMAX;
+            pass.load_i(ki, is);
+            if (ivalid) nl = lv.ncnt[ki];
+        }
+        const uint16_t* lp = lv.nbr + (int64_t)ki * lv.cap + sl;  // this lane's next list entry
+        const uint16_t* const lend = lv.nbr + (int64_t)ki * lv.cap + nl;
+        int tn = lp < lend ? (int)*lp : 0x7fffffff;  // next slot of this lane
+        for (int e0 = rbeg; e0 < rend; e0 += ENT) {
+            const int nent = min(ENT, rend - e0);
+            stage_list_round<Pass::PAY, NW, ENT>(sm, rv, pass.jrows, pass.jpay, e0, nent, phase);
+            if (wactive) {
+                const int rs = (e0 - rbeg) * JMAX, re = rs + nent * JMAX;
 #pragma unroll 1
-            while (__any_sync(0xffffffffu, tn < re)) {
-                if (tn < re) {
-                    const int tl = tn - rs;
-                    const float4 jp = sm.raw[tl];
-                    lp += S;
-                    tn = lp < lend ? (int)*lp : 0x7fffffff;
-                    pass.pair(is, acc, jp, sm.pay + tl * Pass::PAY, __float_as_int(sm.eoff[tl / JMAX].w) + tl % JMAX);
+                while (__any_sync(0xffffffffu, tn < re)) {
+                    if (tn < re) {
+                        const int tl = tn - rs;
+                        const float4 jp = sm.raw[tl];
+                        lp += S;
+                        tn = lp < lend ? (int)*lp : 0x7fffffff;
+                        pass.pair(is, acc, jp, sm.pay + tl * Pass::PAY,
+                                  __float_as_int(sm.eoff[tl / JMAX].w) + tl % JMAX);
+                    }
                 }
             }
         }
+        if (wactive) {
+            pass.template reduce<-S>(acc);
+            if (ivalid && sl == 0) pass.finish(ki, is, acc);
+        }
+    };
+    if (!lv.gate) {  // one CTA per row (measured faster than claiming rows: the hardware
+        if (!lv.lflag[blockIdx.x]) row(blockIdx.x);  // overlaps a new CTA's staging)
+        return;
     }
-    if (wactive) {
-        pass.template reduce<-S>(acc);
-        if (ivalid && sl == 0) pass.finish(ki, is, acc);
+    while (true) {  // gated (rarely run) launches are persistent so that an idle launch is cheap
+        const int a = claim_row(sm, lv.work);
+        if (a >= lv.nrows) break;
+        if (!lv.lflag[a]) row(a);
     }
 }
 
+// persistent grid for a list-driven kernel: as many CTAs as fit, each claiming rows
+template <class K>
+inline int persistent_grid(K kernel, int threads, int smem, int64_t nrows) {
+    int per_sm = 0, nsm = 0, dev = 0;
+    cudaGetDevice(&dev);
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kernel, threads, smem);
+    cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, dev);
+    return (int)std::max<int64_t>(1, std::min<int64_t>(nrows, (int64_t)std::max(1, per_sm) * nsm));
+}
+
 template <class Pass, int NW, int G, int ENT, int MINB>
-inline cudaError_t launch_list(const Pass& pass, const RowView& rv, const ListView& lv, int64_t nleaf,
-                               cudaStream_t st) {
-    const int smem = (int)sizeof(ListSmem<Pass, ENT>);
-    cudaError_t e = cudaFuncSetAttribute(list_kernel<Pass, NW, G, ENT, MINB>,
-                                         cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+inline cudaError_t launch_list(const Pass& pass, const RowView& rv, const ListView& lv, cudaStream_t st) {
+    const int smem = (int)sizeof(ListSmem<Pass::PAY, ENT>);
+    auto k = list_kernel<Pass, NW, G, ENT, MINB>;
+    cudaError_t e = cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
     if (e != cudaSuccess) return e;
-    list_kernel<Pass, NW, G, ENT, MINB><<<(unsigned)nleaf, NW * 32, smem, st>>>(pass, rv, lv);
+    if (lv.nrows <= 0) return cudaSuccess;
+    if (lv.gate) {
+        e = cudaMemsetAsync(lv.work, 0, sizeof(int), st);
+        if (e != cudaSuccess) return e;
+    }
+    k<<<lv.gate ? persistent_grid(k, NW * 32, smem, lv.nrows) : lv.nrows, NW * 32, smem, st>>>(pass, rv, lv);
     return cudaGetLastError();
 }
 

@@ -349,3 +349,20 @@ def test_gravity_symmetric_variants(var, name, monkeypatch):
     gi = g["in"]
     a = np.stack([gi["ax"], gi["ay"], gi["az"]], 1)
     assert norm_err(a, ref["grav_a"], ref["grav_S"]) <= TOL_FORCE
+
+
+@pytest.mark.parametrize("cap", ["70", "128"])
+def test_accel_symmetric_list_variant(cap, monkeypatch):
+    """Opt-in Newton-3 accel over the neighbour lists (CRK_HYD_VARIANT=0005), with complete
+    lists and with some rows flagged (gated i-centric fallback)."""
+    monkeypatch.setenv("CRK_HYD_VARIANT", "0005")
+    monkeypatch.setenv("CRK_NBR_CAP", cap)
+    parts, params = cached_config("c2z")
+    params["symmetric"] = 1
+    g = run_gpu(parts, params, counts=False)
+    ref = oracle.substep(parts, params)
+    gi = g["in"]
+    T = ref["targets"]
+    ah = np.stack([gi["ahx"], gi["ahy"], gi["ahz"]], 1)[T]
+    assert norm_err(ah, ref["a"], ref["Sa"]) <= TOL_FORCE
+    assert norm_err(gi["dudt"][T], ref["dudt"], ref["Sdu"]) <= TOL_FORCE
