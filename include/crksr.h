@@ -57,11 +57,10 @@ typedef struct crk_params {
     int32_t leaf_max_gas_j;  /* gas j-leaf size: 8 */
     double cell_side;    /* chaining-mesh cell side (power of two, <= box/4) */
     int32_t symmetric;   /* kernel-variant bitmask, 0 = every kernel i-centric (each ordered pair
-                            evaluated by its i, bit-reproducible); bit 0: gravity, bit 1: accel/
-                            du-dt evaluate each unordered pair once (Newton's third law) and add
-                            the reactions with float atomics (summation order varies run to run);
-                            bit 2: accel/du-dt i-centric with pair compaction (shared-memory float
-                            atomics per i).  Same set of terms in every variant. */
+                            evaluated by its i, bit-reproducible); bit 0: gravity evaluates each
+                            unordered pair once (Newton's third law) and adds the reactions with
+                            float atomics (summation order varies run to run).  Bits 1-2 are
+                            ignored (former accel variants).  Same set of terms in every variant. */
     int32_t dom_lo[3], dom_hi[3];  /* owned chaining-mesh cells [dom_lo, dom_hi) per axis (3-D domain
                                       decomposition); all-zero dom_hi = whole box.
                                       With a partial domain, i-leaves (and so every output) exist

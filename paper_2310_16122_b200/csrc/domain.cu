@@ -70,20 +70,23 @@ __global__ void k_unpack_particles(int64_t n, int64_t off, const Rec48* __restri
     id[i] = r.id;
 }
 
+// accel record of gas rank k, component c < 9 (hydro.cu load_rec)
+__device__ __forceinline__ int64_t rec_at(int64_t ng, int64_t k, int c) { return (void)ng, 9 * k + c; }
+
 __global__ void k_pack_gas(int64_t n, int what, const int32_t* __restrict__ idx, const float* __restrict__ gV,
-                           const float4* __restrict__ grec, void* out) {
+                           const float4* __restrict__ grec, int64_t ng, void* out) {
     const int64_t t = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
     if (what == 0) {
         if (t < n) reinterpret_cast<float*>(out)[t] = gV[idx[t]];
     } else {
         if (t >= n * 9) return;
         const int64_t k = t / 9;
-        reinterpret_cast<float4*>(out)[t] = grec[(int64_t)idx[k] * 9 + t % 9];
+        reinterpret_cast<float4*>(out)[t] = grec[rec_at(ng, idx[k], (int)(t % 9))];
     }
 }
 
 __global__ void k_unpack_gas(int64_t n, int what, const int32_t* __restrict__ idx, const void* in,
-                             const float4* __restrict__ gpos, float* gV, float4* gposV, float4* grec) {
+                             const float4* __restrict__ gpos, float* gV, float4* gposV, float4* grec, int64_t ng) {
     const int64_t t = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
     if (what == 0) {
         if (t >= n) return;
@@ -95,7 +98,7 @@ __global__ void k_unpack_gas(int64_t n, int what, const int32_t* __restrict__ id
     } else {
         if (t >= n * 9) return;
         const int64_t k = t / 9;
-        grec[(int64_t)idx[k] * 9 + t % 9] = reinterpret_cast<const float4*>(in)[t];
+        grec[rec_at(ng, idx[k], (int)(t % 9))] = reinterpret_cast<const float4*>(in)[t];
     }
 }
 
@@ -209,7 +212,7 @@ crk_status crk_pack_gas(crk_ctx* c, int what, const int32_t* idx, int64_t n, voi
     if (n == 0) return CRK_OK;
     CRK_TRY(cuda_check(c, cudaSetDevice(c->device), "cudaSetDevice"));
     k_pack_gas<<<nb(what == 0 ? n : n * 9), 256, 0, (cudaStream_t)stream>>>(n, what, idx, P<float>(c->gV),
-                                                                            P<float4>(c->grec), out);
+                                                                            P<float4>(c->grec), c->n_gas, out);
     CRK_LAUNCHED(c, "pack gas");
     return CRK_OK;
 }
@@ -221,7 +224,7 @@ crk_status crk_unpack_gas(crk_ctx* c, int what, const int32_t* idx, int64_t n, c
     if (n == 0) return CRK_OK;
     CRK_TRY(cuda_check(c, cudaSetDevice(c->device), "cudaSetDevice"));
     k_unpack_gas<<<nb(what == 0 ? n : n * 9), 256, 0, (cudaStream_t)stream>>>(
-        n, what, idx, in, P<float4>(c->gpos), P<float>(c->gV), P<float4>(c->gposV), P<float4>(c->grec));
+        n, what, idx, in, P<float4>(c->gpos), P<float>(c->gV), P<float4>(c->gposV), P<float4>(c->grec), c->n_gas);
     CRK_LAUNCHED(c, "unpack gas");
     return CRK_OK;
 }

@@ -404,7 +404,7 @@ struct ExtPass : HydCommon {
         const float V = gV[k];
         const float4 vm = gvel[k];
         float4* rec = grec + (int64_t)k * 9;
-        rec[0] = make_float4(s.invH, c * s.A, V, Pk);
+        rec[0] = make_float4(g[8], c * s.A, V, Pk);
         rec[1] = make_float4(s.B[0], s.B[1], s.B[2], r);
         rec[2] = make_float4(c * s.dA[0], c * s.dA[1], c * s.dA[2], ck);
         rec[3] = make_float4(s.dB[0], s.dB[1], s.dB[2], s.dB[3]);
@@ -412,7 +412,7 @@ struct ExtPass : HydCommon {
         rec[5] = make_float4(s.dB[8], vm.x, vm.y, vm.z);
         rec[6] = make_float4(g[0], g[1], g[2], g[3]);
         rec[7] = make_float4(g[4], g[5], g[6], g[7]);
-        rec[8] = make_float4(g[8], s.H2, vm.w, u);
+        rec[8] = make_float4(s.invH, s.H2, vm.w, u);
         const int64_t i = gas_idx[k];
         if (rho) rho[i] = r;
         if (P) P[i] = Pk;
@@ -431,8 +431,13 @@ struct Rec {
     float invH, Ah, V, P, B[3], rho, dAh[3], cs, dB[9], v[3], dv[9], H2, m, u;
 };
 
-__device__ __forceinline__ void unpack_rec(const float4* r, Rec& q) {
-    float4 t = r[0]; q.invH = t.x; q.Ah = t.y; q.V = t.z; q.P = t.w;
+// Accel records (ExtPass::finish): 9 float4 per particle; the first 8 hold everything the
+// pair terms read from a neighbour, the ninth (1/H, H^2, m, u) only the particle's own use.
+// (The 9-float4 stride is odd, so the staged records of consecutive slots start in
+// different shared-memory bank groups; an 8-float4 stride put every slot's component c in
+// the same group: 8-way conflicts, accel 3x slower.)
+__device__ __forceinline__ void unpack_rec8(const float4* r, Rec& q) {
+    float4 t = r[0]; q.dv[8] = t.x; q.Ah = t.y; q.V = t.z; q.P = t.w;
     t = r[1]; q.B[0] = t.x; q.B[1] = t.y; q.B[2] = t.z; q.rho = t.w;
     t = r[2]; q.dAh[0] = t.x; q.dAh[1] = t.y; q.dAh[2] = t.z; q.cs = t.w;
     t = r[3]; q.dB[0] = t.x; q.dB[1] = t.y; q.dB[2] = t.z; q.dB[3] = t.w;
@@ -440,7 +445,18 @@ __device__ __forceinline__ void unpack_rec(const float4* r, Rec& q) {
     t = r[5]; q.dB[8] = t.x; q.v[0] = t.y; q.v[1] = t.z; q.v[2] = t.w;
     t = r[6]; q.dv[0] = t.x; q.dv[1] = t.y; q.dv[2] = t.z; q.dv[3] = t.w;
     t = r[7]; q.dv[4] = t.x; q.dv[5] = t.y; q.dv[6] = t.z; q.dv[7] = t.w;
-    t = r[8]; q.dv[8] = t.x; q.H2 = t.y; q.m = t.z; q.u = t.w;
+}
+// a neighbour's record from its staged 8 float4 and its H (the staged position row's w)
+__device__ __forceinline__ void unpack_rec_j(const float4* r, float H, Rec& q) {
+    unpack_rec8(r, q);
+    q.invH = 1.f / H;
+}
+// a particle's full record from the two planes in global memory
+__device__ __forceinline__ void load_rec(const float4* grec, int64_t ng, int64_t k, Rec& q) {
+    (void)ng;
+    unpack_rec8(grec + 9 * k, q);
+    const float4 t = grec[9 * k + 8];
+    q.invH = t.x; q.H2 = t.y; q.m = t.z; q.u = t.w;
 }
 
 // corrected kernel gradient (scaled by sigma/H^3 via Ah, dAh) at separation x with
@@ -482,7 +498,7 @@ struct AccPass : HydCommon {
     const float4* jpay;   // grec
     const float4* grec;
     float Cl, Cq, e2, dt;
-    int64_t n;
+    int64_t n, ng;
     float *ahx, *ahy, *ahz, *dudt, *vx, *vy, *vz, *u;
     int32_t* cnt;
     struct I { float x, y, z; int idx; Rec r; };
@@ -492,7 +508,7 @@ struct AccPass : HydCommon {
         const float4 p = gpos[k];
         s.x = p.x; s.y = p.y; s.z = p.z; s.idx = k;
         if (COUNT) { s.r.H2 = __fmul_rn(p.w, p.w); return; }
-        unpack_rec(grec + (int64_t)k * 9, s.r);
+        load_rec(grec, ng, k, s.r);
     }
     __device__ float ix(const I& s) const { return s.x; }
     __device__ float iy(const I& s) const { return s.y; }
@@ -512,7 +528,7 @@ struct AccPass : HydCommon {
         }
         if (!in) return;
         Rec q;
-        unpack_rec(pay, q);
+        unpack_rec_j(pay, jp.w, q);
         const float r = sqrtf(r2);
         float gi[3], gj[3];
         grad_wr(&s.r.Ah, s.r.dAh, s.r.B, s.r.dB, s.r.invH, r, x, gi);
@@ -580,16 +596,7 @@ struct AccPass : HydCommon {
     }
 };
 
-// ============================================================== a7 + a8, symmetric (Newton-3) variant
-// Every unordered gas pair is evaluated once (G_ij, Q_ij, the limiter and the pressure
-// terms are shared by both sides): by the warp of the lower 8-particle group (groups are
-// contiguous gas-rank ranges, so "j in this or a later group" is j >= gself).  Lanes own
-// the j-survivors and loop over the group's 8 i-records (shared-memory broadcast); the
-// i-side sums (a, du/dt) stay in registers and are reduced once; the j-side reactions
-// go to a float4 (a, du/dt) accumulator with red.global.add.v4.f32.  Inside the own group
-// the pair is met from both sides, so there only the survivor's half counts.
-// Row staging: TMA bulk copies of gpos rows, accel records and leaf boxes (one mbarrier).
-
+// ============================================================== a7 + a8 pair terms, shared form
 // F = V_a V_b (P_a + P_b + Q_ab) G_ab,  Ea = V_a V_b (P_a + Q/2) v_ab.G_ab,  Eb likewise with P_b
 // (x = x_a - x_b; m_a dv_a/dt gets -F, m_b dv_b/dt gets +F; m_a du_a/dt gets Ea, m_b du_b/dt Eb)
 __device__ __forceinline__ void pair_terms(const Rec& A, const Rec& B, const float x[3], float r2, float Cl,
@@ -631,426 +638,6 @@ __device__ __forceinline__ void pair_terms(const Rec& A, const Rec& B, const flo
     Eb = VV * (B.P + 0.5f * Q) * vG;
 }
 
-namespace syma {
-constexpr int NW = 8, G = 8, ENT = 56, RING = 64, REC = 9;
-struct Smem {
-    float4 raw[ENT * JMAX];
-    float4 pay[ENT * JMAX * REC];
-    float4 ebox[ENT][2];
-    float4 eoff[ENT];
-    int ecnt[ENT];
-    uint64_t bar;
-    uint16_t went[NW][ENT];
-    float4 rpos[NW][RING];
-    uint16_t rslot[NW][RING];
-    float4 ipos[NW][G];
-    float4 irec[NW][G][REC];
-};
-}  // namespace syma
-
-struct AccSymArgs {
-    const float4* gpos;
-    const float4* grec;
-    const int32_t* ifirst;
-    const int32_t* icount;
-    const int32_t* row_off;
-    const int2* erec;
-    const float4* box8;
-    float4* acc;  // (a, du/dt) per gas rank
-    float L[3];
-    float Cl, Cq, e2;
-};
-
-__global__ void __launch_bounds__(syma::NW * 32, 2) acc_sym_kernel(const AccSymArgs A) {
-    using namespace syma;
-    extern __shared__ __align__(128) unsigned char smem_raw[];
-    Smem& sm = *reinterpret_cast<Smem*>(smem_raw);
-    const int a = blockIdx.x;
-    const int ifirst = A.ifirst[a];
-    const int icount = A.icount[a];
-    const int warp = threadIdx.x >> 5;
-    const int lane = threadIdx.x & 31;
-    const int ibase = warp * G;
-    const bool wactive = ibase < icount;
-    const int gself = ifirst + ibase;
-    const int ng = min(G, icount - ibase);
-    float4* rpos = sm.rpos[warp];
-    uint16_t* rslot = sm.rslot[warp];
-    uint16_t* went = sm.went[warp];
-
-    if (threadIdx.x == 0) {
-        mbar_init(&sm.bar, 1);
-        mbar_fence_init();
-    }
-    float lo[3] = {0.f, 0.f, 0.f}, hi[3] = {0.f, 0.f, 0.f}, wcut = 0.f;
-    if (wactive) {
-        const bool iv = lane < ng;
-        float4 p = make_float4(-1e18f, -1e18f, -1e18f, 1.f);
-        if (iv) p = A.gpos[gself + lane];
-        if (lane < G) sm.ipos[warp][lane] = p;
-        for (int t = lane; t < G * REC; t += 32) {
-            const int i = t / REC;
-            sm.irec[warp][i][t % REC] = i < ng ? A.grec[(int64_t)(gself + i) * REC + t % REC]
-                                               : make_float4(0.f, 0.f, 0.f, 0.f);
-        }
-        lo[0] = warp_min(iv ? p.x : INFINITY);
-        lo[1] = warp_min(iv ? p.y : INFINITY);
-        lo[2] = warp_min(iv ? p.z : INFINITY);
-        hi[0] = warp_max(iv ? p.x : -INFINITY);
-        hi[1] = warp_max(iv ? p.y : -INFINITY);
-        hi[2] = warp_max(iv ? p.z : -INFINITY);
-        wcut = warp_max(iv ? __fmul_rn(p.w, p.w) : 0.f) * CULL_SLACK;
-    }
-    // i-side sums of group particle `lane` (lanes < G), reduced over the warp per i
-    float ia0 = 0.f, ia1 = 0.f, ia2 = 0.f, ia3 = 0.f;
-    const float Cl = A.Cl, Cq = A.Cq, e2 = A.e2;
-
-    auto eval_step = [&](int r0, int n) {
-        float4 jp = make_float4(1e18f, 1e18f, 1e18f, 1.f);
-        int t = 0;
-        const bool valid = lane < n;
-        if (valid) {
-            const int s = (r0 + lane) & (RING - 1);
-            jp = rpos[s];
-            t = rslot[s];
-        }
-        Rec rj;
-        unpack_rec(sm.pay + t * REC, rj);
-        const int j = __float_as_int(sm.eoff[t / JMAX].w) + t % JMAX;
-        const bool own = j >= gself && j < gself + ng;  // own group: j-side only
-        const float h2j = __fmul_rn(jp.w, jp.w);
-        float bj0 = 0.f, bj1 = 0.f, bj2 = 0.f, bj3 = 0.f;
-#pragma unroll 2
-        for (int i = 0; i < ng; ++i) {
-            const float4 ip = sm.ipos[warp][i];
-            const float x[3] = {ip.x - jp.x, ip.y - jp.y, ip.z - jp.z};  // x_ij
-            const float r2 = s32_of(x[0], x[1], x[2]);
-            const float h2i = __fmul_rn(ip.w, ip.w);
-            const bool in = valid && r2 < fmaxf(h2i, h2j);
-            if (__ballot_sync(0xffffffffu, in) == 0u) continue;  // no lane pairs with this i
-            Rec ri;
-            unpack_rec(sm.irec[warp][i], ri);
-            float F[3], Ei, Ej;
-            pair_terms(ri, rj, x, r2, Cl, Cq, e2, F, Ei, Ej);
-            const bool side_i = in && !own;
-            const float s0 = warp_sum(side_i ? -F[0] : 0.f), s1 = warp_sum(side_i ? -F[1] : 0.f),
-                        s2 = warp_sum(side_i ? -F[2] : 0.f), s3 = warp_sum(side_i ? Ei : 0.f);
-            if (lane == i) {
-                ia0 += s0; ia1 += s1; ia2 += s2; ia3 += s3;
-            }
-            bj0 += in ? F[0] : 0.f;
-            bj1 += in ? F[1] : 0.f;
-            bj2 += in ? F[2] : 0.f;
-            bj3 += in ? Ej : 0.f;
-        }
-        if (valid) {
-            const float im = 1.f / rj.m;
-            red_add_v4(A.acc + j, bj0 * im, bj1 * im, bj2 * im, bj3 * im);
-        }
-    };
-
-    int wr = 0, rd = 0;
-    uint32_t phase = 0;
-    const int rbeg = A.row_off[a], rend = A.row_off[a + 1];
-    for (int e0 = rbeg; e0 < rend; e0 += ENT) {
-        const int nent = min(ENT, rend - e0);
-        __syncthreads();
-        for (int t = lane * NW + warp; t < nent; t += NW * 32) {  // spread over warps (pairs.cuh)
-            int first, count, leaf, code;
-            unpack_entry(__ldg(A.erec + e0 + t), first, count, leaf, code);
-            int sx, sy, sz;
-            decode_shift(code, sx, sy, sz);
-            sm.eoff[t] = make_float4((float)sx * A.L[0], (float)sy * A.L[1], (float)sz * A.L[2], __int_as_float(first));
-            sm.ecnt[t] = count;
-            const uint32_t pb = (uint32_t)count * 16u;
-            mbar_expect_tx(&sm.bar, pb * (1 + REC) + 32u);
-            bulk_g2s(&sm.raw[t * JMAX], A.gpos + first, pb, &sm.bar);
-            bulk_g2s(&sm.pay[t * JMAX * REC], A.grec + (int64_t)first * REC, pb * REC, &sm.bar);
-            bulk_g2s(&sm.ebox[t][0], A.box8 + 2 * (int64_t)leaf, 32u, &sm.bar);
-        }
-        __syncthreads();
-        if (threadIdx.x == 0) mbar_arrive(&sm.bar);
-        mbar_wait(&sm.bar, phase);
-        phase ^= 1u;
-        if (wactive) {
-            int nsurv = 0;
-            for (int e = lane; e - lane < nent; e += 32) {
-                bool ek = false;
-                if (e < nent) {
-                    const float4 o = sm.eoff[e];
-                    const float4 bl = sm.ebox[e][0], bh = sm.ebox[e][1];
-                    const float gx = fmaxf(fmaxf(bl.x + o.x - hi[0], lo[0] - bh.x - o.x), 0.f);
-                    const float gy = fmaxf(fmaxf(bl.y + o.y - hi[1], lo[1] - bh.y - o.y), 0.f);
-                    const float gz = fmaxf(fmaxf(bl.z + o.z - hi[2], lo[2] - bh.z - o.z), 0.f);
-                    ek = fmaf(gz, gz, fmaf(gy, gy, gx * gx)) < fmaxf(wcut, bl.w * CULL_SLACK) &&
-                         __float_as_int(o.w) + sm.ecnt[e] > gself;
-                }
-                const unsigned em = __ballot_sync(0xffffffffu, ek);
-                if (ek) went[nsurv + __popc(em & ((1u << lane) - 1u))] = (uint16_t)e;
-                nsurv += __popc(em);
-            }
-            __syncwarp();
-            for (int q0 = 0; q0 < nsurv; q0 += 32 / JMAX) {
-                const int qe = q0 + lane / JMAX;
-                const int kk = lane % JMAX;
-                const int e = went[qe < nsurv ? qe : 0];
-                const float4 o = sm.eoff[e];
-                const int t = e * JMAX + kk;
-                float4 p = sm.raw[t];
-                p.x += o.x; p.y += o.y; p.z += o.z;
-                const int j = __float_as_int(o.w) + kk;
-                const bool keep = qe < nsurv && kk < sm.ecnt[e] && j >= gself &&
-                                  box_dist2(p.x, p.y, p.z, lo, hi) < fmaxf(wcut, __fmul_rn(p.w, p.w) * CULL_SLACK);
-                const unsigned msk = __ballot_sync(0xffffffffu, keep);
-                if (keep) {
-                    const int s = (wr + __popc(msk & ((1u << lane) - 1u))) & (RING - 1);
-                    rpos[s] = p;
-                    rslot[s] = (uint16_t)t;
-                }
-                wr += __popc(msk);
-                __syncwarp();
-                if (wr - rd >= 32) {
-                    eval_step(rd, 32);
-                    rd += 32;
-                    __syncwarp();
-                }
-            }
-            if (e0 + ENT < rend && wr > rd) {  // slots are restaged next round: flush
-                eval_step(rd, wr - rd);
-                rd = wr;
-                __syncwarp();
-            }
-        }
-    }
-    if (wactive) {
-        if (wr > rd) eval_step(rd, wr - rd);
-        if (lane < ng) {
-            const float im = 1.f / sm.irec[warp][lane][8].z;  // 1 / m_i
-            red_add_v4(A.acc + gself + lane, ia0 * im, ia1 * im, ia2 * im, ia3 * im);
-        }
-    }
-}
-
-// ============================================================== a7 + a8, pair-compacted i-centric variant
-// Same arithmetic as AccPass (each ordered pair once, by its i), but the lanes never idle
-// on out-of-range pairs: a warp tests the exact symmetric predicate for (i, survivor)
-// pairs of its 8 i-particles (cheap), compacts the passing pairs into a per-warp pair
-// ring and evaluates 32 real pairs per step, each lane with its own (i, j); the per-i
-// sums go to shared memory with red.shared.add.f32 (4 per pair).  Summation order
-// within a warp is scheduling dependent (float shared atomics).
-namespace accc {
-constexpr int NW = 8, G = 8, ENT = 64, RING = 64, PRING = 64, REC = 9;
-struct Smem {
-    float4 raw[ENT * JMAX];
-    float4 pay[ENT * JMAX * REC];
-    float4 ebox[ENT][2];
-    float4 eoff[ENT];
-    int ecnt[ENT];
-    uint64_t bar;
-    uint16_t went[NW][ENT];
-    uint16_t rslot[NW][RING];
-    uint32_t pring[NW][PRING];
-    float4 ipos[NW][G];
-    float4 irec[NW][G][REC];
-    float acc[NW][G][4];
-};
-}  // namespace accc
-
-struct AccCmpArgs {
-    const float4* gpos;
-    const float4* grec;
-    const int32_t* gas_idx;
-    const int32_t* ifirst;
-    const int32_t* icount;
-    const int32_t* row_off;
-    const int2* erec;
-    const float4* box8;
-    float L[3];
-    float Cl, Cq, e2, dt;
-    float *ahx, *ahy, *ahz, *dudt, *vx, *vy, *vz, *u;
-};
-
-__device__ __forceinline__ void red_shared_add(float* p, float v) {
-    asm volatile("red.shared.add.f32 [%0], %1;" ::"r"(smem_u32(p)), "f"(v) : "memory");
-}
-
-__global__ void __launch_bounds__(accc::NW * 32, 2) acc_cmp_kernel(const AccCmpArgs A) {
-    using namespace accc;
-    extern __shared__ __align__(128) unsigned char smem_raw[];
-    Smem& sm = *reinterpret_cast<Smem*>(smem_raw);
-    const int a = blockIdx.x;
-    const int ifirst = A.ifirst[a];
-    const int icount = A.icount[a];
-    const int warp = threadIdx.x >> 5;
-    const int lane = threadIdx.x & 31;
-    const int ibase = warp * G;
-    const bool wactive = ibase < icount;
-    const int gself = ifirst + ibase;
-    const int ng = min(G, icount - ibase);
-    uint16_t* rslot = sm.rslot[warp];
-    uint16_t* went = sm.went[warp];
-    uint32_t* pring = sm.pring[warp];
-
-    if (threadIdx.x == 0) {
-        mbar_init(&sm.bar, 1);
-        mbar_fence_init();
-    }
-    float lo[3] = {0.f, 0.f, 0.f}, hi[3] = {0.f, 0.f, 0.f}, wcut = 0.f;
-    if (wactive) {
-        const bool iv = lane < ng;
-        float4 p = make_float4(-1e18f, -1e18f, -1e18f, 1.f);
-        if (iv) p = A.gpos[gself + lane];
-        if (lane < G) sm.ipos[warp][lane] = p;
-        for (int t = lane; t < G * REC; t += 32) {
-            const int i = t / REC;
-            sm.irec[warp][i][t % REC] = i < ng ? A.grec[(int64_t)(gself + i) * REC + t % REC]
-                                               : make_float4(0.f, 0.f, 0.f, 0.f);
-        }
-        sm.acc[warp][lane >> 2][lane & 3] = 0.f;
-        lo[0] = warp_min(iv ? p.x : INFINITY);
-        lo[1] = warp_min(iv ? p.y : INFINITY);
-        lo[2] = warp_min(iv ? p.z : INFINITY);
-        hi[0] = warp_max(iv ? p.x : -INFINITY);
-        hi[1] = warp_max(iv ? p.y : -INFINITY);
-        hi[2] = warp_max(iv ? p.z : -INFINITY);
-        wcut = warp_max(iv ? __fmul_rn(p.w, p.w) : 0.f) * CULL_SLACK;
-    }
-    const float Cl = A.Cl, Cq = A.Cq, e2 = A.e2;
-
-    // evaluate pairs [prd, prd + n) of the pair ring, one per lane
-    auto eval_pairs = [&](int prd, int n) {
-        if (lane < n) {
-            const uint32_t pr = pring[(prd + lane) & (PRING - 1)];
-            const int i = pr & 7;
-            const int t = pr >> 3;
-            const float4 o = sm.eoff[t / JMAX];
-            const float4 jr = sm.raw[t];
-            const float4 ip = sm.ipos[warp][i];
-            const float x[3] = {ip.x - (jr.x + o.x), ip.y - (jr.y + o.y), ip.z - (jr.z + o.z)};  // x_ij
-            const float r2 = s32_of(x[0], x[1], x[2]);
-            Rec ri, rj;
-            unpack_rec(sm.irec[warp][i], ri);
-            unpack_rec(sm.pay + t * REC, rj);
-            float F[3], Ei, Ej;
-            pair_terms(ri, rj, x, r2, Cl, Cq, e2, F, Ei, Ej);
-            float* ac = sm.acc[warp][i];
-            red_shared_add(ac + 0, -F[0]);
-            red_shared_add(ac + 1, -F[1]);
-            red_shared_add(ac + 2, -F[2]);
-            red_shared_add(ac + 3, Ei);
-        }
-    };
-
-    int wr = 0, rd = 0, pw = 0, prd = 0;
-    // test up to 4 survivors [rd, rd + ns) against the 8 i's: lane = i + 8 s
-    auto test_pairs = [&](int ns) {
-        const int i = lane & 7, s = lane >> 3;
-        bool keep = false;
-        int t = 0;
-        if (s < ns && i < ng) {
-            t = rslot[(rd + s) & (RING - 1)];
-            const float4 o = sm.eoff[t / JMAX];
-            const float4 jr = sm.raw[t];
-            const float4 ip = sm.ipos[warp][i];
-            const float dx = ip.x - (jr.x + o.x), dy = ip.y - (jr.y + o.y), dz = ip.z - (jr.z + o.z);
-            const float r2 = s32_of(dx, dy, dz);
-            const int j = __float_as_int(o.w) + t % JMAX;
-            keep = j != gself + i && r2 < fmaxf(__fmul_rn(ip.w, ip.w), __fmul_rn(jr.w, jr.w));
-        }
-        const unsigned m = __ballot_sync(0xffffffffu, keep);
-        if (keep) pring[(pw + __popc(m & ((1u << lane) - 1u))) & (PRING - 1)] = (uint32_t)i | ((uint32_t)t << 3);
-        pw += __popc(m);
-        rd += ns;
-        __syncwarp();
-        if (pw - prd >= 32) {
-            eval_pairs(prd, 32);
-            prd += 32;
-        }
-        __syncwarp();
-    };
-
-    uint32_t phase = 0;
-    const int rbeg = A.row_off[a], rend = A.row_off[a + 1];
-    for (int e0 = rbeg; e0 < rend; e0 += ENT) {
-        const int nent = min(ENT, rend - e0);
-        __syncthreads();
-        for (int t = lane * NW + warp; t < nent; t += NW * 32) {  // spread over warps (pairs.cuh)
-            int first, count, leaf, code;
-            unpack_entry(__ldg(A.erec + e0 + t), first, count, leaf, code);
-            int sx, sy, sz;
-            decode_shift(code, sx, sy, sz);
-            sm.eoff[t] = make_float4((float)sx * A.L[0], (float)sy * A.L[1], (float)sz * A.L[2], __int_as_float(first));
-            sm.ecnt[t] = count;
-            const uint32_t pb = (uint32_t)count * 16u;
-            mbar_expect_tx(&sm.bar, pb * (1 + REC) + 32u);
-            bulk_g2s(&sm.raw[t * JMAX], A.gpos + first, pb, &sm.bar);
-            bulk_g2s(&sm.pay[t * JMAX * REC], A.grec + (int64_t)first * REC, pb * REC, &sm.bar);
-            bulk_g2s(&sm.ebox[t][0], A.box8 + 2 * (int64_t)leaf, 32u, &sm.bar);
-        }
-        __syncthreads();
-        if (threadIdx.x == 0) mbar_arrive(&sm.bar);
-        mbar_wait(&sm.bar, phase);
-        phase ^= 1u;
-        if (wactive) {
-            int nsurv = 0;
-            for (int e = lane; e - lane < nent; e += 32) {
-                bool ek = false;
-                if (e < nent) {
-                    const float4 o = sm.eoff[e];
-                    const float4 bl = sm.ebox[e][0], bh = sm.ebox[e][1];
-                    const float gx = fmaxf(fmaxf(bl.x + o.x - hi[0], lo[0] - bh.x - o.x), 0.f);
-                    const float gy = fmaxf(fmaxf(bl.y + o.y - hi[1], lo[1] - bh.y - o.y), 0.f);
-                    const float gz = fmaxf(fmaxf(bl.z + o.z - hi[2], lo[2] - bh.z - o.z), 0.f);
-                    ek = fmaf(gz, gz, fmaf(gy, gy, gx * gx)) < fmaxf(wcut, bl.w * CULL_SLACK);
-                }
-                const unsigned em = __ballot_sync(0xffffffffu, ek);
-                if (ek) went[nsurv + __popc(em & ((1u << lane) - 1u))] = (uint16_t)e;
-                nsurv += __popc(em);
-            }
-            __syncwarp();
-            for (int q0 = 0; q0 < nsurv; q0 += 32 / JMAX) {
-                const int qe = q0 + lane / JMAX;
-                const int kk = lane % JMAX;
-                const int e = went[qe < nsurv ? qe : 0];
-                const float4 o = sm.eoff[e];
-                const int t = e * JMAX + kk;
-                float4 p = sm.raw[t];
-                p.x += o.x; p.y += o.y; p.z += o.z;
-                const bool keep = qe < nsurv && kk < sm.ecnt[e] &&
-                                  box_dist2(p.x, p.y, p.z, lo, hi) < fmaxf(wcut, __fmul_rn(p.w, p.w) * CULL_SLACK);
-                const unsigned msk = __ballot_sync(0xffffffffu, keep);
-                if (keep) rslot[(wr + __popc(msk & ((1u << lane) - 1u))) & (RING - 1)] = (uint16_t)t;
-                wr += __popc(msk);
-                __syncwarp();
-                while (wr - rd >= 4) test_pairs(4);
-            }
-            if (wr > rd) test_pairs(wr - rd);  // slots are restaged next round: drain everything
-            if (pw > prd) {
-                eval_pairs(prd, pw - prd);
-                prd = pw;
-            }
-            __syncwarp();
-        }
-    }
-    if (wactive && lane < ng) {
-        __syncwarp(__activemask());
-        const int k = gself + lane;
-        const float im = 1.f / sm.irec[warp][lane][8].z;  // 1 / m_i
-        const float a0 = sm.acc[warp][lane][0] * im, a1 = sm.acc[warp][lane][1] * im;
-        const float a2 = sm.acc[warp][lane][2] * im, du = sm.acc[warp][lane][3] * im;
-        const int64_t i = A.gas_idx[k];
-        if (A.ahx) { A.ahx[i] = a0; A.ahy[i] = a1; A.ahz[i] = a2; }
-        if (A.dudt) A.dudt[i] = du;
-        if (A.dt != 0.f) {
-            A.vx[i] = fmaf(A.dt, a0, A.vx[i]);
-            A.vy[i] = fmaf(A.dt, a1, A.vy[i]);
-            A.vz[i] = fmaf(A.dt, a2, A.vz[i]);
-            A.u[i] = fmaf(A.dt, du, A.u[i]);
-        }
-    }
-}
-
-// caller outputs and kicks from the (a, du/dt) accumulator (gas-rank order)
 // ============================================================== a7 + a8, symmetric over the lists
 // Newton-3 over the neighbour lists: the unordered pair {i, j} is evaluated once, in the
 // row of its lower gas rank (i's list holds every j with s32 < max(H_i^2, H_j^2), a
@@ -1064,6 +651,7 @@ struct AccSymListArgs {
     RowView rv;
     ListView lv;
     float4* acc;         // (a, du/dt) sums, zeroed
+    int64_t ng;
     float Cl, Cq, e2;
 };
 
@@ -1099,7 +687,7 @@ __global__ void __launch_bounds__(ASL_NW * 32, 2) acc_symlist_kernel(const AccSy
         int nl = 0;
         if (wactive) {
             ip = A.gpos[ki];
-            unpack_rec(A.grec + (int64_t)ki * 9, ri);
+            load_rec(A.grec, A.ng, ki, ri);
             if (ivalid) nl = lv.ncnt[ki];
         }
         const float invmi = 1.f / ri.m;
@@ -1129,7 +717,8 @@ __global__ void __launch_bounds__(ASL_NW * 32, 2) acc_symlist_kernel(const AccSy
                         lp += S;
                         tn = lp < lend ? (int)*lp : 0x7fffffff;
                         Rec rj;
-                        unpack_rec(sm.pay + tl * 9, rj);
+                        unpack_rec_j(sm.pay + tl * 9, jp.w, rj);
+                        rj.m = sm.pay[tl * 9 + 8].z;
                         const float x[3] = {ip.x - jp.x, ip.y - jp.y, ip.z - jp.z};  // x_ij
                         const float r2 = s32_of(x[0], x[1], x[2]);
                         float F[3], Ei, Ej;
@@ -1316,60 +905,6 @@ crk_status extras(crk_ctx* c, crk_particles* p, cudaStream_t st) {
     }
 }
 
-static crk_status accel_sym(crk_ctx* c, crk_particles* p, float dt, cudaStream_t st) {
-    const int64_t ng = c->n_gas;
-    CRK_TRY(grow(c, c->gacc, (ng > 0 ? ng : 1) * 16, st));
-    CRK_TRY(cuda_check(c, cudaMemsetAsync(c->gacc.p, 0, (ng > 0 ? ng : 1) * 16, st), "memset"));
-    if (c->nleaf[2] > 0) {
-        AccSymArgs A;
-        A.gpos = P<float4>(c->gpos);
-        A.grec = P<float4>(c->grec);
-        A.ifirst = P<int32_t>(c->lfirst[2]);
-        A.icount = P<int32_t>(c->lcount[2]);
-        A.row_off = P<int32_t>(c->rowoff[1]);
-        A.erec = P<int2>(c->erec[1]);
-        A.box8 = P<float4>(c->lbox8[3]);
-        A.acc = P<float4>(c->gacc);
-        for (int d = 0; d < 3; ++d) A.L[d] = c->lay.L[d];
-        A.Cl = c->prm.av_cl; A.Cq = c->prm.av_cq; A.e2 = c->prm.av_eps2;
-        const int smem = (int)sizeof(syma::Smem);
-        cudaError_t e = cudaFuncSetAttribute(acc_sym_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
-        if (e != cudaSuccess) return cuda_check(c, e, "smem attribute");
-        acc_sym_kernel<<<(unsigned)c->nleaf[2], syma::NW * 32, smem, st>>>(A);
-        CRK_LAUNCHED(c, "accel/dudt (symmetric) kernel");
-    }
-    if (ng > 0) {
-        k_acc_finish<<<(unsigned)((ng + 255) / 256), 256, 0, st>>>(ng, P<float4>(c->gacc), P<int32_t>(c->gas_idx), dt,
-                                                                   p->ahx, p->ahy, p->ahz, p->dudt, p->vx, p->vy,
-                                                                   p->vz, p->u);
-        CRK_LAUNCHED(c, "accel finish");
-    }
-    return CRK_OK;
-}
-
-static crk_status accel_cmp(crk_ctx* c, crk_particles* p, float dt, cudaStream_t st) {
-    if (c->nleaf[2] == 0) return CRK_OK;
-    AccCmpArgs A;
-    A.gpos = P<float4>(c->gpos);
-    A.grec = P<float4>(c->grec);
-    A.gas_idx = P<int32_t>(c->gas_idx);
-    A.ifirst = P<int32_t>(c->lfirst[2]);
-    A.icount = P<int32_t>(c->lcount[2]);
-    A.row_off = P<int32_t>(c->rowoff[1]);
-    A.erec = P<int2>(c->erec[1]);
-    A.box8 = P<float4>(c->lbox8[3]);
-    for (int d = 0; d < 3; ++d) A.L[d] = c->lay.L[d];
-    A.Cl = c->prm.av_cl; A.Cq = c->prm.av_cq; A.e2 = c->prm.av_eps2; A.dt = dt;
-    A.ahx = p->ahx; A.ahy = p->ahy; A.ahz = p->ahz; A.dudt = p->dudt;
-    A.vx = p->vx; A.vy = p->vy; A.vz = p->vz; A.u = p->u;
-    const int smem = (int)sizeof(accc::Smem);
-    cudaError_t e = cudaFuncSetAttribute(acc_cmp_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
-    if (e != cudaSuccess) return cuda_check(c, e, "smem attribute");
-    acc_cmp_kernel<<<(unsigned)c->nleaf[2], accc::NW * 32, smem, st>>>(A);
-    CRK_LAUNCHED(c, "accel/dudt (pair-compacted) kernel");
-    return CRK_OK;
-}
-
 // symmetric accel over the lists (acc_symlist_kernel); if any row is flagged the symmetric
 // kernel and its finish exit on the device and the gated i-centric list kernels run instead
 static crk_status accel_symlist(crk_ctx* c, crk_particles* p, float dt, cudaStream_t st) {
@@ -1383,6 +918,7 @@ static crk_status accel_symlist(crk_ctx* c, crk_particles* p, float dt, cudaStre
     A.rv = hydro_rows(c);
     A.lv = list_view(c);
     A.acc = P<float4>(c->gacc);
+    A.ng = c->n_gas;
     A.Cl = c->prm.av_cl; A.Cq = c->prm.av_cq; A.e2 = c->prm.av_eps2;
     const int smem = (int)sizeof(ListSmem<9, ASL_ENT>);
     cudaError_t e = cudaFuncSetAttribute(acc_symlist_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
@@ -1402,6 +938,7 @@ static crk_status accel_symlist(crk_ctx* c, crk_particles* p, float dt, cudaStre
     g.grec = P<float4>(c->grec);
     g.Cl = c->prm.av_cl; g.Cq = c->prm.av_cq; g.e2 = c->prm.av_eps2; g.dt = dt;
     g.n = c->n;
+    g.ng = c->n_gas;
     g.ahx = p->ahx; g.ahy = p->ahy; g.ahz = p->ahz; g.dudt = p->dudt;
     g.vx = p->vx; g.vy = p->vy; g.vz = p->vz; g.u = p->u;
     g.cnt = nullptr;
@@ -1426,6 +963,7 @@ static crk_status accel_gather(crk_ctx* c, crk_particles* p, float dt, cudaStrea
     g.grec = P<float4>(c->grec);
     g.Cl = c->prm.av_cl; g.Cq = c->prm.av_cq; g.e2 = c->prm.av_eps2; g.dt = dt;
     g.n = c->n;
+    g.ng = c->n_gas;
     g.ahx = p->ahx; g.ahy = p->ahy; g.ahz = p->ahz; g.dudt = p->dudt;
     g.vx = p->vx; g.vy = p->vy; g.vz = p->vz; g.u = p->u;
     g.cnt = nullptr;
@@ -1435,8 +973,6 @@ static crk_status accel_gather(crk_ctx* c, crk_particles* p, float dt, cudaStrea
 
 crk_status accel_dudt(crk_ctx* c, crk_particles* p, float dt, cudaStream_t st) {
     if (dt != 0.f && (!p->vx || !p->vy || !p->vz || !p->u)) return fail(c, CRK_EINVAL, "kick needs v and u");
-    if (c->prm.symmetric & 4) return accel_cmp(c, p, dt, st);
-    if ((c->prm.symmetric & 2) && !c->lay.partial) return accel_sym(c, p, dt, st);
     // opt-in (CRK_HYD_VARIANT=0005): c4 14.8 ms vs 13.3 for the i-centric list kernel (the per-pair
     // red.global reactions cost more than the halved pair work saves)
     if (lists_on(c) && !c->lay.partial && hyd_variant(3) == 5) return accel_symlist(c, p, dt, st);
