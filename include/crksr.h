@@ -135,6 +135,13 @@ crk_status crk_corrections(struct crk_ctx* ctx, crk_particles* parts, void* stre
  * grad v = sum V_j (v_j - v_i) grad W^R_ij (O8).  Reads the (possibly kicked) v. */
 crk_status crk_extras(struct crk_ctx* ctx, crk_particles* parts, void* stream);
 
+/* a5 + a6 in one call, with the results of crk_corrections followed by crk_extras: each
+ * gas particle's neighbour list is walked twice by one kernel (Corrections, then Extras
+ * with the coefficients just computed, PAPER.md:377 upCor -> upBarEx), sharing the staged
+ * neighbour rows.  Call after crk_geometry; leaves the context ready for
+ * crk_hydro_accel_dudt.  Reads v and u (as crk_extras does). */
+crk_status crk_corrections_extras(struct crk_ctx* ctx, crk_particles* parts, void* stream);
+
 /* a7 + a8 Acceleration and Energy (upBarAc, upBarDu): antisymmetrised CRK-SPH momentum
  * and energy derivatives with artificial viscosity (O9); kicks v += dt a_h and
  * u += dt du/dt (dt = 0: derivatives only). */

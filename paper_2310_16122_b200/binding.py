@@ -18,8 +18,8 @@ STATUS = {0: "CRK_OK", -1: "CRK_EINVAL", -2: "CRK_ENOMEM", -3: "CRK_ECUDA", -4: 
 
 # exported symbols declared in include/crksr.h (tests check the .so exports all of them)
 EXPORTS = ["crk_create", "crk_destroy", "crk_build_lists", "crk_gravity_kick", "crk_geometry",
-           "crk_corrections", "crk_extras", "crk_hydro_accel_dudt", "crk_count_pairs", "crk_list_view",
-           "crk_launch_count", "crk_status_string", "crk_last_error", "crk_select_cells", "crk_select_gas",
+           "crk_corrections", "crk_extras", "crk_corrections_extras", "crk_hydro_accel_dudt", "crk_count_pairs",
+           "crk_list_view", "crk_launch_count", "crk_status_string", "crk_last_error", "crk_select_cells", "crk_select_gas",
            "crk_pack_particles", "crk_unpack_particles", "crk_pack_gas", "crk_unpack_gas"]
 
 
@@ -74,7 +74,7 @@ def lib():
         vp = C.c_void_p
         L.crk_create.argtypes = [C.POINTER(CrkParams), C.c_int, C.POINTER(vp)]
         L.crk_destroy.argtypes = [vp]
-        for f in ("crk_build_lists", "crk_geometry", "crk_corrections", "crk_extras"):
+        for f in ("crk_build_lists", "crk_geometry", "crk_corrections", "crk_extras", "crk_corrections_extras"):
             getattr(L, f).argtypes = [vp, C.POINTER(CrkParticles), vp]
         for f in ("crk_gravity_kick", "crk_hydro_accel_dudt"):
             getattr(L, f).argtypes = [vp, C.POINTER(CrkParticles), C.c_float, vp]
@@ -94,8 +94,8 @@ def lib():
         L.crk_pack_gas.argtypes = [vp, C.c_int, vp, C.c_int64, vp, vp]
         L.crk_unpack_gas.argtypes = [vp, C.c_int, vp, C.c_int64, vp, vp]
         for f in ("crk_create", "crk_destroy", "crk_build_lists", "crk_gravity_kick", "crk_geometry",
-                  "crk_corrections", "crk_extras", "crk_hydro_accel_dudt", "crk_count_pairs", "crk_list_view",
-                  "crk_select_cells", "crk_select_gas", "crk_pack_particles", "crk_unpack_particles",
+                  "crk_corrections", "crk_extras", "crk_corrections_extras", "crk_hydro_accel_dudt",
+                  "crk_count_pairs", "crk_list_view", "crk_select_cells", "crk_select_gas", "crk_pack_particles", "crk_unpack_particles",
                   "crk_pack_gas", "crk_unpack_gas"):
             getattr(L, f).restype = C.c_int
         _lib = L
@@ -234,17 +234,24 @@ class Solver:
     def extras(self, parts, stream=None):
         self._call(lib().crk_extras, parts, stream=stream)
 
+    def corrections_extras(self, parts, stream=None):
+        """a5 + a6 fused (crk_corrections_extras): the same results as corrections() then extras()."""
+        self._call(lib().crk_corrections_extras, parts, stream=stream)
+
     def hydro_accel_dudt(self, parts, dt=0.0, stream=None):
         self._call(lib().crk_hydro_accel_dudt, parts, C.c_float(dt), stream=stream)
 
-    def substep(self, parts, dt_grav=0.0, dt_hydro=0.0, stream=None, hydro=True):
+    def substep(self, parts, dt_grav=0.0, dt_hydro=0.0, stream=None, hydro=True, fused=True):
         """The whole short-range substep: a1-a8 in call order."""
         self.build_lists(parts, stream)
         self.gravity_kick(parts, dt_grav, stream)
         if hydro:
             self.geometry(parts, stream)
-            self.corrections(parts, stream)
-            self.extras(parts, stream)
+            if fused:
+                self.corrections_extras(parts, stream)
+            else:
+                self.corrections(parts, stream)
+                self.extras(parts, stream)
             self.hydro_accel_dudt(parts, dt_hydro, stream)
 
     def count_pairs(self, parts, stream=None):

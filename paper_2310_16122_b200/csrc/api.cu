@@ -16,6 +16,7 @@ crk_status gravity_count(crk_ctx* c, crk_particles* p, int32_t* cnt, cudaStream_
 crk_status geometry(crk_ctx* c, crk_particles* p, cudaStream_t st);
 crk_status corrections(crk_ctx* c, crk_particles* p, cudaStream_t st);
 crk_status extras(crk_ctx* c, crk_particles* p, cudaStream_t st);
+crk_status corrections_extras(crk_ctx* c, crk_particles* p, cudaStream_t st);
 crk_status accel_dudt(crk_ctx* c, crk_particles* p, float dt, cudaStream_t st);
 crk_status hydro_count(crk_ctx* c, int32_t* cgather, int32_t* csym, cudaStream_t st);
 
@@ -203,6 +204,15 @@ crk_status crk_extras(crk_ctx* c, crk_particles* p, void* stream) {
     if (c->stage < ST_COR) return fail(c, CRK_ESTATE, "call crk_corrections first");
     if (!p->vx || !p->vy || !p->vz || !p->u) return fail(c, CRK_EINVAL, "extras needs v and u");
     CRK_TRY(extras(c, p, (cudaStream_t)stream));
+    c->stage = ST_EXT;
+    return CRK_OK;
+}
+
+crk_status crk_corrections_extras(crk_ctx* c, crk_particles* p, void* stream) {
+    CRK_TRY(check_parts(c, p, true));
+    if (c->stage < ST_GEO) return fail(c, CRK_ESTATE, "call crk_geometry first");
+    if (!p->vx || !p->vy || !p->vz || !p->u) return fail(c, CRK_EINVAL, "extras needs v and u");
+    CRK_TRY(corrections_extras(c, p, (cudaStream_t)stream));
     c->stage = ST_EXT;
     return CRK_OK;
 }

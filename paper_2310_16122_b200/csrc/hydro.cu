@@ -851,7 +851,7 @@ crk_status geometry(crk_ctx* c, crk_particles* p, cudaStream_t st) {
     return launch_hyd<GeoPass<false>, 128, 2>(c, g, st, "geometry kernel");
 }
 
-crk_status corrections(crk_ctx* c, crk_particles* p, cudaStream_t st) {
+static CorPass cor_pass(crk_ctx* c, crk_particles* p) {
     CorPass g;
     common(c, g);
     g.jrows = P<float4>(c->gposV);
@@ -860,6 +860,11 @@ crk_status corrections(crk_ctx* c, crk_particles* p, cudaStream_t st) {
     g.ng = c->n_gas;
     g.A = p->A; g.B = p->B; g.dA = p->dA; g.dB = p->dB;
     g.n = c->n;
+    return g;
+}
+
+crk_status corrections(crk_ctx* c, crk_particles* p, cudaStream_t st) {
+    CorPass g = cor_pass(c, p);
     if (lists_on(c)) return launch_listed<CorPass, 128, 3, 128, 3>(c, g, st, "corrections kernel");
     switch (hyd_variant(1)) {
         case 1: return launch_hyd<CorPass, 128, 1, 16, 4>(c, g, st, "corrections kernel");
@@ -878,11 +883,14 @@ __global__ void k_gather_gas_state(int64_t ng, const int32_t* gas_idx, const flo
     gu[k] = u[i];
 }
 
-crk_status extras(crk_ctx* c, crk_particles* p, cudaStream_t st) {
-    if (c->n_gas == 0) return CRK_OK;
+static crk_status gather_gas_state(crk_ctx* c, crk_particles* p, cudaStream_t st) {
     k_gather_gas_state<<<(unsigned)((c->n_gas + 255) / 256), 256, 0, st>>>(
         c->n_gas, P<int32_t>(c->gas_idx), p->vx, p->vy, p->vz, p->m, p->u, P<float4>(c->gvel), P<float>(c->gu));
     CRK_LAUNCHED(c, "gather gas state");
+    return CRK_OK;
+}
+
+static ExtPass ext_pass(crk_ctx* c, crk_particles* p) {
     ExtPass g;
     common(c, g);
     g.jrows = P<float4>(c->gposV);
@@ -896,6 +904,13 @@ crk_status extras(crk_ctx* c, crk_particles* p, cudaStream_t st) {
     g.n = c->n;
     g.gamma = c->prm.gamma;
     g.rho = p->rho; g.P = p->P; g.cs = p->cs; g.dv = p->dv;
+    return g;
+}
+
+crk_status extras(crk_ctx* c, crk_particles* p, cudaStream_t st) {
+    if (c->n_gas == 0) return CRK_OK;
+    CRK_TRY(gather_gas_state(c, p, st));
+    ExtPass g = ext_pass(c, p);
     if (lists_on(c)) return launch_listed<ExtPass, 128, 3, 128, 3>(c, g, st, "extras kernel");
     switch (hyd_variant(2)) {
         case 1: return launch_hyd<ExtPass, 128, 1, 16, 4>(c, g, st, "extras kernel");
@@ -903,6 +918,30 @@ crk_status extras(crk_ctx* c, crk_particles* p, cudaStream_t st) {
         case 3: return launch_hyd<Compacted<ExtPass, 64>, 128, 3>(c, {g}, st, "extras kernel");
         default: return launch_hyd<ExtPass, 128, 3>(c, g, st, "extras kernel");
     }
+}
+
+// a5 + a6 fused: one list kernel walks each i's list twice (Corrections, then Extras with
+// the coefficients just computed), sharing the row staging; flagged rows run the on-the-fly
+// Corrections then Extras kernels over the flagged-row list.
+crk_status corrections_extras(crk_ctx* c, crk_particles* p, cudaStream_t st) {
+    if (!lists_on(c)) {
+        CRK_TRY(corrections(c, p, st));
+        return extras(c, p, st);
+    }
+    CRK_TRY(gather_gas_state(c, p, st));
+    const CorPass gc = cor_pass(c, p);
+    const ExtPass ge = ext_pass(c, p);
+    RowView rv = hydro_rows(c);
+    const ListView lv = list_view(c);
+    CRK_TRY(cuda_check(c, (launch_list2<CorPass, ExtPass, HYD_NW, HYD_G, 128, 3>(gc, ge, rv, lv, st)),
+                       "corrections + extras kernel"));
+    c->launches++;
+    rv.rows = lv.frows;
+    rv.nrows = lv.nfrows;
+    CRK_TRY(cuda_check(c, (launch_pairs<CorPass, HYD_NW, HYD_G, 128, 3>(gc, rv, c->nleaf[2], st)), "corrections kernel"));
+    CRK_TRY(cuda_check(c, (launch_pairs<ExtPass, HYD_NW, HYD_G, 128, 3>(ge, rv, c->nleaf[2], st)), "extras kernel"));
+    c->launches += 2;
+    return CRK_OK;
 }
 
 // symmetric accel over the lists (acc_symlist_kernel); if any row is flagged the symmetric

@@ -482,6 +482,105 @@ __global__ void __launch_bounds__(NW * 32, MINB) list_kernel(const Pass pass, co
     }
 }
 
+// Two list walks per row in one kernel: pass A over i's whole list, A's epilogue, then pass
+// B (whose load_i may read what A's epilogue wrote for the same i: the same warp, ordered by
+// __syncwarp).  The staged rows carry B's payload; a row that fits one round is staged once
+// for both walks, longer rows are staged again for B.  Used to fuse Corrections and Extras:
+// Extras needs only i's own coefficients, which Corrections has just produced.
+template <class PA, class PB, int NW, int G, int ENT, int MINB>
+__global__ void __launch_bounds__(NW * 32, MINB) list_kernel2(const PA pa, const PB pb, const RowView rv,
+                                                              const ListView lv) {
+    static_assert(32 % G == 0, "G must divide the warp");
+    static_assert(PA::PAY == 0, "pass A reads positions only");
+    constexpr int S = 32 / G;
+    using SM = ListSmem<PB::PAY, ENT>;
+    extern __shared__ __align__(128) unsigned char smem_raw[];
+    SM& sm = *reinterpret_cast<SM*>(smem_raw);
+    const int a = blockIdx.x;
+    if (lv.lflag[a]) return;
+    const int warp = threadIdx.x >> 5;
+    const int lane = threadIdx.x & 31;
+    const int il = lane / S;
+    const int sl = lane % S;
+    const int ibase = warp * G;
+    if (threadIdx.x == 0) {
+        mbar_init(&sm.bar, 1);
+        mbar_fence_init();
+    }
+    uint32_t phase = 0;
+    const int ifirst = rv.ifirst[a];
+    const int icount = rv.icount[a];
+    const bool wactive = ibase < icount;
+    const bool ivalid = ibase + il < icount;
+    const int rbeg = rv.row_off[a], rend = rv.row_off[a + 1];
+    const int ki = ifirst + ibase + (ivalid ? il : 0);
+    const int nl = (wactive && ivalid) ? lv.ncnt[ki] : 0;
+    const uint16_t* const lbeg = lv.nbr + (int64_t)ki * lv.cap;
+    const bool one_round = rend - rbeg <= ENT;
+
+    // walk this lane's entries of round [e0, e0 + nent) with pass P
+    auto walk = [&](const auto& P, auto& is, auto& acc, const uint16_t*& lp, int& tn, int e0, int nent) {
+        const int rs = (e0 - rbeg) * JMAX, re = rs + nent * JMAX;
+        const uint16_t* const lend = lbeg + nl;
+#pragma unroll 1
+        while (__any_sync(0xffffffffu, tn < re)) {
+            if (tn < re) {
+                const int tl = tn - rs;
+                const float4 jp = sm.raw[tl];
+                lp += S;
+                tn = lp < lend ? (int)*lp : 0x7fffffff;
+                P.pair(is, acc, jp, sm.pay + tl * PB::PAY, __float_as_int(sm.eoff[tl / JMAX].w) + tl % JMAX);
+            }
+        }
+    };
+    {  // pass A
+        typename PA::I is;
+        typename PA::Acc acc;
+        pa.init(acc);
+        if (wactive) pa.load_i(ki, is);
+        const uint16_t* lp = lbeg + sl;
+        int tn = lp < lbeg + nl ? (int)*lp : 0x7fffffff;
+        for (int e0 = rbeg; e0 < rend; e0 += ENT) {
+            const int nent = min(ENT, rend - e0);
+            stage_list_round<PB::PAY, NW, ENT>(sm, rv, pb.jrows, pb.jpay, e0, nent, phase);
+            if (wactive) walk(pa, is, acc, lp, tn, e0, nent);
+        }
+        if (wactive) {
+            pa.template reduce<-S>(acc);
+            if (ivalid && sl == 0) pa.finish(ki, is, acc);
+        }
+    }
+    __syncwarp();
+    {  // pass B
+        typename PB::I is;
+        typename PB::Acc acc;
+        pb.init(acc);
+        if (wactive) pb.load_i(ki, is);
+        const uint16_t* lp = lbeg + sl;
+        int tn = lp < lbeg + nl ? (int)*lp : 0x7fffffff;
+        for (int e0 = rbeg; e0 < rend; e0 += ENT) {
+            const int nent = min(ENT, rend - e0);
+            if (!one_round) stage_list_round<PB::PAY, NW, ENT>(sm, rv, pb.jrows, pb.jpay, e0, nent, phase);
+            if (wactive) walk(pb, is, acc, lp, tn, e0, nent);
+        }
+        if (wactive) {
+            pb.template reduce<-S>(acc);
+            if (ivalid && sl == 0) pb.finish(ki, is, acc);
+        }
+    }
+}
+
+template <class PA, class PB, int NW, int G, int ENT, int MINB>
+inline cudaError_t launch_list2(const PA& pa, const PB& pb, const RowView& rv, const ListView& lv, cudaStream_t st) {
+    const int smem = (int)sizeof(ListSmem<PB::PAY, ENT>);
+    auto k = list_kernel2<PA, PB, NW, G, ENT, MINB>;
+    cudaError_t e = cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+    if (e != cudaSuccess) return e;
+    if (lv.nrows <= 0) return cudaSuccess;
+    k<<<lv.nrows, NW * 32, smem, st>>>(pa, pb, rv, lv);
+    return cudaGetLastError();
+}
+
 // persistent grid for a list-driven kernel: as many CTAs as fit, each claiming rows
 template <class K>
 inline int persistent_grid(K kernel, int threads, int smem, int64_t nrows) {

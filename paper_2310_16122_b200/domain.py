@@ -224,8 +224,7 @@ class DomainRank:
             self.solver.unpack_gas(0, idx, buf, self.stream)
 
     def corrections_extras(self):
-        self.solver.corrections(self.p, self.stream)
-        self.solver.extras(self.p, self.stream)
+        self.solver.corrections_extras(self.p, self.stream)
 
     def r3_pack(self) -> dict:
         return {s: self.solver.pack_gas(1, send, self.stream) for s, (send, _) in self._gas_lists().items()

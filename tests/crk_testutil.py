@@ -19,7 +19,7 @@ FIELDS_SCALAR = ["ax", "ay", "az", "V", "A", "rho", "P", "cs", "ahx", "ahy", "ah
 FIELDS_PLANES = {"B": 3, "dA": 3, "dB": 9, "dv": 9}
 
 
-def run_gpu(parts, params, dt_grav=0.0, dt_hydro=0.0, counts=True, lists=False, hydro=True):
+def run_gpu(parts, params, dt_grav=0.0, dt_hydro=0.0, counts=True, lists=False, hydro=True, fused=True):
     """One substep through the C-ABI; outputs mapped back to INPUT order."""
     import torch
     from paper_2310_16122_b200 import Particles, Solver
@@ -27,7 +27,7 @@ def run_gpu(parts, params, dt_grav=0.0, dt_hydro=0.0, counts=True, lists=False, 
     dev = torch.device("cuda", 0)
     p = Particles.from_host(parts, dev)
     s = Solver(params, 0)
-    s.substep(p, dt_grav, dt_hydro, hydro=hydro)
+    s.substep(p, dt_grav, dt_hydro, hydro=hydro, fused=fused)
     res = {}
     if counts:
         cg, ch, cs = s.count_pairs(p)

@@ -313,15 +313,16 @@ def test_clustered_config3_full_chain_sampled_symmetric_modes():
         assert norm_err(gi["dudt"][T], ref["dudt"], ref["Sdu"]) <= TOL_FORCE
 
 
+@pytest.mark.parametrize("fused", [True, False])
 @pytest.mark.parametrize("cap", [0, 16, 70, 128])
-def test_neighbour_list_capacities(cap, monkeypatch):
+def test_neighbour_list_capacities(cap, fused, monkeypatch):
     """The gas passes read the neighbour lists built by geometry; rows whose lists overflow
     the per-particle capacity run the on-the-fly kernels.  cap 0: lists off; 16: every row
     overflows; 70: a mix (sym counts ~64-80 on c2z); 128: no overflow."""
     monkeypatch.setenv("CRK_NBR_CAP", str(cap))
     parts, params = cached_config("c2z")
     params["symmetric"] = 1
-    g = run_gpu(parts, params, counts=False)
+    g = run_gpu(parts, params, counts=False, fused=fused)
     ref = oracle.substep(parts, params)
     gi = g["in"]
     T = ref["targets"]

@@ -15,7 +15,7 @@ ap.add_argument("--steps", type=int, default=5)
 ap.add_argument("variants", nargs="*", default=[""])
 a = ap.parse_args()
 parts, params = make_config(a.config)
-passes = ["build_lists", "gravity_kick", "geometry", "corrections", "extras", "hydro_accel_dudt"]
+passes = ["build_lists", "gravity_kick", "geometry", "corrections_extras", "hydro_accel_dudt"]
 for var in a.variants:
     for kv in var.split():
         k, v = kv.split("=", 1)
@@ -29,7 +29,7 @@ for var in a.variants:
         for k in passes:
             if it >= 2:
                 ev[k][it - 2][0].record(st)
-            getattr(s, k)(p, stream=st) if k in ("build_lists", "geometry", "corrections", "extras") else getattr(s, k)(p, 0.0, st)
+            getattr(s, k)(p, stream=st) if k in ("build_lists", "geometry", "corrections_extras") else getattr(s, k)(p, 0.0, st)
             if it >= 2:
                 ev[k][it - 2][1].record(st)
     torch.cuda.synchronize()
