@@ -122,7 +122,12 @@ class Particles:
     IN_F32 = ("x", "y", "z", "vx", "vy", "vz", "m", "H", "u")
     OUT1 = ("ax", "ay", "az", "V", "A", "rho", "P", "cs", "ahx", "ahy", "ahz", "dudt")
 
-    def __init__(self, n: int, device, outputs: bool = True):
+    FORCES = ("ax", "ay", "az", "ahx", "ahy", "ahz", "dudt")
+
+    def __init__(self, n: int, device, outputs=True):
+        """outputs: True / "all" = every per-particle output incl. the CRK intermediates (V, A,
+        B, grad A, grad B, rho, P, c, grad v); "forces" = only the substep's results (gravity
+        and hydro accelerations, du/dt; the library skips the intermediate copies); False = none."""
         self.n = int(n)
         self.device = torch.device(device)
         z = lambda *s, dt=torch.float32: torch.zeros(*s, dtype=dt, device=self.device)  # noqa: E731
@@ -132,7 +137,10 @@ class Particles:
         self.id = z(self.n, dt=torch.int64)
         self.perm = z(self.n, dt=torch.int32)
         self.outputs = outputs
-        if outputs:
+        if outputs == "forces":
+            for k in self.FORCES:
+                setattr(self, k, z(self.n))
+        elif outputs:
             for k in self.OUT1:
                 setattr(self, k, z(self.n))
             self.B = z(3, self.n)

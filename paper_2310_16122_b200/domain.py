@@ -150,7 +150,8 @@ class DomainRank:
     """One rank's share of a decomposed substep, in phases (so that ranks can also be
     emulated in one process on one device)."""
 
-    def __init__(self, decomp: Decomposition, r: int, own: dict, device, stream=None):
+    def __init__(self, decomp: Decomposition, r: int, own: dict, device, stream=None, outputs=True):
+        self.outputs = outputs  # Particles outputs of the local set ("forces": results only)
         self.d, self.r, self.device = decomp, r, torch.device(device)
         self.params = decomp.rank_params(r)
         self.own_host = own
@@ -183,7 +184,7 @@ class DomainRank:
     def r1_unpack_and_build(self, recv: dict):
         n_ghost = sum(int(t.shape[0]) for t in recv.values())
         self.n_total = self.n_own + n_ghost
-        p = Particles(self.n_total, self.device)
+        p = Particles(self.n_total, self.device, self.outputs)
         for k in Particles.IN_F32 + ("species", "id"):
             getattr(p, k)[: self.n_own].copy_(getattr(self.own, k))
         off = self.n_own
