@@ -27,6 +27,9 @@ sys.path.insert(0, ROOT)
 # canonical flop per ordered pair (FMA = 2, MUFU = 1, compare/select = 0)
 FLOP_PER_PAIR = {"gravity": 30, "geometry": 22, "corrections_extras": 114 + 103, "accel_dudt": 256}
 PASSES = ["build_lists", "gravity", "geometry", "corrections_extras", "accel_dudt"]
+# the kernel that dominates each pass (profiles/r01/ncu_traffic.json is matched against it)
+_DOM_KERNEL = {"gravity": "crk::grav_pipe_kernel", "geometry": "void crk::pair_kernel<crk::GeoPass",
+               "corrections_extras": "void crk::list_kernel2<crk::CorPass", "accel_dudt": "void crk::list_kernel<crk::AccPass"}
 METRIC = "pair interactions/s & short-range substep time at 1/2/4/8 B200; % FP32 peak"
 
 
@@ -399,7 +402,7 @@ def main():
     try:  # dram bytes per launch of the same kernel from the committed ncu --set full capture
         with open(os.path.join(ROOT, "profiles", "r01", "ncu_traffic.json")) as f:
             tk = json.load(f)["kernels"].get(dom)
-        if tk and args.config == "c4":
+        if tk and args.config == "c4" and tk["kernel"].startswith(_DOM_KERNEL.get(dom, "?")):
             traffic = tk["dram_bytes"]
     except Exception:
         pass
