@@ -124,7 +124,11 @@ crk_status crk_build_lists(struct crk_ctx* ctx, crk_particles* parts, void* stre
  * writes ax/ay/az and kicks v += dt a (dt = 0: forces only). */
 crk_status crk_gravity_kick(struct crk_ctx* ctx, crk_particles* parts, float dt, void* stream);
 
-/* a4 Geometry (upGeo): V_i = 1 / sum_{gas j, s32 < H_i^2, incl. i} W(r_ij, H_i) (O6). */
+/* a4 Geometry (upGeo): V_i = 1 / sum_{gas j, s32 < H_i^2, incl. i} W(r_ij, H_i) (O6).
+ * Also builds the gas neighbour lists read by the later hydro passes.  Independent of
+ * crk_gravity_kick: after crk_build_lists the two may be issued on two different streams
+ * (the caller joins them before crk_corrections / crk_corrections_extras, which read the
+ * gravity-kicked v); every other call of one ctx must be ordered on one stream. */
 crk_status crk_geometry(struct crk_ctx* ctx, crk_particles* parts, void* stream);
 
 /* a5 Corrections (upCor): A, B, grad A, grad B from the moments m0, m1, m2 and their

@@ -249,12 +249,22 @@ class Solver:
     def hydro_accel_dudt(self, parts, dt=0.0, stream=None):
         self._call(lib().crk_hydro_accel_dudt, parts, C.c_float(dt), stream=stream)
 
-    def substep(self, parts, dt_grav=0.0, dt_hydro=0.0, stream=None, hydro=True, fused=True):
-        """The whole short-range substep: a1-a8 in call order."""
+    def substep(self, parts, dt_grav=0.0, dt_hydro=0.0, stream=None, hydro=True, fused=True, side_stream=None):
+        """The whole short-range substep: a1-a8 in call order.  With
+        `side_stream`, gravity (a3) runs there concurrently with geometry (a4) and is joined
+        before corrections/extras (which read the kicked v)."""
         self.build_lists(parts, stream)
-        self.gravity_kick(parts, dt_grav, stream)
+        if side_stream is not None and hydro:
+            main = stream if stream is not None else torch.cuda.current_stream()
+            side_stream.wait_stream(main)
+            self.gravity_kick(parts, dt_grav, side_stream)
+            self.geometry(parts, main)
+            main.wait_stream(side_stream)
+        else:
+            self.gravity_kick(parts, dt_grav, stream)
+            if hydro:
+                self.geometry(parts, stream)
         if hydro:
-            self.geometry(parts, stream)
             if fused:
                 self.corrections_extras(parts, stream)
             else:

@@ -618,6 +618,15 @@ crk_status build_lists(crk_ctx* c, crk_particles* p, cudaStream_t st) {
     CRK_TRY(grow(c, c->gcoef, ng * 16 * 4, st));
     CRK_TRY(grow(c, c->grec, ng * 9 * 16, st));
     CRK_TRY(grow(c, c->gu, ng * 4, st));
+    // scratch of the later passes sized here, in stream order, so that gravity (a3) and
+    // geometry (a4) may run concurrently on two streams without either reallocating
+    CRK_TRY(grow(c, c->gacc, (n > ng ? n : ng) * 16, st));
+    CRK_TRY(grow(c, c->work, 64, st));
+    if (c->nbr_cap > 0) {
+        CRK_TRY(grow(c, c->nbr, (size_t)ng * c->nbr_cap * sizeof(uint16_t), st));
+        CRK_TRY(grow(c, c->ncnt, (size_t)ng * sizeof(int32_t), st));
+        CRK_TRY(grow(c, c->lflag, (size_t)(2 * c->nleaf[2] + 1) * sizeof(int32_t), st));
+    }
     c->stage = ST_LISTS;
     return CRK_OK;
 }

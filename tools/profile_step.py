@@ -14,7 +14,7 @@ ap.add_argument("--warmup", type=int, default=2)
 ap.add_argument("--steps", type=int, default=1)
 a = ap.parse_args()
 parts, params = make_config(a.config)
-p = Particles.from_host(parts, "cuda")
+p = Particles.from_host(parts, "cuda", outputs="forces")  # as bench.py
 s = Solver(params, 0)
 for _ in range(a.warmup):
     s.substep(p)
