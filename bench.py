@@ -359,6 +359,7 @@ def main():
             ev["geometry"][1].record(stream)
         if side is not None:
             stream.wait_stream(side)
+        if timed:
             ev["corrections_extras"][0].record(stream)
         solver.corrections_extras(p, stream)  # a5 + a6 fused (crk_corrections_extras)
         if timed:

@@ -624,7 +624,7 @@ crk_status build_lists(crk_ctx* c, crk_particles* p, cudaStream_t st) {
     CRK_TRY(grow(c, c->work, 64, st));
     if (c->nbr_cap > 0) {
         CRK_TRY(grow(c, c->nbr, (size_t)ng * c->nbr_cap * sizeof(uint16_t), st));
-        CRK_TRY(grow(c, c->ncnt, (size_t)ng * sizeof(int32_t), st));
+        CRK_TRY(grow(c, c->ncnt, (size_t)ng * sizeof(int32_t) + 64, st));  // + pad: 16-byte-aligned bulk reads
         CRK_TRY(grow(c, c->lflag, (size_t)(2 * c->nleaf[2] + 1) * sizeof(int32_t), st));
     }
     c->stage = ST_LISTS;

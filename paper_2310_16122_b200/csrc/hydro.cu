@@ -831,7 +831,7 @@ crk_status geometry(crk_ctx* c, crk_particles* p, cudaStream_t st) {
         g.cnt = nullptr;
         const int64_t ng = c->n_gas > 0 ? c->n_gas : 1;
         CRK_TRY(grow(c, c->nbr, (size_t)ng * c->nbr_cap * sizeof(uint16_t), st));
-        CRK_TRY(grow(c, c->ncnt, (size_t)ng * sizeof(int32_t), st));
+        CRK_TRY(grow(c, c->ncnt, (size_t)ng * sizeof(int32_t) + 64, st));  // + pad: 16-byte-aligned bulk reads
         // lflag: per-row flags, then the compact flagged-row list, then its length
         const size_t fl = (size_t)(2 * c->nleaf[2] + 1) * sizeof(int32_t);
         CRK_TRY(grow(c, c->lflag, fl, st));
