@@ -132,7 +132,17 @@ struct GravSymArgs {
     float L[3];
     float rcut2, eps2;
     float c0, c1, c2, c3, c4, c5;
+    // domain decomposition (grav_pipe_kernel): a particle is owned iff its cell
+    // (x / q) >> cs lies in [dlo, dhi) on every axis; ghosts have no i-groups here
+    bool partial;
+    float inv_q;
+    int cs, dlo[3], dhi[3];
 };
+
+__device__ __forceinline__ bool grav_owned(const GravSymArgs& A, float x, float y, float z) {
+    const int cx = (int)(x * A.inv_q) >> A.cs, cy = (int)(y * A.inv_q) >> A.cs, cz = (int)(z * A.inv_q) >> A.cs;
+    return cx >= A.dlo[0] && cx < A.dhi[0] && cy >= A.dlo[1] && cy < A.dhi[1] && cz >= A.dlo[2] && cz < A.dhi[2];
+}
 
 // all threads: stage row entries [e0, e0 + nent) of leaf a into buffer rb; every thread
 // arrives once on `bar` with the bytes of the copies it issued (barrier count = CTA size)
@@ -586,6 +596,9 @@ __global__ void __launch_bounds__(symw::NW * 32, 16 / symw::NW) grav_warp_kernel
 }
 
 // ------------------------------------------------------------ pipelined warp-independent variant
+// With domain decomposition (A.partial) a pair with a ghost j is evaluated by i's group
+// whatever j's index (the ghost has no group here) and its reaction is dropped (j's own
+// rank evaluates the pair for j).
 // grav_warp_kernel with the L2 latency taken off the critical path: per warp a two-deep
 // software pipeline of async copies (cp.async, no registers held) — the entry records
 // (shifted leaf box + first/count, written by the list build) of chunk c+2 and the
@@ -676,7 +689,7 @@ __global__ void __launch_bounds__(symp::NW * 32, 16 / symp::NW) grav_pipe_kernel
                 int sx, sy, sz;
                 decode_shift(cc >> 8, sx, sy, sz);
                 off = make_float4((float)sx * A.L[0], (float)sy * A.L[1], (float)sz * A.L[2], bl.w);
-                if (first + cnt > gself) {  // entries wholly below this group own no pair
+                if (A.partial || first + cnt > gself) {  // entries wholly below this group own no pair
                     const float gx = fmaxf(fmaxf(bl.x - hi[0], lo[0] - bh.x), 0.f);
                     const float gy = fmaxf(fmaxf(bl.y - hi[1], lo[1] - bh.y), 0.f);
                     const float gz = fmaxf(fmaxf(bl.z - hi[2], lo[2] - bh.z), 0.f);
@@ -748,7 +761,7 @@ __global__ void __launch_bounds__(symp::NW * 32, 16 / symp::NW) grav_pipe_kernel
                 by = __ffma2_rn(wj, dy, by);
                 bz = __ffma2_rn(wj, dz, bz);
             }
-            if (lane < n) red_add_v4(A.acc + j, -(bx.x + bx.y), -(by.x + by.y), -(bz.x + bz.y), 0.f);
+            if (lane < n && j >= 0) red_add_v4(A.acc + j, -(bx.x + bx.y), -(by.x + by.y), -(bz.x + bz.y), 0.f);
         };
 
         int wr = 0, rd = 0;
@@ -767,10 +780,12 @@ __global__ void __launch_bounds__(symp::NW * 32, 16 / symp::NW) grav_pipe_kernel
                 const int qc = q < ns ? q : 0;
                 const int cnt = S.wcnt[b][qc];
                 const float4 o = S.woff[b][qc];
-                const int j = __float_as_int(o.w) + kk;
+                int j = __float_as_int(o.w) + kk;
                 float4 p = S.pp[b][qc * JMAX + kk];
+                bool keep = q < ns && kk < cnt;
+                if (A.partial && keep && !grav_owned(A, p.x, p.y, p.z)) j = -1 - j;  // ghost: no reaction
                 p.x += o.x; p.y += o.y; p.z += o.z;  // exact (O1)
-                bool keep = q < ns && kk < cnt && j >= gself;
+                keep = keep && (j >= gself || j < 0);
                 if (keep) keep = box_dist2(p.x, p.y, p.z, lo, hi) < wcut;
                 const unsigned msk = __ballot_sync(0xffffffffu, keep);
                 if (keep) {
@@ -881,6 +896,13 @@ static cudaError_t launch_grav_sym(crk_ctx* c, GravSymArgs& A, cudaStream_t st) 
     return cudaGetLastError();
 }
 
+// CRK_GRAV_VARIANT: 0 pipelined warp-independent kernel (default; the only one with domain
+// decomposition support), 6 unpipelined, 1-5 and 7 CTA-staged (experiments)
+static int grav_variant() {
+    const char* gv = getenv("CRK_GRAV_VARIANT");
+    return gv ? atoi(gv) : 0;
+}
+
 static crk_status gravity_sym(crk_ctx* c, crk_particles* p, float dt, cudaStream_t st) {
     const int64_t n = c->n;
     CRK_TRY(grow(c, c->gacc, n * 16, st));
@@ -900,8 +922,11 @@ static crk_status gravity_sym(crk_ctx* c, crk_particles* p, float dt, cudaStream
         A.eps2 = c->prm.eps2;
         A.c0 = c->prm.poly[0]; A.c1 = c->prm.poly[1]; A.c2 = c->prm.poly[2];
         A.c3 = c->prm.poly[3]; A.c4 = c->prm.poly[4]; A.c5 = c->prm.poly[5];
-        const char* gv = getenv("CRK_GRAV_VARIANT");
-        const int var = gv ? atoi(gv) : 0;  // 0: pipelined warp-independent kernel; 6: unpipelined; 1-5, 7: CTA-staged
+        A.partial = c->lay.partial;
+        A.inv_q = c->lay.inv_q;
+        A.cs = c->lay.cs;
+        for (int d = 0; d < 3; ++d) { A.dlo[d] = c->lay.dlo[d]; A.dhi[d] = c->lay.dhi[d]; }
+        const int var = grav_variant();
         CRK_TRY(grow(c, c->work, 64, st));
         CRK_TRY(cuda_check(c, cudaMemsetAsync(c->work.p, 0, 16, st), "memset"));
         A.work = P<int>(c->work);
@@ -949,7 +974,7 @@ static crk_status gravity_sym(crk_ctx* c, crk_particles* p, float dt, cudaStream
 
 crk_status gravity_kick(crk_ctx* c, crk_particles* p, float dt, cudaStream_t st) {
     if (dt != 0.f && (!p->vx || !p->vy || !p->vz)) return fail(c, CRK_EINVAL, "kick needs vx, vy, vz");
-    if ((c->prm.symmetric & 1) && !c->lay.partial) return gravity_sym(c, p, dt, st);
+    if ((c->prm.symmetric & 1) && (!c->lay.partial || grav_variant() == 0)) return gravity_sym(c, p, dt, st);
     return launch_grav<false>(c, p, dt, nullptr, st);
 }
 

@@ -90,8 +90,12 @@ def test_exchange_plumbing_gloo_two_ranks():
 
 
 @pytest.mark.gpu
-@pytest.mark.parametrize("name,P", [("c1", 2), ("c2z", 2), ("c2z", 4), ("c2z", 8)])
-def test_decomposed_substep_matches_single_domain_oracle(name, P):
+@pytest.mark.parametrize("name,P,gvar", [("c1", 2, "0"), ("c2z", 2, "0"), ("c2z", 4, "0"), ("c2z", 8, "0"),
+                                         ("c2z", 8, "7")])
+def test_decomposed_substep_matches_single_domain_oracle(name, P, gvar, monkeypatch):
+    """gvar 0: Newton-3 pipelined gravity with ghost pairs (reactions dropped); 7: the
+    i-centric gravity kernel the other variants fall back to under decomposition."""
+    monkeypatch.setenv("CRK_GRAV_VARIANT", gvar)
     import torch
     import oracle
     from paper_2310_16122_b200.domain import DomainRank, substep_inprocess
