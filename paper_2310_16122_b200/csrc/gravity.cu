@@ -617,6 +617,7 @@ struct WarpSm {
 };
 }  // namespace symp
 
+template <bool PARTIAL>
 __global__ void __launch_bounds__(symp::NW * 32, 16 / symp::NW) grav_pipe_kernel(const GravSymArgs A) {
     using namespace symp;
     extern __shared__ __align__(128) unsigned char smem_raw[];
@@ -689,7 +690,7 @@ __global__ void __launch_bounds__(symp::NW * 32, 16 / symp::NW) grav_pipe_kernel
                 int sx, sy, sz;
                 decode_shift(cc >> 8, sx, sy, sz);
                 off = make_float4((float)sx * A.L[0], (float)sy * A.L[1], (float)sz * A.L[2], bl.w);
-                if (A.partial || first + cnt > gself) {  // entries wholly below this group own no pair
+                if (PARTIAL || first + cnt > gself) {  // entries wholly below this group own no pair
                     const float gx = fmaxf(fmaxf(bl.x - hi[0], lo[0] - bh.x), 0.f);
                     const float gy = fmaxf(fmaxf(bl.y - hi[1], lo[1] - bh.y), 0.f);
                     const float gz = fmaxf(fmaxf(bl.z - hi[2], lo[2] - bh.z), 0.f);
@@ -761,7 +762,7 @@ __global__ void __launch_bounds__(symp::NW * 32, 16 / symp::NW) grav_pipe_kernel
                 by = __ffma2_rn(wj, dy, by);
                 bz = __ffma2_rn(wj, dz, bz);
             }
-            if (lane < n && j >= 0) red_add_v4(A.acc + j, -(bx.x + bx.y), -(by.x + by.y), -(bz.x + bz.y), 0.f);
+            if (lane < n && (!PARTIAL || j >= 0)) red_add_v4(A.acc + j, -(bx.x + bx.y), -(by.x + by.y), -(bz.x + bz.y), 0.f);
         };
 
         int wr = 0, rd = 0;
@@ -783,9 +784,9 @@ __global__ void __launch_bounds__(symp::NW * 32, 16 / symp::NW) grav_pipe_kernel
                 int j = __float_as_int(o.w) + kk;
                 float4 p = S.pp[b][qc * JMAX + kk];
                 bool keep = q < ns && kk < cnt;
-                if (A.partial && keep && !grav_owned(A, p.x, p.y, p.z)) j = -1 - j;  // ghost: no reaction
+                if (PARTIAL && keep && !grav_owned(A, p.x, p.y, p.z)) j = -1 - j;  // ghost: no reaction
                 p.x += o.x; p.y += o.y; p.z += o.z;  // exact (O1)
-                keep = keep && (j >= gself || j < 0);
+                keep = keep && (j >= gself || (PARTIAL && j < 0));
                 if (keep) keep = box_dist2(p.x, p.y, p.z, lo, hi) < wcut;
                 const unsigned msk = __ballot_sync(0xffffffffu, keep);
                 if (keep) {
@@ -955,9 +956,10 @@ static crk_status gravity_sym(crk_ctx* c, crk_particles* p, float dt, cudaStream
             int nsm = 0;
             cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, c->device);
             const int smem = (int)sizeof(symp::WarpSm) * symp::NW;
-            e = cudaFuncSetAttribute(grav_pipe_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+            auto k = A.partial ? grav_pipe_kernel<true> : grav_pipe_kernel<false>;
+            e = cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
             if (e == cudaSuccess) {
-                grav_pipe_kernel<<<nsm * (16 / symp::NW), symp::NW * 32, smem, st>>>(A);
+                k<<<nsm * (16 / symp::NW), symp::NW * 32, smem, st>>>(A);
                 e = cudaGetLastError();
             }
             break;
