@@ -325,7 +325,9 @@ def main():
     from paper_2310_16122_b200 import Particles, Solver
 
     dev = torch.device("cuda", local)
-    stream = torch.cuda.current_stream(dev)
+    # a created (non-legacy-default) stream: the legacy default stream would serialise with
+    # the e2e copy streams
+    stream = torch.cuda.Stream(dev)
     cnts = _counts_input_order(parts, params)
     pairs = {"gravity": int(cnts[0].sum()), "gather": int(cnts[1].sum()), "sym": int(cnts[2].sum())}
     pair_int = pairs["gravity"] + 3 * pairs["gather"] + pairs["sym"]
@@ -333,6 +335,7 @@ def main():
     # the substep's results (gravity + hydro accelerations, du/dt); the CRK intermediates stay in
     # the library's scratch (the parity tests request and check them)
     p = Particles.from_host(parts, dev, outputs="forces")
+    torch.cuda.synchronize()
     solver = Solver(params, local)
     ev = {k: (torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)) for k in PASSES}
     side = torch.cuda.Stream(dev) if args.overlap else None

@@ -31,6 +31,22 @@ crk_status cuda_check(crk_ctx* c, cudaError_t e, const char* what) {
     return e == cudaErrorMemoryAllocation ? CRK_ENOMEM : CRK_ECUDA;
 }
 
+__global__ void k_readback(Readback r, char* dst) {
+    for (int i = 0; i < r.n; ++i) {
+        if (r.bytes[i] == 8)
+            *reinterpret_cast<volatile int64_t*>(dst + r.dst[i]) = *reinterpret_cast<const int64_t*>(r.src[i]);
+        else
+            *reinterpret_cast<volatile int32_t*>(dst + r.dst[i]) = *reinterpret_cast<const int32_t*>(r.src[i]);
+    }
+    __threadfence_system();
+}
+
+crk_status readback(crk_ctx* c, const Readback& r, cudaStream_t st) {
+    k_readback<<<1, 1, 0, st>>>(r, static_cast<char*>(c->pinned_dev));
+    CRK_LAUNCHED(c, "readback");
+    return CRK_OK;
+}
+
 crk_status grow(crk_ctx* c, Buf& b, size_t bytes, cudaStream_t st) {
     if (bytes <= b.cap) return CRK_OK;
     if (b.p) {
@@ -120,13 +136,18 @@ crk_status crk_create(const crk_params* params, int device, crk_ctx** out) {
     c->device = device;
     c->lay = L;
     void* h = nullptr;
-    e = cudaMallocHost(&h, 256);
+    e = cudaHostAlloc(&h, 256, cudaHostAllocMapped);
     if (e != cudaSuccess) {
         delete c;
         return CRK_ENOMEM;
     }
     c->pinned.p = h;
     c->pinned.cap = 256;
+    if (cudaHostGetDevicePointer(&c->pinned_dev, h, 0) != cudaSuccess) {
+        cudaFreeHost(h);
+        delete c;
+        return CRK_ECUDA;
+    }
     // gas neighbour-list capacity per particle (CRK_NBR_CAP: tests force overflow / 0 = off)
     const char* nc = getenv("CRK_NBR_CAP");
     c->nbr_cap = nc ? atoi(nc) : 128;

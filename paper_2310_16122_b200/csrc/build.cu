@@ -543,10 +543,13 @@ crk_status build_lists(crk_ctx* c, crk_particles* p, cudaStream_t st) {
         c->launches += 2;
     }
     // totals: leaf counts (4) + n_gas, one synchronisation
-    int32_t* host = P<int32_t>(c->pinned);
-    for (int s = 0; s < 4; ++s)
-        CRK_TRY(cuda_check(c, cudaMemcpyAsync(host + s, cnt + s * (L.ncm + 1) + L.ncm, 4, cudaMemcpyDeviceToHost, st), "d2h"));
-    CRK_TRY(cuda_check(c, cudaMemcpyAsync(host + 4, P<int32_t>(c->grank) + n, 4, cudaMemcpyDeviceToHost, st), "d2h"));
+    volatile int32_t* host = P<int32_t>(c->pinned);
+    {
+        Readback rb;
+        for (int s = 0; s < 4; ++s) rb.add(cnt + s * (L.ncm + 1) + L.ncm, 4 * s, 4);
+        rb.add(P<int32_t>(c->grank) + n, 16, 4);
+        CRK_TRY(readback(c, rb, st));
+    }
     CRK_TRY(cuda_check(c, cudaStreamSynchronize(st), "sync"));
     for (int s = 0; s < 4; ++s) c->nleaf[s] = host[s];
     c->n_gas = host[4];
@@ -579,6 +582,7 @@ crk_status build_lists(crk_ctx* c, crk_particles* p, cudaStream_t st) {
     }
 
     // ---- lists: count, scan, fill
+    Readback rbl;
     for (int m = 0; m < 2; ++m) {
         const int64_t na = c->nleaf[m == 0 ? 0 : 2];
         CRK_TRY(grow(c, c->rowlen[m], (na + 1) * 4, st));
@@ -593,8 +597,9 @@ crk_status build_lists(crk_ctx* c, crk_particles* p, cudaStream_t st) {
         CRK_TRY(cuda_check(c, cub::DeviceScan::ExclusiveSum(c->cub_tmp.p, tmp, P<int32_t>(c->rowlen[m]),
                                                             P<int32_t>(c->rowoff[m]), (int)(na + 1), st), "row scan"));
         c->launches += 2;
-        CRK_TRY(cuda_check(c, cudaMemcpyAsync(host + 8 + m, P<int32_t>(c->rowoff[m]) + na, 4, cudaMemcpyDeviceToHost, st), "d2h"));
+        rbl.add(P<int32_t>(c->rowoff[m]) + na, 4 * (8 + m), 4);
     }
+    CRK_TRY(readback(c, rbl, st));
     CRK_TRY(cuda_check(c, cudaStreamSynchronize(st), "sync"));
     for (int m = 0; m < 2; ++m) {
         c->nent[m] = host[8 + m];

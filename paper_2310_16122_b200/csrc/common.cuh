@@ -29,6 +29,20 @@ crk_status grow(crk_ctx* c, Buf& b, size_t bytes, cudaStream_t st);
 template <class T>
 inline T* P(const Buf& b) { return reinterpret_cast<T*>(b.p); }
 
+// Small device -> host readbacks (list sizes, counts) through the ctx's mapped pinned
+// buffer, written by a one-thread kernel: a cudaMemcpyAsync D2H would queue on the copy
+// engine behind the caller's bulk transfers on other streams (e.g. the previous step's
+// results going down), stalling the build behind them.  `dst` are byte offsets into the
+// pinned buffer; sizes are 4 or 8 bytes.
+struct Readback {
+    const void* src[8];
+    int dst[8];
+    int bytes[8];
+    int n = 0;
+    void add(const void* s, int off, int b) { src[n] = s; dst[n] = off; bytes[n] = b; ++n; }
+};
+crk_status readback(crk_ctx* c, const Readback& r, cudaStream_t st);
+
 // ---------------------------------------------------------------- Morton
 __host__ __device__ inline uint64_t spread3(uint64_t v) {  // 21 bits -> every 3rd bit
     v &= 0x1fffffull;

@@ -78,7 +78,8 @@ struct crk_ctx {
     crk::Buf grec;               // accel records: 9 float4 per gas particle
     crk::Buf gu;                 // float
     crk::Buf gacc;               // float4 force accumulator (symmetric kernels)
-    crk::Buf pinned;             // host pinned totals
+    crk::Buf pinned;             // host pinned totals (mapped: written by k_readback, no copy engine)
+    void* pinned_dev = nullptr;  // device alias of `pinned`
     crk::Buf sel_flag, sel_mask; // selection scratch
     crk::Buf work;               // dynamic work counters of the persistent kernels
     // gas neighbour lists (geometry -> corrections, extras, accel): pairs.cuh ListView

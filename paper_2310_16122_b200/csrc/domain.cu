@@ -131,8 +131,10 @@ static crk_status compact(crk_ctx* c, int64_t n, int32_t* idx_out, int64_t* coun
     CRK_TRY(cuda_check(c, cub::DeviceSelect::Flagged(c->cub_tmp.p, tmp, it, P<uint8_t>(c->sel_flag), idx_out, dnum,
                                                      (int)n, st), "select"));
     c->launches += 2;
-    int64_t* host = reinterpret_cast<int64_t*>(P<char>(c->pinned) + 128);
-    CRK_TRY(cuda_check(c, cudaMemcpyAsync(host, dnum, 8, cudaMemcpyDeviceToHost, st), "d2h"));
+    volatile int64_t* host = reinterpret_cast<int64_t*>(P<char>(c->pinned) + 128);
+    Readback rb;
+    rb.add(dnum, 128, 8);
+    CRK_TRY(readback(c, rb, st));
     CRK_TRY(cuda_check(c, cudaStreamSynchronize(st), "sync"));
     *count_out = *host;
     return CRK_OK;
