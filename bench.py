@@ -168,7 +168,8 @@ def _config(args, parts):
                         "periodic box, one gravity + CRK-SPH short-range substep",
             "particles_per_gpu": n, "l2": "inputs (>1.5 GB) larger than L2", "seq_len": None,
             "outputs": "a_grav, a_hydro, du/dt per particle (CRK intermediates computed, not copied out)",
-            "streams": "gravity (a3) || geometry (a4) on two streams" if getattr(args, "overlap", False) else "one"}
+            "streams": "gravity (a3) || geometry (a4) on two streams" if getattr(args, "overlap", False) else "one",
+            "order": "SoA sorted in place: timed steps see the previous step's order (e2e: random order each step)"}
 
 
 _COUNT_CACHE = {}

@@ -41,6 +41,30 @@ __global__ void k_readback(Readback r, char* dst) {
     __threadfence_system();
 }
 
+__global__ void k_zero(uint4* p16, size_t n16, char* tail, int ntail) {
+    const size_t i = blockIdx.x * (size_t)blockDim.x + threadIdx.x;
+    const size_t stride = (size_t)gridDim.x * blockDim.x;
+    for (size_t k = i; k < n16; k += stride) p16[k] = make_uint4(0u, 0u, 0u, 0u);
+    if (i < (size_t)ntail) tail[i] = 0;
+}
+
+cudaError_t zero_async(void* p, size_t bytes, cudaStream_t st) {
+    if (bytes == 0) return cudaSuccess;
+    char* b = static_cast<char*>(p);
+    const size_t head = (16 - (reinterpret_cast<uintptr_t>(b) & 15)) & 15;  // unaligned prefix bytes
+    const size_t pre = head < bytes ? head : bytes;
+    const size_t n16 = (bytes - pre) / 16;
+    const size_t rest = bytes - pre - 16 * n16;
+    // prefix and suffix (< 16 bytes each) by a second tiny launch
+    if (pre) k_zero<<<1, 32, 0, st>>>(nullptr, 0, b, (int)pre);
+    if (n16 || rest) {
+        const size_t blocks = n16 ? (n16 + 255) / 256 : 1;
+        k_zero<<<(unsigned)(blocks < 4096 ? blocks : 4096), 256, 0, st>>>(reinterpret_cast<uint4*>(b + pre), n16,
+                                                                        b + pre + 16 * n16, (int)rest);
+    }
+    return cudaGetLastError();
+}
+
 crk_status readback(crk_ctx* c, const Readback& r, cudaStream_t st) {
     k_readback<<<1, 1, 0, st>>>(r, static_cast<char*>(c->pinned_dev));
     CRK_LAUNCHED(c, "readback");
@@ -249,9 +273,9 @@ crk_status crk_count_pairs(crk_ctx* c, crk_particles* p, int32_t* cgrav, int32_t
     CRK_TRY(check_parts(c, p, true));
     if (!cgrav || !cgather || !csym) return fail(c, CRK_EINVAL, "null count array");
     cudaStream_t st = (cudaStream_t)stream;
-    CRK_TRY(cuda_check(c, cudaMemsetAsync(cgrav, 0, p->n * 4, st), "memset"));
-    CRK_TRY(cuda_check(c, cudaMemsetAsync(cgather, 0, p->n * 4, st), "memset"));
-    CRK_TRY(cuda_check(c, cudaMemsetAsync(csym, 0, p->n * 4, st), "memset"));
+    CRK_TRY(cuda_check(c, zero_async(cgrav, p->n * 4, st), "memset"));
+    CRK_TRY(cuda_check(c, zero_async(cgather, p->n * 4, st), "memset"));
+    CRK_TRY(cuda_check(c, zero_async(csym, p->n * 4, st), "memset"));
     CRK_TRY(gravity_count(c, p, cgrav, st));
     return hydro_count(c, cgather, csym, st);
 }

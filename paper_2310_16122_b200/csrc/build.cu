@@ -54,6 +54,11 @@ struct SoA {
     int64_t* id;
 };
 
+__global__ void k_copy_i32(int64_t n, const int32_t* __restrict__ src, int32_t* __restrict__ dst) {
+    const int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+    if (i < n) dst[i] = src[i];
+}
+
 __global__ void k_gather_all(int64_t n, const int32_t* __restrict__ perm, SoA in, SoA out) {
     const int64_t k = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
     if (k >= n) return;
@@ -508,12 +513,14 @@ crk_status build_lists(crk_ctx* c, crk_particles* p, cudaStream_t st) {
     tmpS.sp = reinterpret_cast<uint8_t*>(sbase + n * 44);
     k_gather_all<<<nblk(n, 256), 256, 0, st>>>(n, perm, in, tmpS);
     CRK_LAUNCHED(c, "permute gather");
-    if (p->perm)
-        CRK_TRY(cuda_check(c, cudaMemcpyAsync(p->perm, perm, n * 4, cudaMemcpyDeviceToDevice, st), "copy"));
-    CRK_TRY(cuda_check(c, cudaMemsetAsync(c->cell_start.p, 0, L.ncm * 4, st), "memset"));
-    CRK_TRY(cuda_check(c, cudaMemsetAsync(c->cell_end.p, 0, L.ncm * 4, st), "memset"));
-    CRK_TRY(cuda_check(c, cudaMemsetAsync(P<int32_t>(c->gflag) + n, 0, 4, st), "memset"));
-    CRK_TRY(cuda_check(c, cudaMemsetAsync(c->dev_scalars.p, 0, 64, st), "memset"));
+    if (p->perm) {  // a kernel, not a copy-engine memcpy (see zero_async)
+        k_copy_i32<<<nblk(n, 256), 256, 0, st>>>(n, perm, p->perm);
+        CRK_LAUNCHED(c, "perm copy");
+    }
+    CRK_TRY(cuda_check(c, zero_async(c->cell_start.p, L.ncm * 4, st), "memset"));
+    CRK_TRY(cuda_check(c, zero_async(c->cell_end.p, L.ncm * 4, st), "memset"));
+    CRK_TRY(cuda_check(c, zero_async(P<int32_t>(c->gflag) + n, 4, st), "memset"));
+    CRK_TRY(cuda_check(c, zero_async(c->dev_scalars.p, 64, st), "memset"));
     k_scatter_back<<<nblk(n, 256), 256, 0, st>>>(n, tmpS, in, keys, L.fbits, P<float4>(c->xm), P<int32_t>(c->gflag),
                                                  P<int32_t>(c->cell_start), P<int32_t>(c->cell_end));
     CRK_LAUNCHED(c, "permute back");
@@ -588,7 +595,7 @@ crk_status build_lists(crk_ctx* c, crk_particles* p, cudaStream_t st) {
         CRK_TRY(grow(c, c->rowlen[m], (na + 1) * 4, st));
         CRK_TRY(grow(c, c->rowoff[m], (na + 1) * 4, st));
         ListArgs A = list_args(c, m);
-        CRK_TRY(cuda_check(c, cudaMemsetAsync(P<int32_t>(c->rowlen[m]) + na, 0, 4, st), "memset"));
+        CRK_TRY(cuda_check(c, zero_async(P<int32_t>(c->rowlen[m]) + na, 4, st), "memset"));
         if (na > 0) {
             k_lists<false><<<nblk(na * 32, LIST_WARPS * 32), LIST_WARPS * 32, 0, st>>>(A);
             CRK_LAUNCHED(c, "list count");

@@ -42,6 +42,9 @@ struct Readback {
     void add(const void* s, int off, int b) { src[n] = s; dst[n] = off; bytes[n] = b; ++n; }
 };
 crk_status readback(crk_ctx* c, const Readback& r, cudaStream_t st);
+// zero `bytes` of device memory with a kernel (cudaMemsetAsync may be carried out by a copy
+// engine and then queue behind the caller's bulk transfers on other streams)
+cudaError_t zero_async(void* p, size_t bytes, cudaStream_t st);
 
 // ---------------------------------------------------------------- Morton
 __host__ __device__ inline uint64_t spread3(uint64_t v) {  // 21 bits -> every 3rd bit

@@ -599,7 +599,7 @@ inline cudaError_t launch_list(const Pass& pass, const RowView& rv, const ListVi
     if (e != cudaSuccess) return e;
     if (lv.nrows <= 0) return cudaSuccess;
     if (lv.gate) {
-        e = cudaMemsetAsync(lv.work, 0, sizeof(int), st);
+        e = zero_async(lv.work, sizeof(int), st);
         if (e != cudaSuccess) return e;
     }
     k<<<lv.gate ? persistent_grid(k, NW * 32, smem, lv.nrows) : lv.nrows, NW * 32, smem, st>>>(pass, rv, lv);
