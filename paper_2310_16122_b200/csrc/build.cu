@@ -466,7 +466,7 @@ crk_status build_lists(crk_ctx* c, crk_particles* p, cudaStream_t st) {
     CRK_TRY(grow(c, c->idx_a, n * 4, st));
     CRK_TRY(grow(c, c->idx_b, n * 4, st));
     CRK_TRY(grow(c, c->scratch, n * 48 + 64, st));
-    CRK_TRY(grow(c, c->xm, n * 16, st));
+    CRK_TRY(grow(c, c->xm, (n + JMAX) * 16, st));  // + one j-leaf of padding: whole-leaf reads
     CRK_TRY(grow(c, c->gflag, (n + 1) * 4, st));
     CRK_TRY(grow(c, c->grank, (n + 1) * 4, st));
     CRK_TRY(grow(c, c->cell_start, L.ncm * 4, st));

@@ -609,8 +609,7 @@ constexpr int G = 16, RING = 64, NW = 4, CH = 32;
 struct WarpSm {
     float4 er[2][CH][2];      // entry records of two chunks
     float4 pp[2][CH * JMAX];  // particles of the surviving leaves of two chunks
-    float4 woff[2][CH];       // surviving entries: shift offset, first (w)
-    int wcnt[2][CH];
+    float4 woff[2][CH];       // surviving entries: shift offset, first | (count - 1) << 29 (w)
     float4 wpos[RING];
     int widx[RING];
     float2 inx[G / 2], iny[G / 2], inz[G / 2], im[G / 2];
@@ -689,7 +688,9 @@ __global__ void __launch_bounds__(symp::NW * 32, 16 / symp::NW) grav_pipe_kernel
                 cnt = cc & 0xff;
                 int sx, sy, sz;
                 decode_shift(cc >> 8, sx, sy, sz);
-                off = make_float4((float)sx * A.L[0], (float)sy * A.L[1], (float)sz * A.L[2], bl.w);
+                // w: first | (count - 1) << 29, as in the packed list entries
+                off = make_float4((float)sx * A.L[0], (float)sy * A.L[1], (float)sz * A.L[2],
+                                  __int_as_float(first | ((cnt - 1) << 29)));
                 if (PARTIAL || first + cnt > gself) {  // entries wholly below this group own no pair
                     const float gx = fmaxf(fmaxf(bl.x - hi[0], lo[0] - bh.x), 0.f);
                     const float gy = fmaxf(fmaxf(bl.y - hi[1], lo[1] - bh.y), 0.f);
@@ -700,17 +701,13 @@ __global__ void __launch_bounds__(symp::NW * 32, 16 / symp::NW) grav_pipe_kernel
             const unsigned em = __ballot_sync(0xffffffffu, ek);
             const int ns = __popc(em);
             nsurv[b] = ns;
-            if (ek) {
-                const int q = __popc(em & below);
-                S.wcnt[b][q] = cnt;
-                S.woff[b][q] = off;
-            }
+            if (ek) S.woff[b][__popc(em & below)] = off;
             __syncwarp();
             // particles: lane -> (entry q0 + lane / 8, member lane % 8)
             for (int q0 = 0; q0 < ns; q0 += 32 / JMAX) {
                 const int q = q0 + lane / JMAX, kk = lane % JMAX;
-                if (q < ns && kk < S.wcnt[b][q])
-                    cp_async16(&S.pp[b][q * JMAX + kk], xm + __float_as_int(S.woff[b][q].w) + kk);
+                if (q < ns)  // all JMAX slots (xm is padded): members beyond the count are masked later
+                    cp_async16(&S.pp[b][q * JMAX + kk], xm + (__float_as_int(S.woff[b][q].w) & 0x1fffffff) + kk);
             }
             cp_async_commit();
         };
@@ -779,9 +776,10 @@ __global__ void __launch_bounds__(symp::NW * 32, 16 / symp::NW) grav_pipe_kernel
             for (int q0 = 0; q0 < ns; q0 += 32 / JMAX) {
                 const int q = q0 + lane / JMAX, kk = lane % JMAX;
                 const int qc = q < ns ? q : 0;
-                const int cnt = S.wcnt[b][qc];
                 const float4 o = S.woff[b][qc];
-                int j = __float_as_int(o.w) + kk;
+                const int fc = __float_as_int(o.w);
+                const int cnt = (int)((unsigned)fc >> 29) + 1;
+                int j = (fc & 0x1fffffff) + kk;
                 float4 p = S.pp[b][qc * JMAX + kk];
                 bool keep = q < ns && kk < cnt;
                 if (PARTIAL && keep && !grav_owned(A, p.x, p.y, p.z)) j = -1 - j;  // ghost: no reaction
