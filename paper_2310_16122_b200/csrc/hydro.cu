@@ -494,6 +494,7 @@ struct AccPass : HydCommon {
     static constexpr bool SYM = true;
     static constexpr int UNROLL = 1;
     static constexpr int BATCH = COUNT ? 0 : BATCH_;
+    static constexpr bool IREC = !COUNT;  // list walks stage the i-records (pairs.cuh)
     const float4* jrows;  // gpos (x, y, z, H)
     const float4* jpay;   // grec
     const float4* grec;
@@ -509,6 +510,12 @@ struct AccPass : HydCommon {
         s.x = p.x; s.y = p.y; s.z = p.z; s.idx = k;
         if (COUNT) { s.r.H2 = __fmul_rn(p.w, p.w); return; }
         load_rec(grec, ng, k, s.r);
+    }
+    __device__ void load_i_staged(int k, const float4& p, const float4* rec9, I& s) const {
+        s.x = p.x; s.y = p.y; s.z = p.z; s.idx = k;
+        unpack_rec8(rec9, s.r);
+        const float4 t = rec9[8];
+        s.r.invH = t.x; s.r.H2 = t.y; s.r.m = t.z; s.r.u = t.w;
     }
     __device__ float ix(const I& s) const { return s.x; }
     __device__ float iy(const I& s) const { return s.y; }

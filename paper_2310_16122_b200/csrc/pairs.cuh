@@ -355,23 +355,51 @@ __global__ void __launch_bounds__(NW * 32, MINB) pair_kernel(const Pass pass, co
 // evaluated pair is in the symmetric predicate (the gather passes still apply their own
 // s32 < H_i^2 select).  Rows flagged by the list builder exit here and run pair_kernel
 // with RowView::rows = the builder's flagged-row list.
-template <int PAY, int ENT>
+// IREC (passes that declare `static constexpr bool IREC = true`): the first round of a row
+// also stages the row's i-particles' 9-float4 records (pass.grec), position rows and list
+// lengths, so that a new row's i-data come from shared memory instead of dependent global
+// loads at the start of every CTA
+template <class Pass, class = void>
+struct has_irec : std::false_type {};
+template <class Pass>
+struct has_irec<Pass, std::enable_if_t<Pass::IREC>> : std::true_type {};
+constexpr int LIST_IMAX = 64;  // gas i-leaf <= 64
+template <int PAY, int ENT, bool IREC = false>
 struct ListSmem {
     float4 raw[ENT * JMAX];
     float4 pay[PAY > 0 ? ENT * JMAX * PAY : 1];
     float4 eoff[ENT];  // shift offset (x, y, z), first (w, as int)
+    float4 irec[IREC ? LIST_IMAX * 9 : 1];
+    float4 ipos[IREC ? LIST_IMAX : 1];
+    int icnt[IREC ? LIST_IMAX + 8 : 1];
     uint64_t bar;
     int next;          // claimed row
+};
+struct IStage {  // i-data of a row staged with its first round (IREC)
+    const float4* grec;
+    const float4* gpos;
+    const int32_t* ncnt;
+    int ifirst, icount;
 };
 
 // all threads: stage row entries [e0, e0 + nent) — position rows (x, y, z, w) and PAY payload
 // float4 per particle — then apply the periodic shifts in place (once per slot, exact, O1);
 // returns with the round resident and visible to the CTA
-template <int PAY, int NW, int ENT>
-__device__ __forceinline__ void stage_list_round(ListSmem<PAY, ENT>& sm, const RowView& rv, const float4* jrows,
-                                                 const float4* jpay, int e0, int nent, uint32_t& phase) {
+template <int PAY, int NW, int ENT, bool IREC = false>
+__device__ __forceinline__ void stage_list_round(ListSmem<PAY, ENT, IREC>& sm, const RowView& rv, const float4* jrows,
+                                                 const float4* jpay, int e0, int nent, uint32_t& phase,
+                                                 const IStage* ist = nullptr) {
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
     __syncthreads();  // barrier initialised / previous round consumed
+    if constexpr (IREC) {
+        if (ist && threadIdx.x == NW * 32 - 1) {
+            const int c0 = ist->ifirst & ~3, c1 = (ist->ifirst + ist->icount + 3) & ~3;  // 16-byte aligned cover
+            mbar_expect_tx(&sm.bar, (uint32_t)ist->icount * 160u + (uint32_t)(c1 - c0) * 4u);
+            bulk_g2s(sm.irec, ist->grec + (int64_t)ist->ifirst * 9, (uint32_t)ist->icount * 144u, &sm.bar);
+            bulk_g2s(sm.ipos, ist->gpos + ist->ifirst, (uint32_t)ist->icount * 16u, &sm.bar);
+            bulk_g2s(sm.icnt, ist->ncnt + c0, (uint32_t)(c1 - c0) * 4u, &sm.bar);
+        }
+    }
     for (int t = lane * NW + warp; t < nent; t += NW * 32) {
         int first, count, leaf, code;
         unpack_entry(__ldg(rv.erec + e0 + t), first, count, leaf, code);
@@ -400,8 +428,8 @@ __device__ __forceinline__ void stage_list_round(ListSmem<PAY, ENT>& sm, const R
 }
 
 // persistent CTAs claim rows from lv.work; returns the claimed row (>= nrows: done)
-template <int PAY, int ENT>
-__device__ __forceinline__ int claim_row(ListSmem<PAY, ENT>& sm, int* work) {
+template <class SM>
+__device__ __forceinline__ int claim_row(SM& sm, int* work) {
     if (threadIdx.x == 0) sm.next = atomicAdd(work, 1);
     __syncthreads();
     const int a = sm.next;
@@ -413,7 +441,8 @@ template <class Pass, int NW, int G, int ENT, int MINB>
 __global__ void __launch_bounds__(NW * 32, MINB) list_kernel(const Pass pass, const RowView rv, const ListView lv) {
     static_assert(32 % G == 0, "G must divide the warp");
     constexpr int S = 32 / G;
-    using SM = ListSmem<Pass::PAY, ENT>;
+    constexpr bool IREC = has_irec<Pass>::value;
+    using SM = ListSmem<Pass::PAY, ENT, IREC>;
     extern __shared__ __align__(128) unsigned char smem_raw[];
     SM& sm = *reinterpret_cast<SM*>(smem_raw);
     if (lv.gate && *lv.nfrows == 0) return;  // gated fallback: only when some row is flagged
@@ -441,16 +470,33 @@ __global__ void __launch_bounds__(NW * 32, MINB) list_kernel(const Pass pass, co
         pass.init(acc);
         const int ki = ifirst + ibase + (ivalid ? il : 0);
         int nl = 0;
-        if (wactive) {
-            pass.load_i(ki, is);
-            if (ivalid) nl = lv.ncnt[ki];
+        if constexpr (!IREC) {
+            if (wactive) {
+                pass.load_i(ki, is);
+                if (ivalid) nl = lv.ncnt[ki];
+            }
         }
         const uint16_t* lp = lv.nbr + (int64_t)ki * lv.cap + sl;  // this lane's next list entry
-        const uint16_t* const lend = lv.nbr + (int64_t)ki * lv.cap + nl;
+        const uint16_t* lend = lv.nbr + (int64_t)ki * lv.cap + nl;
         int tn = lp < lend ? (int)*lp : 0x7fffffff;  // next slot of this lane
+        IStage ist;
+        if constexpr (IREC) {
+            ist.grec = pass.grec; ist.gpos = pass.gpos; ist.ncnt = lv.ncnt;
+            ist.ifirst = ifirst; ist.icount = icount;
+        }
         for (int e0 = rbeg; e0 < rend; e0 += ENT) {
             const int nent = min(ENT, rend - e0);
-            stage_list_round<Pass::PAY, NW, ENT>(sm, rv, pass.jrows, pass.jpay, e0, nent, phase);
+            stage_list_round<Pass::PAY, NW, ENT, IREC>(sm, rv, pass.jrows, pass.jpay, e0, nent, phase,
+                                                        IREC && e0 == rbeg ? &ist : nullptr);
+            if constexpr (IREC) {
+                if (e0 == rbeg && wactive) {  // i-data from the staged copy
+                    const int ii = ki - ifirst;
+                    pass.load_i_staged(ki, sm.ipos[ii], &sm.irec[ii * 9], is);
+                    nl = ivalid ? sm.icnt[ii + (ifirst & 3)] : 0;
+                    lend = lv.nbr + (int64_t)ki * lv.cap + nl;
+                    tn = lp < lend ? (int)*lp : 0x7fffffff;
+                }
+            }
             if (wactive) {
                 const int rs = (e0 - rbeg) * JMAX, re = rs + nent * JMAX;
 #pragma unroll 1
@@ -593,7 +639,7 @@ inline int persistent_grid(K kernel, int threads, int smem, int64_t nrows) {
 
 template <class Pass, int NW, int G, int ENT, int MINB>
 inline cudaError_t launch_list(const Pass& pass, const RowView& rv, const ListView& lv, cudaStream_t st) {
-    const int smem = (int)sizeof(ListSmem<Pass::PAY, ENT>);
+    const int smem = (int)sizeof(ListSmem<Pass::PAY, ENT, has_irec<Pass>::value>);
     auto k = list_kernel<Pass, NW, G, ENT, MINB>;
     cudaError_t e = cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
     if (e != cudaSuccess) return e;
