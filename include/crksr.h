@@ -65,7 +65,8 @@ typedef struct crk_params {
                                       decomposition); all-zero dom_hi = whole box.
                                       With a partial domain, i-leaves (and so every output) exist
                                       only for owned cells; particles in other cells are ghosts
-                                      (j-side only) and the kernels run i-centric. */
+                                      (j-side only: gravity evaluates a pair with a ghost in
+                                      the owner's group and drops the reaction). */
 } crk_params;
 
 /* Caller-owned particle arrays (device pointers).  Inputs are sorted IN PLACE by
@@ -150,6 +151,27 @@ crk_status crk_corrections_extras(struct crk_ctx* ctx, crk_particles* parts, voi
  * and energy derivatives with artificial viscosity (O9); kicks v += dt a_h and
  * u += dt du/dt (dt = 0: derivatives only). */
 crk_status crk_hydro_accel_dudt(struct crk_ctx* ctx, crk_particles* parts, float dt, void* stream);
+
+/* ---- sub-cycle steps (readings in DESIGN.md §2 "Sub-cycle") ---- */
+
+/* Time-step limit, written asynchronously to *dt_out (a DEVICE float):
+ *   dt = min over particles of  c_acc sqrt(eps / |a_i|)   (eps = sqrt(eps2); a = gravity
+ *        acceleration, plus the hydro acceleration for gas)   and, for gas,  c_cfl H_i / c_i
+ * (c_i the sound speed of Extras).  A grid-wide float minimum by integer atomicMin on the
+ * bits of non-negative floats (the paper's float fetch_min).  Call after
+ * crk_hydro_accel_dudt with ax/ay/az, ahx/ahy/ahz, H, species present (sorted order).
+ * c_cfl, c_acc > 0 (CRK_EINVAL otherwise).  +inf if every term is infinite. */
+crk_status crk_courant_dt(struct crk_ctx* ctx, crk_particles* parts, float c_cfl, float c_acc, float* dt_out,
+                          void* stream);
+
+/* Kick: v += dt a (+ a_h for gas), u += dt du/dt (gas), one fp32 fma each, from the
+ * caller's ax/ay/az, ahx/ahy/ahz, dudt arrays (all required). */
+crk_status crk_kick(struct crk_ctx* ctx, crk_particles* parts, float dt, void* stream);
+
+/* Drift: x' = fl32(x + dt v) rounded to the nearest multiple of q (ties to even) and
+ * wrapped into [0, box) — positions stay on the q lattice (O1).  Requires |dt v| < box/2.
+ * Invalidates the lists: call crk_build_lists before the next force pass (CRK_ESTATE). */
+crk_status crk_drift(struct crk_ctx* ctx, crk_particles* parts, float dt, void* stream);
 
 /* Count mode (after SPEC.md:374-382): per-particle integer pair counts
  * from the same list-driven pair kernels: gravity (j != i, s32 < rcut2), gas gather

@@ -308,3 +308,36 @@ def substep(parts, params, targets=None, dt_grav=0.0, dt_hydro=0.0, brute=False,
                cs=cs[T3], dv=dv[T3], a=ac["a"], dudt=ac["dudt"], Sa=ac["Sa"], Sdu=ac["Sdu"],
                v=ac["v"], u=ac["u"])
     return out
+
+
+# ----------------------------------------------------------------- sub-cycle (NEXT-2)
+def courant_dt(species, H, cs, a, ah, params, c_cfl=0.25, c_acc=0.25):
+    """dt = min_i of C_acc sqrt(eps/|a_i|) (a + a_h for gas) and, for gas, C_cfl H_i / c_i (fp64)."""
+    n = species.shape[0]
+    f = lambda v: np.ascontiguousarray(v, np.float32)  # noqa: E731
+    lib().orc_courant.restype = C.c_double
+    return float(lib().orc_courant(C.c_int64(n), _p(np.ascontiguousarray(species, np.uint8)), _p(f(H)), _p(f(cs)),
+                                   _p(f(a[:, 0])), _p(f(a[:, 1])), _p(f(a[:, 2])), _p(f(ah[:, 0])), _p(f(ah[:, 1])),
+                                   _p(f(ah[:, 2])), C.c_double(params["eps2"]), C.c_double(c_cfl),
+                                   C.c_double(c_acc)))
+
+
+def kick(species, v, u, a, ah, dudt, dt):
+    """v += dt (a + a_h for gas), u += dt du/dt (gas), one fp32 fma each; returns new (v, u)."""
+    n = species.shape[0]
+    f = lambda x: np.ascontiguousarray(x, np.float32).copy()  # noqa: E731
+    vx, vy, vz, uu = f(v[:, 0]), f(v[:, 1]), f(v[:, 2]), f(u)
+    lib().orc_kick(C.c_int64(n), _p(np.ascontiguousarray(species, np.uint8)), C.c_float(dt),
+                   _p(f(a[:, 0])), _p(f(a[:, 1])), _p(f(a[:, 2])), _p(f(ah[:, 0])), _p(f(ah[:, 1])), _p(f(ah[:, 2])),
+                   _p(f(dudt)), _p(vx), _p(vy), _p(vz), _p(uu))
+    return np.stack([vx, vy, vz], 1), uu
+
+
+def drift(x, v, box, dt):
+    """x' = fl32(x + dt v) on the q lattice, wrapped (fp32, bit-exact specification)."""
+    n = x.shape[0]
+    xs = [np.ascontiguousarray(x[:, a], np.float32).copy() for a in range(3)]
+    vs = [np.ascontiguousarray(v[:, a], np.float32) for a in range(3)]
+    b = (C.c_double * 3)(*box)
+    lib().orc_drift(C.c_int64(n), b, C.c_float(dt), _p(xs[0]), _p(xs[1]), _p(xs[2]), _p(vs[0]), _p(vs[1]), _p(vs[2]))
+    return np.stack(xs, 1)

@@ -880,3 +880,68 @@ int orc_neighbour_sets(int64_t n, const float* x, const float* y, const float* z
 }
 
 int orc_num_threads(void) { return omp_get_max_threads(); }
+
+/* ------------------------------------------------------------------ sub-cycle (NEXT-2)
+ * Readings (DESIGN.md §2 "Sub-cycle"; SURVEY.md §8(f) NEXT-2 names the steps, the paper
+ * only that the kernels run several times per step, and a float fetch_min,
+ * PAPER.md:389):
+ *   time step  dt = min_i dt_i,  dt_i = C_acc sqrt(eps / |a_i|) (eps = sqrt(eps2), a the
+ *              gravity acceleration plus, for gas, the hydro one), and for gas also
+ *              C_cfl H_i / c_i — evaluated here in fp64;
+ *   kick       v += dt a, u += dt du/dt: one fp32 fma per component (as specified);
+ *   drift      x' = fl32(x + dt v) (one fp32 fma), rounded to the nearest multiple of
+ *              q = L_max 2^-23 (ties to even), wrapped into [0, L) — positions stay on the
+ *              q lattice (O1).  Specified in fp32 so that it is compared bit for bit. */
+double orc_courant(int64_t n, const uint8_t* species, const float* H, const float* cs, const float* ax,
+                   const float* ay, const float* az, const float* ahx, const float* ahy, const float* ahz,
+                   double eps2, double c_cfl, double c_acc) {
+    const double eps = sqrt(eps2);
+    double best = INFINITY;
+    for (int64_t i = 0; i < n; ++i) {
+        double gx = ax[i], gy = ay[i], gz = az[i];
+        if (species[i] == 1) { gx += ahx[i]; gy += ahy[i]; gz += ahz[i]; }
+        const double a = sqrt(gx * gx + gy * gy + gz * gz);
+        double d = a > 0.0 ? c_acc * sqrt(eps / a) : INFINITY;
+        if (species[i] == 1 && cs[i] > 0.0f) {
+            const double dc = c_cfl * (double)H[i] / (double)cs[i];
+            if (dc < d) d = dc;
+        }
+        if (d < best) best = d;
+    }
+    return best;
+}
+
+void orc_kick(int64_t n, const uint8_t* species, float dt, const float* ax, const float* ay, const float* az,
+              const float* ahx, const float* ahy, const float* ahz, const float* dudt, float* vx, float* vy,
+              float* vz, float* u) {
+    for (int64_t i = 0; i < n; ++i) {
+        float gx = ax[i], gy = ay[i], gz = az[i];
+        if (species[i] == 1) {
+            gx += ahx[i]; gy += ahy[i]; gz += ahz[i];
+            u[i] = fmaf(dt, dudt[i], u[i]);
+        }
+        vx[i] = fmaf(dt, gx, vx[i]);
+        vy[i] = fmaf(dt, gy, vy[i]);
+        vz[i] = fmaf(dt, gz, vz[i]);
+    }
+}
+
+static float drift1(float x, float v, float dt, float q, float L) {
+    const float t = fmaf(dt, v, x);
+    float r = rintf(t / q) * q; /* q a power of two: the division and product are exact */
+    if (r >= L) r -= L;
+    else if (r < 0.0f) r += L;
+    return r;
+}
+
+void orc_drift(int64_t n, const double* box, float dt, float* x, float* y, float* z, const float* vx,
+               const float* vy, const float* vz) {
+    double lmax = box[0] > box[1] ? box[0] : box[1];
+    if (box[2] > lmax) lmax = box[2];
+    const float q = (float)ldexp(lmax, -23);
+    for (int64_t i = 0; i < n; ++i) {
+        x[i] = drift1(x[i], vx[i], dt, q, (float)box[0]);
+        y[i] = drift1(y[i], vy[i], dt, q, (float)box[1]);
+        z[i] = drift1(z[i], vz[i], dt, q, (float)box[2]);
+    }
+}

@@ -20,7 +20,8 @@ STATUS = {0: "CRK_OK", -1: "CRK_EINVAL", -2: "CRK_ENOMEM", -3: "CRK_ECUDA", -4: 
 EXPORTS = ["crk_create", "crk_destroy", "crk_build_lists", "crk_gravity_kick", "crk_geometry",
            "crk_corrections", "crk_extras", "crk_corrections_extras", "crk_hydro_accel_dudt", "crk_count_pairs",
            "crk_list_view", "crk_launch_count", "crk_status_string", "crk_last_error", "crk_select_cells", "crk_select_gas",
-           "crk_pack_particles", "crk_unpack_particles", "crk_pack_gas", "crk_unpack_gas"]
+           "crk_pack_particles", "crk_unpack_particles", "crk_pack_gas", "crk_unpack_gas", "crk_courant_dt",
+           "crk_kick", "crk_drift"]
 
 
 class CrkError(RuntimeError):
@@ -79,6 +80,9 @@ def lib():
         for f in ("crk_gravity_kick", "crk_hydro_accel_dudt"):
             getattr(L, f).argtypes = [vp, C.POINTER(CrkParticles), C.c_float, vp]
         L.crk_count_pairs.argtypes = [vp, C.POINTER(CrkParticles), vp, vp, vp, vp]
+        L.crk_courant_dt.argtypes = [vp, C.POINTER(CrkParticles), C.c_float, C.c_float, vp, vp]
+        for f in ("crk_kick", "crk_drift"):
+            getattr(L, f).argtypes = [vp, C.POINTER(CrkParticles), C.c_float, vp]
         L.crk_list_view.argtypes = [vp, C.POINTER(CrkLists)]
         L.crk_launch_count.argtypes = [vp]
         L.crk_launch_count.restype = C.c_int64
@@ -96,7 +100,7 @@ def lib():
         for f in ("crk_create", "crk_destroy", "crk_build_lists", "crk_gravity_kick", "crk_geometry",
                   "crk_corrections", "crk_extras", "crk_corrections_extras", "crk_hydro_accel_dudt",
                   "crk_count_pairs", "crk_list_view", "crk_select_cells", "crk_select_gas", "crk_pack_particles", "crk_unpack_particles",
-                  "crk_pack_gas", "crk_unpack_gas"):
+                  "crk_pack_gas", "crk_unpack_gas", "crk_courant_dt", "crk_kick", "crk_drift"):
             getattr(L, f).restype = C.c_int
         _lib = L
     return _lib
@@ -271,6 +275,36 @@ class Solver:
                 self.corrections(parts, stream)
                 self.extras(parts, stream)
             self.hydro_accel_dudt(parts, dt_hydro, stream)
+
+    # ---- sub-cycle ----
+    def courant_dt(self, parts, c_cfl=0.25, c_acc=0.25, stream=None):
+        """min over particles of the Courant / acceleration limits (crk_courant_dt); syncs."""
+        out = torch.empty(1, dtype=torch.float32, device=parts.device)
+        self._call(lib().crk_courant_dt, parts, C.c_float(c_cfl), C.c_float(c_acc), C.c_void_p(out.data_ptr()),
+                   stream=stream)
+        return float(out.item())
+
+    def kick(self, parts, dt, stream=None):
+        self._call(lib().crk_kick, parts, C.c_float(dt), stream=stream)
+
+    def drift(self, parts, dt, stream=None):
+        self._call(lib().crk_drift, parts, C.c_float(dt), stream=stream)
+
+    def kdk(self, parts, n_steps, c_cfl=0.25, c_acc=0.25, stream=None):
+        """Kick-drift-kick leapfrog over n_steps sub-cycles, each with the time step of
+        crk_courant_dt: forces at x_n, kick dt/2, drift dt, forces at x_{n+1} (the
+        velocity-dependent hydro terms see v_{n+1/2}), kick dt/2.  Needs the force outputs
+        (ax.., ahx.., dudt).  Returns the time steps taken."""
+        self.substep(parts, stream=stream)
+        dts = []
+        for _ in range(n_steps):
+            dt = self.courant_dt(parts, c_cfl, c_acc, stream)
+            self.kick(parts, 0.5 * dt, stream)
+            self.drift(parts, dt, stream)
+            self.substep(parts, stream=stream)
+            self.kick(parts, 0.5 * dt, stream)
+            dts.append(dt)
+        return dts
 
     def count_pairs(self, parts, stream=None):
         n = parts.n

@@ -10,7 +10,7 @@ CSRC = os.path.join(HERE, "csrc")
 ROOT = os.path.dirname(HERE)
 LIB = os.path.join(HERE, "libcrksr.so")
 OBJDIR = os.path.join(HERE, "_build")
-SOURCES = ["api.cu", "build.cu", "gravity.cu", "hydro.cu", "domain.cu"]
+SOURCES = ["api.cu", "build.cu", "gravity.cu", "hydro.cu", "domain.cu", "integrate.cu"]
 HEADERS = ["ctx.h", "common.cuh", "pairs.cuh"]
 
 NVCC = os.environ.get("NVCC", "/usr/local/cuda/bin/nvcc")

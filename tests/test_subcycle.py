@@ -1,0 +1,198 @@
+"""Sub-cycle steps: time-step limit, kick, drift on the q lattice.
+
+CPU: the oracle's kick / drift / time step against closed forms and invariants.
+GPU (-m gpu): crk_courant_dt, crk_kick, crk_drift against the oracle on the same sorted
+arrays (drift and kick bit-exact: both are specified in fp32; the time step within fp32
+rounding of the per-particle terms), and a two-step kick-drift-kick against the oracle's.
+"""
+import math
+
+import numpy as np
+import pytest
+
+import oracle
+from crk_testutil import cached_config
+
+Q_BITS = 23
+
+
+def _q(box):
+    return math.ldexp(max(box), -Q_BITS)
+
+
+# ----------------------------------------------------------------- CPU pins
+def test_drift_stays_on_lattice_and_wraps():
+    box = [16.0, 8.0, 8.0]
+    q = _q(box)
+    rng = np.random.default_rng(5)
+    n = 4000
+    x = np.floor(rng.random((n, 3)) * np.array(box) / q) * q
+    v = rng.normal(0, 3.0, (n, 3)).astype(np.float32)
+    y = oracle.drift(x.astype(np.float32), v, box, 0.37)
+    assert np.all(np.mod(y.astype(np.float64), q) == 0.0)  # multiples of q (O1)
+    for a in range(3):
+        assert np.all((y[:, a] >= 0) & (y[:, a] < box[a]))
+    # closed form away from rounding: |fl(x + dt v) - (x + dt v)| <= ulp, then <= q/2 to the lattice
+    exact = np.mod(x + 0.37 * v.astype(np.float64), np.array(box))
+    d = np.abs(y - exact)
+    d = np.minimum(d, np.array(box) - d)
+    assert np.all(d <= q / 2 + 1e-6 * np.array(box))
+
+
+def test_drift_exact_cases():
+    box = [8.0, 8.0, 8.0]
+    q = _q(box)
+    x = np.array([[1.0, 7.5, 0.25]], np.float32)
+    v = np.array([[0.0, 2.0, -1.0]], np.float32)
+    y = oracle.drift(x, v, box, 0.5)  # dt v = (0, 1, -0.5): exact, with wraps on y and z
+    assert np.array_equal(y, np.array([[1.0, 0.5, 7.75]], np.float32))
+    back = oracle.drift(y, v, box, -0.5)
+    assert np.array_equal(back, x)
+    # a step of a quarter quantum rounds back to the lattice point (ties to even: 0.5 q -> 0)
+    y = oracle.drift(x, np.array([[q / 4, q / 2, 0.0]], np.float32), box, 1.0)
+    assert y[0, 0] == x[0, 0] and y[0, 1] == x[0, 1]
+
+
+def test_kick_closed_form():
+    sp = np.array([0, 1], np.uint8)
+    v = np.array([[1.0, 0.0, -1.0], [0.5, 0.25, 0.0]], np.float32)
+    u = np.array([0.0, 2.0], np.float32)
+    a = np.array([[2.0, -4.0, 0.0], [1.0, 1.0, 1.0]], np.float32)
+    ah = np.array([[100.0, 100.0, 100.0], [1.0, -1.0, 3.0]], np.float32)  # ignored for DM
+    dudt = np.array([9.0, -2.0], np.float32)
+    v2, u2 = oracle.kick(sp, v, u, a, ah, dudt, 0.5)
+    assert np.array_equal(v2, np.array([[2.0, -2.0, -1.0], [1.5, 0.25, 2.0]], np.float32))
+    assert np.array_equal(u2, np.array([0.0, 1.0], np.float32))
+
+
+def test_courant_closed_forms():
+    params = {"eps2": 0.01}
+    n = 10
+    sp = np.array([1] * 5 + [0] * 5, np.uint8)
+    H = np.full(n, 2.0, np.float32)
+    cs = np.full(n, 4.0, np.float32)
+    z = np.zeros((n, 3), np.float32)
+    # no accelerations: the sound-crossing limit C_cfl H / c
+    assert oracle.courant_dt(sp, H, cs, z, z, params, 0.3, 0.25) == pytest.approx(0.3 * 2.0 / 4.0, rel=1e-15)
+    # a uniform acceleration 9 on the dark matter only: C_acc sqrt(eps / 9) (eps = 0.1) is smaller
+    a = z.copy()
+    a[5:, 0] = 9.0
+    want = min(0.3 * 0.5, 0.25 * math.sqrt(0.1 / 9.0))
+    assert oracle.courant_dt(sp, H, cs, a, z, params, 0.3, 0.25) == pytest.approx(want, rel=1e-15)
+    # gas: gravity and hydro accelerations add (3-4-0 + 0-0-12 -> |a| = 13)
+    a2, ah = z.copy(), z.copy()
+    a2[0] = (3.0, 4.0, 0.0)
+    ah[0] = (0.0, 0.0, 12.0)
+    want = min(0.3 * 0.5, 0.25 * math.sqrt(0.1 / 13.0))
+    assert oracle.courant_dt(sp, H, cs, a2, ah, params, 0.3, 0.25) == pytest.approx(want, rel=1e-15)
+
+
+# ----------------------------------------------------------------- GPU parity
+def _gpu_state(name):
+    import torch
+    from paper_2310_16122_b200 import Particles, Solver
+
+    parts, params = cached_config(name)
+    p = Particles.from_host(parts, "cuda")
+    s = Solver(params, 0)
+    s.substep(p)
+    torch.cuda.synchronize()
+    return parts, params, p, s
+
+
+def _host(p, keys):
+    return {k: getattr(p, k).cpu().numpy() for k in keys}
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("name", ["c1", "c2z"])
+def test_gpu_courant_kick_drift(name):
+    parts, params, p, s = _gpu_state(name)
+    h = _host(p, ["x", "y", "z", "vx", "vy", "vz", "u", "H", "species", "cs", "ax", "ay", "az", "ahx", "ahy",
+                  "ahz", "dudt"])
+    a = np.stack([h["ax"], h["ay"], h["az"]], 1)
+    ah = np.stack([h["ahx"], h["ahy"], h["ahz"]], 1)
+    dt = s.courant_dt(p, 0.25, 0.3)
+    ref = oracle.courant_dt(h["species"], h["H"], h["cs"], a, ah, params, 0.25, 0.3)
+    assert abs(dt - ref) <= 1e-6 * ref
+    # kick: bit-exact (one fp32 fma per component on both sides)
+    s.kick(p, 0.5 * dt)
+    v0 = np.stack([h["vx"], h["vy"], h["vz"]], 1)
+    vk, uk = oracle.kick(h["species"], v0, h["u"], a, ah, h["dudt"], np.float32(0.5 * dt))
+    g = _host(p, ["vx", "vy", "vz", "u"])
+    assert np.array_equal(np.stack([g["vx"], g["vy"], g["vz"]], 1), vk)
+    assert np.array_equal(g["u"], uk)
+    # drift: bit-exact, on the q lattice
+    s.drift(p, dt)
+    xd = oracle.drift(np.stack([h["x"], h["y"], h["z"]], 1), vk, params["box"], np.float32(dt))
+    g = _host(p, ["x", "y", "z"])
+    assert np.array_equal(np.stack([g["x"], g["y"], g["z"]], 1), xd)
+    s.close()
+
+
+@pytest.mark.gpu
+def test_gpu_drift_requires_rebuild():
+    from paper_2310_16122_b200.binding import CrkError
+
+    parts, params, p, s = _gpu_state("c1")
+    s.drift(p, 0.0)
+    with pytest.raises(CrkError):
+        s.gravity_kick(p)
+    s.close()
+
+
+@pytest.mark.gpu
+def test_gpu_kdk_two_steps_matches_oracle():
+    """Two kick-drift-kick sub-cycles on c1 against the oracle's sequence (forces from
+    oracle.substep, the GPU's time steps): positions within a few q, velocities and u
+    within the force tolerance accumulated over the kicks."""
+    import torch
+    from paper_2310_16122_b200 import Particles, Solver
+
+    parts, params = cached_config("c1")
+    p = Particles.from_host(parts, "cuda")
+    s = Solver(params, 0)
+    dts = s.kdk(p, 2, 0.25, 0.3)
+    torch.cuda.synchronize()
+    h = p.to_host()
+    s.close()
+    # the oracle's sequence in input order (the GPU sorts in place; compare by id)
+    st = {k: parts[k].copy() for k in parts}
+    n = st["x"].shape[0]
+    gas = st["species"] == 1
+
+    def forces(st):
+        ref = oracle.substep(st, params)
+        a = ref["grav_a"].astype(np.float32)
+        ah = np.zeros((n, 3), np.float32)
+        du = np.zeros(n, np.float32)
+        ah[ref["targets"]] = ref["a"]
+        du[ref["targets"]] = ref["dudt"]
+        return a, ah, du
+
+    def do_kick(st, dt, f):
+        v, u = oracle.kick(st["species"], np.stack([st["vx"], st["vy"], st["vz"]], 1), st["u"], f[0], f[1], f[2], dt)
+        st["vx"], st["vy"], st["vz"], st["u"] = v[:, 0].copy(), v[:, 1].copy(), v[:, 2].copy(), u
+
+    f = forces(st)
+    for dt in dts:
+        do_kick(st, np.float32(0.5 * dt), f)
+        x = oracle.drift(np.stack([st["x"], st["y"], st["z"]], 1), np.stack([st["vx"], st["vy"], st["vz"]], 1),
+                         params["box"], np.float32(dt))
+        st["x"], st["y"], st["z"] = x[:, 0].copy(), x[:, 1].copy(), x[:, 2].copy()
+        f = forces(st)
+        do_kick(st, np.float32(0.5 * dt), f)
+    pos_of_id = np.empty(n, np.int64)
+    pos_of_id[h["id"]] = np.arange(n)
+    g = pos_of_id[st["id"]]
+    q = _q(params["box"])
+    L = np.array(params["box"])
+    dx = np.abs(np.stack([h["x"][g], h["y"][g], h["z"][g]], 1) - np.stack([st["x"], st["y"], st["z"]], 1))
+    dx = np.minimum(dx, L - dx)
+    assert np.max(dx) <= 4 * q
+    v_ref = np.stack([st["vx"], st["vy"], st["vz"]], 1).astype(np.float64)
+    v_gpu = np.stack([h["vx"][g], h["vy"][g], h["vz"][g]], 1)
+    dv0 = np.abs(v_ref - np.stack([parts["vx"], parts["vy"], parts["vz"]], 1)).max()
+    assert np.max(np.abs(v_gpu - v_ref)) <= 1e-4 * dv0 + 1e-6 * np.abs(v_ref).max()
+    du0 = np.abs(st["u"] - parts["u"]).max()
+    assert np.max(np.abs(h["u"][g] - st["u"])) <= 1e-4 * du0 + 1e-6 * np.abs(st["u"]).max()
