@@ -48,7 +48,7 @@ __global__ void k_zero(uint4* p16, size_t n16, char* tail, int ntail) {
     if (i < (size_t)ntail) tail[i] = 0;
 }
 
-cudaError_t zero_async(void* p, size_t bytes, cudaStream_t st) {
+cudaError_t zero_async(void* p, size_t bytes, cudaStream_t st, crk_ctx* c) {
     if (bytes == 0) return cudaSuccess;
     char* b = static_cast<char*>(p);
     const size_t head = (16 - (reinterpret_cast<uintptr_t>(b) & 15)) & 15;  // unaligned prefix bytes
@@ -56,8 +56,12 @@ cudaError_t zero_async(void* p, size_t bytes, cudaStream_t st) {
     const size_t n16 = (bytes - pre) / 16;
     const size_t rest = bytes - pre - 16 * n16;
     // prefix and suffix (< 16 bytes each) by a second tiny launch
-    if (pre) k_zero<<<1, 32, 0, st>>>(nullptr, 0, b, (int)pre);
+    if (pre) {
+        k_zero<<<1, 32, 0, st>>>(nullptr, 0, b, (int)pre);
+        if (c) c->launches++;
+    }
     if (n16 || rest) {
+        if (c) c->launches++;
         const size_t blocks = n16 ? (n16 + 255) / 256 : 1;
         k_zero<<<(unsigned)(blocks < 4096 ? blocks : 4096), 256, 0, st>>>(reinterpret_cast<uint4*>(b + pre), n16,
                                                                         b + pre + 16 * n16, (int)rest);
@@ -273,9 +277,9 @@ crk_status crk_count_pairs(crk_ctx* c, crk_particles* p, int32_t* cgrav, int32_t
     CRK_TRY(check_parts(c, p, true));
     if (!cgrav || !cgather || !csym) return fail(c, CRK_EINVAL, "null count array");
     cudaStream_t st = (cudaStream_t)stream;
-    CRK_TRY(cuda_check(c, zero_async(cgrav, p->n * 4, st), "memset"));
-    CRK_TRY(cuda_check(c, zero_async(cgather, p->n * 4, st), "memset"));
-    CRK_TRY(cuda_check(c, zero_async(csym, p->n * 4, st), "memset"));
+    CRK_TRY(cuda_check(c, zero_async(cgrav, p->n * 4, st, c), "memset"));
+    CRK_TRY(cuda_check(c, zero_async(cgather, p->n * 4, st, c), "memset"));
+    CRK_TRY(cuda_check(c, zero_async(csym, p->n * 4, st, c), "memset"));
     CRK_TRY(gravity_count(c, p, cgrav, st));
     return hydro_count(c, cgather, csym, st);
 }

@@ -517,10 +517,10 @@ crk_status build_lists(crk_ctx* c, crk_particles* p, cudaStream_t st) {
         k_copy_i32<<<nblk(n, 256), 256, 0, st>>>(n, perm, p->perm);
         CRK_LAUNCHED(c, "perm copy");
     }
-    CRK_TRY(cuda_check(c, zero_async(c->cell_start.p, L.ncm * 4, st), "memset"));
-    CRK_TRY(cuda_check(c, zero_async(c->cell_end.p, L.ncm * 4, st), "memset"));
-    CRK_TRY(cuda_check(c, zero_async(P<int32_t>(c->gflag) + n, 4, st), "memset"));
-    CRK_TRY(cuda_check(c, zero_async(c->dev_scalars.p, 64, st), "memset"));
+    CRK_TRY(cuda_check(c, zero_async(c->cell_start.p, L.ncm * 4, st, c), "memset"));
+    CRK_TRY(cuda_check(c, zero_async(c->cell_end.p, L.ncm * 4, st, c), "memset"));
+    CRK_TRY(cuda_check(c, zero_async(P<int32_t>(c->gflag) + n, 4, st, c), "memset"));
+    CRK_TRY(cuda_check(c, zero_async(c->dev_scalars.p, 64, st, c), "memset"));
     k_scatter_back<<<nblk(n, 256), 256, 0, st>>>(n, tmpS, in, keys, L.fbits, P<float4>(c->xm), P<int32_t>(c->gflag),
                                                  P<int32_t>(c->cell_start), P<int32_t>(c->cell_end));
     CRK_LAUNCHED(c, "permute back");
@@ -595,7 +595,7 @@ crk_status build_lists(crk_ctx* c, crk_particles* p, cudaStream_t st) {
         CRK_TRY(grow(c, c->rowlen[m], (na + 1) * 4, st));
         CRK_TRY(grow(c, c->rowoff[m], (na + 1) * 4, st));
         ListArgs A = list_args(c, m);
-        CRK_TRY(cuda_check(c, zero_async(P<int32_t>(c->rowlen[m]) + na, 4, st), "memset"));
+        CRK_TRY(cuda_check(c, zero_async(P<int32_t>(c->rowlen[m]) + na, 4, st, c), "memset"));
         if (na > 0) {
             k_lists<false><<<nblk(na * 32, LIST_WARPS * 32), LIST_WARPS * 32, 0, st>>>(A);
             CRK_LAUNCHED(c, "list count");

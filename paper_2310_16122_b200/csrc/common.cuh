@@ -44,7 +44,7 @@ struct Readback {
 crk_status readback(crk_ctx* c, const Readback& r, cudaStream_t st);
 // zero `bytes` of device memory with a kernel (cudaMemsetAsync may be carried out by a copy
 // engine and then queue behind the caller's bulk transfers on other streams)
-cudaError_t zero_async(void* p, size_t bytes, cudaStream_t st);
+cudaError_t zero_async(void* p, size_t bytes, cudaStream_t st, crk_ctx* c = nullptr);  // counts launches in c
 
 // ---------------------------------------------------------------- Morton
 __host__ __device__ inline uint64_t spread3(uint64_t v) {  // 21 bits -> every 3rd bit

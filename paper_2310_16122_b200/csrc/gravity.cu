@@ -905,7 +905,7 @@ static int grav_variant() {
 static crk_status gravity_sym(crk_ctx* c, crk_particles* p, float dt, cudaStream_t st) {
     const int64_t n = c->n;
     CRK_TRY(grow(c, c->gacc, n * 16, st));
-    CRK_TRY(cuda_check(c, zero_async(c->gacc.p, n * 16, st), "memset"));
+    CRK_TRY(cuda_check(c, zero_async(c->gacc.p, n * 16, st, c), "memset"));
     if (c->nleaf[0] > 0) {
         GravSymArgs A;
         A.xm = P<float4>(c->xm);
@@ -927,7 +927,7 @@ static crk_status gravity_sym(crk_ctx* c, crk_particles* p, float dt, cudaStream
         for (int d = 0; d < 3; ++d) { A.dlo[d] = c->lay.dlo[d]; A.dhi[d] = c->lay.dhi[d]; }
         const int var = grav_variant();
         CRK_TRY(grow(c, c->work, 64, st));
-        CRK_TRY(cuda_check(c, zero_async(c->work.p, 16, st), "memset"));
+        CRK_TRY(cuda_check(c, zero_async(c->work.p, 16, st, c), "memset"));
         A.work = P<int>(c->work);
         cudaError_t e;
         // measured on c4 (profiles/r01): <8 warps, 320 entries, 1 buffer> 24.6 ms, <4, 320, 1> 30.3,

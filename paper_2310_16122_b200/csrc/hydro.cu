@@ -842,7 +842,7 @@ crk_status geometry(crk_ctx* c, crk_particles* p, cudaStream_t st) {
         // lflag: per-row flags, then the compact flagged-row list, then its length
         const size_t fl = (size_t)(2 * c->nleaf[2] + 1) * sizeof(int32_t);
         CRK_TRY(grow(c, c->lflag, fl, st));
-        CRK_TRY(cuda_check(c, zero_async(c->lflag.p, fl, st), "memset"));
+        CRK_TRY(cuda_check(c, zero_async(c->lflag.p, fl, st, c), "memset"));
         g.lv = list_view(c);
         return launch_hyd<GeoPass<false, true>, 128, 2>(c, g, st, "geometry (list build) kernel");
     }
@@ -956,7 +956,7 @@ crk_status corrections_extras(crk_ctx* c, crk_particles* p, cudaStream_t st) {
 static crk_status accel_symlist(crk_ctx* c, crk_particles* p, float dt, cudaStream_t st) {
     const int64_t ng = c->n_gas;
     CRK_TRY(grow(c, c->gacc, (ng > 0 ? ng : 1) * 16, st));
-    CRK_TRY(cuda_check(c, zero_async(c->gacc.p, (ng > 0 ? ng : 1) * 16, st), "memset"));
+    CRK_TRY(cuda_check(c, zero_async(c->gacc.p, (ng > 0 ? ng : 1) * 16, st, c), "memset"));
     CRK_TRY(grow(c, c->work, 64, st));
     AccSymListArgs A;
     A.gpos = P<float4>(c->gpos);
@@ -969,7 +969,7 @@ static crk_status accel_symlist(crk_ctx* c, crk_particles* p, float dt, cudaStre
     const int smem = (int)sizeof(ListSmem<9, ASL_ENT>);
     cudaError_t e = cudaFuncSetAttribute(acc_symlist_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
     if (e != cudaSuccess) return cuda_check(c, e, "smem attribute");
-    CRK_TRY(cuda_check(c, zero_async(A.lv.work, sizeof(int), st), "memset"));
+    CRK_TRY(cuda_check(c, zero_async(A.lv.work, sizeof(int), st, c), "memset"));
     acc_symlist_kernel<<<persistent_grid(acc_symlist_kernel, ASL_NW * 32, smem, A.lv.nrows), ASL_NW * 32, smem, st>>>(A);
     CRK_LAUNCHED(c, "accel/dudt (symmetric list) kernel");
     k_acc_finish<<<(unsigned)((ng + 255) / 256), 256, 0, st>>>(ng, P<float4>(c->gacc), P<int32_t>(c->gas_idx), dt,
