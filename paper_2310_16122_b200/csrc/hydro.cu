@@ -844,7 +844,7 @@ crk_status geometry(crk_ctx* c, crk_particles* p, cudaStream_t st) {
         CRK_TRY(grow(c, c->lflag, fl, st));
         CRK_TRY(cuda_check(c, zero_async(c->lflag.p, fl, st, c), "memset"));
         g.lv = list_view(c);
-        return launch_hyd<GeoPass<false, true>, 128, 2>(c, g, st, "geometry (list build) kernel");
+        return launch_hyd<GeoPass<false, true>, 128, 4>(c, g, st, "geometry (list build) kernel");
     }
     GeoPass<false> g;
     common(c, g);
@@ -940,7 +940,7 @@ crk_status corrections_extras(crk_ctx* c, crk_particles* p, cudaStream_t st) {
     const ExtPass ge = ext_pass(c, p);
     RowView rv = hydro_rows(c);
     const ListView lv = list_view(c);
-    CRK_TRY(cuda_check(c, (launch_list2<CorPass, ExtPass, HYD_NW, HYD_G, 128, 3>(gc, ge, rv, lv, st)),
+    CRK_TRY(cuda_check(c, (launch_list2<CorPass, ExtPass, HYD_NW, HYD_G, 128, 4>(gc, ge, rv, lv, st)),
                        "corrections + extras kernel"));
     c->launches++;
     rv.rows = lv.frows;
