@@ -292,7 +292,7 @@ constexpr int LIST_WARPS = 8;
 // form of O4 (gaps are multiples of q below 2^24 q).  Tiny boxes use the generic path
 // with the per-axis shift search.
 template <bool FILL>
-__global__ void __launch_bounds__(LIST_WARPS * 32) k_lists(ListArgs A) {
+__global__ void __launch_bounds__(LIST_WARPS * 32, 5) k_lists(ListArgs A) {
     __shared__ int32_t s_b0[LIST_WARPS][32], s_ex[LIST_WARPS][32], s_code[LIST_WARPS][32];
     const int64_t a = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5;
     const int lane = threadIdx.x & 31;
