@@ -173,6 +173,17 @@ crk_status crk_kick(struct crk_ctx* ctx, crk_particles* parts, float dt, void* s
  * Invalidates the lists: call crk_build_lists before the next force pass (CRK_ESTATE). */
 crk_status crk_drift(struct crk_ctx* ctx, crk_particles* parts, float dt, void* stream);
 
+/* Smoothing-length update (NEXT-2 H adaptation), after crk_geometry: for every gas
+ * particle H_out[i] = factor * sqrt(d2_(k)) (fp32 sqrt and product, correctly rounded),
+ * d2_(k) the k_ngb-th smallest O2 squared distance (s32) to another gas particle, selected
+ * among its neighbour list.  Exact when d2_(k) < H_i^2 (the list holds every gas particle
+ * within H_i); otherwise H_out is an upper bound (2 H_i if the list has fewer than k_ngb
+ * entries) and the particle is counted in *n_unconverged (a device int32): rebuild with
+ * H = H_out and update again.  H_out: device, length n, sorted order, gas entries written.
+ * k_ngb in [1, 127], factor > 0 (CRK_EINVAL); needs the lists (CRK_ESTATE without). */
+crk_status crk_update_h(struct crk_ctx* ctx, crk_particles* parts, int32_t k_ngb, float factor, float* H_out,
+                        int32_t* n_unconverged, void* stream);
+
 /* Count mode (after SPEC.md:374-382): per-particle integer pair counts
  * from the same list-driven pair kernels: gravity (j != i, s32 < rcut2), gas gather
  * (gas j != i, s32 < H_i^2) and gas symmetric (s32 < max(H_i^2, H_j^2)); 0 for DM.

@@ -341,3 +341,16 @@ def drift(x, v, box, dt):
     b = (C.c_double * 3)(*box)
     lib().orc_drift(C.c_int64(n), b, C.c_float(dt), _p(xs[0]), _p(xs[1]), _p(xs[2]), _p(vs[0]), _p(vs[1]), _p(vs[2]))
     return np.stack(xs, 1)
+
+
+def knn_h(parts, params, targets, k=64, factor=1.01):
+    """H' = fl32(factor * sqrt(k-th smallest s32 to another gas particle)) and whether that
+    neighbour lies inside the current H (brute force over every gas particle)."""
+    t = _targets(parts, targets)
+    Hn = np.empty(t.shape[0], np.float32)
+    conv = np.empty(t.shape[0], np.int32)
+    b = (C.c_double * 3)(*params["box"])
+    lib().orc_knn_h(C.c_int64(parts["x"].shape[0]), _p(_f32(parts, "x")), _p(_f32(parts, "y")), _p(_f32(parts, "z")),
+                    _p(np.ascontiguousarray(parts["species"], np.uint8)), _p(_f32(parts, "H")), b,
+                    C.c_int64(t.shape[0]), _p(t), C.c_int(k), C.c_float(factor), _p(Hn), _p(conv))
+    return Hn, conv.astype(bool)

@@ -945,3 +945,39 @@ void orc_drift(int64_t n, const double* box, float dt, float* x, float* y, float
         z[i] = drift1(z[i], vz[i], dt, q, (float)box[2]);
     }
 }
+
+/* Smoothing-length update (NEXT-2; DESIGN.md §2 "Sub-cycle"): for each target gas particle
+ * t, d2_(k) = the k-th smallest O2 squared distance s32 to another gas particle (brute force
+ * over every gas particle, min image, fp32 predicate arithmetic as in O2), then
+ * H' = fl32(factor * fl32(sqrt(d2_(k)))), and conv[t] = d2_(k) < fl32(H_t^2) (the GPU selects
+ * among its neighbour list, which holds every particle within H_t). */
+static int cmp_f32(const void* a, const void* b) {
+    const float x = *(const float*)a, y = *(const float*)b;
+    return (x > y) - (x < y);
+}
+
+void orc_knn_h(int64_t n, const float* x, const float* y, const float* z, const uint8_t* species, const float* H,
+               const double* box, int64_t nt, const int64_t* targets, int k, float factor, float* H_out,
+               int32_t* conv) {
+#pragma omp parallel
+    {
+        float* d = (float*)malloc(sizeof(float) * (size_t)n);
+#pragma omp for schedule(dynamic, 4)
+        for (int64_t q = 0; q < nt; ++q) {
+            const int64_t i = targets[q];
+            int64_t m = 0;
+            for (int64_t j = 0; j < n; ++j) {
+                if (j == i || species[j] != 1) continue;
+                const double dx = min_image(x[j], x[i], box[0]);
+                const double dy = min_image(y[j], y[i], box[1]);
+                const double dz = min_image(z[j], z[i], box[2]);
+                d[m++] = s32_of(dx, dy, dz);
+            }
+            qsort(d, (size_t)m, sizeof(float), cmp_f32);
+            const float d2 = m >= k ? d[k - 1] : INFINITY;
+            H_out[q] = factor * sqrtf(d2);
+            conv[q] = d2 < h2_of(H[i]);
+        }
+        free(d);
+    }
+}

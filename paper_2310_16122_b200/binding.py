@@ -21,7 +21,7 @@ EXPORTS = ["crk_create", "crk_destroy", "crk_build_lists", "crk_gravity_kick", "
            "crk_corrections", "crk_extras", "crk_corrections_extras", "crk_hydro_accel_dudt", "crk_count_pairs",
            "crk_list_view", "crk_launch_count", "crk_status_string", "crk_last_error", "crk_select_cells", "crk_select_gas",
            "crk_pack_particles", "crk_unpack_particles", "crk_pack_gas", "crk_unpack_gas", "crk_courant_dt",
-           "crk_kick", "crk_drift"]
+           "crk_kick", "crk_drift", "crk_update_h"]
 
 
 class CrkError(RuntimeError):
@@ -83,6 +83,7 @@ def lib():
         L.crk_courant_dt.argtypes = [vp, C.POINTER(CrkParticles), C.c_float, C.c_float, vp, vp]
         for f in ("crk_kick", "crk_drift"):
             getattr(L, f).argtypes = [vp, C.POINTER(CrkParticles), C.c_float, vp]
+        L.crk_update_h.argtypes = [vp, C.POINTER(CrkParticles), C.c_int32, C.c_float, vp, vp, vp]
         L.crk_list_view.argtypes = [vp, C.POINTER(CrkLists)]
         L.crk_launch_count.argtypes = [vp]
         L.crk_launch_count.restype = C.c_int64
@@ -100,7 +101,7 @@ def lib():
         for f in ("crk_create", "crk_destroy", "crk_build_lists", "crk_gravity_kick", "crk_geometry",
                   "crk_corrections", "crk_extras", "crk_corrections_extras", "crk_hydro_accel_dudt",
                   "crk_count_pairs", "crk_list_view", "crk_select_cells", "crk_select_gas", "crk_pack_particles", "crk_unpack_particles",
-                  "crk_pack_gas", "crk_unpack_gas", "crk_courant_dt", "crk_kick", "crk_drift"):
+                  "crk_pack_gas", "crk_unpack_gas", "crk_courant_dt", "crk_kick", "crk_drift", "crk_update_h"):
             getattr(L, f).restype = C.c_int
         _lib = L
     return _lib
@@ -289,6 +290,28 @@ class Solver:
 
     def drift(self, parts, dt, stream=None):
         self._call(lib().crk_drift, parts, C.c_float(dt), stream=stream)
+
+    def update_h(self, parts, k_ngb=64, factor=1.01, stream=None):
+        """H' from the k-th nearest gas neighbour among the lists (crk_update_h), after
+        geometry.  Returns (H' as a device tensor in sorted order, number unconverged); syncs."""
+        H_out = parts.H.clone()
+        nu = torch.zeros(1, dtype=torch.int32, device=parts.device)
+        self._call(lib().crk_update_h, parts, C.c_int32(k_ngb), C.c_float(factor), C.c_void_p(H_out.data_ptr()),
+                   C.c_void_p(nu.data_ptr()), stream=stream)
+        return H_out, int(nu.item())
+
+    def adapt_h(self, parts, k_ngb=64, factor=1.01, max_iter=8, stream=None):
+        """Iterate build -> geometry -> update_h until every gas particle's k-th neighbour
+        lies inside its H (then H = factor x the k-th neighbour distance exactly).  Returns
+        the number of iterations."""
+        for it in range(1, max_iter + 1):
+            self.build_lists(parts, stream)
+            self.geometry(parts, stream)
+            H_new, nu = self.update_h(parts, k_ngb, factor, stream)
+            parts.H.copy_(H_new)
+            if nu == 0:
+                return it
+        raise RuntimeError(f"H did not converge in {max_iter} iterations")
 
     def kdk(self, parts, n_steps, c_cfl=0.25, c_acc=0.25, stream=None):
         """Kick-drift-kick leapfrog over n_steps sub-cycles, each with the time step of

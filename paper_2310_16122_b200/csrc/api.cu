@@ -17,6 +17,7 @@ crk_status geometry(crk_ctx* c, crk_particles* p, cudaStream_t st);
 crk_status corrections(crk_ctx* c, crk_particles* p, cudaStream_t st);
 crk_status extras(crk_ctx* c, crk_particles* p, cudaStream_t st);
 crk_status corrections_extras(crk_ctx* c, crk_particles* p, cudaStream_t st);
+crk_status update_h(crk_ctx* c, int kth, float factor, float* H_out, int32_t* n_unconverged, cudaStream_t st);
 crk_status accel_dudt(crk_ctx* c, crk_particles* p, float dt, cudaStream_t st);
 crk_status hydro_count(crk_ctx* c, int32_t* cgather, int32_t* csym, cudaStream_t st);
 
@@ -264,6 +265,15 @@ crk_status crk_corrections_extras(crk_ctx* c, crk_particles* p, void* stream) {
     CRK_TRY(corrections_extras(c, p, (cudaStream_t)stream));
     c->stage = ST_EXT;
     return CRK_OK;
+}
+
+crk_status crk_update_h(crk_ctx* c, crk_particles* p, int32_t k_ngb, float factor, float* H_out,
+                        int32_t* n_unconverged, void* stream) {
+    CRK_TRY(check_parts(c, p, true));
+    if (c->stage < ST_GEO) return fail(c, CRK_ESTATE, "call crk_geometry first (it builds the neighbour lists)");
+    if (k_ngb < 1 || k_ngb > 127 || !(factor > 0.f) || !H_out || !n_unconverged)
+        return fail(c, CRK_EINVAL, "k_ngb in [1, 127], factor > 0, H_out and n_unconverged required");
+    return update_h(c, k_ngb, factor, H_out, n_unconverged, (cudaStream_t)stream);
 }
 
 crk_status crk_hydro_accel_dudt(crk_ctx* c, crk_particles* p, float dt, void* stream) {

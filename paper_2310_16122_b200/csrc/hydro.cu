@@ -762,6 +762,66 @@ __global__ void k_acc_finish(int64_t ng, const float4* __restrict__ acc, const i
     }
 }
 
+// ============================================================== smoothing-length update (NEXT-2)
+// H_i' = factor * sqrt(d2_(k)), d2_(k) the k-th smallest s32 (the O2 fp32 squared distance)
+// to another gas particle, selected among i's neighbour list.  The list holds every gas j
+// with s32 < H_i^2, so the selection is exact when d2_(k) < H_i^2; otherwise (the k-th
+// neighbour moved out, or fewer than k entries) H_i' is an upper bound / a doubling and i
+// is counted as unconverged: rebuild the lists with H' and update again.
+__global__ void __launch_bounds__(64) k_update_h(RowView rv, ListView lv, const float4* __restrict__ gpos,
+                                                 const int32_t* __restrict__ gas_idx, int kth, float factor,
+                                                 float* H_out, int* n_unconverged) {
+    const int a = blockIdx.x;
+    const int ii = threadIdx.x;
+    const int icount = rv.icount[a];
+    if (ii >= icount) return;
+    const int ki = rv.ifirst[a] + ii;
+    const int rbeg = rv.row_off[a];
+    const float4 pi = gpos[ki];
+    const float h2i = __fmul_rn(pi.w, pi.w);
+    const int ntrue = lv.ncnt[ki];
+    const bool row_lists = (rv.row_off[a + 1] - rbeg) * JMAX <= 65536;  // longer rows have no lists
+    const int nl = row_lists ? min(ntrue, lv.cap) : 0;
+    const uint16_t* L = lv.nbr + (int64_t)ki * lv.cap;
+    float d2[128];
+    int m = 0;
+    for (int p = 0; p < nl && m < 128; ++p) {
+        const int t = L[p];
+        int first, count, leaf, code;
+        unpack_entry(__ldg(rv.erec + rbeg + t / JMAX), first, count, leaf, code);
+        const int j = first + t % JMAX;
+        if (j == ki) continue;
+        int sx, sy, sz;
+        decode_shift(code, sx, sy, sz);
+        const float4 pj = gpos[j];
+        const float dx = (pj.x + (float)sx * rv.L[0]) - pi.x;  // exact (O1)
+        const float dy = (pj.y + (float)sy * rv.L[1]) - pi.y;
+        const float dz = (pj.z + (float)sz * rv.L[2]) - pi.z;
+        d2[m++] = s32_of(dx, dy, dz);
+    }
+    float sel = INFINITY;
+    for (int c = 0; c < m; ++c) {  // the k-th smallest: #{< v} < k <= #{<= v}
+        const float v = d2[c];
+        int lt = 0, le = 0;
+        for (int e = 0; e < m; ++e) {
+            lt += d2[e] < v;
+            le += d2[e] <= v;
+        }
+        if (lt < kth && kth <= le) { sel = v; break; }
+    }
+    // exact iff the list is complete and the k-th neighbour lies inside H_i; a truncated list
+    // gives an upper bound (its k-th is >= the true one); too few entries grow H (volume x2),
+    // a row without lists shrinks it
+    const bool complete = row_lists && ntrue <= lv.cap;
+    const bool exact = complete && sel < h2i;
+    float Hn;
+    if (!row_lists) Hn = 0.9f * pi.w;
+    else if (sel < INFINITY) Hn = __fmul_rn(factor, __fsqrt_rn(sel));
+    else Hn = 1.26f * pi.w;
+    if (!exact) atomicAdd(n_unconverged, 1);
+    H_out[gas_idx[ki]] = Hn;
+}
+
 // ============================================================== launches
 static RowView hydro_rows(crk_ctx* c) {
     RowView rv;
@@ -1044,6 +1104,15 @@ crk_status hydro_count(crk_ctx* c, int32_t* cgather, int32_t* csym, cudaStream_t
     a.grec = nullptr;
     a.cnt = csym;
     return launch_hyd<AccPass<true>, 128>(c, a, st, "sym count kernel");
+}
+
+crk_status update_h(crk_ctx* c, int kth, float factor, float* H_out, int32_t* n_unconverged, cudaStream_t st) {
+    if (!lists_on(c)) return fail(c, CRK_ESTATE, "update_h needs the neighbour lists (CRK_NBR_CAP > 0)");
+    CRK_TRY(cuda_check(c, zero_async(n_unconverged, sizeof(int32_t), st, c), "memset"));
+    k_update_h<<<(unsigned)c->nleaf[2], 64, 0, st>>>(hydro_rows(c), list_view(c), P<float4>(c->gpos),
+                                                     P<int32_t>(c->gas_idx), kth, factor, H_out, n_unconverged);
+    CRK_LAUNCHED(c, "update H");
+    return CRK_OK;
 }
 
 }  // namespace crk

@@ -196,3 +196,104 @@ def test_gpu_kdk_two_steps_matches_oracle():
     assert np.max(np.abs(v_gpu - v_ref)) <= 1e-4 * dv0 + 1e-6 * np.abs(v_ref).max()
     du0 = np.abs(st["u"] - parts["u"]).max()
     assert np.max(np.abs(h["u"][g] - st["u"])) <= 1e-4 * du0 + 1e-6 * np.abs(st["u"]).max()
+
+
+# ----------------------------------------------------------------- smoothing-length update
+def _lattice_gas(n=16):
+    from gen.configs import make_params
+
+    g = (np.arange(n) + 0.75).astype(np.float64)
+    X, Y, Z = np.meshgrid(g, g, g, indexing="ij")
+    N = n ** 3
+    parts = dict(x=X.ravel().astype(np.float32), y=Y.ravel().astype(np.float32), z=Z.ravel().astype(np.float32),
+                 vx=np.zeros(N, np.float32), vy=np.zeros(N, np.float32), vz=np.zeros(N, np.float32),
+                 m=np.ones(N, np.float32), species=np.ones(N, np.uint8), id=np.arange(N, dtype=np.int64),
+                 H=np.full(N, 2.6, np.float32), u=np.ones(N, np.float32))
+    return parts, make_params([float(n)] * 3)
+
+
+def test_knn_h_lattice_shells():
+    """Unit lattice: shells of 6, 12, 8, 6, 24, 24 points at d^2 = 1..6, so the 64th
+    neighbour is on the d^2 = 6 shell (56 closer) and the 6th on the d^2 = 1 shell."""
+    parts, params = _lattice_gas()
+    t = np.array([0, 123, 4000])
+    Hn, conv = oracle.knn_h(parts, params, t, k=64, factor=1.01)
+    assert np.all(Hn == np.float32(1.01) * np.sqrt(np.float32(6.0)))
+    assert np.all(conv)  # 6 < 2.6^2
+    Hn, conv = oracle.knn_h(parts, params, t, k=6, factor=1.0)
+    assert np.all(Hn == 1.0)
+    Hn, conv = oracle.knn_h(parts, params, t, k=57, factor=1.0)
+    assert np.all(Hn == np.sqrt(np.float32(6.0)))
+    # a smaller H puts the 64th neighbour outside: not converged
+    parts["H"][:] = 2.0
+    Hn, conv = oracle.knn_h(parts, params, t, k=64, factor=1.01)
+    assert not np.any(conv)
+
+
+def test_knn_h_matches_numpy_ranking():
+    """Random gas: the oracle's k-th distance agrees with an fp64 numpy ranking."""
+    from gen.configs import make_params, quantise
+
+    rng = np.random.default_rng(9)
+    n, L = 600, 8.0
+    pos = quantise(rng.random((n, 3)) * L, [L] * 3)
+    parts = dict(x=pos[:, 0].copy(), y=pos[:, 1].copy(), z=pos[:, 2].copy(), species=np.ones(n, np.uint8),
+                 H=np.full(n, 1.5, np.float32))
+    params = make_params([L] * 3)
+    t = np.arange(0, n, 37)
+    Hn, _ = oracle.knn_h(parts, params, t, k=20, factor=1.0)
+    p = pos.astype(np.float64)
+    for q, i in enumerate(t):
+        d = p - p[i]
+        d -= L * np.round(d / L)
+        r = np.sort(np.sqrt((d * d).sum(1)))[1:]  # drop self
+        assert abs(float(Hn[q]) - r[19]) <= 2e-6 * r[19]
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("name,scale", [("c1", 1.0), ("c1", 0.85), ("c2z", 1.0)])
+def test_gpu_update_h(name, scale):
+    """crk_update_h after geometry: converged particles bit-exact with the oracle's kNN,
+    the unconverged count equal to the oracle's."""
+    import torch
+    from paper_2310_16122_b200 import Particles, Solver
+
+    parts, params = cached_config(name)
+    parts["H"] = (parts["H"] * np.float32(scale)).astype(np.float32)
+    p = Particles.from_host(parts, "cuda")
+    s = Solver(params, 0)
+    s.build_lists(p)
+    s.geometry(p)
+    Hn, nu = s.update_h(p, 64, 1.01)
+    torch.cuda.synchronize()
+    h = p.to_host(["perm", "species"])
+    Hg = np.empty_like(parts["H"])
+    Hg[h["perm"].astype(np.int64)] = Hn.cpu().numpy()
+    gas = np.nonzero(parts["species"] == 1)[0]
+    t = gas if name == "c1" else np.sort(np.random.default_rng(2).choice(gas, 300, replace=False))
+    Hr, conv = oracle.knn_h(parts, params, t, 64, 1.01)
+    assert np.array_equal(Hg[t][conv], Hr[conv])
+    if name == "c1":
+        assert nu == int((~conv).sum())
+    s.close()
+
+
+@pytest.mark.gpu
+def test_gpu_adapt_h_converges_to_knn():
+    """Starting from H x 0.8 (most 64th neighbours outside H), build -> geometry -> update_h
+    iterations converge, and the final H is the oracle's kNN value for every sampled particle."""
+    from paper_2310_16122_b200 import Particles, Solver
+
+    parts, params = cached_config("c2z")
+    parts["H"] = (parts["H"] * np.float32(0.8)).astype(np.float32)
+    p = Particles.from_host(parts, "cuda")
+    s = Solver(params, 0)
+    it = s.adapt_h(p, 64, 1.01)
+    assert 2 <= it <= 4
+    h = p.to_host(["perm", "H", "x", "y", "z", "species", "id"])
+    s.close()
+    gas = np.nonzero(h["species"] == 1)[0]
+    t = np.sort(np.random.default_rng(4).choice(gas, 200, replace=False))
+    sorted_parts = {k: h[k] for k in ("x", "y", "z", "species", "H")}
+    Hr, _ = oracle.knn_h(sorted_parts, params, t, 64, 1.01)
+    assert np.array_equal(h["H"][t], Hr)
