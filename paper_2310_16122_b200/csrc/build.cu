@@ -62,19 +62,16 @@ __global__ void k_tie_fix(int64_t n, const uint32_t* __restrict__ keys, int32_t*
 }
 
 // ---------------------------------------------------------------- permute (one gather pass)
-__global__ void k_copy_i32(int64_t n, const int32_t* __restrict__ src, int32_t* __restrict__ dst) {
-    const int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
-    if (i < n) dst[i] = src[i];
-}
 
 // gather the packed records in sorted order straight into the caller's arrays (the records
 // are a copy, so this is safe in place) and derive xm, gas flags and cell runs
 __global__ void k_permute(int64_t n, const int32_t* __restrict__ perm, const float4* __restrict__ rec, SoA dst,
                           const uint32_t* __restrict__ keys, int fbits, float4* xm, int32_t* gflag, int32_t* cstart,
-                          int32_t* cend) {
+                          int32_t* cend, int32_t* perm_out) {
     const int64_t k = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
     if (k >= n) return;
     const int64_t s = perm[k];
+    if (perm_out) perm_out[k] = (int32_t)s;
     const float4 r0 = __ldg(rec + 3 * s), r1 = __ldg(rec + 3 * s + 1), r2 = __ldg(rec + 3 * s + 2);
     dst.f[0][k] = r0.x; dst.f[1][k] = r0.y; dst.f[2][k] = r0.z; dst.f[3][k] = r0.w;
     dst.f[4][k] = r1.x; dst.f[5][k] = r1.y; dst.f[6][k] = r1.z; dst.f[7][k] = r1.w;
@@ -507,16 +504,12 @@ crk_status build_lists(crk_ctx* c, crk_particles* p, cudaStream_t st) {
     CRK_LAUNCHED(c, "tie fix");
 
     // ---- permute the caller's arrays in place: one gather of the packed records
-    if (p->perm) {  // a kernel, not a copy-engine memcpy (see zero_async)
-        k_copy_i32<<<nblk(n, 256), 256, 0, st>>>(n, perm, p->perm);
-        CRK_LAUNCHED(c, "perm copy");
-    }
     CRK_TRY(cuda_check(c, zero_async(c->cell_start.p, L.ncm * 4, st, c), "memset"));
     CRK_TRY(cuda_check(c, zero_async(c->cell_end.p, L.ncm * 4, st, c), "memset"));
     CRK_TRY(cuda_check(c, zero_async(P<int32_t>(c->gflag) + n, 4, st, c), "memset"));
     CRK_TRY(cuda_check(c, zero_async(c->dev_scalars.p, 64, st, c), "memset"));
     k_permute<<<nblk(n, 256), 256, 0, st>>>(n, perm, rec, in, keys, L.fbits, P<float4>(c->xm), P<int32_t>(c->gflag),
-                                            P<int32_t>(c->cell_start), P<int32_t>(c->cell_end));
+                                            P<int32_t>(c->cell_start), P<int32_t>(c->cell_end), p->perm);
     CRK_LAUNCHED(c, "permute");
 
     // ---- gas ranks
