@@ -67,6 +67,11 @@ typedef struct crk_params {
                                       only for owned cells; particles in other cells are ghosts
                                       (j-side only: gravity evaluates a pair with a ghost in
                                       the owner's group and drops the reaction). */
+    float skin;          /* list skin (grid units, >= 0, < cell_side; whole-box domains only): the
+                            leaf-pair lists are built with cutoffs r_c + skin and max H + skin, and
+                            after crk_drift steps totalling less than skin/2 per particle
+                            crk_refresh renews the position-dependent data without re-sorting or
+                            rebuilding the lists.  0 = off. */
 } crk_params;
 
 /* Caller-owned particle arrays (device pointers).  Inputs are sorted IN PLACE by
@@ -170,8 +175,21 @@ crk_status crk_kick(struct crk_ctx* ctx, crk_particles* parts, float dt, void* s
 
 /* Drift: x' = fl32(x + dt v) rounded to the nearest multiple of q (ties to even) and
  * wrapped into [0, box) — positions stay on the q lattice (O1).  Requires |dt v| < box/2.
- * Invalidates the lists: call crk_build_lists before the next force pass (CRK_ESTATE). */
+ * Invalidates the lists: call crk_build_lists (or, with a skin, crk_refresh) before the next
+ * force pass (CRK_ESTATE).  With skin > 0 and lists built, positions are NOT wrapped (they
+ * may leave [0, box) by < skin/2; crk_build_lists wraps them) and the drift's largest
+ * displacement is added to the displacement bound checked by crk_refresh. */
 crk_status crk_drift(struct crk_ctx* ctx, crk_particles* parts, float dt, void* stream);
+
+/* Skin refresh (skin > 0): after crk_drift steps whose displacement bound is < skin/2,
+ * renew the position-dependent data (packed positions, leaf boxes, list entry boxes) of
+ * the lists built by the last crk_build_lists, keeping the order, leaves and lists: every
+ * pair within r_c (or max H) now was within r_c + skin (max H + skin) at the build, so the
+ * lists are still supersets and every force pass gives the same results as after a
+ * rebuild (same pair terms; the order of summation may differ).  Synchronises `stream`
+ * (reads the bound).  CRK_ESTATE if there are no skin lists or the bound is >= skin/2
+ * (rebuild).  H must be unchanged since the build. */
+crk_status crk_refresh(struct crk_ctx* ctx, crk_particles* parts, void* stream);
 
 /* Smoothing-length update (NEXT-2 H adaptation), after crk_geometry: for every gas
  * particle H_out[i] = factor * sqrt(d2_(k)) (fp32 sqrt and product, correctly rounded),

@@ -21,7 +21,7 @@ EXPORTS = ["crk_create", "crk_destroy", "crk_build_lists", "crk_gravity_kick", "
            "crk_corrections", "crk_extras", "crk_corrections_extras", "crk_hydro_accel_dudt", "crk_count_pairs",
            "crk_list_view", "crk_launch_count", "crk_status_string", "crk_last_error", "crk_select_cells", "crk_select_gas",
            "crk_pack_particles", "crk_unpack_particles", "crk_pack_gas", "crk_unpack_gas", "crk_courant_dt",
-           "crk_kick", "crk_drift", "crk_update_h"]
+           "crk_kick", "crk_drift", "crk_update_h", "crk_refresh"]
 
 
 class CrkError(RuntimeError):
@@ -40,6 +40,7 @@ class CrkParams(C.Structure):
         ("cell_side", C.c_double),
         ("symmetric", C.c_int32),
         ("dom_lo", C.c_int32 * 3), ("dom_hi", C.c_int32 * 3),
+        ("skin", C.c_float),
     ]
 
 
@@ -75,7 +76,8 @@ def lib():
         vp = C.c_void_p
         L.crk_create.argtypes = [C.POINTER(CrkParams), C.c_int, C.POINTER(vp)]
         L.crk_destroy.argtypes = [vp]
-        for f in ("crk_build_lists", "crk_geometry", "crk_corrections", "crk_extras", "crk_corrections_extras"):
+        for f in ("crk_build_lists", "crk_geometry", "crk_corrections", "crk_extras", "crk_corrections_extras",
+                  "crk_refresh"):
             getattr(L, f).argtypes = [vp, C.POINTER(CrkParticles), vp]
         for f in ("crk_gravity_kick", "crk_hydro_accel_dudt"):
             getattr(L, f).argtypes = [vp, C.POINTER(CrkParticles), C.c_float, vp]
@@ -101,7 +103,8 @@ def lib():
         for f in ("crk_create", "crk_destroy", "crk_build_lists", "crk_gravity_kick", "crk_geometry",
                   "crk_corrections", "crk_extras", "crk_corrections_extras", "crk_hydro_accel_dudt",
                   "crk_count_pairs", "crk_list_view", "crk_select_cells", "crk_select_gas", "crk_pack_particles", "crk_unpack_particles",
-                  "crk_pack_gas", "crk_unpack_gas", "crk_courant_dt", "crk_kick", "crk_drift", "crk_update_h"):
+                  "crk_pack_gas", "crk_unpack_gas", "crk_courant_dt", "crk_kick", "crk_drift", "crk_update_h",
+                  "crk_refresh"):
             getattr(L, f).restype = C.c_int
         _lib = L
     return _lib
@@ -118,6 +121,7 @@ def params_struct(p: dict) -> CrkParams:
     s.symmetric = int(p.get("symmetric", 1))
     s.dom_lo[:] = list(p.get("dom_lo", (0, 0, 0)))
     s.dom_hi[:] = list(p.get("dom_hi", (0, 0, 0)))
+    s.skin = float(p.get("skin", 0.0))
     return s
 
 
@@ -290,6 +294,10 @@ class Solver:
 
     def drift(self, parts, dt, stream=None):
         self._call(lib().crk_drift, parts, C.c_float(dt), stream=stream)
+
+    def refresh(self, parts, stream=None):
+        """Renew the position-dependent data of the skin lists (crk_refresh); syncs."""
+        self._call(lib().crk_refresh, parts, stream=stream)
 
     def update_h(self, parts, k_ngb=64, factor=1.01, stream=None):
         """H' from the k-th nearest gas neighbour among the lists (crk_update_h), after

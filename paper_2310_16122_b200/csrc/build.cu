@@ -264,7 +264,15 @@ struct ListArgs {
     int2* erec;
     const float4* box8B;    // padded j-leaf boxes (lo, max H^2), (hi, 0)
     float4* ebox;           // gravity only (else null): per entry (lo + shift, first), (hi + shift, count | code << 8)
+    double skin;            // list skin: cutoffs sqrt(cut2) + skin (0: the exact O4 lists)
 };
+
+// cut^2 of the O4 test with the skin: (sqrt(cut2) + skin)^2 (the plain cut2 without one)
+__device__ __forceinline__ double skin_cut2(double cut2, double skin) {
+    if (skin <= 0.0) return cut2;
+    const double c = sqrt(cut2) + skin;
+    return c * c;
+}
 
 __device__ __forceinline__ void put_entry(const ListArgs& A, int p, int b, int code) {
     A.col[p] = b;
@@ -299,6 +307,7 @@ __global__ void __launch_bounds__(LIST_WARPS * 32, 5) k_lists(ListArgs A) {
     double reach2;
     if (A.mode == 0) reach2 = (double)A.rcut2;
     else reach2 = fmax((double)A.maxh2A[a], (double)*A.dmax_h2);
+    reach2 = skin_cut2(reach2, A.skin);
     const double reach = sqrt(reach2 * slack) * (1.0 + 1e-12) + 1e-12;
     int c0[3], c1[3];
     bool generic = false;
@@ -377,7 +386,7 @@ __global__ void __launch_bounds__(LIST_WARPS * 32, 5) k_lists(ListArgs A) {
                         K += (uint64_t)k * k;
                     }
                     const float cut2 = A.mode == 0 ? A.rcut2 : fmaxf(mh2a, blo.w);
-                    keep = (double)K < (double)cut2 * A.q2inv_slack;
+                    keep = (double)K < skin_cut2((double)cut2, A.skin) * A.q2inv_slack;
                 }
                 const unsigned msk = __ballot_sync(0xffffffffu, keep);
                 if (FILL && keep) put_entry(A, outpos + __popc(msk & ((1u << lane) - 1u)), b, cd);
@@ -402,7 +411,8 @@ __global__ void __launch_bounds__(LIST_WARPS * 32, 5) k_lists(ListArgs A) {
                         if (b < b1) {
                             const double cut2 = A.mode == 0 ? (double)A.rcut2
                                                             : fmax((double)mh2a, (double)A.maxh2B[b]);
-                            keep = leaf_pair_test(ba, A.bboxB + 6 * (int64_t)b, A.L, cut2 * slack, code);
+                            keep = leaf_pair_test(ba, A.bboxB + 6 * (int64_t)b, A.L, skin_cut2(cut2, A.skin) * slack,
+                                                  code);
                         }
                         const unsigned msk = __ballot_sync(0xffffffffu, keep);
                         if (FILL && keep) put_entry(A, outpos + __popc(msk & ((1u << lane) - 1u)), b, code);
@@ -447,7 +457,99 @@ static ListArgs list_args(crk_ctx* c, int m) {
     A.erec = P<int2>(c->erec[m]);
     A.box8B = P<float4>(c->lbox8[sb]);
     A.ebox = m == 0 ? P<float4>(c->gebox) : nullptr;
+    A.skin = c->prm.skin;
     return A;
+}
+
+// per-leaf boxes of leaf set s from the packed positions (xm: gravity sets, gpos: gas sets)
+static crk_status leaf_boxes(crk_ctx* c, int s, cudaStream_t st) {
+    if (c->nleaf[s] > 0 && (s == 0 || s == 2)) {
+        k_leaf_bbox_warp<<<nblk(c->nleaf[s] * 32, 256), 256, 0, st>>>(
+            c->nleaf[s], P<int32_t>(c->lfirst[s]), P<int32_t>(c->lcount[s]),
+            s < 2 ? P<float4>(c->xm) : P<float4>(c->gpos), s >= 2, P<float>(c->lbbox[s]),
+            s >= 2 ? P<float>(c->lmaxh2[s]) : nullptr, P<float4>(c->lbox8[s]));
+        CRK_LAUNCHED(c, "leaf bbox");
+    } else if (c->nleaf[s] > 0) {
+        k_leaf_bbox<<<nblk(c->nleaf[s], 128), 128, 0, st>>>(
+            c->nleaf[s], P<int32_t>(c->lfirst[s]), P<int32_t>(c->lcount[s]),
+            s < 2 ? P<float4>(c->xm) : P<float4>(c->gpos), s >= 2, P<float>(c->lbbox[s]),
+            s >= 2 ? P<float>(c->lmaxh2[s]) : nullptr, P<float4>(c->lbox8[s]));
+        CRK_LAUNCHED(c, "leaf bbox");
+    }
+    return CRK_OK;
+}
+
+// ---------------------------------------------------------------- skin refresh (NEXT-2)
+// positions may have left [0, L) by < skin/2 after unwrapped drifts: wrap them (exact)
+__global__ void k_wrap(int64_t n, float* x, float* y, float* z, float Lx, float Ly, float Lz) {
+    const int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+    if (i >= n) return;
+    float* c[3] = {x, y, z};
+    const float L[3] = {Lx, Ly, Lz};
+#pragma unroll
+    for (int a = 0; a < 3; ++a) {
+        float v = c[a][i];
+        if (v >= L[a]) c[a][i] = v - L[a];
+        else if (v < 0.f) c[a][i] = v + L[a];
+    }
+}
+
+__global__ void k_repack(int64_t n, const float* __restrict__ x, const float* __restrict__ y,
+                         const float* __restrict__ z, const float* __restrict__ m, float4* xm) {
+    const int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+    if (i < n) xm[i] = make_float4(x[i], y[i], z[i], m[i]);
+}
+
+__global__ void k_repack_gas(int64_t ng, const int32_t* __restrict__ gas_idx, const float4* __restrict__ xm,
+                             const float* __restrict__ H, float4* gpos) {
+    const int64_t g = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+    if (g >= ng) return;
+    const int32_t i = gas_idx[g];
+    const float4 p = xm[i];
+    gpos[g] = make_float4(p.x, p.y, p.z, H[i]);
+}
+
+// gravity list entry records from the (refreshed) j-leaf boxes, as the list fill writes them
+__global__ void k_entry_boxes(int64_t ne, const int2* __restrict__ erec, const float4* __restrict__ box8, float Lx,
+                              float Ly, float Lz, float4* ebox) {
+    const int64_t p = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+    if (p >= ne) return;
+    const int2 r = erec[p];
+    const int first = r.x & 0x1fffffff, count = ((unsigned)r.x >> 29) + 1;
+    const int b = r.y & 0x03ffffff, code = (unsigned)r.y >> 26;
+    const float ox = (float)(code % 3 - 1) * Lx, oy = (float)((code / 3) % 3 - 1) * Ly, oz = (float)(code / 9 - 1) * Lz;
+    const float4 bl = box8[2 * (int64_t)b], bh = box8[2 * (int64_t)b + 1];
+    ebox[2 * p] = make_float4(bl.x + ox, bl.y + oy, bl.z + oz, __int_as_float(first));
+    ebox[2 * p + 1] = make_float4(bh.x + ox, bh.y + oy, bh.z + oz, __int_as_float(count | (code << 8)));
+}
+
+crk_status refresh(crk_ctx* c, crk_particles* p, cudaStream_t st) {
+    volatile float* host = reinterpret_cast<float*>(P<char>(c->pinned) + 192);
+    Readback rb;
+    rb.add(P<float>(c->disp) + 1, 192, 4);
+    CRK_TRY(readback(c, rb, st));
+    CRK_TRY(cuda_check(c, cudaStreamSynchronize(st), "sync"));
+    if (!(*host < 0.5f * c->prm.skin)) {
+        c->skin_lists = false;
+        return fail(c, CRK_ESTATE, "the displacement since the build reached skin/2: call crk_build_lists");
+    }
+    const int64_t n = c->n;
+    k_repack<<<nblk(n, 256), 256, 0, st>>>(n, p->x, p->y, p->z, p->m, P<float4>(c->xm));
+    CRK_LAUNCHED(c, "repack");
+    if (c->n_gas > 0) {
+        k_repack_gas<<<nblk(c->n_gas, 256), 256, 0, st>>>(c->n_gas, P<int32_t>(c->gas_idx), P<float4>(c->xm), p->H,
+                                                           P<float4>(c->gpos));
+        CRK_LAUNCHED(c, "repack gas");
+    }
+    for (int s = 0; s < 4; ++s) CRK_TRY(leaf_boxes(c, s, st));
+    if (c->nent[0] > 0) {
+        k_entry_boxes<<<nblk(c->nent[0], 256), 256, 0, st>>>(c->nent[0], P<int2>(c->erec[0]), P<float4>(c->lbox8[1]),
+                                                             c->lay.L[0], c->lay.L[1], c->lay.L[2],
+                                                             P<float4>(c->gebox));
+        CRK_LAUNCHED(c, "entry boxes");
+    }
+    c->stage = ST_LISTS;  // the displacement bound keeps accumulating until the next build
+    return CRK_OK;
 }
 
 crk_status build_lists(crk_ctx* c, crk_particles* p, cudaStream_t st) {
@@ -472,6 +574,10 @@ crk_status build_lists(crk_ctx* c, crk_particles* p, cudaStream_t st) {
     CRK_TRY(grow(c, c->gas_idx, n * 4, st));
     CRK_TRY(grow(c, c->gpos, n * 16, st));
     if (n == 0) return fail(c, CRK_EINVAL, "no particles");
+    if (c->prm.skin > 0.f) {  // positions may lie outside the box by < skin/2 after unwrapped drifts
+        k_wrap<<<nblk(n, 256), 256, 0, st>>>(n, p->x, p->y, p->z, L.L[0], L.L[1], L.L[2]);
+        CRK_LAUNCHED(c, "wrap");
+    }
 
     // ---- keys + sort (32-bit keys, 3 (cbits + fbits) significant bits)
     SoA in;
@@ -560,19 +666,7 @@ crk_status build_lists(crk_ctx* c, crk_particles* p, cudaStream_t st) {
                                                       dom, P<int32_t>(c->lfirst[s]), P<int32_t>(c->lcount[s]),
                                                       P<uint64_t>(c->lcell[s]));
         CRK_LAUNCHED(c, "leaf fill");
-        if (c->nleaf[s] > 0 && (s == 0 || s == 2)) {
-            k_leaf_bbox_warp<<<nblk(c->nleaf[s] * 32, 256), 256, 0, st>>>(
-                c->nleaf[s], P<int32_t>(c->lfirst[s]), P<int32_t>(c->lcount[s]),
-                s < 2 ? P<float4>(c->xm) : P<float4>(c->gpos), s >= 2, P<float>(c->lbbox[s]),
-                s >= 2 ? P<float>(c->lmaxh2[s]) : nullptr, P<float4>(c->lbox8[s]));
-            CRK_LAUNCHED(c, "leaf bbox");
-        } else if (c->nleaf[s] > 0) {
-            k_leaf_bbox<<<nblk(c->nleaf[s], 128), 128, 0, st>>>(
-                c->nleaf[s], P<int32_t>(c->lfirst[s]), P<int32_t>(c->lcount[s]),
-                s < 2 ? P<float4>(c->xm) : P<float4>(c->gpos), s >= 2, P<float>(c->lbbox[s]),
-                s >= 2 ? P<float>(c->lmaxh2[s]) : nullptr, P<float4>(c->lbox8[s]));
-            CRK_LAUNCHED(c, "leaf bbox");
-        }
+        CRK_TRY(leaf_boxes(c, s, st));
     }
 
     // ---- lists: count, scan, fill
@@ -626,6 +720,11 @@ crk_status build_lists(crk_ctx* c, crk_particles* p, cudaStream_t st) {
         CRK_TRY(grow(c, c->ncnt, (size_t)ng * sizeof(int32_t) + 64, st));  // + pad: 16-byte-aligned bulk reads
         CRK_TRY(grow(c, c->lflag, (size_t)(2 * c->nleaf[2] + 1) * sizeof(int32_t), st));
     }
+    if (c->prm.skin > 0.f) {
+        CRK_TRY(grow(c, c->disp, 16, st));
+        CRK_TRY(cuda_check(c, zero_async(c->disp.p, 16, st, c), "memset"));
+    }
+    c->skin_lists = c->prm.skin > 0.f;
     c->stage = ST_LISTS;
     return CRK_OK;
 }

@@ -85,4 +85,7 @@ struct crk_ctx {
     // gas neighbour lists (geometry -> corrections, extras, accel): pairs.cuh ListView
     crk::Buf nbr, ncnt, lflag;
     int nbr_cap = 0;             // entries per gas particle (0: lists off)
+    // skin lists (crk_params.skin > 0): valid lists survive drifts until crk_refresh
+    bool skin_lists = false;     // the last build used the skin and no rebuild is due
+    crk::Buf disp;               // device floats: [0] this drift's max |dt v|, [1] bound since the build
 };

@@ -11,6 +11,8 @@
 
 namespace crk {
 
+crk_status refresh(crk_ctx* c, crk_particles* p, cudaStream_t st);  // build.cu
+
 __global__ void k_set_inf(float* dt) { *reinterpret_cast<int*>(dt) = 0x7f800000; }
 
 // dt_i = C_acc sqrt(eps / |a_i|) for every particle (a = gravity + hydro for gas) and also
@@ -61,21 +63,39 @@ __global__ void k_kick(int64_t n, const uint8_t* __restrict__ species, float dt,
 
 // x' = fl32(x + dt v) (one rounding), rounded to the nearest multiple of q (ties to even),
 // wrapped into [0, L): every op exact except the fma (q and L are powers of two)
-__device__ __forceinline__ float drift1(float x, float v, float dt, float inv_q, float q, float L) {
+__device__ __forceinline__ float drift1(float x, float v, float dt, float inv_q, float q, float L, bool wrap) {
     const float t = __fmaf_rn(dt, v, x);
     float r = __fmul_rn(rintf(__fmul_rn(t, inv_q)), q);
-    if (r >= L) r = __fsub_rn(r, L);
-    else if (r < 0.f) r = __fadd_rn(r, L);
+    if (wrap) {
+        if (r >= L) r = __fsub_rn(r, L);
+        else if (r < 0.f) r = __fadd_rn(r, L);
+    }
     return r;
 }
 
+// wrap = false (skin lists): positions may leave [0, L) by < skin/2; the largest |x' - x|
+// (fp32 Euclidean, rounded up by 1 ulp) goes to *dmax (atomicMax on the bits, >= 0)
 __global__ void k_drift(int64_t n, float dt, float inv_q, float q, float Lx, float Ly, float Lz, float* x, float* y,
-                        float* z, const float* vx, const float* vy, const float* vz) {
+                        float* z, const float* vx, const float* vy, const float* vz, bool wrap, float* dmax) {
     const int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
     if (i >= n) return;
-    x[i] = drift1(x[i], vx[i], dt, inv_q, q, Lx);
-    y[i] = drift1(y[i], vy[i], dt, inv_q, q, Ly);
-    z[i] = drift1(z[i], vz[i], dt, inv_q, q, Lz);
+    const float x0 = x[i], y0 = y[i], z0 = z[i];
+    const float x1 = drift1(x0, vx[i], dt, inv_q, q, Lx, wrap);
+    const float y1 = drift1(y0, vy[i], dt, inv_q, q, Ly, wrap);
+    const float z1 = drift1(z0, vz[i], dt, inv_q, q, Lz, wrap);
+    x[i] = x1; y[i] = y1; z[i] = z1;
+    if (!wrap) {
+        const float dx = x1 - x0, dy = y1 - y0, dz = z1 - z0;
+        const float d = nextafterf(sqrtf(fmaf(dz, dz, fmaf(dy, dy, dx * dx))), INFINITY);
+        atomicMax(reinterpret_cast<int*>(dmax), __float_as_int(d));
+    }
+}
+
+// bound since the build += this drift's largest displacement (a sum of maxima bounds every
+// particle's total displacement)
+__global__ void k_disp_accum(float* disp) {
+    disp[1] += disp[0];
+    disp[0] = 0.f;
 }
 
 }  // namespace crk
@@ -124,12 +144,25 @@ crk_status crk_drift(crk_ctx* c, crk_particles* p, float dt, void* stream) {
     if (!p->x || !p->y || !p->z || !p->vx || !p->vy || !p->vz) return fail(c, CRK_EINVAL, "drift needs x, v");
     if (p->n <= 0) return CRK_OK;
     CRK_TRY(cuda_check(c, cudaSetDevice(c->device), "cudaSetDevice"));
+    const bool skin = c->skin_lists && p->n == c->n;  // keep the skin lists: no wrap, track the displacement
     k_drift<<<nb256(p->n), 256, 0, (cudaStream_t)stream>>>(p->n, dt, c->lay.inv_q, (float)c->lay.q, c->lay.L[0],
                                                           c->lay.L[1], c->lay.L[2], p->x, p->y, p->z, p->vx, p->vy,
-                                                          p->vz);
+                                                          p->vz, !skin, skin ? P<float>(c->disp) : nullptr);
     CRK_LAUNCHED(c, "drift");
-    c->stage = ST_NONE;  // positions moved: the lists must be rebuilt
+    if (skin) {
+        k_disp_accum<<<1, 1, 0, (cudaStream_t)stream>>>(P<float>(c->disp));
+        CRK_LAUNCHED(c, "displacement bound");
+    }
+    c->stage = ST_NONE;  // positions moved: crk_build_lists (or crk_refresh with a skin) before the next pass
     return CRK_OK;
+}
+
+crk_status crk_refresh(crk_ctx* c, crk_particles* p, void* stream) {
+    if (!c || !p) return CRK_EINVAL;
+    if (!p->x || !p->y || !p->z || !p->m || !p->H || p->n != c->n) return fail(c, CRK_EINVAL, "refresh needs x, m, H");
+    if (!c->skin_lists) return fail(c, CRK_ESTATE, "no skin lists to refresh: call crk_build_lists");
+    CRK_TRY(cuda_check(c, cudaSetDevice(c->device), "cudaSetDevice"));
+    return refresh(c, p, (cudaStream_t)stream);
 }
 
 }  // extern "C"

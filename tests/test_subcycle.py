@@ -297,3 +297,69 @@ def test_gpu_adapt_h_converges_to_knn():
     sorted_parts = {k: h[k] for k in ("x", "y", "z", "species", "H")}
     Hr, _ = oracle.knn_h(sorted_parts, params, t, 64, 1.01)
     assert np.array_equal(h["H"][t], Hr)
+
+
+# ----------------------------------------------------------------- skin lists (list reuse)
+@pytest.mark.gpu
+@pytest.mark.parametrize("name", ["c1", "c2z"])
+def test_gpu_skin_refresh_matches_oracle(name):
+    """Lists built with a skin, then drifts totalling < skin/2 and crk_refresh instead of a
+    rebuild: counts exact and forces within the bar against the oracle on the drifted
+    positions; past skin/2 the refresh refuses and a rebuild restores the passes."""
+    import torch
+    from paper_2310_16122_b200 import Particles, Solver
+    from paper_2310_16122_b200.binding import CrkError
+    from crk_testutil import norm_err
+
+    parts, params = cached_config(name)
+    params["skin"] = 0.4
+    p = Particles.from_host(parts, "cuda")
+    s = Solver(params, 0)
+    s.substep(p)
+    vmag = float(np.sqrt(parts["vx"].astype(np.float64) ** 2 + parts["vy"] ** 2 + parts["vz"] ** 2).max())
+    dt = 0.09 / vmag  # each drift moves the fastest particle by 0.09 (skin/2 = 0.2)
+    L = np.array(params["box"])
+
+    def passes_and_check():
+        s.gravity_kick(p)
+        s.geometry(p)
+        s.corrections_extras(p)
+        s.hydro_accel_dudt(p)
+        torch.cuda.synchronize()
+        h = p.to_host()
+        pos_of_id = np.empty(parts["id"].shape[0], np.int64)
+        pos_of_id[parts["id"]] = np.arange(parts["id"].shape[0])
+        perm = pos_of_id[h["id"]]  # sorted position -> input index (ids survive every re-sort)
+        cur = {k: parts[k].copy() for k in parts}
+        for k in ("x", "y", "z"):
+            v = np.empty_like(parts[k])
+            v[perm] = np.mod(h[k].astype(np.float64), L["xyz".index(k)]).astype(np.float32)
+            cur[k] = v
+        cg, ch, cs = s.count_pairs(p)
+        ref_c = oracle.counts(cur, params)
+        for c, want in zip((cg, ch, cs), ("grav", "gather", "sym")):
+            got = np.empty(perm.shape[0], np.int32)
+            got[perm] = c.cpu().numpy()
+            assert np.array_equal(got, ref_c[want]), want
+        gas = np.nonzero(cur["species"] == 1)[0]
+        t = gas if name == "c1" else np.sort(np.random.default_rng(6).choice(gas, 200, replace=False))
+        ref = oracle.substep(cur, params, targets=t, grav_targets=t)
+        inv = lambda a: a[np.argsort(perm)]  # noqa: E731  sorted -> input order
+        a = np.stack([inv(h["ax"]), inv(h["ay"]), inv(h["az"])], 1)[t]
+        assert norm_err(a, ref["grav_a"], ref["grav_S"]) <= 1e-4
+        T = ref["targets"]
+        ah = np.stack([inv(h["ahx"]), inv(h["ahy"]), inv(h["ahz"])], 1)[T]
+        assert norm_err(ah, ref["a"], ref["Sa"]) <= 1e-4
+        assert norm_err(inv(h["dudt"])[T], ref["dudt"], ref["Sdu"]) <= 1e-4
+
+    passes_and_check()
+    for _ in range(2):  # 2 x 0.09 < 0.2
+        s.drift(p, dt)
+        s.refresh(p)
+        passes_and_check()
+    s.drift(p, dt)  # 0.27 >= 0.2: a refresh must refuse
+    with pytest.raises(CrkError):
+        s.refresh(p)
+    s.build_lists(p)
+    passes_and_check()
+    s.close()
