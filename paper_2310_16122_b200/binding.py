@@ -258,11 +258,14 @@ class Solver:
     def hydro_accel_dudt(self, parts, dt=0.0, stream=None):
         self._call(lib().crk_hydro_accel_dudt, parts, C.c_float(dt), stream=stream)
 
-    def substep(self, parts, dt_grav=0.0, dt_hydro=0.0, stream=None, hydro=True, fused=True, side_stream=None):
+    def substep(self, parts, dt_grav=0.0, dt_hydro=0.0, stream=None, hydro=True, fused=True, side_stream=None,
+                build=True):
         """The whole short-range substep: a1-a8 in call order.  With
         `side_stream`, gravity (a3) runs there concurrently with geometry (a4) and is joined
-        before corrections/extras (which read the kicked v)."""
-        self.build_lists(parts, stream)
+        before corrections/extras (which read the kicked v).  build=False reuses refreshed skin
+        lists (crk_refresh)."""
+        if build:
+            self.build_lists(parts, stream)
         if side_stream is not None and hydro:
             main = stream if stream is not None else torch.cuda.current_stream()
             side_stream.wait_stream(main)
@@ -324,15 +327,24 @@ class Solver:
     def kdk(self, parts, n_steps, c_cfl=0.25, c_acc=0.25, stream=None):
         """Kick-drift-kick leapfrog over n_steps sub-cycles, each with the time step of
         crk_courant_dt: forces at x_n, kick dt/2, drift dt, forces at x_{n+1} (the
-        velocity-dependent hydro terms see v_{n+1/2}), kick dt/2.  Needs the force outputs
-        (ax.., ahx.., dudt).  Returns the time steps taken."""
+        velocity-dependent hydro terms see v_{n+1/2}), kick dt/2.  With a list skin
+        (params["skin"] > 0) the forces after a drift reuse the lists through crk_refresh
+        while the displacement bound allows, else rebuild.  Needs the force outputs (ax..,
+        ahx.., dudt).  Returns the time steps taken."""
         self.substep(parts, stream=stream)
         dts = []
         for _ in range(n_steps):
             dt = self.courant_dt(parts, c_cfl, c_acc, stream)
             self.kick(parts, 0.5 * dt, stream)
             self.drift(parts, dt, stream)
-            self.substep(parts, stream=stream)
+            rebuild = True
+            if self.params.get("skin", 0.0) > 0.0:
+                try:
+                    self.refresh(parts, stream)
+                    rebuild = False
+                except CrkError:
+                    pass
+            self.substep(parts, stream=stream, build=rebuild)
             self.kick(parts, 0.5 * dt, stream)
             dts.append(dt)
         return dts
