@@ -241,6 +241,21 @@ crk_status crk_pack_gas(struct crk_ctx* ctx, int what, const int32_t* idx, int64
 crk_status crk_unpack_gas(struct crk_ctx* ctx, int what, const int32_t* idx, int64_t n, const void* in,
                           void* stream);
 
+/* ---- long-range gravity, particle mesh (PAPER.md:146-147 force
+ * split; readings in DESIGN.md §2 "Long-range PM") ----
+ * Cloud-in-cell deposit on an n_grid^3 periodic mesh, cuFFT real-to-complex transform, the
+ * Gaussian-filtered Poisson kernel -4 pi G exp(-k^2 r_s^2) / k^2 (zero mode dropped), a
+ * spectral gradient -i k (Nyquist components zeroed), three inverse transforms and
+ * cloud-in-cell interpolation: ax/ay/az (device, length n) receive the long-range
+ * acceleration of every particle, the counterpart of the short-range force with the same
+ * r_s.  Cubic box, n_grid a power of two in [8, 1024], r_s > 0 (CRK_EINVAL otherwise).
+ * Independent of crk_ctx; one crk_pm per device; asynchronous on `stream`. */
+struct crk_pm;
+crk_status crk_pm_create(int n_grid, const double* box, float r_s, float G, int device, struct crk_pm** out);
+crk_status crk_pm_destroy(struct crk_pm* pm);
+crk_status crk_pm_accel(struct crk_pm* pm, int64_t n, const float* x, const float* y, const float* z,
+                        const float* m, float* ax, float* ay, float* az, void* stream);
+
 /* Device views of leaves and lists (after crk_build_lists). */
 crk_status crk_list_view(struct crk_ctx* ctx, crk_lists* out);
 

@@ -354,3 +354,51 @@ def knn_h(parts, params, targets, k=64, factor=1.01):
                     _p(np.ascontiguousarray(parts["species"], np.uint8)), _p(_f32(parts, "H")), b,
                     C.c_int64(t.shape[0]), _p(t), C.c_int(k), C.c_float(factor), _p(Hn), _p(conv))
     return Hn, conv.astype(bool)
+
+
+# ----------------------------------------------------------------- long-range PM (NEXT-3)
+def pm_accel(x, y, z, m, box, n_grid, r_s, G=1.0):
+    """Long-range particle-mesh acceleration in fp64 (DESIGN.md §2 "Long-range PM"):
+    cloud-in-cell deposit (cell centres at (i + 1/2) dx), rho_k by a real FFT,
+    phi_k = -4 pi G exp(-k^2 r_s^2) / k^2 rho_k (zero mode dropped), a_k = -i k phi_k with
+    the Nyquist component of each derivative zeroed, inverse FFTs, cloud-in-cell
+    interpolation.  Plain numpy steps in the order of the method."""
+    L = float(box[0])
+    ng = int(n_grid)
+    dx = L / ng
+    pos = np.stack([np.asarray(x, np.float64), np.asarray(y, np.float64), np.asarray(z, np.float64)], 1) / dx - 0.5
+    base = np.floor(pos)
+    f = pos - base
+    i0 = np.mod(base.astype(np.int64), ng)
+    i1 = np.mod(i0 + 1, ng)
+    w = [(1.0 - f[:, a], f[:, a]) for a in range(3)]
+    idx = [(i0[:, a], i1[:, a]) for a in range(3)]
+    rho = np.zeros((ng, ng, ng))
+    mm = np.asarray(m, np.float64) / dx ** 3
+    for a in range(2):
+        for b in range(2):
+            for c in range(2):
+                np.add.at(rho, (idx[0][a], idx[1][b], idx[2][c]), mm * w[0][a] * w[1][b] * w[2][c])
+    rk = np.fft.rfftn(rho)
+    kf = 2.0 * np.pi / L * np.fft.fftfreq(ng, 1.0 / ng)
+    kh = 2.0 * np.pi / L * np.arange(ng // 2 + 1)
+    KX, KY, KZ = np.meshgrid(kf, kf, kh, indexing="ij")
+    k2 = KX ** 2 + KY ** 2 + KZ ** 2
+    with np.errstate(divide="ignore", invalid="ignore"):
+        g = np.where(k2 > 0, -4.0 * np.pi * G * np.exp(-k2 * r_s ** 2) / k2, 0.0)
+    phi = g * rk
+    nyq = ng // 2
+    D = [KX.copy(), KY.copy(), KZ.copy()]
+    D[0][nyq, :, :] = 0.0
+    D[1][:, nyq, :] = 0.0
+    D[2][:, :, nyq] = 0.0
+    out = []
+    for a in range(3):
+        grid = np.fft.irfftn(-1j * D[a] * phi, s=(ng, ng, ng), axes=(0, 1, 2))
+        acc = np.zeros(pos.shape[0])
+        for ia in range(2):
+            for ib in range(2):
+                for ic in range(2):
+                    acc += w[0][ia] * w[1][ib] * w[2][ic] * grid[idx[0][ia], idx[1][ib], idx[2][ic]]
+        out.append(acc)
+    return np.stack(out, 1)

@@ -21,7 +21,8 @@ EXPORTS = ["crk_create", "crk_destroy", "crk_build_lists", "crk_gravity_kick", "
            "crk_corrections", "crk_extras", "crk_corrections_extras", "crk_hydro_accel_dudt", "crk_count_pairs",
            "crk_list_view", "crk_launch_count", "crk_status_string", "crk_last_error", "crk_select_cells", "crk_select_gas",
            "crk_pack_particles", "crk_unpack_particles", "crk_pack_gas", "crk_unpack_gas", "crk_courant_dt",
-           "crk_kick", "crk_drift", "crk_update_h", "crk_refresh"]
+           "crk_kick", "crk_drift", "crk_update_h", "crk_refresh", "crk_pm_create", "crk_pm_destroy",
+           "crk_pm_accel"]
 
 
 class CrkError(RuntimeError):
@@ -86,6 +87,11 @@ def lib():
         for f in ("crk_kick", "crk_drift"):
             getattr(L, f).argtypes = [vp, C.POINTER(CrkParticles), C.c_float, vp]
         L.crk_update_h.argtypes = [vp, C.POINTER(CrkParticles), C.c_int32, C.c_float, vp, vp, vp]
+        L.crk_pm_create.argtypes = [C.c_int, C.POINTER(C.c_double), C.c_float, C.c_float, C.c_int, C.POINTER(vp)]
+        L.crk_pm_destroy.argtypes = [vp]
+        L.crk_pm_accel.argtypes = [vp, C.c_int64, vp, vp, vp, vp, vp, vp, vp, vp]
+        for f in ("crk_pm_create", "crk_pm_destroy", "crk_pm_accel"):
+            getattr(L, f).restype = C.c_int
         L.crk_list_view.argtypes = [vp, C.POINTER(CrkLists)]
         L.crk_launch_count.argtypes = [vp]
         L.crk_launch_count.restype = C.c_int64
@@ -439,3 +445,39 @@ class Solver:
                 shift=_wrap(lv.shift[m], (ne,), "|i1", d),
             ))
         return out
+
+
+class PM:
+    """Long-range particle-mesh gravity (crk_pm_*): CIC + cuFFT + Gaussian-filtered Poisson."""
+
+    def __init__(self, n_grid: int, box, r_s: float, G: float = 1.0, device=0):
+        b = (C.c_double * 3)(*[float(v) for v in box])
+        h = C.c_void_p()
+        st = lib().crk_pm_create(int(n_grid), b, C.c_float(r_s), C.c_float(G), int(device), C.byref(h))
+        if st != 0:
+            raise CrkError(st, "crk_pm_create")
+        self.pm = h
+        self.device = torch.device("cuda", device)
+
+    def accel(self, x, y, z, m, stream=None):
+        """Long-range acceleration (3 device tensors) of particles at x, y, z with masses m."""
+        n = x.shape[0]
+        out = [torch.empty(n, dtype=torch.float32, device=x.device) for _ in range(3)]
+        s = stream if stream is not None else torch.cuda.current_stream()
+        st = lib().crk_pm_accel(self.pm, C.c_int64(n), *[C.c_void_p(t.data_ptr()) for t in (x, y, z, m, *out)],
+                                C.c_void_p(s.cuda_stream))
+        if st != 0:
+            raise CrkError(st, "crk_pm_accel")
+        return out
+
+    def close(self):
+        if getattr(self, "pm", None):
+            lib().crk_pm_destroy(self.pm)
+            self.pm = None
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
+

@@ -10,7 +10,7 @@ CSRC = os.path.join(HERE, "csrc")
 ROOT = os.path.dirname(HERE)
 LIB = os.path.join(HERE, "libcrksr.so")
 OBJDIR = os.path.join(HERE, "_build")
-SOURCES = ["api.cu", "build.cu", "gravity.cu", "hydro.cu", "domain.cu", "integrate.cu"]
+SOURCES = ["api.cu", "build.cu", "gravity.cu", "hydro.cu", "domain.cu", "integrate.cu", "pm.cu"]
 HEADERS = ["ctx.h", "common.cuh", "pairs.cuh"]
 
 NVCC = os.environ.get("NVCC", "/usr/local/cuda/bin/nvcc")
@@ -55,7 +55,7 @@ def build(force: bool = False, verbose: bool = False) -> str:
                 print(log)
     if force or not os.path.exists(LIB) or any(os.path.getmtime(o) > os.path.getmtime(LIB) for o in objs):
         r = subprocess.run([NVCC, "-shared", "-gencode", "arch=compute_100a,code=sm_100a", "-o", LIB, *objs,
-                            "-lcudart"], capture_output=True, text=True)
+                            "-lcudart", "-lcufft"], capture_output=True, text=True)
         if r.returncode != 0:
             raise RuntimeError(f"link failed:\n{r.stderr}")
     return LIB

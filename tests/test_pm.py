@@ -1,0 +1,71 @@
+"""Long-range particle-mesh gravity (PAPER.md:146-147 force split).
+
+CPU: the oracle's PM against the analytic long-range force of a point mass, momentum
+conservation and a uniform lattice.  GPU (-m gpu): crk_pm_accel against the oracle.
+"""
+import math
+
+import numpy as np
+import pytest
+
+import oracle
+
+
+def _analytic(r, rs, G=1.0, m=1.0):
+    from scipy.special import erf
+
+    return -G * m * (erf(r / (2 * rs)) - r / (rs * math.sqrt(math.pi)) * np.exp(-r * r / (4 * rs * rs))) / r ** 2
+
+
+def test_pm_point_mass_matches_long_range_force():
+    """A unit mass and massless probes at 4-8 grid cells: the PM force is the Gaussian-split
+    long-range force within the CIC / periodic-image error (< 8%), with the right sign."""
+    L, ng, rs = 64.0, 64, 2.0
+    r = np.array([4.0, 5.0, 6.0, 8.0])
+    x = np.concatenate([[32.0], 32.0 + r])
+    y = np.full(x.shape, 32.0)
+    z = np.full(x.shape, 32.0)
+    m = np.concatenate([[1.0], np.zeros(r.shape)])
+    a = oracle.pm_accel(x, y, z, m, [L] * 3, ng, rs)
+    ana = _analytic(r, rs)
+    assert np.all(np.abs(a[1:, 0] / ana - 1.0) < 0.08)
+    assert np.all(np.abs(a[1:, 1:]) < 1e-3 * np.abs(ana)[:, None])  # on the axis: no transverse force
+    # twice r_s: the force at 4 cells drops (more of it is short-range)
+    a2 = oracle.pm_accel(x, y, z, m, [L] * 3, ng, 2 * rs)
+    assert abs(a2[1, 0]) < abs(a[1, 0])
+    assert abs(a2[1, 0] / _analytic(4.0, 2 * rs) - 1.0) < 0.08
+
+
+def test_pm_momentum_conservation_and_uniform_lattice():
+    rng = np.random.default_rng(3)
+    L, ng = 32.0, 32
+    n = 500
+    pos = rng.random((n, 3)) * L
+    m = rng.random(n) + 0.5
+    a = oracle.pm_accel(pos[:, 0], pos[:, 1], pos[:, 2], m, [L] * 3, ng, 1.5)
+    p = (m[:, None] * a).sum(0)
+    assert np.all(np.abs(p) <= 1e-10 * (m[:, None] * np.abs(a)).sum(0))
+    # uniform lattice on the cell centres: no force
+    g = (np.arange(16) + 0.5) * 2.0
+    X, Y, Z = np.meshgrid(g, g, g, indexing="ij")
+    a = oracle.pm_accel(X.ravel(), Y.ravel(), Z.ravel(), np.ones(X.size), [L] * 3, ng, 1.5)
+    assert np.abs(a).max() < 1e-12
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("name,ng,rs", [("c1", 16, 0.7), ("c1", 32, 1.2), ("c2z", 64, 0.69)])
+def test_gpu_pm_matches_oracle(name, ng, rs):
+    import torch
+    from crk_testutil import cached_config
+    from paper_2310_16122_b200 import PM
+
+    parts, params = cached_config(name)
+    dev = torch.device("cuda", 0)
+    t = lambda k: torch.from_numpy(np.ascontiguousarray(parts[k])).to(dev)  # noqa: E731
+    pm = PM(ng, params["box"], rs, 1.0)
+    ax, ay, az = pm.accel(t("x"), t("y"), t("z"), t("m"))
+    torch.cuda.synchronize()
+    g = np.stack([ax.cpu().numpy(), ay.cpu().numpy(), az.cpu().numpy()], 1)
+    ref = oracle.pm_accel(parts["x"], parts["y"], parts["z"], parts["m"], params["box"], ng, rs)
+    assert np.max(np.abs(g - ref)) <= 1e-4 * np.abs(ref).max()
+    pm.close()
