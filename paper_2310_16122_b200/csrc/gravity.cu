@@ -691,7 +691,13 @@ __global__ void __launch_bounds__(symp::NW * 32, 16 / symp::NW) grav_pipe_kernel
                 // w: first | (count - 1) << 29, as in the packed list entries
                 off = make_float4((float)sx * A.L[0], (float)sy * A.L[1], (float)sz * A.L[2],
                                   __int_as_float(first | ((cnt - 1) << 29)));
-                if (PARTIAL || first + cnt > gself) {  // entries wholly below this group own no pair
+                // entries wholly below this group own no pair — unless they are ghosts (a j-leaf
+                // lies in one cell, so its box centre, unshifted, decides its ownership)
+                bool ghost = false;
+                if (PARTIAL)
+                    ghost = !grav_owned(A, 0.5f * (bl.x + bh.x) - off.x, 0.5f * (bl.y + bh.y) - off.y,
+                                        0.5f * (bl.z + bh.z) - off.z);
+                if (first + cnt > gself || ghost) {
                     const float gx = fmaxf(fmaxf(bl.x - hi[0], lo[0] - bh.x), 0.f);
                     const float gy = fmaxf(fmaxf(bl.y - hi[1], lo[1] - bh.y), 0.f);
                     const float gz = fmaxf(fmaxf(bl.z - hi[2], lo[2] - bh.z), 0.f);
