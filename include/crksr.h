@@ -256,7 +256,8 @@ crk_status crk_pm_destroy(struct crk_pm* pm);
 crk_status crk_pm_accel(struct crk_pm* pm, int64_t n, const float* x, const float* y, const float* z,
                         const float* m, float* ax, float* ay, float* az, void* stream);
 
-/* Device views of leaves and lists (after crk_build_lists). */
+/* Device views of leaves and lists (after crk_build_lists).  The first call after a build
+ * decodes the CSR col / shift arrays from the packed entries (synchronises the device). */
 crk_status crk_list_view(struct crk_ctx* ctx, crk_lists* out);
 
 /* Number of kernel launches issued by this ctx since creation (launch accounting). */

@@ -17,6 +17,7 @@ crk_status geometry(crk_ctx* c, crk_particles* p, cudaStream_t st);
 crk_status corrections(crk_ctx* c, crk_particles* p, cudaStream_t st);
 crk_status extras(crk_ctx* c, crk_particles* p, cudaStream_t st);
 crk_status corrections_extras(crk_ctx* c, crk_particles* p, cudaStream_t st);
+crk_status csr_views(crk_ctx* c);
 crk_status update_h(crk_ctx* c, int kth, float factor, float* H_out, int32_t* n_unconverged, cudaStream_t st);
 crk_status accel_dudt(crk_ctx* c, crk_particles* p, float dt, cudaStream_t st);
 crk_status hydro_count(crk_ctx* c, int32_t* cgather, int32_t* csym, cudaStream_t st);
@@ -299,6 +300,8 @@ crk_status crk_count_pairs(crk_ctx* c, crk_particles* p, int32_t* cgrav, int32_t
 crk_status crk_list_view(crk_ctx* c, crk_lists* o) {
     if (!c || !o) return CRK_EINVAL;
     if (c->stage < ST_LISTS) return fail(c, CRK_ESTATE, "call crk_build_lists first");
+    CRK_TRY(cuda_check(c, cudaSetDevice(c->device), "cudaSetDevice"));
+    CRK_TRY(csr_views(c));
     for (int s = 0; s < 4; ++s) {
         o->n_leaf[s] = c->nleaf[s];
         o->leaf_first[s] = P<int32_t>(c->lfirst[s]);

@@ -257,8 +257,6 @@ struct ListArgs {
     int ncell[3];
     int32_t* rowlen;       // pass 1
     const int32_t* rowoff; // pass 2
-    int32_t* col;
-    int8_t* shift;
     const int32_t* jfirst;  // j-leaf first member / count (packed entry records)
     const int32_t* jcount;
     int2* erec;
@@ -275,8 +273,7 @@ __device__ __forceinline__ double skin_cut2(double cut2, double skin) {
 }
 
 __device__ __forceinline__ void put_entry(const ListArgs& A, int p, int b, int code) {
-    A.col[p] = b;
-    A.shift[p] = (int8_t)code;
+    // (the CSR col / shift views of crk_list_view are decoded from erec on demand)
     A.erec[p] = make_int2(A.jfirst[b] | ((A.jcount[b] - 1) << 29), b | (code << 26));
     if (A.ebox) {  // the j-leaf box with the periodic shift applied (exact, O1), next to first / count
         const float ox = (float)(code % 3 - 1) * A.Lf[0], oy = (float)((code / 3) % 3 - 1) * A.Lf[1],
@@ -450,8 +447,6 @@ static ListArgs list_args(crk_ctx* c, int m) {
     A.q2inv_slack = (1.0 + 0x1p-20) / (L.q * L.q);
     A.rowlen = P<int32_t>(c->rowlen[m]);
     A.rowoff = P<int32_t>(c->rowoff[m]);
-    A.col = P<int32_t>(c->col[m]);
-    A.shift = P<int8_t>(c->shift[m]);
     A.jfirst = P<int32_t>(c->lfirst[sb]);
     A.jcount = P<int32_t>(c->lcount[sb]);
     A.erec = P<int2>(c->erec[m]);
@@ -693,8 +688,6 @@ crk_status build_lists(crk_ctx* c, crk_particles* p, cudaStream_t st) {
         c->nent[m] = host[8 + m];
         const int64_t na = c->nleaf[m == 0 ? 0 : 2];
         const int64_t ne = c->nent[m] > 0 ? c->nent[m] : 1;
-        CRK_TRY(grow(c, c->col[m], ne * 4, st));
-        CRK_TRY(grow(c, c->shift[m], ne, st));
         CRK_TRY(grow(c, c->erec[m], ne * 8, st));
         if (m == 0) CRK_TRY(grow(c, c->gebox, ne * 32, st));
         ListArgs A = list_args(c, m);
@@ -725,7 +718,34 @@ crk_status build_lists(crk_ctx* c, crk_particles* p, cudaStream_t st) {
         CRK_TRY(cuda_check(c, zero_async(c->disp.p, 16, st, c), "memset"));
     }
     c->skin_lists = c->prm.skin > 0.f;
+    c->csr_views = false;
     c->stage = ST_LISTS;
+    return CRK_OK;
+}
+
+// crk_list_view's CSR col / shift arrays, decoded from the packed entries
+__global__ void k_decode_entries(int64_t ne, const int2* __restrict__ erec, int32_t* col, int8_t* shift) {
+    const int64_t p = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+    if (p >= ne) return;
+    const int2 r = erec[p];
+    col[p] = r.y & 0x03ffffff;
+    shift[p] = (int8_t)((unsigned)r.y >> 26);
+}
+
+crk_status csr_views(crk_ctx* c) {
+    if (c->csr_views) return CRK_OK;
+    for (int m = 0; m < 2; ++m) {
+        const int64_t ne = c->nent[m] > 0 ? c->nent[m] : 1;
+        CRK_TRY(grow(c, c->col[m], ne * 4, 0));
+        CRK_TRY(grow(c, c->shift[m], ne, 0));
+        if (c->nent[m] > 0) {
+            k_decode_entries<<<nblk(c->nent[m], 256), 256>>>(c->nent[m], P<int2>(c->erec[m]), P<int32_t>(c->col[m]),
+                                                             P<int8_t>(c->shift[m]));
+            CRK_LAUNCHED(c, "decode entries");
+        }
+    }
+    CRK_TRY(cuda_check(c, cudaDeviceSynchronize(), "sync"));
+    c->csr_views = true;
     return CRK_OK;
 }
 

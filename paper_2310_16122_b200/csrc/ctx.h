@@ -87,5 +87,6 @@ struct crk_ctx {
     int nbr_cap = 0;             // entries per gas particle (0: lists off)
     // skin lists (crk_params.skin > 0): valid lists survive drifts until crk_refresh
     bool skin_lists = false;     // the last build used the skin and no rebuild is due
+    bool csr_views = false;      // col / shift decoded for crk_list_view since the last build
     crk::Buf disp;               // device floats: [0] this drift's max |dt v|, [1] bound since the build
 };
