@@ -40,8 +40,17 @@ def fit_grid_poly(rc: float, eps2: float, rs_over: float = 4.5, order: int = 5):
     rr = r[~small]
     f[~small] = (erf(rr / (2 * rs)) - rr / (rs * math.sqrt(math.pi)) * np.exp(-rr * rr / (4 * rs * rs))) / rr**3
     f[small] = 1.0 / (6.0 * math.sqrt(math.pi) * rs**3)  # r -> 0 limit
+    return fit_poly_samples(s, f, rc, eps2, order)
+
+
+def fit_poly_samples(s, f, rc: float, eps2: float, order: int = 5):
+    """Least-squares polynomial in s to samples f(s) of a long-range force per unit
+    separation, constrained to P(rc^2) = (rc^2 + eps2)^-3/2 (KKT system).  With samples of
+    the force a particle-mesh solver actually produces (``PM.force_profile``) this is how
+    HACC derives its grid-force polynomial; fp32 coefficients."""
+    s = np.asarray(s, np.float64)
+    f = np.asarray(f, np.float64)
     V = np.vander(s, order + 1, increasing=True)
-    # equality-constrained least squares via KKT
     cvec = (rc * rc) ** np.arange(order + 1)
     target = (rc * rc + eps2) ** -1.5
     n = order + 1

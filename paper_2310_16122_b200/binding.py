@@ -9,6 +9,7 @@ from __future__ import annotations
 import ctypes as C
 import os
 
+import numpy as np
 import torch
 
 _HERE = os.path.dirname(os.path.abspath(__file__))
@@ -369,8 +370,6 @@ class Solver:
     # ---- ghost exchange (a9) ----
     @staticmethod
     def _mask(m):
-        import numpy as np
-
         return np.ascontiguousarray(m, dtype=np.uint8).tobytes()
 
     def select_cells(self, parts, masks, gas_only=False, n=None, stream=None):
@@ -458,6 +457,8 @@ class PM:
             raise CrkError(st, "crk_pm_create")
         self.pm = h
         self.device = torch.device("cuda", device)
+        self.box = [float(v) for v in box]
+        self.G = float(G)
 
     def accel(self, x, y, z, m, stream=None):
         """Long-range acceleration (3 device tensors) of particles at x, y, z with masses m."""
@@ -469,6 +470,38 @@ class PM:
         if st != 0:
             raise CrkError(st, "crk_pm_accel")
         return out
+
+    def force_profile(self, r, n_dir=16, n_src=4, seed=0):
+        """Measured radial force of this mesh per unit source mass and separation,
+        f(r) = -a_r / (G r), averaged over ``n_dir`` random directions and ``n_src`` random
+        source positions (CIC makes the mesh force depend on the source's sub-cell offset
+        and the probe's orientation).  One crk_pm_accel call per source, massless probes.
+        HACC fits its short-range polynomial to this measured grid force rather than to the
+        analytic one (feed the result to
+        ``gen.configs.fit_poly_samples``)."""
+        r = np.asarray(r, np.float64)
+        rng = np.random.default_rng(seed)
+        box = np.asarray(self.box)
+        acc = np.zeros(r.shape[0])
+        for _ in range(n_src):
+            src = rng.random(3) * box
+            u = rng.standard_normal((n_dir, 3))
+            u /= np.linalg.norm(u, axis=1, keepdims=True)
+            d = (r[None, :, None] * u[:, None, :]).reshape(-1, 3)  # (n_dir * len(r), 3)
+            pos = np.mod(np.concatenate([src[None], src + d]), box)
+            m = np.zeros(pos.shape[0])
+            m[0] = 1.0
+            t = [torch.tensor(v, dtype=torch.float32, device=self.device)
+                 for v in (pos[:, 0], pos[:, 1], pos[:, 2], m)]
+            a = torch.stack(self.accel(*t), 1)[1:].double().cpu().numpy()
+            # positions are fp32: measure the radial component along the realised separation
+            p32 = pos.astype(np.float32).astype(np.float64)
+            dd = p32[1:] - p32[0]
+            dd -= box * np.round(dd / box)
+            rr = np.linalg.norm(dd, axis=1)
+            ar = -(a * dd).sum(1) / np.maximum(rr, 1e-30)
+            acc += (ar / (self.G * np.maximum(rr, 1e-30))).reshape(n_dir, -1).mean(0)
+        return acc / n_src
 
     def close(self):
         if getattr(self, "pm", None):

@@ -69,3 +69,48 @@ def test_gpu_pm_matches_oracle(name, ng, rs):
     ref = oracle.pm_accel(parts["x"], parts["y"], parts["z"], parts["m"], params["box"], ng, rs)
     assert np.max(np.abs(g - ref)) <= 1e-4 * np.abs(ref).max()
     pm.close()
+
+
+def test_fit_poly_samples_recovers_constrained_polynomial():
+    """The constrained least squares behind the grid-force polynomial: samples of a degree-5
+    polynomial that already meets P(rc^2) = (rc^2+eps2)^-3/2 come back unchanged (to fp32),
+    and for any samples the constraint holds exactly."""
+    from gen.configs import fit_poly_samples
+
+    rc, eps2 = 3.1, 0.01
+    c = np.array([0.3, -0.09, 0.015, -1.6e-3, 1e-4, 0.0])
+    s0 = rc * rc
+    c[5] = ((s0 + eps2) ** -1.5 - np.polyval(c[::-1], s0)) / s0**5
+    s = np.linspace(0.0, s0, 400)
+    got = fit_poly_samples(s, np.polyval(c[::-1], s), rc, eps2).astype(np.float64)
+    assert np.allclose(got, c, rtol=1e-5, atol=1e-9)
+    rng = np.random.default_rng(0)
+    got = fit_poly_samples(s, rng.random(s.shape), rc, eps2).astype(np.float64)
+    assert abs(np.polyval(got[::-1], s0) / (s0 + eps2) ** -1.5 - 1.0) < 1e-4  # fp32 coefficients
+
+
+@pytest.mark.gpu
+def test_gpu_force_split_closure():
+    """Short-range PP + long-range PM = the softened Newtonian force of a point mass
+    (PAPER.md:146-147), with the short-range polynomial fitted to the force the mesh
+    actually produces (PM.force_profile); that fit closes the split
+    at least as well as the analytic one inside the cutoff."""
+    import os
+    import sys
+
+    sys.path.insert(0, os.path.join(os.path.dirname(os.path.dirname(os.path.abspath(__file__))), "tools"))
+    import force_split as fs
+    from gen.configs import fit_grid_poly, fit_poly_samples
+    from paper_2310_16122_b200 import PM
+
+    L, ng = 64.0, 64
+    pm = PM(ng, [L] * 3, r_s=fs.RC / 4.5, G=fs.G)
+    s = np.linspace(0.0, fs.RC**2, 129)[1:]
+    poly_mesh = fit_poly_samples(s, pm.force_profile(np.sqrt(s), n_dir=16, n_src=4, seed=1), fs.RC, fs.EPS2)
+    res = fs.closure(L, ng, poly_mesh, fit_grid_poly(fs.RC, fs.EPS2), pm, np.linspace(0.2, 6.0, 30), 12, seeds=[5, 6])
+    pm.close()
+    mesh, ana = res["mesh"], res["analytic"]
+    assert mesh["rms_inside_rc"] <= ana["rms_inside_rc"] * 1.05
+    assert mesh["rms_inside_rc"] < FS_RMS
+    for b in mesh["bins"]:
+        assert b["max_rel"] < FS_MAX, b
