@@ -94,7 +94,7 @@ def test_gpu_force_split_closure():
     """Short-range PP + long-range PM = the softened Newtonian force of a point mass
     (PAPER.md:146-147), with the short-range polynomial fitted to the force the mesh
     actually produces (PM.force_profile); that fit closes the split
-    at least as well as the analytic one inside the cutoff."""
+    much better than the analytic one inside the cutoff."""
     import os
     import sys
 
@@ -110,7 +110,11 @@ def test_gpu_force_split_closure():
     res = fs.closure(L, ng, poly_mesh, fit_grid_poly(fs.RC, fs.EPS2), pm, np.linspace(0.2, 6.0, 30), 12, seeds=[5, 6])
     pm.close()
     mesh, ana = res["mesh"], res["analytic"]
-    assert mesh["rms_inside_rc"] <= ana["rms_inside_rc"] * 1.05
-    assert mesh["rms_inside_rc"] < FS_RMS
+    # measured (tools/force_split.py, profiles/r01/force_split.json): rms inside r_c 1.8% with the
+    # mesh fit, 9.8% with the analytic one (a -14% bias at r = 1.5-2 grid cells)
+    assert mesh["rms_inside_rc"] < 0.5 * ana["rms_inside_rc"]
+    assert mesh["rms_inside_rc"] < 0.04
     for b in mesh["bins"]:
-        assert b["max_rel"] < FS_MAX, b
+        assert b["max_rel"] < 0.2 and b["max_transverse"] < 0.2, b
+        if b["r"][1] <= fs.RC:
+            assert abs(b["mean_rel"]) < 0.03, b  # the analytic fit: -0.04 to -0.14 here

@@ -73,7 +73,7 @@ def closure(L, ng, poly_mesh, poly_ana, pm, radii, n_dir, seeds):
         for name, poly in (("mesh", poly_mesh), ("analytic", poly_ana)):
             a = short_range(pos, L, poly)[1:] + alr
             ar = -(a * d).sum(1) / r
-            at = np.linalg.norm(a + ar[:, None] * (-d / r[:, None]), axis=1)  # transverse part
+            at = np.linalg.norm(a - ar[:, None] * (-d / r[:, None]), axis=1)  # transverse part
             rows[name].append(np.stack([ar / newton - 1.0, at / newton], 1))
         rr_all.append(r)
     r = np.concatenate(rr_all)
