@@ -256,6 +256,36 @@ crk_status crk_pm_destroy(struct crk_pm* pm);
 crk_status crk_pm_accel(struct crk_pm* pm, int64_t n, const float* x, const float* y, const float* z,
                         const float* m, float* ax, float* ay, float* az, void* stream);
 
+/* ---- slab-decomposed particle mesh over P ranks ("cuFFT with NCCL
+ * all-to-all"; the same operator as crk_pm_accel, DESIGN.md §2 "Distributed PM") ----
+ * n = n_grid, nxl = nyl = n / P, nzc = n / 2 + 1; rank r owns the real x-planes
+ * [r nxl, (r+1) nxl) and the spectrum's y-rows [r nyl, (r+1) nyl).  The collectives between
+ * the calls are the caller's (torch.distributed / NCCL in paper_2310_16122_b200/pm_dist.py):
+ *   crk_pm_deposit(mine)             -> rho_full   (n^3 f32, every rank's own particles)
+ *   reduce-scatter(sum) rho_full     -> rho_slab   (nxl n n f32: chunk r of the x-major mesh)
+ *   crk_pm_slab_forward(rho_slab)    -> send       (P blocks of nxl nyl nzc complex64, block r'
+ *                                                   = the y-rows of rank r')
+ *   all-to-all(send)                 -> recv       (block r'' = rank r'''s x-planes)
+ *   crk_pm_slab_solve(recv)          -> send3      (P blocks of 3 nxl nyl nzc complex64: the
+ *                                                   three gradient spectra, x-planes of r'')
+ *   all-to-all(send3)                -> recv3
+ *   crk_pm_slab_inverse(recv3)       -> acc_slab   (3 nxl n n f32, [c][ixl][iy][iz])
+ *   all-gather(acc_slab)             -> acc_full   (P x acc_slab)
+ *   crk_pm_interp(acc_full, mine)    -> ax, ay, az (device, length n_mine)
+ * All buffers are caller-owned device memory; every call is asynchronous on `stream`.
+ * n_grid % nranks != 0, rank out of range or the limits of crk_pm_create -> CRK_EINVAL;
+ * crk_pm_accel refuses a slab handle; crk_pm_slab_* and crk_pm_interp refuse a crk_pm_create
+ * handle (crk_pm_deposit takes either). */
+crk_status crk_pm_slab_create(int n_grid, const double* box, float r_s, float G, int rank, int nranks, int device,
+                              struct crk_pm** out);
+crk_status crk_pm_deposit(struct crk_pm* pm, int64_t n, const float* x, const float* y, const float* z,
+                          const float* m, float* rho_full, void* stream);
+crk_status crk_pm_slab_forward(struct crk_pm* pm, const float* rho_slab, void* send, void* stream);
+crk_status crk_pm_slab_solve(struct crk_pm* pm, const void* recv, void* send3, void* stream);
+crk_status crk_pm_slab_inverse(struct crk_pm* pm, const void* recv3, float* acc_slab, void* stream);
+crk_status crk_pm_interp(struct crk_pm* pm, int64_t n, const float* x, const float* y, const float* z,
+                         const float* acc_full, float* ax, float* ay, float* az, void* stream);
+
 /* Device views of leaves and lists (after crk_build_lists).  The first call after a build
  * decodes the CSR col / shift arrays from the packed entries (synchronises the device). */
 crk_status crk_list_view(struct crk_ctx* ctx, crk_lists* out);

@@ -4,6 +4,6 @@ The product is libcrksr.so (include/crksr.h): hand-written sm_100a CUDA for the
 leaf build, leaf-pair lists, short-range gravity and the CRK-SPH passes.  This
 package is its thin Python binding; see DESIGN.md.
 """
-from .binding import (CrkError, Particles, PM, Solver, lib, LIB_PATH, EXPORTS)  # noqa: F401
+from .binding import (CrkError, Particles, PM, SlabPM, Solver, lib, LIB_PATH, EXPORTS)  # noqa: F401
 
-__all__ = ["CrkError", "Particles", "PM", "Solver", "lib", "LIB_PATH", "EXPORTS"]
+__all__ = ["CrkError", "Particles", "PM", "SlabPM", "Solver", "lib", "LIB_PATH", "EXPORTS"]

@@ -23,7 +23,8 @@ EXPORTS = ["crk_create", "crk_destroy", "crk_build_lists", "crk_gravity_kick", "
            "crk_list_view", "crk_launch_count", "crk_status_string", "crk_last_error", "crk_select_cells", "crk_select_gas",
            "crk_pack_particles", "crk_unpack_particles", "crk_pack_gas", "crk_unpack_gas", "crk_courant_dt",
            "crk_kick", "crk_drift", "crk_update_h", "crk_refresh", "crk_pm_create", "crk_pm_destroy",
-           "crk_pm_accel"]
+           "crk_pm_accel", "crk_pm_slab_create", "crk_pm_deposit", "crk_pm_slab_forward", "crk_pm_slab_solve",
+           "crk_pm_slab_inverse", "crk_pm_interp"]
 
 
 class CrkError(RuntimeError):
@@ -91,7 +92,14 @@ def lib():
         L.crk_pm_create.argtypes = [C.c_int, C.POINTER(C.c_double), C.c_float, C.c_float, C.c_int, C.POINTER(vp)]
         L.crk_pm_destroy.argtypes = [vp]
         L.crk_pm_accel.argtypes = [vp, C.c_int64, vp, vp, vp, vp, vp, vp, vp, vp]
-        for f in ("crk_pm_create", "crk_pm_destroy", "crk_pm_accel"):
+        L.crk_pm_slab_create.argtypes = [C.c_int, C.POINTER(C.c_double), C.c_float, C.c_float, C.c_int, C.c_int,
+                                         C.c_int, C.POINTER(vp)]
+        L.crk_pm_deposit.argtypes = [vp, C.c_int64, vp, vp, vp, vp, vp, vp]
+        for f in ("crk_pm_slab_forward", "crk_pm_slab_solve", "crk_pm_slab_inverse"):
+            getattr(L, f).argtypes = [vp, vp, vp, vp]
+        L.crk_pm_interp.argtypes = [vp, C.c_int64, vp, vp, vp, vp, vp, vp, vp, vp]
+        for f in ("crk_pm_create", "crk_pm_destroy", "crk_pm_accel", "crk_pm_slab_create", "crk_pm_deposit",
+                  "crk_pm_slab_forward", "crk_pm_slab_solve", "crk_pm_slab_inverse", "crk_pm_interp"):
             getattr(L, f).restype = C.c_int
         L.crk_list_view.argtypes = [vp, C.POINTER(CrkLists)]
         L.crk_launch_count.argtypes = [vp]
@@ -514,3 +522,81 @@ class PM:
         except Exception:
             pass
 
+
+
+class SlabPM:
+    """One rank's share of the slab-decomposed particle mesh (crk_pm_slab_*; include/crksr.h).
+    Each method is one C-ABI call on a caller-owned buffer; the collectives between them are
+    the caller's (``pm_dist.pm_accel_distributed`` with torch.distributed)."""
+
+    def __init__(self, n_grid: int, box, r_s: float, G: float, rank: int, nranks: int, device=0):
+        b = (C.c_double * 3)(*[float(v) for v in box])
+        h = C.c_void_p()
+        st = lib().crk_pm_slab_create(int(n_grid), b, C.c_float(r_s), C.c_float(G), int(rank), int(nranks),
+                                      int(device), C.byref(h))
+        if st != 0:
+            raise CrkError(st, "crk_pm_slab_create")
+        self.pm = h
+        self.device = torch.device("cuda", device)
+        self.n, self.rank, self.P = int(n_grid), int(rank), int(nranks)
+        self.nl = self.n // self.P
+        self.nzc = self.n // 2 + 1
+
+    # buffer shapes (include/crksr.h)
+    def sizes(self):
+        n, nl, P, nzc = self.n, self.nl, self.P, self.nzc
+        return dict(rho_full=n ** 3, rho_slab=nl * n * n, send=P * nl * nl * nzc, send3=P * 3 * nl * nl * nzc,
+                    acc_slab=3 * nl * n * n)
+
+    @staticmethod
+    def _s(stream):
+        return C.c_void_p((stream if stream is not None else torch.cuda.current_stream()).cuda_stream)
+
+    @staticmethod
+    def _p(t):
+        return C.c_void_p(t.data_ptr())
+
+    def _ck(self, st, what):
+        if st != 0:
+            raise CrkError(st, what)
+
+    def deposit(self, x, y, z, m, stream=None):
+        rho = torch.empty(self.sizes()["rho_full"], dtype=torch.float32, device=self.device)
+        self._ck(lib().crk_pm_deposit(self.pm, C.c_int64(x.shape[0]), *map(self._p, (x, y, z, m, rho)),
+                                      self._s(stream)), "crk_pm_deposit")
+        return rho
+
+    def forward(self, rho_slab, stream=None):
+        send = torch.empty(self.sizes()["send"], dtype=torch.complex64, device=self.device)
+        self._ck(lib().crk_pm_slab_forward(self.pm, self._p(rho_slab), self._p(send), self._s(stream)),
+                 "crk_pm_slab_forward")
+        return send
+
+    def solve(self, recv, stream=None):
+        send3 = torch.empty(self.sizes()["send3"], dtype=torch.complex64, device=self.device)
+        self._ck(lib().crk_pm_slab_solve(self.pm, self._p(recv), self._p(send3), self._s(stream)),
+                 "crk_pm_slab_solve")
+        return send3
+
+    def inverse(self, recv3, stream=None):
+        acc = torch.empty(self.sizes()["acc_slab"], dtype=torch.float32, device=self.device)
+        self._ck(lib().crk_pm_slab_inverse(self.pm, self._p(recv3), self._p(acc), self._s(stream)),
+                 "crk_pm_slab_inverse")
+        return acc
+
+    def interp(self, x, y, z, acc_full, stream=None):
+        out = [torch.empty(x.shape[0], dtype=torch.float32, device=self.device) for _ in range(3)]
+        self._ck(lib().crk_pm_interp(self.pm, C.c_int64(x.shape[0]), *map(self._p, (x, y, z, acc_full, *out)),
+                                     self._s(stream)), "crk_pm_interp")
+        return out
+
+    def close(self):
+        if getattr(self, "pm", None):
+            lib().crk_pm_destroy(self.pm)
+            self.pm = None
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass

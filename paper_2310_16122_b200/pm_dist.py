@@ -1,0 +1,67 @@
+"""Slab-decomposed long-range particle mesh over ranks (cuFFT with
+NCCL all-to-all; include/crksr.h "slab-decomposed particle mesh").
+
+The kernels are the crk_pm_slab_* calls (``SlabPM``); this module only sequences them with
+the four collectives between them — a reduce-scatter of the deposited mesh, two all-to-all
+transposes and an all-gather of the acceleration slabs — through a ``comm`` object, so the
+same sequence runs over torch.distributed (NCCL) or, in the tests, over P ranks emulated
+on one GPU.
+"""
+from __future__ import annotations
+
+import torch
+
+
+class TorchComm:
+    """The four collectives over torch.distributed (NCCL on B200)."""
+
+    def __init__(self, group=None):
+        import torch.distributed as dist
+
+        self.dist, self.group = dist, group
+
+    def reduce_scatter(self, out, full):
+        self.dist.reduce_scatter_tensor(out, full, group=self.group)
+
+    def all_to_all(self, out, inp):
+        self.dist.all_to_all_single(out, inp, group=self.group)
+
+    def all_gather(self, out, part):
+        self.dist.all_gather_into_tensor(out, part, group=self.group)
+
+
+def pm_accel_distributed(spm, x, y, z, m, comm=None, stream=None):
+    """Long-range acceleration of this rank's particles (x, y, z, m device tensors) with the
+    mesh slab-decomposed over the ranks of ``comm`` (default: the torch.distributed world)."""
+    comm = comm or TorchComm()
+    sz = spm.sizes()
+    rho = spm.deposit(x, y, z, m, stream)
+    rho_slab = torch.empty(sz["rho_slab"], dtype=torch.float32, device=rho.device)
+    comm.reduce_scatter(rho_slab, rho)
+    send = spm.forward(rho_slab, stream)
+    recv = torch.empty_like(send)
+    comm.all_to_all(recv, send)
+    send3 = spm.solve(recv, stream)
+    recv3 = torch.empty_like(send3)
+    comm.all_to_all(recv3, send3)
+    acc = spm.inverse(recv3, stream)
+    acc_full = torch.empty(spm.P * acc.numel(), dtype=torch.float32, device=acc.device)
+    comm.all_gather(acc_full, acc)
+    return spm.interp(x, y, z, acc_full, stream)
+
+
+def pm_accel_emulated(spms, parts):
+    """P ranks emulated on one device, phase by phase (the collectives as tensor copies):
+    ``spms[r]`` is rank r's SlabPM, ``parts[r]`` its (x, y, z, m).  Returns each rank's
+    accelerations; for tests and single-GPU checks of the decomposed path."""
+    P = len(spms)
+    rho = [s.deposit(*p) for s, p in zip(spms, parts)]
+    total = torch.stack(rho).sum(0)
+    slabs = list(total.chunk(P))
+    send = [s.forward(slabs[r].contiguous()) for r, s in enumerate(spms)]
+    recv = [torch.cat([send[q].chunk(P)[r] for q in range(P)]) for r in range(P)]
+    send3 = [s.solve(recv[r]) for r, s in enumerate(spms)]
+    recv3 = [torch.cat([send3[q].chunk(P)[r] for q in range(P)]) for r in range(P)]
+    acc = [s.inverse(recv3[r]) for r, s in enumerate(spms)]
+    acc_full = torch.cat(acc)
+    return [s.interp(p[0], p[1], p[2], acc_full) for s, p in zip(spms, parts)]

@@ -118,3 +118,51 @@ def test_gpu_force_split_closure():
         assert b["max_rel"] < 0.2 and b["max_transverse"] < 0.2, b
         if b["r"][1] <= fs.RC:
             assert abs(b["mean_rel"]) < 0.03, b  # the analytic fit: -0.04 to -0.14 here
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("name,ng,rs,P", [("c1", 16, 0.7, 1), ("c1", 16, 0.7, 8), ("c2z", 64, 0.69, 2),
+                                          ("c2z", 64, 0.69, 4)])
+def test_gpu_slab_pm_matches_oracle(name, ng, rs, P):
+    """The slab-decomposed mesh (crk_pm_slab_*; P ranks emulated on one GPU, particles dealt
+    to ranks at random) gives every particle the oracle's long-range force (the same 1e-4 bar
+    as crk_pm_accel) and agrees with the single-GPU crk_pm_accel to FFT rounding."""
+    import torch
+    from crk_testutil import cached_config
+    from paper_2310_16122_b200 import PM, SlabPM
+    from paper_2310_16122_b200.pm_dist import pm_accel_emulated
+
+    parts, params = cached_config(name)
+    dev = torch.device("cuda", 0)
+    n = parts["x"].shape[0]
+    owner = np.random.default_rng(7).integers(0, P, n)
+    spms = [SlabPM(ng, params["box"], rs, 1.0, r, P) for r in range(P)]
+    mine = [np.flatnonzero(owner == r) for r in range(P)]
+    rank_parts = [tuple(torch.from_numpy(np.ascontiguousarray(parts[k][idx])).to(dev) for k in ("x", "y", "z", "m"))
+                  for idx in mine]
+    acc = pm_accel_emulated(spms, rank_parts)
+    torch.cuda.synchronize()
+    g = np.zeros((n, 3))
+    for idx, a in zip(mine, acc):
+        g[idx] = np.stack([t.cpu().numpy() for t in a], 1)
+    ref = oracle.pm_accel(parts["x"], parts["y"], parts["z"], parts["m"], params["box"], ng, rs)
+    assert np.max(np.abs(g - ref)) <= 1e-4 * np.abs(ref).max()
+    pm = PM(ng, params["box"], rs, 1.0)
+    t = lambda k: torch.from_numpy(np.ascontiguousarray(parts[k])).to(dev)  # noqa: E731
+    one = np.stack([v.cpu().numpy() for v in pm.accel(t("x"), t("y"), t("z"), t("m"))], 1)
+    assert np.max(np.abs(g - one)) <= 1e-5 * np.abs(one).max()
+    pm.close()
+    for s in spms:
+        s.close()
+
+
+def test_slab_pm_rejects_bad_decompositions():
+    """n_grid must split evenly over the ranks; rank in range (CRK_EINVAL, no device work)."""
+    import ctypes as C
+
+    from paper_2310_16122_b200 import lib
+
+    b = (C.c_double * 3)(16.0, 16.0, 16.0)
+    h = C.c_void_p()
+    for ng, rank, P in [(16, 0, 3), (16, 2, 2), (16, -1, 2), (16, 0, 0), (12, 0, 2)]:
+        assert lib().crk_pm_slab_create(ng, b, C.c_float(0.7), C.c_float(1.0), rank, P, 0, C.byref(h)) == -1
