@@ -30,6 +30,43 @@ class TorchComm:
         self.dist.all_gather_into_tensor(out, part, group=self.group)
 
 
+class HostStagedComm(TorchComm):
+    """The same collectives over a CPU backend (gloo): device tensors are staged through host
+    memory.  For checking the distributed sequence with several processes on one GPU."""
+
+    def _run(self, fn, out, *inp):
+        o = out.cpu()
+        fn(o, *[t.cpu() for t in inp], group=self.group)
+        out.copy_(o)
+
+    def reduce_scatter(self, out, full):
+        # gloo has no reduce-scatter of complex/large tensors on every build: all-reduce + chunk
+        f = full.to("cpu", copy=True)
+        self.dist.all_reduce(f, group=self.group)
+        out.copy_(f.chunk(self.dist.get_world_size(self.group))[self.dist.get_rank(self.group)])
+
+    def all_to_all(self, out, inp):
+        self._run(self.dist.all_to_all_single, out, inp)
+
+    def all_gather(self, out, part):
+        self._run(self.dist.all_gather_into_tensor, out, part)
+
+
+# ---- the collectives' semantics on P emulated ranks (lists indexed by rank) ----
+def emu_reduce_scatter(full):
+    P = len(full)
+    return [c.contiguous() for c in torch.stack(full).sum(0).chunk(P)]
+
+
+def emu_all_to_all(inp):
+    P = len(inp)
+    return [torch.cat([inp[q].chunk(P)[r] for q in range(P)]) for r in range(P)]
+
+
+def emu_all_gather(parts):
+    return torch.cat(parts)
+
+
 def pm_accel_distributed(spm, x, y, z, m, comm=None, stream=None):
     """Long-range acceleration of this rank's particles (x, y, z, m device tensors) with the
     mesh slab-decomposed over the ranks of ``comm`` (default: the torch.distributed world)."""
@@ -54,14 +91,8 @@ def pm_accel_emulated(spms, parts):
     """P ranks emulated on one device, phase by phase (the collectives as tensor copies):
     ``spms[r]`` is rank r's SlabPM, ``parts[r]`` its (x, y, z, m).  Returns each rank's
     accelerations; for tests and single-GPU checks of the decomposed path."""
-    P = len(spms)
-    rho = [s.deposit(*p) for s, p in zip(spms, parts)]
-    total = torch.stack(rho).sum(0)
-    slabs = list(total.chunk(P))
-    send = [s.forward(slabs[r].contiguous()) for r, s in enumerate(spms)]
-    recv = [torch.cat([send[q].chunk(P)[r] for q in range(P)]) for r in range(P)]
-    send3 = [s.solve(recv[r]) for r, s in enumerate(spms)]
-    recv3 = [torch.cat([send3[q].chunk(P)[r] for q in range(P)]) for r in range(P)]
-    acc = [s.inverse(recv3[r]) for r, s in enumerate(spms)]
-    acc_full = torch.cat(acc)
+    slabs = emu_reduce_scatter([s.deposit(*p) for s, p in zip(spms, parts)])
+    recv = emu_all_to_all([s.forward(slabs[r]) for r, s in enumerate(spms)])
+    recv3 = emu_all_to_all([s.solve(recv[r]) for r, s in enumerate(spms)])
+    acc_full = emu_all_gather([s.inverse(recv3[r]) for r, s in enumerate(spms)])
     return [s.interp(p[0], p[1], p[2], acc_full) for s, p in zip(spms, parts)]

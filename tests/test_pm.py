@@ -166,3 +166,119 @@ def test_slab_pm_rejects_bad_decompositions():
     h = C.c_void_p()
     for ng, rank, P in [(16, 0, 3), (16, 2, 2), (16, -1, 2), (16, 0, 0), (12, 0, 2)]:
         assert lib().crk_pm_slab_create(ng, b, C.c_float(0.7), C.c_float(1.0), rank, P, 0, C.byref(h)) == -1
+
+
+def _comm_worker(rank, world, port, q):
+    import os
+
+    import torch
+    import torch.distributed as dist
+    from paper_2310_16122_b200.pm_dist import HostStagedComm, TorchComm
+
+    os.environ["MASTER_ADDR"] = "127.0.0.1"
+    os.environ["MASTER_PORT"] = str(port)
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    g = torch.Generator().manual_seed(rank)
+    full = torch.randn(8, generator=g)
+    a2a = torch.randn(6, generator=g).to(torch.complex64) * (1 + 2j)
+    part = torch.randn(3, generator=g)
+    out = {}
+    for name, comm in (("torch", TorchComm()), ("staged", HostStagedComm())):
+        rs = torch.empty(4)
+        comm.reduce_scatter(rs, full)
+        aa = torch.empty_like(a2a)
+        comm.all_to_all(aa, a2a)
+        ag = torch.empty(6)
+        comm.all_gather(ag, part)
+        out[name] = (rs, aa, ag)
+    q.put((rank, full, a2a, part, out))
+    dist.destroy_process_group()
+
+
+def test_slab_pm_collectives_match_emulation_gloo_two_ranks():
+    """The collectives pm_accel_distributed issues (torch.distributed and the host-staged gloo
+    variant, 2 ranks) move data exactly as the single-process emulation the GPU parity tests
+    use (pm_dist.emu_*)."""
+    import os
+
+    import torch
+    import torch.multiprocessing as mp
+    from paper_2310_16122_b200.pm_dist import emu_all_gather, emu_all_to_all, emu_reduce_scatter
+
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    port = 31500 + os.getpid() % 2000
+    procs = [ctx.Process(target=_comm_worker, args=(r, 2, port, q)) for r in range(2)]
+    for p in procs:
+        p.start()
+    res = {}
+    for _ in range(2):
+        r, *rest = q.get(timeout=120)
+        res[r] = rest
+    for p in procs:
+        p.join(60)
+    rs = emu_reduce_scatter([res[r][0] for r in range(2)])
+    aa = emu_all_to_all([res[r][1] for r in range(2)])
+    ag = emu_all_gather([res[r][2] for r in range(2)])
+    for r in range(2):
+        for name in ("torch", "staged"):
+            got = res[r][3][name]
+            assert torch.allclose(got[0], rs[r], atol=1e-6)
+            assert torch.equal(got[1], aa[r])
+            assert torch.equal(got[2], ag)
+
+
+def _slab_pm_worker(rank, world, port, ng, rs, q):
+    import os
+
+    import torch
+    import torch.distributed as dist
+    from crk_testutil import cached_config
+    from paper_2310_16122_b200 import SlabPM
+    from paper_2310_16122_b200.pm_dist import HostStagedComm, pm_accel_distributed
+
+    os.environ["MASTER_ADDR"] = "127.0.0.1"
+    os.environ["MASTER_PORT"] = str(port)
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    parts, params = cached_config("c2z")
+    n = parts["x"].shape[0]
+    mine = np.flatnonzero(np.random.default_rng(11).integers(0, world, n) == rank)
+    dev = torch.device("cuda", 0)
+    t = [torch.from_numpy(np.ascontiguousarray(parts[k][mine])).to(dev) for k in ("x", "y", "z", "m")]
+    spm = SlabPM(ng, params["box"], rs, 1.0, rank, world)
+    a = pm_accel_distributed(spm, *t, comm=HostStagedComm())
+    torch.cuda.synchronize()
+    q.put((rank, mine, np.stack([v.cpu().numpy() for v in a], 1)))
+    spm.close()
+    dist.destroy_process_group()
+
+
+@pytest.mark.gpu
+def test_gpu_slab_pm_two_processes():
+    """pm_accel_distributed end to end over torch.distributed: 2 processes sharing the one GPU
+    (gloo, host-staged collectives), each with its own random half of c2z; every particle
+    gets the oracle's long-range force."""
+    import os
+    import sys
+
+    import torch.multiprocessing as mp
+    from crk_testutil import cached_config
+
+    sys.path.insert(0, os.path.dirname(os.path.abspath(__file__)))
+    ng, rs = 64, 0.69
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    port = 33500 + os.getpid() % 2000
+    procs = [ctx.Process(target=_slab_pm_worker, args=(r, 2, port, ng, rs, q)) for r in range(2)]
+    for p in procs:
+        p.start()
+    parts, params = cached_config("c2z")
+    g = np.full((parts["x"].shape[0], 3), np.nan)
+    for _ in range(2):
+        r, mine, a = q.get(timeout=300)
+        g[mine] = a
+    for p in procs:
+        p.join(60)
+    ref = oracle.pm_accel(parts["x"], parts["y"], parts["z"], parts["m"], params["box"], ng, rs)
+    assert not np.isnan(g).any()
+    assert np.max(np.abs(g - ref)) <= 1e-4 * np.abs(ref).max()
