@@ -595,6 +595,145 @@ __global__ void __launch_bounds__(symw::NW * 32, 16 / symw::NW) grav_warp_kernel
     }
 }
 
+// ------------------------------------------------------------ half-warp shuffle variant
+// The paper's "half-warp" algorithm (Figs. half-warp-layout and
+// half-warp-shuffle), kept as a measured variant (
+// CRK_GRAV_VARIANT=8): lanes 0-15 hold the 16 i-particles of a work item, lanes 16-31 the
+// particles of two surviving j-leaves (8 lanes each).  In step k = 0..15 every lane
+// exchanges its particle with lane ^ (16 | k) by __shfl_xor_sync and adds the force its
+// partner exerts on its own particle: lane l < 16 evaluates (i_l, j), its partner the
+// reverse (j, i_l), so each pair is evaluated twice (once per direction, no per-pair atomics)
+// and the j-side sums reach memory once per j-leaf pair with red.global.add.  A pair
+// (p, q) belongs to the item of its lower index (the other item skips it), the same
+// Newton-3 ownership as the other symmetric kernels.  No domain decomposition.
+namespace symh {
+constexpr int G = 16, NW = 4;
+struct WarpSm {
+    float4 woff[32];  // surviving entries: shift, first (w)
+    int wcnt[32];
+};
+}  // namespace symh
+
+__global__ void __launch_bounds__(symh::NW * 32, 16 / symh::NW) grav_halfwarp_kernel(const GravSymArgs A) {
+    using namespace symh;
+    __shared__ WarpSm wsm[NW];
+    const int warp = threadIdx.x >> 5;
+    const int lane = threadIdx.x & 31;
+    WarpSm& S = wsm[warp];
+    const float wcut = A.rcut2 * CULL_SLACK;
+    const float rc2 = A.rcut2, e2 = A.eps2;
+    const float c0 = A.c0, c1 = A.c1, c2 = A.c2, c3 = A.c3, c4 = A.c4, c5 = A.c5;
+    const unsigned below = (1u << lane) - 1u;
+    const bool lower = lane < 16;
+
+    while (true) {
+        int w = 0;
+        if (lane == 0) w = atomicAdd(A.work, 1);
+        w = __shfl_sync(0xffffffffu, w, 0);
+        if (w >= A.nitems) break;
+        const int a = w / A.split;
+        const int icount = __ldg(A.icount + a);
+        const int ibase = (w % A.split) * G;
+        if (ibase >= icount) continue;
+        const int gself = __ldg(A.ifirst + a) + ibase;
+        const int ng = min(G, icount - ibase);
+        const int rbeg = __ldg(A.row_off + a), rend = __ldg(A.row_off + a + 1);
+
+        // lower half: the item's i-particles (index -1: no particle)
+        float4 ip = make_float4(0.f, 0.f, 0.f, 0.f);
+        int iidx = -1;
+        if (lower && lane < ng) {
+            iidx = gself + lane;
+            ip = __ldg(A.xm + iidx);
+        }
+        float lo[3], hi[3];
+        {
+            const bool iv = iidx >= 0;
+            lo[0] = warp_min(iv ? ip.x : INFINITY);
+            lo[1] = warp_min(iv ? ip.y : INFINITY);
+            lo[2] = warp_min(iv ? ip.z : INFINITY);
+            hi[0] = warp_max(iv ? ip.x : -INFINITY);
+            hi[1] = warp_max(iv ? ip.y : -INFINITY);
+            hi[2] = warp_max(iv ? ip.z : -INFINITY);
+        }
+        float acc[3] = {0.f, 0.f, 0.f};  // lower: the i-particle (whole item); upper: per instance
+
+        for (int e0 = rbeg; e0 < rend; e0 += 32) {
+            // entry cull (as grav_warp_kernel): one list entry per lane against the item's box
+            const int e = e0 + lane;
+            bool ek = false;
+            float4 off = make_float4(0.f, 0.f, 0.f, 0.f);
+            int cnt = 0;
+            if (e < rend) {
+                int first, leaf, code;
+                unpack_entry(__ldg(A.erec + e), first, cnt, leaf, code);
+                int sx, sy, sz;
+                decode_shift(code, sx, sy, sz);
+                off = make_float4((float)sx * A.L[0], (float)sy * A.L[1], (float)sz * A.L[2], __int_as_float(first));
+                if (first + cnt > gself) {
+                    const float4 bl = __ldg(A.box8 + 2 * (int64_t)leaf), bh = __ldg(A.box8 + 2 * (int64_t)leaf + 1);
+                    const float gx = fmaxf(fmaxf(bl.x + off.x - hi[0], lo[0] - bh.x - off.x), 0.f);
+                    const float gy = fmaxf(fmaxf(bl.y + off.y - hi[1], lo[1] - bh.y - off.y), 0.f);
+                    const float gz = fmaxf(fmaxf(bl.z + off.z - hi[2], lo[2] - bh.z - off.z), 0.f);
+                    ek = fmaf(gz, gz, fmaf(gy, gy, gx * gx)) < wcut;
+                }
+            }
+            const unsigned em = __ballot_sync(0xffffffffu, ek);
+            if (ek) {
+                const int q = __popc(em & below);
+                S.woff[q] = off;
+                S.wcnt[q] = cnt;
+            }
+            const int nsurv = __popc(em);
+            __syncwarp();
+            // two surviving j-leaves per half-warp instance
+            for (int q0 = 0; q0 < nsurv; q0 += 2) {
+                float4 op = ip;
+                int oidx = iidx;
+                if (!lower) {
+                    const int qe = q0 + ((lane - 16) >> 3), kk = lane & 7;
+                    oidx = -1;
+                    if (qe < nsurv && kk < S.wcnt[qe]) {
+                        const float4 o = S.woff[qe];
+                        oidx = __float_as_int(o.w) + kk;
+                        op = __ldg(A.xm + oidx);
+                        op.x += o.x; op.y += o.y; op.z += o.z;  // exact (O1)
+                    }
+                }
+#pragma unroll 4
+                for (int k = 0; k < 16; ++k) {
+                    const int m = 16 | k;
+                    const float px = __shfl_xor_sync(0xffffffffu, op.x, m);
+                    const float py = __shfl_xor_sync(0xffffffffu, op.y, m);
+                    const float pz = __shfl_xor_sync(0xffffffffu, op.z, m);
+                    const float pm = __shfl_xor_sync(0xffffffffu, op.w, m);
+                    const int pidx = __shfl_xor_sync(0xffffffffu, oidx, m);
+                    // the pair (i = lower lane's particle, j = upper's) is owned here iff j > i
+                    const bool own = oidx >= 0 && pidx >= 0 && (lower ? pidx > oidx : oidx > pidx);
+                    const float dx = px - op.x, dy = py - op.y, dz = pz - op.z;  // exact (O1)
+                    const float r2 = __fmaf_rn(dz, dz, __fmaf_rn(dy, dy, __fmul_rn(dx, dx)));  // O2 order
+                    const float ri = rsqrtf(r2 + e2);
+                    float p5 = fmaf(c5, r2, c4);
+                    p5 = fmaf(p5, r2, c3);
+                    p5 = fmaf(p5, r2, c2);
+                    p5 = fmaf(p5, r2, c1);
+                    p5 = fmaf(p5, r2, c0);
+                    const float wv = (own && r2 < rc2) ? pm * fmaf(ri * ri, ri, -p5) : 0.f;
+                    acc[0] = fmaf(wv, dx, acc[0]);  // force of the partner on this lane's particle
+                    acc[1] = fmaf(wv, dy, acc[1]);
+                    acc[2] = fmaf(wv, dz, acc[2]);
+                }
+                if (!lower) {  // j-side sums: once per j-particle and instance
+                    if (oidx >= 0) red_add_v4(A.acc + oidx, acc[0], acc[1], acc[2], 0.f);
+                    acc[0] = acc[1] = acc[2] = 0.f;
+                }
+            }
+            __syncwarp();
+        }
+        if (lower && iidx >= 0) red_add_v4(A.acc + iidx, acc[0], acc[1], acc[2], 0.f);
+    }
+}
+
 // ------------------------------------------------------------ pipelined warp-independent variant
 // With domain decomposition (A.partial) a pair with a ghost j is evaluated by i's group
 // whatever j's index (the ghost has no group here) and its reaction is dropped (j's own
@@ -902,7 +1041,8 @@ static cudaError_t launch_grav_sym(crk_ctx* c, GravSymArgs& A, cudaStream_t st) 
 }
 
 // CRK_GRAV_VARIANT: 0 pipelined warp-independent kernel (default; the only one with domain
-// decomposition support), 6 unpipelined, 1-5 and 7 CTA-staged (experiments)
+// decomposition support), 6 unpipelined, 1-5 and 7 CTA-staged, 8 the paper's half-warp
+// shuffle (experiments)
 static int grav_variant() {
     const char* gv = getenv("CRK_GRAV_VARIANT");
     return gv ? atoi(gv) : 0;
@@ -954,6 +1094,15 @@ static crk_status gravity_sym(crk_ctx* c, crk_particles* p, float dt, cudaStream
             break;
         }
         case 7: e = launch_grav_sym<8, 320, 1>(c, A, st); break;
+        case 8: {  // the paper's half-warp shuffle algorithm (every pair evaluated once per direction)
+            A.split = (c->prm.leaf_max_i + symh::G - 1) / symh::G;
+            A.nitems = (int)(c->nleaf[0] * A.split);
+            int nsm = 0;
+            cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, c->device);
+            grav_halfwarp_kernel<<<nsm * (16 / symh::NW), symh::NW * 32, 0, st>>>(A);
+            e = cudaGetLastError();
+            break;
+        }
         default: {  // pipelined warp-independent (c4: 16.0 ms)
             A.split = (c->prm.leaf_max_i + symp::G - 1) / symp::G;
             A.nitems = (int)(c->nleaf[0] * A.split);

@@ -338,7 +338,7 @@ def test_neighbour_list_capacities(cap, fused, monkeypatch):
     assert norm_err(gi["dudt"][T], ref["dudt"], ref["Sdu"]) <= TOL_FORCE
 
 
-@pytest.mark.parametrize("var", ["0", "1", "6", "7"])
+@pytest.mark.parametrize("var", ["0", "1", "6", "7", "8"])
 @pytest.mark.parametrize("name", ["c1", "c2z"])
 def test_gravity_symmetric_variants(var, name, monkeypatch):
     """Every Newton-3 gravity kernel variant (CRK_GRAV_VARIANT) against the oracle."""

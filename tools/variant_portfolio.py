@@ -16,6 +16,7 @@ PORTFOLIOS = {
     "lists + pipelined Newton-3 gravity (default)": {},
     "lists, CTA-staged Newton-3 gravity": {"CRK_GRAV_VARIANT": "7"},
     "lists, warp gravity without pipeline": {"CRK_GRAV_VARIANT": "6"},
+    "lists, half-warp shuffle gravity (the paper's algorithm)": {"CRK_GRAV_VARIANT": "8"},
     "lists, Newton-3 accel": {"CRK_HYD_VARIANT": "0005"},
     "on-the-fly culling everywhere (no neighbour lists)": {"CRK_NBR_CAP": "0", "CRK_GRAV_VARIANT": "7"},
 }
