@@ -1079,7 +1079,7 @@ static crk_status accel_gather(crk_ctx* c, crk_particles* p, float dt, cudaStrea
 
 crk_status accel_dudt(crk_ctx* c, crk_particles* p, float dt, cudaStream_t st) {
     if (dt != 0.f && (!p->vx || !p->vy || !p->vz || !p->u)) return fail(c, CRK_EINVAL, "kick needs v and u");
-    // opt-in (CRK_HYD_VARIANT=0005): c4 14.8 ms vs 13.3 for the i-centric list kernel (the per-pair
+    // opt-in (CRK_HYD_VARIANT=0005): c4 14.9 ms vs 12.3 for the i-centric list kernel (the per-pair
     // red.global reactions cost more than the halved pair work saves)
     if (lists_on(c) && !c->lay.partial && hyd_variant(3) == 5) return accel_symlist(c, p, dt, st);
     // gather variant: batch-32 pair-compacted evaluation (2: batch 64, 3: uncompacted)
