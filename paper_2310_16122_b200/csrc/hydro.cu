@@ -1077,6 +1077,37 @@ static crk_status accel_gather(crk_ctx* c, crk_particles* p, float dt, cudaStrea
     return launch_hyd<AccPass<false, BT>, ENT, 2>(c, g, st, "accel/dudt kernel");
 }
 
+// experiment (CRK_HYD_VARIANT=0004 / 0006): 8 lanes per i (4 i per warp, 16 warps per CTA, one
+// CTA per SM): a quarter-warp then reads one i's consecutive slots (no bank conflicts between
+// two i's) at the cost of the overlap between two CTAs' staging
+template <int ENT>
+static crk_status accel_s8(crk_ctx* c, crk_particles* p, float dt, cudaStream_t st) {
+    if (!lists_on(c)) return accel_gather<32, 72>(c, p, dt, st);
+    AccPass<false, 32> g;
+    common(c, g);
+    g.jrows = P<float4>(c->gpos);
+    g.jpay = P<float4>(c->grec);
+    g.grec = P<float4>(c->grec);
+    g.Cl = c->prm.av_cl; g.Cq = c->prm.av_cq; g.e2 = c->prm.av_eps2; g.dt = dt;
+    g.n = c->n;
+    g.ng = c->n_gas;
+    g.ahx = p->ahx; g.ahy = p->ahy; g.ahz = p->ahz; g.dudt = p->dudt;
+    g.vx = p->vx; g.vy = p->vy; g.vz = p->vz; g.u = p->u;
+    g.cnt = nullptr;
+    if (c->nleaf[2] == 0) return CRK_OK;
+    RowView rv = hydro_rows(c);
+    CRK_TRY(grow(c, c->work, 64, st));
+    CRK_TRY(cuda_check(c, (launch_list<AccPass<false, 32>, 16, 4, ENT, 1>(g, rv, list_view(c), st)), "accel/dudt kernel"));
+    c->launches++;
+    const ListView lv = list_view(c);
+    rv.rows = lv.frows;
+    rv.nrows = lv.nfrows;
+    CRK_TRY(cuda_check(c, (launch_pairs<AccPass<false, 32>, HYD_NW, HYD_G, 72, 2>(g, rv, c->nleaf[2], st)),
+                       "accel/dudt kernel"));
+    c->launches++;
+    return CRK_OK;
+}
+
 crk_status accel_dudt(crk_ctx* c, crk_particles* p, float dt, cudaStream_t st) {
     if (dt != 0.f && (!p->vx || !p->vy || !p->vz || !p->u)) return fail(c, CRK_EINVAL, "kick needs v and u");
     // opt-in (CRK_HYD_VARIANT=0005): c4 14.9 ms vs 12.3 for the i-centric list kernel (the per-pair
@@ -1086,6 +1117,8 @@ crk_status accel_dudt(crk_ctx* c, crk_particles* p, float dt, cudaStream_t st) {
     switch (hyd_variant(3)) {
         case 2: return accel_gather<64, 64>(c, p, dt, st);
         case 3: return accel_gather<0, 72>(c, p, dt, st);
+        case 4: return accel_s8<72>(c, p, dt, st);
+        case 6: return accel_s8<128>(c, p, dt, st);
         default: return accel_gather<32, 72>(c, p, dt, st);
     }
 }

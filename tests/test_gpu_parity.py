@@ -352,11 +352,12 @@ def test_gravity_symmetric_variants(var, name, monkeypatch):
     assert norm_err(a, ref["grav_a"], ref["grav_S"]) <= TOL_FORCE
 
 
+@pytest.mark.parametrize("var", ["0005", "0004", "0006"])
 @pytest.mark.parametrize("cap", ["70", "128"])
-def test_accel_symmetric_list_variant(cap, monkeypatch):
-    """Opt-in Newton-3 accel over the neighbour lists (CRK_HYD_VARIANT=0005), with complete
-    lists and with some rows flagged (gated i-centric fallback)."""
-    monkeypatch.setenv("CRK_HYD_VARIANT", "0005")
+def test_accel_symmetric_list_variant(cap, var, monkeypatch):
+    """Opt-in accel list variants: Newton-3 over the neighbour lists (CRK_HYD_VARIANT=0005) and
+    8 lanes per i (0004, 0006), with complete lists and with some rows flagged (fallbacks)."""
+    monkeypatch.setenv("CRK_HYD_VARIANT", var)
     monkeypatch.setenv("CRK_NBR_CAP", cap)
     parts, params = cached_config("c2z")
     params["symmetric"] = 1

@@ -18,6 +18,8 @@ PORTFOLIOS = {
     "lists, warp gravity without pipeline": {"CRK_GRAV_VARIANT": "6"},
     "lists, half-warp shuffle gravity (the paper's algorithm)": {"CRK_GRAV_VARIANT": "8"},
     "lists, Newton-3 accel": {"CRK_HYD_VARIANT": "0005"},
+    "lists, accel with 8 lanes per i (one 16-warp CTA per SM)": {"CRK_HYD_VARIANT": "0004"},
+    "lists, accel with 8 lanes per i, 128-entry staging rounds": {"CRK_HYD_VARIANT": "0006"},
     "on-the-fly culling everywhere (no neighbour lists)": {"CRK_NBR_CAP": "0", "CRK_GRAV_VARIANT": "7"},
 }
 PASSES = ["build_lists", "gravity_kick", "geometry", "corrections_extras", "hydro_accel_dudt"]
