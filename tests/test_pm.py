@@ -282,3 +282,93 @@ def test_gpu_slab_pm_two_processes():
     ref = oracle.pm_accel(parts["x"], parts["y"], parts["z"], parts["m"], params["box"], ng, rs)
     assert not np.isnan(g).any()
     assert np.max(np.abs(g - ref)) <= 1e-4 * np.abs(ref).max()
+
+
+class _FakeSlabPM:
+    """Test double with SlabPM's buffer shapes whose phases are position-dependent maps, so
+    that any misrouted chunk in a collective changes the result (no physics here)."""
+
+    def __init__(self, n, rank, P):
+        self.n, self.rank, self.P, self.nl, self.nzc = n, rank, P, n // P, n // 2 + 1
+
+    def sizes(self):
+        n, nl, P, nzc = self.n, self.nl, self.P, self.nzc
+        return dict(rho_full=n ** 3, rho_slab=nl * n * n, send=P * nl * nl * nzc, send3=P * 3 * nl * nl * nzc,
+                    acc_slab=3 * nl * n * n)
+
+    def deposit(self, x, y, z, m, stream=None):
+        import torch
+
+        rho = torch.zeros(self.n ** 3)
+        idx = (x.long() * self.n + y.long()) * self.n + z.long()
+        return rho.index_add_(0, idx, m)
+
+    def forward(self, rho_slab, stream=None):
+        import torch
+
+        k = torch.arange(self.sizes()["send"])
+        return torch.complex(rho_slab[k % rho_slab.numel()], (1000 * self.rank + k).float())
+
+    def solve(self, recv, stream=None):
+        import torch
+
+        k = torch.arange(self.sizes()["send3"])
+        return recv[k % recv.numel()] * (1 + self.rank) + k.float()
+
+    def inverse(self, recv3, stream=None):
+        import torch
+
+        k = torch.arange(self.sizes()["acc_slab"])
+        r = recv3[k % recv3.numel()]
+        return r.real + 0.5 * r.imag + self.rank
+
+    def interp(self, x, y, z, acc_full, stream=None):
+        i = ((x.long() * self.n + y.long()) * self.n + z.long()) % acc_full.numel()
+        return [acc_full[i], acc_full[(i + 1) % acc_full.numel()], acc_full[(i + 7) % acc_full.numel()]]
+
+
+def _seq_worker(rank, world, port, q):
+    import os
+
+    import torch
+    import torch.distributed as dist
+    from paper_2310_16122_b200.pm_dist import TorchComm, pm_accel_distributed
+
+    os.environ["MASTER_ADDR"] = "127.0.0.1"
+    os.environ["MASTER_PORT"] = str(port)
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    g = torch.Generator().manual_seed(100 + rank)
+    n = 8
+    x, y, z = (torch.randint(0, n, (50,), generator=g).float() for _ in range(3))
+    m = torch.rand(50, generator=g)
+    a = pm_accel_distributed(_FakeSlabPM(n, rank, world), x, y, z, m, comm=TorchComm())
+    q.put((rank, (x, y, z, m), [t.clone() for t in a]))
+    dist.destroy_process_group()
+
+
+def test_distributed_pm_sequence_matches_emulation_gloo_two_ranks():
+    """pm_accel_distributed over 2 gloo ranks (CPU, test-double phases) produces exactly what
+    the single-process emulation produces from the same per-rank inputs: the N>1 sequencing
+    is the one the GPU parity tests check against the oracle."""
+    import os
+
+    import torch
+    import torch.multiprocessing as mp
+    from paper_2310_16122_b200.pm_dist import pm_accel_emulated
+
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    port = 35500 + os.getpid() % 2000
+    procs = [ctx.Process(target=_seq_worker, args=(r, 2, port, q)) for r in range(2)]
+    for p in procs:
+        p.start()
+    res = {}
+    for _ in range(2):
+        r, inp, out = q.get(timeout=120)
+        res[r] = (inp, out)
+    for p in procs:
+        p.join(60)
+    emu = pm_accel_emulated([_FakeSlabPM(8, r, 2) for r in range(2)], [res[r][0] for r in range(2)])
+    for r in range(2):
+        for got, exp in zip(res[r][1], emu[r]):
+            assert torch.allclose(got, exp, rtol=1e-6, atol=1e-5)
