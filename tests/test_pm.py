@@ -372,3 +372,28 @@ def test_distributed_pm_sequence_matches_emulation_gloo_two_ranks():
     for r in range(2):
         for got, exp in zip(res[r][1], emu[r]):
             assert torch.allclose(got, exp, rtol=1e-6, atol=1e-5)
+
+
+@pytest.mark.gpu
+def test_gpu_slab_pm_rank_without_particles():
+    """A rank that owns no particles still takes part in every phase (deposits nothing,
+    interpolates for nobody); the other rank's particles get the oracle's force."""
+    import torch
+    from crk_testutil import cached_config
+    from paper_2310_16122_b200 import SlabPM
+    from paper_2310_16122_b200.pm_dist import pm_accel_emulated
+
+    parts, params = cached_config("c1")
+    ng, rs = 16, 0.7
+    dev = torch.device("cuda", 0)
+    full = tuple(torch.from_numpy(np.ascontiguousarray(parts[k])).to(dev) for k in ("x", "y", "z", "m"))
+    empty = tuple(torch.empty(0, dtype=torch.float32, device=dev) for _ in range(4))
+    spms = [SlabPM(ng, params["box"], rs, 1.0, r, 2) for r in range(2)]
+    acc = pm_accel_emulated(spms, [empty, full])
+    torch.cuda.synchronize()
+    assert all(t.numel() == 0 for t in acc[0])
+    g = np.stack([t.cpu().numpy() for t in acc[1]], 1)
+    ref = oracle.pm_accel(parts["x"], parts["y"], parts["z"], parts["m"], params["box"], ng, rs)
+    assert np.max(np.abs(g - ref)) <= 1e-4 * np.abs(ref).max()
+    for s in spms:
+        s.close()
