@@ -21,13 +21,19 @@ import numpy as np
 _HERE = os.path.dirname(os.path.abspath(__file__))
 _SRC = os.path.join(_HERE, "oracle.c")
 _LIB = os.path.join(_HERE, "liboracle.so")
+# tools/mutation_check.py points this at a deliberately mutated build of oracle.c to show that
+# the pins in tests/ catch each mutation; nothing else sets it
+_LIB_OVERRIDE = os.environ.get("CRK_ORACLE_LIB")
+
+CFLAGS = ["-O2", "-fopenmp", "-ffp-contract=off", "-fno-fast-math", "-std=c11", "-fPIC", "-shared"]
 
 
 def build(force: bool = False) -> str:
     """Compile oracle.c (gcc, fp64, no FP contraction so the fp32 predicate is exact)."""
+    if _LIB_OVERRIDE:
+        return _LIB_OVERRIDE
     if force or not os.path.exists(_LIB) or os.path.getmtime(_LIB) < os.path.getmtime(_SRC):
-        cmd = ["gcc", "-O2", "-fopenmp", "-ffp-contract=off", "-fno-fast-math", "-std=c11",
-               "-fPIC", "-shared", "-o", _LIB, _SRC, "-lm"]
+        cmd = ["gcc", *CFLAGS, "-o", _LIB, _SRC, "-lm"]
         subprocess.check_call(cmd)
     return _LIB
 

@@ -447,9 +447,11 @@ int orc_counts(int64_t n, const float* x, const float* y, const float* z, const 
 /* ------------------------------------------------------------------ O5: gravity
  * a_i = G sum_{j != i, s32 < rcut2} m_j x_ji [ (s + eps2)^-3/2 - sum_k c_k s^k ],
  * x_ji = x_j - x_i (minimum image), s = |x_ji|^2 in exact fp64.  All species.
- * S_i = sum_j G m_j |x_ji| ((s + eps2)^-3/2 + |P5(s)|): the parity-error normaliser of
- * SURVEY.md §8(c), taken term-wise because the pair term is a difference that cancels
- * at the cutoff (continuity constraint) — DESIGN.md §6.
+ * S_i = sum_j |a_ij| + 1e-2 sum_j G m_j |x_ji| ((s + eps2)^-3/2 + |P5(s)|): the
+ * parity-error normaliser of SURVEY.md §8(c) (sum of |pair terms|) plus a 1% floor of the
+ * two terms' magnitudes, because the pair term is a difference that the continuity
+ * constraint drives to zero at the cutoff, where fp32 cannot resolve it below the ulp of
+ * its terms (a lone pair at r_c) — DESIGN.md §6.
  * Kick: v_i += dt a_i (v_out; pass dt = 0 for forces only). */
 int orc_gravity(int64_t n, const float* x, const float* y, const float* z, const float* m,
                 const float* vx, const float* vy, const float* vz, const orc_params* p,
@@ -478,9 +480,9 @@ int orc_gravity(int64_t n, const float* x, const float* y, const float* z, const
                 double f = newton - poly;
                 double w = (double)p->G * (double)m[j] * f;
                 for (int q = 0; q < 3; ++q) a[q] += w * d[q];
-                /* error scale of the pair term: magnitudes of the two terms of the difference
-                 * (fp32 cancellation near the cutoff) */
-                s_abs += fabs((double)p->G * (double)m[j]) * (newton + fabs(poly)) * sqrt(s);
+                /* error scale: |pair term| plus a 1% floor of the magnitudes of the two terms
+                 * of the difference (fp32 cancellation near the cutoff) */
+                s_abs += fabs((double)p->G * (double)m[j]) * (fabs(f) + 1e-2 * (newton + fabs(poly))) * sqrt(s);
             }
             for (int q = 0; q < 3; ++q) acc[3 * t + q] = a[q];
             S[t] = s_abs;

@@ -209,11 +209,14 @@ def test_lists_superset_of_particle_pairs(c1):
 
 
 # ----------------------------------------------------------------- O2 counts
-def _np_s32(parts, idx):
-    """fp32 s = fma(dz,dz,fma(dy,dy,dx*dx)); exact emulation for quantised inputs (the
-    fp64 sum of q^2-multiples below 2^50 q^2 is exact, so one rounding to fp32 = fma)."""
-    P = np.stack([parts[k] for k in "xyz"], 1).astype(np.float64)[idx]
-    return P
+def _s32_emulated(d):
+    """fp32 s = fma(dz,dz, fma(dy,dy, dx*dx)) for rows of exact differences d (fp64): each
+    fp64 product and sum of q^2-multiples below 2^50 q^2 is exact, so rounding once to
+    fp32 after each step is the fused operation."""
+    d32 = d.astype(np.float32)
+    t = (d32[:, 0] * d32[:, 0]).astype(np.float32)
+    t = (d32[:, 1].astype(np.float64) * d32[:, 1] + t.astype(np.float64)).astype(np.float32)
+    return (d32[:, 2].astype(np.float64) * d32[:, 2] + t.astype(np.float64)).astype(np.float32)
 
 
 @pytest.mark.parametrize("name", ["lat:8,8,16:0.15:5", "c1"])
@@ -260,6 +263,22 @@ def test_predicate_strict_at_cutoff():
     assert np.all(oracle.gravity(outside, params)["a"] == 0)
 
 
+@pytest.mark.parametrize("kk,inside", [((1289220, 989691, 0), False), ((848717, 414813, 1322568), True)])
+def test_predicate_fp32_sequence_edge_cases(kk, inside):
+    """O2 is the fp32 sequence fma(dz,dz, fma(dy,dy, dx*dx)) with a strict '<' (q = 2^-19 here).
+    Pair 1: exact s = rcut2 - 3.9e-7 but the sequence rounds to exactly rcut2, so the pair is
+    OUT (a '<=' predicate, or one on the exact s, would take it in).  Pair 2: the sequence
+    gives 9.6099987 < rcut2, so the pair is IN, while rounding the exact s once to fp32 gives
+    rcut2 (out).  Both found by exhaustive search over quantised separations."""
+    box = [16.0] * 3
+    params = make_params(box)
+    q = 16.0 * 2.0**-23
+    d = np.asarray(kk, np.float64) * q
+    parts = make_parts(np.array([[1.0, 1, 1], 1.0 + d]), [0, 1], box)
+    assert np.array_equal(np.array([parts[k][1] - parts[k][0] for k in "xyz"], np.float64), d)
+    assert oracle.counts(parts, params)["grav"].tolist() == ([1, 1] if inside else [0, 0])
+
+
 # ----------------------------------------------------------------- O5 gravity
 def test_gravity_newtonian_limit():
     """P5 = 0, eps -> 0: inverse-square attraction of magnitude G m / r^2."""
@@ -275,6 +294,47 @@ def test_gravity_newtonian_limit():
         r = np.linalg.norm(dq)
         assert np.allclose(a[0], 2.0 * 1.3 * dq / r**3, rtol=1e-6, atol=0)
         assert np.allclose(a[1], -2.0 * 0.7 * dq / r**3, rtol=1e-6, atol=0)
+
+
+@pytest.mark.parametrize("eps2", [0.25, 0.7])
+def test_gravity_two_body_plummer_softened(eps2):
+    """O5 closed form with a large softening and P5 = 0: a_1 = G m_2 x_21 / (r^2 + eps^2)^{3/2}
+    (Plummer softening on s = r^2, PAPER.md:147 short-range force; SURVEY.md §8(c) O5 pin
+    "two-body closed form").  A softening applied to r instead, (r + eps)^-3, differs by
+    tens of percent at these separations."""
+    box = [16.0] * 3
+    params = make_params(box, eps2=eps2, poly=[0] * 6, G=1.5)
+    for d, (m1, m2) in (([0.3, -0.2, 0.1], (0.5, 2.0)), ([1.1, 0.7, -1.9], (1.25, 0.75)),
+                        ([-2.2, 1.4, 0.6], (0.9, 0.4))):
+        parts = make_parts(np.array([[8.0, 8, 8], 8 + np.asarray(d)]), [1, 0], box, m=[m1, m2])
+        a = oracle.gravity(parts, params)["a"]
+        x21 = np.array([parts[k][1] - parts[k][0] for k in "xyz"], np.float64)
+        s = float(x21 @ x21)
+        e = float(np.float32(eps2))
+        m1, m2 = float(np.float32(m1)), float(np.float32(m2))
+        assert np.allclose(a[0], 1.5 * m2 * x21 / (s + e) ** 1.5, rtol=1e-13, atol=0)
+        assert np.allclose(a[1], -1.5 * m1 * x21 / (s + e) ** 1.5, rtol=1e-13, atol=0)
+
+
+def test_gravity_error_normaliser_is_pair_sum_plus_floor(c1):
+    """S_i (the parity normaliser) lies between sum_j |a_ij| and 1.06 sum_j |a_ij|
+    on a lattice: the 1% floor of the two terms' magnitudes adds ~4%, not a multiple."""
+    parts, params = c1
+    n = parts["x"].shape[0]
+    tg = np.arange(0, n, 41)
+    g = oracle.gravity(parts, params, targets=tg)
+    P = np.stack([parts[k] for k in "xyz"], 1).astype(np.float64)
+    L = np.asarray(params["box"])
+    poly = np.asarray(params["poly"], np.float64)
+    rc2 = np.float32(params["rcut2"])
+    for t, i in enumerate(tg):
+        d = P - P[i]
+        d -= L * np.round(d / L)
+        s = (d * d).sum(1)
+        inside = (_s32_emulated(d) < rc2) & (np.arange(n) != i)
+        f = (s[inside] + params["eps2"]) ** -1.5 - sum(c * s[inside] ** k for k, c in enumerate(poly))
+        absum = (parts["m"][inside] * np.sqrt(s[inside]) * np.abs(f)).sum()
+        assert absum <= g["S"][t] <= 1.06 * absum
 
 
 @pytest.mark.parametrize("k", range(6))
@@ -460,6 +520,121 @@ def test_accel_two_particle_textbook_sph():
     assert np.allclose(out["a"][0], a1, rtol=1e-7)
     assert np.allclose(0.25 * out["a"][0], -0.375 * out["a"][1], rtol=1e-12)
     assert np.all(out["dudt"] == 0)
+
+
+def _wendland_g(r, H):
+    """(dW/dr)/r of the textbook Wendland C4 (analytic derivative of the polynomial in q)."""
+    q = r / H
+    t = max(1.0 - q, 0.0)
+    dwdq = -6 * t**5 * (1 + 6 * q + 35 / 3 * q * q) + t**6 * (6 + 70 / 3 * q)
+    return SIGMA / H**3 * dwdq / H / r
+
+
+_X2 = np.array([[5.0, 5, 5], [5.6, 5.8, 4.7]])  # x_12 = (-0.6, -0.8, 0.3), r = 1.04
+
+
+def _two_gas_accel(v, dv, H=2.0, rho=(1.0, 1.2), cs=(0.8, 1.1), P=(0.7, 1.3), V=(0.9, 1.1), m=(0.25, 0.375)):
+    """oracle.accel on two gas particles with forced plain-SPH coefficients (A=1, B=0,
+    grad A = grad B = 0) and prescribed rho, c, P, V, grad v; returns (out, x_12, g, v_12)."""
+    box = [16.0] * 3
+    params = make_params(box)
+    parts = make_parts(_X2, [1, 1], box, H=[H, H], m=list(m), v=np.asarray(v, np.float64))
+    n = 2
+    A, B, dA, dB = np.ones(n), np.zeros((n, 3)), np.zeros((n, 3)), np.zeros((n, 9))
+    out = oracle.accel(parts, params, np.asarray(V, float), A, B, dA, dB, np.asarray(rho, float),
+                       np.asarray(P, float), np.asarray(cs, float), np.asarray(dv, float).reshape(2, 9), [0, 1])
+    x12 = np.array([parts[k][0] - parts[k][1] for k in "xyz"], np.float64)
+    v12 = np.array([parts[k][0] - parts[k][1] for k in ("vx", "vy", "vz")], np.float64)
+    g = _wendland_g(float(np.linalg.norm(x12)), float(np.float32(H)))
+    return out, x12, g, v12, params
+
+
+def _q_textbook(mu, rho, cs, params):
+    """Q_ij = sum over the two particles of rho_k (-C_l c_k mu + C_q mu^2) (O9 AV), one mu
+    (equal H)."""
+    cl, cq = params["av_cl"], params["av_cq"]
+    return sum(r * (-cl * c * mu + cq * mu * mu) for r, c in zip(rho, cs))
+
+
+@pytest.mark.parametrize("approaching", [True, False])
+def test_accel_two_particle_viscosity_closed_form(approaching):
+    """O9 artificial viscosity on a head-on pair with A=1, B=0, grad v = 0 (so the limiter is
+    phi = 0 and v* = v_12): mu = v_12.eta/(eta^2 + eps_AV^2) < 0 for an approaching pair and
+    Q = sum_k rho_k (-C_l c_k mu + C_q mu^2) > 0; a receding pair has mu clamped to 0 and Q = 0.
+    a_1 = -(V1 V2/m1)(P1 + P2 + Q) g x_12 and du_1/dt = (V1 V2/m1)(P1 + Q/2) v_12.g x_12 with
+    g = W'(r)/r (PAPER.md:377 Acceleration/Energy)."""
+    u = np.array([0.3, 0.4, -0.15])
+    sgn = 1.0 if approaching else -1.0
+    v = np.array([sgn * u, -sgn * u])
+    out, x12, g, v12, params = _two_gas_accel(v, np.zeros((2, 9)))
+    H = float(np.float32(2.0))
+    eta = x12 / H
+    mu = min(0.0, float(v12 @ eta) / (float(eta @ eta) + params["av_eps2"]))
+    assert (mu < 0) == approaching
+    rho, cs, P, V, m = (1.0, 1.2), (0.8, 1.1), (0.7, 1.3), (0.9, 1.1), (0.25, 0.375)  # m exact in fp32
+    Q = _q_textbook(mu, rho, cs, params)
+    assert (Q > 0) == approaching
+    G = g * x12
+    a1 = -(V[0] * V[1] / m[0]) * (P[0] + P[1] + Q) * G
+    du1 = (V[0] * V[1] / m[0]) * (P[0] + 0.5 * Q) * float(v12 @ G)
+    a2 = (V[0] * V[1] / m[1]) * (P[0] + P[1] + Q) * G
+    du2 = (V[0] * V[1] / m[1]) * (P[1] + 0.5 * Q) * float(v12 @ G)
+    assert np.allclose(out["a"][0], a1, rtol=1e-12, atol=0)
+    assert np.allclose(out["a"][1], a2, rtol=1e-12, atol=0)
+    assert abs(out["dudt"][0] - du1) <= 1e-12 * abs(du1)
+    assert abs(out["dudt"][1] - du2) <= 1e-12 * abs(du2)
+
+
+@pytest.mark.parametrize("ab,phi", [((1.0, 2.0), 4 * 0.5 / 1.5**2), ((1.5, 1.5), 1.0), ((3.0, 1.0), 0.75),
+                                    ((3.0, -1.0), 0.0), ((1.0, 0.0), 0.0)])
+def test_accel_van_leer_limiter_closed_form(ab, phi):
+    """O9 limiter: with v = 0 and grad v_1 = a I, grad v_2 = b I, r = (x.grad v_1.x)/(x.grad v_2.x)
+    = a/b and phi = 4r/(1+r)^2 (0 for r <= 0 or a zero denominator), v* = -phi (a+b)/2 x_12,
+    so the viscous pressure Q enters the force through phi alone: r = 0.5 -> 8/9, 1 -> 1,
+    3 -> 3/4, -3 -> 0, b = 0 -> 0."""
+    a, b = ab
+    dv = np.stack([a * np.eye(3).ravel(), b * np.eye(3).ravel()])
+    out, x12, g, v12, params = _two_gas_accel(np.zeros((2, 3)), dv)
+    H = float(np.float32(2.0))
+    eta = x12 / H
+    vs = -0.5 * phi * (a + b) * x12
+    mu = min(0.0, float(vs @ eta) / (float(eta @ eta) + params["av_eps2"]))
+    rho, cs, P, V, m = (1.0, 1.2), (0.8, 1.1), (0.7, 1.3), (0.9, 1.1), (0.25, 0.375)
+    Q = _q_textbook(mu, rho, cs, params)
+    assert (Q > 0) == (phi > 0)
+    a1 = -(V[0] * V[1] / m[0]) * (P[0] + P[1] + Q) * g * x12
+    assert np.allclose(out["a"][0], a1, rtol=1e-12, atol=0)
+    assert np.all(out["dudt"] == 0)
+
+
+def test_extras_density_reproduces_linear_field():
+    """O8 RK density rho_i = sum_j m_j W^R_ij: with masses m_j = V_j f(x_j) for a linear f, CRK
+    linear reproduction (O7) gives rho_i = f(x_i) — this pins that the sum carries the
+    NEIGHBOUR's mass (the configs have equal gas masses, where m_i and m_j coincide)."""
+    box, parts = make_lattice((16, 16, 16), 0.15, 13, shuffle=False)
+    params = make_params(box)
+    gas = np.nonzero(parts["species"] == 1)[0]
+    V = oracle.geometry(parts, params, gas)  # V depends on positions and H only
+    P = np.stack([parts[k] for k in "xyz"], 1).astype(np.float64)
+    f = lambda x: 0.2 + 0.01 * x[:, 0] - 0.005 * x[:, 1] + 0.008 * x[:, 2]  # noqa: E731
+    parts["m"] = parts["m"].copy()
+    parts["m"][gas] = (V * f(P[gas])).astype(np.float32)
+    interior = gas[np.all((P[gas] > 5) & (P[gas] < 11), axis=1)][:25]
+    out = oracle.substep(parts, params, targets=interior)
+    # masses are fp32-rounded: agreement at fp32 input precision
+    assert np.allclose(out["rho"], f(P[interior]), rtol=3e-7, atol=0)
+
+
+def test_extras_sound_speed_closed_form(c1):
+    """O8 EOS: P = (gamma-1) rho u and c = sqrt(gamma P / rho), so c^2 = gamma (gamma-1) u
+    whatever the density: a closed form independent of the kernel sums."""
+    parts, params = c1
+    gas = np.nonzero(parts["species"] == 1)[0][::29]
+    out = oracle.substep(parts, params, targets=gas)
+    gam = params["gamma"]
+    u = parts["u"][gas].astype(np.float64)
+    assert np.allclose(out["cs"] ** 2, gam * (gam - 1) * u, rtol=1e-13, atol=0)
+    assert np.all(out["rho"] > 0.5 * 0.157) and np.all(out["rho"] < 2.0 * 0.157)
 
 
 # ----------------------------------------------------------------- oracle self-consistency
