@@ -65,7 +65,8 @@ def fit_poly_samples(s, f, rc: float, eps2: float, order: int = 5):
 
 def make_params(box, rc=3.1, eps2=0.01, G=1.0, gamma=5.0 / 3.0, av_cl=2.0, av_cq=1.0,
                 av_eps2=0.01, leaf_max_i=128, leaf_max_j=8, leaf_max_gas_i=64,
-                leaf_max_gas_j=8, cell_side=4.0, poly=None, symmetric=1, skin=0.0):
+                leaf_max_gas_j=8, cell_side=4.0, poly=None, symmetric=1, skin=0.0, grav_kernel=0,
+                hydro_kernel=0, nbr_cap=0):
     """Parameter set (SURVEY.md §8(b) crk_params; defaults §8(c) O5-O9, §8(d))."""
     box = [float(b) for b in box]
     if poly is None:
@@ -87,6 +88,8 @@ def make_params(box, rc=3.1, eps2=0.01, G=1.0, gamma=5.0 / 3.0, av_cl=2.0, av_cq
         cell_side=float(cell_side),
         symmetric=int(symmetric),  # kernel variant bitmask (solver option, not physics)
         skin=float(np.float32(skin)),  # list skin (solver option, not physics)
+        # kernel variants and neighbour-list capacity (solver options, include/crksr.h)
+        grav_kernel=int(grav_kernel), hydro_kernel=int(hydro_kernel), nbr_cap=int(nbr_cap),
     )
 
 

@@ -72,6 +72,20 @@ typedef struct crk_params {
                             after crk_drift steps totalling less than skin/2 per particle
                             crk_refresh renews the position-dependent data without re-sorting or
                             rebuilding the lists.  0 = off. */
+    int32_t grav_kernel; /* gravity kernel variant when symmetric & 1 (DESIGN.md §7 and the variant
+                            portfolio): 0 = the pipelined warp-independent
+                            Newton-3 kernel (the benchmarked default; the only one with domain
+                            decomposition, the others fall back to the i-centric kernel there),
+                            6 = warp-independent without the copy pipeline, 7 = CTA-staged,
+                            8 = the paper's half-warp XOR-shuffle algorithm.
+                            Other values: CRK_EINVAL. */
+    int32_t hydro_kernel;/* accel/du-dt kernel variant: 0 = i-centric list walk (default),
+                            4 = 8 lanes per i in 16-warp CTAs, 5 = Newton-3 over the lists (whole-box
+                            domains), 6 = as 4 with 128-entry staging rounds.  Other: CRK_EINVAL. */
+    int32_t nbr_cap;     /* gas neighbour-list capacity per particle (entries; lists built by
+                            crk_geometry, walked by corrections, extras and accel): 0 = default
+                            (128), < 0 = no lists (every gas pass culls on the fly), else the
+                            capacity (rows whose lists overflow it use the on-the-fly kernels). */
 } crk_params;
 
 /* Caller-owned particle arrays (device pointers).  Inputs are sorted IN PLACE by
@@ -196,7 +210,7 @@ crk_status crk_refresh(struct crk_ctx* ctx, crk_particles* parts, void* stream);
  * d2_(k) the k_ngb-th smallest O2 squared distance (s32) to another gas particle, selected
  * among its neighbour list.  Exact when d2_(k) < H_i^2 (the list holds every gas particle
  * within H_i); otherwise H_out is an upper bound (2 H_i if the list has fewer than k_ngb
- * entries) and the particle is counted in *n_unconverged (a device int32): rebuild with
+ * entries) (a device int32): rebuild with
  * H = H_out and update again.  H_out: device, length n, sorted order, gas entries written.
  * k_ngb in [1, 127], factor > 0 (CRK_EINVAL); needs the lists (CRK_ESTATE without). */
 crk_status crk_update_h(struct crk_ctx* ctx, crk_particles* parts, int32_t k_ngb, float factor, float* H_out,

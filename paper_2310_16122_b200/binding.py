@@ -44,6 +44,7 @@ class CrkParams(C.Structure):
         ("symmetric", C.c_int32),
         ("dom_lo", C.c_int32 * 3), ("dom_hi", C.c_int32 * 3),
         ("skin", C.c_float),
+        ("grav_kernel", C.c_int32), ("hydro_kernel", C.c_int32), ("nbr_cap", C.c_int32),
     ]
 
 
@@ -137,6 +138,9 @@ def params_struct(p: dict) -> CrkParams:
     s.dom_lo[:] = list(p.get("dom_lo", (0, 0, 0)))
     s.dom_hi[:] = list(p.get("dom_hi", (0, 0, 0)))
     s.skin = float(p.get("skin", 0.0))
+    s.grav_kernel = int(p.get("grav_kernel", 0))
+    s.hydro_kernel = int(p.get("hydro_kernel", 0))
+    s.nbr_cap = int(p.get("nbr_cap", 0))
     return s
 
 

@@ -4,7 +4,6 @@
 #include <cstring>
 #include <new>
 
-#include <cstdlib>
 
 #include "common.cuh"
 
@@ -144,6 +143,13 @@ static crk_status validate(const crk_params* p, Layout& L, std::string& why) {
     }
     if (!(p->skin >= 0.f) || p->skin >= p->cell_side) { why = "skin must be in [0, cell_side)"; return CRK_EINVAL; }
     if (p->skin > 0.f && L.partial) { why = "a skin needs a whole-box domain"; return CRK_EINVAL; }
+    if (!(p->grav_kernel == 0 || p->grav_kernel == 6 || p->grav_kernel == 7 || p->grav_kernel == 8)) {
+        why = "grav_kernel must be 0, 6, 7 or 8"; return CRK_EINVAL;
+    }
+    if (!(p->hydro_kernel == 0 || (p->hydro_kernel >= 4 && p->hydro_kernel <= 6))) {
+        why = "hydro_kernel must be 0, 4, 5 or 6"; return CRK_EINVAL;
+    }
+    if (p->nbr_cap > 65535) { why = "nbr_cap must be <= 65535"; return CRK_EINVAL; }
     return CRK_OK;
 }
 
@@ -180,10 +186,8 @@ crk_status crk_create(const crk_params* params, int device, crk_ctx** out) {
         delete c;
         return CRK_ECUDA;
     }
-    // gas neighbour-list capacity per particle (CRK_NBR_CAP: tests force overflow / 0 = off)
-    const char* nc = getenv("CRK_NBR_CAP");
-    c->nbr_cap = nc ? atoi(nc) : 128;
-    if (c->nbr_cap < 0) c->nbr_cap = 0;
+    // gas neighbour-list capacity per particle (crk_params.nbr_cap: 0 = default, < 0 = off)
+    c->nbr_cap = params->nbr_cap == 0 ? 128 : (params->nbr_cap < 0 ? 0 : params->nbr_cap);
     // the gravity kernel's dynamic shared memory fits in the default 48 KB
     *out = c;
     return CRK_OK;

@@ -8,6 +8,8 @@
 // HBM-bound; every kernel is a streaming pass except the list kernels (one warp per i-leaf).
 #include <cub/cub.cuh>
 
+#include <cstring>
+#include <cmath>
 #include "common.cuh"
 
 namespace crk {
@@ -643,11 +645,24 @@ crk_status build_lists(crk_ctx* c, crk_particles* p, cudaStream_t st) {
         Readback rb;
         for (int s = 0; s < 4; ++s) rb.add(cnt + s * (L.ncm + 1) + L.ncm, 4 * s, 4);
         rb.add(P<int32_t>(c->grank) + n, 16, 4);
+        rb.add(P<int32_t>(c->dev_scalars), 20, 4);  // max fl32(H^2) over gas (k_gas_pack), float bits
         CRK_TRY(readback(c, rb, st));
     }
     CRK_TRY(cuda_check(c, cudaStreamSynchronize(st), "sync"));
     for (int s = 0; s < 4; ++s) c->nleaf[s] = host[s];
     c->n_gas = host[4];
+    {
+        // packed list entries keep the j-leaf index in 26 bits (leaf | shift << 26)
+        if (c->nleaf[1] >= (1 << 26) || c->nleaf[3] >= (1 << 26))
+            return fail(c, CRK_ECAPACITY, "more than 2^26 - 1 j-leaves (packed list entries)");
+        // H < box/4 (as r_c): the minimum-image and one-shift list search assume it
+        const int32_t hb = host[5];
+        float h2max;
+        memcpy(&h2max, &hb, 4);
+        for (int a = 0; a < 3; ++a)
+            if (!(std::sqrt((double)h2max) < c->prm.box[a] / 4))
+                return fail(c, CRK_EINVAL, "every gas H must be < box/4");
+    }
     for (int s = 0; s < 4; ++s) {
         const int64_t nl = c->nleaf[s] > 0 ? c->nleaf[s] : 1;
         CRK_TRY(grow(c, c->lfirst[s], nl * 4, st));

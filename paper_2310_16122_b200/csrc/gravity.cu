@@ -598,7 +598,7 @@ __global__ void __launch_bounds__(symw::NW * 32, 16 / symw::NW) grav_warp_kernel
 // ------------------------------------------------------------ half-warp shuffle variant
 // The paper's "half-warp" algorithm (Figs. half-warp-layout and
 // half-warp-shuffle), kept as a measured variant (
-// CRK_GRAV_VARIANT=8): lanes 0-15 hold the 16 i-particles of a work item, lanes 16-31 the
+// crk_params.grav_kernel = 8): lanes 0-15 hold the 16 i-particles of a work item, lanes 16-31 the
 // particles of two surviving j-leaves (8 lanes each).  In step k = 0..15 every lane
 // exchanges its particle with lane ^ (16 | k) by __shfl_xor_sync and adds the force its
 // partner exerts on its own particle: lane l < 16 evaluates (i_l, j), its partner the
@@ -1040,13 +1040,6 @@ static cudaError_t launch_grav_sym(crk_ctx* c, GravSymArgs& A, cudaStream_t st) 
     return cudaGetLastError();
 }
 
-// CRK_GRAV_VARIANT: 0 pipelined warp-independent kernel (default; the only one with domain
-// decomposition support), 6 unpipelined, 1-5 and 7 CTA-staged, 8 the paper's half-warp
-// shuffle (experiments)
-static int grav_variant() {
-    const char* gv = getenv("CRK_GRAV_VARIANT");
-    return gv ? atoi(gv) : 0;
-}
 
 static crk_status gravity_sym(crk_ctx* c, crk_particles* p, float dt, cudaStream_t st) {
     const int64_t n = c->n;
@@ -1071,7 +1064,7 @@ static crk_status gravity_sym(crk_ctx* c, crk_particles* p, float dt, cudaStream
         A.inv_q = c->lay.inv_q;
         A.cs = c->lay.cs;
         for (int d = 0; d < 3; ++d) { A.dlo[d] = c->lay.dlo[d]; A.dhi[d] = c->lay.dhi[d]; }
-        const int var = grav_variant();
+        const int var = c->prm.grav_kernel;
         CRK_TRY(grow(c, c->work, 64, st));
         CRK_TRY(cuda_check(c, zero_async(c->work.p, 16, st, c), "memset"));
         A.work = P<int>(c->work);
@@ -1079,11 +1072,6 @@ static crk_status gravity_sym(crk_ctx* c, crk_particles* p, float dt, cudaStream
         // measured on c4 (profiles/r01): <8 warps, 320 entries, 1 buffer> 24.6 ms, <4, 320, 1> 30.3,
         // <8, 320, 2> 36.2, <4, 256, 2> 41.9 (the second row buffer costs occupancy)
         switch (var) {
-        case 1: e = launch_grav_sym<4, 320, 1>(c, A, st); break;
-        case 2: e = launch_grav_sym<8, 320, 2>(c, A, st); break;
-        case 3: e = launch_grav_sym<8, 320, 1, 8, 3>(c, A, st); break;
-        case 4: e = launch_grav_sym<16, 320, 1, 8, 1>(c, A, st); break;
-        case 5: e = launch_grav_sym<8, 256, 1, 8, 3>(c, A, st); break;
         case 6: {  // warp-independent (c4: 17.3 ms vs 20.4 for <8, 320, 1>)
             A.split = (c->prm.leaf_max_i + symw::G - 1) / symw::G;
             A.nitems = (int)(c->nleaf[0] * A.split);
@@ -1129,7 +1117,7 @@ static crk_status gravity_sym(crk_ctx* c, crk_particles* p, float dt, cudaStream
 
 crk_status gravity_kick(crk_ctx* c, crk_particles* p, float dt, cudaStream_t st) {
     if (dt != 0.f && (!p->vx || !p->vy || !p->vz)) return fail(c, CRK_EINVAL, "kick needs vx, vy, vz");
-    if ((c->prm.symmetric & 1) && (!c->lay.partial || grav_variant() == 0)) return gravity_sym(c, p, dt, st);
+    if ((c->prm.symmetric & 1) && (!c->lay.partial || c->prm.grav_kernel == 0)) return gravity_sym(c, p, dt, st);
     return launch_grav<false>(c, p, dt, nullptr, st);
 }
 

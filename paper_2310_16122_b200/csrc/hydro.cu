@@ -5,8 +5,6 @@
 // Gas state lives in the ctx in gas-rank order (gpos, gvel, gV, gcoef, grec) so that
 // the j-tiles of every pass are contiguous; the caller's per-particle outputs are
 // written at gas_idx[k] in each pass epilogue.
-#include <cstdlib>
-#include <cstring>
 
 #include "pairs.cuh"
 
@@ -478,16 +476,6 @@ __device__ __forceinline__ void grad_wr(const float* Ah, const float* dAh, const
     }
 }
 
-// pair-compacted variants of the gather passes (pairs.cuh batch_of): same arithmetic, the
-// in-range test is the passes' own (s32 < H_i^2)
-template <class Base, int BT>
-struct Compacted : Base {
-    static constexpr int BATCH = BT;
-    __device__ __forceinline__ bool in(const typename Base::I& s, const float4& jp) const {
-        return s32_of(s.x - jp.x, s.y - jp.y, s.z - jp.z) < s.H2;
-    }
-};
-
 template <bool COUNT, int BATCH_ = 32>
 struct AccPass : HydCommon {
     static constexpr int PAY = COUNT ? 0 : 9;
@@ -843,12 +831,6 @@ static crk_status launch_hyd(crk_ctx* c, const Pass& ps, cudaStream_t st, const 
     return CRK_OK;
 }
 
-// tuning hook (experiments only): CRK_HYD_VARIANT=<digit per pass: geo cor ext acc>, 0 = default, 1 = G4
-static int hyd_variant(int pass) {
-    const char* v = getenv("CRK_HYD_VARIANT");
-    if (!v || (int)strlen(v) <= pass) return 0;
-    return v[pass] - '0';
-}
 
 static void common(crk_ctx* c, HydCommon& h) {
     h.gpos = P<float4>(c->gpos);
@@ -914,7 +896,6 @@ crk_status geometry(crk_ctx* c, crk_particles* p, cudaStream_t st) {
     g.gposV = P<float4>(c->gposV);
     g.Vout = p->V;
     g.cnt = nullptr;
-    if (hyd_variant(0) == 1) return launch_hyd<GeoPass<false>, 128, 1, 16, 4>(c, g, st, "geometry kernel");
     return launch_hyd<GeoPass<false>, 128, 2>(c, g, st, "geometry kernel");
 }
 
@@ -933,12 +914,7 @@ static CorPass cor_pass(crk_ctx* c, crk_particles* p) {
 crk_status corrections(crk_ctx* c, crk_particles* p, cudaStream_t st) {
     CorPass g = cor_pass(c, p);
     if (lists_on(c)) return launch_listed<CorPass, 128, 3, 128, 3>(c, g, st, "corrections kernel");
-    switch (hyd_variant(1)) {
-        case 1: return launch_hyd<CorPass, 128, 1, 16, 4>(c, g, st, "corrections kernel");
-        case 2: return launch_hyd<Compacted<CorPass, 32>, 128, 3>(c, {g}, st, "corrections kernel");
-        case 3: return launch_hyd<Compacted<CorPass, 64>, 128, 3>(c, {g}, st, "corrections kernel");
-        default: return launch_hyd<CorPass, 128, 3>(c, g, st, "corrections kernel");
-    }
+    return launch_hyd<CorPass, 128, 3>(c, g, st, "corrections kernel");
 }
 
 __global__ void k_gather_gas_state(int64_t ng, const int32_t* gas_idx, const float* vx, const float* vy,
@@ -979,12 +955,7 @@ crk_status extras(crk_ctx* c, crk_particles* p, cudaStream_t st) {
     CRK_TRY(gather_gas_state(c, p, st));
     ExtPass g = ext_pass(c, p);
     if (lists_on(c)) return launch_listed<ExtPass, 128, 3, 128, 3>(c, g, st, "extras kernel");
-    switch (hyd_variant(2)) {
-        case 1: return launch_hyd<ExtPass, 128, 1, 16, 4>(c, g, st, "extras kernel");
-        case 2: return launch_hyd<Compacted<ExtPass, 32>, 128, 3>(c, {g}, st, "extras kernel");
-        case 3: return launch_hyd<Compacted<ExtPass, 64>, 128, 3>(c, {g}, st, "extras kernel");
-        default: return launch_hyd<ExtPass, 128, 3>(c, g, st, "extras kernel");
-    }
+    return launch_hyd<ExtPass, 128, 3>(c, g, st, "extras kernel");
 }
 
 // a5 + a6 fused: one list kernel walks each i's list twice (Corrections, then Extras with
@@ -1077,7 +1048,7 @@ static crk_status accel_gather(crk_ctx* c, crk_particles* p, float dt, cudaStrea
     return launch_hyd<AccPass<false, BT>, ENT, 2>(c, g, st, "accel/dudt kernel");
 }
 
-// experiment (CRK_HYD_VARIANT=0004 / 0006): 8 lanes per i (4 i per warp, 16 warps per CTA, one
+// experiment (crk_params.hydro_kernel = 4 / 6): 8 lanes per i (4 i per warp, 16 warps per CTA, one
 // CTA per SM): a quarter-warp then reads one i's consecutive slots (no bank conflicts between
 // two i's) at the cost of the overlap between two CTAs' staging
 template <int ENT>
@@ -1110,13 +1081,10 @@ static crk_status accel_s8(crk_ctx* c, crk_particles* p, float dt, cudaStream_t 
 
 crk_status accel_dudt(crk_ctx* c, crk_particles* p, float dt, cudaStream_t st) {
     if (dt != 0.f && (!p->vx || !p->vy || !p->vz || !p->u)) return fail(c, CRK_EINVAL, "kick needs v and u");
-    // opt-in (CRK_HYD_VARIANT=0005): c4 14.9 ms vs 12.3 for the i-centric list kernel (the per-pair
+    // opt-in (hydro_kernel = 5): c4 14.9 ms vs 12.3 for the i-centric list kernel (the per-pair
     // red.global reactions cost more than the halved pair work saves)
-    if (lists_on(c) && !c->lay.partial && hyd_variant(3) == 5) return accel_symlist(c, p, dt, st);
-    // gather variant: batch-32 pair-compacted evaluation (2: batch 64, 3: uncompacted)
-    switch (hyd_variant(3)) {
-        case 2: return accel_gather<64, 64>(c, p, dt, st);
-        case 3: return accel_gather<0, 72>(c, p, dt, st);
+    if (lists_on(c) && !c->lay.partial && c->prm.hydro_kernel == 5) return accel_symlist(c, p, dt, st);
+    switch (c->prm.hydro_kernel) {
         case 4: return accel_s8<72>(c, p, dt, st);
         case 6: return accel_s8<128>(c, p, dt, st);
         default: return accel_gather<32, 72>(c, p, dt, st);
@@ -1140,7 +1108,7 @@ crk_status hydro_count(crk_ctx* c, int32_t* cgather, int32_t* csym, cudaStream_t
 }
 
 crk_status update_h(crk_ctx* c, int kth, float factor, float* H_out, int32_t* n_unconverged, cudaStream_t st) {
-    if (!lists_on(c)) return fail(c, CRK_ESTATE, "update_h needs the neighbour lists (CRK_NBR_CAP > 0)");
+    if (!lists_on(c)) return fail(c, CRK_ESTATE, "update_h needs the neighbour lists (crk_params.nbr_cap >= 0)");
     CRK_TRY(cuda_check(c, zero_async(n_unconverged, sizeof(int32_t), st, c), "memset"));
     k_update_h<<<(unsigned)c->nleaf[2], 64, 0, st>>>(hydro_rows(c), list_view(c), P<float4>(c->gpos),
                                                      P<int32_t>(c->gas_idx), kth, factor, H_out, n_unconverged);

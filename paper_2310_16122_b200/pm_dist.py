@@ -9,6 +9,8 @@ on one GPU.
 """
 from __future__ import annotations
 
+import contextlib
+
 import torch
 
 
@@ -69,22 +71,38 @@ def emu_all_gather(parts):
 
 def pm_accel_distributed(spm, x, y, z, m, comm=None, stream=None):
     """Long-range acceleration of this rank's particles (x, y, z, m device tensors) with the
-    mesh slab-decomposed over the ranks of ``comm`` (default: the torch.distributed world)."""
+    mesh slab-decomposed over the ranks of ``comm`` (default: the torch.distributed world).
+
+    Everything — the SlabPM kernels, the collectives and the buffers' allocations — is
+    issued on ONE stream, ``stream`` (default: the current stream), made current for the
+    whole sequence: torch.distributed orders its collectives after the current stream's
+    work, and the caching allocator ties each buffer to the stream that allocated it, so no
+    kernel can read a buffer before the collective that fills it lands, nor a buffer be
+    reused while a collective still reads it.  The caller's inputs must be ready on
+    ``stream`` (it waits for the current stream when a different one is given)."""
     comm = comm or TorchComm()
     sz = spm.sizes()
-    rho = spm.deposit(x, y, z, m, stream)
-    rho_slab = torch.empty(sz["rho_slab"], dtype=torch.float32, device=rho.device)
-    comm.reduce_scatter(rho_slab, rho)
-    send = spm.forward(rho_slab, stream)
-    recv = torch.empty_like(send)
-    comm.all_to_all(recv, send)
-    send3 = spm.solve(recv, stream)
-    recv3 = torch.empty_like(send3)
-    comm.all_to_all(recv3, send3)
-    acc = spm.inverse(recv3, stream)
-    acc_full = torch.empty(spm.P * acc.numel(), dtype=torch.float32, device=acc.device)
-    comm.all_gather(acc_full, acc)
-    return spm.interp(x, y, z, acc_full, stream)
+    on_gpu = x.device.type == "cuda"  # (CPU tensors: the test doubles of tests/test_pm.py)
+    if on_gpu and stream is not None:
+        stream.wait_stream(torch.cuda.current_stream(x.device))
+    with torch.cuda.stream(stream) if on_gpu and stream is not None else contextlib.nullcontext():
+        rho = spm.deposit(x, y, z, m)
+        rho_slab = torch.empty(sz["rho_slab"], dtype=torch.float32, device=rho.device)
+        comm.reduce_scatter(rho_slab, rho)
+        send = spm.forward(rho_slab)
+        recv = torch.empty_like(send)
+        comm.all_to_all(recv, send)
+        send3 = spm.solve(recv)
+        recv3 = torch.empty_like(send3)
+        comm.all_to_all(recv3, send3)
+        acc = spm.inverse(recv3)
+        acc_full = torch.empty(spm.P * acc.numel(), dtype=torch.float32, device=acc.device)
+        comm.all_gather(acc_full, acc)
+        out = spm.interp(x, y, z, acc_full)
+    if on_gpu and stream is not None:
+        for t in (x, y, z, *out):
+            t.record_stream(stream)
+    return out
 
 
 def pm_accel_emulated(spms, parts):

@@ -4,6 +4,15 @@ import numpy as np
 _CACHE = {}
 
 
+def free_port() -> int:
+    """A TCP port on 127.0.0.1 that is free right now (for gloo rendezvous in the tests)."""
+    import socket
+
+    with socket.socket() as sk:
+        sk.bind(("127.0.0.1", 0))
+        return sk.getsockname()[1]
+
+
 def cached_config(name, **kw):
     """Generator outputs are deterministic; cache them per session."""
     from gen import make_config

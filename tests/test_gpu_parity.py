@@ -315,13 +315,13 @@ def test_clustered_config3_full_chain_sampled_symmetric_modes():
 
 @pytest.mark.parametrize("fused", [True, False])
 @pytest.mark.parametrize("cap", [0, 16, 70, 128])
-def test_neighbour_list_capacities(cap, fused, monkeypatch):
+def test_neighbour_list_capacities(cap, fused):
     """The gas passes read the neighbour lists built by geometry; rows whose lists overflow
     the per-particle capacity run the on-the-fly kernels.  cap 0: lists off; 16: every row
     overflows; 70: a mix (sym counts ~64-80 on c2z); 128: no overflow."""
-    monkeypatch.setenv("CRK_NBR_CAP", str(cap))
     parts, params = cached_config("c2z")
     params["symmetric"] = 1
+    params["nbr_cap"] = cap if cap > 0 else -1
     g = run_gpu(parts, params, counts=False, fused=fused)
     ref = oracle.substep(parts, params)
     gi = g["in"]
@@ -338,13 +338,13 @@ def test_neighbour_list_capacities(cap, fused, monkeypatch):
     assert norm_err(gi["dudt"][T], ref["dudt"], ref["Sdu"]) <= TOL_FORCE
 
 
-@pytest.mark.parametrize("var", ["0", "1", "6", "7", "8"])
+@pytest.mark.parametrize("var", [0, 6, 7, 8])
 @pytest.mark.parametrize("name", ["c1", "c2z"])
-def test_gravity_symmetric_variants(var, name, monkeypatch):
-    """Every Newton-3 gravity kernel variant (CRK_GRAV_VARIANT) against the oracle."""
-    monkeypatch.setenv("CRK_GRAV_VARIANT", var)
+def test_gravity_symmetric_variants(var, name):
+    """Every Newton-3 gravity kernel variant (crk_params.grav_kernel) against the oracle."""
     parts, params = cached_config(name)
     params["symmetric"] = 1
+    params["grav_kernel"] = var
     g = run_gpu(parts, params, counts=False, hydro=False)
     ref = oracle.substep(parts, params)
     gi = g["in"]
@@ -352,15 +352,15 @@ def test_gravity_symmetric_variants(var, name, monkeypatch):
     assert norm_err(a, ref["grav_a"], ref["grav_S"]) <= TOL_FORCE
 
 
-@pytest.mark.parametrize("var", ["0005", "0004", "0006"])
-@pytest.mark.parametrize("cap", ["70", "128"])
-def test_accel_symmetric_list_variant(cap, var, monkeypatch):
-    """Opt-in accel list variants: Newton-3 over the neighbour lists (CRK_HYD_VARIANT=0005) and
-    8 lanes per i (0004, 0006), with complete lists and with some rows flagged (fallbacks)."""
-    monkeypatch.setenv("CRK_HYD_VARIANT", var)
-    monkeypatch.setenv("CRK_NBR_CAP", cap)
+@pytest.mark.parametrize("var", [5, 4, 6])
+@pytest.mark.parametrize("cap", [70, 128])
+def test_accel_symmetric_list_variant(cap, var):
+    """Opt-in accel list variants: Newton-3 over the neighbour lists (hydro_kernel 5) and
+    8 lanes per i (4, 6), with complete lists and with some rows flagged (fallbacks)."""
     parts, params = cached_config("c2z")
     params["symmetric"] = 1
+    params["hydro_kernel"] = var
+    params["nbr_cap"] = cap
     g = run_gpu(parts, params, counts=False)
     ref = oracle.substep(parts, params)
     gi = g["in"]

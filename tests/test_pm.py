@@ -8,6 +8,8 @@ import math
 import numpy as np
 import pytest
 
+from crk_testutil import free_port
+
 import oracle
 
 
@@ -191,7 +193,8 @@ def _comm_worker(rank, world, port, q):
         ag = torch.empty(6)
         comm.all_gather(ag, part)
         out[name] = (rs, aa, ag)
-    q.put((rank, full, a2a, part, out))
+    q.put((rank, full.numpy(), a2a.numpy(), part.numpy(),
+           {k: tuple(t.numpy() for t in v) for k, v in out.items()}))
     dist.destroy_process_group()
 
 
@@ -207,14 +210,15 @@ def test_slab_pm_collectives_match_emulation_gloo_two_ranks():
 
     ctx = mp.get_context("spawn")
     q = ctx.Queue()
-    port = 31500 + os.getpid() % 2000
+    port = free_port()
     procs = [ctx.Process(target=_comm_worker, args=(r, 2, port, q)) for r in range(2)]
     for p in procs:
         p.start()
     res = {}
     for _ in range(2):
-        r, *rest = q.get(timeout=120)
-        res[r] = rest
+        r, full, a2a, part, out = q.get(timeout=120)
+        T = torch.from_numpy
+        res[r] = [T(full), T(a2a), T(part), {k: tuple(T(t) for t in v) for k, v in out.items()}]
     for p in procs:
         p.join(60)
     rs = emu_reduce_scatter([res[r][0] for r in range(2)])
@@ -268,7 +272,7 @@ def test_gpu_slab_pm_two_processes():
     ng, rs = 64, 0.69
     ctx = mp.get_context("spawn")
     q = ctx.Queue()
-    port = 33500 + os.getpid() % 2000
+    port = free_port()
     procs = [ctx.Process(target=_slab_pm_worker, args=(r, 2, port, ng, rs, q)) for r in range(2)]
     for p in procs:
         p.start()
@@ -342,7 +346,7 @@ def _seq_worker(rank, world, port, q):
     x, y, z = (torch.randint(0, n, (50,), generator=g).float() for _ in range(3))
     m = torch.rand(50, generator=g)
     a = pm_accel_distributed(_FakeSlabPM(n, rank, world), x, y, z, m, comm=TorchComm())
-    q.put((rank, (x, y, z, m), [t.clone() for t in a]))
+    q.put((rank, tuple(t.numpy() for t in (x, y, z, m)), [t.numpy().copy() for t in a]))
     dist.destroy_process_group()
 
 
@@ -358,14 +362,14 @@ def test_distributed_pm_sequence_matches_emulation_gloo_two_ranks():
 
     ctx = mp.get_context("spawn")
     q = ctx.Queue()
-    port = 35500 + os.getpid() % 2000
+    port = free_port()
     procs = [ctx.Process(target=_seq_worker, args=(r, 2, port, q)) for r in range(2)]
     for p in procs:
         p.start()
     res = {}
     for _ in range(2):
         r, inp, out = q.get(timeout=120)
-        res[r] = (inp, out)
+        res[r] = (tuple(torch.from_numpy(t) for t in inp), [torch.from_numpy(t) for t in out])
     for p in procs:
         p.join(60)
     emu = pm_accel_emulated([_FakeSlabPM(8, r, 2) for r in range(2)], [res[r][0] for r in range(2)])

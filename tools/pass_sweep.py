@@ -1,7 +1,7 @@
-"""Per-pass CUDA-event times of one workload under several env-var variants, generated once.
+"""Per-pass CUDA-event times of one workload under several solver options, generated once.
 
-  python tools/pass_sweep.py --config c4 --steps 5 "CRK_GRAV_VARIANT=0" "CRK_GRAV_VARIANT=3" ...
-Each argument is a space-separated list of VAR=value settings applied before a fresh Solver.
+  python tools/pass_sweep.py --config c4 --steps 5 "grav_kernel=0" "grav_kernel=6 nbr_cap=-1" ...
+Each argument is a space-separated list of crk_params key=value settings for a fresh Solver.
 """
 import argparse, os, sys, json
 sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
@@ -17,11 +17,9 @@ a = ap.parse_args()
 parts, params = make_config(a.config)
 passes = ["build_lists", "gravity_kick", "geometry", "corrections_extras", "hydro_accel_dudt"]
 for var in a.variants:
-    for kv in var.split():
-        k, v = kv.split("=", 1)
-        os.environ[k] = v
+    opts = {kv.split("=", 1)[0]: int(kv.split("=", 1)[1]) for kv in var.split()}
     p = Particles.from_host(parts, "cuda")
-    s = Solver(params, 0)
+    s = Solver(dict(params, **opts), 0)
     st = torch.cuda.current_stream()
     ev = {k: [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)) for _ in range(a.steps)]
           for k in passes}

@@ -14,13 +14,13 @@ from paper_2310_16122_b200 import Particles, Solver
 
 PORTFOLIOS = {
     "lists + pipelined Newton-3 gravity (default)": {},
-    "lists, CTA-staged Newton-3 gravity": {"CRK_GRAV_VARIANT": "7"},
-    "lists, warp gravity without pipeline": {"CRK_GRAV_VARIANT": "6"},
-    "lists, half-warp shuffle gravity (the paper's algorithm)": {"CRK_GRAV_VARIANT": "8"},
-    "lists, Newton-3 accel": {"CRK_HYD_VARIANT": "0005"},
-    "lists, accel with 8 lanes per i (one 16-warp CTA per SM)": {"CRK_HYD_VARIANT": "0004"},
-    "lists, accel with 8 lanes per i, 128-entry staging rounds": {"CRK_HYD_VARIANT": "0006"},
-    "on-the-fly culling everywhere (no neighbour lists)": {"CRK_NBR_CAP": "0", "CRK_GRAV_VARIANT": "7"},
+    "lists, CTA-staged Newton-3 gravity": {"grav_kernel": 7},
+    "lists, warp gravity without pipeline": {"grav_kernel": 6},
+    "lists, half-warp shuffle gravity (the paper's algorithm)": {"grav_kernel": 8},
+    "lists, Newton-3 accel": {"hydro_kernel": 5},
+    "lists, accel with 8 lanes per i (one 16-warp CTA per SM)": {"hydro_kernel": 4},
+    "lists, accel with 8 lanes per i, 128-entry staging rounds": {"hydro_kernel": 6},
+    "on-the-fly culling everywhere (no neighbour lists)": {"nbr_cap": -1, "grav_kernel": 7},
 }
 PASSES = ["build_lists", "gravity_kick", "geometry", "corrections_extras", "hydro_accel_dudt"]
 
@@ -31,12 +31,9 @@ ap.add_argument("--out", default="gpurun_out/variant_portfolio.json")
 a = ap.parse_args()
 parts, params = make_config(a.config)
 times = {}
-for name, env in PORTFOLIOS.items():
-    for k in ("CRK_GRAV_VARIANT", "CRK_HYD_VARIANT", "CRK_NBR_CAP"):
-        os.environ.pop(k, None)
-    os.environ.update(env)
+for name, opts in PORTFOLIOS.items():
     p = Particles.from_host(parts, "cuda", outputs="forces")
-    s = Solver(params, 0)
+    s = Solver(dict(params, **opts), 0)
     st = torch.cuda.current_stream()
     ev = {k: [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)) for _ in range(a.steps)]
           for k in PASSES}
