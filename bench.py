@@ -107,9 +107,28 @@ def dist_env():
     return rank, world, local
 
 
-def oracle_sample(parts, params, cnts, n_grav=20000, n_gas=1500, seed=1):
+def _cpu_model():
+    try:
+        out = subprocess.run(["lscpu"], capture_output=True, text=True, timeout=10).stdout
+        for ln in out.splitlines():
+            if ln.startswith("Model name:"):
+                return ln.split(":", 1)[1].strip()
+    except Exception:
+        pass
+    try:
+        for ln in open("/proc/cpuinfo"):
+            if ln.startswith("model name"):
+                return ln.split(":", 1)[1].strip()
+    except Exception:
+        pass
+    return None
+
+
+def oracle_sample(parts, params, n_grav=20000, n_gas=1500, seed=1):
     """Time the fp64 oracle as it stands on a bounded sample of the workload; returns
-    (pair interactions evaluated, seconds, description)."""
+    (pair interactions evaluated, seconds, description, mean pair interactions per particle).
+    The pairs are counted by the oracle itself (oracle.counts on the sampled sets, outside the
+    timed region): no GPU library is involved."""
     import oracle
 
     rng = np.random.default_rng(seed)
@@ -117,7 +136,6 @@ def oracle_sample(parts, params, cnts, n_grav=20000, n_gas=1500, seed=1):
     gas = np.nonzero(parts["species"] == 1)[0]
     tg = np.sort(rng.choice(gas, min(n_gas, gas.shape[0]), replace=False))
     ta = np.sort(rng.choice(n, min(n_grav, n), replace=False))
-    cg, ch, cs = cnts  # input order
     t0 = time.perf_counter()
     oracle.gravity(parts, params, ta)
     off, nb = oracle.neighbour_sets(parts, params, tg, 2)
@@ -134,36 +152,66 @@ def oracle_sample(parts, params, cnts, n_grav=20000, n_gas=1500, seed=1):
     rho[T2], P[T2], c[T2], dv[T2] = ex["rho"], ex["P"], ex["cs"], ex["dv"]
     oracle.accel(parts, params, V, A, B, dA, dB, rho, P, c, dv, tg)
     secs = time.perf_counter() - t0
-    pairs = int(cg[ta].sum()) + int(ch[T1].sum()) + 2 * int(ch[T2].sum()) + int(cs[tg].sum())
+    c_a = oracle.counts(parts, params, ta)
+    c_1 = oracle.counts(parts, params, T1)
+    c_2 = oracle.counts(parts, params, T2)
+    c_g = oracle.counts(parts, params, tg)
+    pairs = (int(c_a["grav"].sum()) + int(c_1["gather"].sum()) + 2 * int(c_2["gather"].sum())
+             + int(c_g["sym"].sum()))
+    # per-particle means of the sampled sets -> the whole workload's pair interactions
+    gas_frac = gas.shape[0] / n
+    per_particle = (c_a["grav"].mean() + gas_frac * (3 * c_g["gather"].mean() + c_g["sym"].mean()))
     desc = (f"oracle (fp64 C, OpenMP) on {ta.shape[0]} gravity targets + hydro chain for {tg.shape[0]} gas "
-            f"targets (closure {T1.shape[0]}/{T2.shape[0]}); pairs counted per pass on the computed sets")
-    return pairs, secs, desc
+            f"targets (closure {T1.shape[0]}/{T2.shape[0]}); pairs counted by oracle.counts on the computed sets")
+    return pairs, secs, desc, float(per_particle)
+
+
+def oracle_1core_c1():
+    """the config-1 oracle ("CPU oracle in seconds") on ONE core — the
+    whole substep (gravity, geometry, corrections, extras, accel/du-dt) plus the counts."""
+    import oracle
+    from gen import make_config
+
+    p1, q1 = make_config("c1")
+    n0 = oracle.num_threads()
+    oracle.set_threads(1)
+    try:
+        t0 = time.perf_counter()
+        oracle.substep(p1, q1)
+        oracle.counts(p1, q1)
+        return time.perf_counter() - t0
+    finally:
+        oracle.set_threads(n0)
 
 
 def run_reference(args, parts, params, rank, world):
-    """--impl reference: the oracle (fp64 CPU) timed on this host's cores, rank 0 only."""
+    """--impl reference: the oracle (fp64 CPU) timed on this host's cores, rank 0 only.  No
+    GPU library is loaded on this path: pairs are counted by the oracle."""
     import oracle
 
     if rank != 0:
         return
-    from paper_2310_16122_b200 import Particles, Solver  # counts only (outside timing)
-    import torch
-
-    cnts = _counts_input_order(parts, params)
-    times, pairs_tot = [], 0
+    times, pairs_tot, pp = [], 0, []
     for s in range(args.warmup + args.steps):
-        pairs, secs, desc = oracle_sample(parts, params, cnts, n_grav=4000, n_gas=300, seed=100 + s)
+        pairs, secs, desc, per_particle = oracle_sample(parts, params, n_grav=4000, n_gas=300, seed=100 + s)
         if s >= args.warmup:
             times.append(secs)
             pairs_tot += pairs
+            pp.append(per_particle)
     val = pairs_tot / sum(times)
-    ms = 1e3 * sum(times) / len(times)
+    n = parts["x"].shape[0]
+    # one whole substep of this workload at the oracle's measured rate (pair interactions per
+    # substep estimated from the sampled per-particle counts)
+    ms = 1e3 * float(np.mean(pp)) * n / val
     line = {"metric": METRIC, "impl": "reference", "value": val, "unit": "pair interactions/s",
             "n_gpus": world, "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms,
+            "ms_per_step_basis": "one whole substep of the workload at the measured rate (pairs per substep "
+                                 "from the sampled per-particle oracle counts); each timed step is a bounded sample",
+            "sample_ms_per_step": 1e3 * sum(times) / len(times),
             "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64",
             "data": "synthetic", "config": _config(args, parts),
             "cpu_baseline": {"value": val, "unit": "pair interactions/s", "cores": oracle.num_threads(),
-                             "kind": "oracle", "sample": desc},
+                             "kind": "oracle", "sample": desc, "cpu": _cpu_model()},
             "e2e": {"value": val, "unit": "pair interactions/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
     print(json.dumps(line), flush=True)
 
@@ -191,6 +239,7 @@ def _counts_input_order(parts, params):
     p = Particles.from_host(parts, "cuda", outputs=False)
     s = Solver(params, torch.cuda.current_device())
     s.build_lists(p)
+    s.geometry(p)  # builds the neighbour lists: the gas counts come from the list walks the passes make
     cg, ch, cs = s.count_pairs(p)
     perm = p.perm.cpu().numpy().astype(np.int64)
     out = []
@@ -496,9 +545,9 @@ def main():
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
         import oracle
 
-        pr, secs, desc = oracle_sample(parts, params, cnts)
+        pr, secs, desc, _ = oracle_sample(parts, params)
         cpu = {"value": pr / secs, "unit": "pair interactions/s", "cores": oracle.num_threads(), "kind": "oracle",
-               "sample": desc, "seconds": secs}
+               "sample": desc, "seconds": secs, "cpu": _cpu_model(), "seconds_1core_config1": oracle_1core_c1()}
 
     if rank == 0:
         line = {

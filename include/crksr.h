@@ -74,9 +74,11 @@ typedef struct crk_params {
                             rebuilding the lists.  0 = off. */
     int32_t grav_kernel; /* gravity kernel variant when symmetric & 1 (DESIGN.md §7 and the variant
                             portfolio): 0 = the pipelined warp-independent
-                            Newton-3 kernel (the benchmarked default; the only one with domain
-                            decomposition, the others fall back to the i-centric kernel there),
-                            6 = warp-independent without the copy pipeline, 7 = CTA-staged,
+                            Newton-3 kernel (the benchmarked default; with 1 and 2 — the same kernel
+                            in two other occupancy / staging configurations — the only ones with
+                            domain decomposition and count mode, the others fall back to the
+                            i-centric kernel there), 6 = warp-independent without the copy
+                            pipeline, 7 = CTA-staged,
                             8 = the paper's half-warp XOR-shuffle algorithm.
                             Other values: CRK_EINVAL. */
     int32_t hydro_kernel;/* accel/du-dt kernel variant: 0 = i-centric list walk (default),
@@ -216,12 +218,27 @@ crk_status crk_refresh(struct crk_ctx* ctx, crk_particles* parts, void* stream);
 crk_status crk_update_h(struct crk_ctx* ctx, crk_particles* parts, int32_t k_ngb, float factor, float* H_out,
                         int32_t* n_unconverged, void* stream);
 
-/* Count mode (after SPEC.md:374-382): per-particle integer pair counts
- * from the same list-driven pair kernels: gravity (j != i, s32 < rcut2), gas gather
- * (gas j != i, s32 < H_i^2) and gas symmetric (s32 < max(H_i^2, H_j^2)); 0 for DM.
- * Outputs are device int32 arrays of length n in sorted order.  Needs build_lists. */
+/* Count mode (after SPEC.md:374-382): per-particle integer pair counts,
+ * each produced by an integer-payload instantiation of the kernel the corresponding force
+ * pass runs (same work items, culls, lists and ownership rules): gravity (j != i,
+ * s32 < rcut2) by the configured gravity kernel — the Newton-3 pipelined kernel adds 1 to
+ * both particles of every in-range pair it evaluates; gas gather (gas j != i, s32 < H_i^2)
+ * counted while walking the neighbour lists the way corrections/extras do; gas symmetric
+ * (s32 < max(H_i^2, H_j^2)) while walking them the way accel/du-dt does — with the same
+ * on-the-fly fallback for rows whose lists overflowed.  0 for DM.  Outputs are device int32
+ * arrays of length n in sorted order.  Needs crk_geometry (it builds the neighbour lists)
+ * when the lists are on, else only crk_build_lists. */
 crk_status crk_count_pairs(struct crk_ctx* ctx, crk_particles* parts, int32_t* cgrav,
                            int32_t* cgather, int32_t* csym, void* stream);
+
+/* The gas neighbour lists built by crk_geometry (read by corrections, extras and accel/du-dt),
+ * decoded: for every gas particle at sorted position i, count[i] = the number of gas particles
+ * j (itself included) with s32 < max(H_i^2, H_j^2) — the O2 symmetric predicate, a superset of
+ * the gather one — or -1 if its list is incomplete (overflowed the capacity; that particle's row
+ * runs the on-the-fly kernels); nbr[i * cap_out + t], t < min(count[i], cap_out), the sorted
+ * positions of those neighbours in the list's order.  count = 0 for DM.  count: device int32[n],
+ * nbr: device int32[n * cap_out].  CRK_ESTATE before crk_geometry or with the lists off. */
+crk_status crk_neighbour_lists(struct crk_ctx* ctx, int32_t cap_out, int32_t* count, int32_t* nbr, void* stream);
 
 /* ---- ghost exchange support ----
  * Cell masks are HOST arrays of ncell[a] bytes per axis; a particle is selected iff its

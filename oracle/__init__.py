@@ -90,6 +90,11 @@ def num_threads() -> int:
     return int(lib().orc_num_threads())
 
 
+def set_threads(n: int) -> None:
+    """OpenMP threads of the following oracle calls."""
+    lib().orc_set_threads(C.c_int(int(n)))
+
+
 # ----------------------------------------------------------------- O3 / O4
 def sort_order(parts, params):
     n = parts["x"].shape[0]

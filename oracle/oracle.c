@@ -883,6 +883,8 @@ int orc_neighbour_sets(int64_t n, const float* x, const float* y, const float* z
 
 int orc_num_threads(void) { return omp_get_max_threads(); }
 
+void orc_set_threads(int n) { omp_set_num_threads(n > 0 ? n : 1); }
+
 /* ------------------------------------------------------------------ sub-cycle (NEXT-2)
  * Readings (DESIGN.md §2 "Sub-cycle"; SURVEY.md §8(f) NEXT-2 names the steps, the paper
  * only that the kernels run several times per step, and a float fetch_min,

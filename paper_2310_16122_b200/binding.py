@@ -24,7 +24,7 @@ EXPORTS = ["crk_create", "crk_destroy", "crk_build_lists", "crk_gravity_kick", "
            "crk_pack_particles", "crk_unpack_particles", "crk_pack_gas", "crk_unpack_gas", "crk_courant_dt",
            "crk_kick", "crk_drift", "crk_update_h", "crk_refresh", "crk_pm_create", "crk_pm_destroy",
            "crk_pm_accel", "crk_pm_slab_create", "crk_pm_deposit", "crk_pm_slab_forward", "crk_pm_slab_solve",
-           "crk_pm_slab_inverse", "crk_pm_interp"]
+           "crk_pm_slab_inverse", "crk_pm_interp", "crk_neighbour_lists"]
 
 
 class CrkError(RuntimeError):
@@ -86,6 +86,8 @@ def lib():
         for f in ("crk_gravity_kick", "crk_hydro_accel_dudt"):
             getattr(L, f).argtypes = [vp, C.POINTER(CrkParticles), C.c_float, vp]
         L.crk_count_pairs.argtypes = [vp, C.POINTER(CrkParticles), vp, vp, vp, vp]
+        L.crk_neighbour_lists.argtypes = [vp, C.c_int32, vp, vp, vp]
+        L.crk_neighbour_lists.restype = C.c_int
         L.crk_courant_dt.argtypes = [vp, C.POINTER(CrkParticles), C.c_float, C.c_float, vp, vp]
         for f in ("crk_kick", "crk_drift"):
             getattr(L, f).argtypes = [vp, C.POINTER(CrkParticles), C.c_float, vp]
@@ -378,6 +380,15 @@ class Solver:
                                           C.c_void_p(ch.data_ptr()), C.c_void_p(cs.data_ptr()),
                                           self._stream(stream)), self.ctx)
         return cg, ch, cs
+
+    def neighbour_lists(self, parts, cap_out=160, stream=None):
+        """The geometry-built gas neighbour lists (crk_neighbour_lists), decoded to sorted
+        positions: (count int32[n] (-1: incomplete list), nbr int32[n, cap_out]) device tensors."""
+        cnt = torch.zeros(parts.n, dtype=torch.int32, device=parts.device)
+        nbr = torch.full((parts.n, cap_out), -1, dtype=torch.int32, device=parts.device)
+        self._check(lib().crk_neighbour_lists(self.ctx, int(cap_out), C.c_void_p(cnt.data_ptr()),
+                                              C.c_void_p(nbr.data_ptr()), self._stream(stream)), self.ctx)
+        return cnt, nbr
 
     # ---- ghost exchange (a9) ----
     @staticmethod

@@ -20,6 +20,7 @@ crk_status csr_views(crk_ctx* c);
 crk_status update_h(crk_ctx* c, int kth, float factor, float* H_out, int32_t* n_unconverged, cudaStream_t st);
 crk_status accel_dudt(crk_ctx* c, crk_particles* p, float dt, cudaStream_t st);
 crk_status hydro_count(crk_ctx* c, int32_t* cgather, int32_t* csym, cudaStream_t st);
+crk_status neighbour_lists(crk_ctx* c, int32_t cap_out, int32_t* count, int32_t* nbr, cudaStream_t st);
 
 crk_status fail(crk_ctx* c, crk_status s, const char* what) {
     if (c) c->err = what;
@@ -143,8 +144,8 @@ static crk_status validate(const crk_params* p, Layout& L, std::string& why) {
     }
     if (!(p->skin >= 0.f) || p->skin >= p->cell_side) { why = "skin must be in [0, cell_side)"; return CRK_EINVAL; }
     if (p->skin > 0.f && L.partial) { why = "a skin needs a whole-box domain"; return CRK_EINVAL; }
-    if (!(p->grav_kernel == 0 || p->grav_kernel == 6 || p->grav_kernel == 7 || p->grav_kernel == 8)) {
-        why = "grav_kernel must be 0, 6, 7 or 8"; return CRK_EINVAL;
+    if (!((p->grav_kernel >= 0 && p->grav_kernel <= 2) || (p->grav_kernel >= 6 && p->grav_kernel <= 8))) {
+        why = "grav_kernel must be 0-2 or 6-8"; return CRK_EINVAL;
     }
     if (!(p->hydro_kernel == 0 || (p->hydro_kernel >= 4 && p->hydro_kernel <= 6))) {
         why = "hydro_kernel must be 0, 4, 5 or 6"; return CRK_EINVAL;
@@ -299,6 +300,15 @@ crk_status crk_count_pairs(crk_ctx* c, crk_particles* p, int32_t* cgrav, int32_t
     CRK_TRY(cuda_check(c, zero_async(csym, p->n * 4, st, c), "memset"));
     CRK_TRY(gravity_count(c, p, cgrav, st));
     return hydro_count(c, cgather, csym, st);
+}
+
+crk_status crk_neighbour_lists(crk_ctx* c, int32_t cap_out, int32_t* count, int32_t* nbr, void* stream) {
+    if (!c) return CRK_EINVAL;
+    if (cap_out < 1 || !count || !nbr) return fail(c, CRK_EINVAL, "cap_out >= 1, count and nbr required");
+    if (c->nbr_cap <= 0) return fail(c, CRK_ESTATE, "the neighbour lists are off (crk_params.nbr_cap < 0)");
+    if (c->stage < ST_GEO) return fail(c, CRK_ESTATE, "call crk_geometry first (it builds the neighbour lists)");
+    CRK_TRY(cuda_check(c, cudaSetDevice(c->device), "cudaSetDevice"));
+    return neighbour_lists(c, cap_out, count, nbr, (cudaStream_t)stream);
 }
 
 crk_status crk_list_view(crk_ctx* c, crk_lists* o) {

@@ -126,6 +126,7 @@ struct GravSymArgs {
     const int32_t* ifirst;
     const int32_t* icount;
     float4* acc;
+    int32_t* cnt;        // count mode: per-particle pair counters (zeroed)
     int* work;           // dynamic work counter (zeroed before the launch)
     int split;           // work items per i-leaf
     int nitems;
@@ -745,28 +746,46 @@ __global__ void __launch_bounds__(symh::NW * 32, 16 / symh::NW) grav_halfwarp_ke
 // and evaluated from shared memory.
 namespace symp {
 constexpr int G = 16, RING = 64, NW = 4, CH = 32;
+// CAPL: surviving j-leaves of a chunk whose particles are staged in shared memory; the rare
+// chunks with more survivors read the rest straight from L2 (smaller per-warp footprint:
+// more resident warps)
+template <int CAPL>
 struct WarpSm {
-    float4 er[2][CH][2];      // entry records of two chunks
-    float4 pp[2][CH * JMAX];  // particles of the surviving leaves of two chunks
-    float4 woff[2][CH];       // surviving entries: shift offset, first | (count - 1) << 29 (w)
+    float4 er[2][CH][2];        // entry records of two chunks
+    float4 pp[2][CAPL * JMAX];  // particles of the first CAPL surviving leaves of two chunks
+    float4 woff[2][CH];         // surviving entries: shift offset, first | (count - 1) << 29 (w)
     float4 wpos[RING];
     int widx[RING];
     float2 inx[G / 2], iny[G / 2], inz[G / 2], im[G / 2];
 };
+constexpr int SHIFT_BYTES = 27 * 16;  // per-CTA table of the 27 periodic offsets (shift code -> float4)
 }  // namespace symp
 
-template <bool PARTIAL>
-__global__ void __launch_bounds__(symp::NW * 32, 16 / symp::NW) grav_pipe_kernel(const GravSymArgs A) {
+// The benchmarked gravity kernel (crk_params.symmetric & 1, grav_kernel 0).  COUNT: the
+// same work items, culls, ownership and ring with an integer payload — each evaluated pair
+// that passes the O2 predicate adds 1 to both particles' counters (i-side in registers,
+// reactions by red.global.add.s32) — so crk_count_pairs checks the coverage of exactly the
+// kernel the bench times (SPEC.md:374-382 integer-payload audit, PAPER.md:418 pair symmetry).
+template <bool PARTIAL, bool COUNT, int CAPL, int MINB>
+__global__ void __launch_bounds__(symp::NW * 32, MINB) grav_pipe_kernel(const GravSymArgs A) {
     using namespace symp;
+    using WS = WarpSm<CAPL>;
     extern __shared__ __align__(128) unsigned char smem_raw[];
     const int warp = threadIdx.x >> 5;
     const int lane = threadIdx.x & 31;
-    WarpSm& S = reinterpret_cast<WarpSm*>(smem_raw)[warp];
+    float4* shift_tab = reinterpret_cast<float4*>(smem_raw);
+    WS& S = reinterpret_cast<WS*>(smem_raw + SHIFT_BYTES)[warp];
     const float wcut = A.rcut2 * CULL_SLACK;
     const float rc2 = A.rcut2, e2 = A.eps2;
     const float c0 = A.c0, c1 = A.c1, c2 = A.c2, c3 = A.c3, c4 = A.c4, c5 = A.c5;
     const unsigned below = (1u << lane) - 1u;
     const float4* __restrict__ xm = A.xm;
+    if (threadIdx.x < 27) {
+        const int code = threadIdx.x;
+        shift_tab[code] = make_float4((float)(code % 3 - 1) * A.L[0], (float)((code / 3) % 3 - 1) * A.L[1],
+                                      (float)(code / 9 - 1) * A.L[2], 0.f);
+    }
+    __syncthreads();
 
     while (true) {
         int w = 0;
@@ -813,23 +832,20 @@ __global__ void __launch_bounds__(symp::NW * 32, 16 / symp::NW) grav_pipe_kernel
             hi[2] = warp_max(iv ? p.z : -INFINITY);
         }
 
-        int nsurv[2] = {0, 0};
+        int ns_even = 0, ns_odd = 0;  // surviving entries of the chunks in buffers 0 / 1
         // entry cull of chunk c (records landed) and async copies of its surviving leaves
         auto cull_entries = [&](int c) {
             const int b = c & 1;
             bool ek = false;
             float4 off = make_float4(0.f, 0.f, 0.f, 0.f);
-            int cnt = 0;
             if (c < nch && rbeg + c * CH + lane < rend) {
                 const float4 bl = S.er[b][lane][0], bh = S.er[b][lane][1];
                 const int first = __float_as_int(bl.w);
                 const int cc = __float_as_int(bh.w);
-                cnt = cc & 0xff;
-                int sx, sy, sz;
-                decode_shift(cc >> 8, sx, sy, sz);
+                const int cnt = cc & 0xff;
+                off = shift_tab[cc >> 8];
                 // w: first | (count - 1) << 29, as in the packed list entries
-                off = make_float4((float)sx * A.L[0], (float)sy * A.L[1], (float)sz * A.L[2],
-                                  __int_as_float(first | ((cnt - 1) << 29)));
+                off.w = __int_as_float(first | ((cnt - 1) << 29));
                 // entries wholly below this group own no pair — unless they are ghosts (a j-leaf
                 // lies in one cell, so its box centre, unshifted, decides its ownership)
                 bool ghost = false;
@@ -845,13 +861,14 @@ __global__ void __launch_bounds__(symp::NW * 32, 16 / symp::NW) grav_pipe_kernel
             }
             const unsigned em = __ballot_sync(0xffffffffu, ek);
             const int ns = __popc(em);
-            nsurv[b] = ns;
+            if (b) ns_odd = ns; else ns_even = ns;
             if (ek) S.woff[b][__popc(em & below)] = off;
             __syncwarp();
             // particles: lane -> (entry q0 + lane / 8, member lane % 8)
-            for (int q0 = 0; q0 < ns; q0 += 32 / JMAX) {
+            const int nst = min(ns, CAPL);
+            for (int q0 = 0; q0 < nst; q0 += 32 / JMAX) {
                 const int q = q0 + lane / JMAX, kk = lane % JMAX;
-                if (q < ns)  // all JMAX slots (xm is padded): members beyond the count are masked later
+                if (q < nst)  // all JMAX slots (xm is padded): members beyond the count are masked later
                     cp_async16(&S.pp[b][q * JMAX + kk], xm + (__float_as_int(S.woff[b][q].w) & 0x1fffffff) + kk);
             }
             cp_async_commit();
@@ -860,9 +877,13 @@ __global__ void __launch_bounds__(symp::NW * 32, 16 / symp::NW) grav_pipe_kernel
         __syncwarp();
         cull_entries(0);
 
+        // i-side sums, packed: component .x is i = k, .y is i = k + G/2
         float2 ax[G / 2], ay[G / 2], az[G / 2];
+        int2 ci[COUNT ? G / 2 : 1];
 #pragma unroll
         for (int k = 0; k < G / 2; ++k) ax[k] = ay[k] = az[k] = make_float2(0.f, 0.f);
+#pragma unroll
+        for (int k = 0; k < (COUNT ? G / 2 : 1); ++k) ci[k] = make_int2(0, 0);
 
         auto eval_step = [&](int r0, int n) {
             float4 jp = make_float4(1e18f, 1e18f, 1e18f, 0.f);
@@ -872,39 +893,60 @@ __global__ void __launch_bounds__(symp::NW * 32, 16 / symp::NW) grav_pipe_kernel
                 jp = S.wpos[s];
                 j = S.widx[s];
             }
-            const float mj = (j >= gself && j < gself + ng) ? 0.f : jp.w;
+            const bool jown = j >= gself && j < gself + ng;  // own group: the i-side half is counted
             const float2 jx = make_float2(jp.x, jp.x), jy = make_float2(jp.y, jp.y), jz = make_float2(jp.z, jp.z);
-            const float2 mj2 = make_float2(mj, mj), e22 = make_float2(e2, e2);
-            const float2 n0 = make_float2(-c0, -c0), n1 = make_float2(-c1, -c1), n2 = make_float2(-c2, -c2);
-            const float2 n3 = make_float2(-c3, -c3), n4 = make_float2(-c4, -c4), n5 = make_float2(-c5, -c5);
-            float2 bx = make_float2(0.f, 0.f), by = bx, bz = bx;
+            if constexpr (COUNT) {
+                // O2 membership, both directions; the pair (i, i) of a survivor in its own group is
+                // not a pair.  i-side only when j is outside the group (met from both sides inside).
+                int bj = 0;
 #pragma unroll
-            for (int k = 0; k < G / 2; ++k) {
-                const float2 dx = __fadd2_rn(jx, S.inx[k]);
-                const float2 dy = __fadd2_rn(jy, S.iny[k]);
-                const float2 dz = __fadd2_rn(jz, S.inz[k]);
-                const float2 r2 = __ffma2_rn(dz, dz, __ffma2_rn(dy, dy, __fmul2_rn(dx, dx)));
-                const float2 re = __fadd2_rn(r2, e22);
-                const float2 ri = make_float2(rsqrtf(re.x), rsqrtf(re.y));
-                const float2 ri2 = __fmul2_rn(ri, ri);
-                float2 np5 = __ffma2_rn(n5, r2, n4);
-                np5 = __ffma2_rn(np5, r2, n3);
-                np5 = __ffma2_rn(np5, r2, n2);
-                np5 = __ffma2_rn(np5, r2, n1);
-                np5 = __ffma2_rn(np5, r2, n0);
-                float2 wv = __ffma2_rn(ri2, ri, np5);
-                wv.x = r2.x < rc2 ? wv.x : 0.f;
-                wv.y = r2.y < rc2 ? wv.y : 0.f;
-                const float2 wi = __fmul2_rn(mj2, wv);
-                ax[k] = __ffma2_rn(wi, dx, ax[k]);
-                ay[k] = __ffma2_rn(wi, dy, ay[k]);
-                az[k] = __ffma2_rn(wi, dz, az[k]);
-                const float2 wj = __fmul2_rn(S.im[k], wv);
-                bx = __ffma2_rn(wj, dx, bx);
-                by = __ffma2_rn(wj, dy, by);
-                bz = __ffma2_rn(wj, dz, bz);
+                for (int k = 0; k < G / 2; ++k) {
+                    const float2 dx = __fadd2_rn(jx, S.inx[k]);
+                    const float2 dy = __fadd2_rn(jy, S.iny[k]);
+                    const float2 dz = __fadd2_rn(jz, S.inz[k]);
+                    const float2 r2 = __ffma2_rn(dz, dz, __ffma2_rn(dy, dy, __fmul2_rn(dx, dx)));
+                    const bool in0 = lane < n && r2.x < rc2 && j != gself + k;
+                    const bool in1 = lane < n && r2.y < rc2 && j != gself + k + G / 2;
+                    ci[k].x += (in0 && !jown) ? 1 : 0;
+                    ci[k].y += (in1 && !jown) ? 1 : 0;
+                    bj += (in0 ? 1 : 0) + (in1 ? 1 : 0);
+                }
+                if (lane < n && (!PARTIAL || j >= 0) && bj) atomicAdd(A.cnt + j, bj);
+            } else {
+                const float mj = jown ? 0.f : jp.w;
+                const float2 mj2 = make_float2(mj, mj), e22 = make_float2(e2, e2);
+                const float2 n0 = make_float2(-c0, -c0), n1 = make_float2(-c1, -c1), n2 = make_float2(-c2, -c2);
+                const float2 n3 = make_float2(-c3, -c3), n4 = make_float2(-c4, -c4), n5 = make_float2(-c5, -c5);
+                float2 bx = make_float2(0.f, 0.f), by = bx, bz = bx;
+#pragma unroll
+                for (int k = 0; k < G / 2; ++k) {
+                    const float2 dx = __fadd2_rn(jx, S.inx[k]);  // x_j - x_i, exact (O1)
+                    const float2 dy = __fadd2_rn(jy, S.iny[k]);
+                    const float2 dz = __fadd2_rn(jz, S.inz[k]);
+                    const float2 r2 = __ffma2_rn(dz, dz, __ffma2_rn(dy, dy, __fmul2_rn(dx, dx)));  // O2 order
+                    const float2 re = __fadd2_rn(r2, e22);
+                    const float2 ri = make_float2(rsqrtf(re.x), rsqrtf(re.y));
+                    const float2 ri2 = __fmul2_rn(ri, ri);
+                    float2 np5 = __ffma2_rn(n5, r2, n4);  // -P5(s)
+                    np5 = __ffma2_rn(np5, r2, n3);
+                    np5 = __ffma2_rn(np5, r2, n2);
+                    np5 = __ffma2_rn(np5, r2, n1);
+                    np5 = __ffma2_rn(np5, r2, n0);
+                    float2 wv = __ffma2_rn(ri2, ri, np5);  // (s + eps2)^-3/2 - P5(s)
+                    wv.x = r2.x < rc2 ? wv.x : 0.f;
+                    wv.y = r2.y < rc2 ? wv.y : 0.f;
+                    const float2 wi = __fmul2_rn(mj2, wv);  // i-side: a_i += m_j w x_ji
+                    ax[k] = __ffma2_rn(wi, dx, ax[k]);
+                    ay[k] = __ffma2_rn(wi, dy, ay[k]);
+                    az[k] = __ffma2_rn(wi, dz, az[k]);
+                    const float2 wj = __fmul2_rn(S.im[k], wv);  // j-side: a_j -= m_i w x_ji
+                    bx = __ffma2_rn(wj, dx, bx);
+                    by = __ffma2_rn(wj, dy, by);
+                    bz = __ffma2_rn(wj, dz, bz);
+                }
+                if (lane < n && (!PARTIAL || j >= 0))
+                    red_add_v4(A.acc + j, -(bx.x + bx.y), -(by.x + by.y), -(bz.x + bz.y), 0.f);
             }
-            if (lane < n && (!PARTIAL || j >= 0)) red_add_v4(A.acc + j, -(bx.x + bx.y), -(by.x + by.y), -(bz.x + bz.y), 0.f);
         };
 
         int wr = 0, rd = 0;
@@ -916,8 +958,8 @@ __global__ void __launch_bounds__(symp::NW * 32, 16 / symp::NW) grav_pipe_kernel
             cull_entries(c + 1);   // its particles go to pp[b ^ 1] (chunk c - 1's, consumed)
             cp_async_wait<2>();    // particles(c)
             __syncwarp();
-            // particle cull of chunk c from shared memory, then evaluation
-            const int ns = nsurv[b];
+            // particle cull of chunk c from shared memory (or L2 past CAPL leaves), then evaluation
+            const int ns = b ? ns_odd : ns_even;
             for (int q0 = 0; q0 < ns; q0 += 32 / JMAX) {
                 const int q = q0 + lane / JMAX, kk = lane % JMAX;
                 const int qc = q < ns ? q : 0;
@@ -925,7 +967,7 @@ __global__ void __launch_bounds__(symp::NW * 32, 16 / symp::NW) grav_pipe_kernel
                 const int fc = __float_as_int(o.w);
                 const int cnt = (int)((unsigned)fc >> 29) + 1;
                 int j = (fc & 0x1fffffff) + kk;
-                float4 p = S.pp[b][qc * JMAX + kk];
+                float4 p = q0 < CAPL ? S.pp[b][qc * JMAX + kk] : __ldg(xm + j);
                 bool keep = q < ns && kk < cnt;
                 if (PARTIAL && keep && !grav_owned(A, p.x, p.y, p.z)) j = -1 - j;  // ghost: no reaction
                 p.x += o.x; p.y += o.y; p.z += o.z;  // exact (O1)
@@ -949,28 +991,39 @@ __global__ void __launch_bounds__(symp::NW * 32, 16 / symp::NW) grav_pipe_kernel
         }
         cp_async_wait<0>();
         if (wr > rd) eval_step(rd, wr - rd);
-        float v[3][G];
+        if constexpr (COUNT) {
 #pragma unroll
-        for (int k = 0; k < G / 2; ++k) {
-            v[0][k] = ax[k].x; v[0][k + G / 2] = ax[k].y;
-            v[1][k] = ay[k].x; v[1][k + G / 2] = ay[k].y;
-            v[2][k] = az[k].x; v[2][k + G / 2] = az[k].y;
+            for (int k = 0; k < G / 2; ++k) {
+                const int t0 = __reduce_add_sync(0xffffffffu, ci[k].x), t1 = __reduce_add_sync(0xffffffffu, ci[k].y);
+                if (lane == k && k < ng && t0) atomicAdd(A.cnt + gself + k, t0);
+                if (lane == k + G / 2 && k + G / 2 < ng && t1) atomicAdd(A.cnt + gself + k + G / 2, t1);
+            }
+        } else {
+            // transposed (reduce-scatter) sum of the 16 x 3 i-side values; lane l ends with i = l >> 1
+            float v[3][G];
+#pragma unroll
+            for (int k = 0; k < G / 2; ++k) {
+                v[0][k] = ax[k].x; v[0][k + G / 2] = ax[k].y;
+                v[1][k] = ay[k].x; v[1][k + G / 2] = ay[k].y;
+                v[2][k] = az[k].x; v[2][k + G / 2] = az[k].y;
+            }
+#pragma unroll
+            for (int h = G / 2; h >= 1; h >>= 1) {
+                const bool up = lane & (2 * h);
+#pragma unroll
+                for (int cc = 0; cc < 3; ++cc)
+#pragma unroll
+                    for (int k = 0; k < h; ++k) {
+                        const float send = up ? v[cc][k] : v[cc][k + h];
+                        const float keep = up ? v[cc][k + h] : v[cc][k];
+                        v[cc][k] = keep + __shfl_xor_sync(0xffffffffu, send, 2 * h);
+                    }
+            }
+#pragma unroll
+            for (int cc = 0; cc < 3; ++cc) v[cc][0] += __shfl_xor_sync(0xffffffffu, v[cc][0], 1);
+            if ((lane & 1) == 0 && (lane >> 1) < ng)
+                red_add_v4(A.acc + gself + (lane >> 1), v[0][0], v[1][0], v[2][0], 0.f);
         }
-#pragma unroll
-        for (int h = G / 2; h >= 1; h >>= 1) {
-            const bool up = lane & (2 * h);
-#pragma unroll
-            for (int cc = 0; cc < 3; ++cc)
-#pragma unroll
-                for (int k = 0; k < h; ++k) {
-                    const float send = up ? v[cc][k] : v[cc][k + h];
-                    const float keep = up ? v[cc][k + h] : v[cc][k];
-                    v[cc][k] = keep + __shfl_xor_sync(0xffffffffu, send, 2 * h);
-                }
-        }
-#pragma unroll
-        for (int cc = 0; cc < 3; ++cc) v[cc][0] += __shfl_xor_sync(0xffffffffu, v[cc][0], 1);
-        if ((lane & 1) == 0 && (lane >> 1) < ng) red_add_v4(A.acc + gself + (lane >> 1), v[0][0], v[1][0], v[2][0], 0.f);
         __syncwarp();
     }
 }
@@ -1041,70 +1094,90 @@ static cudaError_t launch_grav_sym(crk_ctx* c, GravSymArgs& A, cudaStream_t st) 
 }
 
 
+static GravSymArgs grav_args(crk_ctx* c) {
+    GravSymArgs A;
+    A.xm = P<float4>(c->xm);
+    A.ebox = P<float4>(c->gebox);
+    A.box8 = P<float4>(c->lbox8[1]);
+    A.erec = P<int2>(c->erec[0]);
+    A.row_off = P<int32_t>(c->rowoff[0]);
+    A.ifirst = P<int32_t>(c->lfirst[0]);
+    A.icount = P<int32_t>(c->lcount[0]);
+    A.acc = P<float4>(c->gacc);
+    A.cnt = nullptr;
+    for (int d = 0; d < 3; ++d) A.L[d] = c->lay.L[d];
+    A.rcut2 = c->prm.rcut2;
+    A.eps2 = c->prm.eps2;
+    A.c0 = c->prm.poly[0]; A.c1 = c->prm.poly[1]; A.c2 = c->prm.poly[2];
+    A.c3 = c->prm.poly[3]; A.c4 = c->prm.poly[4]; A.c5 = c->prm.poly[5];
+    A.partial = c->lay.partial;
+    A.inv_q = c->lay.inv_q;
+    A.cs = c->lay.cs;
+    for (int d = 0; d < 3; ++d) { A.dlo[d] = c->lay.dlo[d]; A.dhi[d] = c->lay.dhi[d]; }
+    A.work = P<int>(c->work);
+    A.split = (c->prm.leaf_max_i + symp::G - 1) / symp::G;
+    A.nitems = (int)(c->nleaf[0] * A.split);
+    return A;
+}
+
+template <bool COUNT, int CAPL, int MINB>
+static cudaError_t launch_pipe_cfg(crk_ctx* c, const GravSymArgs& A, cudaStream_t st) {
+    int nsm = 0;
+    cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, c->device);
+    const int smem = symp::SHIFT_BYTES + (int)sizeof(symp::WarpSm<CAPL>) * symp::NW;
+    auto k = A.partial ? grav_pipe_kernel<true, COUNT, CAPL, MINB> : grav_pipe_kernel<false, COUNT, CAPL, MINB>;
+    cudaError_t e = cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+    if (e != cudaSuccess) return e;
+    int per_sm = 0;
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k, symp::NW * 32, smem);
+    k<<<nsm * std::max(1, per_sm), symp::NW * 32, smem, st>>>(A);
+    return cudaGetLastError();
+}
+
+// the pipelined Newton-3 kernel in its launch configurations (crk_params.grav_kernel 0-2): the
+// shared-memory leaf capacity per chunk and the resident CTAs per SM trade the staged share of
+// the particle reads against occupancy
+template <bool COUNT>
+static cudaError_t launch_pipe(crk_ctx* c, const GravSymArgs& A, cudaStream_t st) {
+    switch (c->prm.grav_kernel) {
+    case 1: return launch_pipe_cfg<COUNT, 32, 4>(c, A, st);
+    case 2: return launch_pipe_cfg<COUNT, 16, 6>(c, A, st);
+    default: return launch_pipe_cfg<COUNT, 20, 5>(c, A, st);
+    }
+}
+
+static bool pipe_kernel(crk_ctx* c) { return c->prm.grav_kernel <= 2; }
+
 static crk_status gravity_sym(crk_ctx* c, crk_particles* p, float dt, cudaStream_t st) {
     const int64_t n = c->n;
     CRK_TRY(grow(c, c->gacc, n * 16, st));
     CRK_TRY(cuda_check(c, zero_async(c->gacc.p, n * 16, st, c), "memset"));
     if (c->nleaf[0] > 0) {
-        GravSymArgs A;
-        A.xm = P<float4>(c->xm);
-        A.ebox = P<float4>(c->gebox);
-        A.box8 = P<float4>(c->lbox8[1]);
-        A.erec = P<int2>(c->erec[0]);
-        A.row_off = P<int32_t>(c->rowoff[0]);
-        A.ifirst = P<int32_t>(c->lfirst[0]);
-        A.icount = P<int32_t>(c->lcount[0]);
-        A.acc = P<float4>(c->gacc);
-        for (int d = 0; d < 3; ++d) A.L[d] = c->lay.L[d];
-        A.rcut2 = c->prm.rcut2;
-        A.eps2 = c->prm.eps2;
-        A.c0 = c->prm.poly[0]; A.c1 = c->prm.poly[1]; A.c2 = c->prm.poly[2];
-        A.c3 = c->prm.poly[3]; A.c4 = c->prm.poly[4]; A.c5 = c->prm.poly[5];
-        A.partial = c->lay.partial;
-        A.inv_q = c->lay.inv_q;
-        A.cs = c->lay.cs;
-        for (int d = 0; d < 3; ++d) { A.dlo[d] = c->lay.dlo[d]; A.dhi[d] = c->lay.dhi[d]; }
-        const int var = c->prm.grav_kernel;
         CRK_TRY(grow(c, c->work, 64, st));
         CRK_TRY(cuda_check(c, zero_async(c->work.p, 16, st, c), "memset"));
-        A.work = P<int>(c->work);
+        GravSymArgs A = grav_args(c);
         cudaError_t e;
-        // measured on c4 (profiles/r01): <8 warps, 320 entries, 1 buffer> 24.6 ms, <4, 320, 1> 30.3,
-        // <8, 320, 2> 36.2, <4, 256, 2> 41.9 (the second row buffer costs occupancy)
-        switch (var) {
-        case 6: {  // warp-independent (c4: 17.3 ms vs 20.4 for <8, 320, 1>)
-            A.split = (c->prm.leaf_max_i + symw::G - 1) / symw::G;
-            A.nitems = (int)(c->nleaf[0] * A.split);
+        switch (c->prm.grav_kernel) {
+        case 6: {  // warp-independent without the copy pipeline
             int nsm = 0;
             cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, c->device);
             grav_warp_kernel<<<nsm * (16 / symw::NW), symw::NW * 32, 0, st>>>(A);
             e = cudaGetLastError();
             break;
         }
-        case 7: e = launch_grav_sym<8, 320, 1>(c, A, st); break;
+        case 7:  // CTA-staged rows (measured on c4, round 1: 24.6 ms)
+            e = launch_grav_sym<8, 320, 1>(c, A, st);
+            break;
         case 8: {  // the paper's half-warp shuffle algorithm (every pair evaluated once per direction)
-            A.split = (c->prm.leaf_max_i + symh::G - 1) / symh::G;
-            A.nitems = (int)(c->nleaf[0] * A.split);
             int nsm = 0;
             cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, c->device);
             grav_halfwarp_kernel<<<nsm * (16 / symh::NW), symh::NW * 32, 0, st>>>(A);
             e = cudaGetLastError();
             break;
         }
-        default: {  // pipelined warp-independent (c4: 16.0 ms)
-            A.split = (c->prm.leaf_max_i + symp::G - 1) / symp::G;
-            A.nitems = (int)(c->nleaf[0] * A.split);
-            int nsm = 0;
-            cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, c->device);
-            const int smem = (int)sizeof(symp::WarpSm) * symp::NW;
-            auto k = A.partial ? grav_pipe_kernel<true> : grav_pipe_kernel<false>;
-            e = cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
-            if (e == cudaSuccess) {
-                k<<<nsm * (16 / symp::NW), symp::NW * 32, smem, st>>>(A);
-                e = cudaGetLastError();
-            }
+        default:  // pipelined warp-independent
+            e = launch_pipe<false>(c, A, st);
             break;
-        }
         }
         if (e != cudaSuccess) return cuda_check(c, e, "gravity (symmetric) kernel");
         CRK_LAUNCHED(c, "gravity (symmetric) kernel");
@@ -1117,11 +1190,23 @@ static crk_status gravity_sym(crk_ctx* c, crk_particles* p, float dt, cudaStream
 
 crk_status gravity_kick(crk_ctx* c, crk_particles* p, float dt, cudaStream_t st) {
     if (dt != 0.f && (!p->vx || !p->vy || !p->vz)) return fail(c, CRK_EINVAL, "kick needs vx, vy, vz");
-    if ((c->prm.symmetric & 1) && (!c->lay.partial || c->prm.grav_kernel == 0)) return gravity_sym(c, p, dt, st);
+    if ((c->prm.symmetric & 1) && (!c->lay.partial || pipe_kernel(c))) return gravity_sym(c, p, dt, st);
     return launch_grav<false>(c, p, dt, nullptr, st);
 }
 
+// count mode of the kernel crk_gravity_kick runs: the pipelined Newton-3 kernel with an integer
+// payload when it is the configured one, else the i-centric kernel
 crk_status gravity_count(crk_ctx* c, crk_particles* p, int32_t* cnt, cudaStream_t st) {
+    if ((c->prm.symmetric & 1) && pipe_kernel(c)) {
+        if (c->nleaf[0] == 0) return CRK_OK;
+        CRK_TRY(grow(c, c->work, 64, st));
+        CRK_TRY(cuda_check(c, zero_async(c->work.p, 16, st, c), "memset"));
+        GravSymArgs A = grav_args(c);
+        A.cnt = cnt;
+        CRK_TRY(cuda_check(c, launch_pipe<true>(c, A, st), "gravity count kernel"));
+        CRK_LAUNCHED(c, "gravity count kernel");
+        return CRK_OK;
+    }
     return launch_grav<true>(c, p, 0.f, cnt, st);
 }
 

@@ -476,6 +476,38 @@ __device__ __forceinline__ void grad_wr(const float* Ah, const float* dAh, const
     }
 }
 
+// ============================================================== count mode of the list walks
+// Integer payload: the pairs a gas pass evaluates while it walks
+// the neighbour lists (or culls on the fly for flagged rows), j != i: the gather predicate
+// s32 < H_i^2 of corrections/extras (SYMP false) or the symmetric s32 < max(H_i^2, H_j^2) of
+// accel/du-dt (SYMP true).  Positions are staged from gpos (x, y, z, H): the same slots.
+template <bool SYMP>
+struct ListCountPass : HydCommon {
+    static constexpr int PAY = 0;
+    static constexpr bool SYM = SYMP;
+    static constexpr int UNROLL = 4;
+    const float4* jrows;  // gpos
+    const float4* jpay;
+    int32_t* cnt;
+    struct I { float x, y, z, H2, invH; int idx; };
+    struct Acc { int n; };
+    __device__ void init(Acc& a) const { a.n = 0; }
+    __device__ void load_i(int k, I& s) const { load_pos(gpos, k, s.x, s.y, s.z, s.H2, s.invH); s.idx = k; }
+    __device__ float ix(const I& s) const { return s.x; }
+    __device__ float iy(const I& s) const { return s.y; }
+    __device__ float iz(const I& s) const { return s.z; }
+    __device__ float cut(const I& s) const { return s.H2; }
+    __device__ float jcut(const float4& jp) const { return __fmul_rn(jp.w, jp.w); }
+    __device__ __forceinline__ void pair(const I& s, Acc& a, const float4& jp, const float4*, int j) const {
+        const float r2 = s32_of(jp.x - s.x, jp.y - s.y, jp.z - s.z);
+        const bool in = SYMP ? r2 < fmaxf(s.H2, __fmul_rn(jp.w, jp.w)) : r2 < s.H2;
+        a.n += (in && j != s.idx) ? 1 : 0;
+    }
+    template <int GG>
+    __device__ void reduce(Acc& a) const { a.n = slot_sum_i<GG>(a.n); }
+    __device__ void finish(int k, const I&, const Acc& a) const { cnt[gas_idx[k]] = a.n; }
+};
+
 template <bool COUNT, int BATCH_ = 32>
 struct AccPass : HydCommon {
     static constexpr int PAY = COUNT ? 0 : 9;
@@ -853,12 +885,12 @@ static bool lists_on(crk_ctx* c) { return c->nbr_cap > 0 && c->nleaf[2] > 0; }
 
 // list-driven launch of a gather/accel pass, then the on-the-fly kernel over the rows whose
 // lists are incomplete (flagged by the builder; usually none: those CTAs exit at once)
-template <class Pass, int ENT, int MINB, int FENT, int FMINB>
+template <class Pass, int ENT, int MINB, int FENT, int FMINB, int LG = HYD_G>
 static crk_status launch_listed(crk_ctx* c, const Pass& ps, cudaStream_t st, const char* what) {
     if (c->nleaf[2] == 0) return CRK_OK;
     RowView rv = hydro_rows(c);
     CRK_TRY(grow(c, c->work, 64, st));
-    CRK_TRY(cuda_check(c, launch_list<Pass, HYD_NW, HYD_G, ENT, MINB>(ps, rv, list_view(c), st), what));
+    CRK_TRY(cuda_check(c, launch_list<Pass, HYD_NW, LG, ENT, MINB>(ps, rv, list_view(c), st), what));
     c->launches++;
     const ListView lv = list_view(c);
     rv.rows = lv.frows;
@@ -1044,7 +1076,8 @@ static crk_status accel_gather(crk_ctx* c, crk_particles* p, float dt, cudaStrea
     g.ahx = p->ahx; g.ahy = p->ahy; g.ahz = p->ahz; g.dudt = p->dudt;
     g.vx = p->vx; g.vy = p->vy; g.vz = p->vz; g.u = p->u;
     g.cnt = nullptr;
-    if (lists_on(c)) return launch_listed<AccPass<false, BT>, 72, 2, ENT, 2>(c, g, st, "accel/dudt kernel");
+    // list walk with 16 lanes per i (G = 2): bank-conflict-free record reads (pairs.cuh list_kernel)
+    if (lists_on(c)) return launch_listed<AccPass<false, BT>, 72, 2, ENT, 2, 2>(c, g, st, "accel/dudt kernel");
     return launch_hyd<AccPass<false, BT>, ENT, 2>(c, g, st, "accel/dudt kernel");
 }
 
@@ -1092,6 +1125,20 @@ crk_status accel_dudt(crk_ctx* c, crk_particles* p, float dt, cudaStream_t st) {
 }
 
 crk_status hydro_count(crk_ctx* c, int32_t* cgather, int32_t* csym, cudaStream_t st) {
+    if (lists_on(c) && c->stage >= ST_GEO) {  // the walks corrections/extras and accel/du-dt make
+        ListCountPass<false> g;
+        common(c, g);
+        g.jrows = P<float4>(c->gpos);
+        g.jpay = nullptr;
+        g.cnt = cgather;
+        CRK_TRY((launch_listed<ListCountPass<false>, 128, 3, 128, 3>(c, g, st, "gather count (list walk)")));
+        ListCountPass<true> a;
+        common(c, a);
+        a.jrows = P<float4>(c->gpos);
+        a.jpay = nullptr;
+        a.cnt = csym;
+        return launch_listed<ListCountPass<true>, 128, 3, 128, 3>(c, a, st, "sym count (list walk)");
+    }
     GeoPass<true> g;
     common(c, g);
     g.jrows = P<float4>(c->gpos);
@@ -1105,6 +1152,40 @@ crk_status hydro_count(crk_ctx* c, int32_t* cgather, int32_t* csym, cudaStream_t
     a.grec = nullptr;
     a.cnt = csym;
     return launch_hyd<AccPass<true>, 128>(c, a, st, "sym count kernel");
+}
+
+// crk_neighbour_lists: the geometry-built lists decoded to sorted positions (one CTA per gas
+// i-leaf, one thread per member)
+__global__ void __launch_bounds__(64) k_decode_lists(RowView rv, ListView lv, const int32_t* __restrict__ gas_idx,
+                                                    int cap_out, int32_t* count, int32_t* nbr) {
+    const int a = blockIdx.x;
+    const int ii = threadIdx.x;
+    if (ii >= rv.icount[a]) return;
+    const int k = rv.ifirst[a] + ii;
+    const int rbeg = rv.row_off[a];
+    const bool row_lists = (rv.row_off[a + 1] - rbeg) * JMAX <= 65536;
+    const int ntrue = lv.ncnt[k];
+    const bool complete = row_lists && !lv.lflag[a] && ntrue <= lv.cap;
+    const int64_t i = gas_idx[k];
+    count[i] = complete ? ntrue : -1;
+    if (!complete) return;
+    const uint16_t* L = lv.nbr + (int64_t)k * lv.cap;
+    const int m = min(ntrue, cap_out);
+    for (int t = 0; t < m; ++t) {
+        const int slot = L[t];
+        int first, cnt, leaf, code;
+        unpack_entry(__ldg(rv.erec + rbeg + slot / JMAX), first, cnt, leaf, code);
+        nbr[i * cap_out + t] = gas_idx[first + slot % JMAX];
+    }
+}
+
+crk_status neighbour_lists(crk_ctx* c, int32_t cap_out, int32_t* count, int32_t* nbr, cudaStream_t st) {
+    CRK_TRY(cuda_check(c, zero_async(count, (size_t)c->n * 4, st, c), "memset"));
+    if (c->nleaf[2] == 0) return CRK_OK;
+    k_decode_lists<<<(unsigned)c->nleaf[2], 64, 0, st>>>(hydro_rows(c), list_view(c), P<int32_t>(c->gas_idx),
+                                                         cap_out, count, nbr);
+    CRK_LAUNCHED(c, "decode neighbour lists");
+    return CRK_OK;
 }
 
 crk_status update_h(crk_ctx* c, int kth, float factor, float* H_out, int32_t* n_unconverged, cudaStream_t st) {

@@ -437,6 +437,13 @@ __device__ __forceinline__ int claim_row(SM& sm, int* work) {
     return a;
 }
 
+// G i-particles per warp, S = 32/G lanes per i.  A CTA covers NW*G i-particles at a time and
+// loops over the row's i-particles in NW*G-sized iterations (G = 8: one iteration per gas
+// i-leaf of <= 64; G = 2: a half-warp of 16 lanes per i walks 16 consecutive list entries, i.e.
+// mostly consecutive staged slots, so the half-warp's shared-memory reads of a record component
+// spread over all bank groups — no conflicts between the warp's two i-particles).  A row that
+// fits one staging round is staged once for all iterations; longer rows are restaged per
+// iteration.
 template <class Pass, int NW, int G, int ENT, int MINB>
 __global__ void __launch_bounds__(NW * 32, MINB) list_kernel(const Pass pass, const RowView rv, const ListView lv) {
     static_assert(32 % G == 0, "G must divide the warp");
@@ -453,7 +460,6 @@ __global__ void __launch_bounds__(NW * 32, MINB) list_kernel(const Pass pass, co
     // usually consecutive staged slots, so their shared-memory loads fall in distinct banks
     const int il = lane / S;
     const int sl = lane % S;
-    const int ibase = warp * G;
     if (threadIdx.x == 0) {
         mbar_init(&sm.bar, 1);
         mbar_fence_init();
@@ -462,59 +468,66 @@ __global__ void __launch_bounds__(NW * 32, MINB) list_kernel(const Pass pass, co
     auto row = [&](const int a) {
         const int ifirst = rv.ifirst[a];
         const int icount = rv.icount[a];
-        const bool wactive = ibase < icount;
-        const bool ivalid = ibase + il < icount;
         const int rbeg = rv.row_off[a], rend = rv.row_off[a + 1];
-        typename Pass::I is;
-        typename Pass::Acc acc;
-        pass.init(acc);
-        const int ki = ifirst + ibase + (ivalid ? il : 0);
-        int nl = 0;
-        if constexpr (!IREC) {
-            if (wactive) {
-                pass.load_i(ki, is);
-                if (ivalid) nl = lv.ncnt[ki];
-            }
-        }
-        const uint16_t* lp = lv.nbr + (int64_t)ki * lv.cap + sl;  // this lane's next list entry
-        const uint16_t* lend = lv.nbr + (int64_t)ki * lv.cap + nl;
-        int tn = lp < lend ? (int)*lp : 0x7fffffff;  // next slot of this lane
+        const bool one_round = rend - rbeg <= ENT;
+        const int nit = (icount + NW * G - 1) / (NW * G);
         IStage ist;
         if constexpr (IREC) {
             ist.grec = pass.grec; ist.gpos = pass.gpos; ist.ncnt = lv.ncnt;
             ist.ifirst = ifirst; ist.icount = icount;
         }
-        for (int e0 = rbeg; e0 < rend; e0 += ENT) {
-            const int nent = min(ENT, rend - e0);
-            stage_list_round<Pass::PAY, NW, ENT, IREC>(sm, rv, pass.jrows, pass.jpay, e0, nent, phase,
-                                                        IREC && e0 == rbeg ? &ist : nullptr);
-            if constexpr (IREC) {
-                if (e0 == rbeg && wactive) {  // i-data from the staged copy
-                    const int ii = ki - ifirst;
-                    pass.load_i_staged(ki, sm.ipos[ii], &sm.irec[ii * 9], is);
-                    nl = ivalid ? sm.icnt[ii + (ifirst & 3)] : 0;
-                    lend = lv.nbr + (int64_t)ki * lv.cap + nl;
-                    tn = lp < lend ? (int)*lp : 0x7fffffff;
+        if (one_round)
+            stage_list_round<Pass::PAY, NW, ENT, IREC>(sm, rv, pass.jrows, pass.jpay, rbeg, rend - rbeg, phase,
+                                                        IREC ? &ist : nullptr);
+        for (int it = 0; it < nit; ++it) {
+            const int ibase = (it * NW + warp) * G;
+            const bool wactive = ibase < icount;
+            const bool ivalid = ibase + il < icount;
+            typename Pass::I is;
+            typename Pass::Acc acc;
+            pass.init(acc);
+            const int ki = ifirst + ibase + (ivalid ? il : 0);
+            int nl = 0;
+            if (wactive) {
+                bool staged = false;
+                if constexpr (IREC) {
+                    if (one_round) {  // i-data from the staged copy
+                        const int ii = ki - ifirst;
+                        pass.load_i_staged(ki, sm.ipos[ii], &sm.irec[ii * 9], is);
+                        nl = ivalid ? sm.icnt[ii + (ifirst & 3)] : 0;
+                        staged = true;
+                    }
+                }
+                if (!staged) {
+                    pass.load_i(ki, is);
+                    if (ivalid) nl = lv.ncnt[ki];
                 }
             }
-            if (wactive) {
-                const int rs = (e0 - rbeg) * JMAX, re = rs + nent * JMAX;
+            const uint16_t* lp = lv.nbr + (int64_t)ki * lv.cap + sl;  // this lane's next list entry
+            const uint16_t* const lend = lv.nbr + (int64_t)ki * lv.cap + nl;
+            int tn = lp < lend ? (int)*lp : 0x7fffffff;  // next slot of this lane
+            for (int e0 = rbeg; e0 < rend; e0 += ENT) {
+                const int nent = min(ENT, rend - e0);
+                if (!one_round) stage_list_round<Pass::PAY, NW, ENT, IREC>(sm, rv, pass.jrows, pass.jpay, e0, nent, phase);
+                if (wactive) {
+                    const int rs = (e0 - rbeg) * JMAX, re = rs + nent * JMAX;
 #pragma unroll 1
-                while (__any_sync(0xffffffffu, tn < re)) {
-                    if (tn < re) {
-                        const int tl = tn - rs;
-                        const float4 jp = sm.raw[tl];
-                        lp += S;
-                        tn = lp < lend ? (int)*lp : 0x7fffffff;
-                        pass.pair(is, acc, jp, sm.pay + tl * Pass::PAY,
-                                  __float_as_int(sm.eoff[tl / JMAX].w) + tl % JMAX);
+                    while (__any_sync(0xffffffffu, tn < re)) {
+                        if (tn < re) {
+                            const int tl = tn - rs;
+                            const float4 jp = sm.raw[tl];
+                            lp += S;
+                            tn = lp < lend ? (int)*lp : 0x7fffffff;
+                            pass.pair(is, acc, jp, sm.pay + tl * Pass::PAY,
+                                      __float_as_int(sm.eoff[tl / JMAX].w) + tl % JMAX);
+                        }
                     }
                 }
             }
-        }
-        if (wactive) {
-            pass.template reduce<-S>(acc);
-            if (ivalid && sl == 0) pass.finish(ki, is, acc);
+            if (wactive) {
+                pass.template reduce<-S>(acc);
+                if (ivalid && sl == 0) pass.finish(ki, is, acc);
+            }
         }
     };
     if (!lv.gate) {  // one CTA per row (measured faster than claiming rows: the hardware
