@@ -257,6 +257,18 @@ crk_status crk_select_cells(struct crk_ctx* ctx, const float* x, const float* y,
 crk_status crk_select_gas(struct crk_ctx* ctx, const uint8_t* mask_x, const uint8_t* mask_y,
                           const uint8_t* mask_z, int32_t* idx_out, int64_t* count_out, void* stream);
 
+/* Device-count variants (no host synchronisation; the weak-scaling exchange of domain.py):
+ * the mask is ONE device array of ncell[0] + ncell[1] + ncell[2] bytes (x, then y, then z
+ * masks); the number selected is written to *count_dev (device int32). */
+crk_status crk_select_cells_dev(struct crk_ctx* ctx, const float* x, const float* y, const float* z,
+                                const uint8_t* species, int gas_only, int64_t n, const uint8_t* dmask,
+                                int32_t* idx_out, int32_t* count_dev, void* stream);
+crk_status crk_select_gas_dev(struct crk_ctx* ctx, const uint8_t* dmask, int32_t* idx_out, int32_t* count_dev,
+                              void* stream);
+/* R1 pack of the first min(*count_dev, cap) selected particles (idx: device, capacity cap). */
+crk_status crk_pack_particles_dev(struct crk_ctx* ctx, const crk_particles* parts, const int32_t* idx,
+                                  const int32_t* count_dev, int64_t cap, void* out, void* stream);
+
 /* R1: pack / unpack whole particles as 48-byte records (x y z vx vy vz m H u, species,
  * id).  unpack writes records [0, n) to parts entries [offset, offset + n). */
 crk_status crk_pack_particles(struct crk_ctx* ctx, const crk_particles* parts, const int32_t* idx,
@@ -271,6 +283,14 @@ crk_status crk_pack_gas(struct crk_ctx* ctx, int what, const int32_t* idx, int64
                         void* stream);
 crk_status crk_unpack_gas(struct crk_ctx* ctx, int what, const int32_t* idx, int64_t n, const void* in,
                           void* stream);
+/* R2 with velocities (the decomposed substep's R2): per gas rank idx[t], a float4 (V, vx, vy, vz)
+ * — the volume and the gravity-kicked velocity its owner's Extras reads (a ghost's R1 copy
+ * predates the owner's kick).  unpack writes V into the corrections/extras j-rows and v into
+ * the caller's arrays (sorted position gas_idx of the ghost).  After crk_geometry. */
+crk_status crk_pack_gas_state(struct crk_ctx* ctx, const crk_particles* parts, const int32_t* idx, int64_t n,
+                              void* out, void* stream);
+crk_status crk_unpack_gas_state(struct crk_ctx* ctx, crk_particles* parts, const int32_t* idx, int64_t n,
+                                const void* in, void* stream);
 
 /* ---- long-range gravity, particle mesh (PAPER.md:146-147 force
  * split; readings in DESIGN.md §2 "Long-range PM") ----

@@ -24,7 +24,9 @@ EXPORTS = ["crk_create", "crk_destroy", "crk_build_lists", "crk_gravity_kick", "
            "crk_pack_particles", "crk_unpack_particles", "crk_pack_gas", "crk_unpack_gas", "crk_courant_dt",
            "crk_kick", "crk_drift", "crk_update_h", "crk_refresh", "crk_pm_create", "crk_pm_destroy",
            "crk_pm_accel", "crk_pm_slab_create", "crk_pm_deposit", "crk_pm_slab_forward", "crk_pm_slab_solve",
-           "crk_pm_slab_inverse", "crk_pm_interp", "crk_neighbour_lists"]
+           "crk_pm_slab_inverse", "crk_pm_interp", "crk_neighbour_lists",
+           "crk_select_cells_dev", "crk_select_gas_dev", "crk_pack_particles_dev", "crk_pack_gas_state",
+           "crk_unpack_gas_state"]
 
 
 class CrkError(RuntimeError):
@@ -115,6 +117,14 @@ def lib():
                                        vp, C.POINTER(C.c_int64), vp]
         L.crk_select_gas.argtypes = [vp, C.c_char_p, C.c_char_p, C.c_char_p, vp, C.POINTER(C.c_int64), vp]
         L.crk_pack_particles.argtypes = [vp, C.POINTER(CrkParticles), vp, C.c_int64, vp, vp]
+        L.crk_select_cells_dev.argtypes = [vp, vp, vp, vp, vp, C.c_int, C.c_int64, vp, vp, vp, vp]
+        L.crk_select_gas_dev.argtypes = [vp, vp, vp, vp, vp]
+        L.crk_pack_particles_dev.argtypes = [vp, C.POINTER(CrkParticles), vp, vp, C.c_int64, vp, vp]
+        L.crk_pack_gas_state.argtypes = [vp, C.POINTER(CrkParticles), vp, C.c_int64, vp, vp]
+        L.crk_unpack_gas_state.argtypes = [vp, C.POINTER(CrkParticles), vp, C.c_int64, vp, vp]
+        for f in ("crk_select_cells_dev", "crk_select_gas_dev", "crk_pack_particles_dev", "crk_pack_gas_state",
+                  "crk_unpack_gas_state"):
+            getattr(L, f).restype = C.c_int
         L.crk_unpack_particles.argtypes = [vp, C.POINTER(CrkParticles), C.c_int64, C.c_int64, vp, vp]
         L.crk_pack_gas.argtypes = [vp, C.c_int, vp, C.c_int64, vp, vp]
         L.crk_unpack_gas.argtypes = [vp, C.c_int, vp, C.c_int64, vp, vp]
@@ -202,8 +212,13 @@ class Particles:
         return s
 
     def to_host(self, keys=None) -> dict:
+        """Host copies of the first n entries (the arrays may have a larger capacity)."""
         keys = keys or [k for k in _PF if getattr(self, k, None) is not None]
-        return {k: getattr(self, k).cpu().numpy() for k in keys}
+        out = {}
+        for k in keys:
+            t = getattr(self, k)
+            out[k] = (t[:, : self.n] if t.ndim == 2 else t[: self.n]).cpu().numpy()
+        return out
 
 
 class _CAI:
@@ -415,6 +430,26 @@ class Solver:
                                          self._stream(stream)), self.ctx)
         return out[: cnt.value]
 
+    def select_cells_dev(self, parts, dmask, idx_out, count_dev, n, gas_only=False, stream=None):
+        """Indices of parts[:n] in the masked cells into idx_out, the count into count_dev
+        (device int32 scalar); dmask: device uint8 (x, y, z masks concatenated); no host sync."""
+        self._check(lib().crk_select_cells_dev(self.ctx, C.c_void_p(parts.x.data_ptr()), C.c_void_p(parts.y.data_ptr()),
+                                               C.c_void_p(parts.z.data_ptr()), C.c_void_p(parts.species.data_ptr()),
+                                               int(gas_only), int(n), C.c_void_p(dmask.data_ptr()),
+                                               C.c_void_p(idx_out.data_ptr()), C.c_void_p(count_dev.data_ptr()),
+                                               self._stream(stream)), self.ctx)
+
+    def select_gas_dev(self, dmask, idx_out, count_dev, stream=None):
+        self._check(lib().crk_select_gas_dev(self.ctx, C.c_void_p(dmask.data_ptr()), C.c_void_p(idx_out.data_ptr()),
+                                             C.c_void_p(count_dev.data_ptr()), self._stream(stream)), self.ctx)
+
+    def pack_particles_dev(self, parts, idx, count_dev, out, stream=None):
+        """R1 records of the first min(count, capacity) selected particles into out (cap, 12) f32."""
+        ps = parts.struct()
+        self._check(lib().crk_pack_particles_dev(self.ctx, C.byref(ps), C.c_void_p(idx.data_ptr()),
+                                                 C.c_void_p(count_dev.data_ptr()), int(out.shape[0]),
+                                                 C.c_void_p(out.data_ptr()), self._stream(stream)), self.ctx)
+
     def pack_particles(self, parts, idx, stream=None):
         out = torch.empty((idx.numel(), 12), dtype=torch.float32, device=parts.device)
         ps = parts.struct()
@@ -433,6 +468,19 @@ class Solver:
         self._check(lib().crk_pack_gas(self.ctx, int(what), C.c_void_p(idx.data_ptr()), idx.numel(),
                                        C.c_void_p(out.data_ptr()), self._stream(stream)), self.ctx)
         return out
+
+    def pack_gas_state(self, parts, idx, stream=None):
+        """R2 records (V, vx, vy, vz) of the gas ranks idx (crk_pack_gas_state)."""
+        out = torch.empty((idx.numel(), 4), dtype=torch.float32, device=idx.device)
+        ps = parts.struct()
+        self._check(lib().crk_pack_gas_state(self.ctx, C.byref(ps), C.c_void_p(idx.data_ptr()), idx.numel(),
+                                             C.c_void_p(out.data_ptr()), self._stream(stream)), self.ctx)
+        return out
+
+    def unpack_gas_state(self, parts, idx, buf, stream=None):
+        ps = parts.struct()
+        self._check(lib().crk_unpack_gas_state(self.ctx, C.byref(ps), C.c_void_p(idx.data_ptr()), idx.numel(),
+                                               C.c_void_p(buf.data_ptr()), self._stream(stream)), self.ctx)
 
     def unpack_gas(self, what, idx, buf, stream=None):
         self._check(lib().crk_unpack_gas(self.ctx, int(what), C.c_void_p(idx.data_ptr()), idx.numel(),

@@ -210,7 +210,7 @@ crk_status crk_destroy(crk_ctx* c) {
             if (b->p) cudaFree(b->p);
     }
     for (int m = 0; m < 2; ++m) {
-        Buf* lb[] = {&c->rowlen[m], &c->rowoff[m], &c->col[m], &c->shift[m], &c->erec[m]};
+        Buf* lb[] = {&c->rowlen[m], &c->rowoff[m], &c->col[m], &c->shift[m], &c->erec[m], &c->rowend[m], &c->csroff[m]};
         for (Buf* b : lb)
             if (b->p) cudaFree(b->p);
     }
@@ -327,8 +327,8 @@ crk_status crk_list_view(crk_ctx* c, crk_lists* o) {
     o->n_gas = c->n_gas;
     o->gas_idx = P<int32_t>(c->gas_idx);
     for (int m = 0; m < 2; ++m) {
-        o->n_entries[m] = c->nent[m];
-        o->row_off[m] = P<int32_t>(c->rowoff[m]);
+        o->n_entries[m] = c->nlist[m];
+        o->row_off[m] = P<int32_t>(c->csroff[m]);
         o->col[m] = P<int32_t>(c->col[m]);
         o->shift[m] = P<int8_t>(c->shift[m]);
     }

@@ -257,8 +257,9 @@ struct ListArgs {
     float inv_q;
     double q2inv_slack;    // (1 + 2^-20) / q^2, exact
     int ncell[3];
-    int32_t* rowlen;       // pass 1
-    const int32_t* rowoff; // pass 2
+    int32_t* rowlen;       // bound pass: candidate j-leaves per row (upper bound of its length)
+    const int32_t* rowoff; // fill pass: where each row starts (exclusive scan of the bounds)
+    int32_t* rowend;       // fill pass: where each row ends
     const int32_t* jfirst;  // j-leaf first member / count (packed entry records)
     const int32_t* jcount;
     int2* erec;
@@ -294,6 +295,10 @@ constexpr int LIST_WARPS = 8;
 // cells are flattened across the lanes (warp scan) and tested with the exact integer
 // form of O4 (gaps are multiples of q below 2^24 q).  Tiny boxes use the generic path
 // with the per-axis shift search.
+// Two launches: FILL = false only sums the candidate j-leaves of the surviving cells (an
+// upper bound of the row's length: no leaf tests), FILL = true tests and writes the row at the
+// start its bound reserved and records where it ends — one pass of leaf tests instead of a
+// count pass and a fill pass.
 template <bool FILL>
 __global__ void __launch_bounds__(LIST_WARPS * 32, 5) k_lists(ListArgs A) {
     __shared__ int32_t s_b0[LIST_WARPS][32], s_ex[LIST_WARPS][32], s_code[LIST_WARPS][32];
@@ -353,6 +358,10 @@ __global__ void __launch_bounds__(LIST_WARPS * 32, 5) k_lists(ListArgs A) {
                 if (lane >= o) pre += v;
             }
             const int tot = __shfl_sync(0xffffffffu, pre, 31);
+            if (!FILL) {  // bound: every candidate leaf of the surviving cells
+                total += tot;
+                continue;
+            }
             s_b0[w][lane] = b0;
             s_ex[w][lane] = pre - nb;
             s_code[w][lane] = code;
@@ -403,6 +412,10 @@ __global__ void __launch_bounds__(LIST_WARPS * 32, 5) k_lists(ListArgs A) {
                     const uint32_t wz = (uint32_t)((cz % A.ncell[2] + A.ncell[2]) % A.ncell[2]);
                     const uint64_t m = morton3(wx, wy, wz);
                     const int b0 = A.loffB[m], b1 = A.loffB[m + 1];
+                    if (!FILL) {
+                        total += b1 - b0;
+                        continue;
+                    }
                     for (int bb = b0; bb < b1; bb += 32) {
                         const int b = bb + lane;
                         bool keep = false;
@@ -420,7 +433,10 @@ __global__ void __launch_bounds__(LIST_WARPS * 32, 5) k_lists(ListArgs A) {
                     }
                 }
     }
-    if (!FILL && lane == 0) A.rowlen[a] = total;
+    if (lane == 0) {
+        if (FILL) A.rowend[a] = outpos;
+        else A.rowlen[a] = total;
+    }
 }
 
 // ---------------------------------------------------------------- driver
@@ -449,6 +465,7 @@ static ListArgs list_args(crk_ctx* c, int m) {
     A.q2inv_slack = (1.0 + 0x1p-20) / (L.q * L.q);
     A.rowlen = P<int32_t>(c->rowlen[m]);
     A.rowoff = P<int32_t>(c->rowoff[m]);
+    A.rowend = P<int32_t>(c->rowend[m]);
     A.jfirst = P<int32_t>(c->lfirst[sb]);
     A.jcount = P<int32_t>(c->lcount[sb]);
     A.erec = P<int2>(c->erec[m]);
@@ -507,10 +524,13 @@ __global__ void k_repack_gas(int64_t ng, const int32_t* __restrict__ gas_idx, co
 }
 
 // gravity list entry records from the (refreshed) j-leaf boxes, as the list fill writes them
-__global__ void k_entry_boxes(int64_t ne, const int2* __restrict__ erec, const float4* __restrict__ box8, float Lx,
-                              float Ly, float Lz, float4* ebox) {
-    const int64_t p = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
-    if (p >= ne) return;
+// (one warp per row: rows are written at their bound, so the gaps between them hold no entries)
+__global__ void k_entry_boxes(int64_t na, const int32_t* __restrict__ rowoff, const int32_t* __restrict__ rowend,
+                              const int2* __restrict__ erec, const float4* __restrict__ box8, float Lx, float Ly,
+                              float Lz, float4* ebox) {
+    const int64_t a = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5;
+    if (a >= na) return;
+    for (int p = rowoff[a] + (threadIdx.x & 31); p < rowend[a]; p += 32) {
     const int2 r = erec[p];
     const int first = r.x & 0x1fffffff, count = ((unsigned)r.x >> 29) + 1;
     const int b = r.y & 0x03ffffff, code = (unsigned)r.y >> 26;
@@ -518,6 +538,7 @@ __global__ void k_entry_boxes(int64_t ne, const int2* __restrict__ erec, const f
     const float4 bl = box8[2 * (int64_t)b], bh = box8[2 * (int64_t)b + 1];
     ebox[2 * p] = make_float4(bl.x + ox, bl.y + oy, bl.z + oz, __int_as_float(first));
     ebox[2 * p + 1] = make_float4(bh.x + ox, bh.y + oy, bh.z + oz, __int_as_float(count | (code << 8)));
+    }
 }
 
 crk_status refresh(crk_ctx* c, crk_particles* p, cudaStream_t st) {
@@ -539,8 +560,9 @@ crk_status refresh(crk_ctx* c, crk_particles* p, cudaStream_t st) {
         CRK_LAUNCHED(c, "repack gas");
     }
     for (int s = 0; s < 4; ++s) CRK_TRY(leaf_boxes(c, s, st));
-    if (c->nent[0] > 0) {
-        k_entry_boxes<<<nblk(c->nent[0], 256), 256, 0, st>>>(c->nent[0], P<int2>(c->erec[0]), P<float4>(c->lbox8[1]),
+    if (c->nleaf[0] > 0) {
+        k_entry_boxes<<<nblk(c->nleaf[0] * 32, 256), 256, 0, st>>>(c->nleaf[0], P<int32_t>(c->rowoff[0]),
+                                                             P<int32_t>(c->rowend[0]), P<int2>(c->erec[0]), P<float4>(c->lbox8[1]),
                                                              c->lay.L[0], c->lay.L[1], c->lay.L[2],
                                                              P<float4>(c->gebox));
         CRK_LAUNCHED(c, "entry boxes");
@@ -685,11 +707,12 @@ crk_status build_lists(crk_ctx* c, crk_particles* p, cudaStream_t st) {
         const int64_t na = c->nleaf[m == 0 ? 0 : 2];
         CRK_TRY(grow(c, c->rowlen[m], (na + 1) * 4, st));
         CRK_TRY(grow(c, c->rowoff[m], (na + 1) * 4, st));
+        CRK_TRY(grow(c, c->rowend[m], (na + 1) * 4, st));
         ListArgs A = list_args(c, m);
         CRK_TRY(cuda_check(c, zero_async(P<int32_t>(c->rowlen[m]) + na, 4, st, c), "memset"));
         if (na > 0) {
             k_lists<false><<<nblk(na * 32, LIST_WARPS * 32), LIST_WARPS * 32, 0, st>>>(A);
-            CRK_LAUNCHED(c, "list count");
+            CRK_LAUNCHED(c, "list bound");
         }
         tmp = c->cub_tmp.cap;
         CRK_TRY(cuda_check(c, cub::DeviceScan::ExclusiveSum(c->cub_tmp.p, tmp, P<int32_t>(c->rowlen[m]),
@@ -738,24 +761,53 @@ crk_status build_lists(crk_ctx* c, crk_particles* p, cudaStream_t st) {
     return CRK_OK;
 }
 
-// crk_list_view's CSR col / shift arrays, decoded from the packed entries
-__global__ void k_decode_entries(int64_t ne, const int2* __restrict__ erec, int32_t* col, int8_t* shift) {
-    const int64_t p = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
-    if (p >= ne) return;
-    const int2 r = erec[p];
-    col[p] = r.y & 0x03ffffff;
-    shift[p] = (int8_t)((unsigned)r.y >> 26);
+// crk_list_view's CSR (compacted: rows are stored at their bounds) col / shift arrays, decoded
+// from the packed entries, one warp per row
+__global__ void k_decode_rows(int64_t na, const int32_t* __restrict__ rowoff, const int32_t* __restrict__ rowend,
+                              const int32_t* __restrict__ csroff, const int2* __restrict__ erec, int32_t* col,
+                              int8_t* shift) {
+    const int64_t a = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5;
+    if (a >= na) return;
+    const int lane = threadIdx.x & 31;
+    const int b0 = rowoff[a], b1 = rowend[a], o = csroff[a];
+    for (int p = b0 + lane; p < b1; p += 32) {
+        const int2 r = erec[p];
+        col[o + p - b0] = r.y & 0x03ffffff;
+        shift[o + p - b0] = (int8_t)((unsigned)r.y >> 26);
+    }
+}
+
+__global__ void k_row_lengths(int64_t na, const int32_t* __restrict__ rowoff, const int32_t* __restrict__ rowend,
+                              int32_t* len) {
+    const int64_t a = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+    if (a < na) len[a] = rowend[a] - rowoff[a];
+    if (a == na) len[a] = 0;
 }
 
 crk_status csr_views(crk_ctx* c) {
     if (c->csr_views) return CRK_OK;
     for (int m = 0; m < 2; ++m) {
-        const int64_t ne = c->nent[m] > 0 ? c->nent[m] : 1;
-        CRK_TRY(grow(c, c->col[m], ne * 4, 0));
-        CRK_TRY(grow(c, c->shift[m], ne, 0));
-        if (c->nent[m] > 0) {
-            k_decode_entries<<<nblk(c->nent[m], 256), 256>>>(c->nent[m], P<int2>(c->erec[m]), P<int32_t>(c->col[m]),
-                                                             P<int8_t>(c->shift[m]));
+        const int64_t na = c->nleaf[m == 0 ? 0 : 2];
+        CRK_TRY(grow(c, c->csroff[m], (na + 1) * 4, 0));
+        k_row_lengths<<<nblk(na + 1, 256), 256>>>(na, P<int32_t>(c->rowoff[m]), P<int32_t>(c->rowend[m]),
+                                                  P<int32_t>(c->rowlen[m]));
+        CRK_LAUNCHED(c, "row lengths");
+        size_t tmp = 0;
+        cub::DeviceScan::ExclusiveSum(nullptr, tmp, P<int32_t>(c->rowlen[m]), P<int32_t>(c->csroff[m]), (int)(na + 1));
+        CRK_TRY(grow(c, c->cub_tmp, tmp, 0));
+        tmp = c->cub_tmp.cap;
+        CRK_TRY(cuda_check(c, cub::DeviceScan::ExclusiveSum(c->cub_tmp.p, tmp, P<int32_t>(c->rowlen[m]),
+                                                            P<int32_t>(c->csroff[m]), (int)(na + 1)), "csr scan"));
+        c->launches += 2;
+        int32_t tot = 0;
+        CRK_TRY(cuda_check(c, cudaMemcpy(&tot, P<int32_t>(c->csroff[m]) + na, 4, cudaMemcpyDeviceToHost), "csr size"));
+        c->nlist[m] = tot;
+        CRK_TRY(grow(c, c->col[m], (size_t)(tot > 0 ? tot : 1) * 4, 0));
+        CRK_TRY(grow(c, c->shift[m], (size_t)(tot > 0 ? tot : 1), 0));
+        if (na > 0) {
+            k_decode_rows<<<nblk(na * 32, 256), 256>>>(na, P<int32_t>(c->rowoff[m]), P<int32_t>(c->rowend[m]),
+                                                       P<int32_t>(c->csroff[m]), P<int2>(c->erec[m]),
+                                                       P<int32_t>(c->col[m]), P<int8_t>(c->shift[m]));
             CRK_LAUNCHED(c, "decode entries");
         }
     }

@@ -46,7 +46,8 @@ struct crk_ctx {
     int stage = crk::ST_NONE;
     int64_t n = 0, n_gas = 0;
     int64_t nleaf[4] = {0, 0, 0, 0};
-    int64_t nent[2] = {0, 0};
+    int64_t nent[2] = {0, 0};     // list capacity (entries allocated: the rows' upper bounds)
+    int64_t nlist[2] = {0, 0};    // entries in the lists (set by csr_views)
     int64_t launches = 0;
     std::string err;
 
@@ -67,6 +68,8 @@ struct crk_ctx {
     crk::Buf dev_scalars;        // [0] float max H^2 ; [1..] int64 totals
     // lists (0 gravity, 1 hydro)
     crk::Buf rowlen[2], rowoff[2], col[2], shift[2];
+    crk::Buf rowend[2];          // row a holds entries [rowoff[a], rowend[a]) (rows written at their bound)
+    crk::Buf csroff[2];          // crk_list_view: compacted CSR row offsets
     crk::Buf erec[2];            // packed entries: int2 (first | (count-1) << 29, leaf | shift << 26)
     crk::Buf gebox;              // gravity entries: float4 (lo + shift, first), (hi + shift, count)
     // gas-ordered state

@@ -122,7 +122,8 @@ struct GravSymArgs {
     const float4* ebox;  // per list entry: (lo + shift, first), (hi + shift, count | shift code << 8)
     const float4* box8;  // gravity j-leaf padded boxes
     const int2* erec;    // packed list entries
-    const int32_t* row_off;
+    const int32_t* row_off;  // row a: entries [row_off[a], row_end[a])
+    const int32_t* row_end;
     const int32_t* ifirst;
     const int32_t* icount;
     float4* acc;
@@ -133,6 +134,7 @@ struct GravSymArgs {
     float L[3];
     float rcut2, eps2;
     float c0, c1, c2, c3, c4, c5;
+    float nc[6];         // -c0 .. -c5 (read straight from the parameter bank in the packed Horner chain)
     // domain decomposition (grav_pipe_kernel): a particle is owned iff its cell
     // (x / q) >> cs lies in [dlo, dhi) on every axis; ghosts have no i-groups here
     bool partial;
@@ -202,7 +204,7 @@ __global__ void __launch_bounds__(NW * 32, MINB) grav_sym_kernel(const GravSymAr
     if (w < A.nitems) {
         const int a0 = w / A.split;
         const int r0 = A.row_off[a0];
-        grav_stage<NW, ENT, NB, G>(sm, A, 0, r0, min(ENT, A.row_off[a0 + 1] - r0));
+        grav_stage<NW, ENT, NB, G>(sm, A, 0, r0, min(ENT, A.row_end[a0] - r0));
     }
     while (w < A.nitems) {
         // claim and prefetch the next work item into the other buffer (free since the
@@ -213,7 +215,7 @@ __global__ void __launch_bounds__(NW * 32, MINB) grav_sym_kernel(const GravSymAr
         if (NB == 2 && wn < A.nitems) {
             const int an = wn / A.split;
             const int rn = A.row_off[an];
-            grav_stage<NW, ENT, NB, G>(sm, A, b ^ 1, rn, min(ENT, A.row_off[an + 1] - rn));
+            grav_stage<NW, ENT, NB, G>(sm, A, b ^ 1, rn, min(ENT, A.row_end[an] - rn));
         }
 
         const int a = w / A.split;
@@ -223,7 +225,7 @@ __global__ void __launch_bounds__(NW * 32, MINB) grav_sym_kernel(const GravSymAr
         const bool wactive = ibase < icount;
         const int gself = ifirst + ibase;  // this warp's group: [gself, gself + ng)
         const int ng = min(G, icount - ibase);
-        const int rbeg = A.row_off[a], rend = A.row_off[a + 1];
+        const int rbeg = A.row_off[a], rend = A.row_end[a];
 
         float lo[3] = {0.f, 0.f, 0.f}, hi[3] = {0.f, 0.f, 0.f};
         if (wactive) {
@@ -434,7 +436,7 @@ __global__ void __launch_bounds__(symw::NW * 32, 16 / symw::NW) grav_warp_kernel
         if (ibase >= icount) continue;
         const int gself = __ldg(A.ifirst + a) + ibase;  // this warp's group: [gself, gself + ng)
         const int ng = min(G, icount - ibase);
-        const int rbeg = __ldg(A.row_off + a), rend = __ldg(A.row_off + a + 1);
+        const int rbeg = __ldg(A.row_off + a), rend = __ldg(A.row_end + a);
 
         float lo[3], hi[3];
         {
@@ -638,7 +640,7 @@ __global__ void __launch_bounds__(symh::NW * 32, 16 / symh::NW) grav_halfwarp_ke
         if (ibase >= icount) continue;
         const int gself = __ldg(A.ifirst + a) + ibase;
         const int ng = min(G, icount - ibase);
-        const int rbeg = __ldg(A.row_off + a), rend = __ldg(A.row_off + a + 1);
+        const int rbeg = __ldg(A.row_off + a), rend = __ldg(A.row_end + a);
 
         // lower half: the item's i-particles (index -1: no particle)
         float4 ip = make_float4(0.f, 0.f, 0.f, 0.f);
@@ -798,7 +800,7 @@ __global__ void __launch_bounds__(symp::NW * 32, MINB) grav_pipe_kernel(const Gr
         if (ibase >= icount) continue;
         const int gself = __ldg(A.ifirst + a) + ibase;
         const int ng = min(G, icount - ibase);
-        const int rbeg = __ldg(A.row_off + a), rend = __ldg(A.row_off + a + 1);
+        const int rbeg = __ldg(A.row_off + a), rend = __ldg(A.row_end + a);
         const int nch = (rend - rbeg + CH - 1) / CH;
 
         auto issue_entries = [&](int c) {  // entry records of chunk c -> er[c & 1]
@@ -915,8 +917,9 @@ __global__ void __launch_bounds__(symp::NW * 32, MINB) grav_pipe_kernel(const Gr
             } else {
                 const float mj = jown ? 0.f : jp.w;
                 const float2 mj2 = make_float2(mj, mj), e22 = make_float2(e2, e2);
-                const float2 n0 = make_float2(-c0, -c0), n1 = make_float2(-c1, -c1), n2 = make_float2(-c2, -c2);
-                const float2 n3 = make_float2(-c3, -c3), n4 = make_float2(-c4, -c4), n5 = make_float2(-c5, -c5);
+                const float2 n0 = make_float2(A.nc[0], A.nc[0]), n1 = make_float2(A.nc[1], A.nc[1]);
+                const float2 n2 = make_float2(A.nc[2], A.nc[2]), n3 = make_float2(A.nc[3], A.nc[3]);
+                const float2 n4 = make_float2(A.nc[4], A.nc[4]), n5 = make_float2(A.nc[5], A.nc[5]);
                 float2 bx = make_float2(0.f, 0.f), by = bx, bz = bx;
 #pragma unroll
                 for (int k = 0; k < G / 2; ++k) {
@@ -1049,6 +1052,7 @@ static RowView grav_rows(crk_ctx* c) {
     rv.ifirst = P<int32_t>(c->lfirst[0]);
     rv.icount = P<int32_t>(c->lcount[0]);
     rv.row_off = P<int32_t>(c->rowoff[0]);
+    rv.row_end = P<int32_t>(c->rowend[0]);
     rv.erec = P<int2>(c->erec[0]);
     rv.box8 = P<float4>(c->lbox8[1]);
     for (int a = 0; a < 3; ++a) rv.L[a] = c->lay.L[a];
@@ -1101,6 +1105,7 @@ static GravSymArgs grav_args(crk_ctx* c) {
     A.box8 = P<float4>(c->lbox8[1]);
     A.erec = P<int2>(c->erec[0]);
     A.row_off = P<int32_t>(c->rowoff[0]);
+    A.row_end = P<int32_t>(c->rowend[0]);
     A.ifirst = P<int32_t>(c->lfirst[0]);
     A.icount = P<int32_t>(c->lcount[0]);
     A.acc = P<float4>(c->gacc);
@@ -1110,6 +1115,7 @@ static GravSymArgs grav_args(crk_ctx* c) {
     A.eps2 = c->prm.eps2;
     A.c0 = c->prm.poly[0]; A.c1 = c->prm.poly[1]; A.c2 = c->prm.poly[2];
     A.c3 = c->prm.poly[3]; A.c4 = c->prm.poly[4]; A.c5 = c->prm.poly[5];
+    for (int k = 0; k < 6; ++k) A.nc[k] = -c->prm.poly[k];
     A.partial = c->lay.partial;
     A.inv_q = c->lay.inv_q;
     A.cs = c->lay.cs;

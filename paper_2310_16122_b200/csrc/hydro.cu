@@ -707,7 +707,7 @@ __global__ void __launch_bounds__(ASL_NW * 32, 2) acc_symlist_kernel(const AccSy
         const int icount = rv.icount[a];
         const bool wactive = ibase < icount;
         const bool ivalid = ibase + il < icount;
-        const int rbeg = rv.row_off[a], rend = rv.row_off[a + 1];
+        const int rbeg = rv.row_off[a], rend = rv.row_end[a];
         const int ki = rv.ifirst[a] + ibase + (ivalid ? il : 0);
         Rec ri;
         float4 ip = make_float4(0.f, 0.f, 0.f, 0.f);
@@ -800,7 +800,7 @@ __global__ void __launch_bounds__(64) k_update_h(RowView rv, ListView lv, const 
     const float4 pi = gpos[ki];
     const float h2i = __fmul_rn(pi.w, pi.w);
     const int ntrue = lv.ncnt[ki];
-    const bool row_lists = (rv.row_off[a + 1] - rbeg) * JMAX <= 65536;  // longer rows have no lists
+    const bool row_lists = (rv.row_end[a] - rbeg) * JMAX <= 65536;  // longer rows have no lists
     const int nl = row_lists ? min(ntrue, lv.cap) : 0;
     const uint16_t* L = lv.nbr + (int64_t)ki * lv.cap;
     float d2[128];
@@ -848,6 +848,7 @@ static RowView hydro_rows(crk_ctx* c) {
     rv.ifirst = P<int32_t>(c->lfirst[2]);
     rv.icount = P<int32_t>(c->lcount[2]);
     rv.row_off = P<int32_t>(c->rowoff[1]);
+    rv.row_end = P<int32_t>(c->rowend[1]);
     rv.erec = P<int2>(c->erec[1]);
     rv.box8 = P<float4>(c->lbox8[3]);
     for (int a = 0; a < 3; ++a) rv.L[a] = c->lay.L[a];
@@ -1076,8 +1077,9 @@ static crk_status accel_gather(crk_ctx* c, crk_particles* p, float dt, cudaStrea
     g.ahx = p->ahx; g.ahy = p->ahy; g.ahz = p->ahz; g.dudt = p->dudt;
     g.vx = p->vx; g.vy = p->vy; g.vz = p->vz; g.u = p->u;
     g.cnt = nullptr;
-    // list walk with 16 lanes per i (G = 2): bank-conflict-free record reads (pairs.cuh list_kernel)
-    if (lists_on(c)) return launch_listed<AccPass<false, BT>, 72, 2, ENT, 2, 2>(c, g, st, "accel/dudt kernel");
+    // (16 lanes per i, G = 2, measured slower on c4: 15.8 vs 12.3 ms — a list's consecutive entries
+    // are 68 of the row's 512 slots, so their bank groups are no less random than 8 i's runs)
+    if (lists_on(c)) return launch_listed<AccPass<false, BT>, 72, 2, ENT, 2>(c, g, st, "accel/dudt kernel");
     return launch_hyd<AccPass<false, BT>, ENT, 2>(c, g, st, "accel/dudt kernel");
 }
 
@@ -1163,7 +1165,7 @@ __global__ void __launch_bounds__(64) k_decode_lists(RowView rv, ListView lv, co
     if (ii >= rv.icount[a]) return;
     const int k = rv.ifirst[a] + ii;
     const int rbeg = rv.row_off[a];
-    const bool row_lists = (rv.row_off[a + 1] - rbeg) * JMAX <= 65536;
+    const bool row_lists = (rv.row_end[a] - rbeg) * JMAX <= 65536;
     const int ntrue = lv.ncnt[k];
     const bool complete = row_lists && !lv.lflag[a] && ntrue <= lv.cap;
     const int64_t i = gas_idx[k];

@@ -22,7 +22,8 @@ namespace crk {
 struct RowView {
     const int32_t* ifirst;
     const int32_t* icount;
-    const int32_t* row_off;
+    const int32_t* row_off;  // row a: entries [row_off[a], row_end[a])
+    const int32_t* row_end;
     const int2* erec;     // packed entries (first | (count-1) << 29, leaf | shift << 26)
     const float4* box8;   // padded j-leaf boxes: (lo, max H^2), (hi, 0)
     float L[3];
@@ -118,7 +119,7 @@ __device__ __forceinline__ void pair_row(const Pass& pass, const RowView& rv, Pa
     const int ibase = warp * G;
     const bool wactive = ibase < icount;
     const bool ivalid = ibase + il < icount;
-    const int rbeg = rv.row_off[a], rend = rv.row_off[a + 1];
+    const int rbeg = rv.row_off[a], rend = rv.row_end[a];
     int rbase = 0;  // row-relative slot of the current round's first entry
     [[maybe_unused]] int lcap = 0;
     if constexpr (is_build<Pass>::value)  // slots are 16-bit: longer rows get no lists
@@ -438,12 +439,9 @@ __device__ __forceinline__ int claim_row(SM& sm, int* work) {
 }
 
 // G i-particles per warp, S = 32/G lanes per i.  A CTA covers NW*G i-particles at a time and
-// loops over the row's i-particles in NW*G-sized iterations (G = 8: one iteration per gas
-// i-leaf of <= 64; G = 2: a half-warp of 16 lanes per i walks 16 consecutive list entries, i.e.
-// mostly consecutive staged slots, so the half-warp's shared-memory reads of a record component
-// spread over all bank groups — no conflicts between the warp's two i-particles).  A row that
-// fits one staging round is staged once for all iterations; longer rows are restaged per
-// iteration.
+// loops over the row's i-particles in NW*G-sized iterations (G = 8 with 8 warps: one iteration
+// per gas i-leaf of <= 64).  A row that fits one staging round is staged once for all
+// iterations; longer rows are restaged per iteration.
 template <class Pass, int NW, int G, int ENT, int MINB>
 __global__ void __launch_bounds__(NW * 32, MINB) list_kernel(const Pass pass, const RowView rv, const ListView lv) {
     static_assert(32 % G == 0, "G must divide the warp");
@@ -468,7 +466,7 @@ __global__ void __launch_bounds__(NW * 32, MINB) list_kernel(const Pass pass, co
     auto row = [&](const int a) {
         const int ifirst = rv.ifirst[a];
         const int icount = rv.icount[a];
-        const int rbeg = rv.row_off[a], rend = rv.row_off[a + 1];
+        const int rbeg = rv.row_off[a], rend = rv.row_end[a];
         const bool one_round = rend - rbeg <= ENT;
         const int nit = (icount + NW * G - 1) / (NW * G);
         IStage ist;
@@ -571,23 +569,22 @@ __global__ void __launch_bounds__(NW * 32, MINB) list_kernel2(const PA pa, const
     const int icount = rv.icount[a];
     const bool wactive = ibase < icount;
     const bool ivalid = ibase + il < icount;
-    const int rbeg = rv.row_off[a], rend = rv.row_off[a + 1];
+    const int rbeg = rv.row_off[a], rend = rv.row_end[a];
     const int ki = ifirst + ibase + (ivalid ? il : 0);
     const int nl = (wactive && ivalid) ? lv.ncnt[ki] : 0;
     const uint16_t* const lbeg = lv.nbr + (int64_t)ki * lv.cap;
     const bool one_round = rend - rbeg <= ENT;
 
     // walk this lane's entries of round [e0, e0 + nent) with pass P
-    auto walk = [&](const auto& P, auto& is, auto& acc, const uint16_t*& lp, int& tn, int e0, int nent) {
+    auto walk = [&](const auto& P, auto& is, auto& acc, int& lp, int& tn, int e0, int nent) {
         const int rs = (e0 - rbeg) * JMAX, re = rs + nent * JMAX;
-        const uint16_t* const lend = lbeg + nl;
 #pragma unroll 1
         while (__any_sync(0xffffffffu, tn < re)) {
             if (tn < re) {
                 const int tl = tn - rs;
                 const float4 jp = sm.raw[tl];
                 lp += S;
-                tn = lp < lend ? (int)*lp : 0x7fffffff;
+                tn = lp < nl ? (int)__ldg(lbeg + lp) : 0x7fffffff;
                 P.pair(is, acc, jp, sm.pay + tl * PB::PAY, __float_as_int(sm.eoff[tl / JMAX].w) + tl % JMAX);
             }
         }
@@ -597,8 +594,8 @@ __global__ void __launch_bounds__(NW * 32, MINB) list_kernel2(const PA pa, const
         typename PA::Acc acc;
         pa.init(acc);
         if (wactive) pa.load_i(ki, is);
-        const uint16_t* lp = lbeg + sl;
-        int tn = lp < lbeg + nl ? (int)*lp : 0x7fffffff;
+        int lp = sl;
+        int tn = lp < nl ? (int)__ldg(lbeg + lp) : 0x7fffffff;
         for (int e0 = rbeg; e0 < rend; e0 += ENT) {
             const int nent = min(ENT, rend - e0);
             stage_list_round<PB::PAY, NW, ENT>(sm, rv, pb.jrows, pb.jpay, e0, nent, phase);
@@ -615,8 +612,8 @@ __global__ void __launch_bounds__(NW * 32, MINB) list_kernel2(const PA pa, const
         typename PB::Acc acc;
         pb.init(acc);
         if (wactive) pb.load_i(ki, is);
-        const uint16_t* lp = lbeg + sl;
-        int tn = lp < lbeg + nl ? (int)*lp : 0x7fffffff;
+        int lp = sl;
+        int tn = lp < nl ? (int)__ldg(lbeg + lp) : 0x7fffffff;
         for (int e0 = rbeg; e0 < rend; e0 += ENT) {
             const int nent = min(ENT, rend - e0);
             if (!one_round) stage_list_round<PB::PAY, NW, ENT>(sm, rv, pb.jrows, pb.jpay, e0, nent, phase);

@@ -1,22 +1,32 @@
 """3-D domain decomposition with leaf-granular ghost exchange.
 
-Host-side plumbing only: the decomposition and the cell masks are small host logic;
-the selection, packing and unpacking run in libcrksr.so (crk_select_cells /
-crk_select_gas / crk_pack_* / crk_unpack_*) and the transfers are NCCL send/recv
-through torch.distributed (batch_isend_irecv).  The paper runs one MPI rank per GPU
- but does not describe the exchange; this follows north_star's
-"3-D spatial domain decomposition with overload/ghost zones refreshed by send/recv".
+Host-side plumbing only: the decomposition and the cell masks are small host logic; the
+selection, packing and unpacking run in libcrksr.so (crk_select_cells_dev /
+crk_select_gas_dev / crk_pack_particles_dev / crk_unpack_* / crk_pack_gas) and the
+transfers are NCCL send/recv through torch.distributed (batch_isend_irecv).  The paper
+runs one MPI rank per GPU (§3.4) but does not describe the exchange; this
+follows north_star's "3-D spatial domain decomposition with overload/ghost zones refreshed
+by send/recv".
 
-Per substep (rank r owning the chaining-mesh cells D_r):
+Per substep (rank r owning the chaining-mesh cells D_r; its peers s share a halo):
   R1  own particles in D_r ∩ halo_h(D_s) -> peer s (48-byte records); build lists over
       own + ghosts with i-leaves only in D_r (so lists = the global lists' own rows);
-  gravity (i-centric), geometry;
-  R2  V of own gas in D_r ∩ halo_h(D_s) -> peer s (order: gas rank = key order on both);
+  gravity, geometry;
+  R2  V and the gravity-kicked v of own gas in D_r ∩ halo_h(D_s) -> peer s (order: gas rank =
+      key order on both sides; Extras of the receiver's own gas reads both);
   corrections, extras;
   R3  accel records of the same gas -> peer s;
-  accel / du-dt.
+  accel / du-dt; kicked v, u written back to the own set.
 halo width h = ceil(reach / cell_side), reach = max(r_c, H_max) (1 + 2^-20) with H_max the
-global maximum smoothing length (one all-reduce).
+global maximum smoothing length (one all-reduce when H changes).
+
+Built for weak scaling: the ghost plan (the peers' cell masks, uploaded
+once to the device) persists across substeps; every selection writes its count to device
+memory (no host synchronisation); the R1 counts (all particles and gas, per peer) travel in
+one small exchange and reach the host in ONE readback, which sizes the local set and every
+later message exactly (R2/R3 carry the same gas as R1); the local particle set and all
+message buffers are allocated once and grown geometrically, never per substep.  Host syncs
+per substep: that readback plus crk_build_lists' own size readbacks.
 """
 from __future__ import annotations
 
@@ -124,6 +134,12 @@ class DistExchange:
             for s, t in recvs.items():
                 dev_recvs[s].copy_(t)
 
+    def exchange(self, sends: dict, recvs: dict):
+        """Preallocated, exactly sized messages: sends / recvs {peer: tensor}; empty tensors are
+        skipped (both sides know the sizes)."""
+        self._p2p({s: t for s, t in sends.items() if t.numel() > 0},
+                  {s: t for s, t in recvs.items() if t.numel() > 0})
+
     def alltoallv(self, sends: dict, width: int, dtype=torch.float32) -> dict:
         """sends: {peer: tensor (n, width)} -> {peer: tensor (m, width)} (counts exchanged first)."""
         peers = [s for s in range(self.world) if s != self.rank]
@@ -131,9 +147,10 @@ class DistExchange:
                                    device=self.device) for s in peers}
         cnt_in = {s: torch.zeros(1, dtype=torch.int64, device=self.device) for s in peers}
         self._p2p(cnt_out, cnt_in)
+        counts = torch.cat([cnt_in[s] for s in peers]).cpu() if peers else torch.zeros(0, dtype=torch.int64)
         outs = {s: sends[s].contiguous() for s in peers if s in sends and sends[s].shape[0] > 0}
-        ins = {s: torch.empty((int(cnt_in[s].item()), width), dtype=dtype, device=self.device)
-               for s in peers if int(cnt_in[s].item()) > 0}
+        ins = {s: torch.empty((int(c), width), dtype=dtype, device=self.device)
+               for s, c in zip(peers, counts.tolist()) if c > 0}
         self._p2p(outs, ins)
         return ins
 
@@ -144,6 +161,29 @@ class DistExchange:
         t = torch.tensor([v], dtype=torch.float64, device=dev)
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
         return float(t.item())
+
+
+class EmuExchange:
+    """The same exchange between ranks emulated in one process (tests, tools/decomp_bench.py):
+    messages are device-to-device copies, in the order every real rank would post them."""
+
+    def __init__(self, ranks):
+        self.ranks = ranks
+
+    def exchange_all(self, sends, recvs):
+        """sends[r] / recvs[r]: {peer: tensor} of rank r."""
+        for r, snd in enumerate(sends):
+            for s, t in snd.items():
+                if t.numel() > 0:
+                    recvs[s][r].copy_(t)
+
+
+def _grow(t, n, **kw):
+    """t if it holds n rows, else a new tensor with 1.25 n rows (geometric growth)."""
+    if t is not None and t.shape[0] >= n:
+        return t
+    shape = (max(int(1.25 * n), 16),) + tuple(kw.pop("tail", ()))
+    return torch.empty(shape, **kw)
 
 
 class DomainRank:
@@ -160,6 +200,10 @@ class DomainRank:
         self.solver = Solver(self.params, self.device.index if self.device.index is not None else 0)
         self.stream = stream
         self.h = None
+        self.p = None          # the local set (own + ghosts), capacity >= n_total
+        self.n_total = self.n_own
+        self._buf = {}
+        self.check = False  # tests: verify the R2/R3 index-set sizes against the R1 counts (syncs)
 
     def local_hmax2(self) -> float:
         gas = self.own_host["species"] == 1
@@ -167,116 +211,232 @@ class DomainRank:
             return 0.0
         return float((self.own_host["H"][gas].astype(np.float32) ** 2).max())
 
-    # R1 ---------------------------------------------------------------
-    def r1_pack(self, h: int) -> dict:
+    # persistent ghost plan ------------------------------------------------
+    def plan(self, h: int):
+        """Device cell masks per peer for halo width h (kept until h changes): send[s] selects
+        own cells in halo_h(D_s), recv[s] the cells of D_s in halo_h(D_r)."""
+        if self.h == h:
+            return
         self.h = h
-        out = {}
+        self.peers, self.mask_send, self.mask_recv = [], {}, {}
         for s in range(self.d.P):
             if s == self.r:
                 continue
-            m = self.d.masks(recv=s, send=self.r, h=h)
-            if m is None:
+            ms = self.d.masks(recv=s, send=self.r, h=h)
+            mr = self.d.masks(recv=self.r, send=s, h=h)
+            if ms is None and mr is None:
                 continue
-            idx = self.solver.select_cells(self.own, m, n=self.n_own, stream=self.stream)
-            out[s] = self.solver.pack_particles(self.own, idx, stream=self.stream)
-        return out
+            self.peers.append(s)
+            for dst, m in ((self.mask_send, ms), (self.mask_recv, mr)):
+                dst[s] = None if m is None else torch.from_numpy(np.concatenate(m)).to(self.device)
+        npr = len(self.peers)
+        self.cnt_send = torch.zeros((max(npr, 1), 2), dtype=torch.int32, device=self.device)
+        self.cnt_recv = torch.zeros((max(npr, 1), 2), dtype=torch.int32, device=self.device)
+        self.idx_r1 = {s: torch.empty(max(self.n_own, 1), dtype=torch.int32, device=self.device)
+                       for s in self.peers}
+        self.idx_tmp = torch.empty(max(self.n_own, 1), dtype=torch.int32, device=self.device)
+        self.sbuf, self.rbuf = {}, {}
 
-    def r1_unpack_and_build(self, recv: dict):
-        n_ghost = sum(int(t.shape[0]) for t in recv.values())
-        self.n_total = self.n_own + n_ghost
-        p = Particles(self.n_total, self.device, self.outputs)
+    # R1 ---------------------------------------------------------------
+    def r1_select_pack(self):
+        """Select and pack each peer's R1 particles (counts stay on the device) into the
+        persistent send buffers; returns the (peers, 2) device counts (all, gas)."""
+        for q, s in enumerate(self.peers):
+            m = self.mask_send[s]
+            if m is None:
+                self.cnt_send[q].zero_()
+                continue
+            self.solver.select_cells_dev(self.own, m, self.idx_r1[s], self.cnt_send[q, 0:1], self.n_own,
+                                         stream=self.stream)
+            self.solver.select_cells_dev(self.own, m, self.idx_tmp, self.cnt_send[q, 1:2], self.n_own,
+                                         gas_only=True, stream=self.stream)
+            cap = self.sbuf[s].shape[0] if s in self.sbuf else 0
+            if cap:
+                self.solver.pack_particles_dev(self.own, self.idx_r1[s], self.cnt_send[q, 0:1], self.sbuf[s],
+                                               stream=self.stream)
+        return self.cnt_send
+
+    def r1_sizes(self, counts_host: np.ndarray):
+        """counts_host: (2, peers, 2) = [sent, received] x peer x (all, gas), the one readback.
+        Sizes the buffers (repacking any send buffer that was too small) and the local set."""
+        self.n_send = {s: int(counts_host[0, q, 0]) for q, s in enumerate(self.peers)}
+        self.g_send = {s: int(counts_host[0, q, 1]) for q, s in enumerate(self.peers)}
+        self.n_recv = {s: int(counts_host[1, q, 0]) for q, s in enumerate(self.peers)}
+        self.g_recv = {s: int(counts_host[1, q, 1]) for q, s in enumerate(self.peers)}
+        for q, s in enumerate(self.peers):
+            n = self.n_send[s]
+            old = self.sbuf.get(s)
+            if n > 0 and (old is None or old.shape[0] < n):  # grown: pack again at the new size
+                self.sbuf[s] = _grow(None, n, tail=(12,), dtype=torch.float32, device=self.device)
+                self.solver.pack_particles_dev(self.own, self.idx_r1[s], self.cnt_send[q, 0:1], self.sbuf[s],
+                                               stream=self.stream)
+            self.rbuf[s] = _grow(self.rbuf.get(s), self.n_recv[s], tail=(12,), dtype=torch.float32,
+                                 device=self.device)
+        self.n_total = self.n_own + sum(self.n_recv.values())
+
+    def r1_messages(self):
+        return ({s: self.sbuf[s][: self.n_send[s]] for s in self.peers if self.n_send[s] > 0},
+                {s: self.rbuf[s][: self.n_recv[s]] for s in self.peers if self.n_recv[s] > 0})
+
+    def r1_unpack_and_build(self):
+        cap = 0 if self.p is None else self.p.x.shape[0]
+        if cap < self.n_total:
+            self.p = Particles(max(int(1.1 * self.n_total), 16), self.device, self.outputs)
+        p = self.p
+        p.n = self.n_total
         for k in Particles.IN_F32 + ("species", "id"):
             getattr(p, k)[: self.n_own].copy_(getattr(self.own, k))
         off = self.n_own
-        for s in sorted(recv):
-            self.solver.unpack_particles(p, off, recv[s], stream=self.stream)
-            off += recv[s].shape[0]
-        self.p = p
-        self._gl = None
+        for s in self.peers:
+            n = self.n_recv[s]
+            if n > 0:
+                self.solver.unpack_particles(p, off, self.rbuf[s][:n], stream=self.stream)
+                off += n
         self.solver.build_lists(p, self.stream)
+        self._gas_idx()
+
+    def _gas_idx(self):
+        """Gas ranks (device) of the R2/R3 send set (own gas in each peer's halo) and receive
+        set (that peer's ghost gas), in key order — the same particles, in the same order, on
+        both sides; sizes known from the R1 counts (no readback)."""
+        self.gsend, self.grecv = {}, {}
+        cnt = torch.zeros(2, dtype=torch.int32, device=self.device)
+        for s in self.peers:
+            for dst, m, n, c in ((self.gsend, self.mask_send[s], self.g_send[s], cnt[0:1]),
+                                 (self.grecv, self.mask_recv[s], self.g_recv[s], cnt[1:2])):
+                if m is None or n == 0:
+                    dst[s] = None
+                    continue
+                key = ("gidx", id(dst), s)
+                buf = _grow(self._buf.get(key), self.n_total, dtype=torch.int32, device=self.device)
+                self._buf[key] = buf
+                self.solver.select_gas_dev(m, buf, c, stream=self.stream)
+                if self.check:
+                    assert int(c.item()) == n, "ghost gas set does not match the R1 gas count"
+                dst[s] = buf[:n]
 
     # passes -------------------------------------------------------------
     def gravity_geometry(self, dt_grav=0.0):
         self.solver.gravity_kick(self.p, dt_grav, self.stream)
         self.solver.geometry(self.p, self.stream)
 
-    def _gas_lists(self):
-        if getattr(self, "_gl", None) is None:
-            self._gl = {}
-            ng = self.n_total  # capacity bound
-            for s in range(self.d.P):
-                if s == self.r:
-                    continue
-                ms = self.d.masks(recv=s, send=self.r, h=self.h)
-                mr = self.d.masks(recv=self.r, send=s, h=self.h)
-                send = self.solver.select_gas(ms, self.device, self.stream, ng) if ms is not None else None
-                rec = self.solver.select_gas(mr, self.device, self.stream, ng) if mr is not None else None
-                self._gl[s] = (send, rec)
-        return self._gl
+    def _gas_messages(self, what: int):
+        w = 4 if what == 0 else 36  # R2: (V, v); R3: the accel record
+        sends, recvs = {}, {}
+        for s in self.peers:
+            if self.gsend[s] is not None:
+                sends[s] = (self.solver.pack_gas_state(self.p, self.gsend[s], self.stream) if what == 0
+                            else self.solver.pack_gas(what, self.gsend[s], self.stream))
+            if self.grecv[s] is not None:
+                key = ("grecv", what, s)
+                buf = _grow(self._buf.get(key), self.g_recv[s], tail=(w,), dtype=torch.float32, device=self.device)
+                self._buf[key] = buf
+                recvs[s] = buf[: self.g_recv[s]]
+        return sends, recvs
 
-    def r2_pack(self) -> dict:
-        return {s: self.solver.pack_gas(0, send, self.stream) for s, (send, _) in self._gas_lists().items()
-                if send is not None and send.numel() > 0}
+    def _gas_unpack(self, what: int, recvs: dict):
+        for s, buf in recvs.items():
+            if what == 0:
+                self.solver.unpack_gas_state(self.p, self.grecv[s], buf, self.stream)
+            else:
+                self.solver.unpack_gas(what, self.grecv[s], buf, self.stream)
 
-    def r2_unpack(self, recv: dict):
-        for s, buf in recv.items():
-            idx = self._gas_lists()[s][1]
-            assert idx is not None and idx.numel() == buf.shape[0], "R2 message does not match the ghost set"
-            self.solver.unpack_gas(0, idx, buf, self.stream)
+    def r2_messages(self):
+        return self._gas_messages(0)
+
+    def r2_unpack(self, recvs: dict):
+        self._gas_unpack(0, recvs)
 
     def corrections_extras(self):
         self.solver.corrections_extras(self.p, self.stream)
 
-    def r3_pack(self) -> dict:
-        return {s: self.solver.pack_gas(1, send, self.stream) for s, (send, _) in self._gas_lists().items()
-                if send is not None and send.numel() > 0}
+    def r3_messages(self):
+        return self._gas_messages(1)
 
-    def r3_unpack(self, recv: dict):
-        for s, buf in recv.items():
-            idx = self._gas_lists()[s][1]
-            assert idx is not None and idx.numel() == buf.shape[0], "R3 message does not match the ghost set"
-            self.solver.unpack_gas(1, idx, buf, self.stream)
+    def r3_unpack(self, recvs: dict):
+        self._gas_unpack(1, recvs)
 
     def accel(self, dt_hydro=0.0):
         self.solver.hydro_accel_dudt(self.p, dt_hydro, self.stream)
 
+    def writeback(self):
+        """Kicked velocities and internal energies of the own particles back into the own set
+        (the next substep's R1 reads them): own rows are the sorted positions with perm < n_own."""
+        perm = self.p.perm[: self.n_total].long()
+        own = perm < self.n_own
+        src = perm[own]
+        for k in ("vx", "vy", "vz", "u"):
+            getattr(self.own, k).index_copy_(0, src, getattr(self.p, k)[: self.n_total][own])
+
     def own_mask(self) -> torch.Tensor:
-        """Sorted positions holding own particles (inputs 0..n_own-1 are own)."""
-        return self.p.perm < self.n_own
+        """Sorted positions (of the local set) holding own particles (inputs 0..n_own-1 are own)."""
+        return self.p.perm[: self.n_total] < self.n_own
 
     def close(self):
         self.solver.close()
 
 
+def _counts_host(ranks_cnt_send, ranks_cnt_recv):
+    return [np.stack([cs.cpu().numpy(), cr.cpu().numpy()]) for cs, cr in zip(ranks_cnt_send, ranks_cnt_recv)]
+
+
 def substep_inprocess(ranks, dt_grav=0.0, dt_hydro=0.0):
-    """Run one decomposed substep for ranks emulated sequentially in one process (tests)."""
+    """One decomposed substep for ranks emulated sequentially in one process (tests): the same
+    phases and messages as substep_dist, the transfers as device copies."""
     hmax2 = max(rk.local_hmax2() for rk in ranks)
     h = ranks[0].d.halo_width(hmax2)
-    sends = [rk.r1_pack(h) for rk in ranks]
     for rk in ranks:
-        rk.r1_unpack_and_build({s: sends[s][rk.r] for s in range(len(ranks)) if rk.r in sends[s]})
+        rk.plan(h)
+    cs = [rk.r1_select_pack() for rk in ranks]
+    for rk in ranks:  # count exchange
+        for q, s in enumerate(rk.peers):
+            rk.cnt_recv[q].copy_(cs[s][ranks[s].peers.index(rk.r)])
+    for rk in ranks:
+        rk.r1_sizes(np.stack([rk.cnt_send.cpu().numpy(), rk.cnt_recv.cpu().numpy()]))
+    msgs = [rk.r1_messages() for rk in ranks]
+    EmuExchange(ranks).exchange_all([m[0] for m in msgs], [m[1] for m in msgs])
+    for rk in ranks:
+        rk.r1_unpack_and_build()
     for rk in ranks:
         rk.gravity_geometry(dt_grav)
-    sends = [rk.r2_pack() for rk in ranks]
-    for rk in ranks:
-        rk.r2_unpack({s: sends[s][rk.r] for s in range(len(ranks)) if rk.r in sends[s]})
+    msgs = [rk.r2_messages() for rk in ranks]
+    EmuExchange(ranks).exchange_all([m[0] for m in msgs], [m[1] for m in msgs])
+    for rk, m in zip(ranks, msgs):
+        rk.r2_unpack(m[1])
     for rk in ranks:
         rk.corrections_extras()
-    sends = [rk.r3_pack() for rk in ranks]
-    for rk in ranks:
-        rk.r3_unpack({s: sends[s][rk.r] for s in range(len(ranks)) if rk.r in sends[s]})
+    msgs = [rk.r3_messages() for rk in ranks]
+    EmuExchange(ranks).exchange_all([m[0] for m in msgs], [m[1] for m in msgs])
+    for rk, m in zip(ranks, msgs):
+        rk.r3_unpack(m[1])
     for rk in ranks:
         rk.accel(dt_hydro)
+        if dt_grav != 0.0 or dt_hydro != 0.0:
+            rk.writeback()
 
 
 def substep_dist(rk: DomainRank, ex: DistExchange, dt_grav=0.0, dt_hydro=0.0, hmax2=None):
-    """One decomposed substep on this rank, exchanging with the other ranks."""
+    """One decomposed substep on this rank, exchanging with the other ranks: one host
+    readback (the R1 counts) besides crk_build_lists' own."""
     if hmax2 is None:
         hmax2 = ex.allreduce_max(rk.local_hmax2())
-    h = rk.d.halo_width(hmax2)
-    rk.r1_unpack_and_build(ex.alltoallv(rk.r1_pack(h), 12))
+    rk.plan(rk.d.halo_width(hmax2))
+    cnt_send = rk.r1_select_pack()
+    npr = len(rk.peers)
+    ex.exchange({s: cnt_send[q] for q, s in enumerate(rk.peers)},
+                {s: rk.cnt_recv[q] for q, s in enumerate(rk.peers)})
+    host = torch.stack([cnt_send[:npr], rk.cnt_recv[:npr]]).cpu().numpy()  # the one readback
+    rk.r1_sizes(host)
+    ex.exchange(*rk.r1_messages())
+    rk.r1_unpack_and_build()
     rk.gravity_geometry(dt_grav)
-    rk.r2_unpack(ex.alltoallv(rk.r2_pack(), 1))
+    sends, recvs = rk.r2_messages()
+    ex.exchange(sends, recvs)
+    rk.r2_unpack(recvs)
     rk.corrections_extras()
-    rk.r3_unpack(ex.alltoallv(rk.r3_pack(), 36))
+    sends, recvs = rk.r3_messages()
+    ex.exchange(sends, recvs)
+    rk.r3_unpack(recvs)
     rk.accel(dt_hydro)
+    if dt_grav != 0.0 or dt_hydro != 0.0:
+        rk.writeback()

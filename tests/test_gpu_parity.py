@@ -178,6 +178,35 @@ def test_call_order_and_errors():
 
 
 # ------------------------------------------------------------------ full sizes, sampled outputs
+def _sampled_lists(parts, params, g, rng, n_rows=200):
+    """Full-size list parity on sampled rows: the sort order in full, and
+    for n_rows random i-leaves of each list the leaf (first, count, bbox) and the whole CSR
+    row, bit-exact after the canonical row sort, against oracle.list_rows(rows=...)."""
+    order, keys, cellm = oracle.sort_order(parts, params)
+    assert np.array_equal(g["perm"], order)
+    lv = g["lv"]
+    for m, (ki, kj) in enumerate(((0, 1), (2, 3))):
+        la = oracle.leaves(parts, params, order, cellm, ki)
+        lb = oracle.leaves(parts, params, order, cellm, kj)
+        gl = lv["leaves"][ki]
+        nA = la["count"].shape[0]
+        assert int(gl["first"].shape[0]) == nA and int(lv["leaves"][kj]["first"].shape[0]) == lb["count"].shape[0]
+        rows = np.sort(rng.choice(nA, min(n_rows, nA), replace=False))
+        rt = __import__("torch").as_tensor(rows, device=gl["first"].device)
+        assert np.array_equal(gl["first"][rt].cpu().numpy(), la["first"][rows])
+        assert np.array_equal(gl["count"][rt].cpu().numpy(), la["count"][rows])
+        assert np.array_equal(gl["bbox"][rt].cpu().numpy(), la["bbox"][rows])
+        off, col, sh = oracle.list_rows(la, lb, params, m, rows)
+        gv = lv["lists"][m]
+        goff = gv["row_off"].cpu().numpy()
+        gcol, gsh = gv["col"], gv["shift"]
+        for r, a in enumerate(rows):
+            b0, b1 = int(goff[a]), int(goff[a + 1])
+            got = _canon_rows(np.array([0, b1 - b0]), gcol[b0:b1].cpu().numpy(), gsh[b0:b1].cpu().numpy())[0]
+            exp = _canon_rows(np.array([0, off[r + 1] - off[r]]), col[off[r]:off[r + 1]], sh[off[r]:off[r + 1]])[0]
+            assert np.array_equal(got[0], exp[0]) and np.array_equal(got[1], exp[1]), (m, int(a))
+
+
 def _sampled(name, n_samp, seed=5):
     parts, params = cached_config(name)
     rng = np.random.default_rng(seed)
@@ -185,7 +214,8 @@ def _sampled(name, n_samp, seed=5):
     gas = np.nonzero(parts["species"] == 1)[0]
     tg = np.sort(rng.choice(gas, n_samp, replace=False))
     ta = np.sort(rng.choice(n, n_samp, replace=False))
-    g = run_gpu(parts, params)
+    g = run_gpu(parts, params, lists=True)
+    _sampled_lists(parts, params, g, rng)
     ref = oracle.substep(parts, params, targets=tg, grav_targets=ta)
     rc = oracle.counts(parts, params, targets=np.concatenate([ta, tg]))
     gi = g["in"]

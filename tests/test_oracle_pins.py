@@ -175,6 +175,29 @@ def test_lists_equal_brute_force(c1, mode):
         assert np.array_equal(sh[off[a]:off[a + 1]], code)
 
 
+def test_list_slack_only_leaf_pair():
+    """O4 slack: two single-particle leaves whose exact gap^2 lies in [rcut2, rcut2 (1 + 2^-20))
+    (separation (1375212, 866239) q, q = 2^-19: 5.5e-7 relative above rcut2) are listed — the
+    slack that makes the fp64 leaf test a superset of the fp32 particle predicate — while a
+    gap^2 just past the band is not."""
+    box = [16.0] * 3
+    params = make_params(box)
+    q = 16.0 * 2.0**-23
+    for kk, listed in (((1375212, 866239, 0), True), ((1375212, 866241, 0), False)):
+        d = np.asarray(kk, np.float64) * q
+        s = float(d @ d)
+        assert (s < float(np.float32(params["rcut2"])) * (1 + 2.0**-20)) == listed
+        p0 = np.array([3.5, 3.5, 1.0])  # the two particles in different cells: one leaf each
+        parts = make_parts(np.array([p0, p0 + d]), [0, 0], box)
+        order, cellm, ls = _leaf_sets(parts, params)
+        off, col, sh = oracle.list_rows(ls[0], ls[1], params, 0)
+        a0 = int(np.nonzero(ls[0]["first"] == 0)[0][0])  # the i-leaf of the first sorted particle
+        other = [b for b in range(ls[1]["count"].shape[0]) if ls[1]["first"][b] != ls[0]["first"][a0]]
+        assert len(other) == 1
+        assert (other[0] in col[off[a0]:off[a0 + 1]]) == listed
+        assert oracle.counts(parts, params)["grav"].tolist() == [0, 0]  # out under the fp32 predicate
+
+
 def test_lists_superset_of_particle_pairs(c1):
     """Every particle pair inside the cutoff belongs to a listed leaf pair (O4 slack)."""
     parts, params = c1

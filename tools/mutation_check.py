@@ -69,6 +69,8 @@ MUTATIONS = [
      "vout[3 * t + 0] = (double)vx[i] + dt * a[0];", "vout[3 * t + 0] = (double)vx[i] - dt * a[0];"),
     ("predicate_le", "gravity predicate s32 <= rcut2 instead of strict (O2)",
      "case PRED_GRAV: return s < c->rcut2;", "case PRED_GRAV: return s <= c->rcut2;"),
+    ("list_no_slack", "leaf-pair test without the 2^-20 slack (O4)",
+     "return d2 < cut2 * (1.0 + ldexp(1.0, -20));", "return d2 < cut2;"),
     ("predicate_fp64", "membership decided on the fp64 s instead of the fp32 fma sequence (O2)",
      "float t = fx * fx;", "double t = (double)fx * fx + (double)fy * fy + (double)fz * fz; return (float)t;"),
 ]
