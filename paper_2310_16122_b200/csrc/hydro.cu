@@ -132,6 +132,96 @@ struct GeoPass : HydCommon {
     }
 };
 
+// symmetric 3x3 / 3x3x3 index of the accumulated moments (CorPass accumulators)
+__device__ __forceinline__ int sym2(int a, int b) {
+    if (a > b) { int t = a; a = b; b = t; }
+    return a == 0 ? b : (a == 1 ? 2 + b : 5);
+}
+__device__ __forceinline__ int sym3(int a, int b, int g) {
+    int x = a, y = b, z = g, t;
+    if (x > y) { t = x; x = y; y = t; }
+    if (y > z) { t = y; y = z; z = t; }
+    if (x > y) { t = x; x = y; y = t; }
+    const int tab[3][3][3] = {{{0, 1, 2}, {0, 3, 4}, {0, 0, 5}},
+                              {{0, 0, 0}, {0, 6, 7}, {0, 0, 8}},
+                              {{0, 0, 0}, {0, 0, 0}, {0, 0, 9}}};
+    return tab[x][y][z];
+}
+
+// O7 coefficients A, B, grad A, grad B of one particle from its accumulated moments (d = x_j - x_i
+// convention, unscaled kernel: am* = sum V_j d.. wt, ag* = sum V_j d.. gt), 1/H its support
+__device__ __forceinline__ void cor_coefficients(float invH, float am0, const float am1[3], const float am2[6],
+                                                 const float ag0[3], const float ag1[6], const float ag2[10],
+                                                 float& Ai, float Bi[3], float dAi[3], float dBi[3][3]) {
+    const float c = SIGMA_W * invH * invH * invH;
+    const float cg = c * invH * invH;
+    // moments in x_ij = -d convention (O7), delta terms added here
+    const float m0 = c * am0;
+    float m1[3], m2[3][3], g0[3], g1[3][3], g2[3][3][3];
+#pragma unroll
+    for (int p = 0; p < 3; ++p) {
+        m1[p] = -c * am1[p];
+        g0[p] = -cg * ag0[p];
+    }
+#pragma unroll
+    for (int p = 0; p < 3; ++p)
+#pragma unroll
+        for (int q = 0; q < 3; ++q) {
+            m2[p][q] = c * am2[sym2(p, q)];
+            g1[p][q] = cg * ag1[sym2(p, q)] + (p == q ? m0 : 0.f);
+#pragma unroll
+            for (int g = 0; g < 3; ++g)
+                g2[p][q][g] = -cg * ag2[sym3(p, q, g)] + (p == g ? m1[q] : 0.f) + (q == g ? m1[p] : 0.f);
+        }
+    // fp32 cofactor inverse of m2
+    const float c00 = m2[1][1] * m2[2][2] - m2[1][2] * m2[2][1];
+    const float c01 = m2[1][2] * m2[2][0] - m2[1][0] * m2[2][2];
+    const float c02 = m2[1][0] * m2[2][1] - m2[1][1] * m2[2][0];
+    const float det = m2[0][0] * c00 + m2[0][1] * c01 + m2[0][2] * c02;
+    const float tr = (m2[0][0] + m2[1][1] + m2[2][2]) * (1.f / 3.f);
+    if (fabsf(det) < 1e-10f * tr * tr * tr) {
+        Ai = 1.f / m0;
+#pragma unroll
+        for (int p = 0; p < 3; ++p) {
+            Bi[p] = 0.f;
+            dAi[p] = -g0[p] / (m0 * m0);
+#pragma unroll
+            for (int g = 0; g < 3; ++g) dBi[p][g] = 0.f;
+        }
+    } else {
+        const float id = 1.f / det;
+        float mi[3][3];
+        mi[0][0] = c00 * id;
+        mi[0][1] = (m2[0][2] * m2[2][1] - m2[0][1] * m2[2][2]) * id;
+        mi[0][2] = (m2[0][1] * m2[1][2] - m2[0][2] * m2[1][1]) * id;
+        mi[1][0] = c01 * id;
+        mi[1][1] = (m2[0][0] * m2[2][2] - m2[0][2] * m2[2][0]) * id;
+        mi[1][2] = (m2[0][2] * m2[1][0] - m2[0][0] * m2[1][2]) * id;
+        mi[2][0] = c02 * id;
+        mi[2][1] = (m2[0][1] * m2[2][0] - m2[0][0] * m2[2][1]) * id;
+        mi[2][2] = (m2[0][0] * m2[1][1] - m2[0][1] * m2[1][0]) * id;
+#pragma unroll
+        for (int p = 0; p < 3; ++p) Bi[p] = -(mi[p][0] * m1[0] + mi[p][1] * m1[1] + mi[p][2] * m1[2]);
+        Ai = 1.f / (m0 + Bi[0] * m1[0] + Bi[1] * m1[1] + Bi[2] * m1[2]);
+#pragma unroll
+        for (int g = 0; g < 3; ++g) {
+            float rhs[3];
+#pragma unroll
+            for (int p = 0; p < 3; ++p)
+                rhs[p] = g1[p][g] + g2[p][0][g] * Bi[0] + g2[p][1][g] * Bi[1] + g2[p][2][g] * Bi[2];
+#pragma unroll
+            for (int p = 0; p < 3; ++p) dBi[p][g] = -(mi[p][0] * rhs[0] + mi[p][1] * rhs[1] + mi[p][2] * rhs[2]);
+        }
+#pragma unroll
+        for (int g = 0; g < 3; ++g) {
+            float t = g0[g];
+#pragma unroll
+            for (int p = 0; p < 3; ++p) t += dBi[p][g] * m1[p] + Bi[p] * g1[p][g];
+            dAi[g] = -Ai * Ai * t;
+        }
+    }
+}
+
 // ============================================================== a5 Corrections (upCor)
 // Moments over gas j with s32 < H_i^2 (j incl. i), accumulated with d = x_j - x_i
 // (x_ij = -d); the symmetric gradient moments need only 6 + 10 accumulators.
@@ -220,74 +310,8 @@ struct CorPass : HydCommon {
         return tab[x][y][z];
     }
     __device__ void finish(int k, const I& s, const Acc& a) const {
-        const float c = SIGMA_W * s.invH * s.invH * s.invH;
-        const float cg = c * s.invH * s.invH;
-        // moments in x_ij = -d convention (O7), delta terms added here
-        const float m0 = c * a.m0;
-        float m1[3], m2[3][3], g0[3], g1[3][3], g2[3][3][3];
-#pragma unroll
-        for (int p = 0; p < 3; ++p) {
-            m1[p] = -c * a.m1[p];
-            g0[p] = -cg * a.g0[p];
-        }
-#pragma unroll
-        for (int p = 0; p < 3; ++p)
-#pragma unroll
-            for (int q = 0; q < 3; ++q) {
-                m2[p][q] = c * a.m2[s2(p, q)];
-                g1[p][q] = cg * a.g1[s2(p, q)] + (p == q ? m0 : 0.f);
-#pragma unroll
-                for (int g = 0; g < 3; ++g)
-                    g2[p][q][g] = -cg * a.g2[s3(p, q, g)] + (p == g ? m1[q] : 0.f) + (q == g ? m1[p] : 0.f);
-            }
-        // fp32 cofactor inverse of m2
-        const float c00 = m2[1][1] * m2[2][2] - m2[1][2] * m2[2][1];
-        const float c01 = m2[1][2] * m2[2][0] - m2[1][0] * m2[2][2];
-        const float c02 = m2[1][0] * m2[2][1] - m2[1][1] * m2[2][0];
-        const float det = m2[0][0] * c00 + m2[0][1] * c01 + m2[0][2] * c02;
-        const float tr = (m2[0][0] + m2[1][1] + m2[2][2]) * (1.f / 3.f);
         float Ai, Bi[3], dAi[3], dBi[3][3];
-        if (fabsf(det) < 1e-10f * tr * tr * tr) {
-            Ai = 1.f / m0;
-#pragma unroll
-            for (int p = 0; p < 3; ++p) {
-                Bi[p] = 0.f;
-                dAi[p] = -g0[p] / (m0 * m0);
-#pragma unroll
-                for (int g = 0; g < 3; ++g) dBi[p][g] = 0.f;
-            }
-        } else {
-            const float id = 1.f / det;
-            float mi[3][3];
-            mi[0][0] = c00 * id;
-            mi[0][1] = (m2[0][2] * m2[2][1] - m2[0][1] * m2[2][2]) * id;
-            mi[0][2] = (m2[0][1] * m2[1][2] - m2[0][2] * m2[1][1]) * id;
-            mi[1][0] = c01 * id;
-            mi[1][1] = (m2[0][0] * m2[2][2] - m2[0][2] * m2[2][0]) * id;
-            mi[1][2] = (m2[0][2] * m2[1][0] - m2[0][0] * m2[1][2]) * id;
-            mi[2][0] = c02 * id;
-            mi[2][1] = (m2[0][1] * m2[2][0] - m2[0][0] * m2[2][1]) * id;
-            mi[2][2] = (m2[0][0] * m2[1][1] - m2[0][1] * m2[1][0]) * id;
-#pragma unroll
-            for (int p = 0; p < 3; ++p) Bi[p] = -(mi[p][0] * m1[0] + mi[p][1] * m1[1] + mi[p][2] * m1[2]);
-            Ai = 1.f / (m0 + Bi[0] * m1[0] + Bi[1] * m1[1] + Bi[2] * m1[2]);
-#pragma unroll
-            for (int g = 0; g < 3; ++g) {
-                float rhs[3];
-#pragma unroll
-                for (int p = 0; p < 3; ++p)
-                    rhs[p] = g1[p][g] + g2[p][0][g] * Bi[0] + g2[p][1][g] * Bi[1] + g2[p][2][g] * Bi[2];
-#pragma unroll
-                for (int p = 0; p < 3; ++p) dBi[p][g] = -(mi[p][0] * rhs[0] + mi[p][1] * rhs[1] + mi[p][2] * rhs[2]);
-            }
-#pragma unroll
-            for (int g = 0; g < 3; ++g) {
-                float t = g0[g];
-#pragma unroll
-                for (int p = 0; p < 3; ++p) t += dBi[p][g] * m1[p] + Bi[p] * g1[p][g];
-                dAi[g] = -Ai * Ai * t;
-            }
-        }
+        cor_coefficients(s.invH, a.m0, a.m1, a.m2, a.g0, a.g1, a.g2, Ai, Bi, dAi, dBi);
         float vals[16];
         vals[0] = Ai;
 #pragma unroll
@@ -412,6 +436,169 @@ struct ExtPass : HydCommon {
         rec[7] = make_float4(g[4], g[5], g[6], g[7]);
         rec[8] = make_float4(s.invH, s.H2, vm.w, u);
         const int64_t i = gas_idx[k];
+        if (rho) rho[i] = r;
+        if (P) P[i] = Pk;
+        if (cs) cs[i] = ck;
+        if (dv)
+#pragma unroll
+            for (int t = 0; t < 9; ++t) dv[t * n + i] = g[t];
+    }
+};
+
+// ============================================================== a5 + a6 in ONE list walk
+// Corrections and Extras from one walk of each gas particle's list: Extras' sums are linear in
+// quantities known per pair, so with x = x_ij = -d, W~ = wt, G~ = gt (unscaled) and e = V_j (v_j - v_i)
+//   rho / c      = A (M0 + B.M1x),                       M0 = sum m_j W~,  M1x_c = sum m_j W~ x_c
+//   d_b v^a / c  = dA_b (S0_a + B.S1x_a) + A (sum_c dB_c,b S1x_ac + B_b S0_a)
+//                + (1/H^2) A (T0x_ab + sum_c B_c T1x_abc)
+//   S0_a = sum e_a W~, S1x_ac = sum e_a W~ x_c, T0x_ab = sum e_a G~ x_b, T1x_abc = sum e_a G~ x_b x_c
+// (c = sigma/H^3): the same sums as ExtPass's per-pair corrected-kernel gradient (O7, O8), reordered
+// — accumulated during the Corrections walk, combined with i's coefficients in the epilogue, so the
+// second walk (and its kernel evaluations) is gone.  43 accumulators on top of Corrections' 29.
+struct CorExtPass : HydCommon {
+    static constexpr int PAY = 1;
+    static constexpr bool SYM = false;
+    static constexpr int UNROLL = 1;
+    const float4* jrows;  // gposV (x, y, z, V)
+    const float4* jpay;   // gvel (vx, vy, vz, m)
+    const float* gV;
+    const float4* gvel;
+    const float* gu;
+    float4* grec;
+    int64_t ng, n;
+    float gamma;
+    float *A, *B, *dA, *dB, *rho, *P, *cs, *dv;  // caller (may be null)
+    struct I { float x, y, z, H2, invH, vx, vy, vz; };
+    struct Acc {
+        float m0, m1[3], m2[6], g0[3], g1[6], g2[10];  // Corrections (d convention)
+        float M0, M1[3], S0[3], S1[9], T0[9], T1[18];   // Extras moments (d convention)
+    };
+    __device__ void init(Acc& a) const {
+        a.m0 = a.M0 = 0.f;
+#pragma unroll
+        for (int t = 0; t < 3; ++t) a.m1[t] = a.g0[t] = a.M1[t] = a.S0[t] = 0.f;
+#pragma unroll
+        for (int t = 0; t < 6; ++t) a.m2[t] = a.g1[t] = 0.f;
+#pragma unroll
+        for (int t = 0; t < 10; ++t) a.g2[t] = 0.f;
+#pragma unroll
+        for (int t = 0; t < 9; ++t) a.S1[t] = a.T0[t] = 0.f;
+#pragma unroll
+        for (int t = 0; t < 18; ++t) a.T1[t] = 0.f;
+    }
+    __device__ void load_i(int k, I& s) const {
+        load_pos(gpos, k, s.x, s.y, s.z, s.H2, s.invH);
+        const float4 v = gvel[k];
+        s.vx = v.x; s.vy = v.y; s.vz = v.z;
+    }
+    __device__ float ix(const I& s) const { return s.x; }
+    __device__ float iy(const I& s) const { return s.y; }
+    __device__ float iz(const I& s) const { return s.z; }
+    __device__ float cut(const I& s) const { return s.H2; }
+    __device__ float jcut(const float4&) const { return 0.f; }
+    __device__ __forceinline__ void pair(const I& s, Acc& a, const float4& jp, const float4* pay, int) const {
+        const float d0 = jp.x - s.x, d1 = jp.y - s.y, d2 = jp.z - s.z;  // d = x_j - x_i, exact (O1)
+        const float r2 = s32_of(d0, d1, d2);
+        float wt, gt;
+        wendland_t(r2, s.invH, wt, gt);
+        const bool in = r2 < s.H2;
+        wt = in ? wt : 0.f;
+        gt = in ? gt : 0.f;
+        const float dd[6] = {d0 * d0, d0 * d1, d0 * d2, d1 * d1, d1 * d2, d2 * d2};
+        const float d[3] = {d0, d1, d2};
+        // Corrections' moments
+        const float w = jp.w * wt, gw = jp.w * gt;
+        a.m0 += w;
+#pragma unroll
+        for (int t = 0; t < 3; ++t) { a.m1[t] = fmaf(w, d[t], a.m1[t]); a.g0[t] = fmaf(gw, d[t], a.g0[t]); }
+#pragma unroll
+        for (int t = 0; t < 6; ++t) { a.m2[t] = fmaf(w, dd[t], a.m2[t]); a.g1[t] = fmaf(gw, dd[t], a.g1[t]); }
+        const float gd0 = gw * d0, gd1 = gw * d1, gd2 = gw * d2;
+        // symmetric third moment, index set 000,001,002,011,012,022,111,112,122,222
+        a.g2[0] = fmaf(gd0, dd[0], a.g2[0]);
+        a.g2[1] = fmaf(gd0, dd[1], a.g2[1]);
+        a.g2[2] = fmaf(gd0, dd[2], a.g2[2]);
+        a.g2[3] = fmaf(gd0, dd[3], a.g2[3]);
+        a.g2[4] = fmaf(gd0, dd[4], a.g2[4]);
+        a.g2[5] = fmaf(gd0, dd[5], a.g2[5]);
+        a.g2[6] = fmaf(gd1, dd[3], a.g2[6]);
+        a.g2[7] = fmaf(gd1, dd[4], a.g2[7]);
+        a.g2[8] = fmaf(gd1, dd[5], a.g2[8]);
+        a.g2[9] = fmaf(gd2, dd[5], a.g2[9]);
+        // Extras' moments
+        const float4 vj = pay[0];
+        const float mW = vj.w * wt;
+        a.M0 += mW;
+#pragma unroll
+        for (int t = 0; t < 3; ++t) a.M1[t] = fmaf(mW, d[t], a.M1[t]);
+        const float e[3] = {jp.w * (vj.x - s.vx), jp.w * (vj.y - s.vy), jp.w * (vj.z - s.vz)};
+#pragma unroll
+        for (int al = 0; al < 3; ++al) {
+            const float eW = e[al] * wt, eG = e[al] * gt;
+            a.S0[al] += eW;
+#pragma unroll
+            for (int t = 0; t < 3; ++t) {
+                a.S1[3 * al + t] = fmaf(eW, d[t], a.S1[3 * al + t]);
+                a.T0[3 * al + t] = fmaf(eG, d[t], a.T0[3 * al + t]);
+            }
+#pragma unroll
+            for (int t = 0; t < 6; ++t) a.T1[6 * al + t] = fmaf(eG, dd[t], a.T1[6 * al + t]);
+        }
+    }
+    template <int GG>
+    __device__ void reduce(Acc& a) const {
+        float* v = reinterpret_cast<float*>(&a);
+#pragma unroll
+        for (int t = 0; t < (int)(sizeof(Acc) / sizeof(float)); ++t) v[t] = slot_sum<GG>(v[t]);
+    }
+    __device__ void finish(int k, const I& s, const Acc& a) const {
+        float Ai, Bi[3], dAi[3], dBi[3][3];
+        cor_coefficients(s.invH, a.m0, a.m1, a.m2, a.g0, a.g1, a.g2, Ai, Bi, dAi, dBi);
+        const float c = SIGMA_W * s.invH * s.invH * s.invH;
+        const float cg = c * s.invH * s.invH;
+        // x = -d: M1x = -M1, S1x = -S1, T0x = -T0, T1x = T1
+        const float r = c * Ai * (a.M0 - (Bi[0] * a.M1[0] + Bi[1] * a.M1[1] + Bi[2] * a.M1[2]));
+        float g[9];
+#pragma unroll
+        for (int al = 0; al < 3; ++al) {
+            const float* S1 = a.S1 + 3 * al;
+            const float* T0 = a.T0 + 3 * al;
+            const float* T1 = a.T1 + 6 * al;
+            const float lin = a.S0[al] - (Bi[0] * S1[0] + Bi[1] * S1[1] + Bi[2] * S1[2]);
+#pragma unroll
+            for (int be = 0; be < 3; ++be) {
+                const float t1 = -(dBi[0][be] * S1[0] + dBi[1][be] * S1[1] + dBi[2][be] * S1[2]) + Bi[be] * a.S0[al];
+                float t3 = -T0[be];
+#pragma unroll
+                for (int cc = 0; cc < 3; ++cc) t3 += Bi[cc] * T1[sym2(be, cc)];
+                g[3 * al + be] = c * (dAi[be] * lin + Ai * t1) + cg * Ai * t3;
+            }
+        }
+        const float u = gu[k];
+        const float Pk = (gamma - 1.f) * r * u;
+        const float ck = sqrtf(gamma * Pk / r);
+        const float V = gV[k];
+        const float4 vm = gvel[k];
+        float4* rec = grec + (int64_t)k * 9;
+        rec[0] = make_float4(g[8], c * Ai, V, Pk);
+        rec[1] = make_float4(Bi[0], Bi[1], Bi[2], r);
+        rec[2] = make_float4(c * dAi[0], c * dAi[1], c * dAi[2], ck);
+        rec[3] = make_float4(dBi[0][0], dBi[0][1], dBi[0][2], dBi[1][0]);
+        rec[4] = make_float4(dBi[1][1], dBi[1][2], dBi[2][0], dBi[2][1]);
+        rec[5] = make_float4(dBi[2][2], vm.x, vm.y, vm.z);
+        rec[6] = make_float4(g[0], g[1], g[2], g[3]);
+        rec[7] = make_float4(g[4], g[5], g[6], g[7]);
+        rec[8] = make_float4(s.invH, s.H2, vm.w, u);
+        const int64_t i = gas_idx[k];
+        if (A) A[i] = Ai;
+#pragma unroll
+        for (int p = 0; p < 3; ++p) {
+            if (B) B[p * n + i] = Bi[p];
+            if (dA) dA[p * n + i] = dAi[p];
+        }
+        if (dB)
+#pragma unroll
+            for (int t = 0; t < 9; ++t) dB[t * n + i] = dBi[t / 3][t % 3];
         if (rho) rho[i] = r;
         if (P) P[i] = Pk;
         if (cs) cs[i] = ck;
@@ -1000,6 +1187,22 @@ crk_status corrections_extras(crk_ctx* c, crk_particles* p, cudaStream_t st) {
         return extras(c, p, st);
     }
     CRK_TRY(gather_gas_state(c, p, st));
+    if (c->prm.hydro_kernel != 1) {  // one list walk (CorExtPass), on-the-fly kernel for flagged rows
+        CorExtPass g;
+        common(c, g);
+        g.jrows = P<float4>(c->gposV);
+        g.jpay = P<float4>(c->gvel);
+        g.gV = P<float>(c->gV);
+        g.gvel = P<float4>(c->gvel);
+        g.gu = P<float>(c->gu);
+        g.grec = P<float4>(c->grec);
+        g.ng = c->n_gas;
+        g.n = c->n;
+        g.gamma = c->prm.gamma;
+        g.A = p->A; g.B = p->B; g.dA = p->dA; g.dB = p->dB;
+        g.rho = p->rho; g.P = p->P; g.cs = p->cs; g.dv = p->dv;
+        return launch_listed<CorExtPass, 128, 2, 128, 2>(c, g, st, "corrections + extras (one walk) kernel");
+    }
     const CorPass gc = cor_pass(c, p);
     const ExtPass ge = ext_pass(c, p);
     RowView rv = hydro_rows(c);

@@ -96,6 +96,15 @@ class Decomposition:
             out.append(m)
         return out
 
+    def domain_mask(self, r: int):
+        """Per-axis cell masks of D_r itself (the cells rank r owns)."""
+        out = []
+        for a in range(3):
+            m = np.zeros(self.ncell[a], np.uint8)
+            m[self.lo[r][a]:self.hi[r][a]] = 1
+            out.append(m)
+        return out
+
     def cells_of(self, parts: dict):
         q = max(self.params["box"]) * 2.0**-23
         cs = int(round(math.log2(self.params["cell_side"] / q)))
@@ -206,10 +215,11 @@ class DomainRank:
         self.check = False  # tests: verify the R2/R3 index-set sizes against the R1 counts (syncs)
 
     def local_hmax2(self) -> float:
-        gas = self.own_host["species"] == 1
-        if not gas.any():
+        """max fl32(H^2) over the own gas (device arrays: the own set changes with migration)."""
+        gas = self.own.species == 1
+        if not bool(gas.any()):
             return 0.0
-        return float((self.own_host["H"][gas].astype(np.float32) ** 2).max())
+        return float((self.own.H[gas] * self.own.H[gas]).max())
 
     # persistent ghost plan ------------------------------------------------
     def plan(self, h: int):
@@ -279,6 +289,14 @@ class DomainRank:
                 {s: self.rbuf[s][: self.n_recv[s]] for s in self.peers if self.n_recv[s] > 0})
 
     def r1_unpack_and_build(self):
+        self.r1_unpack()
+        self.build()
+
+    def build(self):
+        self.solver.build_lists(self.p, self.stream)
+        self._gas_idx()
+
+    def r1_unpack(self):
         cap = 0 if self.p is None else self.p.x.shape[0]
         if cap < self.n_total:
             self.p = Particles(max(int(1.1 * self.n_total), 16), self.device, self.outputs)
@@ -292,8 +310,6 @@ class DomainRank:
             if n > 0:
                 self.solver.unpack_particles(p, off, self.rbuf[s][:n], stream=self.stream)
                 off += n
-        self.solver.build_lists(p, self.stream)
-        self._gas_idx()
 
     def _gas_idx(self):
         """Gas ranks (device) of the R2/R3 send set (own gas in each peer's halo) and receive
@@ -368,6 +384,54 @@ class DomainRank:
         for k in ("vx", "vy", "vz", "u"):
             getattr(self.own, k).index_copy_(0, src, getattr(self.p, k)[: self.n_total][own])
 
+    # particle migration ---------------------------------------------------
+    def migrate_select_pack(self):
+        """After drifts: select the own particles now in another rank's domain (packed per new
+        owner) and those still in D_r; device counts (P + 1 of them: one per rank, own last)."""
+        P = self.d.P
+        if not hasattr(self, "dom_masks"):
+            self.dom_masks = [torch.from_numpy(np.concatenate(self.d.domain_mask(s))).to(self.device) for s in range(P)]
+            self.mig_cnt = torch.zeros(P, dtype=torch.int32, device=self.device)
+            self.mig_cnt_recv = torch.zeros(P, dtype=torch.int32, device=self.device)
+        n = self.n_own
+        self.mig_idx = {s: _grow(self._buf.get(("mig", s)), max(n, 1), dtype=torch.int32, device=self.device)
+                        for s in range(P)}
+        for s, t in self.mig_idx.items():
+            self._buf[("mig", s)] = t
+            self.solver.select_cells_dev(self.own, self.dom_masks[s], t, self.mig_cnt[s:s + 1], n, stream=self.stream)
+        return self.mig_cnt
+
+    def migrate_finish(self, sent: np.ndarray, recv: np.ndarray, exchange):
+        """sent[s] / recv[s]: particles leaving to / arriving from rank s (host counts; sent[r] =
+        those staying).  exchange(sends, recvs) moves the packed records; the own set is rebuilt
+        as the staying particles followed by the arrivals."""
+        P, r = self.d.P, self.r
+        sends, recvs = {}, {}
+        for s in range(P):
+            if s == r:
+                continue
+            if sent[s] > 0:
+                buf = torch.empty((int(sent[s]), 12), dtype=torch.float32, device=self.device)
+                self.solver.pack_particles_dev(self.own, self.mig_idx[s], self.mig_cnt[s:s + 1], buf, stream=self.stream)
+                sends[s] = buf
+            if recv[s] > 0:
+                recvs[s] = torch.empty((int(recv[s]), 12), dtype=torch.float32, device=self.device)
+        stay = torch.empty((max(int(sent[r]), 1), 12), dtype=torch.float32, device=self.device)
+        if sent[r] > 0:
+            self.solver.pack_particles_dev(self.own, self.mig_idx[r], self.mig_cnt[r:r + 1], stay, stream=self.stream)
+        exchange(sends, recvs)
+        n_new = int(sent[r]) + int(sum(recv[s] for s in range(P) if s != r))
+        own = Particles(n_new, self.device, outputs=False)
+        off = 0
+        for buf in [stay[: int(sent[r])]] + [recvs[s] for s in sorted(recvs)]:
+            if buf.shape[0] > 0:
+                self.solver.unpack_particles(own, off, buf, stream=self.stream)
+                off += buf.shape[0]
+        self.own, self.n_own = own, n_new
+        self.idx_r1 = {s: _grow(None, max(n_new, 1), dtype=torch.int32, device=self.device) for s in self.peers} \
+            if self.h is not None else {}
+        self.idx_tmp = torch.empty(max(n_new, 1), dtype=torch.int32, device=self.device)
+
     def own_mask(self) -> torch.Tensor:
         """Sorted positions (of the local set) holding own particles (inputs 0..n_own-1 are own)."""
         return self.p.perm[: self.n_total] < self.n_own
@@ -413,6 +477,53 @@ def substep_inprocess(ranks, dt_grav=0.0, dt_hydro=0.0):
         rk.accel(dt_hydro)
         if dt_grav != 0.0 or dt_hydro != 0.0:
             rk.writeback()
+
+
+def migrate_inprocess(ranks):
+    """Particle migration for ranks emulated in one process (after drifts)."""
+    P = len(ranks)
+    cnt = [rk.migrate_select_pack().cpu().numpy() for rk in ranks]
+    pending = {}
+
+    def exchange_for(r):
+        def ex(sends, recvs):
+            for s, t in sends.items():
+                pending[(r, s)] = t
+        return ex
+
+    for rk in ranks:  # senders first: keep each rank's packed departures
+        sent = cnt[rk.r]
+        recv = np.array([cnt[s][rk.r] if s != rk.r else 0 for s in range(P)])
+        rk._mig_plan = (sent, recv)
+    # two phases so that every rank packs before any rank rebuilds its own set
+    packs = {}
+    for rk in ranks:
+        sent, recv = rk._mig_plan
+        for s in range(P):
+            if s != rk.r and sent[s] > 0:
+                buf = torch.empty((int(sent[s]), 12), dtype=torch.float32, device=rk.device)
+                rk.solver.pack_particles_dev(rk.own, rk.mig_idx[s], rk.mig_cnt[s:s + 1], buf, stream=rk.stream)
+                packs[(rk.r, s)] = buf
+    for rk in ranks:
+        sent, recv = rk._mig_plan
+
+        def ex(sends, recvs, r=rk.r):
+            for s, t in recvs.items():
+                t.copy_(packs[(s, r)])
+        rk.migrate_finish(sent, recv, ex)
+
+
+def migrate_dist(rk: DomainRank, ex: DistExchange):
+    """Particle migration on this rank (after drifts): per-destination counts in one small
+    exchange and one readback, then the records."""
+    P = rk.d.P
+    cnt = rk.migrate_select_pack()
+    peers = [s for s in range(P) if s != rk.r]
+    ex.exchange({s: cnt[s:s + 1] for s in peers}, {s: rk.mig_cnt_recv[s:s + 1] for s in peers})
+    host = torch.stack([cnt, rk.mig_cnt_recv]).cpu().numpy()
+    recv = host[1].copy()
+    recv[rk.r] = 0
+    rk.migrate_finish(host[0], recv, ex.exchange)
 
 
 def substep_dist(rk: DomainRank, ex: DistExchange, dt_grav=0.0, dt_hydro=0.0, hmax2=None):

@@ -277,3 +277,62 @@ def test_config5_eight_ranks_weak_scaled_sampled():
             assert err <= 1e-4
             assert abs(g[5] - ref["dudt"][i]) <= 1e-4 * ref["Sdu"][i]
             assert g[6] == rc["gather"][ic[int(g[1])]] and g[7] == rc["sym"][ic[int(g[1])]]
+
+
+@pytest.mark.gpu
+def test_migration_after_drift_then_decomposed_substep():
+    """Particle migration: the ranks own the split of c2z at P = 4; every
+    particle then drifts (the fp32 drift of oracle.drift / crk_drift, dt = 4: ~0.4 cell widths
+    rms) and migrate hands the ones that left their domain to the new owners.  Afterwards
+    every particle is owned exactly once, by the owner of its new cell, and a decomposed
+    substep gives the single-domain oracle's counts (exact) and forces on the drifted set."""
+    import torch
+    import oracle
+    from paper_2310_16122_b200.domain import DomainRank, migrate_inprocess, substep_inprocess
+
+    parts, params = cached_config("c2z")
+    n = parts["x"].shape[0]
+    P = 4
+    d = _decomp(params, P)
+    ranks = [DomainRank(d, r, d.split(parts, r), "cuda:0") for r in range(P)]
+    pos = np.stack([parts[k] for k in "xyz"], 1)
+    vel = np.stack([parts[k] for k in ("vx", "vy", "vz")], 1)
+    xd = oracle.drift(pos, vel, params["box"], 4.0)
+    moved = parts.copy()
+    moved["x"], moved["y"], moved["z"] = (np.ascontiguousarray(xd[:, a]) for a in range(3))
+    pos_of_id = np.empty(n, np.int64)
+    pos_of_id[parts["id"]] = np.arange(n)
+    for rk in ranks:  # the drift, applied to each rank's own particles
+        ids = rk.own.id.cpu().numpy()
+        for a, k in enumerate("xyz"):
+            getattr(rk.own, k).copy_(torch.from_numpy(np.ascontiguousarray(xd[pos_of_id[ids], a])))
+    cx, cy, cz = d.cells_of(moved)
+    owner = d.owner_of_cells(cx, cy, cz)
+    before = np.empty(n, np.int64)
+    for rk in ranks:
+        before[pos_of_id[rk.own.id.cpu().numpy()]] = rk.r
+    assert np.count_nonzero(before != owner) > 100  # the drift moved particles across domains
+    migrate_inprocess(ranks)
+    seen = np.zeros(n, np.int64)
+    for rk in ranks:
+        idx = pos_of_id[rk.own.id.cpu().numpy()]
+        seen[idx] += 1
+        assert np.all(owner[idx] == rk.r)
+    assert np.all(seen == 1)
+    for rk in ranks:
+        rk.check = True
+    substep_inprocess(ranks)
+    torch.cuda.synchronize()
+    a = np.full((n, 3), np.nan)
+    cnt = np.full(n, -1, np.int64)
+    for rk in ranks:
+        own = rk.own_mask().cpu().numpy()
+        h = rk.p.to_host(["id", "ax", "ay", "az"])
+        cg = rk.solver.count_pairs(rk.p)[0].cpu().numpy()
+        idx = pos_of_id[h["id"][own]]
+        a[idx] = np.stack([h["ax"], h["ay"], h["az"]], 1)[own]
+        cnt[idx] = cg[own]
+        rk.close()
+    assert np.array_equal(cnt, oracle.counts(moved, params)["grav"])
+    ref = oracle.gravity(moved, params)
+    assert norm_err(a, ref["a"], ref["S"]) <= 1e-4

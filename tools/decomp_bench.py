@@ -40,6 +40,7 @@ for rk in ranks:
     rk.plan(h)
 T = lambda: torch.cuda.Event(enable_timing=True)  # noqa: E731
 res = {r: [] for r in range(a.P)}
+phases = {r: [] for r in range(a.P)}
 ex = EmuExchange(ranks)
 
 
@@ -64,7 +65,11 @@ for rep in range(a.reps + 1):
     msgs = [rk.r1_messages() for rk in ranks]
     ex.exchange_all([m[0] for m in msgs], [m[1] for m in msgs])
     for rk in ranks:
-        phase(t, rk, lambda: (rk.r1_unpack_and_build(), rk.gravity_geometry(0.0)))
+        phase(t, rk, rk.r1_unpack)
+        phase(t, rk, lambda: rk.solver.build_lists(rk.p, rk.stream))
+        phase(t, rk, rk._gas_idx)
+        phase(t, rk, lambda: rk.solver.gravity_kick(rk.p, 0.0, rk.stream))
+        phase(t, rk, lambda: rk.solver.geometry(rk.p, rk.stream))
         free = torch.cuda.mem_get_info()[0] / 2**30
         if free < a.min_free_gb:
             raise SystemExit(f"device memory nearly exhausted after rank {rk.r} ({free:.1f} GB free): use a smaller config")
@@ -80,9 +85,13 @@ for rep in range(a.reps + 1):
     if rep > 0:
         for r in range(a.P):
             res[r].append(sum(x.elapsed_time(y) for x, y in t[r]))
+            phases[r].append([x.elapsed_time(y) for x, y in t[r]])
 msg_bytes = [int(sum(rk.n_send.values()) * 48 + sum(rk.g_send.values()) * (16 + 144)) for rk in ranks]
 print(json.dumps({"P": a.P, "config": a.config, "halo_cells": h,
                   "ghosts_per_rank": [int(rk.n_total - rk.n_own) for rk in ranks],
                   "bytes_sent_per_rank": msg_bytes,
                   "rank_ms": [round(sum(v) / len(v), 2) for v in res.values()],
-                  "max_rank_ms": round(max(sum(v) / len(v) for v in res.values()), 2)}))
+                  "max_rank_ms": round(max(sum(v) / len(v) for v in res.values()), 2),
+                  "phase_names": ["r1 select+pack", "r1 unpack", "build", "gas idx", "gravity", "geometry", "r2 pack",
+                                  "r2 unpack+cor/ext", "r3 pack", "r3 unpack+accel"],
+                  "rank_phase_ms": [[round(float(x), 2) for x in np.median(np.asarray(v), 0)] for v in phases.values()]}))

@@ -19,13 +19,18 @@ METRICS = ",".join([
     "smsp__sass_thread_inst_executed_op_fmul_pred_on.sum", "smsp__sass_thread_inst_executed_op_fmul2_pred_on.sum",
     "sm__pipe_fma_cycles_active.avg.pct_of_peak_sustained_active", "smsp__issue_active.avg.pct_of_peak_sustained_active",
 ])
-PASS_OF = {"grav_pipe_kernel": "gravity", "GeoPass": "geometry", "list_kernel2": "corrections_extras",
+PASS_OF = {"grav_pipe_kernel": "gravity", "GeoPass": "geometry", "list_kernel2": "corrections_extras", "CorExtPass": "corrections_extras",
            "AccPass": "accel_dudt"}
 N_SM, LANES, F_MAX = 148, 128, 1965e6
 
 
 def _num(v):
     return float(v.replace(",", "")) if v not in ("", "n/a") else 0.0
+
+
+_SCALE = {"ns": 1e-9, "nsecond": 1e-9, "us": 1e-6, "usecond": 1e-6, "ms": 1e-3, "msecond": 1e-3, "s": 1.0,
+          "second": 1.0, "hz": 1.0, "khz": 1e3, "mhz": 1e6, "ghz": 1e9, "byte": 1.0, "kbyte": 1e3, "mbyte": 1e6,
+          "gbyte": 1e9, "tbyte": 1e12}
 
 
 def main(rep, out):
@@ -39,14 +44,11 @@ def main(rep, out):
         pas = next((p for k, p in PASS_OF.items() if k in name), None)
         if pas is None:
             continue
-        t = _num(d[col["gpu__time_duration.sum"]]) * {"nsecond": 1e-9, "usecond": 1e-6, "msecond": 1e-3,
-                                                       "second": 1.0}[units[col["gpu__time_duration.sum"]]]
+        t = _num(d[col["gpu__time_duration.sum"]]) * _SCALE[units[col["gpu__time_duration.sum"]].lower()]
         g = lambda m: _num(d[col["smsp__sass_thread_inst_executed_op_" + m + "_pred_on.sum"]])  # noqa: E731
         flops = 2 * g("ffma") + 4 * g("ffma2") + g("fadd") + 2 * g("fadd2") + g("fmul") + 2 * g("fmul2")
-        f = _num(d[col["sm__cycles_elapsed.avg.per_second"]])
-        f = f * {"hz": 1, "khz": 1e3, "mhz": 1e6, "ghz": 1e9}.get(units[col["sm__cycles_elapsed.avg.per_second"]].lower(), 1)
-        dram = _num(d[col["dram__bytes_read.sum"]]) + _num(d[col["dram__bytes_write.sum"]])
-        dram *= {"byte": 1, "kbyte": 1e3, "mbyte": 1e6, "gbyte": 1e9}.get(units[col["dram__bytes_read.sum"]].lower(), 1)
+        f = _num(d[col["sm__cycles_elapsed.avg.per_second"]]) * _SCALE[units[col["sm__cycles_elapsed.avg.per_second"]].lower()]
+        dram = sum(_num(d[col[m]]) * _SCALE[units[col[m]].lower()] for m in ("dram__bytes_read.sum", "dram__bytes_write.sum"))
         if pas in res and res[pas]["ms"] >= t * 1e3:
             continue  # keep the dominant launch of the pass
         res[pas] = {"kernel": name[:120], "ms": t * 1e3, "executed_fp32_flop": flops,
