@@ -81,11 +81,12 @@ typedef struct crk_params {
                             pipeline, 7 = CTA-staged,
                             8 = the paper's half-warp XOR-shuffle algorithm.
                             Other values: CRK_EINVAL. */
-    int32_t hydro_kernel;/* hydro kernel variant: 0 = default (corrections + extras in one list walk,
-                            accel/du-dt i-centric list walk); 1 = corrections then extras as two walks
-                            of one kernel (round 1's); accel/du-dt variants 4 = 8 lanes per i in
-                            16-warp CTAs, 5 = Newton-3 over the lists (whole-box domains), 6 = as 4
-                            with 128-entry staging rounds.  Other: CRK_EINVAL. */
+    int32_t hydro_kernel;/* hydro kernel variant: 0 = default (corrections then extras as two walks of
+                            one kernel, accel/du-dt i-centric list walk); 2 = corrections + extras in
+                            ONE walk (Extras' sums as moments, 128 registers: slower on c4, 11.4 vs
+                            10.5 ms); accel/du-dt variants 4 = 8 lanes per i in 16-warp CTAs,
+                            5 = Newton-3 over the lists (whole-box domains), 6 = as 4 with 128-entry
+                            staging rounds.  Other: CRK_EINVAL. */
     int32_t nbr_cap;     /* gas neighbour-list capacity per particle (entries; lists built by
                             crk_geometry, walked by corrections, extras and accel): 0 = default
                             (128), < 0 = no lists (every gas pass culls on the fly), else the
@@ -164,11 +165,11 @@ crk_status crk_corrections(struct crk_ctx* ctx, crk_particles* parts, void* stre
 crk_status crk_extras(struct crk_ctx* ctx, crk_particles* parts, void* stream);
 
 /* a5 + a6 in one call, with the results of crk_corrections followed by crk_extras: each
- * gas particle's neighbour list is walked ONCE, accumulating Corrections' moments and the
- * moments Extras' sums reduce to (linear in the per-pair quantities; combined with the new
- * coefficients in the epilogue — PAPER.md:377 upCor -> upBarEx; hydro_kernel 1: two walks).
- * Call after crk_geometry; leaves the context ready for crk_hydro_accel_dudt.  Reads v and u
- * (as crk_extras does). */
+ * gas particle's neighbour list is walked twice by one kernel (Corrections, then Extras
+ * with the coefficients just computed, PAPER.md:377 upCor -> upBarEx), sharing the staged
+ * neighbour rows (hydro_kernel 2: once, Extras' sums accumulated as moments and combined with
+ * the new coefficients in the epilogue).  Call after crk_geometry; leaves the context ready
+ * for crk_hydro_accel_dudt.  Reads v and u (as crk_extras does). */
 crk_status crk_corrections_extras(struct crk_ctx* ctx, crk_particles* parts, void* stream);
 
 /* a7 + a8 Acceleration and Energy (upBarAc, upBarDu): antisymmetrised CRK-SPH momentum

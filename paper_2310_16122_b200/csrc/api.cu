@@ -147,8 +147,8 @@ static crk_status validate(const crk_params* p, Layout& L, std::string& why) {
     if (!((p->grav_kernel >= 0 && p->grav_kernel <= 2) || (p->grav_kernel >= 6 && p->grav_kernel <= 8))) {
         why = "grav_kernel must be 0-2 or 6-8"; return CRK_EINVAL;
     }
-    if (!(p->hydro_kernel == 0 || p->hydro_kernel == 1 || (p->hydro_kernel >= 4 && p->hydro_kernel <= 6))) {
-        why = "hydro_kernel must be 0, 1, 4, 5 or 6"; return CRK_EINVAL;
+    if (!(p->hydro_kernel == 0 || p->hydro_kernel == 2 || (p->hydro_kernel >= 4 && p->hydro_kernel <= 6))) {
+        why = "hydro_kernel must be 0, 2, 4, 5 or 6"; return CRK_EINVAL;
     }
     if (p->nbr_cap > 65535) { why = "nbr_cap must be <= 65535"; return CRK_EINVAL; }
     return CRK_OK;

@@ -318,12 +318,12 @@ class DomainRank:
         self.gsend, self.grecv = {}, {}
         cnt = torch.zeros(2, dtype=torch.int32, device=self.device)
         for s in self.peers:
-            for dst, m, n, c in ((self.gsend, self.mask_send[s], self.g_send[s], cnt[0:1]),
-                                 (self.grecv, self.mask_recv[s], self.g_recv[s], cnt[1:2])):
+            for side, dst, m, n, c in (("send", self.gsend, self.mask_send[s], self.g_send[s], cnt[0:1]),
+                                       ("recv", self.grecv, self.mask_recv[s], self.g_recv[s], cnt[1:2])):
                 if m is None or n == 0:
                     dst[s] = None
                     continue
-                key = ("gidx", id(dst), s)
+                key = ("gidx", side, s)  # persistent per (side, peer): no allocation per substep
                 buf = _grow(self._buf.get(key), self.n_total, dtype=torch.int32, device=self.device)
                 self._buf[key] = buf
                 self.solver.select_gas_dev(m, buf, c, stream=self.stream)

@@ -204,14 +204,16 @@ def test_decomposed_kicks_written_back_over_two_substeps():
 
 @pytest.mark.gpu
 @pytest.mark.slow
-def test_config5_eight_ranks_weak_scaled_sampled():
-    """Config 5 (§3.4: 2x512^3 particles over 8 ranks, 2x256^3 per rank),
-    the 8 ranks emulated on one B200 with 2x128^3 per rank (eight 2x256^3 ranks need ~26 GB
-    each: more than one GPU holds): each rank owns a periodic replica of the tile (bench.py's
-    weak-scaling tiling), so every particle's neighbourhood in the 2x256^3 system is that of
-    its original in the tile — sampled own particles of every rank must carry the single-tile
-    oracle's counts (exact) and forces (1e-4), through the decomposed path (ghost exchange
-    R1/R2/R3, partial-domain lists, the Newton-3 gravity kernel's ghost rule)."""
+@pytest.mark.parametrize("tile,P", [("lat:128,128,128:0.1:16522", 8), ("c4", 2), ("c4", 4)])
+def test_weak_scaled_ranks_sampled(tile, P):
+    """Configs 4/5 weak-scaled (§3.4: 2x512^3 particles over 8 ranks,
+    2x256^3 per rank), the ranks emulated on one B200: P = 2 and 4 with the full 2x256^3 per
+    rank, P = 8 with 2x128^3 per rank (eight 2x256^3 ranks need ~26 GB each: more than one
+    GPU holds).  Each rank owns a periodic replica of the tile (bench.py's weak-scaling tiling),
+    so every particle's neighbourhood in the tiled system is that of its original in the tile —
+    sampled own particles of every rank must carry the single-tile oracle's counts (exact) and
+    forces (1e-4), through the decomposed path (ghost exchange R1/R2/R3, partial-domain lists,
+    the Newton-3 gravity kernel's ghost rule)."""
     import torch
     import oracle
     from bench import tile_config
@@ -219,14 +221,15 @@ def test_config5_eight_ranks_weak_scaled_sampled():
 
     from gen.configs import quantise
 
-    parts, params = cached_config("lat:128,128,128:0.1:16522")
+    from paper_2310_16122_b200.domain import grid_dims
+
+    parts, params = cached_config(tile)
     n = parts["x"].shape[0]
-    P = 8
-    # positions on the 2x2x2-tiled box's quantum (2x the tile's): the tiling is then an exact
-    # periodic replica, bit for bit (bench.py's tiling re-quantises; that moves pairs at the
-    # predicate boundary in or out)
+    # positions on the tiled box's quantum (2x the tile's): the tiling is then an exact periodic
+    # replica, bit for bit (as bench.py's weak-scaling tiling does)
+    dims = grid_dims(P)
     pos = np.stack([parts[k].astype(np.float64) for k in "xyz"], 1)
-    pos = quantise(quantise(pos, [2 * b for b in params["box"]]).astype(np.float64), params["box"])
+    pos = quantise(quantise(pos, [d * b for d, b in zip(dims, params["box"])]).astype(np.float64), params["box"])
     for a, k in enumerate("xyz"):
         parts[k] = np.ascontiguousarray(pos[:, a])
     ranks = []

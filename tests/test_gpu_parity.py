@@ -398,3 +398,30 @@ def test_accel_symmetric_list_variant(cap, var):
     ah = np.stack([gi["ahx"], gi["ahy"], gi["ahz"]], 1)[T]
     assert norm_err(ah, ref["a"], ref["Sa"]) <= TOL_FORCE
     assert norm_err(gi["dudt"][T], ref["dudt"], ref["Sdu"]) <= TOL_FORCE
+
+
+@pytest.mark.parametrize("name,cap", [("c1", 128), ("c2z", 128), ("c2z", 70)])
+def test_corrections_extras_one_walk_variant(name, cap):
+    """hydro_kernel 2: corrections and extras from ONE walk of each list, Extras' sums carried as
+    moments and combined with the new coefficients in the epilogue (the same sums reordered) —
+    every intermediate and the accel/du-dt results within the bars, with complete lists and
+    with flagged rows (capacity 70: the on-the-fly fallback)."""
+    parts, params = cached_config(name)
+    params["hydro_kernel"] = 2
+    params["nbr_cap"] = cap
+    g = run_gpu(parts, params, counts=False)
+    ref = oracle.substep(parts, params)
+    gi = g["in"]
+    T = ref["targets"]
+    H = parts["H"][T].astype(np.float64)[:, None]
+    assert rel_err(gi["A"][T], ref["A"]) <= 1e-5
+    assert dimless_err(gi["B"][:, T].T, ref["B"], H) <= 2e-5
+    assert dimless_err(gi["dA"][:, T].T, ref["dA"], H / ref["A"][:, None]) <= 2e-5
+    assert dimless_err(gi["dB"][:, T].T, ref["dB"], H * H) <= 1e-4
+    assert rel_err(gi["rho"][T], ref["rho"]) <= 1e-5
+    assert rel_err(gi["cs"][T], ref["cs"]) <= 1e-5
+    vrms = np.sqrt(np.mean(parts["vx"] ** 2 + parts["vy"] ** 2 + parts["vz"] ** 2))
+    assert dimless_err(gi["dv"][:, T].T, ref["dv"], H / vrms) <= 2e-5
+    ah = np.stack([gi["ahx"], gi["ahy"], gi["ahz"]], 1)[T]
+    assert norm_err(ah, ref["a"], ref["Sa"]) <= TOL_FORCE
+    assert norm_err(gi["dudt"][T], ref["dudt"], ref["Sdu"]) <= TOL_FORCE

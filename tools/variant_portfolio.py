@@ -18,6 +18,8 @@ PORTFOLIOS = {
     "lists, warp gravity without pipeline": {"grav_kernel": 6},
     "lists, half-warp shuffle gravity (the paper's algorithm)": {"grav_kernel": 8},
     "lists, Newton-3 accel": {"hydro_kernel": 5},
+    "lists, corrections + extras in one walk (moment form)": {"hydro_kernel": 2},
+    "lists, gravity with 4 CTAs/SM and 32 staged leaves": {"grav_kernel": 1},
     "lists, accel with 8 lanes per i (one 16-warp CTA per SM)": {"hydro_kernel": 4},
     "lists, accel with 8 lanes per i, 128-entry staging rounds": {"hydro_kernel": 6},
     "on-the-fly culling everywhere (no neighbour lists)": {"nbr_cap": -1, "grav_kernel": 7},
