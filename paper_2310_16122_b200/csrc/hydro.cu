@@ -1207,7 +1207,7 @@ crk_status corrections_extras(crk_ctx* c, crk_particles* p, cudaStream_t st) {
     const ExtPass ge = ext_pass(c, p);
     RowView rv = hydro_rows(c);
     const ListView lv = list_view(c);
-    CRK_TRY(cuda_check(c, (launch_list2<CorPass, ExtPass, HYD_NW, HYD_G, 128, 3>(gc, ge, rv, lv, st)),
+    CRK_TRY(cuda_check(c, (launch_list2<CorPass, ExtPass, HYD_NW, HYD_G, 128, 4>(gc, ge, rv, lv, st)),
                        "corrections + extras kernel"));
     c->launches++;
     rv.rows = lv.frows;
