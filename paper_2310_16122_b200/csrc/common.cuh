@@ -204,6 +204,19 @@ __device__ __forceinline__ void cp_async_wait() { asm volatile("cp.async.wait_gr
 __device__ __forceinline__ void fence_proxy_async_smem() {
     asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
 }
+// shared-memory stores through 32-bit shared addresses (a base kept in a register instead of
+// the generic->shared window conversion the compiler rematerialises under register pressure)
+__device__ __forceinline__ uint32_t opaque_u32(uint32_t v) {
+    asm("mov.b32 %0, %1;" : "=r"(v) : "r"(v));
+    return v;
+}
+__device__ __forceinline__ void sts128(uint32_t a, const float4& v) {
+    asm volatile("st.shared.v4.f32 [%0], {%1, %2, %3, %4};" ::"r"(a), "f"(v.x), "f"(v.y), "f"(v.z), "f"(v.w)
+                 : "memory");
+}
+__device__ __forceinline__ void sts32(uint32_t a, int v) {
+    asm volatile("st.shared.b32 [%0], %1;" ::"r"(a), "r"(v) : "memory");
+}
 // fire-and-forget vector atomic add (REDG.E.ADD.F32x4)
 __device__ __forceinline__ void red_add_v4(float4* p, float a, float b, float c, float d) {
     asm volatile("red.global.add.v4.f32 [%0], {%1, %2, %3, %4};" ::"l"(p), "f"(a), "f"(b), "f"(c), "f"(d)

@@ -12,10 +12,11 @@ ap = argparse.ArgumentParser()
 ap.add_argument("--config", default="c4")
 ap.add_argument("--warmup", type=int, default=2)
 ap.add_argument("--steps", type=int, default=1)
+ap.add_argument("--set", nargs="*", default=[], help="crk_params overrides k=v")
 a = ap.parse_args()
 parts, params = make_config(a.config)
 p = Particles.from_host(parts, "cuda", outputs="forces")  # as bench.py
-s = Solver(params, 0)
+s = Solver(dict(params, **{kv.split("=")[0]: int(kv.split("=")[1]) for kv in a.set}), 0)
 for _ in range(a.warmup):
     s.substep(p)
 torch.cuda.synchronize()
