@@ -144,8 +144,8 @@ static crk_status validate(const crk_params* p, Layout& L, std::string& why) {
     }
     if (!(p->skin >= 0.f) || p->skin >= p->cell_side) { why = "skin must be in [0, cell_side)"; return CRK_EINVAL; }
     if (p->skin > 0.f && L.partial) { why = "a skin needs a whole-box domain"; return CRK_EINVAL; }
-    if (!((p->grav_kernel >= 0 && p->grav_kernel <= 4) || (p->grav_kernel >= 6 && p->grav_kernel <= 8))) {
-        why = "grav_kernel must be 0-4 or 6-8"; return CRK_EINVAL;
+    if (!((p->grav_kernel >= 0 && p->grav_kernel <= 2) || (p->grav_kernel >= 6 && p->grav_kernel <= 8))) {
+        why = "grav_kernel must be 0-2 or 6-8"; return CRK_EINVAL;
     }
     if (!(p->hydro_kernel == 0 || p->hydro_kernel == 2 || (p->hydro_kernel >= 4 && p->hydro_kernel <= 6))) {
         why = "hydro_kernel must be 0, 2, 4, 5 or 6"; return CRK_EINVAL;
@@ -201,7 +201,7 @@ crk_status crk_destroy(crk_ctx* c) {
     Buf* bufs[] = {&c->keys_a, &c->keys_b, &c->idx_a, &c->idx_b, &c->cub_tmp, &c->scratch, &c->xm,
                    &c->cell_start, &c->cell_end, &c->leaf_cnt, &c->gflag, &c->grank, &c->gas_idx,
                    &c->dev_scalars, &c->gpos, &c->gvel, &c->gV, &c->gcoef, &c->grec, &c->gu,
-                   &c->gacc, &c->gposV, &c->sel_flag, &c->sel_mask, &c->work, &c->nbr, &c->ncnt, &c->lflag, &c->gebox, &c->disp};
+                   &c->gacc, &c->gposV, &c->sel_flag, &c->sel_mask, &c->work, &c->nbr, &c->ncnt, &c->lflag, &c->gmask, &c->disp};
     for (Buf* b : bufs)
         if (b->p) cudaFree(b->p);
     for (int s = 0; s < 4; ++s) {

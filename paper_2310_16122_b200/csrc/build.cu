@@ -264,9 +264,47 @@ struct ListArgs {
     const int32_t* jcount;
     int2* erec;
     const float4* box8B;    // padded j-leaf boxes (lo, max H^2), (hi, 0)
-    float4* ebox;           // gravity only (else null): per entry (lo + shift, first), (hi + shift, count | code << 8)
     double skin;            // list skin: cutoffs sqrt(cut2) + skin (0: the exact O4 lists)
 };
+
+// ---------------------------------------------------------------- gravity entry masks
+// Bit g of a gravity entry's mask is set iff the entry's j-leaf can hold a pair for i-group g of
+// the row's leaf (i-particles [first + 16g, first + 16g + 16)): the leaf reaches past the
+// group's first particle (Newton-3: pairs with j below the group belong to an earlier group) or
+// is a ghost (no group of its own on this rank), and the fp32 box-box distance of the group's
+// bounding box to the shifted j-leaf box is below rcut2 * CULL_SLACK (a superset of O2).  This
+// is grav_pipe_kernel's entry cull, computed once per entry by the list build (and again by
+// crk_refresh) instead of by every group's warp over the whole row.
+// group bounding boxes of leaf (f0, cnt <= 128) into gb[8][6] (lo xyz, hi xyz); one warp
+__device__ __forceinline__ void group_boxes(const float4* __restrict__ xm, int f0, int cnt, float (*gb)[6], int lane) {
+#pragma unroll
+    for (int t = 0; t < 4; ++t) {
+        const int k = lane + 32 * t;  // group 2t + lane / 16
+        float lo[3] = {INFINITY, INFINITY, INFINITY}, hi[3] = {-INFINITY, -INFINITY, -INFINITY};
+        if (k < cnt) {
+            const float4 p = xm[f0 + k];
+            lo[0] = hi[0] = p.x; lo[1] = hi[1] = p.y; lo[2] = hi[2] = p.z;
+        }
+#pragma unroll
+        for (int o = 1; o < 16; o <<= 1)
+#pragma unroll
+            for (int d = 0; d < 3; ++d) {
+                lo[d] = fminf(lo[d], __shfl_xor_sync(0xffffffffu, lo[d], o));
+                hi[d] = fmaxf(hi[d], __shfl_xor_sync(0xffffffffu, hi[d], o));
+            }
+        if ((lane & 15) == 0)
+#pragma unroll
+            for (int d = 0; d < 3; ++d) { gb[2 * t + lane / 16][d] = lo[d]; gb[2 * t + lane / 16][3 + d] = hi[d]; }
+    }
+    __syncwarp();
+}
+// a j-leaf lies in one cell: its (unshifted) box centre decides whether it is a ghost
+__device__ __forceinline__ bool leaf_ghost(const float4& bl, const float4& bh, float inv_q, int cs, const int* dlo,
+                                           const int* dhi) {
+    const int cx = (int)(0.5f * (bl.x + bh.x) * inv_q) >> cs, cy = (int)(0.5f * (bl.y + bh.y) * inv_q) >> cs,
+              cz = (int)(0.5f * (bl.z + bh.z) * inv_q) >> cs;
+    return !(cx >= dlo[0] && cx < dhi[0] && cy >= dlo[1] && cy < dhi[1] && cz >= dlo[2] && cz < dhi[2]);
+}
 
 // cut^2 of the O4 test with the skin: (sqrt(cut2) + skin)^2 (the plain cut2 without one)
 __device__ __forceinline__ double skin_cut2(double cut2, double skin) {
@@ -278,13 +316,6 @@ __device__ __forceinline__ double skin_cut2(double cut2, double skin) {
 __device__ __forceinline__ void put_entry(const ListArgs& A, int p, int b, int code) {
     // (the CSR col / shift views of crk_list_view are decoded from erec on demand)
     A.erec[p] = make_int2(A.jfirst[b] | ((A.jcount[b] - 1) << 29), b | (code << 26));
-    if (A.ebox) {  // the j-leaf box with the periodic shift applied (exact, O1), next to first / count
-        const float ox = (float)(code % 3 - 1) * A.Lf[0], oy = (float)((code / 3) % 3 - 1) * A.Lf[1],
-                    oz = (float)(code / 9 - 1) * A.Lf[2];
-        const float4 bl = A.box8B[2 * (int64_t)b], bh = A.box8B[2 * (int64_t)b + 1];
-        A.ebox[2 * (int64_t)p] = make_float4(bl.x + ox, bl.y + oy, bl.z + oz, __int_as_float(A.jfirst[b]));
-        A.ebox[2 * (int64_t)p + 1] = make_float4(bh.x + ox, bh.y + oy, bh.z + oz, __int_as_float(A.jcount[b] | (code << 8)));
-    }
 }
 
 constexpr int LIST_WARPS = 8;
@@ -306,6 +337,7 @@ __global__ void __launch_bounds__(LIST_WARPS * 32, 5) k_lists(ListArgs A) {
     const int lane = threadIdx.x & 31;
     const int w = threadIdx.x >> 5;
     if (a >= A.nA) return;
+
     const float* ba = A.bboxA + 6 * a;
     const double slack = 1.0 + 0x1p-20;
     double reach2;
@@ -442,6 +474,10 @@ __global__ void __launch_bounds__(LIST_WARPS * 32, 5) k_lists(ListArgs A) {
 // ---------------------------------------------------------------- driver
 static inline unsigned nblk(int64_t n, int b) { return (unsigned)((n + b - 1) / b); }
 
+static bool want_masks(const crk_ctx* c) {  // only the pipelined Newton-3 kernel (grav_kernel 0-2) reads them
+    return (c->prm.symmetric & 1) && c->prm.grav_kernel <= 2;
+}
+
 static ListArgs list_args(crk_ctx* c, int m) {
     const Layout& L = c->lay;
     const int sa = m == 0 ? 0 : 2, sb = m == 0 ? 1 : 3;
@@ -470,7 +506,6 @@ static ListArgs list_args(crk_ctx* c, int m) {
     A.jcount = P<int32_t>(c->lcount[sb]);
     A.erec = P<int2>(c->erec[m]);
     A.box8B = P<float4>(c->lbox8[sb]);
-    A.ebox = m == 0 ? P<float4>(c->gebox) : nullptr;
     A.skin = c->prm.skin;
     return A;
 }
@@ -523,22 +558,91 @@ __global__ void k_repack_gas(int64_t ng, const int32_t* __restrict__ gas_idx, co
     gpos[g] = make_float4(p.x, p.y, p.z, H[i]);
 }
 
-// gravity list entry records from the (refreshed) j-leaf boxes, as the list fill writes them
-// (one warp per row: rows are written at their bound, so the gaps between them hold no entries)
-__global__ void k_entry_boxes(int64_t na, const int32_t* __restrict__ rowoff, const int32_t* __restrict__ rowend,
-                              const int2* __restrict__ erec, const float4* __restrict__ box8, float Lx, float Ly,
-                              float Lz, float4* ebox) {
+// gravity entry masks of the list's rows (after the fill and after crk_refresh); one warp per row.
+// Latency-bound (row start -> records -> boxes): few registers for many resident warps (the
+// next entry's record and box requested while the current one is tested); the 8 group boxes in shared memory as packed pairs (groups 2t, 2t + 1),
+// two groups per packed-FP32 test.
+__global__ void __launch_bounds__(256, 5) k_entry_masks(int64_t na, const int32_t* __restrict__ rowoff,
+                                                        const int32_t* __restrict__ rowend, const int2* __restrict__ erec,
+                                                        const float4* __restrict__ box8, const int32_t* __restrict__ ifirst,
+                                                        const int32_t* __restrict__ icount, const float4* __restrict__ xm,
+                                                        float Lx, float Ly, float Lz, float wcut, bool partial, float inv_q,
+                                                        int cs, int3 dlo3, int3 dhi3, uint8_t* __restrict__ gmask) {
+    __shared__ float s_gb[8][8][6];
+    __shared__ float4 s_b[8][4][3];  // [warp][t][axis]: (lo, lo, -hi, -hi) of groups (2t, 2t + 1)
+    __shared__ float4 s_off[27];     // periodic offset of each shift code
     const int64_t a = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5;
-    if (a >= na) return;
-    for (int p = rowoff[a] + (threadIdx.x & 31); p < rowend[a]; p += 32) {
-    const int2 r = erec[p];
-    const int first = r.x & 0x1fffffff, count = ((unsigned)r.x >> 29) + 1;
-    const int b = r.y & 0x03ffffff, code = (unsigned)r.y >> 26;
-    const float ox = (float)(code % 3 - 1) * Lx, oy = (float)((code / 3) % 3 - 1) * Ly, oz = (float)(code / 9 - 1) * Lz;
-    const float4 bl = box8[2 * (int64_t)b], bh = box8[2 * (int64_t)b + 1];
-    ebox[2 * p] = make_float4(bl.x + ox, bl.y + oy, bl.z + oz, __int_as_float(first));
-    ebox[2 * p + 1] = make_float4(bh.x + ox, bh.y + oy, bh.z + oz, __int_as_float(count | (code << 8)));
+    const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+    if (threadIdx.x < 27) {
+        const int code = threadIdx.x;
+        s_off[code] = make_float4((float)(code % 3 - 1) * Lx, (float)((code / 3) % 3 - 1) * Ly, (float)(code / 9 - 1) * Lz, 0.f);
     }
+    __syncthreads();
+    if (a >= na) return;
+    const int f0 = ifirst[a], cnt = icount[a];
+    const int p0 = rowoff[a], pend = rowend[a];
+    // the first entry's record and box are requested before the group boxes are reduced
+    int2 r;
+    float4 bl, bh;
+    auto load1 = [&](int q) {
+        r = q < pend ? erec[q] : make_int2(0, 0);
+        const int64_t b = r.y & 0x03ffffff;
+        bl = box8[2 * b];
+        bh = box8[2 * b + 1];
+    };
+    load1(p0 + lane);
+    group_boxes(xm, f0, cnt, s_gb[w], lane);  // empty groups: lo = +inf, hi = -inf (never in reach)
+    if (lane < 12) {
+        const int d = lane / 4, t = lane % 4;
+        s_b[w][t][d] = make_float4(s_gb[w][2 * t][d], s_gb[w][2 * t + 1][d], -s_gb[w][2 * t][3 + d], -s_gb[w][2 * t + 1][3 + d]);
+    }
+    __syncwarp();
+    const int dlo[3] = {dlo3.x, dlo3.y, dlo3.z}, dhi[3] = {dhi3.x, dhi3.y, dhi3.z};
+    // re-read per test (volatile asm) instead of 24 loop-invariant registers: the kernel wants many warps
+    const uint32_t sb = smem_u32(s_b[w]);
+    for (int q = p0 + lane; q < pend; q += 32) {
+        const int2 rc = r;
+        const float4 lc = bl, hc = bh;
+        load1(q + 32);
+        const float4 of = s_off[(unsigned)rc.y >> 26];
+        const float lo[3] = {lc.x + of.x, lc.y + of.y, lc.z + of.z};  // exact (O1)
+        const float hi[3] = {hc.x + of.x, hc.y + of.y, hc.z + of.z};
+        uint32_t m = 0;
+#pragma unroll
+        for (int t = 0; t < 4; ++t) {
+            float2 g[3];
+#pragma unroll
+            for (int d = 0; d < 3; ++d) {
+                float4 gb;
+                asm volatile("ld.shared.v4.f32 {%0, %1, %2, %3}, [%4];"
+                             : "=f"(gb.x), "=f"(gb.y), "=f"(gb.z), "=f"(gb.w)
+                             : "r"(sb + 16u * (3 * t + d)));
+                const float2 u1 = __fadd2_rn(make_float2(lo[d], lo[d]), make_float2(gb.z, gb.w));    // lo_j - hi_g
+                const float2 u2 = __fadd2_rn(make_float2(gb.x, gb.y), make_float2(-hi[d], -hi[d]));  // lo_g - hi_j
+                g[d] = make_float2(fmaxf(fmaxf(u1.x, u2.x), 0.f), fmaxf(fmaxf(u1.y, u2.y), 0.f));
+            }
+            const float2 d2 = __ffma2_rn(g[2], g[2], __ffma2_rn(g[1], g[1], __fmul2_rn(g[0], g[0])));
+            m |= ((d2.x < wcut ? 1u : 0u) | (d2.y < wcut ? 2u : 0u)) << (2 * t);
+        }
+        // Newton-3: group g pairs with the leaf only if the leaf reaches past its first particle
+        // (16 g < first + count - f0), unless the leaf is a ghost
+        const int jend = (rc.x & 0x1fffffff) + ((unsigned)rc.x >> 29) + 1 - f0;
+        const int ngr = jend <= 0 ? 0 : min(8, (jend + 15) >> 4);
+        if (!(partial && leaf_ghost(lc, hc, inv_q, cs, dlo, dhi))) m &= (1u << ngr) - 1u;
+        gmask[q] = (uint8_t)m;
+    }
+}
+
+crk_status entry_masks(crk_ctx* c, cudaStream_t st) {
+    if (c->nleaf[0] <= 0 || !want_masks(c)) return CRK_OK;
+    const Layout& L = c->lay;
+    k_entry_masks<<<nblk(c->nleaf[0] * 32, 256), 256, 0, st>>>(
+        c->nleaf[0], P<int32_t>(c->rowoff[0]), P<int32_t>(c->rowend[0]), P<int2>(c->erec[0]), P<float4>(c->lbox8[1]),
+        P<int32_t>(c->lfirst[0]), P<int32_t>(c->lcount[0]), P<float4>(c->xm), L.L[0], L.L[1], L.L[2],
+        c->prm.rcut2 * CULL_SLACK, L.partial, L.inv_q, L.cs, make_int3(L.dlo[0], L.dlo[1], L.dlo[2]),
+        make_int3(L.dhi[0], L.dhi[1], L.dhi[2]), P<uint8_t>(c->gmask));
+    CRK_LAUNCHED(c, "entry masks");
+    return CRK_OK;
 }
 
 crk_status refresh(crk_ctx* c, crk_particles* p, cudaStream_t st) {
@@ -560,13 +664,7 @@ crk_status refresh(crk_ctx* c, crk_particles* p, cudaStream_t st) {
         CRK_LAUNCHED(c, "repack gas");
     }
     for (int s = 0; s < 4; ++s) CRK_TRY(leaf_boxes(c, s, st));
-    if (c->nleaf[0] > 0) {
-        k_entry_boxes<<<nblk(c->nleaf[0] * 32, 256), 256, 0, st>>>(c->nleaf[0], P<int32_t>(c->rowoff[0]),
-                                                             P<int32_t>(c->rowend[0]), P<int2>(c->erec[0]), P<float4>(c->lbox8[1]),
-                                                             c->lay.L[0], c->lay.L[1], c->lay.L[2],
-                                                             P<float4>(c->gebox));
-        CRK_LAUNCHED(c, "entry boxes");
-    }
+    CRK_TRY(entry_masks(c, st));
     c->stage = ST_LISTS;  // the displacement bound keeps accumulating until the next build
     return CRK_OK;
 }
@@ -727,13 +825,14 @@ crk_status build_lists(crk_ctx* c, crk_particles* p, cudaStream_t st) {
         const int64_t na = c->nleaf[m == 0 ? 0 : 2];
         const int64_t ne = c->nent[m] > 0 ? c->nent[m] : 1;
         CRK_TRY(grow(c, c->erec[m], ne * 8, st));
-        if (m == 0) CRK_TRY(grow(c, c->gebox, ne * 32, st));
+        if (m == 0) CRK_TRY(grow(c, c->gmask, ne + 256, st));
         ListArgs A = list_args(c, m);
         if (na > 0) {
             k_lists<true><<<nblk(na * 32, LIST_WARPS * 32), LIST_WARPS * 32, 0, st>>>(A);
             CRK_LAUNCHED(c, "list fill");
         }
     }
+    CRK_TRY(entry_masks(c, st));
     // ---- gas-ordered state buffers for the hydro passes
     const int64_t ng = c->n_gas > 0 ? c->n_gas : 1;
     CRK_TRY(grow(c, c->gvel, ng * 16, st));

@@ -71,7 +71,8 @@ struct crk_ctx {
     crk::Buf rowend[2];          // row a holds entries [rowoff[a], rowend[a]) (rows written at their bound)
     crk::Buf csroff[2];          // crk_list_view: compacted CSR row offsets
     crk::Buf erec[2];            // packed entries: int2 (first | (count-1) << 29, leaf | shift << 26)
-    crk::Buf gebox;              // gravity entries: float4 (lo + shift, first), (hi + shift, count)
+    crk::Buf gmask;              // gravity entries: uint8 mask of the i-groups (16 i) of the row's leaf the entry
+                                 // can reach (box test + Newton-3 / ghost rule), + 256 B pad for word reads
     // gas-ordered state
     crk::Buf gpos;               // float4 (x, y, z, H)
     crk::Buf gvel;               // float4 (vx, vy, vz, m)

@@ -119,7 +119,7 @@ struct Smem {
 
 struct GravSymArgs {
     const float4* xm;
-    const float4* ebox;  // per list entry: (lo + shift, first), (hi + shift, count | shift code << 8)
+    const uint8_t* gmask;  // per list entry: the i-groups of the row's leaf it can reach (k_entry_masks)
     const float4* box8;  // gravity j-leaf padded boxes
     const int2* erec;    // packed list entries
     const int32_t* row_off;  // row a: entries [row_off[a], row_end[a])
@@ -742,21 +742,23 @@ __global__ void __launch_bounds__(symh::NW * 32, 16 / symh::NW) grav_halfwarp_ke
 // With domain decomposition (A.partial) a pair with a ghost j is evaluated by i's group
 // whatever j's index (the ghost has no group here) and its reaction is dropped (j's own
 // rank evaluates the pair for j).
-// grav_warp_kernel with the L2 latency taken off the critical path: per warp a two-deep
-// software pipeline of async copies (cp.async, no registers held) — the entry records
-// (shifted leaf box + first/count, written by the list build) of chunk c+2 and the
-// particles of the surviving leaves of chunk c+1 are in flight while chunk c is culled
-// and evaluated from shared memory.
+// Per warp a two-deep software pipeline of async copies (cp.async, no registers held): the
+// entry cull is precomputed by the list build as one bit per (entry, i-group) (k_entry_masks:
+// box test + Newton-3 / ghost rule), so the warp scans its row's mask bytes four entries per
+// lane, queues the surviving entries, and streams chunks of 32 of them — the packed entries
+// of chunk c+2 and the particles of chunk c+1 are in flight while chunk c is culled per
+// particle and evaluated from shared memory.
 namespace symp {
-constexpr int G = 16, RING = 64, NW = 4, CH = 32;
+constexpr int G = 16, RING = 64, NW = 4, CH = 32, QCAP = 256;
 // CAPL: surviving j-leaves of a chunk whose particles are staged in shared memory; the rare
 // chunks with more survivors read the rest straight from L2 (smaller per-warp footprint:
 // more resident warps)
 template <int CAPL>
 struct WarpSm {
-    float4 er[2][CH][2];        // entry records of two chunks
-    float4 pp[2][CAPL * JMAX];  // particles of the first CAPL surviving leaves of two chunks
-    float4 woff[2][CH];         // surviving entries: shift offset, first | (count - 1) << 29 (w)
+    int2 ec[2][CH];             // packed list entries of two chunks of surviving entries
+    int sq[QCAP];               // queue of surviving entry indices (mask scan)
+    float4 pp[2][CAPL * JMAX];  // particles of the first CAPL leaves of two chunks
+    float4 woff[2][CH];         // chunk entries: shift offset, first | (count - 1) << 29 (w)
     float4 wpos[RING];
     int widx[RING];
     float2 inx[G / 2], iny[G / 2], inz[G / 2], im[G / 2];
@@ -780,7 +782,6 @@ __global__ void __launch_bounds__(symp::NW * 32, MINB) grav_pipe_kernel(const Gr
     WS& S = reinterpret_cast<WS*>(smem_raw + SHIFT_BYTES)[warp];
     const float wcut = A.wcut;
     const float rc2 = A.rcut2, e2 = A.eps2;
-    const float c0 = A.c0, c1 = A.c1, c2 = A.c2, c3 = A.c3, c4 = A.c4, c5 = A.c5;
     const unsigned below = (1u << lane) - 1u;
     const float4* __restrict__ xm = A.xm;
     if (threadIdx.x < 27) {
@@ -796,24 +797,51 @@ __global__ void __launch_bounds__(symp::NW * 32, MINB) grav_pipe_kernel(const Gr
         w = __shfl_sync(0xffffffffu, w, 0);
         if (w >= A.nitems) break;
         const int a = w / A.split;
+        const int gbit = w % A.split;  // the group's bit in the entry masks
         const int icount = __ldg(A.icount + a);
-        const int ibase = (w % A.split) * G;
+        const int ibase = gbit * G;
         if (ibase >= icount) continue;
         const int gself = __ldg(A.ifirst + a) + ibase;
         const int ng = min(G, icount - ibase);
         const int rbeg = __ldg(A.row_off + a), rend = __ldg(A.row_end + a);
-        const int nch = (rend - rbeg + CH - 1) / CH;
 
-        auto issue_entries = [&](int c) {  // entry records of chunk c -> er[c & 1]
-            const int e = rbeg + c * CH + lane;
-            if (c < nch && e < rend) {
-                cp_async16(&S.er[c & 1][lane][0], A.ebox + 2 * (int64_t)e);
-                cp_async16(&S.er[c & 1][lane][1], A.ebox + 2 * (int64_t)e + 1);
+        // mask scan: queue the row's entries whose bit gbit is set, in row order, until at least
+        // CH wait or the row is exhausted (lane l reads the mask bytes of entries es + 4l .. + 3)
+        int es = rbeg & ~3, qw = 0, qr = 0;
+        auto refill = [&]() {
+            while (qw - qr < CH && es < rend) {
+                const int e = es + 4 * lane;
+                uint32_t sel = 0;
+                if (e < rend) {
+                    const uint32_t wv = __ldg(reinterpret_cast<const uint32_t*>(A.gmask) + (e >> 2));
+                    const uint32_t t = (wv >> gbit) & 0x01010101u;
+                    sel = (t | (t >> 7) | (t >> 14) | (t >> 21)) & 0xfu;
+                    if (e < rbeg) sel &= 0xfu << (rbeg - e);
+                    if (rend - e < 4) sel &= (1u << (rend - e)) - 1u;
+                }
+                const int cnt = __popc(sel);
+                const unsigned b0 = __ballot_sync(0xffffffffu, cnt & 1), b1 = __ballot_sync(0xffffffffu, cnt & 2),
+                               b2 = __ballot_sync(0xffffffffu, cnt & 4);
+                int pos = qw + __popc(b0 & below) + 2 * __popc(b1 & below) + 4 * __popc(b2 & below);
+                while (sel) {
+                    S.sq[pos & (QCAP - 1)] = e + __ffs(sel) - 1;
+                    sel &= sel - 1;
+                    ++pos;
+                }
+                qw += __popc(b0) + 2 * __popc(b1) + 4 * __popc(b2);
+                es += 128;
             }
-            cp_async_commit();
+            __syncwarp();
         };
-        issue_entries(0);
-        issue_entries(1);
+        // the next <= CH queued entries: their packed records -> ec[buf]
+        auto issue_chunk = [&](int buf) {
+            refill();
+            const int n = min(CH, qw - qr);
+            if (lane < n) cp_async8(&S.ec[buf][lane], A.erec + S.sq[(qr + lane) & (QCAP - 1)]);
+            cp_async_commit();
+            qr += n;
+            return n;
+        };
 
         float lo[3], hi[3];
         {
@@ -834,53 +862,27 @@ __global__ void __launch_bounds__(symp::NW * 32, MINB) grav_pipe_kernel(const Gr
             hi[1] = warp_max(iv ? p.y : -INFINITY);
             hi[2] = warp_max(iv ? p.z : -INFINITY);
         }
+        int n0 = issue_chunk(0), n1 = issue_chunk(1), n2 = 0;  // entries of chunks c, c + 1, c + 2
 
-        int ns_even = 0, ns_odd = 0;  // surviving entries of the chunks in buffers 0 / 1
-        // entry cull of chunk c (records landed) and async copies of its surviving leaves
-        auto cull_entries = [&](int c) {
-            const int b = c & 1;
-            bool ek = false;
-            float4 off = make_float4(0.f, 0.f, 0.f, 0.f);
-            if (c < nch && rbeg + c * CH + lane < rend) {
-                const float4 bl = S.er[b][lane][0], bh = S.er[b][lane][1];
-                const int first = __float_as_int(bl.w);
-                const int cc = __float_as_int(bh.w);
-                const int cnt = cc & 0xff;
-                off = shift_tab[cc >> 8];
-                // w: first | (count - 1) << 29, as in the packed list entries
-                off.w = __int_as_float(first | ((cnt - 1) << 29));
-                // entries wholly below this group own no pair — unless they are ghosts (a j-leaf
-                // lies in one cell, so its box centre, unshifted, decides its ownership)
-                bool ghost = false;
-                if (PARTIAL)
-                    ghost = !grav_owned(A, 0.5f * (bl.x + bh.x) - off.x, 0.5f * (bl.y + bh.y) - off.y,
-                                        0.5f * (bl.z + bh.z) - off.z);
-                if (first + cnt > gself || ghost) {
-                    const float gx = fmaxf(fmaxf(bl.x - hi[0], lo[0] - bh.x), 0.f);
-                    const float gy = fmaxf(fmaxf(bl.y - hi[1], lo[1] - bh.y), 0.f);
-                    const float gz = fmaxf(fmaxf(bl.z - hi[2], lo[2] - bh.z), 0.f);
-                    ek = fmaf(gz, gz, fmaf(gy, gy, gx * gx)) < wcut;
-                }
-            }
-            const unsigned em = __ballot_sync(0xffffffffu, ek);
-            const int ns = __popc(em);
-            if (b) ns_odd = ns; else ns_even = ns;
-            if (ek) {
-                // the lane that owns a surviving entry issues its leaf's particle copies (all JMAX
-                // slots: xm is padded, members beyond the count are masked by the particle cull)
-                const int q = __popc(em & below);
-                S.woff[b][q] = off;
-                if (q < CAPL) {
-                    const float4* src = xm + (__float_as_int(off.w) & 0x1fffffff);
+        // chunk entries landed in ec[buf]: shift offsets and the lane's leaf's particle copies
+        // (all JMAX slots: xm is padded, members beyond the count are masked by the particle cull)
+        auto decode = [&](int buf, int n) {
+            if (lane < n) {
+                const int2 r = S.ec[buf][lane];
+                float4 off = shift_tab[(unsigned)r.y >> 26];
+                off.w = __int_as_float(r.x);  // first | (count - 1) << 29
+                S.woff[buf][lane] = off;
+                if (lane < CAPL) {
+                    const float4* src = xm + (r.x & 0x1fffffff);
 #pragma unroll
-                    for (int m = 0; m < JMAX; ++m) cp_async16(&S.pp[b][q * JMAX + m], src + m);
+                    for (int m = 0; m < JMAX; ++m) cp_async16(&S.pp[buf][lane * JMAX + m], src + m);
                 }
             }
             cp_async_commit();
         };
         cp_async_wait<1>();  // entries(0)
         __syncwarp();
-        cull_entries(0);
+        decode(0, n0);
 
         // i-side sums, packed: component .x is i = k, .y is i = k + G/2
         float2 ax[G / 2], ay[G / 2], az[G / 2];
@@ -956,17 +958,17 @@ __global__ void __launch_bounds__(symp::NW * 32, MINB) grav_pipe_kernel(const Gr
         };
 
         int wr = 0, rd = 0;
-        for (int c = 0; c < nch; ++c) {
+        for (int c = 0; n0 > 0; ++c) {
             const int b = c & 1;
-            issue_entries(c + 2);  // into er[b]: chunk c's records were consumed by cull_entries(c)
-            cp_async_wait<2>();    // entries(c + 1)
+            n2 = issue_chunk(b);  // chunk c + 2 into ec[b]: chunk c's entries were decoded
+            cp_async_wait<2>();   // entries(c + 1)
             __syncwarp();
-            cull_entries(c + 1);   // its particles go to pp[b ^ 1] (chunk c - 1's, consumed)
-            cp_async_wait<2>();    // particles(c)
+            decode(b ^ 1, n1);    // its particles go to pp[b ^ 1] (chunk c - 1's, consumed)
+            cp_async_wait<2>();   // particles(c)
             __syncwarp();
             // particle cull of chunk c from shared memory (or L2 past CAPL leaves), then evaluation:
             // lane -> (surviving entry q0 + lane / JMAX, member lane % JMAX)
-            const int ns = b ? ns_odd : ns_even;
+            const int ns = n0;
             const int kk = lane % JMAX;
             const uint32_t ring_pos = opaque_u32(smem_u32(S.wpos)), ring_idx = ring_pos + (uint32_t)sizeof(S.wpos);
             auto cull_iter = [&](int q0, bool staged) {
@@ -999,6 +1001,8 @@ __global__ void __launch_bounds__(symp::NW * 32, MINB) grav_pipe_kernel(const Gr
             for (int q0 = 0; q0 < nst; q0 += 32 / JMAX) cull_iter(q0, true);
             for (int q0 = nst; q0 < ns; q0 += 32 / JMAX) cull_iter(q0, false);  // rare: past CAPL leaves
             __syncwarp();
+            n0 = n1;
+            n1 = n2;
         }
         cp_async_wait<0>();
         if (wr > rd) eval_step(rd, wr - rd);
@@ -1034,336 +1038,6 @@ __global__ void __launch_bounds__(symp::NW * 32, MINB) grav_pipe_kernel(const Gr
             for (int cc = 0; cc < 3; ++cc) v[cc][0] += __shfl_xor_sync(0xffffffffu, v[cc][0], 1);
             if ((lane & 1) == 0 && (lane >> 1) < ng)
                 red_add_v4(A.acc + gself + (lane >> 1), v[0][0], v[1][0], v[2][0], 0.f);
-        }
-        __syncwarp();
-    }
-}
-
-// ------------------------------------------------------------ half-group rings (grav_kernel 3)
-// The pipelined Newton-3 kernel with the warp split into two half-warps, one per half of the
-// 16-particle i-group (half A = i 0..7, half B = i 8..15 in sorted order: the two spatial halves
-// of the group's Morton block).  The particle cull tests every candidate against both half
-// boxes and appends it to the ring of each half it can reach, so a survivor far from one half
-// is evaluated against the other half only (evaluated pairs ~0.84x of one 16-i ring on c4); an
-// eval step takes up to 16 survivors per ring, lane (h, s) evaluating survivor s of ring h
-// against the 8 i of half h, two at a time in packed FP32 (i = 8h + k and 8h + k + 4).  The
-// i-side sums are 8 float2 per lane instead of 16 (fewer registers, more resident warps).  A
-// survivor in both rings gets one reaction per half.  Same entry records, cull, ownership and
-// ghost rules as grav_pipe_kernel; COUNT is the integer-payload audit of exactly this kernel.
-namespace symq {
-constexpr int G = 16, H = 8, RING = 64, NW = 4, CH = 32;
-template <int CAPL>
-struct WarpSm {
-    float4 er[2][CH][2];        // entry records of two chunks
-    float4 pp[2][CAPL * JMAX];  // particles of the first CAPL surviving entries of two chunks
-    float4 woff[2][CH];         // surviving entries: shift offset, first | (count - 1) << 29 (w)
-    float4 rpos[2][RING];       // rings of half A / half B: shifted position, m
-    int ridx[2][RING];          // j (ghosts: -1 - j)
-    float4 ixy[4][2];           // [k][h]: (-x_a, -x_b, -y_a, -y_b), a = 8h + k, b = a + 4
-    float4 izm[4][2];           // [k][h]: (-z_a, -z_b, m_a, m_b)
-};
-}  // namespace symq
-
-template <bool PARTIAL, bool COUNT, int CAPL, int MINB>
-__global__ void __launch_bounds__(symq::NW * 32, MINB) grav_q2_kernel(const GravSymArgs A) {
-    using namespace symq;
-    static_assert(CAPL % (32 / JMAX) == 0, "staged leaves in whole cull iterations");
-    using WS = WarpSm<CAPL>;
-    extern __shared__ __align__(128) unsigned char smem_raw[];
-    const int warp = threadIdx.x >> 5;
-    const int lane = threadIdx.x & 31;
-    const int h = lane >> 4, s = lane & 15;
-    float4* shift_tab = reinterpret_cast<float4*>(smem_raw);
-    WS& S = reinterpret_cast<WS*>(smem_raw + symp::SHIFT_BYTES)[warp];
-    const float wcut = A.rcut2 * CULL_SLACK;
-    const float rc2 = A.rcut2;
-    const unsigned below = (1u << lane) - 1u;
-    const float4* __restrict__ xm = A.xm;
-    if (threadIdx.x < 27) {
-        const int code = threadIdx.x;
-        shift_tab[code] = make_float4((float)(code % 3 - 1) * A.L[0], (float)((code / 3) % 3 - 1) * A.L[1],
-                                      (float)(code / 9 - 1) * A.L[2], 0.f);
-    }
-    __syncthreads();
-
-    while (true) {
-        int w = 0;
-        if (lane == 0) w = atomicAdd(A.work, 1);
-        w = __shfl_sync(0xffffffffu, w, 0);
-        if (w >= A.nitems) break;
-        const int a = w / A.split;
-        const int icount = __ldg(A.icount + a);
-        const int ibase = (w % A.split) * G;
-        if (ibase >= icount) continue;
-        const int gself = __ldg(A.ifirst + a) + ibase;
-        const int ng = min(G, icount - ibase);
-        const int rbeg = __ldg(A.row_off + a), rend = __ldg(A.row_end + a);
-        const int nch = (rend - rbeg + CH - 1) / CH;
-
-        auto issue_entries = [&](int c) {  // entry records of chunk c -> er[c & 1]
-            const int e = rbeg + c * CH + lane;
-            if (c < nch && e < rend) {
-                cp_async16(&S.er[c & 1][lane][0], A.ebox + 2 * (int64_t)e);
-                cp_async16(&S.er[c & 1][lane][1], A.ebox + 2 * (int64_t)e + 1);
-            }
-            cp_async_commit();
-        };
-        issue_entries(0);
-        issue_entries(1);
-
-        // i-particles: lane (h, s) holds i = s (both half-warps hold the whole group)
-        float lo[3], hi[3];      // group box
-        float2 blo[3], nbhi[3];  // half boxes (A in .x, B in .y); -hi
-        {
-            const bool iv = s < ng;
-            float4 p = make_float4(-1e18f, -1e18f, -1e18f, 0.f);
-            if (iv) p = __ldg(xm + gself + s);
-            if (h == 0) {
-                const int k = s & 3, hb = s >> 3, sl = (s >> 2) & 1;
-                float* xy = reinterpret_cast<float*>(&S.ixy[k][hb]);
-                float* zm = reinterpret_cast<float*>(&S.izm[k][hb]);
-                xy[sl] = -p.x; xy[2 + sl] = -p.y;
-                zm[sl] = -p.z; zm[2 + sl] = p.w;
-            }
-            float l3[3] = {iv ? p.x : INFINITY, iv ? p.y : INFINITY, iv ? p.z : INFINITY};
-            float h3[3] = {iv ? p.x : -INFINITY, iv ? p.y : -INFINITY, iv ? p.z : -INFINITY};
-#pragma unroll
-            for (int o = 1; o < 8; o <<= 1)
-#pragma unroll
-                for (int d = 0; d < 3; ++d) {
-                    l3[d] = fminf(l3[d], __shfl_xor_sync(0xffffffffu, l3[d], o));
-                    h3[d] = fmaxf(h3[d], __shfl_xor_sync(0xffffffffu, h3[d], o));
-                }
-#pragma unroll
-            for (int d = 0; d < 3; ++d) {  // lanes s < 8 hold half A's box, s >= 8 half B's
-                const float la = __shfl_sync(0xffffffffu, l3[d], 0), lb = __shfl_sync(0xffffffffu, l3[d], 8);
-                const float ha = __shfl_sync(0xffffffffu, h3[d], 0), hb = __shfl_sync(0xffffffffu, h3[d], 8);
-                blo[d] = make_float2(la, lb);
-                nbhi[d] = make_float2(-ha, -hb);
-                lo[d] = fminf(la, lb);
-                hi[d] = fmaxf(ha, hb);
-            }
-        }
-
-        int ns_even = 0, ns_odd = 0;  // surviving entries of the chunks in buffers 0 / 1
-        // entry cull of chunk c (records landed) and async copies of its surviving leaves,
-        // issued by the lane that owns the entry
-        auto cull_entries = [&](int c) {
-            const int b = c & 1;
-            bool ek = false;
-            float4 off = make_float4(0.f, 0.f, 0.f, 0.f);
-            int first = 0;
-            if (c < nch && rbeg + c * CH + lane < rend) {
-                const float4 bl = S.er[b][lane][0], bh = S.er[b][lane][1];
-                first = __float_as_int(bl.w);
-                const int cc = __float_as_int(bh.w);
-                const int cnt = cc & 0xff;
-                off = shift_tab[cc >> 8];
-                off.w = __int_as_float(first | ((cnt - 1) << 29));
-                bool ghost = false;
-                if (PARTIAL)
-                    ghost = !grav_owned(A, 0.5f * (bl.x + bh.x) - off.x, 0.5f * (bl.y + bh.y) - off.y,
-                                        0.5f * (bl.z + bh.z) - off.z);
-                if (first + cnt > gself || ghost) {
-                    const float gx = fmaxf(fmaxf(bl.x - hi[0], lo[0] - bh.x), 0.f);
-                    const float gy = fmaxf(fmaxf(bl.y - hi[1], lo[1] - bh.y), 0.f);
-                    const float gz = fmaxf(fmaxf(bl.z - hi[2], lo[2] - bh.z), 0.f);
-                    ek = fmaf(gz, gz, fmaf(gy, gy, gx * gx)) < wcut;
-                }
-            }
-            const unsigned em = __ballot_sync(0xffffffffu, ek);
-            if (b) ns_odd = __popc(em); else ns_even = __popc(em);
-            if (ek) {
-                const int q = __popc(em & below);
-                S.woff[b][q] = off;
-                if (q < CAPL) {  // all JMAX slots (xm is padded): members beyond the count are masked later
-                    float4* dst = &S.pp[b][q * JMAX];
-#pragma unroll
-                    for (int m = 0; m < JMAX; ++m) cp_async16(dst + m, xm + first + m);
-                }
-            }
-            cp_async_commit();
-        };
-        cp_async_wait<1>();  // entries(0)
-        __syncwarp();
-        cull_entries(0);
-
-        // i-side sums of half h: component .x is i = 8h + k, .y is i = 8h + k + 4
-        float2 ax[4], ay[4], az[4];
-        int2 ci[COUNT ? 4 : 1];
-#pragma unroll
-        for (int k = 0; k < 4; ++k) ax[k] = ay[k] = az[k] = make_float2(0.f, 0.f);
-#pragma unroll
-        for (int k = 0; k < (COUNT ? 4 : 1); ++k) ci[k] = make_int2(0, 0);
-
-        int wrA = 0, rdA = 0, wrB = 0, rdB = 0;
-        // one eval step: up to 16 survivors of each ring
-        auto eval_step = [&]() {
-            const int nA = min(16, wrA - rdA), nB = min(16, wrB - rdB);
-            const int nh = h ? nB : nA;
-            const bool valid = s < nh;
-            float4 jp = make_float4(1e18f, 1e18f, 1e18f, 0.f);
-            int j = 0;
-            if (valid) {
-                const int q = ((h ? rdB : rdA) + s) & (RING - 1);
-                jp = S.rpos[h][q];
-                j = S.ridx[h][q];
-            }
-            rdA += nA;
-            rdB += nB;
-            const bool jown = j >= gself && j < gself + ng;  // own group: the i-side half is counted
-            const float2 jx = make_float2(jp.x, jp.x), jy = make_float2(jp.y, jp.y), jz = make_float2(jp.z, jp.z);
-            if constexpr (COUNT) {
-                int bj = 0;
-#pragma unroll
-                for (int k = 0; k < 4; ++k) {
-                    const float4 xy = S.ixy[k][h], zm = S.izm[k][h];
-                    const float2 dx = __fadd2_rn(jx, make_float2(xy.x, xy.y));
-                    const float2 dy = __fadd2_rn(jy, make_float2(xy.z, xy.w));
-                    const float2 dz = __fadd2_rn(jz, make_float2(zm.x, zm.y));
-                    const float2 r2 = __ffma2_rn(dz, dz, __ffma2_rn(dy, dy, __fmul2_rn(dx, dx)));
-                    const int ia = gself + 8 * h + k;
-                    const bool in0 = valid && r2.x < rc2 && j != ia;
-                    const bool in1 = valid && r2.y < rc2 && j != ia + 4;
-                    ci[k].x += (in0 && !jown) ? 1 : 0;
-                    ci[k].y += (in1 && !jown) ? 1 : 0;
-                    bj += (in0 ? 1 : 0) + (in1 ? 1 : 0);
-                }
-                if (valid && (!PARTIAL || j >= 0) && bj) atomicAdd(A.cnt + j, bj);
-            } else {
-                const float mj = jown ? 0.f : jp.w;
-                const float2 mj2 = make_float2(mj, mj), e22 = make_float2(A.eps2, A.eps2);
-                const float2 n0 = make_float2(A.nc[0], A.nc[0]), n1 = make_float2(A.nc[1], A.nc[1]);
-                const float2 n2 = make_float2(A.nc[2], A.nc[2]), n3 = make_float2(A.nc[3], A.nc[3]);
-                const float2 n4 = make_float2(A.nc[4], A.nc[4]), n5 = make_float2(A.nc[5], A.nc[5]);
-                float2 bx = make_float2(0.f, 0.f), by = bx, bz = bx;
-#pragma unroll
-                for (int k = 0; k < 4; ++k) {
-                    const float4 xy = S.ixy[k][h], zm = S.izm[k][h];
-                    const float2 dx = __fadd2_rn(jx, make_float2(xy.x, xy.y));  // x_j - x_i, exact (O1)
-                    const float2 dy = __fadd2_rn(jy, make_float2(xy.z, xy.w));
-                    const float2 dz = __fadd2_rn(jz, make_float2(zm.x, zm.y));
-                    const float2 r2 = __ffma2_rn(dz, dz, __ffma2_rn(dy, dy, __fmul2_rn(dx, dx)));  // O2 order
-                    const float2 re = __fadd2_rn(r2, e22);
-                    const float2 ri = make_float2(rsqrtf(re.x), rsqrtf(re.y));
-                    const float2 ri2 = __fmul2_rn(ri, ri);
-                    float2 np5 = __ffma2_rn(n5, r2, n4);  // -P5(s)
-                    np5 = __ffma2_rn(np5, r2, n3);
-                    np5 = __ffma2_rn(np5, r2, n2);
-                    np5 = __ffma2_rn(np5, r2, n1);
-                    np5 = __ffma2_rn(np5, r2, n0);
-                    float2 wv = __ffma2_rn(ri2, ri, np5);  // (s + eps2)^-3/2 - P5(s)
-                    wv.x = r2.x < rc2 ? wv.x : 0.f;
-                    wv.y = r2.y < rc2 ? wv.y : 0.f;
-                    const float2 wi = __fmul2_rn(mj2, wv);  // i-side: a_i += m_j w x_ji
-                    ax[k] = __ffma2_rn(wi, dx, ax[k]);
-                    ay[k] = __ffma2_rn(wi, dy, ay[k]);
-                    az[k] = __ffma2_rn(wi, dz, az[k]);
-                    const float2 wj = __fmul2_rn(make_float2(zm.z, zm.w), wv);  // j-side: a_j -= m_i w x_ji
-                    bx = __ffma2_rn(wj, dx, bx);
-                    by = __ffma2_rn(wj, dy, by);
-                    bz = __ffma2_rn(wj, dz, bz);
-                }
-                if (valid && (!PARTIAL || j >= 0))
-                    red_add_v4(A.acc + j, -(bx.x + bx.y), -(by.x + by.y), -(bz.x + bz.y), 0.f);
-            }
-        };
-
-        for (int c = 0; c < nch; ++c) {
-            const int b = c & 1;
-            issue_entries(c + 2);  // into er[b]: chunk c's records were consumed by cull_entries(c)
-            cp_async_wait<2>();    // entries(c + 1)
-            __syncwarp();
-            cull_entries(c + 1);   // its particles go to pp[b ^ 1] (chunk c - 1's, consumed)
-            cp_async_wait<2>();    // particles(c)
-            __syncwarp();
-            const int ns = b ? ns_odd : ns_even;
-            for (int q0 = 0; q0 < ns; q0 += 32 / JMAX) {
-                const int q = q0 + lane / JMAX, kk = lane % JMAX;
-                const int qc = q < ns ? q : 0;
-                const float4 o = S.woff[b][qc];
-                const int fc = __float_as_int(o.w);
-                const int cnt = (int)((unsigned)fc >> 29) + 1;
-                int j = (fc & 0x1fffffff) + kk;
-                float4 p = q0 < CAPL ? S.pp[b][qc * JMAX + kk] : __ldg(xm + j);
-                bool keep = q < ns && kk < cnt;
-                if (PARTIAL && keep && !grav_owned(A, p.x, p.y, p.z)) j = -1 - j;  // ghost: no reaction
-                p.x += o.x; p.y += o.y; p.z += o.z;  // exact (O1)
-                keep = keep && (j >= gself || (PARTIAL && j < 0));
-                // squared distances to both half boxes (packed: A in .x, B in .y)
-                const float2 px = make_float2(p.x, p.x), py = make_float2(p.y, p.y), pz = make_float2(p.z, p.z);
-                const float2 mx = make_float2(-p.x, -p.x), my = make_float2(-p.y, -p.y), mz = make_float2(-p.z, -p.z);
-                const float2 lx = __fadd2_rn(blo[0], mx), ux = __fadd2_rn(px, nbhi[0]);
-                const float2 ly = __fadd2_rn(blo[1], my), uy = __fadd2_rn(py, nbhi[1]);
-                const float2 lz = __fadd2_rn(blo[2], mz), uz = __fadd2_rn(pz, nbhi[2]);
-                const float2 gx = make_float2(fmaxf(fmaxf(lx.x, ux.x), 0.f), fmaxf(fmaxf(lx.y, ux.y), 0.f));
-                const float2 gy = make_float2(fmaxf(fmaxf(ly.x, uy.x), 0.f), fmaxf(fmaxf(ly.y, uy.y), 0.f));
-                const float2 gz = make_float2(fmaxf(fmaxf(lz.x, uz.x), 0.f), fmaxf(fmaxf(lz.y, uz.y), 0.f));
-                const float2 d2 = __ffma2_rn(gz, gz, __ffma2_rn(gy, gy, __fmul2_rn(gx, gx)));
-                const bool kA = keep && d2.x < wcut, kB = keep && d2.y < wcut;
-                const unsigned mA = __ballot_sync(0xffffffffu, kA), mB = __ballot_sync(0xffffffffu, kB);
-                if (kA) {
-                    const int t = (wrA + __popc(mA & below)) & (RING - 1);
-                    S.rpos[0][t] = p;
-                    S.ridx[0][t] = j;
-                }
-                if (kB) {
-                    const int t = (wrB + __popc(mB & below)) & (RING - 1);
-                    S.rpos[1][t] = p;
-                    S.ridx[1][t] = j;
-                }
-                wrA += __popc(mA);
-                wrB += __popc(mB);
-                __syncwarp();
-                // keep both rings at <= 32 waiting (the next iteration adds <= 32 each)
-                while ((wrA - rdA >= 16 && wrB - rdB >= 16) || wrA - rdA > 32 || wrB - rdB > 32) {
-                    eval_step();
-                    __syncwarp();
-                }
-            }
-            __syncwarp();
-        }
-        cp_async_wait<0>();
-        while (wrA > rdA || wrB > rdB) eval_step();
-        if constexpr (COUNT) {
-#pragma unroll
-            for (int k = 0; k < 4; ++k) {
-                int t0 = ci[k].x, t1 = ci[k].y;
-#pragma unroll
-                for (int o = 1; o < 16; o <<= 1) {
-                    t0 += __shfl_xor_sync(0xffffffffu, t0, o);
-                    t1 += __shfl_xor_sync(0xffffffffu, t1, o);
-                }
-                const int ia = 8 * h + k;
-                if (s == 0 && ia < ng && t0) atomicAdd(A.cnt + gself + ia, t0);
-                if (s == 0 && ia + 4 < ng && t1) atomicAdd(A.cnt + gself + ia + 4, t1);
-            }
-        } else {
-            // transposed (reduce-scatter) sum over the 16 lanes of a half of its 8 x 3 i-side values;
-            // lane s ends with i = 8h + (s >> 1)
-            float v[3][8];
-#pragma unroll
-            for (int k = 0; k < 4; ++k) {
-                v[0][k] = ax[k].x; v[0][k + 4] = ax[k].y;
-                v[1][k] = ay[k].x; v[1][k + 4] = ay[k].y;
-                v[2][k] = az[k].x; v[2][k + 4] = az[k].y;
-            }
-#pragma unroll
-            for (int hh = 4; hh >= 1; hh >>= 1) {
-                const bool up = lane & (2 * hh);
-#pragma unroll
-                for (int cc = 0; cc < 3; ++cc)
-#pragma unroll
-                    for (int k = 0; k < hh; ++k) {
-                        const float send = up ? v[cc][k] : v[cc][k + hh];
-                        const float keep = up ? v[cc][k + hh] : v[cc][k];
-                        v[cc][k] = keep + __shfl_xor_sync(0xffffffffu, send, 2 * hh);
-                    }
-            }
-#pragma unroll
-            for (int cc = 0; cc < 3; ++cc) v[cc][0] += __shfl_xor_sync(0xffffffffu, v[cc][0], 1);
-            const int ii = 8 * h + (s >> 1);
-            if ((s & 1) == 0 && ii < ng) red_add_v4(A.acc + gself + ii, v[0][0], v[1][0], v[2][0], 0.f);
         }
         __syncwarp();
     }
@@ -1439,7 +1113,7 @@ static cudaError_t launch_grav_sym(crk_ctx* c, GravSymArgs& A, cudaStream_t st) 
 static GravSymArgs grav_args(crk_ctx* c) {
     GravSymArgs A;
     A.xm = P<float4>(c->xm);
-    A.ebox = P<float4>(c->gebox);
+    A.gmask = P<uint8_t>(c->gmask);
     A.box8 = P<float4>(c->lbox8[1]);
     A.erec = P<int2>(c->erec[0]);
     A.row_off = P<int32_t>(c->rowoff[0]);
@@ -1482,32 +1156,16 @@ static cudaError_t launch_pipe_cfg(crk_ctx* c, const GravSymArgs& A, cudaStream_
 // the pipelined Newton-3 kernel in its launch configurations (crk_params.grav_kernel 0-2): the
 // shared-memory leaf capacity per chunk and the resident CTAs per SM trade the staged share of
 // the particle reads against occupancy
-template <bool COUNT, int CAPL, int MINB>
-static cudaError_t launch_q2_cfg(crk_ctx* c, const GravSymArgs& A, cudaStream_t st) {
-    int nsm = 0;
-    cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, c->device);
-    const int smem = symp::SHIFT_BYTES + (int)sizeof(symq::WarpSm<CAPL>) * symq::NW;
-    auto k = A.partial ? grav_q2_kernel<true, COUNT, CAPL, MINB> : grav_q2_kernel<false, COUNT, CAPL, MINB>;
-    cudaError_t e = cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
-    if (e != cudaSuccess) return e;
-    int per_sm = 0;
-    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k, symq::NW * 32, smem);
-    k<<<nsm * std::max(1, per_sm), symq::NW * 32, smem, st>>>(A);
-    return cudaGetLastError();
-}
-
 template <bool COUNT>
 static cudaError_t launch_pipe(crk_ctx* c, const GravSymArgs& A, cudaStream_t st) {
     switch (c->prm.grav_kernel) {
     case 1: return launch_pipe_cfg<COUNT, 32, 4>(c, A, st);
     case 2: return launch_pipe_cfg<COUNT, 16, 6>(c, A, st);
-    case 3: return launch_q2_cfg<COUNT, 20, 5>(c, A, st);
-    case 4: return launch_q2_cfg<COUNT, 12, 6>(c, A, st);
     default: return launch_pipe_cfg<COUNT, 20, 5>(c, A, st);
     }
 }
 
-static bool pipe_kernel(crk_ctx* c) { return c->prm.grav_kernel <= 4; }
+static bool pipe_kernel(crk_ctx* c) { return c->prm.grav_kernel <= 2; }
 
 static crk_status gravity_sym(crk_ctx* c, crk_particles* p, float dt, cudaStream_t st) {
     const int64_t n = c->n;
