@@ -335,6 +335,31 @@ struct CorPass : HydCommon {
     }
 };
 
+// ---------------------------------------------------------------- accel records
+// The accel/du-dt pass reads a neighbour's state as one 9-float4 record (ExtPass::finish writes it),
+// laid out so that the packed-FP32 pair terms (AccPass::pair) find their operand pairs aligned in
+// the registers of 128-bit loads: (g = 0, 1) pairs of B, dA, dB for the corrected kernel
+// gradient, (p = 0, 1) pairs of grad v for the limiter, and (x, y) of v.
+//   0: dB0 dB1 dB3 dB4 | 1: dB6 dB7 B0 B1 | 2: dAh0 dAh1 dv0 dv3 | 3: dv1 dv4 dv2 dv5
+//   4: v0 v1 dB2 dB5   | 5: dB8 B2 dAh2 Ah | 6: dv6 dv7 dv8 v2     | 7: V P rho cs
+//   8: 1/H H^2 m u (the particle's own use only)
+// dB[3p + g] = d B_g / d x_p, dv[3a + b] = d v^a / d x_b, Ah = sigma A / H^3, dAh = sigma grad A / H^3.
+// (The 9-float4 stride is odd, so staged records of consecutive slots start in different
+// shared-memory bank groups; an 8-float4 stride put every slot's component in the same group.)
+__device__ __forceinline__ void write_rec(float4* rec, float Ah, const float B[3], const float dAh[3], const float dB[9],
+                                          float vx, float vy, float vz, const float dv[9], float V, float P, float rho,
+                                          float cs, float invH, float H2, float m, float u) {
+    rec[0] = make_float4(dB[0], dB[1], dB[3], dB[4]);
+    rec[1] = make_float4(dB[6], dB[7], B[0], B[1]);
+    rec[2] = make_float4(dAh[0], dAh[1], dv[0], dv[3]);
+    rec[3] = make_float4(dv[1], dv[4], dv[2], dv[5]);
+    rec[4] = make_float4(vx, vy, dB[2], dB[5]);
+    rec[5] = make_float4(dB[8], B[2], dAh[2], Ah);
+    rec[6] = make_float4(dv[6], dv[7], dv[8], vz);
+    rec[7] = make_float4(V, P, rho, cs);
+    rec[8] = make_float4(invH, H2, m, u);
+}
+
 // ============================================================== a6 Extras (upBarEx)
 // rho = sum m_j W^R_ij, P = (gamma-1) rho u, c = sqrt(gamma P / rho),
 // d_b v^a = sum V_j (v^a_j - v^a_i) d_b W^R_ij ; the epilogue also packs the accel
@@ -425,16 +450,8 @@ struct ExtPass : HydCommon {
         for (int t = 0; t < 9; ++t) g[t] = c * a.g[t];
         const float V = gV[k];
         const float4 vm = gvel[k];
-        float4* rec = grec + (int64_t)k * 9;
-        rec[0] = make_float4(g[8], c * s.A, V, Pk);
-        rec[1] = make_float4(s.B[0], s.B[1], s.B[2], r);
-        rec[2] = make_float4(c * s.dA[0], c * s.dA[1], c * s.dA[2], ck);
-        rec[3] = make_float4(s.dB[0], s.dB[1], s.dB[2], s.dB[3]);
-        rec[4] = make_float4(s.dB[4], s.dB[5], s.dB[6], s.dB[7]);
-        rec[5] = make_float4(s.dB[8], vm.x, vm.y, vm.z);
-        rec[6] = make_float4(g[0], g[1], g[2], g[3]);
-        rec[7] = make_float4(g[4], g[5], g[6], g[7]);
-        rec[8] = make_float4(s.invH, s.H2, vm.w, u);
+        const float dAh[3] = {c * s.dA[0], c * s.dA[1], c * s.dA[2]};
+        write_rec(grec + (int64_t)k * 9, c * s.A, s.B, dAh, s.dB, vm.x, vm.y, vm.z, g, V, Pk, r, ck, s.invH, s.H2, vm.w, u);
         const int64_t i = gas_idx[k];
         if (rho) rho[i] = r;
         if (P) P[i] = Pk;
@@ -579,16 +596,9 @@ struct CorExtPass : HydCommon {
         const float ck = sqrtf(gamma * Pk / r);
         const float V = gV[k];
         const float4 vm = gvel[k];
-        float4* rec = grec + (int64_t)k * 9;
-        rec[0] = make_float4(g[8], c * Ai, V, Pk);
-        rec[1] = make_float4(Bi[0], Bi[1], Bi[2], r);
-        rec[2] = make_float4(c * dAi[0], c * dAi[1], c * dAi[2], ck);
-        rec[3] = make_float4(dBi[0][0], dBi[0][1], dBi[0][2], dBi[1][0]);
-        rec[4] = make_float4(dBi[1][1], dBi[1][2], dBi[2][0], dBi[2][1]);
-        rec[5] = make_float4(dBi[2][2], vm.x, vm.y, vm.z);
-        rec[6] = make_float4(g[0], g[1], g[2], g[3]);
-        rec[7] = make_float4(g[4], g[5], g[6], g[7]);
-        rec[8] = make_float4(s.invH, s.H2, vm.w, u);
+        const float dAh[3] = {c * dAi[0], c * dAi[1], c * dAi[2]};
+        const float dBf[9] = {dBi[0][0], dBi[0][1], dBi[0][2], dBi[1][0], dBi[1][1], dBi[1][2], dBi[2][0], dBi[2][1], dBi[2][2]};
+        write_rec(grec + (int64_t)k * 9, c * Ai, Bi, dAh, dBf, vm.x, vm.y, vm.z, g, V, Pk, r, ck, s.invH, s.H2, vm.w, u);
         const int64_t i = gas_idx[k];
         if (A) A[i] = Ai;
 #pragma unroll
@@ -616,20 +626,16 @@ struct Rec {
     float invH, Ah, V, P, B[3], rho, dAh[3], cs, dB[9], v[3], dv[9], H2, m, u;
 };
 
-// Accel records (ExtPass::finish): 9 float4 per particle; the first 8 hold everything the
-// pair terms read from a neighbour, the ninth (1/H, H^2, m, u) only the particle's own use.
-// (The 9-float4 stride is odd, so the staged records of consecutive slots start in
-// different shared-memory bank groups; an 8-float4 stride put every slot's component c in
-// the same group: 8-way conflicts, accel 3x slower.)
+// the Rec form of a record (write_rec layout) for the scalar pair terms of the Newton-3 variant
 __device__ __forceinline__ void unpack_rec8(const float4* r, Rec& q) {
-    float4 t = r[0]; q.dv[8] = t.x; q.Ah = t.y; q.V = t.z; q.P = t.w;
-    t = r[1]; q.B[0] = t.x; q.B[1] = t.y; q.B[2] = t.z; q.rho = t.w;
-    t = r[2]; q.dAh[0] = t.x; q.dAh[1] = t.y; q.dAh[2] = t.z; q.cs = t.w;
-    t = r[3]; q.dB[0] = t.x; q.dB[1] = t.y; q.dB[2] = t.z; q.dB[3] = t.w;
-    t = r[4]; q.dB[4] = t.x; q.dB[5] = t.y; q.dB[6] = t.z; q.dB[7] = t.w;
-    t = r[5]; q.dB[8] = t.x; q.v[0] = t.y; q.v[1] = t.z; q.v[2] = t.w;
-    t = r[6]; q.dv[0] = t.x; q.dv[1] = t.y; q.dv[2] = t.z; q.dv[3] = t.w;
-    t = r[7]; q.dv[4] = t.x; q.dv[5] = t.y; q.dv[6] = t.z; q.dv[7] = t.w;
+    float4 t = r[0]; q.dB[0] = t.x; q.dB[1] = t.y; q.dB[3] = t.z; q.dB[4] = t.w;
+    t = r[1]; q.dB[6] = t.x; q.dB[7] = t.y; q.B[0] = t.z; q.B[1] = t.w;
+    t = r[2]; q.dAh[0] = t.x; q.dAh[1] = t.y; q.dv[0] = t.z; q.dv[3] = t.w;
+    t = r[3]; q.dv[1] = t.x; q.dv[4] = t.y; q.dv[2] = t.z; q.dv[5] = t.w;
+    t = r[4]; q.v[0] = t.x; q.v[1] = t.y; q.dB[2] = t.z; q.dB[5] = t.w;
+    t = r[5]; q.dB[8] = t.x; q.B[2] = t.y; q.dAh[2] = t.z; q.Ah = t.w;
+    t = r[6]; q.dv[6] = t.x; q.dv[7] = t.y; q.dv[8] = t.z; q.v[2] = t.w;
+    t = r[7]; q.V = t.x; q.P = t.y; q.rho = t.z; q.cs = t.w;
 }
 // a neighbour's record from its staged 8 float4 and its H (the staged position row's w)
 __device__ __forceinline__ void unpack_rec_j(const float4* r, float H, Rec& q) {
@@ -709,76 +715,117 @@ struct AccPass : HydCommon {
     int64_t n, ng;
     float *ahx, *ahy, *ahz, *dudt, *vx, *vy, *vz, *u;
     int32_t* cnt;
-    struct I { float x, y, z; int idx; Rec r; };
-    struct Acc { float a[3], du; int nn; };
-    __device__ void init(Acc& a) const { a.a[0] = a.a[1] = a.a[2] = a.du = 0.f; a.nn = 0; }
+    struct I { float x, y, z; int idx; float4 R[9]; };  // position and own record (write_rec layout)
+    struct Acc { float2 a01; float a2, du; int nn; };
+    __device__ void init(Acc& a) const { a.a01 = make_float2(0.f, 0.f); a.a2 = a.du = 0.f; a.nn = 0; }
     __device__ void load_i(int k, I& s) const {
         const float4 p = gpos[k];
         s.x = p.x; s.y = p.y; s.z = p.z; s.idx = k;
-        if (COUNT) { s.r.H2 = __fmul_rn(p.w, p.w); return; }
-        load_rec(grec, ng, k, s.r);
+        if (COUNT) { s.R[8].y = __fmul_rn(p.w, p.w); return; }
+#pragma unroll
+        for (int t = 0; t < 9; ++t) s.R[t] = grec[9 * (int64_t)k + t];
     }
     __device__ void load_i_staged(int k, const float4& p, const float4* rec9, I& s) const {
         s.x = p.x; s.y = p.y; s.z = p.z; s.idx = k;
-        unpack_rec8(rec9, s.r);
-        const float4 t = rec9[8];
-        s.r.invH = t.x; s.r.H2 = t.y; s.r.m = t.z; s.r.u = t.w;
+#pragma unroll
+        for (int t = 0; t < 9; ++t) s.R[t] = rec9[t];
     }
     __device__ float ix(const I& s) const { return s.x; }
     __device__ float iy(const I& s) const { return s.y; }
     __device__ float iz(const I& s) const { return s.z; }
-    __device__ float cut(const I& s) const { return s.r.H2; }
+    __device__ float cut(const I& s) const { return s.R[8].y; }
     __device__ float jcut(const float4& jp) const { return __fmul_rn(jp.w, jp.w); }
     __device__ __forceinline__ bool in(const I& s, const float4& jp) const {
-        return s32_of(s.x - jp.x, s.y - jp.y, s.z - jp.z) < fmaxf(s.r.H2, __fmul_rn(jp.w, jp.w));
+        return s32_of(s.x - jp.x, s.y - jp.y, s.z - jp.z) < fmaxf(s.R[8].y, __fmul_rn(jp.w, jp.w));
+    }
+    // corrected kernel gradient of one particle (record Q) at separation sg * x_ij, packed over the
+    // (x, y) components: wt, gt its kernel factors (gt already times 1/H^2 and sigma-free), lin = 1 + sg B.x
+    __device__ __forceinline__ static void grad_wr2(const float4* Q, float sg, float2 x01, float x2, float wt, float gt,
+                                                   float lin, float2& o01, float& o2) {
+        const float2 dB01 = make_float2(Q[0].x, Q[0].y), dB34 = make_float2(Q[0].z, Q[0].w);
+        const float2 dB67 = make_float2(Q[1].x, Q[1].y), B01 = make_float2(Q[1].z, Q[1].w);
+        const float2 dAh01 = make_float2(Q[2].x, Q[2].y);
+        const float dB2 = Q[4].z, dB5 = Q[4].w, dB8 = Q[5].x, B2 = Q[5].y, dAh2 = Q[5].z, Ah = Q[5].w;
+        const float sx0 = sg * x01.x, sx1 = sg * x01.y, sx2 = sg * x2;
+        // t1_g = sg sum_p dB[3p + g] x_p + B_g
+        const float2 t01 = __ffma2_rn(dB67, make_float2(sx2, sx2), __ffma2_rn(dB34, make_float2(sx1, sx1),
+                                                                             __ffma2_rn(dB01, make_float2(sx0, sx0), B01)));
+        const float t2 = fmaf(dB8, sx2, fmaf(dB5, sx1, fmaf(dB2, sx0, B2)));
+        const float alg = Ah * lin * gt * sg;
+        // out_g = wt (dAh_g lin + Ah t1_g) + alg sg x_g
+        o01 = __ffma2_rn(make_float2(alg, alg), x01,
+                         __fmul2_rn(make_float2(wt, wt), __ffma2_rn(dAh01, make_float2(lin, lin), __fmul2_rn(make_float2(Ah, Ah), t01))));
+        o2 = fmaf(alg, x2, wt * fmaf(dAh2, lin, Ah * t2));
     }
     __device__ __forceinline__ void pair(const I& s, Acc& acc, const float4& jp, const float4* pay, int j) const {
-        float x[3] = {s.x - jp.x, s.y - jp.y, s.z - jp.z};  // x_ij
-        const float r2 = s32_of(x[0], x[1], x[2]);
-        const bool in = r2 < fmaxf(s.r.H2, __fmul_rn(jp.w, jp.w));
+        const float2 x01 = __fadd2_rn(make_float2(s.x, s.y), make_float2(-jp.x, -jp.y));  // x_ij, exact (O1)
+        const float x2 = s.z - jp.z;
+        const float r2 = s32_of(x01.x, x01.y, x2);
+        const bool in = r2 < fmaxf(s.R[8].y, __fmul_rn(jp.w, jp.w));
         if (COUNT) {
             acc.nn += (in && j != s.idx) ? 1 : 0;
             return;
         }
         if (!in) return;
-        Rec q;
-        unpack_rec_j(pay, jp.w, q);
+        float4 Q[8];
+#pragma unroll
+        for (int t = 0; t < 8; ++t) Q[t] = pay[t];
+        const float4* Ri = s.R;
         const float r = sqrtf(r2);
-        float gi[3], gj[3];
-        grad_wr(&s.r.Ah, s.r.dAh, s.r.B, s.r.dB, s.r.invH, r, x, gi);
-        const float xm[3] = {-x[0], -x[1], -x[2]};
-        grad_wr(&q.Ah, q.dAh, q.B, q.dB, q.invH, r, xm, gj);
-        float G[3];
-#pragma unroll
-        for (int g = 0; g < 3; ++g) G[g] = 0.5f * (gi[g] - gj[g]);
-        // limiter on x.grad v.x
-        float gvi[3], gvj[3];
-#pragma unroll
-        for (int p = 0; p < 3; ++p) {
-            gvi[p] = s.r.dv[3 * p] * x[0] + s.r.dv[3 * p + 1] * x[1] + s.r.dv[3 * p + 2] * x[2];
-            gvj[p] = q.dv[3 * p] * x[0] + q.dv[3 * p + 1] * x[1] + q.dv[3 * p + 2] * x[2];
-        }
-        const float xgi = x[0] * gvi[0] + x[1] * gvi[1] + x[2] * gvi[2];
-        const float xgj = x[0] * gvj[0] + x[1] * gvj[1] + x[2] * gvj[2];
+        // Wendland C4 factors of i (.x, support H_i) and j (.y, H_j), packed
+        const float2 ih = make_float2(Ri[8].x, 1.f / jp.w);
+        const float2 q = __fmul2_rn(make_float2(r, r), ih);
+        float2 t = __fadd2_rn(make_float2(1.f, 1.f), make_float2(-q.x, -q.y));
+        t = make_float2(fmaxf(t.x, 0.f), fmaxf(t.y, 0.f));
+        const float2 t2 = __fmul2_rn(t, t);
+        const float2 t5 = __fmul2_rn(__fmul2_rn(t2, t2), t);
+        const float2 wt = __fmul2_rn(__fmul2_rn(t5, t),
+                                     __ffma2_rn(q, __ffma2_rn(q, make_float2(35.f / 3.f, 35.f / 3.f), make_float2(6.f, 6.f)),
+                                                make_float2(1.f, 1.f)));
+        const float2 ih2 = __fmul2_rn(ih, ih);
+        const float2 gt = __fmul2_rn(__fmul2_rn(make_float2(-56.f / 3.f, -56.f / 3.f), ih2),
+                                     __fmul2_rn(t5, __ffma2_rn(make_float2(5.f, 5.f), q, make_float2(1.f, 1.f))));
+        // lin = 1 + B_i.x_ij (i), 1 - B_j.x_ij (j)
+        const float lin_i = fmaf(Ri[5].y, x2, fmaf(Ri[1].w, x01.y, fmaf(Ri[1].z, x01.x, 1.f)));
+        const float lin_j = fmaf(-Q[5].y, x2, fmaf(-Q[1].w, x01.y, fmaf(-Q[1].z, x01.x, 1.f)));
+        float2 gi01, gj01;
+        float gi2, gj2;
+        grad_wr2(Ri, 1.f, x01, x2, wt.x, gt.x, lin_i, gi01, gi2);
+        grad_wr2(Q, -1.f, x01, x2, wt.y, gt.y, lin_j, gj01, gj2);
+        const float2 G01 = __fmul2_rn(make_float2(0.5f, 0.5f), __fadd2_rn(gi01, make_float2(-gj01.x, -gj01.y)));
+        const float G2 = 0.5f * (gi2 - gj2);
+        // limiter on x.grad v.x: gv_p = sum_b dv[3p + b] x_b, packed over p = 0, 1
+        const float2 gvi01 = __ffma2_rn(make_float2(Ri[3].z, Ri[3].w), make_float2(x2, x2),
+                                        __ffma2_rn(make_float2(Ri[3].x, Ri[3].y), make_float2(x01.y, x01.y),
+                                                   __fmul2_rn(make_float2(Ri[2].z, Ri[2].w), make_float2(x01.x, x01.x))));
+        const float2 gvj01 = __ffma2_rn(make_float2(Q[3].z, Q[3].w), make_float2(x2, x2),
+                                        __ffma2_rn(make_float2(Q[3].x, Q[3].y), make_float2(x01.y, x01.y),
+                                                   __fmul2_rn(make_float2(Q[2].z, Q[2].w), make_float2(x01.x, x01.x))));
+        const float gvi2 = fmaf(Ri[6].z, x2, fmaf(Ri[6].y, x01.y, Ri[6].x * x01.x));
+        const float gvj2 = fmaf(Q[6].z, x2, fmaf(Q[6].y, x01.y, Q[6].x * x01.x));
+        const float2 xi = __fmul2_rn(x01, gvi01), xj = __fmul2_rn(x01, gvj01);
+        const float xgi = fmaf(x2, gvi2, xi.x + xi.y);
+        const float xgj = fmaf(x2, gvj2, xj.x + xj.y);
         // phi = 4r/(1+r)^2 with r = xgi/xgj, written as 4 xgi xgj / (xgi + xgj)^2 (r > 0 <=> xgi xgj > 0)
         const float pr = xgi * xgj;
         const float sm = xgi + xgj;
         const float phi = pr > 0.f ? fminf(1.f, 4.f * pr / (sm * sm)) : 0.f;
-        float vij[3], vs[3];
-#pragma unroll
-        for (int p = 0; p < 3; ++p) {
-            vij[p] = s.r.v[p] - q.v[p];
-            vs[p] = vij[p] - 0.5f * phi * (gvi[p] + gvj[p]);
-        }
-        const float vsx = vs[0] * x[0] + vs[1] * x[1] + vs[2] * x[2];
-        const float mui = fminf(0.f, vsx * s.r.invH / fmaf(r2, s.r.invH * s.r.invH, e2));
-        const float muj = fminf(0.f, vsx * q.invH / fmaf(r2, q.invH * q.invH, e2));
-        const float Q = s.r.rho * mui * (Cq * mui - Cl * s.r.cs) + q.rho * muj * (Cq * muj - Cl * q.cs);
-        const float fa = -q.V * (s.r.P + q.P + Q);
-        const float fu = q.V * (s.r.P + 0.5f * Q) * (vij[0] * G[0] + vij[1] * G[1] + vij[2] * G[2]);
-        acc.a[0] = fmaf(fa, G[0], acc.a[0]);
-        acc.a[1] = fmaf(fa, G[1], acc.a[1]);
-        acc.a[2] = fmaf(fa, G[2], acc.a[2]);
+        const float hp = -0.5f * phi;
+        const float2 vij01 = __fadd2_rn(make_float2(Ri[4].x, Ri[4].y), make_float2(-Q[4].x, -Q[4].y));
+        const float vij2 = Ri[6].w - Q[6].w;
+        const float2 vs01 = __ffma2_rn(make_float2(hp, hp), __fadd2_rn(gvi01, gvj01), vij01);
+        const float vs2 = fmaf(hp, gvi2 + gvj2, vij2);
+        const float2 vx = __fmul2_rn(vs01, x01);
+        const float vsx = fmaf(vs2, x2, vx.x + vx.y);
+        // mu_i, mu_j packed: min(0, vsx / H / (r^2 / H^2 + eps^2))
+        const float2 den = __ffma2_rn(make_float2(r2, r2), ih2, make_float2(e2, e2));
+        const float2 mu = make_float2(fminf(0.f, vsx * ih.x / den.x), fminf(0.f, vsx * ih.y / den.y));
+        const float Q2 = Ri[7].z * mu.x * (Cq * mu.x - Cl * Ri[7].w) + Q[7].z * mu.y * (Cq * mu.y - Cl * Q[7].w);
+        const float fa = -Q[7].x * (Ri[7].y + Q[7].y + Q2);
+        const float2 vg = __fmul2_rn(vij01, G01);
+        const float fu = Q[7].x * (Ri[7].y + 0.5f * Q2) * fmaf(vij2, G2, vg.x + vg.y);
+        acc.a01 = __ffma2_rn(make_float2(fa, fa), G01, acc.a01);
+        acc.a2 = fmaf(fa, G2, acc.a2);
         acc.du += fu;
     }
     template <int GG>
@@ -787,8 +834,9 @@ struct AccPass : HydCommon {
             a.nn = slot_sum_i<GG>(a.nn);
             return;
         }
-#pragma unroll
-        for (int t = 0; t < 3; ++t) a.a[t] = slot_sum<GG>(a.a[t]);
+        a.a01.x = slot_sum<GG>(a.a01.x);
+        a.a01.y = slot_sum<GG>(a.a01.y);
+        a.a2 = slot_sum<GG>(a.a2);
         a.du = slot_sum<GG>(a.du);
     }
     __device__ void finish(int k, const I& s, const Acc& a) const {
@@ -797,8 +845,8 @@ struct AccPass : HydCommon {
             cnt[i] = a.nn;
             return;
         }
-        const float f = s.r.V / s.r.m;
-        const float a0 = f * a.a[0], a1 = f * a.a[1], a2 = f * a.a[2], du = f * a.du;
+        const float f = s.R[7].x / s.R[8].z;  // V / m
+        const float a0 = f * a.a01.x, a1 = f * a.a01.y, a2 = f * a.a2, du = f * a.du;
         if (ahx) { ahx[i] = a0; ahy[i] = a1; ahz[i] = a2; }
         if (dudt) dudt[i] = du;
         if (dt != 0.f) {
