@@ -19,6 +19,7 @@ FLAGS = [
     "-O3", "-std=c++17", "-lineinfo", "--use_fast_math",
     "-Xcompiler", "-fPIC", "-Xptxas", "-v",
     "-I", os.path.join(ROOT, "include"),
+] + ([f"-D{d}" for d in os.environ.get("CRK_DEFS", "").split()]) + [
 ]
 
 
