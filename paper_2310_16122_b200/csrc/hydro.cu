@@ -622,53 +622,6 @@ struct CorExtPass : HydCommon {
 // Antisymmetrised CRK-SPH (O9): G_ij = (grad W^R_ij - grad W^R_ji)/2, each half with its
 // own particle's coefficients and H; artificial viscosity with a van Leer limited
 // midpoint velocity reconstruction.  Symmetric predicate s32 < max(H_i^2, H_j^2).
-struct Rec {
-    float invH, Ah, V, P, B[3], rho, dAh[3], cs, dB[9], v[3], dv[9], H2, m, u;
-};
-
-// the Rec form of a record (write_rec layout) for the scalar pair terms of the Newton-3 variant
-__device__ __forceinline__ void unpack_rec8(const float4* r, Rec& q) {
-    float4 t = r[0]; q.dB[0] = t.x; q.dB[1] = t.y; q.dB[3] = t.z; q.dB[4] = t.w;
-    t = r[1]; q.dB[6] = t.x; q.dB[7] = t.y; q.B[0] = t.z; q.B[1] = t.w;
-    t = r[2]; q.dAh[0] = t.x; q.dAh[1] = t.y; q.dv[0] = t.z; q.dv[3] = t.w;
-    t = r[3]; q.dv[1] = t.x; q.dv[4] = t.y; q.dv[2] = t.z; q.dv[5] = t.w;
-    t = r[4]; q.v[0] = t.x; q.v[1] = t.y; q.dB[2] = t.z; q.dB[5] = t.w;
-    t = r[5]; q.dB[8] = t.x; q.B[2] = t.y; q.dAh[2] = t.z; q.Ah = t.w;
-    t = r[6]; q.dv[6] = t.x; q.dv[7] = t.y; q.dv[8] = t.z; q.v[2] = t.w;
-    t = r[7]; q.V = t.x; q.P = t.y; q.rho = t.z; q.cs = t.w;
-}
-// a neighbour's record from its staged 8 float4 and its H (the staged position row's w)
-__device__ __forceinline__ void unpack_rec_j(const float4* r, float H, Rec& q) {
-    unpack_rec8(r, q);
-    q.invH = 1.f / H;
-}
-// a particle's full record from the two planes in global memory
-__device__ __forceinline__ void load_rec(const float4* grec, int64_t ng, int64_t k, Rec& q) {
-    (void)ng;
-    unpack_rec8(grec + 9 * k, q);
-    const float4 t = grec[9 * k + 8];
-    q.invH = t.x; q.H2 = t.y; q.m = t.z; q.u = t.w;
-}
-
-// corrected kernel gradient (scaled by sigma/H^3 via Ah, dAh) at separation x with
-// sign sg (x = sg * x_ij), for a particle with record q
-__device__ __forceinline__ void grad_wr(const float* Ah, const float* dAh, const float* B, const float* dB,
-                                        float invH, float r, const float x[3], float out[3]) {
-    const float q = r * invH;
-    const float t = fmaxf(1.f - q, 0.f);
-    const float t2 = t * t;
-    const float t5 = t2 * t2 * t;
-    const float wt = t5 * t * fmaf(q, fmaf(q, 35.f / 3.f, 6.f), 1.f);
-    const float gt = (-56.f / 3.f) * invH * invH * t5 * fmaf(5.f, q, 1.f);
-    const float lin = 1.f + B[0] * x[0] + B[1] * x[1] + B[2] * x[2];
-    const float alg = (*Ah) * lin * gt;
-#pragma unroll
-    for (int g = 0; g < 3; ++g) {
-        const float t1 = dB[g] * x[0] + dB[3 + g] * x[1] + dB[6 + g] * x[2] + B[g];
-        out[g] = wt * (dAh[g] * lin + (*Ah) * t1) + alg * x[g];
-    }
-}
-
 // ============================================================== count mode of the list walks
 // Integer payload: the pairs a gas pass evaluates while it walks
 // the neighbour lists (or culls on the fly for flagged rows), j != i: the gather predicate
@@ -700,6 +653,94 @@ struct ListCountPass : HydCommon {
     __device__ void reduce(Acc& a) const { a.n = slot_sum_i<GG>(a.n); }
     __device__ void finish(int k, const I&, const Acc& a) const { cnt[gas_idx[k]] = a.n; }
 };
+
+// ============================================================== a7 + a8 pair terms, packed FP32
+// The antisymmetrised pair terms of one pair (i, j) from the two accel records (write_rec layout),
+// x_ij = x01, x2 (x_i - x_j), r2 = s32: the corrected kernel gradients of both particles (the
+// kernel factors of i and j packed, the gradients packed over components), the limiter and the
+// artificial viscosity.  Returns G_ij = (grad W^R_ij - grad W^R_ji) / 2, PQ = P_i + P_j + Q_ij,
+// Qh = Q_ij / 2 and vG = v_ij . G_ij; the i-centric pass makes m_i dv_i/dt += -V_i V_j PQ G and
+// m_i du_i/dt += V_i V_j (P_i + Qh) vG from them, the Newton-3 pass both particles' terms.
+struct AccTerms {
+    float2 G01;
+    float G2, PQ, Qh, vG;
+};
+__device__ __forceinline__ static void grad_wr2(const float4* Q, float sg, float2 x01, float x2, float wt, float gt,
+                                               float lin, float2& o01, float& o2) {
+    const float2 dB01 = make_float2(Q[0].x, Q[0].y), dB34 = make_float2(Q[0].z, Q[0].w);
+    const float2 dB67 = make_float2(Q[1].x, Q[1].y), B01 = make_float2(Q[1].z, Q[1].w);
+    const float2 dAh01 = make_float2(Q[2].x, Q[2].y);
+    const float dB2 = Q[4].z, dB5 = Q[4].w, dB8 = Q[5].x, B2 = Q[5].y, dAh2 = Q[5].z, Ah = Q[5].w;
+    const float sx0 = sg * x01.x, sx1 = sg * x01.y, sx2 = sg * x2;
+    // t1_g = sg sum_p dB[3p + g] x_p + B_g
+    const float2 t01 = __ffma2_rn(dB67, make_float2(sx2, sx2), __ffma2_rn(dB34, make_float2(sx1, sx1),
+                                                                         __ffma2_rn(dB01, make_float2(sx0, sx0), B01)));
+    const float t2 = fmaf(dB8, sx2, fmaf(dB5, sx1, fmaf(dB2, sx0, B2)));
+    const float alg = Ah * lin * gt * sg;
+    // out_g = wt (dAh_g lin + Ah t1_g) + alg sg x_g
+    o01 = __ffma2_rn(make_float2(alg, alg), x01,
+                     __fmul2_rn(make_float2(wt, wt), __ffma2_rn(dAh01, make_float2(lin, lin), __fmul2_rn(make_float2(Ah, Ah), t01))));
+    o2 = fmaf(alg, x2, wt * fmaf(dAh2, lin, Ah * t2));
+}
+__device__ __forceinline__ AccTerms acc_terms(const float4* Ri, const float4* Q, float Hj, float2 x01, float x2, float r2,
+                                              float Cl, float Cq, float e2) {
+    const float r = sqrtf(r2);
+    // Wendland C4 factors of i (.x, support H_i) and j (.y, H_j), packed
+    const float2 ih = make_float2(Ri[8].x, 1.f / Hj);
+    const float2 q = __fmul2_rn(make_float2(r, r), ih);
+    float2 t = __fadd2_rn(make_float2(1.f, 1.f), make_float2(-q.x, -q.y));
+    t = make_float2(fmaxf(t.x, 0.f), fmaxf(t.y, 0.f));
+    const float2 t2 = __fmul2_rn(t, t);
+    const float2 t5 = __fmul2_rn(__fmul2_rn(t2, t2), t);
+    const float2 wt = __fmul2_rn(__fmul2_rn(t5, t),
+                                 __ffma2_rn(q, __ffma2_rn(q, make_float2(35.f / 3.f, 35.f / 3.f), make_float2(6.f, 6.f)),
+                                            make_float2(1.f, 1.f)));
+    const float2 ih2 = __fmul2_rn(ih, ih);
+    const float2 gt = __fmul2_rn(__fmul2_rn(make_float2(-56.f / 3.f, -56.f / 3.f), ih2),
+                                 __fmul2_rn(t5, __ffma2_rn(make_float2(5.f, 5.f), q, make_float2(1.f, 1.f))));
+    // lin = 1 + B_i.x_ij (i), 1 - B_j.x_ij (j)
+    const float lin_i = fmaf(Ri[5].y, x2, fmaf(Ri[1].w, x01.y, fmaf(Ri[1].z, x01.x, 1.f)));
+    const float lin_j = fmaf(-Q[5].y, x2, fmaf(-Q[1].w, x01.y, fmaf(-Q[1].z, x01.x, 1.f)));
+    float2 gi01, gj01;
+    float gi2, gj2;
+    grad_wr2(Ri, 1.f, x01, x2, wt.x, gt.x, lin_i, gi01, gi2);
+    grad_wr2(Q, -1.f, x01, x2, wt.y, gt.y, lin_j, gj01, gj2);
+    AccTerms T;
+    T.G01 = __fmul2_rn(make_float2(0.5f, 0.5f), __fadd2_rn(gi01, make_float2(-gj01.x, -gj01.y)));
+    T.G2 = 0.5f * (gi2 - gj2);
+    // limiter on x.grad v.x: gv_p = sum_b dv[3p + b] x_b, packed over p = 0, 1
+    const float2 gvi01 = __ffma2_rn(make_float2(Ri[3].z, Ri[3].w), make_float2(x2, x2),
+                                    __ffma2_rn(make_float2(Ri[3].x, Ri[3].y), make_float2(x01.y, x01.y),
+                                               __fmul2_rn(make_float2(Ri[2].z, Ri[2].w), make_float2(x01.x, x01.x))));
+    const float2 gvj01 = __ffma2_rn(make_float2(Q[3].z, Q[3].w), make_float2(x2, x2),
+                                    __ffma2_rn(make_float2(Q[3].x, Q[3].y), make_float2(x01.y, x01.y),
+                                               __fmul2_rn(make_float2(Q[2].z, Q[2].w), make_float2(x01.x, x01.x))));
+    const float gvi2 = fmaf(Ri[6].z, x2, fmaf(Ri[6].y, x01.y, Ri[6].x * x01.x));
+    const float gvj2 = fmaf(Q[6].z, x2, fmaf(Q[6].y, x01.y, Q[6].x * x01.x));
+    const float2 xi = __fmul2_rn(x01, gvi01), xj = __fmul2_rn(x01, gvj01);
+    const float xgi = fmaf(x2, gvi2, xi.x + xi.y);
+    const float xgj = fmaf(x2, gvj2, xj.x + xj.y);
+    // phi = 4r/(1+r)^2 with r = xgi/xgj, written as 4 xgi xgj / (xgi + xgj)^2 (r > 0 <=> xgi xgj > 0)
+    const float pr = xgi * xgj;
+    const float sm = xgi + xgj;
+    const float phi = pr > 0.f ? fminf(1.f, 4.f * pr / (sm * sm)) : 0.f;
+    const float hp = -0.5f * phi;
+    const float2 vij01 = __fadd2_rn(make_float2(Ri[4].x, Ri[4].y), make_float2(-Q[4].x, -Q[4].y));
+    const float vij2 = Ri[6].w - Q[6].w;
+    const float2 vs01 = __ffma2_rn(make_float2(hp, hp), __fadd2_rn(gvi01, gvj01), vij01);
+    const float vs2 = fmaf(hp, gvi2 + gvj2, vij2);
+    const float2 vx = __fmul2_rn(vs01, x01);
+    const float vsx = fmaf(vs2, x2, vx.x + vx.y);
+    // mu_i, mu_j packed: min(0, vsx / H / (r^2 / H^2 + eps^2))
+    const float2 den = __ffma2_rn(make_float2(r2, r2), ih2, make_float2(e2, e2));
+    const float2 mu = make_float2(fminf(0.f, vsx * ih.x / den.x), fminf(0.f, vsx * ih.y / den.y));
+    const float Qv = Ri[7].z * mu.x * (Cq * mu.x - Cl * Ri[7].w) + Q[7].z * mu.y * (Cq * mu.y - Cl * Q[7].w);
+    T.PQ = Ri[7].y + Q[7].y + Qv;
+    T.Qh = 0.5f * Qv;
+    const float2 vg = __fmul2_rn(vij01, T.G01);
+    T.vG = fmaf(vij2, T.G2, vg.x + vg.y);
+    return T;
+}
 
 template <bool COUNT, int BATCH_ = 32>
 struct AccPass : HydCommon {
@@ -738,25 +779,6 @@ struct AccPass : HydCommon {
     __device__ __forceinline__ bool in(const I& s, const float4& jp) const {
         return s32_of(s.x - jp.x, s.y - jp.y, s.z - jp.z) < fmaxf(s.R[8].y, __fmul_rn(jp.w, jp.w));
     }
-    // corrected kernel gradient of one particle (record Q) at separation sg * x_ij, packed over the
-    // (x, y) components: wt, gt its kernel factors (gt already times 1/H^2 and sigma-free), lin = 1 + sg B.x
-    __device__ __forceinline__ static void grad_wr2(const float4* Q, float sg, float2 x01, float x2, float wt, float gt,
-                                                   float lin, float2& o01, float& o2) {
-        const float2 dB01 = make_float2(Q[0].x, Q[0].y), dB34 = make_float2(Q[0].z, Q[0].w);
-        const float2 dB67 = make_float2(Q[1].x, Q[1].y), B01 = make_float2(Q[1].z, Q[1].w);
-        const float2 dAh01 = make_float2(Q[2].x, Q[2].y);
-        const float dB2 = Q[4].z, dB5 = Q[4].w, dB8 = Q[5].x, B2 = Q[5].y, dAh2 = Q[5].z, Ah = Q[5].w;
-        const float sx0 = sg * x01.x, sx1 = sg * x01.y, sx2 = sg * x2;
-        // t1_g = sg sum_p dB[3p + g] x_p + B_g
-        const float2 t01 = __ffma2_rn(dB67, make_float2(sx2, sx2), __ffma2_rn(dB34, make_float2(sx1, sx1),
-                                                                             __ffma2_rn(dB01, make_float2(sx0, sx0), B01)));
-        const float t2 = fmaf(dB8, sx2, fmaf(dB5, sx1, fmaf(dB2, sx0, B2)));
-        const float alg = Ah * lin * gt * sg;
-        // out_g = wt (dAh_g lin + Ah t1_g) + alg sg x_g
-        o01 = __ffma2_rn(make_float2(alg, alg), x01,
-                         __fmul2_rn(make_float2(wt, wt), __ffma2_rn(dAh01, make_float2(lin, lin), __fmul2_rn(make_float2(Ah, Ah), t01))));
-        o2 = fmaf(alg, x2, wt * fmaf(dAh2, lin, Ah * t2));
-    }
     __device__ __forceinline__ void pair(const I& s, Acc& acc, const float4& jp, const float4* pay, int j) const {
         const float2 x01 = __fadd2_rn(make_float2(s.x, s.y), make_float2(-jp.x, -jp.y));  // x_ij, exact (O1)
         const float x2 = s.z - jp.z;
@@ -770,62 +792,11 @@ struct AccPass : HydCommon {
         float4 Q[8];
 #pragma unroll
         for (int t = 0; t < 8; ++t) Q[t] = pay[t];
-        const float4* Ri = s.R;
-        const float r = sqrtf(r2);
-        // Wendland C4 factors of i (.x, support H_i) and j (.y, H_j), packed
-        const float2 ih = make_float2(Ri[8].x, 1.f / jp.w);
-        const float2 q = __fmul2_rn(make_float2(r, r), ih);
-        float2 t = __fadd2_rn(make_float2(1.f, 1.f), make_float2(-q.x, -q.y));
-        t = make_float2(fmaxf(t.x, 0.f), fmaxf(t.y, 0.f));
-        const float2 t2 = __fmul2_rn(t, t);
-        const float2 t5 = __fmul2_rn(__fmul2_rn(t2, t2), t);
-        const float2 wt = __fmul2_rn(__fmul2_rn(t5, t),
-                                     __ffma2_rn(q, __ffma2_rn(q, make_float2(35.f / 3.f, 35.f / 3.f), make_float2(6.f, 6.f)),
-                                                make_float2(1.f, 1.f)));
-        const float2 ih2 = __fmul2_rn(ih, ih);
-        const float2 gt = __fmul2_rn(__fmul2_rn(make_float2(-56.f / 3.f, -56.f / 3.f), ih2),
-                                     __fmul2_rn(t5, __ffma2_rn(make_float2(5.f, 5.f), q, make_float2(1.f, 1.f))));
-        // lin = 1 + B_i.x_ij (i), 1 - B_j.x_ij (j)
-        const float lin_i = fmaf(Ri[5].y, x2, fmaf(Ri[1].w, x01.y, fmaf(Ri[1].z, x01.x, 1.f)));
-        const float lin_j = fmaf(-Q[5].y, x2, fmaf(-Q[1].w, x01.y, fmaf(-Q[1].z, x01.x, 1.f)));
-        float2 gi01, gj01;
-        float gi2, gj2;
-        grad_wr2(Ri, 1.f, x01, x2, wt.x, gt.x, lin_i, gi01, gi2);
-        grad_wr2(Q, -1.f, x01, x2, wt.y, gt.y, lin_j, gj01, gj2);
-        const float2 G01 = __fmul2_rn(make_float2(0.5f, 0.5f), __fadd2_rn(gi01, make_float2(-gj01.x, -gj01.y)));
-        const float G2 = 0.5f * (gi2 - gj2);
-        // limiter on x.grad v.x: gv_p = sum_b dv[3p + b] x_b, packed over p = 0, 1
-        const float2 gvi01 = __ffma2_rn(make_float2(Ri[3].z, Ri[3].w), make_float2(x2, x2),
-                                        __ffma2_rn(make_float2(Ri[3].x, Ri[3].y), make_float2(x01.y, x01.y),
-                                                   __fmul2_rn(make_float2(Ri[2].z, Ri[2].w), make_float2(x01.x, x01.x))));
-        const float2 gvj01 = __ffma2_rn(make_float2(Q[3].z, Q[3].w), make_float2(x2, x2),
-                                        __ffma2_rn(make_float2(Q[3].x, Q[3].y), make_float2(x01.y, x01.y),
-                                                   __fmul2_rn(make_float2(Q[2].z, Q[2].w), make_float2(x01.x, x01.x))));
-        const float gvi2 = fmaf(Ri[6].z, x2, fmaf(Ri[6].y, x01.y, Ri[6].x * x01.x));
-        const float gvj2 = fmaf(Q[6].z, x2, fmaf(Q[6].y, x01.y, Q[6].x * x01.x));
-        const float2 xi = __fmul2_rn(x01, gvi01), xj = __fmul2_rn(x01, gvj01);
-        const float xgi = fmaf(x2, gvi2, xi.x + xi.y);
-        const float xgj = fmaf(x2, gvj2, xj.x + xj.y);
-        // phi = 4r/(1+r)^2 with r = xgi/xgj, written as 4 xgi xgj / (xgi + xgj)^2 (r > 0 <=> xgi xgj > 0)
-        const float pr = xgi * xgj;
-        const float sm = xgi + xgj;
-        const float phi = pr > 0.f ? fminf(1.f, 4.f * pr / (sm * sm)) : 0.f;
-        const float hp = -0.5f * phi;
-        const float2 vij01 = __fadd2_rn(make_float2(Ri[4].x, Ri[4].y), make_float2(-Q[4].x, -Q[4].y));
-        const float vij2 = Ri[6].w - Q[6].w;
-        const float2 vs01 = __ffma2_rn(make_float2(hp, hp), __fadd2_rn(gvi01, gvj01), vij01);
-        const float vs2 = fmaf(hp, gvi2 + gvj2, vij2);
-        const float2 vx = __fmul2_rn(vs01, x01);
-        const float vsx = fmaf(vs2, x2, vx.x + vx.y);
-        // mu_i, mu_j packed: min(0, vsx / H / (r^2 / H^2 + eps^2))
-        const float2 den = __ffma2_rn(make_float2(r2, r2), ih2, make_float2(e2, e2));
-        const float2 mu = make_float2(fminf(0.f, vsx * ih.x / den.x), fminf(0.f, vsx * ih.y / den.y));
-        const float Q2 = Ri[7].z * mu.x * (Cq * mu.x - Cl * Ri[7].w) + Q[7].z * mu.y * (Cq * mu.y - Cl * Q[7].w);
-        const float fa = -Q[7].x * (Ri[7].y + Q[7].y + Q2);
-        const float2 vg = __fmul2_rn(vij01, G01);
-        const float fu = Q[7].x * (Ri[7].y + 0.5f * Q2) * fmaf(vij2, G2, vg.x + vg.y);
-        acc.a01 = __ffma2_rn(make_float2(fa, fa), G01, acc.a01);
-        acc.a2 = fmaf(fa, G2, acc.a2);
+        const AccTerms T = acc_terms(s.R, Q, jp.w, x01, x2, r2, Cl, Cq, e2);
+        const float fa = -Q[7].x * T.PQ;                       // -V_j (P_i + P_j + Q)
+        const float fu = Q[7].x * (s.R[7].y + T.Qh) * T.vG;   // V_j (P_i + Q/2) v_ij.G
+        acc.a01 = __ffma2_rn(make_float2(fa, fa), T.G01, acc.a01);
+        acc.a2 = fmaf(fa, T.G2, acc.a2);
         acc.du += fu;
     }
     template <int GG>
@@ -858,55 +829,16 @@ struct AccPass : HydCommon {
     }
 };
 
-// ============================================================== a7 + a8 pair terms, shared form
-// F = V_a V_b (P_a + P_b + Q_ab) G_ab,  Ea = V_a V_b (P_a + Q/2) v_ab.G_ab,  Eb likewise with P_b
-// (x = x_a - x_b; m_a dv_a/dt gets -F, m_b dv_b/dt gets +F; m_a du_a/dt gets Ea, m_b du_b/dt Eb)
-__device__ __forceinline__ void pair_terms(const Rec& A, const Rec& B, const float x[3], float r2, float Cl,
-                                           float Cq, float e2, float F[3], float& Ea, float& Eb) {
-    const float r = sqrtf(r2);
-    float ga[3], gb[3];
-    grad_wr(&A.Ah, A.dAh, A.B, A.dB, A.invH, r, x, ga);
-    const float xm[3] = {-x[0], -x[1], -x[2]};
-    grad_wr(&B.Ah, B.dAh, B.B, B.dB, B.invH, r, xm, gb);
-    float G[3], gva[3], gvb[3];
-#pragma unroll
-    for (int g = 0; g < 3; ++g) G[g] = 0.5f * (ga[g] - gb[g]);
-#pragma unroll
-    for (int p = 0; p < 3; ++p) {
-        gva[p] = A.dv[3 * p] * x[0] + A.dv[3 * p + 1] * x[1] + A.dv[3 * p + 2] * x[2];
-        gvb[p] = B.dv[3 * p] * x[0] + B.dv[3 * p + 1] * x[1] + B.dv[3 * p + 2] * x[2];
-    }
-    const float xga = x[0] * gva[0] + x[1] * gva[1] + x[2] * gva[2];
-    const float xgb = x[0] * gvb[0] + x[1] * gvb[1] + x[2] * gvb[2];
-    const float pr = xga * xgb, sm = xga + xgb;
-    const float phi = pr > 0.f ? fminf(1.f, 4.f * pr / (sm * sm)) : 0.f;
-    float vab[3], vs[3];
-#pragma unroll
-    for (int p = 0; p < 3; ++p) {
-        vab[p] = A.v[p] - B.v[p];
-        vs[p] = vab[p] - 0.5f * phi * (gva[p] + gvb[p]);
-    }
-    const float vsx = vs[0] * x[0] + vs[1] * x[1] + vs[2] * x[2];
-    const float mua = fminf(0.f, vsx * A.invH / fmaf(r2, A.invH * A.invH, e2));
-    const float mub = fminf(0.f, vsx * B.invH / fmaf(r2, B.invH * B.invH, e2));
-    const float Q = A.rho * mua * (Cq * mua - Cl * A.cs) + B.rho * mub * (Cq * mub - Cl * B.cs);
-    const float VV = A.V * B.V;
-    const float PQ = VV * (A.P + B.P + Q);
-    F[0] = PQ * G[0];
-    F[1] = PQ * G[1];
-    F[2] = PQ * G[2];
-    const float vG = vab[0] * G[0] + vab[1] * G[1] + vab[2] * G[2];
-    Ea = VV * (A.P + 0.5f * Q) * vG;
-    Eb = VV * (B.P + 0.5f * Q) * vG;
-}
-
-// ============================================================== a7 + a8, symmetric over the lists
-// Newton-3 over the neighbour lists: the unordered pair {i, j} is evaluated once, in the
-// row of its lower gas rank (i's list holds every j with s32 < max(H_i^2, H_j^2), a
-// symmetric predicate, so j's list holds i).  G_ij, Q_ij, the limiter and the pressure
-// terms are shared by both sides; i's sums stay in registers (S lanes per i), j's go to a
-// float4 (a, du/dt) accumulator with red.global.add.v4.f32.  Only when no row is flagged
-// (every list complete); otherwise the CTAs exit and the gated i-centric kernels run.
+// ============================================================== a7 + a8, Newton-3 over the lists
+// Each unordered pair {i, j} is evaluated once, in the row of its lower gas rank (i's list holds
+// every j with s32 < max(H_i^2, H_j^2), a symmetric predicate, so j's list holds i): one CTA per
+// gas i-leaf row, the row's j-records staged by TMA in rounds of ENT entries with its i-records
+// and i-lists (16-bit staging slots, copied to shared memory so that skipping the entries with a
+// lower rank is a shared-memory scan, not a chain of global loads).  The pair terms are the
+// packed ones of the i-centric pass (acc_terms); i's sums stay in registers (4 lanes per i), j's
+// terms go to a float4 (a, du/dt) accumulator with red.global.add.v4.f32.  Only when no row is
+// flagged (every list complete) and the domain is whole (a ghost has no row of its own);
+// otherwise the CTAs exit and the gated i-centric kernels run.
 struct AccSymListArgs {
     const float4* gpos;  // (x, y, z, H)
     const float4* grec;  // accel records
@@ -917,86 +849,105 @@ struct AccSymListArgs {
     float Cl, Cq, e2;
 };
 
-constexpr int ASL_NW = 8, ASL_G = 8, ASL_ENT = 72;
+constexpr int ASL_NW = 8, ASL_G = 8, ASL_ENT = 64;
+using AslSmem = ListSmem<9, ASL_ENT, true>;
+constexpr int ASL_LIST_OFF = (int)((sizeof(AslSmem) + 127) / 128 * 128);  // the row's lists follow
 
 __global__ void __launch_bounds__(ASL_NW * 32, 2) acc_symlist_kernel(const AccSymListArgs A) {
     constexpr int S = 32 / ASL_G;
-    using SM = ListSmem<9, ASL_ENT>;
     extern __shared__ __align__(128) unsigned char smem_raw[];
-    SM& sm = *reinterpret_cast<SM*>(smem_raw);
-    if (*A.lv.nfrows != 0) return;
+    AslSmem& sm = *reinterpret_cast<AslSmem*>(smem_raw);
+    uint16_t* lst = reinterpret_cast<uint16_t*>(smem_raw + ASL_LIST_OFF);
     const RowView& rv = A.rv;
     const ListView& lv = A.lv;
+    if (*lv.nfrows != 0) return;
+    const int a = blockIdx.x;
     const int warp = threadIdx.x >> 5;
     const int lane = threadIdx.x & 31;
     const int il = lane / S, sl = lane % S;
     const int ibase = warp * ASL_G;
+    const int cap = lv.cap;
     if (threadIdx.x == 0) {
         mbar_init(&sm.bar, 1);
         mbar_fence_init();
     }
     uint32_t phase = 0;
-    while (true) {
-        const int a = claim_row(sm, lv.work);
-        if (a >= lv.nrows) break;
-        const int icount = rv.icount[a];
-        const bool wactive = ibase < icount;
-        const bool ivalid = ibase + il < icount;
-        const int rbeg = rv.row_off[a], rend = rv.row_end[a];
-        const int ki = rv.ifirst[a] + ibase + (ivalid ? il : 0);
-        Rec ri;
-        float4 ip = make_float4(0.f, 0.f, 0.f, 0.f);
-        int nl = 0;
-        if (wactive) {
-            ip = A.gpos[ki];
-            load_rec(A.grec, A.ng, ki, ri);
-            if (ivalid) nl = lv.ncnt[ki];
+    const int ifirst = rv.ifirst[a], icount = rv.icount[a];
+    const bool wactive = ibase < icount;
+    const bool ivalid = ibase + il < icount;
+    const int ki = ifirst + ibase + (ivalid ? il : 0);
+    const int rbeg = rv.row_off[a], rend = rv.row_end[a];
+    IStage ist;
+    ist.grec = A.grec; ist.gpos = A.gpos; ist.ncnt = lv.ncnt;
+    ist.ifirst = ifirst; ist.icount = icount;
+    // the row's lists (consecutive gas ranks: one contiguous block; cap is a multiple of 8)
+    ist.lsrc = lv.nbr + (int64_t)ifirst * cap;
+    ist.ldst = lst;
+    ist.lbytes = (uint32_t)(icount * cap * (int)sizeof(uint16_t));
+    const uint16_t* L = lst + (ibase + il) * cap;
+    float4 Ri[9];
+    float ix = 0.f, iy = 0.f, iz = 0.f;
+    int nl = 0, lp = sl, tn = 0x7fffffff;
+    float2 s01 = make_float2(0.f, 0.f);
+    float s2 = 0.f, s3 = 0.f;
+    for (int e0 = rbeg; e0 < rend; e0 += ASL_ENT) {
+        const int nent = min(ASL_ENT, rend - e0);
+        stage_list_round<9, ASL_NW, ASL_ENT, true>(sm, rv, A.gpos, A.grec, e0, nent, phase,
+                                                   e0 == rbeg ? &ist : nullptr);
+        if (e0 == rbeg && wactive) {  // i-data from the staged copy
+            const int ii = ki - ifirst;
+            const float4 p = sm.ipos[ii];
+            ix = p.x; iy = p.y; iz = p.z;
+#pragma unroll
+            for (int t = 0; t < 9; ++t) Ri[t] = sm.irec[ii * 9 + t];
+            nl = ivalid ? sm.icnt[ii + (ifirst & 3)] : 0;
+            tn = lp < nl ? (int)L[lp] : 0x7fffffff;
         }
-        const float invmi = 1.f / ri.m;
-        float s0 = 0.f, s1 = 0.f, s2 = 0.f, s3 = 0.f;
-        const uint16_t* lp = lv.nbr + (int64_t)ki * lv.cap + sl;
-        const uint16_t* const lend = lv.nbr + (int64_t)ki * lv.cap + nl;
-        int tn = lp < lend ? (int)*lp : 0x7fffffff;
-        for (int e0 = rbeg; e0 < rend; e0 += ASL_ENT) {
-            const int nent = min(ASL_ENT, rend - e0);
-            stage_list_round<9, ASL_NW, ASL_ENT>(sm, rv, A.gpos, A.grec, e0, nent, phase);
-            if (wactive) {
-                const int rs = (e0 - rbeg) * JMAX, re = rs + nent * JMAX;
-                // skip this lane's entries the lower rank does not own (j <= i), within the round
-                auto skip = [&]() {
-                    while (tn < re && __float_as_int(sm.eoff[(tn - rs) / JMAX].w) + (tn - rs) % JMAX <= ki) {
-                        lp += S;
-                        tn = lp < lend ? (int)*lp : 0x7fffffff;
-                    }
-                };
-                skip();
+        if (!wactive) continue;
+        const int rs = (e0 - rbeg) * JMAX, re = rs + nent * JMAX;
+        auto rank = [&](int tl) { return __float_as_int(sm.eoff[tl / JMAX].w) + tl % JMAX; };
+        // this lane's next entry of the round that this row owns (j above i; a parity rule that
+        // balances the owned counts, owner i iff (i + j even) == (i < j), measured 18.6 ms on c4)
+        auto skip = [&]() {
+            while (tn < re && rank(tn - rs) <= ki) {
+                lp += S;
+                tn = lp < nl ? (int)L[lp] : 0x7fffffff;
+            }
+        };
+        skip();
 #pragma unroll 1
-                while (__any_sync(0xffffffffu, tn < re)) {
-                    if (tn < re) {
-                        const int tl = tn - rs;
-                        const int j = __float_as_int(sm.eoff[tl / JMAX].w) + tl % JMAX;
-                        const float4 jp = sm.raw[tl];
-                        lp += S;
-                        tn = lp < lend ? (int)*lp : 0x7fffffff;
-                        Rec rj;
-                        unpack_rec_j(sm.pay + tl * 9, jp.w, rj);
-                        rj.m = sm.pay[tl * 9 + 8].z;
-                        const float x[3] = {ip.x - jp.x, ip.y - jp.y, ip.z - jp.z};  // x_ij
-                        const float r2 = s32_of(x[0], x[1], x[2]);
-                        float F[3], Ei, Ej;
-                        pair_terms(ri, rj, x, r2, A.Cl, A.Cq, A.e2, F, Ei, Ej);
-                        s0 -= F[0]; s1 -= F[1]; s2 -= F[2]; s3 += Ei;
-                        const float im = 1.f / rj.m;
-                        red_add_v4(A.acc + j, F[0] * im, F[1] * im, F[2] * im, Ej * im);
-                        skip();
-                    }
-                }
+        while (__any_sync(0xffffffffu, tn < re)) {
+            if (tn < re) {
+                const int tl = tn - rs;
+                const int j = rank(tl);
+                const float4 jp = sm.raw[tl];
+                const float4* pay = sm.pay + tl * 9;
+                float4 Q[8];
+#pragma unroll
+                for (int t = 0; t < 8; ++t) Q[t] = pay[t];
+                const float imj = 1.f / pay[8].z;
+                const float2 x01 = __fadd2_rn(make_float2(ix, iy), make_float2(-jp.x, -jp.y));  // x_ij, exact (O1)
+                const float x2 = iz - jp.z;
+                const float r2 = s32_of(x01.x, x01.y, x2);
+                const AccTerms T = acc_terms(Ri, Q, jp.w, x01, x2, r2, A.Cl, A.Cq, A.e2);
+                const float VV = Ri[7].x * Q[7].x;
+                const float f = VV * T.PQ;   // F = V_i V_j (P_i + P_j + Q) G: m_i dv_i -= F, m_j dv_j += F
+                const float vg = VV * T.vG;
+                s01 = __ffma2_rn(make_float2(-f, -f), T.G01, s01);
+                s2 = fmaf(-f, T.G2, s2);
+                s3 = fmaf(Ri[7].y + T.Qh, vg, s3);  // m_i du_i/dt += V_i V_j (P_i + Q/2) v_ij.G
+                const float fj = f * imj;
+                red_add_v4(A.acc + j, fj * T.G01.x, fj * T.G01.y, fj * T.G2, (Q[7].y + T.Qh) * vg * imj);
+                lp += S;
+                tn = lp < nl ? (int)L[lp] : 0x7fffffff;
+                skip();
             }
         }
-        if (wactive) {
-            s0 = slot_sum<-S>(s0); s1 = slot_sum<-S>(s1); s2 = slot_sum<-S>(s2); s3 = slot_sum<-S>(s3);
-            if (ivalid && sl == 0) red_add_v4(A.acc + ki, s0 * invmi, s1 * invmi, s2 * invmi, s3 * invmi);
-        }
+    }
+    if (wactive) {
+        s01.x = slot_sum<-S>(s01.x); s01.y = slot_sum<-S>(s01.y); s2 = slot_sum<-S>(s2); s3 = slot_sum<-S>(s3);
+        const float imi = 1.f / Ri[8].z;
+        if (ivalid && sl == 0) red_add_v4(A.acc + ki, s01.x * imi, s01.y * imi, s2 * imi, s3 * imi);
     }
 }
 
@@ -1281,11 +1232,10 @@ static crk_status accel_symlist(crk_ctx* c, crk_particles* p, float dt, cudaStre
     A.acc = P<float4>(c->gacc);
     A.ng = c->n_gas;
     A.Cl = c->prm.av_cl; A.Cq = c->prm.av_cq; A.e2 = c->prm.av_eps2;
-    const int smem = (int)sizeof(ListSmem<9, ASL_ENT>);
+    const int smem = ASL_LIST_OFF + ASL_NW * ASL_G * c->nbr_cap * (int)sizeof(uint16_t);
     cudaError_t e = cudaFuncSetAttribute(acc_symlist_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
     if (e != cudaSuccess) return cuda_check(c, e, "smem attribute");
-    CRK_TRY(cuda_check(c, zero_async(A.lv.work, sizeof(int), st, c), "memset"));
-    acc_symlist_kernel<<<persistent_grid(acc_symlist_kernel, ASL_NW * 32, smem, A.lv.nrows), ASL_NW * 32, smem, st>>>(A);
+    if (A.lv.nrows > 0) acc_symlist_kernel<<<A.lv.nrows, ASL_NW * 32, smem, st>>>(A);
     CRK_LAUNCHED(c, "accel/dudt (symmetric list) kernel");
     k_acc_finish<<<(unsigned)((ng + 255) / 256), 256, 0, st>>>(ng, P<float4>(c->gacc), P<int32_t>(c->gas_idx), dt,
                                                                p->ahx, p->ahy, p->ahz, p->dudt, p->vx, p->vy, p->vz,
@@ -1369,7 +1319,8 @@ crk_status accel_dudt(crk_ctx* c, crk_particles* p, float dt, cudaStream_t st) {
     if (dt != 0.f && (!p->vx || !p->vy || !p->vz || !p->u)) return fail(c, CRK_EINVAL, "kick needs v and u");
     // opt-in (hydro_kernel = 5): c4 14.9 ms vs 12.3 for the i-centric list kernel (the per-pair
     // red.global reactions cost more than the halved pair work saves)
-    if (lists_on(c) && !c->lay.partial && c->prm.hydro_kernel == 5) return accel_symlist(c, p, dt, st);
+    if (lists_on(c) && !c->lay.partial && c->prm.hydro_kernel == 5 && c->nbr_cap % 8 == 0 && c->nbr_cap <= 256)
+        return accel_symlist(c, p, dt, st);
     switch (c->prm.hydro_kernel) {
         case 4: return accel_s8<72>(c, p, dt, st);
         case 6: return accel_s8<128>(c, p, dt, st);

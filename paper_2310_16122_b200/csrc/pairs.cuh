@@ -381,6 +381,9 @@ struct IStage {  // i-data of a row staged with its first round (IREC)
     const float4* gpos;
     const int32_t* ncnt;
     int ifirst, icount;
+    const void* lsrc = nullptr;  // optional: a further contiguous block (the row's neighbour lists)
+    void* ldst = nullptr;
+    uint32_t lbytes = 0;         // multiple of 16
 };
 
 // all threads: stage row entries [e0, e0 + nent) — position rows (x, y, z, w) and PAY payload
@@ -399,6 +402,10 @@ __device__ __forceinline__ void stage_list_round(ListSmem<PAY, ENT, IREC>& sm, c
             bulk_g2s(sm.irec, ist->grec + (int64_t)ist->ifirst * 9, (uint32_t)ist->icount * 144u, &sm.bar);
             bulk_g2s(sm.ipos, ist->gpos + ist->ifirst, (uint32_t)ist->icount * 16u, &sm.bar);
             bulk_g2s(sm.icnt, ist->ncnt + c0, (uint32_t)(c1 - c0) * 4u, &sm.bar);
+        }
+        if (ist && ist->lbytes && threadIdx.x == NW * 32 - 2) {
+            mbar_expect_tx(&sm.bar, ist->lbytes);
+            bulk_g2s(ist->ldst, ist->lsrc, ist->lbytes, &sm.bar);
         }
     }
     for (int t = lane * NW + warp; t < nent; t += NW * 32) {

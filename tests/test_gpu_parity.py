@@ -383,7 +383,7 @@ def test_gravity_symmetric_variants(var, name):
 
 
 @pytest.mark.parametrize("var", [5, 4, 6])
-@pytest.mark.parametrize("cap", [70, 128])
+@pytest.mark.parametrize("cap", [72, 128])
 def test_accel_symmetric_list_variant(cap, var):
     """Opt-in accel list variants: Newton-3 over the neighbour lists (hydro_kernel 5) and
     8 lanes per i (4, 6), with complete lists and with some rows flagged (fallbacks)."""
