@@ -289,8 +289,10 @@ def run_multi(args, parts, params, rank, world, local, gen_s):
     rk = DomainRank(d, rank, own, dev, outputs="forces")
     ex = DistExchange(rank, world, dev)
     hmax2 = ex.allreduce_max(rk.local_hmax2())
+    # overlapped R2/R3 exchange: on with NCCL by default; CRK_OVERLAP=1/0 forces it (tests: gloo ranks)
+    overlap = {"1": True, "0": False}.get(os.environ.get("CRK_OVERLAP", ""))
     for _ in range(args.warmup):
-        substep_dist(rk, ex, args.dt, args.dt, hmax2)
+        substep_dist(rk, ex, args.dt, args.dt, hmax2, overlap=overlap)
     torch.cuda.synchronize()
     dist.barrier()
     e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
@@ -298,7 +300,7 @@ def run_multi(args, parts, params, rank, world, local, gen_s):
     with ClockSampler(local) as clk:
         e0.record()
         for _ in range(args.steps):
-            substep_dist(rk, ex, args.dt, args.dt, hmax2)
+            substep_dist(rk, ex, args.dt, args.dt, hmax2, overlap=overlap)
         e1.record()
         torch.cuda.synchronize()
     red_dev = "cpu" if dist.get_backend() == "gloo" else dev
@@ -318,7 +320,10 @@ def run_multi(args, parts, params, rank, world, local, gen_s):
                 "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f32",
                 "data": "synthetic",
                 "config": dict(_config(args, parts), parallelism=f"3-D domain decomposition {d.dims}, "
-                               f"ghost exchange R1/R2/R3 over {dist.get_backend()} send/recv", global_box=gp["box"],
+                               f"ghost exchange R1/R2/R3 over {dist.get_backend()} send/recv"
+                               + (", R2/R3 overlapped with the interior rows" if (overlap if overlap is not None else
+                                                                                  dist.get_backend() == "nccl") else ""),
+                               global_box=gp["box"],
                                ghost_particles_total=int(pr[3].item()), generator_s=round(gen_s, 1)),
                 "substep_ms": ms_step,
                 "pairs": {"gravity": int(pr[0].item()), "gather": int(pr[1].item()), "sym": int(pr[2].item())},

@@ -172,6 +172,15 @@ crk_status crk_extras(struct crk_ctx* ctx, crk_particles* parts, void* stream);
  * for crk_hydro_accel_dudt.  Reads v and u (as crk_extras does). */
 crk_status crk_corrections_extras(struct crk_ctx* ctx, crk_particles* parts, void* stream);
 
+/* Row subset of the following crk_corrections, crk_extras, crk_corrections_extras and
+ * crk_hydro_accel_dudt calls (a9, the overlap of the ghost exchange with computation, PAPER.md:252
+ * §3.4): 0 = every gas i-leaf row (the default, reset by crk_build_lists),
+ * 1 = the rows whose neighbour rows hold no ghost j-leaf (they read no ghost data, so they may run
+ * while the R2 / R3 messages are in flight), 2 = the other rows (run after the messages landed).
+ * Calls 1 then 2 give the results of one call with 0.  For a whole-box domain every row is
+ * interior.  CRK_EINVAL for another value, CRK_ESTATE before crk_build_lists. */
+crk_status crk_select_rows(struct crk_ctx* ctx, int32_t which);
+
 /* a7 + a8 Acceleration and Energy (upBarAc, upBarDu): antisymmetrised CRK-SPH momentum
  * and energy derivatives with artificial viscosity (O9); kicks v += dt a_h and
  * u += dt du/dt (dt = 0: derivatives only). */

@@ -26,7 +26,7 @@ EXPORTS = ["crk_create", "crk_destroy", "crk_build_lists", "crk_gravity_kick", "
            "crk_pm_accel", "crk_pm_slab_create", "crk_pm_deposit", "crk_pm_slab_forward", "crk_pm_slab_solve",
            "crk_pm_slab_inverse", "crk_pm_interp", "crk_neighbour_lists",
            "crk_select_cells_dev", "crk_select_gas_dev", "crk_pack_particles_dev", "crk_pack_gas_state",
-           "crk_unpack_gas_state"]
+           "crk_unpack_gas_state", "crk_select_rows"]
 
 
 class CrkError(RuntimeError):
@@ -94,6 +94,8 @@ def lib():
         for f in ("crk_kick", "crk_drift"):
             getattr(L, f).argtypes = [vp, C.POINTER(CrkParticles), C.c_float, vp]
         L.crk_update_h.argtypes = [vp, C.POINTER(CrkParticles), C.c_int32, C.c_float, vp, vp, vp]
+        L.crk_select_rows.argtypes = [vp, C.c_int32]
+        L.crk_select_rows.restype = C.c_int
         L.crk_pm_create.argtypes = [C.c_int, C.POINTER(C.c_double), C.c_float, C.c_float, C.c_int, C.POINTER(vp)]
         L.crk_pm_destroy.argtypes = [vp]
         L.crk_pm_accel.argtypes = [vp, C.c_int64, vp, vp, vp, vp, vp, vp, vp, vp]
@@ -293,6 +295,13 @@ class Solver:
 
     def hydro_accel_dudt(self, parts, dt=0.0, stream=None):
         self._call(lib().crk_hydro_accel_dudt, parts, C.c_float(dt), stream=stream)
+
+    ROWS_ALL, ROWS_INTERIOR, ROWS_GHOST = 0, 1, 2
+
+    def select_rows(self, which: int):
+        """crk_select_rows: the row subset of the next corrections / extras / accel calls (0 all,
+        1 rows whose neighbour rows hold no ghost, 2 the others)."""
+        self._check(lib().crk_select_rows(self.ctx, C.c_int32(which)), self.ctx)
 
     def substep(self, parts, dt_grav=0.0, dt_hydro=0.0, stream=None, hydro=True, fused=True, side_stream=None,
                 build=True):

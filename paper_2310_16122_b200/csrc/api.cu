@@ -201,7 +201,7 @@ crk_status crk_destroy(crk_ctx* c) {
     Buf* bufs[] = {&c->keys_a, &c->keys_b, &c->idx_a, &c->idx_b, &c->cub_tmp, &c->scratch, &c->xm,
                    &c->cell_start, &c->cell_end, &c->leaf_cnt, &c->gflag, &c->grank, &c->gas_idx,
                    &c->dev_scalars, &c->gpos, &c->gvel, &c->gV, &c->gcoef, &c->grec, &c->gu,
-                   &c->gacc, &c->gposV, &c->sel_flag, &c->sel_mask, &c->work, &c->nbr, &c->ncnt, &c->lflag, &c->gmask, &c->disp};
+                   &c->gacc, &c->gposV, &c->sel_flag, &c->sel_mask, &c->work, &c->nbr, &c->ncnt, &c->lflag, &c->gmask, &c->rclass, &c->disp};
     for (Buf* b : bufs)
         if (b->p) cudaFree(b->p);
     for (int s = 0; s < 4; ++s) {
@@ -272,6 +272,14 @@ crk_status crk_corrections_extras(crk_ctx* c, crk_particles* p, void* stream) {
     if (!p->vx || !p->vy || !p->vz || !p->u) return fail(c, CRK_EINVAL, "extras needs v and u");
     CRK_TRY(corrections_extras(c, p, (cudaStream_t)stream));
     c->stage = ST_EXT;
+    return CRK_OK;
+}
+
+crk_status crk_select_rows(crk_ctx* c, int32_t which) {
+    if (!c) return CRK_EINVAL;
+    if (which < 0 || which > 2) return fail(c, CRK_EINVAL, "which must be 0 (all rows), 1 (interior) or 2 (ghost rows)");
+    if (which != 0 && c->stage < ST_LISTS) return fail(c, CRK_ESTATE, "call crk_build_lists first");
+    c->row_sel = which;
     return CRK_OK;
 }
 

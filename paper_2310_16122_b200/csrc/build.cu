@@ -265,6 +265,8 @@ struct ListArgs {
     int2* erec;
     const float4* box8B;    // padded j-leaf boxes (lo, max H^2), (hi, 0)
     double skin;            // list skin: cutoffs sqrt(cut2) + skin (0: the exact O4 lists)
+    uint8_t* rclass;        // fill pass, hydro lists of a partial domain (else null): 1 = the row holds a ghost j-leaf
+    int dlo[3], dhi[3];     // owned cells [dlo, dhi)
 };
 
 // ---------------------------------------------------------------- gravity entry masks
@@ -355,6 +357,7 @@ __global__ void __launch_bounds__(LIST_WARPS * 32, 5) k_lists(ListArgs A) {
     }
     int outpos = FILL ? A.rowoff[a] : 0;
     int total = 0;
+    bool ghost_ref = false;  // (hydro fill of a partial domain) some candidate j-leaf is a ghost
     const float mh2a = A.mode == 1 ? A.maxh2A[a] : 0.f;
     if (!generic) {
         const int nx = c1[0] - c0[0] + 1, ny = c1[1] - c0[1] + 1, nz = c1[2] - c0[2] + 1;
@@ -381,6 +384,9 @@ __global__ void __launch_bounds__(LIST_WARPS * 32, 5) k_lists(ListArgs A) {
                     b0 = A.loffB[m];
                     nb = A.loffB[m + 1] - b0;
                     code = (sc[0] + 1) + 3 * (sc[1] + 1) + 9 * (sc[2] + 1);
+                    if (FILL && A.rclass && nb > 0)  // a ghost cell (conservative: before the leaf tests)
+                        ghost_ref |= !(wc[0] >= A.dlo[0] && wc[0] < A.dhi[0] && wc[1] >= A.dlo[1] && wc[1] < A.dhi[1] &&
+                                       wc[2] >= A.dlo[2] && wc[2] < A.dhi[2]);
                 }
             }
             int pre = nb;  // inclusive warp scan
@@ -444,6 +450,9 @@ __global__ void __launch_bounds__(LIST_WARPS * 32, 5) k_lists(ListArgs A) {
                     const uint32_t wz = (uint32_t)((cz % A.ncell[2] + A.ncell[2]) % A.ncell[2]);
                     const uint64_t m = morton3(wx, wy, wz);
                     const int b0 = A.loffB[m], b1 = A.loffB[m + 1];
+                    if (FILL && A.rclass && b1 > b0)
+                        ghost_ref |= !((int)wx >= A.dlo[0] && (int)wx < A.dhi[0] && (int)wy >= A.dlo[1] &&
+                                       (int)wy < A.dhi[1] && (int)wz >= A.dlo[2] && (int)wz < A.dhi[2]);
                     if (!FILL) {
                         total += b1 - b0;
                         continue;
@@ -465,9 +474,11 @@ __global__ void __launch_bounds__(LIST_WARPS * 32, 5) k_lists(ListArgs A) {
                     }
                 }
     }
+    if (FILL && A.rclass) ghost_ref = __any_sync(0xffffffffu, ghost_ref);
     if (lane == 0) {
         if (FILL) A.rowend[a] = outpos;
         else A.rowlen[a] = total;
+        if (FILL && A.rclass) A.rclass[a] = ghost_ref ? 1 : 0;
     }
 }
 
@@ -503,6 +514,8 @@ static ListArgs list_args(crk_ctx* c, int m) {
     A.rowoff = P<int32_t>(c->rowoff[m]);
     A.rowend = P<int32_t>(c->rowend[m]);
     A.jfirst = P<int32_t>(c->lfirst[sb]);
+    A.rclass = (m == 1 && L.partial) ? P<uint8_t>(c->rclass) : nullptr;
+    for (int d = 0; d < 3; ++d) { A.dlo[d] = L.dlo[d]; A.dhi[d] = L.dhi[d]; }
     A.jcount = P<int32_t>(c->lcount[sb]);
     A.erec = P<int2>(c->erec[m]);
     A.box8B = P<float4>(c->lbox8[sb]);
@@ -826,6 +839,10 @@ crk_status build_lists(crk_ctx* c, crk_particles* p, cudaStream_t st) {
         const int64_t ne = c->nent[m] > 0 ? c->nent[m] : 1;
         CRK_TRY(grow(c, c->erec[m], ne * 8, st));
         if (m == 0) CRK_TRY(grow(c, c->gmask, ne + 256, st));
+        if (m == 1) {  // row classes (interior / holds ghosts) for crk_select_rows; all interior when whole
+            CRK_TRY(grow(c, c->rclass, na + 16, st));
+            if (!L.partial) CRK_TRY(cuda_check(c, zero_async(c->rclass.p, na + 16, st, c), "memset"));
+        }
         ListArgs A = list_args(c, m);
         if (na > 0) {
             k_lists<true><<<nblk(na * 32, LIST_WARPS * 32), LIST_WARPS * 32, 0, st>>>(A);
@@ -856,6 +873,7 @@ crk_status build_lists(crk_ctx* c, crk_particles* p, cudaStream_t st) {
     }
     c->skin_lists = c->prm.skin > 0.f;
     c->csr_views = false;
+    c->row_sel = 0;
     c->stage = ST_LISTS;
     return CRK_OK;
 }

@@ -71,6 +71,7 @@ struct crk_ctx {
     crk::Buf rowend[2];          // row a holds entries [rowoff[a], rowend[a]) (rows written at their bound)
     crk::Buf csroff[2];          // crk_list_view: compacted CSR row offsets
     crk::Buf erec[2];            // packed entries: int2 (first | (count-1) << 29, leaf | shift << 26)
+    crk::Buf rclass;             // per gas i-leaf row: 1 = its hydro list holds a ghost j-leaf (crk_select_rows)
     crk::Buf gmask;              // gravity entries: uint8 mask of the i-groups (16 i) of the row's leaf the entry
                                  // can reach (box test + Newton-3 / ghost rule), + 256 B pad for word reads
     // gas-ordered state
@@ -92,5 +93,6 @@ struct crk_ctx {
     // skin lists (crk_params.skin > 0): valid lists survive drifts until crk_refresh
     bool skin_lists = false;     // the last build used the skin and no rebuild is due
     bool csr_views = false;      // col / shift decoded for crk_list_view since the last build
+    int row_sel = 0;             // crk_select_rows: 0 all rows, 1 interior rows, 2 rows holding ghosts
     crk::Buf disp;               // device floats: [0] this drift's max |dt v|, [1] bound since the build
 };

@@ -860,7 +860,7 @@ __global__ void __launch_bounds__(ASL_NW * 32, 2) acc_symlist_kernel(const AccSy
     uint16_t* lst = reinterpret_cast<uint16_t*>(smem_raw + ASL_LIST_OFF);
     const RowView& rv = A.rv;
     const ListView& lv = A.lv;
-    if (*lv.nfrows != 0) return;
+    if (*lv.nfrows != 0 || !row_selected(rv, blockIdx.x)) return;
     const int a = blockIdx.x;
     const int warp = threadIdx.x >> 5;
     const int lane = threadIdx.x & 31;
@@ -1029,7 +1029,9 @@ __global__ void __launch_bounds__(64) k_update_h(RowView rv, ListView lv, const 
 }
 
 // ============================================================== launches
-static RowView hydro_rows(crk_ctx* c) {
+// sel: the passes that honour crk_select_rows (corrections, extras, accel/du-dt); geometry and
+// the count passes always cover every row
+static RowView hydro_rows(crk_ctx* c, bool sel = false) {
     RowView rv;
     rv.ifirst = P<int32_t>(c->lfirst[2]);
     rv.icount = P<int32_t>(c->lcount[2]);
@@ -1038,14 +1040,16 @@ static RowView hydro_rows(crk_ctx* c) {
     rv.erec = P<int2>(c->erec[1]);
     rv.box8 = P<float4>(c->lbox8[3]);
     for (int a = 0; a < 3; ++a) rv.L[a] = c->lay.L[a];
+    rv.rclass = P<uint8_t>(c->rclass);
+    rv.rsel = sel ? c->row_sel : 0;
     return rv;
 }
 
 template <class Pass, int ENT, int MINB = 1, int NW = HYD_NW, int G = HYD_G>
-static crk_status launch_hyd(crk_ctx* c, const Pass& ps, cudaStream_t st, const char* what) {
+static crk_status launch_hyd(crk_ctx* c, const Pass& ps, cudaStream_t st, const char* what, bool sel = false) {
     if (c->nleaf[2] == 0) return CRK_OK;
     static_assert(NW * G >= 64, "a CTA covers a whole gas i-leaf (<= 64)");
-    CRK_TRY(cuda_check(c, launch_pairs<Pass, NW, G, ENT, MINB>(ps, hydro_rows(c), c->nleaf[2], st), what));
+    CRK_TRY(cuda_check(c, launch_pairs<Pass, NW, G, ENT, MINB>(ps, hydro_rows(c, sel), c->nleaf[2], st), what));
     c->launches++;
     return CRK_OK;
 }
@@ -1075,7 +1079,7 @@ static bool lists_on(crk_ctx* c) { return c->nbr_cap > 0 && c->nleaf[2] > 0; }
 template <class Pass, int ENT, int MINB, int FENT, int FMINB, int LG = HYD_G>
 static crk_status launch_listed(crk_ctx* c, const Pass& ps, cudaStream_t st, const char* what) {
     if (c->nleaf[2] == 0) return CRK_OK;
-    RowView rv = hydro_rows(c);
+    RowView rv = hydro_rows(c, true);
     CRK_TRY(grow(c, c->work, 64, st));
     CRK_TRY(cuda_check(c, launch_list<Pass, HYD_NW, LG, ENT, MINB>(ps, rv, list_view(c), st), what));
     c->launches++;
@@ -1133,7 +1137,7 @@ static CorPass cor_pass(crk_ctx* c, crk_particles* p) {
 crk_status corrections(crk_ctx* c, crk_particles* p, cudaStream_t st) {
     CorPass g = cor_pass(c, p);
     if (lists_on(c)) return launch_listed<CorPass, 128, 3, 128, 3>(c, g, st, "corrections kernel");
-    return launch_hyd<CorPass, 128, 3>(c, g, st, "corrections kernel");
+    return launch_hyd<CorPass, 128, 3>(c, g, st, "corrections kernel", true);
 }
 
 __global__ void k_gather_gas_state(int64_t ng, const int32_t* gas_idx, const float* vx, const float* vy,
@@ -1174,7 +1178,7 @@ crk_status extras(crk_ctx* c, crk_particles* p, cudaStream_t st) {
     CRK_TRY(gather_gas_state(c, p, st));
     ExtPass g = ext_pass(c, p);
     if (lists_on(c)) return launch_listed<ExtPass, 128, 3, 128, 3>(c, g, st, "extras kernel");
-    return launch_hyd<ExtPass, 128, 3>(c, g, st, "extras kernel");
+    return launch_hyd<ExtPass, 128, 3>(c, g, st, "extras kernel", true);
 }
 
 // a5 + a6 fused: one list kernel walks each i's list twice (Corrections, then Extras with
@@ -1204,7 +1208,7 @@ crk_status corrections_extras(crk_ctx* c, crk_particles* p, cudaStream_t st) {
     }
     const CorPass gc = cor_pass(c, p);
     const ExtPass ge = ext_pass(c, p);
-    RowView rv = hydro_rows(c);
+    RowView rv = hydro_rows(c, true);
     const ListView lv = list_view(c);
     CRK_TRY(cuda_check(c, (launch_list2<CorPass, ExtPass, HYD_NW, HYD_G, 128, 4>(gc, ge, rv, lv, st)),
                        "corrections + extras kernel"));
@@ -1227,7 +1231,7 @@ static crk_status accel_symlist(crk_ctx* c, crk_particles* p, float dt, cudaStre
     AccSymListArgs A;
     A.gpos = P<float4>(c->gpos);
     A.grec = P<float4>(c->grec);
-    A.rv = hydro_rows(c);
+    A.rv = hydro_rows(c, true);
     A.lv = list_view(c);
     A.acc = P<float4>(c->gacc);
     A.ng = c->n_gas;
@@ -1255,7 +1259,7 @@ static crk_status accel_symlist(crk_ctx* c, crk_particles* p, float dt, cudaStre
     g.cnt = nullptr;
     ListView lv = list_view(c);
     lv.gate = 1;
-    RowView rv = hydro_rows(c);
+    RowView rv = hydro_rows(c, true);
     CRK_TRY(cuda_check(c, launch_list<AccPass<false, 32>, HYD_NW, HYD_G, 72, 2>(g, rv, lv, st), "accel/dudt kernel"));
     c->launches++;
     rv.rows = lv.frows;
@@ -1302,7 +1306,7 @@ static crk_status accel_s8(crk_ctx* c, crk_particles* p, float dt, cudaStream_t 
     g.vx = p->vx; g.vy = p->vy; g.vz = p->vz; g.u = p->u;
     g.cnt = nullptr;
     if (c->nleaf[2] == 0) return CRK_OK;
-    RowView rv = hydro_rows(c);
+    RowView rv = hydro_rows(c, true);
     CRK_TRY(grow(c, c->work, 64, st));
     CRK_TRY(cuda_check(c, (launch_list<AccPass<false, 32>, 16, 4, ENT, 1>(g, rv, list_view(c), st)), "accel/dudt kernel"));
     c->launches++;
@@ -1319,7 +1323,8 @@ crk_status accel_dudt(crk_ctx* c, crk_particles* p, float dt, cudaStream_t st) {
     if (dt != 0.f && (!p->vx || !p->vy || !p->vz || !p->u)) return fail(c, CRK_EINVAL, "kick needs v and u");
     // opt-in (hydro_kernel = 5): c4 14.9 ms vs 12.3 for the i-centric list kernel (the per-pair
     // red.global reactions cost more than the halved pair work saves)
-    if (lists_on(c) && !c->lay.partial && c->prm.hydro_kernel == 5 && c->nbr_cap % 8 == 0 && c->nbr_cap <= 256)
+    if (lists_on(c) && !c->lay.partial && c->row_sel == 0 && c->prm.hydro_kernel == 5 && c->nbr_cap % 8 == 0 &&
+        c->nbr_cap <= 256)
         return accel_symlist(c, p, dt, st);
     switch (c->prm.hydro_kernel) {
         case 4: return accel_s8<72>(c, p, dt, st);

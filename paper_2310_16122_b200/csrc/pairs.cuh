@@ -29,7 +29,13 @@ struct RowView {
     float L[3];
     const int32_t* rows = nullptr;  // non-null: run only rows[0 .. *nrows) (list fallback), grid-strided
     const int32_t* nrows = nullptr;
+    // row subset (crk_select_rows): 0 every row, 1 the rows whose lists reference no ghost, 2 the
+    // others (rclass[a] = 1: row a's list holds a ghost j-leaf), so that a decomposed substep can
+    // run the interior rows while the ghost exchange is in flight
+    const uint8_t* rclass = nullptr;
+    int rsel = 0;
 };
+__device__ __forceinline__ bool row_selected(const RowView& rv, int a) { return rv.rsel == 0 || rv.rclass[a] == rv.rsel - 1; }
 
 // Per-particle neighbour lists of the gas passes: row-relative staging
 // slots (entry index within the i-leaf's CSR row * JMAX + member), ascending, of every
@@ -343,11 +349,12 @@ __global__ void __launch_bounds__(NW * 32, MINB) pair_kernel(const Pass pass, co
     }
     uint32_t phase = 0;
     if (!rv.rows) {
-        pair_row<Pass, NW, G, ENT>(pass, rv, sm, blockIdx.x, phase);
+        if (row_selected(rv, blockIdx.x)) pair_row<Pass, NW, G, ENT>(pass, rv, sm, blockIdx.x, phase);
         return;
     }
     const int nrows = *rv.nrows;
-    for (int w = blockIdx.x; w < nrows; w += gridDim.x) pair_row<Pass, NW, G, ENT>(pass, rv, sm, rv.rows[w], phase);
+    for (int w = blockIdx.x; w < nrows; w += gridDim.x)
+        if (row_selected(rv, rv.rows[w])) pair_row<Pass, NW, G, ENT>(pass, rv, sm, rv.rows[w], phase);
 }
 
 // ---------------------------------------------------------------- list-driven consumer
@@ -536,13 +543,13 @@ __global__ void __launch_bounds__(NW * 32, MINB) list_kernel(const Pass pass, co
         }
     };
     if (!lv.gate) {  // one CTA per row (measured faster than claiming rows: the hardware
-        if (!lv.lflag[blockIdx.x]) row(blockIdx.x);  // overlaps a new CTA's staging)
+        if (!lv.lflag[blockIdx.x] && row_selected(rv, blockIdx.x)) row(blockIdx.x);  // overlaps a new CTA's staging)
         return;
     }
     while (true) {  // gated (rarely run) launches are persistent so that an idle launch is cheap
         const int a = claim_row(sm, lv.work);
         if (a >= lv.nrows) break;
-        if (!lv.lflag[a]) row(a);
+        if (!lv.lflag[a] && row_selected(rv, a)) row(a);
     }
 }
 
@@ -561,7 +568,7 @@ __global__ void __launch_bounds__(NW * 32, MINB) list_kernel2(const PA pa, const
     extern __shared__ __align__(128) unsigned char smem_raw[];
     SM& sm = *reinterpret_cast<SM*>(smem_raw);
     const int a = blockIdx.x;
-    if (lv.lflag[a]) return;
+    if (lv.lflag[a] || !row_selected(rv, a)) return;
     const int warp = threadIdx.x >> 5;
     const int lane = threadIdx.x & 31;
     const int il = lane / S;

@@ -375,6 +375,26 @@ class DomainRank:
     def accel(self, dt_hydro=0.0):
         self.solver.hydro_accel_dudt(self.p, dt_hydro, self.stream)
 
+    # the same passes on a row subset (crk_select_rows): interior rows (no ghost in their
+    # neighbour rows) while a message is in flight, the rows holding ghosts after it landed
+    def corrections_extras_rows(self, which: int):
+        self.solver.select_rows(which)
+        self.solver.corrections_extras(self.p, self.stream)
+        self.solver.select_rows(0)
+
+    def accel_rows(self, which: int, dt_hydro=0.0):
+        self.solver.select_rows(which)
+        self.solver.hydro_accel_dudt(self.p, dt_hydro, self.stream)
+        self.solver.select_rows(0)
+
+    def compute_stream(self):
+        return self.stream if self.stream is not None else torch.cuda.current_stream(self.device)
+
+    def comm_stream(self):
+        if getattr(self, "_comm", None) is None:
+            self._comm = torch.cuda.Stream(self.device)
+        return self._comm
+
     def writeback(self):
         """Kicked velocities and internal energies of the own particles back into the own set
         (the next substep's R1 reads them): own rows are the sorted positions with perm < n_own."""
@@ -444,9 +464,10 @@ def _counts_host(ranks_cnt_send, ranks_cnt_recv):
     return [np.stack([cs.cpu().numpy(), cr.cpu().numpy()]) for cs, cr in zip(ranks_cnt_send, ranks_cnt_recv)]
 
 
-def substep_inprocess(ranks, dt_grav=0.0, dt_hydro=0.0):
+def substep_inprocess(ranks, dt_grav=0.0, dt_hydro=0.0, overlap=False):
     """One decomposed substep for ranks emulated sequentially in one process (tests): the same
-    phases and messages as substep_dist, the transfers as device copies."""
+    phases and messages as substep_dist, the transfers as device copies.  overlap: the pass
+    order of substep_dist's overlapped exchange (interior rows before the messages land)."""
     hmax2 = max(rk.local_hmax2() for rk in ranks)
     h = ranks[0].d.halo_width(hmax2)
     for rk in ranks:
@@ -464,17 +485,29 @@ def substep_inprocess(ranks, dt_grav=0.0, dt_hydro=0.0):
     for rk in ranks:
         rk.gravity_geometry(dt_grav)
     msgs = [rk.r2_messages() for rk in ranks]
+    if overlap:  # the interior rows before the messages land
+        for rk in ranks:
+            rk.corrections_extras_rows(1)
     EmuExchange(ranks).exchange_all([m[0] for m in msgs], [m[1] for m in msgs])
     for rk, m in zip(ranks, msgs):
         rk.r2_unpack(m[1])
     for rk in ranks:
-        rk.corrections_extras()
+        if overlap:
+            rk.corrections_extras_rows(2)
+        else:
+            rk.corrections_extras()
     msgs = [rk.r3_messages() for rk in ranks]
+    if overlap:
+        for rk in ranks:
+            rk.accel_rows(1, dt_hydro)
     EmuExchange(ranks).exchange_all([m[0] for m in msgs], [m[1] for m in msgs])
     for rk, m in zip(ranks, msgs):
         rk.r3_unpack(m[1])
     for rk in ranks:
-        rk.accel(dt_hydro)
+        if overlap:
+            rk.accel_rows(2, dt_hydro)
+        else:
+            rk.accel(dt_hydro)
         if dt_grav != 0.0 or dt_hydro != 0.0:
             rk.writeback()
 
@@ -526,9 +559,31 @@ def migrate_dist(rk: DomainRank, ex: DistExchange):
     rk.migrate_finish(host[0], recv, ex.exchange)
 
 
-def substep_dist(rk: DomainRank, ex: DistExchange, dt_grav=0.0, dt_hydro=0.0, hmax2=None):
+def _overlapped(rk: DomainRank, ex: DistExchange, msgs, interior, rest):
+    """Post one exchange on the rank's communication stream (after the compute stream's packing)
+    and run `interior` on the compute stream meanwhile; the compute stream then waits for the
+    messages and runs `rest`.  NCCL's send/recv are enqueued on the current (communication)
+    stream and their wait() orders that stream, not the host: no synchronisation."""
+    sends, recvs = msgs
+    cs, comm = rk.compute_stream(), rk.comm_stream()
+    comm.wait_stream(cs)  # the packed messages
+    with torch.cuda.stream(comm):
+        ex.exchange(sends, recvs)
+    interior()
+    cs.wait_stream(comm)
+    for t in list(sends.values()) + list(recvs.values()):
+        t.record_stream(comm)
+    rest(recvs)
+
+
+def substep_dist(rk: DomainRank, ex: DistExchange, dt_grav=0.0, dt_hydro=0.0, hmax2=None, overlap=None):
     """One decomposed substep on this rank, exchanging with the other ranks: one host
-    readback (the R1 counts) besides crk_build_lists' own."""
+    readback (the R1 counts) besides crk_build_lists' own.  overlap (default: on with NCCL):
+    R2 is in flight while Corrections + Extras run on the interior rows (rows whose neighbour
+    rows hold no ghost), R3 while Acceleration does; the rows holding ghosts follow."""
+    if overlap is None:
+        import torch.distributed as dist
+        overlap = rk.device.type == "cuda" and dist.get_backend() == "nccl"
     if hmax2 is None:
         hmax2 = ex.allreduce_max(rk.local_hmax2())
     rk.plan(rk.d.halo_width(hmax2))
@@ -541,13 +596,19 @@ def substep_dist(rk: DomainRank, ex: DistExchange, dt_grav=0.0, dt_hydro=0.0, hm
     ex.exchange(*rk.r1_messages())
     rk.r1_unpack_and_build()
     rk.gravity_geometry(dt_grav)
-    sends, recvs = rk.r2_messages()
-    ex.exchange(sends, recvs)
-    rk.r2_unpack(recvs)
-    rk.corrections_extras()
-    sends, recvs = rk.r3_messages()
-    ex.exchange(sends, recvs)
-    rk.r3_unpack(recvs)
-    rk.accel(dt_hydro)
+    if overlap:
+        _overlapped(rk, ex, rk.r2_messages(), lambda: rk.corrections_extras_rows(1),
+                    lambda recvs: (rk.r2_unpack(recvs), rk.corrections_extras_rows(2)))
+        _overlapped(rk, ex, rk.r3_messages(), lambda: rk.accel_rows(1, dt_hydro),
+                    lambda recvs: (rk.r3_unpack(recvs), rk.accel_rows(2, dt_hydro)))
+    else:
+        sends, recvs = rk.r2_messages()
+        ex.exchange(sends, recvs)
+        rk.r2_unpack(recvs)
+        rk.corrections_extras()
+        sends, recvs = rk.r3_messages()
+        ex.exchange(sends, recvs)
+        rk.r3_unpack(recvs)
+        rk.accel(dt_hydro)
     if dt_grav != 0.0 or dt_hydro != 0.0:
         rk.writeback()
