@@ -749,16 +749,15 @@ __global__ void __launch_bounds__(symh::NW * 32, 16 / symh::NW) grav_halfwarp_ke
 // of chunk c+2 and the particles of chunk c+1 are in flight while chunk c is culled per
 // particle and evaluated from shared memory.
 namespace symp {
-constexpr int G = 16, RING = 64, NW = 4, CH = 32, QCAP = 256;
-// CAPL: surviving j-leaves of a chunk whose particles are staged in shared memory; the rare
-// chunks with more survivors read the rest straight from L2 (smaller per-warp footprint:
-// more resident warps)
+constexpr int G = 16, RING = 64, NW = 4, QCAP = 256;
+// CAPL: the chunk size, surviving j-leaves whose particles are staged in shared memory per chunk
+// (the queued chunks are full: a chunk larger than CAPL read a third of its leaves from L2)
 template <int CAPL>
 struct WarpSm {
-    int2 ec[2][CH];             // packed list entries of two chunks of surviving entries
+    int2 ec[2][CAPL];           // packed list entries of two chunks of surviving entries
     int sq[QCAP];               // queue of surviving entry indices (mask scan)
     float4 pp[2][CAPL * JMAX];  // particles of the first CAPL leaves of two chunks
-    float4 woff[2][CH];         // chunk entries: shift offset, first | (count - 1) << 29 (w)
+    float4 woff[2][CAPL];       // chunk entries: shift offset, first | (count - 1) << 29 (w)
     float4 wpos[RING];
     int widx[RING];
     float2 inx[G / 2], iny[G / 2], inz[G / 2], im[G / 2];
@@ -806,10 +805,10 @@ __global__ void __launch_bounds__(symp::NW * 32, MINB) grav_pipe_kernel(const Gr
         const int rbeg = __ldg(A.row_off + a), rend = __ldg(A.row_end + a);
 
         // mask scan: queue the row's entries whose bit gbit is set, in row order, until at least
-        // CH wait or the row is exhausted (lane l reads the mask bytes of entries es + 4l .. + 3)
+        // CAPL wait or the row is exhausted (lane l reads the mask bytes of entries es + 4l .. + 3)
         int es = rbeg & ~3, qw = 0, qr = 0;
         auto refill = [&]() {
-            while (qw - qr < CH && es < rend) {
+            while (qw - qr < CAPL && es < rend) {
                 const int e = es + 4 * lane;
                 uint32_t sel = 0;
                 if (e < rend) {
@@ -833,10 +832,10 @@ __global__ void __launch_bounds__(symp::NW * 32, MINB) grav_pipe_kernel(const Gr
             }
             __syncwarp();
         };
-        // the next <= CH queued entries: their packed records -> ec[buf]
+        // the next <= CAPL queued entries: their packed records -> ec[buf]
         auto issue_chunk = [&](int buf) {
             refill();
-            const int n = min(CH, qw - qr);
+            const int n = min(CAPL, qw - qr);
             if (lane < n) cp_async8(&S.ec[buf][lane], A.erec + S.sq[(qr + lane) & (QCAP - 1)]);
             cp_async_commit();
             qr += n;
@@ -966,19 +965,19 @@ __global__ void __launch_bounds__(symp::NW * 32, MINB) grav_pipe_kernel(const Gr
             decode(b ^ 1, n1);    // its particles go to pp[b ^ 1] (chunk c - 1's, consumed)
             cp_async_wait<2>();   // particles(c)
             __syncwarp();
-            // particle cull of chunk c from shared memory (or L2 past CAPL leaves), then evaluation:
+            // particle cull of chunk c from shared memory, then evaluation:
             // lane -> (surviving entry q0 + lane / JMAX, member lane % JMAX)
             const int ns = n0;
             const int kk = lane % JMAX;
             const uint32_t ring_pos = opaque_u32(smem_u32(S.wpos)), ring_idx = ring_pos + (uint32_t)sizeof(S.wpos);
-            auto cull_iter = [&](int q0, bool staged) {
+            auto cull_iter = [&](int q0) {
                 const int q = q0 + lane / JMAX;
                 const bool qv = q < ns;
                 const int qc = qv ? q : 0;
                 const float4 o = S.woff[b][qc];
                 const int fc = __float_as_int(o.w);
                 int j = (fc & 0x1fffffff) + kk;
-                float4 p = staged ? S.pp[b][qc * JMAX + kk] : __ldg(xm + j);
+                float4 p = S.pp[b][qc * JMAX + kk];
                 bool keep = qv && kk <= (int)((unsigned)fc >> 29);
                 if (PARTIAL && keep && !grav_owned(A, p.x, p.y, p.z)) j = -1 - j;  // ghost: no reaction
                 p.x += o.x; p.y += o.y; p.z += o.z;  // exact (O1)
@@ -997,9 +996,7 @@ __global__ void __launch_bounds__(symp::NW * 32, MINB) grav_pipe_kernel(const Gr
                     __syncwarp();
                 }
             };
-            const int nst = min(ns, CAPL);
-            for (int q0 = 0; q0 < nst; q0 += 32 / JMAX) cull_iter(q0, true);
-            for (int q0 = nst; q0 < ns; q0 += 32 / JMAX) cull_iter(q0, false);  // rare: past CAPL leaves
+            for (int q0 = 0; q0 < ns; q0 += 32 / JMAX) cull_iter(q0);
             __syncwarp();
             n0 = n1;
             n1 = n2;
@@ -1161,7 +1158,7 @@ static cudaError_t launch_pipe(crk_ctx* c, const GravSymArgs& A, cudaStream_t st
     switch (c->prm.grav_kernel) {
     case 1: return launch_pipe_cfg<COUNT, 32, 4>(c, A, st);
     case 2: return launch_pipe_cfg<COUNT, 16, 6>(c, A, st);
-    default: return launch_pipe_cfg<COUNT, 20, 5>(c, A, st);
+    default: return launch_pipe_cfg<COUNT, 24, 5>(c, A, st);
     }
 }
 
