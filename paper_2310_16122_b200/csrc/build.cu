@@ -26,7 +26,7 @@ struct SoA {
 };
 
 __global__ void k_keys(int64_t n, SoA in, float inv_q, int cs, int fbits, uint32_t* keys, int32_t* idx,
-                       float4* rec) {
+                       float4* rec, int32_t* ccount) {
     const int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
     if (i >= n) return;
     const float x = in.f[0][i], y = in.f[1][i], z = in.f[2][i];
@@ -41,6 +41,106 @@ __global__ void k_keys(int64_t n, SoA in, float inv_q, int cs, int fbits, uint32
     const uint64_t fm = morton3((xi & msk) >> sh, (yi & msk) >> sh, (zi & msk) >> sh);
     keys[i] = (uint32_t)((cm << (3 * fbits)) | fm);
     idx[i] = (int32_t)i;
+    // cell histogram, one atomic per run of equal cells in the warp (sorted inputs: ~1 per warp)
+    const unsigned same = __match_any_sync(__activemask(), (uint32_t)cm);
+    if ((threadIdx.x & 31) == __ffs(same) - 1) atomicAdd(ccount + cm, __popc(same));
+}
+
+// counting sort by cell: each particle's slot in its cell's range (order within a cell arbitrary;
+// the per-cell sort by the in-cell key and the id tie fix make the order total, O3)
+__global__ void k_cell_scatter(int64_t n, const uint32_t* __restrict__ keys, int fbits, const int32_t* __restrict__ coff,
+                               int32_t* cursor, uint32_t* keys_out, int32_t* idx_out) {
+    const int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+    if (i >= n) return;
+    const uint32_t key = keys[i];
+    const uint32_t cell = key >> (3 * fbits);
+    const unsigned same = __match_any_sync(__activemask(), cell);
+    const int lane = threadIdx.x & 31, leader = __ffs(same) - 1;
+    int base = 0;
+    if (lane == leader) base = atomicAdd(cursor + cell, __popc(same));
+    base = __shfl_sync(same, base, leader);
+    const int pos = coff[cell] + base + __popc(same & ((1u << lane) - 1u));
+    keys_out[pos] = key;
+    idx_out[pos] = (int32_t)i;
+}
+
+// lanes holding the same 6-bit digit (65 for none): the classic multisplit from 7 ballots
+__device__ __forceinline__ unsigned same_digit_lanes(uint32_t d) {
+    unsigned m = __ballot_sync(0xffffffffu, d < 64u);
+    m = d < 64u ? m : ~m;
+#pragma unroll
+    for (int b = 0; b < 6; ++b) {
+        const unsigned q = __ballot_sync(0xffffffffu, (d >> b) & 1u);
+        m &= ((d >> b) & 1u) ? q : ~q;
+    }
+    return m;
+}
+// per-cell sort of the cell-scattered keys by their in-cell bits (3 fbits): one warp per cell, an LSD
+// radix sort in shared memory, 6 bits per pass, each pass stable (ranks from ballots in input
+// order); equal keys keep the scatter's order and k_tie_fix then orders them by id (O3).
+// Cells of more than CELL_SORT_MAX particles get a segment in (beg, end) for CUB's segmented sort
+// (clustered inputs), the others an empty one.
+constexpr int CELL_SORT_MAX = 256;
+__global__ void __launch_bounds__(256) k_cell_sort(int64_t ncm, int fine_bits, const int32_t* __restrict__ coff,
+                                                   const uint32_t* __restrict__ keys_in, const int32_t* __restrict__ idx_in,
+                                                   uint32_t* keys_out, int32_t* idx_out, int32_t* beg, int32_t* end) {
+    __shared__ uint2 s[8][2][CELL_SORT_MAX];  // (key, index), double buffer
+    __shared__ int cnt[8][64];
+    const int w = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    const unsigned below = (1u << lane) - 1u;
+    const int64_t c = blockIdx.x * 8 + w;
+    if (c >= ncm) return;
+    const int o = coff[c], nc = coff[c + 1] - o;
+    const bool big = nc > CELL_SORT_MAX;
+    if (lane == 0) {
+        beg[c] = big ? o : 0;
+        end[c] = big ? o + nc : 0;
+    }
+    if (big || nc == 0) return;
+    uint2* src = s[w][0];
+    uint2* dst = s[w][1];
+    for (int t = lane; t < nc; t += 32) src[t] = make_uint2(keys_in[o + t], (uint32_t)idx_in[o + t]);
+    __syncwarp();
+    for (int sh = 0; sh < fine_bits; sh += 6) {
+        cnt[w][lane] = 0;
+        cnt[w][lane + 32] = 0;
+        __syncwarp();
+        for (int t0 = 0; t0 < nc; t0 += 32) {  // histogram
+            const int t = t0 + lane;
+            const uint32_t d = t < nc ? (src[t].x >> sh) & 63u : 64u;
+            if (d < 64u) atomicAdd(&cnt[w][d], 1);
+        }
+        __syncwarp();
+        // exclusive scan of the 64 counts (two per lane)
+        const int c0 = cnt[w][2 * lane], c1 = cnt[w][2 * lane + 1];
+        int x = c0 + c1;
+#pragma unroll
+        for (int d = 1; d < 32; d <<= 1) {
+            const int y = __shfl_up_sync(0xffffffffu, x, d);
+            if (lane >= d) x += y;
+        }
+        __syncwarp();
+        cnt[w][2 * lane] = x - c0 - c1;
+        cnt[w][2 * lane + 1] = x - c1;
+        __syncwarp();
+        for (int t0 = 0; t0 < nc; t0 += 32) {  // stable scatter
+            const int t = t0 + lane;
+            const uint2 v = t < nc ? src[t] : make_uint2(0u, 0u);
+            const uint32_t d = t < nc ? (v.x >> sh) & 63u : 64u;
+            const unsigned same = same_digit_lanes(d);
+            const int base = d < 64u ? cnt[w][d] : 0;
+            if (d < 64u) dst[base + __popc(same & below)] = v;
+            __syncwarp();
+            if (d < 64u && lane == __ffs(same) - 1) cnt[w][d] = base + __popc(same);
+            __syncwarp();
+        }
+        uint2* tsw = src; src = dst; dst = tsw;
+    }
+    for (int t = lane; t < nc; t += 32) {
+        const uint2 v = src[t];
+        keys_out[o + t] = v.x;
+        idx_out[o + t] = (int32_t)v.y;
+    }
 }
 
 // Runs of equal keys (coincident to 1/2^fbits of a cell) are ordered by id: total order (O3).
@@ -716,13 +816,18 @@ crk_status build_lists(crk_ctx* c, crk_particles* p, cudaStream_t st) {
     in.sp = p->species;
     in.id = p->id;
     float4* rec = P<float4>(c->scratch);
+    // counting sort by cell, then a segmented sort of every cell by its in-cell key (the leaf-count
+    // buffer, written later, holds the cell histogram and offsets meanwhile)
+    int32_t* ccount = P<int32_t>(c->leaf_cnt);
+    int32_t* coff = ccount + (L.ncm + 1);
+    CRK_TRY(cuda_check(c, zero_async(ccount, (L.ncm + 1) * 4, st, c), "memset"));
     k_keys<<<nblk(n, 256), 256, 0, st>>>(n, in, L.inv_q, L.cs, L.fbits, P<uint32_t>(c->keys_a), P<int32_t>(c->idx_a),
-                                         rec);
+                                         rec, ccount);
     CRK_LAUNCHED(c, "keys");
-    cub::DoubleBuffer<uint32_t> dk(P<uint32_t>(c->keys_a), P<uint32_t>(c->keys_b));
-    cub::DoubleBuffer<int32_t> dv(P<int32_t>(c->idx_a), P<int32_t>(c->idx_b));
     size_t tmp = 0;
-    cub::DeviceRadixSort::SortPairs(nullptr, tmp, dk, dv, (int)n, 0, bits, st);
+    cub::DeviceSegmentedSort::SortPairs(nullptr, tmp, P<uint32_t>(c->keys_b), P<uint32_t>(c->keys_a),
+                                        P<int32_t>(c->idx_b), P<int32_t>(c->idx_a), (int)n, (int)L.ncm, coff, coff + 1,
+                                        st);
     size_t tmp2 = 0;
     cub::DeviceScan::ExclusiveSum(nullptr, tmp2, P<int32_t>(c->gflag), P<int32_t>(c->grank), (int)(n + 1), st);
     size_t tmp3 = 0;
@@ -732,10 +837,30 @@ crk_status build_lists(crk_ctx* c, crk_particles* p, cudaStream_t st) {
     need = need > (size_t)(n + 1) * 4 ? need : (size_t)(n + 1) * 4;
     CRK_TRY(grow(c, c->cub_tmp, need, st));
     tmp = c->cub_tmp.cap;
-    CRK_TRY(cuda_check(c, cub::DeviceRadixSort::SortPairs(c->cub_tmp.p, tmp, dk, dv, (int)n, 0, bits, st), "radix sort"));
-    c->launches += 2 + (bits + 7) / 8;  // histogram, scan, one onesweep pass per 8 bits
-    const uint32_t* keys = dk.Current();
-    int32_t* perm = dv.Current();
+    CRK_TRY(cuda_check(c, cub::DeviceScan::ExclusiveSum(c->cub_tmp.p, tmp, ccount, coff, (int)(L.ncm + 1), st),
+                       "cell scan"));
+    c->launches += 2;
+    CRK_TRY(cuda_check(c, zero_async(c->cell_end.p, L.ncm * 4, st, c), "memset"));  // the scatter's cursors
+    k_cell_scatter<<<nblk(n, 256), 256, 0, st>>>(n, P<uint32_t>(c->keys_a), L.fbits, coff, P<int32_t>(c->cell_end),
+                                                 P<uint32_t>(c->keys_b), P<int32_t>(c->idx_b));
+    CRK_LAUNCHED(c, "cell scatter");
+    // cells up to CELL_SORT_MAX particles: one warp each (radix by the in-cell bits); larger ones
+    // (clustered inputs): CUB's segmented
+    // sort over (beg, end) segments, empty for the small cells
+    int32_t* beg = ccount;  // the histogram is consumed
+    int32_t* end = ccount + 2 * (L.ncm + 1);
+    k_cell_sort<<<nblk(L.ncm, 8), 256, 0, st>>>(L.ncm, 3 * L.fbits, coff, P<uint32_t>(c->keys_b), P<int32_t>(c->idx_b),
+                                                P<uint32_t>(c->keys_a), P<int32_t>(c->idx_a), beg, end);
+    CRK_LAUNCHED(c, "cell sort");
+    tmp = c->cub_tmp.cap;
+    CRK_TRY(cuda_check(c, cub::DeviceSegmentedSort::SortPairs(c->cub_tmp.p, tmp, P<uint32_t>(c->keys_b),
+                                                              P<uint32_t>(c->keys_a), P<int32_t>(c->idx_b),
+                                                              P<int32_t>(c->idx_a), (int)n, (int)L.ncm, beg, end,
+                                                              st), "segmented sort (large cells)"));
+    c->launches += 3;
+    (void)bits;
+    const uint32_t* keys = P<uint32_t>(c->keys_a);
+    int32_t* perm = P<int32_t>(c->idx_a);
     k_tie_fix<<<nblk(n, 256), 256, 0, st>>>(n, keys, perm, p->id);
     CRK_LAUNCHED(c, "tie fix");
 
