@@ -83,7 +83,8 @@ __device__ __forceinline__ unsigned same_digit_lanes(uint32_t d) {
 constexpr int CELL_SORT_MAX = 256;
 __global__ void __launch_bounds__(256) k_cell_sort(int64_t ncm, int fine_bits, const int32_t* __restrict__ coff,
                                                    const uint32_t* __restrict__ keys_in, const int32_t* __restrict__ idx_in,
-                                                   uint32_t* keys_out, int32_t* idx_out, int32_t* beg, int32_t* end) {
+                                                   uint32_t* keys_out, int32_t* idx_out, int32_t* beg, int32_t* end,
+                                                   int* nbig) {
     __shared__ uint2 s[8][2][CELL_SORT_MAX];  // (key, index), double buffer
     __shared__ int cnt[8][64];
     const int w = threadIdx.x >> 5, lane = threadIdx.x & 31;
@@ -95,6 +96,7 @@ __global__ void __launch_bounds__(256) k_cell_sort(int64_t ncm, int fine_bits, c
     if (lane == 0) {
         beg[c] = big ? o : 0;
         end[c] = big ? o + nc : 0;
+        if (big) atomicAdd(nbig, 1);
     }
     if (big || nc == 0) return;
     uint2* src = s[w][0];
@@ -849,15 +851,27 @@ crk_status build_lists(crk_ctx* c, crk_particles* p, cudaStream_t st) {
     // sort over (beg, end) segments, empty for the small cells
     int32_t* beg = ccount;  // the histogram is consumed
     int32_t* end = ccount + 2 * (L.ncm + 1);
+    CRK_TRY(grow(c, c->work, 64, st));
+    int* nbig = P<int>(c->work) + 12;
+    CRK_TRY(cuda_check(c, zero_async(nbig, 4, st, c), "memset"));
     k_cell_sort<<<nblk(L.ncm, 8), 256, 0, st>>>(L.ncm, 3 * L.fbits, coff, P<uint32_t>(c->keys_b), P<int32_t>(c->idx_b),
-                                                P<uint32_t>(c->keys_a), P<int32_t>(c->idx_a), beg, end);
+                                                P<uint32_t>(c->keys_a), P<int32_t>(c->idx_a), beg, end, nbig);
     CRK_LAUNCHED(c, "cell sort");
-    tmp = c->cub_tmp.cap;
-    CRK_TRY(cuda_check(c, cub::DeviceSegmentedSort::SortPairs(c->cub_tmp.p, tmp, P<uint32_t>(c->keys_b),
-                                                              P<uint32_t>(c->keys_a), P<int32_t>(c->idx_b),
-                                                              P<int32_t>(c->idx_a), (int)n, (int)L.ncm, beg, end,
-                                                              st), "segmented sort (large cells)"));
-    c->launches += 3;
+    {  // CUB's segmented sort only when some cell is large: it reads partition sizes back with a
+       // copy-engine transfer, which would queue behind the caller's bulk copies
+        Readback rb;
+        rb.add(nbig, 64, 4);
+        CRK_TRY(readback(c, rb, st));
+        CRK_TRY(cuda_check(c, cudaStreamSynchronize(st), "sync"));
+        if (reinterpret_cast<volatile int32_t*>(P<char>(c->pinned))[16] > 0) {
+            tmp = c->cub_tmp.cap;
+            CRK_TRY(cuda_check(c, cub::DeviceSegmentedSort::SortPairs(c->cub_tmp.p, tmp, P<uint32_t>(c->keys_b),
+                                                                      P<uint32_t>(c->keys_a), P<int32_t>(c->idx_b),
+                                                                      P<int32_t>(c->idx_a), (int)n, (int)L.ncm, beg,
+                                                                      end, st), "segmented sort (large cells)"));
+            c->launches += 3;
+        }
+    }
     (void)bits;
     const uint32_t* keys = P<uint32_t>(c->keys_a);
     int32_t* perm = P<int32_t>(c->idx_a);
