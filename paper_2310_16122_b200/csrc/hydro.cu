@@ -236,17 +236,17 @@ struct CorPass : HydCommon {
     float *A, *B, *dA, *dB;  // caller planes (n)
     int64_t n;
     struct I { float x, y, z, H2, invH; };
+    // moments, paired for packed FP32 (components named by their d indices):
+    //   m1: (0, 1), 2;  m2: (00, 01), (02, 12), 11, 22;  likewise g0, g1;
+    //   g2: (000, 001), (002, 012), (022, 122), 011, 111, 112, 222
     struct Acc {
-        float m0, m1[3], m2[6], g0[3], g1[6], g2[10];
+        float m0, m1_2, g0_2, m2_11, m2_22, g1_11, g1_22, g2_011, g2_111, g2_112, g2_222;
+        float2 m1_01, m2_a, m2_b, g0_01, g1_a, g1_b, g2_a, g2_b, g2_c;
     };
     __device__ void init(Acc& a) const {
-        a.m0 = 0.f;
-#pragma unroll
-        for (int t = 0; t < 3; ++t) a.m1[t] = a.g0[t] = 0.f;
-#pragma unroll
-        for (int t = 0; t < 6; ++t) a.m2[t] = a.g1[t] = 0.f;
-#pragma unroll
-        for (int t = 0; t < 10; ++t) a.g2[t] = 0.f;
+        a.m0 = a.m1_2 = a.g0_2 = a.m2_11 = a.m2_22 = a.g1_11 = a.g1_22 = 0.f;
+        a.g2_011 = a.g2_111 = a.g2_112 = a.g2_222 = 0.f;
+        a.m1_01 = a.m2_a = a.m2_b = a.g0_01 = a.g1_a = a.g1_b = a.g2_a = a.g2_b = a.g2_c = make_float2(0.f, 0.f);
     }
     __device__ void load_i(int k, I& s) const { load_pos(gpos, k, s.x, s.y, s.z, s.H2, s.invH); }
     __device__ float ix(const I& s) const { return s.x; }
@@ -255,44 +255,52 @@ struct CorPass : HydCommon {
     __device__ float cut(const I& s) const { return s.H2; }
     __device__ float jcut(const float4&) const { return 0.f; }
     __device__ __forceinline__ void pair(const I& s, Acc& a, const float4& jp, const float4*, int) const {
-        const float d0 = jp.x - s.x, d1 = jp.y - s.y, d2 = jp.z - s.z;
-        const float r2 = s32_of(d0, d1, d2);
+        const float2 d01 = __fadd2_rn(make_float2(jp.x, jp.y), make_float2(-s.x, -s.y));  // d = x_j - x_i
+        const float d2 = jp.z - s.z;
+        const float r2 = s32_of(d01.x, d01.y, d2);
         float wt, gt;
         wendland_t(r2, s.invH, wt, gt);
         const bool in = r2 < s.H2;
-        const float w = in ? jp.w * wt : 0.f;
-        const float gw = in ? jp.w * gt : 0.f;  // (times 1/H^2 in finish)
-        const float wd0 = w * d0, wd1 = w * d1, wd2 = w * d2;
+        const float2 wg = __fmul2_rn(make_float2(jp.w, jp.w), make_float2(wt, gt));
+        const float w = in ? wg.x : 0.f;
+        const float gw = in ? wg.y : 0.f;  // (times 1/H^2 in finish)
+        const float2 wd01 = __fmul2_rn(make_float2(w, w), d01);
+        const float wd2 = w * d2;
         a.m0 += w;
-        a.m1[0] += wd0; a.m1[1] += wd1; a.m1[2] += wd2;
-        a.m2[0] = fmaf(wd0, d0, a.m2[0]); a.m2[1] = fmaf(wd0, d1, a.m2[1]); a.m2[2] = fmaf(wd0, d2, a.m2[2]);
-        a.m2[3] = fmaf(wd1, d1, a.m2[3]); a.m2[4] = fmaf(wd1, d2, a.m2[4]); a.m2[5] = fmaf(wd2, d2, a.m2[5]);
-        const float gd0 = gw * d0, gd1 = gw * d1, gd2 = gw * d2;
-        a.g0[0] += gd0; a.g0[1] += gd1; a.g0[2] += gd2;
-        a.g1[0] = fmaf(gd0, d0, a.g1[0]); a.g1[1] = fmaf(gd0, d1, a.g1[1]); a.g1[2] = fmaf(gd0, d2, a.g1[2]);
-        a.g1[3] = fmaf(gd1, d1, a.g1[3]); a.g1[4] = fmaf(gd1, d2, a.g1[4]); a.g1[5] = fmaf(gd2, d2, a.g1[5]);
-        const float e00 = gd0 * d0, e01 = gd0 * d1, e11 = gd1 * d1;
-        // fully symmetric third moment d_a d_b d_g gw: index set 000,001,002,011,012,022,111,112,122,222
-        a.g2[0] = fmaf(e00, d0, a.g2[0]);
-        a.g2[1] = fmaf(e00, d1, a.g2[1]);
-        a.g2[2] = fmaf(e00, d2, a.g2[2]);
-        a.g2[3] = fmaf(e01, d1, a.g2[3]);
-        a.g2[4] = fmaf(e01, d2, a.g2[4]);
-        a.g2[5] = fmaf(gd0 * d2, d2, a.g2[5]);
-        a.g2[6] = fmaf(e11, d1, a.g2[6]);
-        a.g2[7] = fmaf(e11, d2, a.g2[7]);
-        a.g2[8] = fmaf(gd1 * d2, d2, a.g2[8]);
-        a.g2[9] = fmaf(gd2 * d2, d2, a.g2[9]);
+        a.m1_01 = __fadd2_rn(a.m1_01, wd01);
+        a.m1_2 += wd2;
+        a.m2_a = __ffma2_rn(make_float2(wd01.x, wd01.x), d01, a.m2_a);  // (00, 01)
+        a.m2_b = __ffma2_rn(make_float2(wd2, wd2), d01, a.m2_b);        // (02, 12)
+        a.m2_11 = fmaf(wd01.y, d01.y, a.m2_11);
+        a.m2_22 = fmaf(wd2, d2, a.m2_22);
+        const float2 gd01 = __fmul2_rn(make_float2(gw, gw), d01);
+        const float gd2 = gw * d2;
+        a.g0_01 = __fadd2_rn(a.g0_01, gd01);
+        a.g0_2 += gd2;
+        a.g1_a = __ffma2_rn(make_float2(gd01.x, gd01.x), d01, a.g1_a);
+        a.g1_b = __ffma2_rn(make_float2(gd2, gd2), d01, a.g1_b);
+        a.g1_11 = fmaf(gd01.y, d01.y, a.g1_11);
+        a.g1_22 = fmaf(gd2, d2, a.g1_22);
+        // fully symmetric third moment d_a d_b d_g gw
+        const float2 e = __fmul2_rn(make_float2(gd01.x, gd01.x), d01);          // (e00, e01)
+        a.g2_a = __ffma2_rn(make_float2(e.x, e.x), d01, a.g2_a);                // (000, 001)
+        a.g2_b = __ffma2_rn(make_float2(d2, d2), e, a.g2_b);                    // (002, 012)
+        a.g2_011 = fmaf(e.y, d01.y, a.g2_011);
+        const float2 f = __fmul2_rn(gd01, make_float2(d2, d2));                 // (gd0 d2, gd1 d2)
+        a.g2_c = __ffma2_rn(make_float2(d2, d2), f, a.g2_c);                    // (022, 122)
+        const float e11 = gd01.y * d01.y;
+        a.g2_111 = fmaf(e11, d01.y, a.g2_111);
+        a.g2_112 = fmaf(e11, d2, a.g2_112);
+        a.g2_222 = fmaf(gd2 * d2, d2, a.g2_222);
     }
     template <int GG>
     __device__ void reduce(Acc& a) const {
-        a.m0 = slot_sum<GG>(a.m0);
+        float* p[11] = {&a.m0, &a.m1_2, &a.g0_2, &a.m2_11, &a.m2_22, &a.g1_11, &a.g1_22, &a.g2_011, &a.g2_111, &a.g2_112, &a.g2_222};
 #pragma unroll
-        for (int t = 0; t < 3; ++t) { a.m1[t] = slot_sum<GG>(a.m1[t]); a.g0[t] = slot_sum<GG>(a.g0[t]); }
+        for (int t = 0; t < 11; ++t) *p[t] = slot_sum<GG>(*p[t]);
+        float2* q[9] = {&a.m1_01, &a.m2_a, &a.m2_b, &a.g0_01, &a.g1_a, &a.g1_b, &a.g2_a, &a.g2_b, &a.g2_c};
 #pragma unroll
-        for (int t = 0; t < 6; ++t) { a.m2[t] = slot_sum<GG>(a.m2[t]); a.g1[t] = slot_sum<GG>(a.g1[t]); }
-#pragma unroll
-        for (int t = 0; t < 10; ++t) a.g2[t] = slot_sum<GG>(a.g2[t]);
+        for (int t = 0; t < 9; ++t) { q[t]->x = slot_sum<GG>(q[t]->x); q[t]->y = slot_sum<GG>(q[t]->y); }
     }
     __device__ static int s2(int a, int b) {  // symmetric 3x3 index
         if (a > b) { int t = a; a = b; b = t; }
@@ -311,7 +319,14 @@ struct CorPass : HydCommon {
     }
     __device__ void finish(int k, const I& s, const Acc& a) const {
         float Ai, Bi[3], dAi[3], dBi[3][3];
-        cor_coefficients(s.invH, a.m0, a.m1, a.m2, a.g0, a.g1, a.g2, Ai, Bi, dAi, dBi);
+        // canonical index sets: m2 / g1 {00, 01, 02, 11, 12, 22}, g2 {000, 001, 002, 011, 012, 022, 111, 112, 122, 222}
+        const float m1[3] = {a.m1_01.x, a.m1_01.y, a.m1_2};
+        const float m2[6] = {a.m2_a.x, a.m2_a.y, a.m2_b.x, a.m2_11, a.m2_b.y, a.m2_22};
+        const float g0[3] = {a.g0_01.x, a.g0_01.y, a.g0_2};
+        const float g1[6] = {a.g1_a.x, a.g1_a.y, a.g1_b.x, a.g1_11, a.g1_b.y, a.g1_22};
+        const float g2[10] = {a.g2_a.x, a.g2_a.y, a.g2_b.x, a.g2_011, a.g2_b.y, a.g2_c.x, a.g2_111, a.g2_112, a.g2_c.y,
+                              a.g2_222};
+        cor_coefficients(s.invH, a.m0, m1, m2, g0, g1, g2, Ai, Bi, dAi, dBi);
         float vals[16];
         vals[0] = Ai;
 #pragma unroll
