@@ -398,11 +398,13 @@ struct ExtPass : HydCommon {
         float A, B[3], dA[3], dB[9];
         float vx, vy, vz;
     };
-    struct Acc { float rho, g[9]; };
+    // grad v sums g[3a + b] (a: velocity component, b: derivative) paired over b = 0, 1:
+    // g01[a] = (g[3a], g[3a + 1]), g2[a] = g[3a + 2]
+    struct Acc { float rho, g2[3]; float2 g01[3]; };
     __device__ void init(Acc& a) const {
         a.rho = 0.f;
 #pragma unroll
-        for (int t = 0; t < 9; ++t) a.g[t] = 0.f;
+        for (int t = 0; t < 3; ++t) { a.g2[t] = 0.f; a.g01[t] = make_float2(0.f, 0.f); }
     }
     __device__ void load_i(int k, I& s) const {
         load_pos(gpos, k, s.x, s.y, s.z, s.H2, s.invH);
@@ -421,38 +423,48 @@ struct ExtPass : HydCommon {
     __device__ float jcut(const float4&) const { return 0.f; }
     __device__ __forceinline__ void pair(const I& s, Acc& a, const float4& jp, const float4* pay, int) const {
         // x_ij = x_i - x_j
-        const float x0 = s.x - jp.x, x1 = s.y - jp.y, x2 = s.z - jp.z;
-        const float r2 = s32_of(x0, x1, x2);
+        const float2 x01 = __fadd2_rn(make_float2(s.x, s.y), make_float2(-jp.x, -jp.y));
+        const float x2 = s.z - jp.z;
+        const float r2 = s32_of(x01.x, x01.y, x2);
         const bool in = r2 < s.H2;  // branch-free: out-of-range pairs add exact zeros
         float wt, gt;
         wendland_t(r2, s.invH, wt, gt);
         wt = in ? wt : 0.f;
         gt = in ? gt * (s.invH * s.invH) : 0.f;
-        const float lin = 1.f + s.B[0] * x0 + s.B[1] * x1 + s.B[2] * x2;
+        const float lin = fmaf(s.B[2], x2, fmaf(s.B[1], x01.y, fmaf(s.B[0], x01.x, 1.f)));
         const float4 vj = pay[0];
         a.rho = fmaf(vj.w, s.A * lin * wt, a.rho);
         const float alg = s.A * lin * gt;
-        float gw[3];
-#pragma unroll
-        for (int g = 0; g < 3; ++g) {
-            const float t1 = s.dB[g] * x0 + s.dB[3 + g] * x1 + s.dB[6 + g] * x2 + s.B[g];
-            const float xg = g == 0 ? x0 : (g == 1 ? x1 : x2);
-            gw[g] = wt * (s.dA[g] * lin + s.A * t1) + alg * xg;
-        }
+        // t1_g = sum_p dB[3p + g] x_p + B_g, packed over g = 0, 1
+        const float2 t01 = __ffma2_rn(make_float2(s.dB[6], s.dB[7]), make_float2(x2, x2),
+                                      __ffma2_rn(make_float2(s.dB[3], s.dB[4]), make_float2(x01.y, x01.y),
+                                                 __ffma2_rn(make_float2(s.dB[0], s.dB[1]), make_float2(x01.x, x01.x),
+                                                            make_float2(s.B[0], s.B[1]))));
+        const float t2 = fmaf(s.dB[8], x2, fmaf(s.dB[5], x01.y, fmaf(s.dB[2], x01.x, s.B[2])));
+        // gw_g = wt (dA_g lin + A t1_g) + alg x_g
+        const float2 gw01 = __ffma2_rn(make_float2(alg, alg), x01,
+                                       __fmul2_rn(make_float2(wt, wt),
+                                                  __ffma2_rn(make_float2(s.dA[0], s.dA[1]), make_float2(lin, lin),
+                                                             __fmul2_rn(make_float2(s.A, s.A), t01))));
+        const float gw2 = fmaf(alg, x2, wt * fmaf(s.dA[2], lin, s.A * t2));
         const float Vj = jp.w;
-        const float e0 = Vj * (vj.x - s.vx), e1 = Vj * (vj.y - s.vy), e2 = Vj * (vj.z - s.vz);
+        const float2 e01 = __fmul2_rn(make_float2(Vj, Vj), __fadd2_rn(make_float2(vj.x, vj.y), make_float2(-s.vx, -s.vy)));
+        const float e[3] = {e01.x, e01.y, Vj * (vj.z - s.vz)};
 #pragma unroll
-        for (int b = 0; b < 3; ++b) {
-            a.g[b] = fmaf(e0, gw[b], a.g[b]);
-            a.g[3 + b] = fmaf(e1, gw[b], a.g[3 + b]);
-            a.g[6 + b] = fmaf(e2, gw[b], a.g[6 + b]);
+        for (int c = 0; c < 3; ++c) {
+            a.g01[c] = __ffma2_rn(make_float2(e[c], e[c]), gw01, a.g01[c]);
+            a.g2[c] = fmaf(e[c], gw2, a.g2[c]);
         }
     }
     template <int GG>
     __device__ void reduce(Acc& a) const {
         a.rho = slot_sum<GG>(a.rho);
 #pragma unroll
-        for (int t = 0; t < 9; ++t) a.g[t] = slot_sum<GG>(a.g[t]);
+        for (int t = 0; t < 3; ++t) {
+            a.g2[t] = slot_sum<GG>(a.g2[t]);
+            a.g01[t].x = slot_sum<GG>(a.g01[t].x);
+            a.g01[t].y = slot_sum<GG>(a.g01[t].y);
+        }
     }
     __device__ void finish(int k, const I& s, const Acc& a) const {
         const float c = SIGMA_W * s.invH * s.invH * s.invH;
@@ -462,7 +474,11 @@ struct ExtPass : HydCommon {
         const float ck = sqrtf(gamma * Pk / r);
         float g[9];
 #pragma unroll
-        for (int t = 0; t < 9; ++t) g[t] = c * a.g[t];
+        for (int t = 0; t < 3; ++t) {
+            g[3 * t] = c * a.g01[t].x;
+            g[3 * t + 1] = c * a.g01[t].y;
+            g[3 * t + 2] = c * a.g2[t];
+        }
         const float V = gV[k];
         const float4 vm = gvel[k];
         const float dAh[3] = {c * s.dA[0], c * s.dA[1], c * s.dA[2]};
