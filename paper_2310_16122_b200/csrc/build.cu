@@ -696,16 +696,11 @@ __global__ void __launch_bounds__(256, 5) k_entry_masks(int64_t na, const int32_
     if (a >= na) return;
     const int f0 = ifirst[a], cnt = icount[a];
     const int p0 = rowoff[a], pend = rowend[a];
-    // the first entry's record and box are requested before the group boxes are reduced
-    int2 r;
-    float4 bl, bh;
-    auto load1 = [&](int q) {
-        r = q < pend ? erec[q] : make_int2(0, 0);
-        const int64_t b = r.y & 0x03ffffff;
-        bl = box8[2 * b];
-        bh = box8[2 * b + 1];
-    };
-    load1(p0 + lane);
+    // two-stage prefetch: the record two iterations ahead, the box of the next entry (whose record
+    // landed an iteration ago) — the record -> box dependency is off the loop's critical path
+    auto rec = [&](int q) { return q < pend ? erec[q] : make_int2(0, 0); };
+    int2 r = rec(p0 + lane), rn = rec(p0 + lane + 32);
+    float4 bl = box8[2 * (int64_t)(r.y & 0x03ffffff)], bh = box8[2 * (int64_t)(r.y & 0x03ffffff) + 1];
     group_boxes(xm, f0, cnt, s_gb[w], lane);  // empty groups: lo = +inf, hi = -inf (never in reach)
     if (lane < 12) {
         const int d = lane / 4, t = lane % 4;
@@ -718,7 +713,11 @@ __global__ void __launch_bounds__(256, 5) k_entry_masks(int64_t na, const int32_
     for (int q = p0 + lane; q < pend; q += 32) {
         const int2 rc = r;
         const float4 lc = bl, hc = bh;
-        load1(q + 32);
+        const int2 rnn = rec(q + 64);
+        bl = box8[2 * (int64_t)(rn.y & 0x03ffffff)];
+        bh = box8[2 * (int64_t)(rn.y & 0x03ffffff) + 1];
+        r = rn;
+        rn = rnn;
         const float4 of = s_off[(unsigned)rc.y >> 26];
         const float lo[3] = {lc.x + of.x, lc.y + of.y, lc.z + of.z};  // exact (O1)
         const float hi[3] = {hc.x + of.x, hc.y + of.y, hc.z + of.z};
