@@ -136,6 +136,11 @@ struct GravSymArgs {
     float wcut;          // rcut2 * CULL_SLACK (the culls' bound, a kernel parameter so that it stays a constant operand)
     float c0, c1, c2, c3, c4, c5;
     float nc[6];         // -c0 .. -c5 (read straight from the parameter bank in the packed Horner chain)
+    // the pipelined kernel's force evaluation in t = s + eps2 (one packed add less per pair, DESIGN.md §2 O5g):
+    // -P5(t - eps2) = sum_m ne[m] t^m (coefficients re-expanded in double on the host) and the cutoff
+    // t < rce = fl(rcut2 + eps2)
+    float ne[6];
+    float rce;
     // domain decomposition (grav_pipe_kernel): a particle is owned iff its cell
     // (x / q) >> cs lies in [dlo, dhi) on every axis; ghosts have no i-groups here
     bool partial;
@@ -439,7 +444,7 @@ __global__ void __launch_bounds__(symw::NW * 32, 16 / symw::NW) grav_warp_kernel
         const int ng = min(G, icount - ibase);
         const int rbeg = __ldg(A.row_off + a), rend = __ldg(A.row_end + a);
 
-        float lo[3], hi[3];
+        float lo[3], hi[3];  // the group's box (nlh: (-lo, -hi) per axis, packed for the particle cull)
         {
             const bool iv = lane < ng;
             float4 p = make_float4(-1e18f, -1e18f, -1e18f, 0.f);  // far sentinel: finite products
@@ -650,7 +655,7 @@ __global__ void __launch_bounds__(symh::NW * 32, 16 / symh::NW) grav_halfwarp_ke
             iidx = gself + lane;
             ip = __ldg(A.xm + iidx);
         }
-        float lo[3], hi[3];
+        float lo[3], hi[3];  // the group's box (nlh: (-lo, -hi) per axis, packed for the particle cull)
         {
             const bool iv = iidx >= 0;
             lo[0] = warp_min(iv ? ip.x : INFINITY);
@@ -842,7 +847,7 @@ __global__ void __launch_bounds__(symp::NW * 32, MINB) grav_pipe_kernel(const Gr
             return n;
         };
 
-        float lo[3], hi[3];
+        float lo[3], hi[3];  // the group's box (nlh: (-lo, -hi) per axis, packed for the particle cull)
         {
             const bool iv = lane < ng;
             float4 p = make_float4(-1e18f, -1e18f, -1e18f, 0.f);
@@ -861,6 +866,7 @@ __global__ void __launch_bounds__(symp::NW * 32, MINB) grav_pipe_kernel(const Gr
             hi[1] = warp_max(iv ? p.y : -INFINITY);
             hi[2] = warp_max(iv ? p.z : -INFINITY);
         }
+        const float2 nlh[3] = {make_float2(-lo[0], -hi[0]), make_float2(-lo[1], -hi[1]), make_float2(-lo[2], -hi[2])};
         int n0 = issue_chunk(0), n1 = issue_chunk(1), n2 = 0;  // entries of chunks c, c + 1, c + 2
 
         // chunk entries landed in ec[buf]: shift offsets and the lane's leaf's particle copies
@@ -921,27 +927,28 @@ __global__ void __launch_bounds__(symp::NW * 32, MINB) grav_pipe_kernel(const Gr
             } else {
                 const float mj = jown ? 0.f : jp.w;
                 const float2 mj2 = make_float2(mj, mj), e22 = make_float2(e2, e2);
-                const float2 n0 = make_float2(A.nc[0], A.nc[0]), n1 = make_float2(A.nc[1], A.nc[1]);
-                const float2 n2 = make_float2(A.nc[2], A.nc[2]), n3 = make_float2(A.nc[3], A.nc[3]);
-                const float2 n4 = make_float2(A.nc[4], A.nc[4]), n5 = make_float2(A.nc[5], A.nc[5]);
+                const float2 n0 = make_float2(A.ne[0], A.ne[0]), n1 = make_float2(A.ne[1], A.ne[1]);
+                const float2 n2 = make_float2(A.ne[2], A.ne[2]), n3 = make_float2(A.ne[3], A.ne[3]);
+                const float2 n4 = make_float2(A.ne[4], A.ne[4]), n5 = make_float2(A.ne[5], A.ne[5]);
+                const float rce = A.rce;
                 float2 bx = make_float2(0.f, 0.f), by = bx, bz = bx;
 #pragma unroll
                 for (int k = 0; k < G / 2; ++k) {
                     const float2 dx = __fadd2_rn(jx, S.inx[k]);  // x_j - x_i, exact (O1)
                     const float2 dy = __fadd2_rn(jy, S.iny[k]);
                     const float2 dz = __fadd2_rn(jz, S.inz[k]);
-                    const float2 r2 = __ffma2_rn(dz, dz, __ffma2_rn(dy, dy, __fmul2_rn(dx, dx)));  // O2 order
-                    const float2 re = __fadd2_rn(r2, e22);
+                    // t = s + eps2, accumulated from eps2 (the force's cutoff t < rce; see ne, rce)
+                    const float2 re = __ffma2_rn(dz, dz, __ffma2_rn(dy, dy, __ffma2_rn(dx, dx, e22)));
                     const float2 ri = make_float2(rsqrtf(re.x), rsqrtf(re.y));
                     const float2 ri2 = __fmul2_rn(ri, ri);
-                    float2 np5 = __ffma2_rn(n5, r2, n4);  // -P5(s)
-                    np5 = __ffma2_rn(np5, r2, n3);
-                    np5 = __ffma2_rn(np5, r2, n2);
-                    np5 = __ffma2_rn(np5, r2, n1);
-                    np5 = __ffma2_rn(np5, r2, n0);
-                    float2 wv = __ffma2_rn(ri2, ri, np5);  // (s + eps2)^-3/2 - P5(s)
-                    wv.x = r2.x < rc2 ? wv.x : 0.f;
-                    wv.y = r2.y < rc2 ? wv.y : 0.f;
+                    float2 np5 = __ffma2_rn(n5, re, n4);  // -P5(t - eps2)
+                    np5 = __ffma2_rn(np5, re, n3);
+                    np5 = __ffma2_rn(np5, re, n2);
+                    np5 = __ffma2_rn(np5, re, n1);
+                    np5 = __ffma2_rn(np5, re, n0);
+                    float2 wv = __ffma2_rn(ri2, ri, np5);  // t^-3/2 - P5(s)
+                    wv.x = re.x < rce ? wv.x : 0.f;
+                    wv.y = re.y < rce ? wv.y : 0.f;
                     const float2 wi = __fmul2_rn(mj2, wv);  // i-side: a_i += m_j w x_ji
                     ax[k] = __ffma2_rn(wi, dx, ax[k]);
                     ay[k] = __ffma2_rn(wi, dy, ay[k]);
@@ -980,8 +987,17 @@ __global__ void __launch_bounds__(symp::NW * 32, MINB) grav_pipe_kernel(const Gr
                 float4 p = S.pp[b][qc * JMAX + kk];
                 bool keep = qv && kk <= (int)((unsigned)fc >> 29);
                 if (PARTIAL && keep && !grav_owned(A, p.x, p.y, p.z)) j = -1 - j;  // ghost: no reaction
-                p.x += o.x; p.y += o.y; p.z += o.z;  // exact (O1)
-                keep = keep & (j >= gself || (PARTIAL && j < 0)) & (box_dist2(p.x, p.y, p.z, lo, hi) < wcut);
+                const float2 pxy = __fadd2_rn(make_float2(p.x, p.y), make_float2(o.x, o.y));  // exact (O1)
+                p.x = pxy.x; p.y = pxy.y; p.z += o.z;
+                // box_dist2 packed: (p - lo, p - hi) per axis; max(-(p - lo), p - hi, 0) = max(lo - p, p - hi, 0)
+                // exactly (fl(b - a) = -fl(a - b)), so the cull set is box_dist2's
+                const float2 ux = __fadd2_rn(make_float2(p.x, p.x), nlh[0]);
+                const float2 uy = __fadd2_rn(make_float2(p.y, p.y), nlh[1]);
+                const float2 uz = __fadd2_rn(make_float2(p.z, p.z), nlh[2]);
+                const float gx = fmaxf(fmaxf(-ux.x, ux.y), 0.f), gy = fmaxf(fmaxf(-uy.x, uy.y), 0.f);
+                const float gz = fmaxf(fmaxf(-uz.x, uz.y), 0.f);
+                const float d2 = fmaf(gz, gz, fmaf(gy, gy, gx * gx));
+                keep = keep & (j >= gself || (PARTIAL && j < 0)) & (d2 < wcut);
                 const unsigned msk = __ballot_sync(0xffffffffu, keep);
                 const uint32_t t = (uint32_t)(wr + __popc(msk & below)) & (RING - 1);
                 if (keep) {
@@ -1126,6 +1142,19 @@ static GravSymArgs grav_args(crk_ctx* c) {
     A.c0 = c->prm.poly[0]; A.c1 = c->prm.poly[1]; A.c2 = c->prm.poly[2];
     A.c3 = c->prm.poly[3]; A.c4 = c->prm.poly[4]; A.c5 = c->prm.poly[5];
     for (int k = 0; k < 6; ++k) A.nc[k] = -c->prm.poly[k];
+    {  // P5(s) = sum_k c_k (t - eps2)^k = sum_m d_m t^m, d_m = sum_{k>=m} C(k, m) c_k (-eps2)^(k-m)
+        const double e = c->prm.eps2;
+        for (int m = 0; m < 6; ++m) {
+            double d = 0.0, binom = 1.0, pw = 1.0;
+            for (int k = m; k < 6; ++k) {
+                d += binom * (double)c->prm.poly[k] * pw;
+                binom = binom * (double)(k + 1) / (double)(k + 1 - m);
+                pw *= -e;
+            }
+            A.ne[m] = (float)-d;
+        }
+        A.rce = c->prm.rcut2 + c->prm.eps2;
+    }
     A.partial = c->lay.partial;
     A.inv_q = c->lay.inv_q;
     A.cs = c->lay.cs;
