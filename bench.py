@@ -277,6 +277,83 @@ def tile_config(parts, params, P, r):
     return own, gp
 
 
+def _e2e_multi(args, rk, ex, own, dev, hmax2, overlap, red_dev):
+    """e2e at N > 1 through the public API: every step, each rank copies its own particles' inputs
+    up from pinned host memory (into the second of two own sets, during the previous step) and its
+    local set's results down (snapshotted on the device at the end of the step, then copied on a
+    second copy stream during the next one).  Returns (max-over-ranks ms per step, (h2d, d2h)
+    bytes per step of this rank) or (None, None) if it fails."""
+    import torch
+    import torch.distributed as dist
+    from paper_2310_16122_b200 import Particles
+    from paper_2310_16122_b200.domain import substep_dist
+
+    try:
+        host = {k: torch.from_numpy(np.ascontiguousarray(own[k])).pin_memory()
+                for k in Particles.IN_F32 + ("species", "id")}
+        bi = sum(t.numel() * t.element_size() for t in host.values())
+        outk = list(Particles.FORCES) + ["perm"]
+        owns = [rk.own, Particles(rk.n_own, dev, outputs=False)]
+        stream = torch.cuda.current_stream(dev)
+        h2d, d2h = torch.cuda.Stream(dev), torch.cuda.Stream(dev)
+        ev_in = [torch.cuda.Event(), torch.cuda.Event()]
+        ev_done = [torch.cuda.Event(), torch.cuda.Event()]
+        ev_out = [torch.cuda.Event(), torch.cuda.Event()]
+        snap, hout = [None, None], [None, None]
+        nbytes = [0]
+
+        def run(nsteps):
+            h2d.wait_stream(stream)
+            with torch.cuda.stream(h2d):
+                owns[0].load(host, non_blocking=True)
+            ev_in[0].record(h2d)
+            for k in range(nsteps):
+                b = k % 2
+                stream.wait_event(ev_in[b])
+                rk.own = owns[b]
+                substep_dist(rk, ex, 0.0, 0.0, hmax2, overlap=overlap)
+                n = rk.n_total
+                if snap[b] is None or snap[b][0].shape[0] < n:
+                    snap[b] = [torch.empty(int(1.1 * n) + 16, dtype=getattr(rk.p, key).dtype, device=dev)
+                               for key in outk]
+                    hout[b] = [torch.empty(t.shape[0], dtype=t.dtype).pin_memory() for t in snap[b]]
+                if k >= 2:
+                    stream.wait_event(ev_out[b])  # step k-2's results of this snapshot are down
+                for t, key in zip(snap[b], outk):
+                    t[:n].copy_(getattr(rk.p, key)[:n])
+                ev_done[b].record(stream)
+                if k + 1 < nsteps:
+                    nb = (k + 1) % 2
+                    if k >= 1:
+                        h2d.wait_event(ev_done[nb])  # step k - 1 is done with that set's inputs
+                    with torch.cuda.stream(h2d):
+                        owns[nb].load(host, non_blocking=True)
+                    ev_in[nb].record(h2d)
+                d2h.wait_event(ev_done[b])
+                with torch.cuda.stream(d2h):
+                    for t, h in zip(snap[b], hout[b]):
+                        h[:n].copy_(t[:n], non_blocking=True)
+                ev_out[b].record(d2h)
+                nbytes[0] = sum(n * t.element_size() for t in snap[b])
+            stream.wait_stream(d2h)
+
+        run(2)
+        torch.cuda.synchronize()
+        dist.barrier()
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        e0.record(stream)
+        run(args.steps)
+        e1.record(stream)
+        torch.cuda.synchronize()
+        ms = torch.tensor([e0.elapsed_time(e1) / args.steps], device=red_dev)
+        dist.all_reduce(ms, op=dist.ReduceOp.MAX)
+        rk.own = owns[0]
+        return float(ms.item()), (bi, nbytes[0])
+    except Exception as exc:  # pragma: no cover
+        print(f"e2e (N > 1) failed: {exc}", file=sys.stderr)
+        return None, None
+
+
 def run_multi(args, parts, params, rank, world, local, gen_s):
     """N > 1: 3-D domain decomposition, ghost exchange over NCCL, weak scaling."""
     import torch
@@ -307,6 +384,7 @@ def run_multi(args, parts, params, rank, world, local, gen_s):
     ms = torch.tensor([e0.elapsed_time(e1) / args.steps], device=red_dev)
     dist.all_reduce(ms, op=dist.ReduceOp.MAX)
     launches = (rk.solver.launch_count() - l0) // max(args.steps, 1)
+    e2e_ms, e2e_bytes = _e2e_multi(args, rk, ex, own, dev, hmax2, overlap, red_dev)
     cg, ch, cs = rk.solver.count_pairs(rk.p)
     own_m = rk.own_mask()
     pr = torch.tensor([int(cg[own_m].sum()), int(ch[own_m].sum()), int(cs[own_m].sum()),
@@ -329,7 +407,14 @@ def run_multi(args, parts, params, rank, world, local, gen_s):
                 "pairs": {"gravity": int(pr[0].item()), "gather": int(pr[1].item()), "sym": int(pr[2].item())},
                 "pair_interactions_per_step": int(pair_int),
                 "clocks": clk.summary(), "gpu_launches": int(launches),
-                "e2e": None, "cpu_baseline": None, "roofline": None}
+                "e2e": None if e2e_ms is None else {
+                    "value": pair_int / (e2e_ms * 1e-3), "unit": "pair interactions/s", "ms_per_step": e2e_ms,
+                    "h2d_bytes_per_step": e2e_bytes[0], "d2h_bytes_per_step": e2e_bytes[1],
+                    "bytes_basis": "rank 0's own-particle inputs up, its local set's results down (every rank does "
+                                   "the same on its own link); time = max over ranks",
+                    "overlap": "per rank: H2D of step k+1 into a second own set and D2H of step k's results "
+                               "(snapshotted on the device) on two copy streams during the next step"},
+                "cpu_baseline": None, "roofline": None}
         print(json.dumps(line), flush=True)
     rk.close()
 

@@ -224,8 +224,8 @@ crk_status crk_refresh(struct crk_ctx* ctx, crk_particles* parts, void* stream);
  * particle H_out[i] = factor * sqrt(d2_(k)) (fp32 sqrt and product, correctly rounded),
  * d2_(k) the k_ngb-th smallest O2 squared distance (s32) to another gas particle, selected
  * among its neighbour list.  Exact when d2_(k) < H_i^2 (the list holds every gas particle
- * within H_i); otherwise H_out is an upper bound (2 H_i if the list has fewer than k_ngb
- * entries) (a device int32): rebuild with
+ * within H_i); otherwise H_out is an upper bound, or 1.26 H_i (twice the volume) if the list
+ * has fewer than k_ngb entries; such particles are counted in n_unconverged (a device int32): rebuild with
  * H = H_out and update again.  H_out: device, length n, sorted order, gas entries written.
  * k_ngb in [1, 127], factor > 0 (CRK_EINVAL); needs the lists (CRK_ESTATE without). */
 crk_status crk_update_h(struct crk_ctx* ctx, crk_particles* parts, int32_t k_ngb, float factor, float* H_out,

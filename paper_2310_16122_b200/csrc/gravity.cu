@@ -130,6 +130,7 @@ struct GravSymArgs {
     int32_t* cnt;        // count mode: per-particle pair counters (zeroed)
     int* work;           // dynamic work counter (zeroed before the launch)
     int split;           // work items per i-leaf
+    int lsplit;          // log2(split) (leaf_max_i / 16 is a power of two: 1, 2, 4 or 8)
     int nitems;
     float L[3];
     float rcut2, eps2;
@@ -800,8 +801,8 @@ __global__ void __launch_bounds__(symp::NW * 32, MINB) grav_pipe_kernel(const Gr
         if (lane == 0) w = atomicAdd(A.work, 1);
         w = __shfl_sync(0xffffffffu, w, 0);
         if (w >= A.nitems) break;
-        const int a = w / A.split;
-        const int gbit = w % A.split;  // the group's bit in the entry masks
+        const int a = w >> A.lsplit;
+        const int gbit = w & (A.split - 1);  // the group's bit in the entry masks
         const int icount = __ldg(A.icount + a);
         const int ibase = gbit * G;
         if (ibase >= icount) continue;
@@ -1161,6 +1162,8 @@ static GravSymArgs grav_args(crk_ctx* c) {
     for (int d = 0; d < 3; ++d) { A.dlo[d] = c->lay.dlo[d]; A.dhi[d] = c->lay.dhi[d]; }
     A.work = P<int>(c->work);
     A.split = (c->prm.leaf_max_i + symp::G - 1) / symp::G;
+    A.lsplit = 0;
+    while ((1 << A.lsplit) < A.split) ++A.lsplit;  // api.cu validates leaf_max_i in {16, 32, 64, 128}
     A.nitems = (int)(c->nleaf[0] * A.split);
     return A;
 }

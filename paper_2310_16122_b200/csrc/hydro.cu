@@ -1107,12 +1107,12 @@ static bool lists_on(crk_ctx* c) { return c->nbr_cap > 0 && c->nleaf[2] > 0; }
 
 // list-driven launch of a gather/accel pass, then the on-the-fly kernel over the rows whose
 // lists are incomplete (flagged by the builder; usually none: those CTAs exit at once)
-template <class Pass, int ENT, int MINB, int FENT, int FMINB, int LG = HYD_G>
+template <class Pass, int ENT, int MINB, int FENT, int FMINB, int LG = HYD_G, bool SL = false>
 static crk_status launch_listed(crk_ctx* c, const Pass& ps, cudaStream_t st, const char* what) {
     if (c->nleaf[2] == 0) return CRK_OK;
     RowView rv = hydro_rows(c, true);
     CRK_TRY(grow(c, c->work, 64, st));
-    CRK_TRY(cuda_check(c, launch_list<Pass, HYD_NW, LG, ENT, MINB>(ps, rv, list_view(c), st), what));
+    CRK_TRY(cuda_check(c, (launch_list<Pass, HYD_NW, LG, ENT, MINB, SL>(ps, rv, list_view(c), st)), what));
     c->launches++;
     const ListView lv = list_view(c);
     rv.rows = lv.frows;
@@ -1241,7 +1241,9 @@ crk_status corrections_extras(crk_ctx* c, crk_particles* p, cudaStream_t st) {
     const ExtPass ge = ext_pass(c, p);
     RowView rv = hydro_rows(c, true);
     const ListView lv = list_view(c);
-    CRK_TRY(cuda_check(c, (launch_list2<CorPass, ExtPass, HYD_NW, HYD_G, 128, 4>(gc, ge, rv, lv, st)),
+    // the row's lists staged in shared memory while 4 CTAs per SM still fit (cap <= 160)
+    CRK_TRY(cuda_check(c, (launch_list2<CorPass, ExtPass, HYD_NW, HYD_G, 128, 4>(gc, ge, rv, lv, st,
+                                                                                lv.cap <= 160)),
                        "corrections + extras kernel"));
     c->launches++;
     rv.rows = lv.frows;
@@ -1315,6 +1317,10 @@ static crk_status accel_gather(crk_ctx* c, crk_particles* p, float dt, cudaStrea
     g.cnt = nullptr;
     // (16 lanes per i, G = 2, measured slower on c4: 15.8 vs 12.3 ms — a list's consecutive entries
     // are 68 of the row's 512 slots, so their bank groups are no less random than 8 i's runs)
+    // the row's lists staged in shared memory (rounds of 64 entries: 99.5% of the c4 rows are one
+    // round) while two CTAs per SM still fit (cap <= 144); else rounds of 72 and global list reads
+    if (lists_on(c) && c->nbr_cap <= 144 && c->nbr_cap % 8 == 0)
+        return launch_listed<AccPass<false, BT>, 64, 2, ENT, 2, HYD_G, true>(c, g, st, "accel/dudt kernel");
     if (lists_on(c)) return launch_listed<AccPass<false, BT>, 72, 2, ENT, 2>(c, g, st, "accel/dudt kernel");
     return launch_hyd<AccPass<false, BT>, ENT, 2>(c, g, st, "accel/dudt kernel");
 }

@@ -410,10 +410,10 @@ __device__ __forceinline__ void stage_list_round(ListSmem<PAY, ENT, IREC>& sm, c
             bulk_g2s(sm.ipos, ist->gpos + ist->ifirst, (uint32_t)ist->icount * 16u, &sm.bar);
             bulk_g2s(sm.icnt, ist->ncnt + c0, (uint32_t)(c1 - c0) * 4u, &sm.bar);
         }
-        if (ist && ist->lbytes && threadIdx.x == NW * 32 - 2) {
-            mbar_expect_tx(&sm.bar, ist->lbytes);
-            bulk_g2s(ist->ldst, ist->lsrc, ist->lbytes, &sm.bar);
-        }
+    }
+    if (ist && ist->lbytes && threadIdx.x == NW * 32 - 2) {
+        mbar_expect_tx(&sm.bar, ist->lbytes);
+        bulk_g2s(ist->ldst, ist->lsrc, ist->lbytes, &sm.bar);
     }
     for (int t = lane * NW + warp; t < nent; t += NW * 32) {
         int first, count, leaf, code;
@@ -458,14 +458,20 @@ __device__ __forceinline__ int claim_row(SM& sm, int* work) {
 // iterations; longer rows are restaged per iteration.
 // SEL: honour the row subset (crk_select_rows); a separate instantiation, since the check alone
 // cost the accel walk 0.23 ms on c4 (code generation of the row body)
-template <class Pass, int NW, int G, int ENT, int MINB, bool SEL = false>
+// SL: the row's neighbour lists staged into shared memory with its first round (as list_kernel2);
+// needs one i-iteration per row (NW * G >= the gas i-leaf size)
+template <int PAY, int ENT, bool IREC>
+__host__ __device__ constexpr int list_sl_off() { return (int)((sizeof(ListSmem<PAY, ENT, IREC>) + 127) / 128 * 128); }
+template <class Pass, int NW, int G, int ENT, int MINB, bool SEL = false, bool SL = false>
 __global__ void __launch_bounds__(NW * 32, MINB) list_kernel(const Pass pass, const RowView rv, const ListView lv) {
     static_assert(32 % G == 0, "G must divide the warp");
+    static_assert(!SL || NW * G >= LIST_IMAX, "staged lists: one i-iteration per row");
     constexpr int S = 32 / G;
     constexpr bool IREC = has_irec<Pass>::value;
     using SM = ListSmem<Pass::PAY, ENT, IREC>;
     extern __shared__ __align__(128) unsigned char smem_raw[];
     SM& sm = *reinterpret_cast<SM*>(smem_raw);
+    uint16_t* const lst = reinterpret_cast<uint16_t*>(smem_raw + list_sl_off<Pass::PAY, ENT, IREC>());
     if (lv.gate && *lv.nfrows == 0) return;  // gated fallback: only when some row is flagged
 
     const int warp = threadIdx.x >> 5;
@@ -490,9 +496,14 @@ __global__ void __launch_bounds__(NW * 32, MINB) list_kernel(const Pass pass, co
             ist.grec = pass.grec; ist.gpos = pass.gpos; ist.ncnt = lv.ncnt;
             ist.ifirst = ifirst; ist.icount = icount;
         }
+        if constexpr (SL) {
+            ist.lsrc = lv.nbr + (int64_t)ifirst * lv.cap;
+            ist.ldst = lst;
+            ist.lbytes = (uint32_t)(icount * lv.cap * (int)sizeof(uint16_t));
+        }
         if (one_round)
             stage_list_round<Pass::PAY, NW, ENT, IREC>(sm, rv, pass.jrows, pass.jpay, rbeg, rend - rbeg, phase,
-                                                        IREC ? &ist : nullptr);
+                                                        (IREC || SL) ? &ist : nullptr);
         for (int it = 0; it < nit; ++it) {
             const int ibase = (it * NW + warp) * G;
             const bool wactive = ibase < icount;
@@ -519,10 +530,21 @@ __global__ void __launch_bounds__(NW * 32, MINB) list_kernel(const Pass pass, co
             }
             const uint16_t* lp = lv.nbr + (int64_t)ki * lv.cap + sl;  // this lane's next list entry
             const uint16_t* const lend = lv.nbr + (int64_t)ki * lv.cap + nl;
-            int tn = lp < lend ? (int)*lp : 0x7fffffff;  // next slot of this lane
+            // SL: the same entries in the staged copy of the row's lists (offset ls from the start)
+            const uint16_t* const lsm = lst + (ki - ifirst) * lv.cap;
+            int ls = sl;
+            auto next = [&]() -> int {
+                if constexpr (SL) return ls < nl ? (int)lsm[ls] : 0x7fffffff;
+                return lp < lend ? (int)*lp : 0x7fffffff;
+            };
+            int tn = (!SL || one_round) ? next() : 0x7fffffff;  // next slot of this lane
             for (int e0 = rbeg; e0 < rend; e0 += ENT) {
                 const int nent = min(ENT, rend - e0);
-                if (!one_round) stage_list_round<Pass::PAY, NW, ENT, IREC>(sm, rv, pass.jrows, pass.jpay, e0, nent, phase);
+                if (!one_round) {
+                    stage_list_round<Pass::PAY, NW, ENT, IREC>(sm, rv, pass.jrows, pass.jpay, e0, nent, phase,
+                                                                (SL && e0 == rbeg) ? &ist : nullptr);
+                    if (SL && e0 == rbeg) tn = next();  // the lists landed with the first round
+                }
                 if (wactive) {
                     const int rs = (e0 - rbeg) * JMAX, re = rs + nent * JMAX;
 #pragma unroll 1
@@ -531,7 +553,8 @@ __global__ void __launch_bounds__(NW * 32, MINB) list_kernel(const Pass pass, co
                             const int tl = tn - rs;
                             const float4 jp = sm.raw[tl];
                             lp += S;
-                            tn = lp < lend ? (int)*lp : 0x7fffffff;
+                            ls += S;
+                            tn = next();
                             pass.pair(is, acc, jp, sm.pay + tl * Pass::PAY,
                                       __float_as_int(sm.eoff[tl / JMAX].w) + tl % JMAX);
                         }
@@ -560,7 +583,12 @@ __global__ void __launch_bounds__(NW * 32, MINB) list_kernel(const Pass pass, co
 // __syncwarp).  The staged rows carry B's payload; a row that fits one round is staged once
 // for both walks, longer rows are staged again for B.  Used to fuse Corrections and Extras:
 // Extras needs only i's own coefficients, which Corrections has just produced.
-template <class PA, class PB, int NW, int G, int ENT, int MINB>
+// SL: the row's neighbour lists (consecutive gas ranks: one contiguous block of icount * cap
+// 16-bit entries) are staged into shared memory with the first round, so that the walks read
+// their next entry from shared memory instead of a dependent global load per pair
+template <int PAY, int ENT>
+__host__ __device__ constexpr int list2_sl_off() { return (int)((sizeof(ListSmem<PAY, ENT>) + 127) / 128 * 128); }
+template <class PA, class PB, int NW, int G, int ENT, int MINB, bool SL = false>
 __global__ void __launch_bounds__(NW * 32, MINB) list_kernel2(const PA pa, const PB pb, const RowView rv,
                                                               const ListView lv) {
     static_assert(32 % G == 0, "G must divide the warp");
@@ -569,6 +597,7 @@ __global__ void __launch_bounds__(NW * 32, MINB) list_kernel2(const PA pa, const
     using SM = ListSmem<PB::PAY, ENT>;
     extern __shared__ __align__(128) unsigned char smem_raw[];
     SM& sm = *reinterpret_cast<SM*>(smem_raw);
+    uint16_t* const lst = reinterpret_cast<uint16_t*>(smem_raw + list2_sl_off<PB::PAY, ENT>());
     const int a = blockIdx.x;
     if (lv.lflag[a] || !row_selected(rv, a)) return;
     const int warp = threadIdx.x >> 5;
@@ -589,7 +618,15 @@ __global__ void __launch_bounds__(NW * 32, MINB) list_kernel2(const PA pa, const
     const int ki = ifirst + ibase + (ivalid ? il : 0);
     const int nl = (wactive && ivalid) ? lv.ncnt[ki] : 0;
     const uint16_t* const lbeg = lv.nbr + (int64_t)ki * lv.cap;
+    const uint16_t* const lsm = lst + (ibase + il) * lv.cap;  // SL: i's staged list
     const bool one_round = rend - rbeg <= ENT;
+    IStage ist;
+    if constexpr (SL) {
+        ist.lsrc = lv.nbr + (int64_t)ifirst * lv.cap;
+        ist.ldst = lst;
+        ist.lbytes = (uint32_t)(icount * lv.cap * (int)sizeof(uint16_t));
+    }
+    auto lget = [&](int q) -> int { return SL ? (int)lsm[q] : (int)__ldg(lbeg + q); };
 
     // walk this lane's entries of round [e0, e0 + nent) with pass P (one entry per iteration:
     // two per iteration with a far sentinel measured slower here, 11.1 vs 10.5 ms on c4 — the
@@ -602,7 +639,7 @@ __global__ void __launch_bounds__(NW * 32, MINB) list_kernel2(const PA pa, const
                 const int tl = tn - rs;
                 const float4 jp = sm.raw[tl];
                 lp += S;
-                tn = lp < nl ? (int)__ldg(lbeg + lp) : 0x7fffffff;
+                tn = lp < nl ? lget(lp) : 0x7fffffff;
                 P.pair(is, acc, jp, sm.pay + tl * PB::PAY, __float_as_int(sm.eoff[tl / JMAX].w) + tl % JMAX);
             }
         }
@@ -613,10 +650,12 @@ __global__ void __launch_bounds__(NW * 32, MINB) list_kernel2(const PA pa, const
         pa.init(acc);
         if (wactive) pa.load_i(ki, is);
         int lp = sl;
-        int tn = lp < nl ? (int)__ldg(lbeg + lp) : 0x7fffffff;
+        int tn = (!SL && lp < nl) ? (int)__ldg(lbeg + lp) : 0x7fffffff;
         for (int e0 = rbeg; e0 < rend; e0 += ENT) {
             const int nent = min(ENT, rend - e0);
-            stage_list_round<PB::PAY, NW, ENT>(sm, rv, pb.jrows, pb.jpay, e0, nent, phase);
+            stage_list_round<PB::PAY, NW, ENT>(sm, rv, pb.jrows, pb.jpay, e0, nent, phase,
+                                               (SL && e0 == rbeg) ? &ist : nullptr);
+            if (SL && e0 == rbeg) tn = lp < nl ? lget(lp) : 0x7fffffff;  // the lists landed with the round
             if (wactive) walk(pa, is, acc, lp, tn, e0, nent);
         }
         if (wactive) {
@@ -631,7 +670,7 @@ __global__ void __launch_bounds__(NW * 32, MINB) list_kernel2(const PA pa, const
         pb.init(acc);
         if (wactive) pb.load_i(ki, is);
         int lp = sl;
-        int tn = lp < nl ? (int)__ldg(lbeg + lp) : 0x7fffffff;
+        int tn = lp < nl ? lget(lp) : 0x7fffffff;
         for (int e0 = rbeg; e0 < rend; e0 += ENT) {
             const int nent = min(ENT, rend - e0);
             if (!one_round) stage_list_round<PB::PAY, NW, ENT>(sm, rv, pb.jrows, pb.jpay, e0, nent, phase);
@@ -645,9 +684,13 @@ __global__ void __launch_bounds__(NW * 32, MINB) list_kernel2(const PA pa, const
 }
 
 template <class PA, class PB, int NW, int G, int ENT, int MINB>
-inline cudaError_t launch_list2(const PA& pa, const PB& pb, const RowView& rv, const ListView& lv, cudaStream_t st) {
-    const int smem = (int)sizeof(ListSmem<PB::PAY, ENT>);
-    auto k = list_kernel2<PA, PB, NW, G, ENT, MINB>;
+inline cudaError_t launch_list2(const PA& pa, const PB& pb, const RowView& rv, const ListView& lv, cudaStream_t st,
+                                bool stage_lists = false) {
+    // staged lists: one gas i-leaf's lists (<= NW * G lists of cap 16-bit entries, 16-byte multiples)
+    const bool sl = stage_lists && lv.cap % 8 == 0;
+    const int smem = sl ? list2_sl_off<PB::PAY, ENT>() + NW * G * lv.cap * (int)sizeof(uint16_t)
+                        : (int)sizeof(ListSmem<PB::PAY, ENT>);
+    auto k = sl ? list_kernel2<PA, PB, NW, G, ENT, MINB, true> : list_kernel2<PA, PB, NW, G, ENT, MINB, false>;
     cudaError_t e = cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
     if (e != cudaSuccess) return e;
     if (lv.nrows <= 0) return cudaSuccess;
@@ -665,10 +708,12 @@ inline int persistent_grid(K kernel, int threads, int smem, int64_t nrows) {
     return (int)std::max<int64_t>(1, std::min<int64_t>(nrows, (int64_t)std::max(1, per_sm) * nsm));
 }
 
-template <class Pass, int NW, int G, int ENT, int MINB>
+template <class Pass, int NW, int G, int ENT, int MINB, bool SL = false>
 inline cudaError_t launch_list(const Pass& pass, const RowView& rv, const ListView& lv, cudaStream_t st) {
-    const int smem = (int)sizeof(ListSmem<Pass::PAY, ENT, has_irec<Pass>::value>);
-    auto k = rv.rsel ? list_kernel<Pass, NW, G, ENT, MINB, true> : list_kernel<Pass, NW, G, ENT, MINB, false>;
+    constexpr bool IREC = has_irec<Pass>::value;
+    const int smem = SL ? list_sl_off<Pass::PAY, ENT, IREC>() + NW * G * lv.cap * (int)sizeof(uint16_t)
+                        : (int)sizeof(ListSmem<Pass::PAY, ENT, IREC>);
+    auto k = rv.rsel ? list_kernel<Pass, NW, G, ENT, MINB, true, SL> : list_kernel<Pass, NW, G, ENT, MINB, false, SL>;
     cudaError_t e = cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
     if (e != cudaSuccess) return e;
     if (lv.nrows <= 0) return cudaSuccess;
