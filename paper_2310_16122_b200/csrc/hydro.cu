@@ -78,7 +78,7 @@ struct GeoPass : HydCommon {
         float wt, gt;
         wendland_t(r2, s.invH, wt, gt);
         a.w.x += r2 < s.H2 ? wt : 0.f;
-        return r2 < fmaxf(s.H2, __fmul_rn(jp.w, jp.w));
+        return r2 < fmaxf(s.H2, jp.w);  // (ring rows of the list build carry H_j^2, pairs.cuh)
     }
     __device__ __forceinline__ void pair_list2(const I& s, Acc& a, const float4& p0, const float4& p1, bool& ok0,
                                                bool& ok1) const {
@@ -88,8 +88,8 @@ struct GeoPass : HydCommon {
         float2 wt, gt;
         wendland_t2(r2, s.invH, wt, gt);
         a.w = __fadd2_rn(a.w, f2sel(r2.x < s.H2, r2.y < s.H2, wt));
-        ok0 = r2.x < fmaxf(s.H2, __fmul_rn(p0.w, p0.w));
-        ok1 = r2.y < fmaxf(s.H2, __fmul_rn(p1.w, p1.w));
+        ok0 = r2.x < fmaxf(s.H2, p0.w);
+        ok1 = r2.y < fmaxf(s.H2, p1.w);
     }
     __device__ __forceinline__ void pair(const I& s, Acc& a, const float4& jp, const float4*, int j) const {
         const float dx = jp.x - s.x, dy = jp.y - s.y, dz = jp.z - s.z;

@@ -306,6 +306,7 @@ __device__ __forceinline__ void pair_row(const Pass& pass, const RowView& rv, Pa
                 const unsigned msk = __ballot_sync(0xffffffffu, keep);
                 if (keep) {
                     const int s = (wr + __popc(msk & ((1u << lane) - 1u))) & (RING - 1);
+                    if constexpr (is_build<Pass>::value) p.w = pass.jcut(p);  // the list predicate's H_j^2, once
                     rpos[s] = p;
                     rslot[s] = (uint16_t)t;
                 }
