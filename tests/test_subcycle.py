@@ -51,6 +51,10 @@ def test_drift_exact_cases():
     # a step of a quarter quantum rounds back to the lattice point (ties to even: 0.5 q -> 0)
     y = oracle.drift(x, np.array([[q / 4, q / 2, 0.0]], np.float32), box, 1.0)
     assert y[0, 0] == x[0, 0] and y[0, 1] == x[0, 1]
+    # to the NEAREST lattice point, in both directions: +3q/4 goes up a quantum, -q/4 stays
+    # (rounding toward zero would give x and z - q)
+    y = oracle.drift(x, np.array([[0.75 * q, 0.0, -0.25 * q]], np.float32), box, 1.0)
+    assert np.array_equal(y, np.array([[1.0 + q, 7.5, 0.25]], np.float32))
 
 
 def test_kick_closed_form():

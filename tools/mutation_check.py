@@ -24,7 +24,7 @@ import time
 
 ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
 SRC = os.path.join(ROOT, "oracle", "oracle.c")
-PINS = os.path.join(ROOT, "tests", "test_oracle_pins.py")
+PINS = [os.path.join(ROOT, "tests", "test_oracle_pins.py"), os.path.join(ROOT, "tests", "test_subcycle.py")]
 
 # (name, what it misreads, original text, replacement); the original must occur exactly once
 MUTATIONS = [
@@ -73,6 +73,18 @@ MUTATIONS = [
      "return d2 < cut2 * (1.0 + ldexp(1.0, -20));", "return d2 < cut2;"),
     ("predicate_fp64", "membership decided on the fp64 s instead of the fp32 fma sequence (O2)",
      "float t = fx * fx;", "double t = (double)fx * fx + (double)fy * fy + (double)fz * fz; return (float)t;"),
+    ("wendland_sigma_c2", "W normalised with Wendland C2's 21/(2 pi) instead of C4's 495/(32 pi) (O6)",
+     "return sigma / (H * H * H) * pow(t, 6)", "return 21.0 / (2.0 * ORC_PI) / (H * H * H) * pow(t, 6)"),
+    ("wendland_c2_shape", "W of Wendland C2 shape (1-q)^4 (1 + 4q) instead of C4 (O6)",
+     "pow(t, 6) * (1.0 + 6.0 * q + 35.0 * q * q / 3.0)", "pow(t, 4) * (1.0 + 4.0 * q)"),
+    ("no_min_image", "periodic differences without the minimum image (O1)",
+     "if (d > 0.5 * L) d -= L;", "if (0) d -= L;"),
+    ("drift_truncate", "drift rounded toward zero instead of to the nearest lattice point (sub-cycle)",
+     "float r = rintf(t / q) * q;", "float r = truncf(t / q) * q;"),
+    ("courant_no_cfl", "Courant limit H / c without the C_cfl factor (sub-cycle)",
+     "const double dc = c_cfl * (double)H[i] / (double)cs[i];", "const double dc = (double)H[i] / (double)cs[i];"),
+    ("knn_off_by_one", "H from the (k+1)-th instead of the k-th neighbour distance (sub-cycle)",
+     "const float d2 = m >= k ? d[k - 1] : INFINITY;", "const float d2 = m > k ? d[k] : INFINITY;"),
 ]
 
 
@@ -98,7 +110,7 @@ def run_one(m, tmp, flags, timeout=600):
         return name, "error", "compile: " + r.stderr[-300:]
     env = dict(os.environ, CRK_ORACLE_LIB=so, OMP_NUM_THREADS="2")
     t0 = time.time()
-    r = subprocess.run([sys.executable, "-m", "pytest", PINS, "-x", "-q", "-p", "no:cacheprovider"],
+    r = subprocess.run([sys.executable, "-m", "pytest", *PINS, "-m", "not gpu", "-x", "-q", "-p", "no:cacheprovider"],
                        capture_output=True, text=True, cwd=ROOT, env=env, timeout=timeout)
     failed = [ln.split("::", 1)[1].split(" ")[0] for ln in r.stdout.splitlines() if ln.startswith("FAILED")]
     status = "killed" if r.returncode == 1 and failed else ("survived" if r.returncode == 0 else "error")
