@@ -278,9 +278,39 @@ crk_status crk_select_cells_dev(struct crk_ctx* ctx, const float* x, const float
                                 int32_t* idx_out, int32_t* count_dev, void* stream);
 crk_status crk_select_gas_dev(struct crk_ctx* ctx, const uint8_t* dmask, int32_t* idx_out, int32_t* count_dev,
                               void* stream);
+/* crk_select_gas_dev for nsets masks at once (R2/R3 send and receive sets of every peer), after
+ * crk_build_lists: set k (mask at dmasks + k * (ncell[0] + ncell[1] + ncell[2])) gets the ascending
+ * gas ranks of the gas particles in its cells at idx_out + k * stride (device; entries past stride
+ * are dropped: stride >= every set's size keeps them all), its full size at counts_dev[k] (device
+ * int32) — the same (key-order) result as nsets calls of crk_select_gas_dev, from one count pass,
+ * one scan and one write pass.  1 <= nsets <= 16. */
+crk_status crk_select_gas_multi_dev(struct crk_ctx* ctx, const uint8_t* dmasks, int32_t nsets, int32_t* idx_out,
+                                    int64_t stride, int32_t* counts_dev, void* stream);
+
+/* R1 selection for every peer in ONE pass over the particles (§3.4: the overload
+ * zone each neighbour rank needs): dmasks holds npeers concatenated masks of the layout above
+ * (peer q at dmasks + q * (ncell[0] + ncell[1] + ncell[2])); peer q's selected indices go to
+ * idx_out + q * stride (device, capacity stride >= n), counts_dev[2 q] = how many were selected,
+ * counts_dev[2 q + 1] = how many of those are gas (device int32, zeroed by the call).  Within a
+ * peer the order of the indices is NOT deterministic (warp-aggregated atomics); the receiver's
+ * build sorts the ghosts by (cell, fine key, id), so nothing downstream depends on it.
+ * 1 <= npeers <= 26, else CRK_EINVAL. */
+crk_status crk_select_peers_dev(struct crk_ctx* ctx, const float* x, const float* y, const float* z,
+                                const uint8_t* species, int64_t n, const uint8_t* dmasks, int32_t npeers,
+                                int32_t* idx_out, int64_t stride, int32_t* counts_dev, void* stream);
 /* R1 pack of the first min(*count_dev, cap) selected particles (idx: device, capacity cap). */
 crk_status crk_pack_particles_dev(struct crk_ctx* ctx, const crk_particles* parts, const int32_t* idx,
                                   const int32_t* count_dev, int64_t cap, void* out, void* stream);
+
+/* The own particles of a sorted local set (after crk_build_lists on own + ghosts, own first
+ * in the input): dst rows [0, n_own) = the src rows whose perm (input index) is < n_own, in
+ * ascending sorted position, every input field (x y z vx vy vz m H u species id).  The
+ * decomposed substep carries its own set this way (§3.4, one rank per GPU over
+ * sub-cycles): the next build sorts nearly sorted input and R1 needs no own copy.  src->n =
+ * the local set's size, src->perm from the build; dst has room for n_own rows; src and dst
+ * must not overlap.  Device pointers; asynchronous on stream. */
+crk_status crk_compact_own(struct crk_ctx* ctx, const crk_particles* src, int64_t n_own, crk_particles* dst,
+                           void* stream);
 
 /* R1: pack / unpack whole particles as 48-byte records (x y z vx vy vz m H u, species,
  * id).  unpack writes records [0, n) to parts entries [offset, offset + n). */

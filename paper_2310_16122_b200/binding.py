@@ -26,7 +26,8 @@ EXPORTS = ["crk_create", "crk_destroy", "crk_build_lists", "crk_gravity_kick", "
            "crk_pm_accel", "crk_pm_slab_create", "crk_pm_deposit", "crk_pm_slab_forward", "crk_pm_slab_solve",
            "crk_pm_slab_inverse", "crk_pm_interp", "crk_neighbour_lists",
            "crk_select_cells_dev", "crk_select_gas_dev", "crk_pack_particles_dev", "crk_pack_gas_state",
-           "crk_unpack_gas_state", "crk_select_rows"]
+           "crk_unpack_gas_state", "crk_select_rows", "crk_select_peers_dev", "crk_compact_own",
+           "crk_select_gas_multi_dev"]
 
 
 class CrkError(RuntimeError):
@@ -121,11 +122,15 @@ def lib():
         L.crk_pack_particles.argtypes = [vp, C.POINTER(CrkParticles), vp, C.c_int64, vp, vp]
         L.crk_select_cells_dev.argtypes = [vp, vp, vp, vp, vp, C.c_int, C.c_int64, vp, vp, vp, vp]
         L.crk_select_gas_dev.argtypes = [vp, vp, vp, vp, vp]
+        L.crk_select_peers_dev.argtypes = [vp, vp, vp, vp, vp, C.c_int64, vp, C.c_int32, vp, C.c_int64, vp, vp]
+        L.crk_compact_own.argtypes = [vp, C.POINTER(CrkParticles), C.c_int64, C.POINTER(CrkParticles), vp]
+        L.crk_select_gas_multi_dev.argtypes = [vp, vp, C.c_int32, vp, C.c_int64, vp, vp]
         L.crk_pack_particles_dev.argtypes = [vp, C.POINTER(CrkParticles), vp, vp, C.c_int64, vp, vp]
         L.crk_pack_gas_state.argtypes = [vp, C.POINTER(CrkParticles), vp, C.c_int64, vp, vp]
         L.crk_unpack_gas_state.argtypes = [vp, C.POINTER(CrkParticles), vp, C.c_int64, vp, vp]
         for f in ("crk_select_cells_dev", "crk_select_gas_dev", "crk_pack_particles_dev", "crk_pack_gas_state",
-                  "crk_unpack_gas_state"):
+                  "crk_unpack_gas_state", "crk_select_peers_dev", "crk_compact_own",
+                  "crk_select_gas_multi_dev"):
             getattr(L, f).restype = C.c_int
         L.crk_unpack_particles.argtypes = [vp, C.POINTER(CrkParticles), C.c_int64, C.c_int64, vp, vp]
         L.crk_pack_gas.argtypes = [vp, C.c_int, vp, C.c_int64, vp, vp]
@@ -447,6 +452,32 @@ class Solver:
                                                int(gas_only), int(n), C.c_void_p(dmask.data_ptr()),
                                                C.c_void_p(idx_out.data_ptr()), C.c_void_p(count_dev.data_ptr()),
                                                self._stream(stream)), self.ctx)
+
+    def select_peers_dev(self, parts, n, dmasks, idx_out, counts_dev, stream=None):
+        """R1 selection of every peer in one pass: dmasks (npeers, ncx + ncy + ncz) uint8 device,
+        idx_out (npeers, >= n) int32 device, counts_dev (npeers, 2) int32 device = (all, gas)
+        per peer; no host sync (crk_select_peers_dev)."""
+        npeers = int(dmasks.shape[0])
+        self._check(lib().crk_select_peers_dev(self.ctx, C.c_void_p(parts.x.data_ptr()), C.c_void_p(parts.y.data_ptr()),
+                                               C.c_void_p(parts.z.data_ptr()), C.c_void_p(parts.species.data_ptr()),
+                                               int(n), C.c_void_p(dmasks.data_ptr()), npeers,
+                                               C.c_void_p(idx_out.data_ptr()), int(idx_out.stride(0)),
+                                               C.c_void_p(counts_dev.data_ptr()), self._stream(stream)), self.ctx)
+
+    def compact_own(self, src, n_total, n_own, dst, stream=None):
+        """dst[:n_own] = the rows of the sorted local set src[:n_total] whose perm < n_own, in
+        sorted order (crk_compact_own)."""
+        ps, pd = src.struct(), dst.struct()
+        ps.n = int(n_total)
+        self._check(lib().crk_compact_own(self.ctx, C.byref(ps), int(n_own), C.byref(pd), self._stream(stream)),
+                    self.ctx)
+
+    def select_gas_multi_dev(self, dmasks, idx_out, counts_dev, stream=None):
+        """crk_select_gas_dev for every row of dmasks (nsets, ncx + ncy + ncz) at once: ascending
+        gas ranks of set k in idx_out[k] (nsets, >= n_gas), its size in counts_dev[k]."""
+        self._check(lib().crk_select_gas_multi_dev(self.ctx, C.c_void_p(dmasks.data_ptr()), int(dmasks.shape[0]),
+                                                   C.c_void_p(idx_out.data_ptr()), int(idx_out.stride(0)),
+                                                   C.c_void_p(counts_dev.data_ptr()), self._stream(stream)), self.ctx)
 
     def select_gas_dev(self, dmask, idx_out, count_dev, stream=None):
         self._check(lib().crk_select_gas_dev(self.ctx, C.c_void_p(dmask.data_ptr()), C.c_void_p(idx_out.data_ptr()),

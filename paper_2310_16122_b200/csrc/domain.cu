@@ -34,6 +34,176 @@ __global__ void k_cell_flags_gas(int64_t ng, const float4* __restrict__ gpos, fl
     flag[k] = (mx[cx] && my[cy] && mz[cz]) ? 1 : 0;
 }
 
+// R1 selection of every peer in one pass: per particle its cell, then per peer the mask test;
+// selected indices appended with one atomic per warp and peer (ballot prefix within the warp)
+__global__ void k_select_peers(int64_t n, const float* __restrict__ x, const float* __restrict__ y,
+                               const float* __restrict__ z, const uint8_t* __restrict__ sp, float inv_q, int cs,
+                               const uint8_t* __restrict__ dmasks, int mstride, int ncx, int ncy, int npeers,
+                               int32_t* __restrict__ idx_out, int64_t stride, int32_t* __restrict__ counts) {
+    const int lane = threadIdx.x & 31;
+    const unsigned below = (1u << lane) - 1u;
+    for (int64_t i0 = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) & ~(int64_t)31; i0 < n;
+         i0 += (int64_t)gridDim.x * blockDim.x) {
+        const int64_t i = i0 + lane;
+        const bool v = i < n;
+        uint32_t cx = 0, cy = 0, cz = 0;
+        bool gas = false;
+        if (v) {
+            cx = (uint32_t)(x[i] * inv_q) >> cs;
+            cy = (uint32_t)(y[i] * inv_q) >> cs;
+            cz = (uint32_t)(z[i] * inv_q) >> cs;
+            gas = sp && sp[i] == 1;
+        }
+        for (int q = 0; q < npeers; ++q) {
+            const uint8_t* m = dmasks + (int64_t)q * mstride;
+            const bool f = v && m[cx] && m[ncx + cy] && m[ncx + ncy + cz];
+            const unsigned b = __ballot_sync(0xffffffffu, f);
+            if (!b) continue;
+            const unsigned bg = __ballot_sync(0xffffffffu, f && gas);
+            int base = 0;
+            if (lane == 0) {
+                base = atomicAdd(counts + 2 * q, __popc(b));
+                if (bg) atomicAdd(counts + 2 * q + 1, __popc(bg));
+            }
+            base = __shfl_sync(0xffffffffu, base, 0);
+            if (f) idx_out[q * stride + base + __popc(b & below)] = (int32_t)i;
+        }
+    }
+}
+
+__global__ void k_flag_own(int64_t n, const int32_t* __restrict__ perm, int64_t n_own, uint8_t* flag) {
+    const int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+    if (i < n) flag[i] = perm[i] < n_own ? 1 : 0;
+}
+
+// dst row t = src row idx[t], every input field
+__global__ void k_gather_rows(int64_t n, const int32_t* __restrict__ idx, const float* __restrict__ x,
+                              const float* __restrict__ y, const float* __restrict__ z, const float* __restrict__ vx,
+                              const float* __restrict__ vy, const float* __restrict__ vz, const float* __restrict__ m,
+                              const float* __restrict__ H, const float* __restrict__ u, const uint8_t* __restrict__ sp,
+                              const int64_t* __restrict__ id, float* dx, float* dy, float* dz, float* dvx, float* dvy,
+                              float* dvz, float* dm, float* dH, float* du, uint8_t* dsp, int64_t* did) {
+    const int64_t t = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+    if (t >= n) return;
+    const int64_t i = idx[t];
+    dx[t] = x[i]; dy[t] = y[i]; dz[t] = z[i];
+    dvx[t] = vx[i]; dvy[t] = vy[i]; dvz[t] = vz[i];
+    dm[t] = m[i]; dH[t] = H[i]; du[t] = u[i];
+    dsp[t] = sp[i];
+    did[t] = id[i];
+}
+
+// ---- order-preserving selection of gas ranks for several cell-mask sets at once
+// blocks of GM_B = 1024 consecutive gas ranks (8 warps x 4 sub-steps of 32); per element a bit
+// per set; counts per (set, block), an exclusive scan over the blocks per set, then the writes
+// at block offset + warp offset + ballot prefix, so every set's output is in ascending rank order
+constexpr int GM_W = 8, GM_B = GM_W * 128, GM_MAXSETS = 16;
+__device__ __forceinline__ uint32_t gm_bits(const float4* __restrict__ gpos, int64_t k, int64_t ng, float inv_q,
+                                            int cs, const uint8_t* __restrict__ dm, int mstride, int ncx, int ncy,
+                                            int nsets) {
+    if (k >= ng) return 0u;
+    const float4 p = gpos[k];
+    const uint32_t cx = (uint32_t)(p.x * inv_q) >> cs, cy = (uint32_t)(p.y * inv_q) >> cs,
+                   cz = (uint32_t)(p.z * inv_q) >> cs;
+    uint32_t b = 0u;
+    for (int q = 0; q < nsets; ++q) {
+        const uint8_t* m = dm + (int64_t)q * mstride;
+        if (m[cx] && m[ncx + cy] && m[ncx + ncy + cz]) b |= 1u << q;
+    }
+    return b;
+}
+
+__global__ void __launch_bounds__(GM_W * 32) k_gas_multi_count(int64_t ng, const float4* __restrict__ gpos, float inv_q,
+                                                              int cs, const uint8_t* __restrict__ dm, int mstride,
+                                                              int ncx, int ncy, int nsets, int32_t* __restrict__ blkcnt,
+                                                              int64_t nblk) {
+    __shared__ int s_cnt[GM_MAXSETS];
+    if (threadIdx.x < GM_MAXSETS) s_cnt[threadIdx.x] = 0;
+    __syncthreads();
+    const int w = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    const int64_t base = blockIdx.x * (int64_t)GM_B + w * 128;
+    int c[GM_MAXSETS];
+#pragma unroll
+    for (int q = 0; q < GM_MAXSETS; ++q) c[q] = 0;
+#pragma unroll
+    for (int j = 0; j < 4; ++j) {
+        const uint32_t b = gm_bits(gpos, base + 32 * j + lane, ng, inv_q, cs, dm, mstride, ncx, ncy, nsets);
+#pragma unroll
+        for (int q = 0; q < GM_MAXSETS; ++q)
+            if (q < nsets) c[q] += __popc(__ballot_sync(0xffffffffu, (b >> q) & 1u));
+    }
+    if (lane == 0)
+        for (int q = 0; q < nsets; ++q)
+            if (c[q]) atomicAdd(&s_cnt[q], c[q]);
+    __syncthreads();
+    if (threadIdx.x < nsets) blkcnt[(int64_t)threadIdx.x * nblk + blockIdx.x] = s_cnt[threadIdx.x];
+}
+
+// one CTA per set: exclusive scan of its block counts (in place), the set's total to counts[q]
+__global__ void __launch_bounds__(1024) k_gas_multi_scan(int32_t* __restrict__ blkcnt, int64_t nblk,
+                                                        int32_t* __restrict__ counts) {
+    using Scan = cub::BlockScan<int32_t, 1024>;
+    __shared__ typename Scan::TempStorage tmp;
+    __shared__ int32_t s_carry;
+    int32_t* row = blkcnt + (int64_t)blockIdx.x * nblk;
+    if (threadIdx.x == 0) s_carry = 0;
+    __syncthreads();
+    for (int64_t b0 = 0; b0 < nblk; b0 += 1024) {
+        const int64_t b = b0 + threadIdx.x;
+        const int32_t v = b < nblk ? row[b] : 0;
+        int32_t ex, tot;
+        Scan(tmp).ExclusiveSum(v, ex, tot);
+        const int32_t carry = s_carry;
+        if (b < nblk) row[b] = carry + ex;
+        __syncthreads();
+        if (threadIdx.x == 0) s_carry = carry + tot;
+        __syncthreads();
+    }
+    if (threadIdx.x == 0) counts[blockIdx.x] = s_carry;
+}
+
+__global__ void __launch_bounds__(GM_W * 32) k_gas_multi_write(int64_t ng, const float4* __restrict__ gpos, float inv_q,
+                                                              int cs, const uint8_t* __restrict__ dm, int mstride,
+                                                              int ncx, int ncy, int nsets,
+                                                              const int32_t* __restrict__ blkoff, int64_t nblk,
+                                                              int32_t* __restrict__ idx_out, int64_t stride) {
+    __shared__ int s_w[GM_MAXSETS][GM_W];
+    const int w = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    const unsigned below = (1u << lane) - 1u;
+    const int64_t base = blockIdx.x * (int64_t)GM_B + w * 128;
+    uint32_t bits[4];
+#pragma unroll
+    for (int j = 0; j < 4; ++j) bits[j] = gm_bits(gpos, base + 32 * j + lane, ng, inv_q, cs, dm, mstride, ncx, ncy, nsets);
+    for (int q = 0; q < nsets; ++q) {
+        int c = 0;
+#pragma unroll
+        for (int j = 0; j < 4; ++j) c += __popc(__ballot_sync(0xffffffffu, (bits[j] >> q) & 1u));
+        if (lane == 0) s_w[q][w] = c;
+    }
+    __syncthreads();
+    if (threadIdx.x < nsets) {  // exclusive prefix over the warps, plus the block's offset
+        int run = blkoff[(int64_t)threadIdx.x * nblk + blockIdx.x];
+        for (int v = 0; v < GM_W; ++v) {
+            const int t = s_w[threadIdx.x][v];
+            s_w[threadIdx.x][v] = run;
+            run += t;
+        }
+    }
+    __syncthreads();
+    for (int q = 0; q < nsets; ++q) {
+        int off = s_w[q][w];
+        int32_t* out = idx_out + (int64_t)q * stride;
+#pragma unroll
+        for (int j = 0; j < 4; ++j) {
+            const bool f = (bits[j] >> q) & 1u;
+            const unsigned b = __ballot_sync(0xffffffffu, f);
+            const int pos = off + __popc(b & below);
+            if (f && pos < stride) out[pos] = (int32_t)(base + 32 * j + lane);
+            off += __popc(b);
+        }
+    }
+}
+
 struct Rec48 {
     float f[9];
     float sp;
@@ -255,6 +425,75 @@ crk_status crk_select_cells_dev(crk_ctx* c, const float* x, const float* y, cons
                                         dmask + nc[0] + nc[1], P<uint8_t>(c->sel_flag));
     CRK_LAUNCHED(c, "cell flags");
     return compact_dev(c, n, idx_out, count_dev, st);
+}
+
+crk_status crk_select_peers_dev(crk_ctx* c, const float* x, const float* y, const float* z, const uint8_t* species,
+                                int64_t n, const uint8_t* dmasks, int32_t npeers, int32_t* idx_out, int64_t stride,
+                                int32_t* counts_dev, void* stream) {
+    if (!c || !counts_dev || !dmasks || n < 0 || npeers < 1 || npeers > 26 || stride < n ||
+        (n > 0 && (!x || !y || !z || !idx_out)))
+        return fail(c, CRK_EINVAL, "bad args");
+    if (n >= (int64_t)1 << 31) return fail(c, CRK_ECAPACITY, "more than 2^31 particles");
+    CRK_TRY(cuda_check(c, cudaSetDevice(c->device), "cudaSetDevice"));
+    cudaStream_t st = (cudaStream_t)stream;
+    CRK_TRY(cuda_check(c, zero_async(counts_dev, (size_t)npeers * 2 * sizeof(int32_t), st, c), "memset"));
+    if (n == 0) return CRK_OK;
+    const int* nc = c->lay.ncell;
+    int dev = c->device, nsm = 0;
+    cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, dev);
+    const int64_t blocks = std::min<int64_t>(nb(n), (int64_t)nsm * 8);
+    k_select_peers<<<(unsigned)blocks, 256, 0, st>>>(n, x, y, z, species, c->lay.inv_q, c->lay.cs, dmasks,
+                                                     nc[0] + nc[1] + nc[2], nc[0], nc[1], npeers, idx_out, stride,
+                                                     counts_dev);
+    CRK_LAUNCHED(c, "select peers");
+    return CRK_OK;
+}
+
+crk_status crk_compact_own(crk_ctx* c, const crk_particles* src, int64_t n_own, crk_particles* dst, void* stream) {
+    if (!c || !src || !dst || n_own < 0 || n_own > src->n) return fail(c, CRK_EINVAL, "bad args");
+    if (n_own == 0) return CRK_OK;
+    if (!src->perm || !src->x || !dst->x || !dst->species || !dst->id) return fail(c, CRK_EINVAL, "null field");
+    if (src->n >= (int64_t)1 << 31) return fail(c, CRK_ECAPACITY, "more than 2^31 particles");
+    CRK_TRY(cuda_check(c, cudaSetDevice(c->device), "cudaSetDevice"));
+    cudaStream_t st = (cudaStream_t)stream;
+    const int64_t n = src->n;
+    CRK_TRY(grow(c, c->sel_flag, n, st));
+    CRK_TRY(grow(c, c->idx_a, n * 4, st));  // build scratch, free between builds
+    k_flag_own<<<nb(n), 256, 0, st>>>(n, src->perm, n_own, P<uint8_t>(c->sel_flag));
+    CRK_LAUNCHED(c, "flag own");
+    CRK_TRY(grow(c, c->dev_scalars, 64, st));
+    CRK_TRY(compact_dev(c, n, P<int32_t>(c->idx_a), reinterpret_cast<int32_t*>(P<char>(c->dev_scalars) + 48), st));
+    k_gather_rows<<<nb(n_own), 256, 0, st>>>(n_own, P<int32_t>(c->idx_a), src->x, src->y, src->z, src->vx, src->vy,
+                                             src->vz, src->m, src->H, src->u, src->species, src->id, dst->x, dst->y,
+                                             dst->z, dst->vx, dst->vy, dst->vz, dst->m, dst->H, dst->u, dst->species,
+                                             dst->id);
+    CRK_LAUNCHED(c, "gather own");
+    return CRK_OK;
+}
+
+crk_status crk_select_gas_multi_dev(crk_ctx* c, const uint8_t* dmasks, int32_t nsets, int32_t* idx_out, int64_t stride,
+                                    int32_t* counts_dev, void* stream) {
+    if (!c || !dmasks || !counts_dev || nsets < 1 || nsets > GM_MAXSETS) return fail(c, CRK_EINVAL, "bad args");
+    if (c->stage < ST_LISTS) return fail(c, CRK_ESTATE, "call crk_build_lists first");
+    const int64_t ng = c->n_gas;
+    if (stride < 0 || (ng > 0 && stride > 0 && !idx_out)) return fail(c, CRK_EINVAL, "bad idx_out / stride");
+    CRK_TRY(cuda_check(c, cudaSetDevice(c->device), "cudaSetDevice"));
+    cudaStream_t st = (cudaStream_t)stream;
+    if (ng == 0) return cuda_check(c, zero_async(counts_dev, (size_t)nsets * 4, st, c), "memset");
+    const int64_t nblk = (ng + GM_B - 1) / GM_B;
+    CRK_TRY(grow(c, c->sel_flag, (size_t)nsets * nblk * 4, st));  // block counts -> offsets
+    int32_t* blk = P<int32_t>(c->sel_flag);
+    const int* nc = c->lay.ncell;
+    const int ms = nc[0] + nc[1] + nc[2];
+    k_gas_multi_count<<<(unsigned)nblk, GM_W * 32, 0, st>>>(ng, P<float4>(c->gpos), c->lay.inv_q, c->lay.cs, dmasks, ms,
+                                                            nc[0], nc[1], nsets, blk, nblk);
+    CRK_LAUNCHED(c, "gas multi count");
+    k_gas_multi_scan<<<(unsigned)nsets, 1024, 0, st>>>(blk, nblk, counts_dev);
+    CRK_LAUNCHED(c, "gas multi scan");
+    k_gas_multi_write<<<(unsigned)nblk, GM_W * 32, 0, st>>>(ng, P<float4>(c->gpos), c->lay.inv_q, c->lay.cs, dmasks, ms,
+                                                            nc[0], nc[1], nsets, blk, nblk, idx_out, stride);
+    CRK_LAUNCHED(c, "gas multi write");
+    return CRK_OK;
 }
 
 crk_status crk_select_gas_dev(crk_ctx* c, const uint8_t* dmask, int32_t* idx_out, int32_t* count_dev, void* stream) {

@@ -1,8 +1,8 @@
 """3-D domain decomposition with leaf-granular ghost exchange.
 
 Host-side plumbing only: the decomposition and the cell masks are small host logic; the
-selection, packing and unpacking run in libcrksr.so (crk_select_cells_dev /
-crk_select_gas_dev / crk_pack_particles_dev / crk_unpack_* / crk_pack_gas) and the
+selection, packing and unpacking run in libcrksr.so (crk_select_peers_dev /
+crk_select_gas_multi_dev / crk_pack_particles_dev / crk_unpack_* / crk_pack_gas / crk_compact_own) and the
 transfers are NCCL send/recv through torch.distributed (batch_isend_irecv).  The paper
 runs one MPI rank per GPU (§3.4) but does not describe the exchange; this
 follows north_star's "3-D spatial domain decomposition with overload/ghost zones refreshed
@@ -16,7 +16,8 @@ Per substep (rank r owning the chaining-mesh cells D_r; its peers s share a halo
       key order on both sides; Extras of the receiver's own gas reads both);
   corrections, extras;
   R3  accel records of the same gas -> peer s;
-  accel / du-dt; kicked v, u written back to the own set.
+  accel / du-dt; the own rows (with their kicks) carried in this build's sorted order into
+      the next substep's local set (no own copy in R1, a nearly sorted input for the build).
 halo width h = ceil(reach / cell_side), reach = max(r_c, H_max) (1 + 2^-20) with H_max the
 global maximum smoothing length (one all-reduce when H changes).
 
@@ -187,6 +188,15 @@ class EmuExchange:
                     recvs[s][r].copy_(t)
 
 
+def _rows_view(parts: Particles, n: int) -> Particles:
+    """The first n rows of a particle set's inputs as a Particles (views, no outputs)."""
+    v = Particles.__new__(Particles)
+    v.n, v.device, v.outputs = int(n), parts.device, False
+    for k in Particles.IN_F32 + ("species", "id", "perm"):
+        setattr(v, k, getattr(parts, k)[:n])
+    return v
+
+
 def _grow(t, n, **kw):
     """t if it holds n rows, else a new tensor with 1.25 n rows (geometric growth)."""
     if t is not None and t.shape[0] >= n:
@@ -205,6 +215,7 @@ class DomainRank:
         self.params = decomp.rank_params(r)
         self.own_host = own
         self.n_own = own["x"].shape[0]
+        self._q = None         # the spare local-set buffer the own rows are carried into (carry_own)
         self.own = Particles.from_host(own, self.device, outputs=False)
         self.solver = Solver(self.params, self.device.index if self.device.index is not None else 0)
         self.stream = stream
@@ -213,6 +224,28 @@ class DomainRank:
         self.n_total = self.n_own
         self._buf = {}
         self.check = False  # tests: verify the R2/R3 index-set sizes against the R1 counts (syncs)
+
+    @property
+    def own(self):
+        """The own particles: a set the caller gave (the constructor, migration, a reload), or,
+        after a substep, the own rows carried in sorted order at the start of the next local set."""
+        return self._own_view if self._own_local else self._own_ext
+
+    @own.setter
+    def own(self, v):
+        self._own_ext = v
+        self._own_local = False
+
+    def carry_own(self):
+        """After a substep: the own particles (with its kicks) into the spare local-set buffer in
+        the sorted order of this substep's build (crk_compact_own); the next substep's local set
+        starts from them — R1 needs no own copy and the build sorts nearly sorted input."""
+        cap = 0 if self._q is None else self._q.x.shape[0]
+        if cap < self.n_own:
+            self._q = Particles(max(int(1.1 * self.n_total), 16), self.device, self.outputs)
+        self.solver.compact_own(self.p, self.n_total, self.n_own, self._q, stream=self.stream)
+        self._own_view = _rows_view(self._q, self.n_own)
+        self._own_local = True
 
     def local_hmax2(self) -> float:
         """max fl32(H^2) over the own gas (device arrays: the own set changes with migration)."""
@@ -242,24 +275,36 @@ class DomainRank:
         npr = len(self.peers)
         self.cnt_send = torch.zeros((max(npr, 1), 2), dtype=torch.int32, device=self.device)
         self.cnt_recv = torch.zeros((max(npr, 1), 2), dtype=torch.int32, device=self.device)
-        self.idx_r1 = {s: torch.empty(max(self.n_own, 1), dtype=torch.int32, device=self.device)
-                       for s in self.peers}
-        self.idx_tmp = torch.empty(max(self.n_own, 1), dtype=torch.int32, device=self.device)
+        # every peer's send mask as one (peers, ncx + ncy + ncz) device array: one selection pass for all
+        nm = sum(self.d.ncell)
+        rows = [self.mask_send[s] if self.mask_send[s] is not None
+                else torch.zeros(nm, dtype=torch.uint8, device=self.device) for s in self.peers]
+        self.mask_all = torch.stack(rows) if rows else None
+        # the R2/R3 gas sets, (send, recv) per peer, selected in one pass after each build
+        grows = []
+        for s in self.peers:
+            for m in (self.mask_send[s], self.mask_recv[s]):
+                grows.append(m if m is not None else torch.zeros(nm, dtype=torch.uint8, device=self.device))
+        self.gmask_all = torch.stack(grows) if grows else None
+        self.gcnt = torch.zeros(max(2 * npr, 1), dtype=torch.int32, device=self.device)
+        self._alloc_sel(self.n_own)
         self.sbuf, self.rbuf = {}, {}
+
+    def _alloc_sel(self, n):
+        npr = len(self.peers)
+        self.idx_all = torch.empty((max(npr, 1), max(n, 1)), dtype=torch.int32, device=self.device)
+        self.idx_r1 = {s: self.idx_all[q] for q, s in enumerate(self.peers)}
 
     # R1 ---------------------------------------------------------------
     def r1_select_pack(self):
         """Select and pack each peer's R1 particles (counts stay on the device) into the
-        persistent send buffers; returns the (peers, 2) device counts (all, gas)."""
+        persistent send buffers; returns the (peers, 2) device counts (all, gas).  One pass over
+        the own particles selects for every peer (crk_select_peers_dev)."""
+        if not self.peers:
+            return self.cnt_send
+        self.solver.select_peers_dev(self.own, self.n_own, self.mask_all, self.idx_all, self.cnt_send,
+                                     stream=self.stream)
         for q, s in enumerate(self.peers):
-            m = self.mask_send[s]
-            if m is None:
-                self.cnt_send[q].zero_()
-                continue
-            self.solver.select_cells_dev(self.own, m, self.idx_r1[s], self.cnt_send[q, 0:1], self.n_own,
-                                         stream=self.stream)
-            self.solver.select_cells_dev(self.own, m, self.idx_tmp, self.cnt_send[q, 1:2], self.n_own,
-                                         gas_only=True, stream=self.stream)
             cap = self.sbuf[s].shape[0] if s in self.sbuf else 0
             if cap:
                 self.solver.pack_particles_dev(self.own, self.idx_r1[s], self.cnt_send[q, 0:1], self.sbuf[s],
@@ -297,13 +342,23 @@ class DomainRank:
         self._gas_idx()
 
     def r1_unpack(self):
-        cap = 0 if self.p is None else self.p.x.shape[0]
-        if cap < self.n_total:
-            self.p = Particles(max(int(1.1 * self.n_total), 16), self.device, self.outputs)
+        keys = Particles.IN_F32 + ("species", "id")
+        if self._own_local:  # the carried own rows already start the next local set
+            self.p, self._q = self._q, self.p
+            if self.p.x.shape[0] < self.n_total:
+                old = self.p
+                self.p = Particles(max(int(1.1 * self.n_total), 16), self.device, self.outputs)
+                for k in keys:
+                    getattr(self.p, k)[: self.n_own].copy_(getattr(old, k)[: self.n_own])
+                self._own_view = _rows_view(self.p, self.n_own)
+        else:
+            cap = 0 if self.p is None else self.p.x.shape[0]
+            if cap < self.n_total:
+                self.p = Particles(max(int(1.1 * self.n_total), 16), self.device, self.outputs)
+            for k in keys:
+                getattr(self.p, k)[: self.n_own].copy_(getattr(self.own, k))
         p = self.p
         p.n = self.n_total
-        for k in Particles.IN_F32 + ("species", "id"):
-            getattr(p, k)[: self.n_own].copy_(getattr(self.own, k))
         off = self.n_own
         for s in self.peers:
             n = self.n_recv[s]
@@ -314,22 +369,26 @@ class DomainRank:
     def _gas_idx(self):
         """Gas ranks (device) of the R2/R3 send set (own gas in each peer's halo) and receive
         set (that peer's ghost gas), in key order — the same particles, in the same order, on
-        both sides; sizes known from the R1 counts (no readback)."""
+        both sides; sizes known from the R1 counts (no readback).  Every peer's two sets come
+        from one order-preserving selection pass (crk_select_gas_multi_dev)."""
         self.gsend, self.grecv = {}, {}
-        cnt = torch.zeros(2, dtype=torch.int32, device=self.device)
-        for s in self.peers:
-            for side, dst, m, n, c in (("send", self.gsend, self.mask_send[s], self.g_send[s], cnt[0:1]),
-                                       ("recv", self.grecv, self.mask_recv[s], self.g_recv[s], cnt[1:2])):
-                if m is None or n == 0:
-                    dst[s] = None
-                    continue
-                key = ("gidx", side, s)  # persistent per (side, peer): no allocation per substep
-                buf = _grow(self._buf.get(key), self.n_total, dtype=torch.int32, device=self.device)
-                self._buf[key] = buf
-                self.solver.select_gas_dev(m, buf, c, stream=self.stream)
+        if not self.peers:
+            return
+        need = max([self.g_send[s] for s in self.peers] + [self.g_recv[s] for s in self.peers] + [1])
+        buf = self._buf.get("gidx")
+        if buf is None or buf.shape[1] < need:  # persistent, grown geometrically
+            buf = torch.empty((2 * len(self.peers), max(need, int(1.1 * need))), dtype=torch.int32, device=self.device)
+            self._buf["gidx"] = buf
+        self.solver.select_gas_multi_dev(self.gmask_all, buf, self.gcnt, stream=self.stream)
+        if self.check:
+            got = self.gcnt.cpu().numpy()
+        for q, s in enumerate(self.peers):
+            for k, (dst, m, n) in enumerate(((self.gsend, self.mask_send[s], self.g_send[s]),
+                                             (self.grecv, self.mask_recv[s], self.g_recv[s]))):
                 if self.check:
-                    assert int(c.item()) == n, "ghost gas set does not match the R1 gas count"
-                dst[s] = buf[:n]
+                    assert int(got[2 * q + k]) == (n if m is not None else 0), \
+                        "ghost gas set does not match the R1 gas count"
+                dst[s] = None if (m is None or n == 0) else buf[2 * q + k, :n]
 
     # passes -------------------------------------------------------------
     def gravity_geometry(self, dt_grav=0.0):
@@ -395,15 +454,6 @@ class DomainRank:
             self._comm = torch.cuda.Stream(self.device)
         return self._comm
 
-    def writeback(self):
-        """Kicked velocities and internal energies of the own particles back into the own set
-        (the next substep's R1 reads them): own rows are the sorted positions with perm < n_own."""
-        perm = self.p.perm[: self.n_total].long()
-        own = perm < self.n_own
-        src = perm[own]
-        for k in ("vx", "vy", "vz", "u"):
-            getattr(self.own, k).index_copy_(0, src, getattr(self.p, k)[: self.n_total][own])
-
     # particle migration ---------------------------------------------------
     def migrate_select_pack(self):
         """After drifts: select the own particles now in another rank's domain (packed per new
@@ -448,9 +498,8 @@ class DomainRank:
                 self.solver.unpack_particles(own, off, buf, stream=self.stream)
                 off += buf.shape[0]
         self.own, self.n_own = own, n_new
-        self.idx_r1 = {s: _grow(None, max(n_new, 1), dtype=torch.int32, device=self.device) for s in self.peers} \
-            if self.h is not None else {}
-        self.idx_tmp = torch.empty(max(n_new, 1), dtype=torch.int32, device=self.device)
+        if self.h is not None:
+            self._alloc_sel(n_new)
 
     def own_mask(self) -> torch.Tensor:
         """Sorted positions (of the local set) holding own particles (inputs 0..n_own-1 are own)."""
@@ -508,8 +557,7 @@ def substep_inprocess(ranks, dt_grav=0.0, dt_hydro=0.0, overlap=False):
             rk.accel_rows(2, dt_hydro)
         else:
             rk.accel(dt_hydro)
-        if dt_grav != 0.0 or dt_hydro != 0.0:
-            rk.writeback()
+        rk.carry_own()
 
 
 def migrate_inprocess(ranks):
@@ -610,5 +658,4 @@ def substep_dist(rk: DomainRank, ex: DistExchange, dt_grav=0.0, dt_hydro=0.0, hm
         ex.exchange(sends, recvs)
         rk.r3_unpack(recvs)
         rk.accel(dt_hydro)
-    if dt_grav != 0.0 or dt_hydro != 0.0:
-        rk.writeback()
+    rk.carry_own()  # the kicked own set, in this build's order, starts the next local set

@@ -81,6 +81,8 @@ for rep in range(a.reps + 1):
     ex.exchange_all([m[0] for m in msgs], [m[1] for m in msgs])
     for rk, m in zip(ranks, msgs):
         phase(t, rk, lambda: (rk.r3_unpack(m[1]), rk.accel(0.0)))
+    for rk in ranks:
+        phase(t, rk, rk.carry_own)
     torch.cuda.synchronize()
     if rep > 0:
         for r in range(a.P):
@@ -93,5 +95,5 @@ print(json.dumps({"P": a.P, "config": a.config, "halo_cells": h,
                   "rank_ms": [round(sum(v) / len(v), 2) for v in res.values()],
                   "max_rank_ms": round(max(sum(v) / len(v) for v in res.values()), 2),
                   "phase_names": ["r1 select+pack", "r1 unpack", "build", "gas idx", "gravity", "geometry", "r2 pack",
-                                  "r2 unpack+cor/ext", "r3 pack", "r3 unpack+accel"],
+                                  "r2 unpack+cor/ext", "r3 pack", "r3 unpack+accel", "carry own"],
                   "rank_phase_ms": [[round(float(x), 2) for x in np.median(np.asarray(v), 0)] for v in phases.values()]}))
