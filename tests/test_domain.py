@@ -385,3 +385,59 @@ def test_overlapped_exchange_order_is_identical(P):
                 assert np.allclose(a[k], b[k], rtol=0, atol=1e-5 * np.abs(a[k]).max()), k
             else:
                 assert np.array_equal(a[k], b[k], equal_nan=True), k
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("P", [4, 8])
+def test_fused_selections_and_carried_own_set(P):
+    """The one-pass selections of the exchange equal the per-peer calls: R1 (crk_select_peers_dev,
+    per peer the same particle set and gas count as crk_select_cells_dev; its order is free) and
+    the R2/R3 gas sets (crk_select_gas_multi_dev, element for element the key-ordered result of
+    crk_select_gas_dev); after a substep the own set carried by crk_compact_own holds exactly the
+    own particles, in the sorted order of the build."""
+    import torch
+    from paper_2310_16122_b200.domain import DomainRank, substep_inprocess
+
+    parts, params = cached_config("c2z")
+    d = _decomp(params, P)
+    ranks = [DomainRank(d, r, d.split(parts, r), "cuda:0", outputs="forces") for r in range(P)]
+    substep_inprocess(ranks)
+    torch.cuda.synchronize()
+    for rk in ranks:
+        # carried own set: the own rows of the sorted local set, in order
+        perm = rk.p.perm[: rk.n_total].cpu().numpy()
+        own_sorted_ids = rk.p.id[: rk.n_total].cpu().numpy()[perm < rk.n_own]
+        assert np.array_equal(rk.own.id.cpu().numpy(), own_sorted_ids)
+        assert np.array_equal(np.sort(own_sorted_ids), np.sort(rk.own_host["id"]))
+        for k in ("x", "vx", "H", "u"):
+            assert np.array_equal(getattr(rk.own, k).cpu().numpy(),
+                                  getattr(rk.p, k)[: rk.n_total].cpu().numpy()[perm < rk.n_own])
+        # R1: fused vs per peer (sets), on the carried own set
+        cnt = rk.r1_select_pack().cpu().numpy()
+        for q, s in enumerate(rk.peers):
+            m = rk.mask_send[s]
+            if m is None:
+                assert cnt[q, 0] == 0 and cnt[q, 1] == 0
+                continue
+            idx = torch.empty(rk.n_own, dtype=torch.int32, device="cuda:0")
+            c = torch.zeros(1, dtype=torch.int32, device="cuda:0")
+            rk.solver.select_cells_dev(rk.own, m, idx, c, rk.n_own)
+            ref = np.sort(idx[: int(c.item())].cpu().numpy())
+            got = np.sort(rk.idx_all[q, : cnt[q, 0]].cpu().numpy())
+            assert np.array_equal(got, ref)
+            rk.solver.select_cells_dev(rk.own, m, idx, c, rk.n_own, gas_only=True)
+            assert int(c.item()) == cnt[q, 1]
+        # R2/R3 gas sets (the build of this substep is still current): fused vs per set, in order
+        buf = torch.empty((rk.gmask_all.shape[0], rk.n_total), dtype=torch.int32, device="cuda:0")
+        gc = torch.zeros(rk.gmask_all.shape[0], dtype=torch.int32, device="cuda:0")
+        rk.solver.select_gas_multi_dev(rk.gmask_all, buf, gc)
+        gcn = gc.cpu().numpy()
+        for k in range(rk.gmask_all.shape[0]):
+            idx = torch.empty(rk.n_total, dtype=torch.int32, device="cuda:0")
+            c = torch.zeros(1, dtype=torch.int32, device="cuda:0")
+            rk.solver.select_gas_dev(rk.gmask_all[k], idx, c)
+            n = int(c.item())
+            assert gcn[k] == n
+            assert np.array_equal(buf[k, :n].cpu().numpy(), idx[:n].cpu().numpy())
+    for rk in ranks:
+        rk.close()
