@@ -246,6 +246,7 @@ class DomainRank:
         self.solver.compact_own(self.p, self.n_total, self.n_own, self._q, stream=self.stream)
         self._own_view = _rows_view(self._q, self.n_own)
         self._own_local = True
+        self._own_ext = None  # (the caller's set is no longer needed: its memory goes back)
 
     def local_hmax2(self) -> float:
         """max fl32(H^2) over the own gas (device arrays: the own set changes with migration)."""
