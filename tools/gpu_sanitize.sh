@@ -1,4 +1,5 @@
 #!/bin/bash
+# NOTE: compute-sanitizer is closed on the GPU pool since round 2 session 3 (runs exit 86).
 # compute-sanitizer on config 1 (outputs under gpurun_out/r2s3/)
 mkdir -p gpurun_out/r2s3
 python -c "import __graft_entry__ as g; g.build()" || exit 1
