@@ -240,8 +240,7 @@ class DomainRank:
         """After a substep: the own particles (with its kicks) into the spare local-set buffer in
         the sorted order of this substep's build (crk_compact_own); the next substep's local set
         starts from them — R1 needs no own copy and the build sorts nearly sorted input."""
-        cap = 0 if self._q is None else self._q.x.shape[0]
-        if cap < self.n_own:
+        if self._q is None or self._q.x.shape[0] < self.n_own:
             self._q = Particles(max(int(1.1 * self.n_total), 16), self.device, self.outputs)
         self.solver.compact_own(self.p, self.n_total, self.n_own, self._q, stream=self.stream)
         self._own_view = _rows_view(self._q, self.n_own)

@@ -441,3 +441,39 @@ def test_fused_selections_and_carried_own_set(P):
             assert np.array_equal(buf[k, :n].cpu().numpy(), idx[:n].cpu().numpy())
     for rk in ranks:
         rk.close()
+
+
+@pytest.mark.gpu
+def test_decomposed_substep_with_an_empty_rank():
+    """A rank that owns no particle (all of c1's particles moved into the lower half of the box
+    along x, P = 2): it still receives ghosts, selects nothing, carries an empty own set, and the
+    decomposed substep over two substeps equals the single-domain oracle on the owned ones."""
+    import torch
+    import oracle
+    from paper_2310_16122_b200.domain import DomainRank, substep_inprocess
+
+    parts, params = cached_config("c1")
+    parts = {k: np.array(v, copy=True) for k, v in parts.items()}
+    L = params["box"][0]
+    q = max(params["box"]) * 2.0**-23
+    parts["x"] = (np.floor(parts["x"].astype(np.float64) * 0.5 / q) * q).astype(np.float32)  # on the O1 lattice
+    d = _decomp(params, 2)
+    own = [d.split(parts, r) for r in range(2)]
+    assert own[1]["x"].shape[0] == 0 and own[0]["x"].shape[0] == parts["x"].shape[0]
+    ranks = [DomainRank(d, r, own[r], "cuda:0", outputs="forces") for r in range(2)]
+    for _ in range(2):
+        substep_inprocess(ranks)
+    torch.cuda.synchronize()
+    assert ranks[1].n_own == 0 and ranks[1].own.x.shape[0] == 0
+    rk = ranks[0]
+    n = parts["x"].shape[0]
+    pos_of_id = np.empty(n, np.int64)
+    pos_of_id[parts["id"]] = np.arange(n)
+    h = rk.p.to_host(["id", "ax", "ay", "az"])
+    m = rk.own_mask().cpu().numpy()
+    a = np.full((n, 3), np.nan)
+    a[pos_of_id[h["id"][m]]] = np.stack([h["ax"], h["ay"], h["az"]], 1)[m]
+    ref = oracle.substep(parts, params)
+    assert norm_err(a, ref["grav_a"], ref["grav_S"]) <= 1e-4
+    for r in ranks:
+        r.close()
