@@ -293,7 +293,8 @@ def _e2e_multi(args, rk, ex, own, dev, hmax2, overlap, red_dev):
                 for k in Particles.IN_F32 + ("species", "id")}
         bi = sum(t.numel() * t.element_size() for t in host.values())
         outk = list(Particles.FORCES) + ["perm"]
-        owns = [rk.own, Particles(rk.n_own, dev, outputs=False)]
+        # two own sets of our own (rk.own may be a view into the rank's carried local set)
+        owns = [Particles(rk.n_own, dev, outputs=False), Particles(rk.n_own, dev, outputs=False)]
         stream = torch.cuda.current_stream(dev)
         h2d, d2h = torch.cuda.Stream(dev), torch.cuda.Stream(dev)
         ev_in = [torch.cuda.Event(), torch.cuda.Event()]

@@ -18,7 +18,7 @@ def _line(out: str) -> dict:
     return json.loads(lines[0])
 
 
-def _check_common(d: dict, n: int):
+def _check_common(d: dict, n: int, timing=True):
     assert d["metric"].startswith("pair interactions/s")
     assert d["n_gpus"] == n and d["unit"] == "pair interactions/s" and d["higher_is_better"] is True
     assert d["value"] > 0 and d["ms_per_step"] > 0 and d["scaling"] == "weak"
@@ -26,7 +26,8 @@ def _check_common(d: dict, n: int):
     e = d["e2e"]
     assert e and e["value"] > 0 and e["unit"] == d["unit"]
     assert e["h2d_bytes_per_step"] > 0 and e["d2h_bytes_per_step"] > 0
-    assert e["value"] < d["value"] * 1.05  # the copies are inside e2e's timed region
+    if timing:  # (ranks sharing one GPU over gloo time each other's work: no relation to check)
+        assert e["value"] < d["value"] * 1.05  # the copies are inside e2e's timed region
     assert "clocks" in d
 
 
@@ -54,5 +55,5 @@ def test_bench_two_ranks_sharing_the_gpu():
                        cwd=ROOT, capture_output=True, text=True, timeout=1500, env=env)
     assert r.returncode == 0, r.stderr[-3000:]
     d = _line(r.stdout)
-    _check_common(d, 2)
+    _check_common(d, 2, timing=False)
     assert d["config"]["ghost_particles_total"] > 0
