@@ -452,7 +452,13 @@ crk_status crk_select_peers_dev(crk_ctx* c, const float* x, const float* y, cons
 crk_status crk_compact_own(crk_ctx* c, const crk_particles* src, int64_t n_own, crk_particles* dst, void* stream) {
     if (!c || !src || !dst || n_own < 0 || n_own > src->n) return fail(c, CRK_EINVAL, "bad args");
     if (n_own == 0) return CRK_OK;
-    if (!src->perm || !src->x || !dst->x || !dst->species || !dst->id) return fail(c, CRK_EINVAL, "null field");
+    const crk_particles* both[2] = {src, dst};
+    for (const crk_particles* q : both) {
+        const void* f[] = {q->x, q->y, q->z, q->vx, q->vy, q->vz, q->m, q->H, q->u, q->species, q->id};
+        for (const void* ptr : f)
+            if (!ptr) return fail(c, CRK_EINVAL, "null input field");
+    }
+    if (!src->perm) return fail(c, CRK_EINVAL, "null perm (call crk_build_lists on src first)");
     if (src->n >= (int64_t)1 << 31) return fail(c, CRK_ECAPACITY, "more than 2^31 particles");
     CRK_TRY(cuda_check(c, cudaSetDevice(c->device), "cudaSetDevice"));
     cudaStream_t st = (cudaStream_t)stream;
