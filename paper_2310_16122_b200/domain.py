@@ -513,10 +513,12 @@ def _counts_host(ranks_cnt_send, ranks_cnt_recv):
     return [np.stack([cs.cpu().numpy(), cr.cpu().numpy()]) for cs, cr in zip(ranks_cnt_send, ranks_cnt_recv)]
 
 
-def substep_inprocess(ranks, dt_grav=0.0, dt_hydro=0.0, overlap=False):
+def substep_inprocess(ranks, dt_grav=0.0, dt_hydro=0.0, overlap=False, carry=True):
     """One decomposed substep for ranks emulated sequentially in one process (tests): the same
     phases and messages as substep_dist, the transfers as device copies.  overlap: the pass
-    order of substep_dist's overlapped exchange (interior rows before the messages land)."""
+    order of substep_dist's overlapped exchange (interior rows before the messages land).
+    carry=False skips carrying the own sets into the next substep (a last substep: no spare
+    local-set buffer is allocated — eight full-size ranks emulated on one GPU need the room)."""
     hmax2 = max(rk.local_hmax2() for rk in ranks)
     h = ranks[0].d.halo_width(hmax2)
     for rk in ranks:
@@ -557,7 +559,8 @@ def substep_inprocess(ranks, dt_grav=0.0, dt_hydro=0.0, overlap=False):
             rk.accel_rows(2, dt_hydro)
         else:
             rk.accel(dt_hydro)
-        rk.carry_own()
+        if carry:
+            rk.carry_own()
 
 
 def migrate_inprocess(ranks):

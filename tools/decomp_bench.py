@@ -7,7 +7,7 @@ without the transfers between ranks.  max over ranks / the single-domain substep
 weak-scaling efficiency that the transfers' time (NVLink) then lowers further.
 
   python tools/decomp_bench.py --P 8 [--config c4] [--reps 3]
-(--config lat:128,128,128:0.1:16522 for P = 8: eight c4-sized ranks do not fit one GPU's memory)
+(P = 8 at c4 per rank fits one GPU's memory only with --no-carry; or --config lat:128,128,128:0.1:16522)
 """
 import argparse
 import json
@@ -27,6 +27,9 @@ ap.add_argument("--P", type=int, default=2)
 ap.add_argument("--reps", type=int, default=3)
 ap.add_argument("--config", default="c4")
 ap.add_argument("--min-free-gb", type=float, default=12.0)
+ap.add_argument("--no-carry", action="store_true",
+                help="do not carry the own sets (no spare local-set buffer: eight c4-sized ranks then fit one "
+                     "GPU; the build sorts the random-order own set every substep, an upper bound)")
 a = ap.parse_args()
 parts, params = make_config(a.config)
 ranks = []
@@ -81,15 +84,16 @@ for rep in range(a.reps + 1):
     ex.exchange_all([m[0] for m in msgs], [m[1] for m in msgs])
     for rk, m in zip(ranks, msgs):
         phase(t, rk, lambda: (rk.r3_unpack(m[1]), rk.accel(0.0)))
-    for rk in ranks:
-        phase(t, rk, rk.carry_own)
+    if not a.no_carry:
+        for rk in ranks:
+            phase(t, rk, rk.carry_own)
     torch.cuda.synchronize()
     if rep > 0:
         for r in range(a.P):
             res[r].append(sum(x.elapsed_time(y) for x, y in t[r]))
             phases[r].append([x.elapsed_time(y) for x, y in t[r]])
 msg_bytes = [int(sum(rk.n_send.values()) * 48 + sum(rk.g_send.values()) * (16 + 144)) for rk in ranks]
-print(json.dumps({"P": a.P, "config": a.config, "halo_cells": h,
+print(json.dumps({"P": a.P, "config": a.config, "carry_own": not a.no_carry, "halo_cells": h,
                   "ghosts_per_rank": [int(rk.n_total - rk.n_own) for rk in ranks],
                   "bytes_sent_per_rank": msg_bytes,
                   "rank_ms": [round(sum(v) / len(v), 2) for v in res.values()],
