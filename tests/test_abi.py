@@ -58,3 +58,16 @@ def test_parameter_validation_without_gpu(libpath):
         st = lib().crk_create(C.byref(params_struct(p)), 0, C.byref(h))
         assert st == -1, p
     assert lib().crk_status_string(-4) == b"call order violated"
+
+
+def test_exchange_calls_reject_bad_arguments_without_gpu(libpath):
+    """The weak-scaling exchange calls validate their arguments before touching the device
+    (CRK_EINVAL = -1): no context, no masks or counts, peer / set numbers out of range."""
+    from paper_2310_16122_b200.binding import CrkParticles, lib
+
+    L = lib()
+    vp = C.c_void_p
+    p = CrkParticles()
+    assert L.crk_select_peers_dev(None, vp(), vp(), vp(), vp(), 10, vp(), 2, vp(), 10, vp(), None) == -1
+    assert L.crk_select_gas_multi_dev(None, vp(), 2, vp(), 10, vp(), None) == -1
+    assert L.crk_compact_own(None, C.byref(p), 0, C.byref(p), None) == -1
